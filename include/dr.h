@@ -1,0 +1,249 @@
+/*
+ * dr.h — C ABI of the B200-native DR-CircuitGNN hot path (arXiv 2508.16769).
+ *
+ * Library: paper_2508_16769_b200/libdr.so (sm_100a). Plain C types only.
+ * Citations: P:<n> = /root/reference/PAPER.md line n (section / equation /
+ * algorithm named beside it); Q<n> = a reading listed in DESIGN.md.
+ *
+ * Conventions (all entry points)
+ *   - Tensors are DEVICE pointers owned by the caller, fp32, row-major,
+ *     contiguous, unless documented otherwise. The library never frees caller
+ *     memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream). Compute calls are asynchronous and stream-ordered; internal
+ *     streams fork from and join back to `stream` with events.
+ *   - Validation of sizes, pointers and k is synchronous and precedes any
+ *     launch; on failure nothing is launched and a non-zero dr_status is
+ *     returned, with detail in dr_last_error(). Asynchronous kernel faults
+ *     surface as DR_ERR_CUDA at a later call or at the caller's synchronise.
+ *   - On failure outputs are unspecified; no handle is created; nothing leaks.
+ *   - GPU restrictions of this build: 1 <= k <= 128 and k a power of two
+ *     (§4.3: "the number of non-zero elements remaining ... is a power
+ *     of two to maximize GPU parallel resource utilization"); k <= dim <= 256
+ *     (CBSR indices are one byte); dim % 4 == 0; every relation nnz < 2^31.
+ */
+#ifndef DR_H_
+#define DR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+typedef enum {
+    DR_OK = 0,
+    DR_ERR_INVALID_ARGUMENT = 1,   /* null pointer, negative size, bad enum       */
+    DR_ERR_BAD_K = 2,              /* k outside the restrictions above            */
+    DR_ERR_SHAPE_MISMATCH = 3,     /* tensor / graph / layer dims disagree        */
+    DR_ERR_OUT_OF_RANGE = 4,       /* CSR column or row pointer out of range      */
+    DR_ERR_DUPLICATE_EDGE = 5,     /* CSR row not strictly increasing             */
+    DR_ERR_TRANSPOSE_MISMATCH = 6, /* pinned != pins^T, or CSC != CSR^T           */
+    DR_ERR_NONFINITE = 7,          /* non-finite edge weight                      */
+    DR_ERR_TAPE_MISMATCH = 8,      /* tape/workspace too small or from other call */
+    DR_ERR_OUT_OF_MEMORY = 9,
+    DR_ERR_CUDA = 10,
+    DR_ERR_NCCL = 11,
+    DR_ERR_UNSUPPORTED = 12
+} dr_status;
+
+const char *dr_status_str(dr_status s);
+/* Thread-local detail of this thread's last failure ("" if none). */
+const char *dr_last_error(void);
+/* Library build string (arch, version). */
+const char *dr_version(void);
+
+/* ------------------------------------------------------------------ graph
+ * A circuit heterograph (§2.2): node types cell (n_cell) and net
+ * (n_net); relations near (cell<-cell, geometric), pins (net<-cell) and
+ * pinned (cell<-net), pins and pinned mutually transposed. Each
+ * relation is an n_dst x n_src adjacency A^psi, rows = destinations (Eq. 4,
+ * P:236-238), given as HOST CSR read only during dr_graph_create.
+ */
+typedef struct dr_graph dr_graph;        /* opaque, immutable, safe for concurrent readers */
+typedef enum { DR_NEAR = 0, DR_PINS = 1, DR_PINNED = 2 } dr_rel;
+/* Module of a relation: its degree normaliser and root-weight semantics
+ * ("two SageConv modules and one GraphConv module"; reading Q1/Q12):
+ *   DR_SAGE_MEAN     : c_i = 1/max(deg_in(i),1),        s_j = 1
+ *   DR_GRAPHCONV_SYM : c_i = max(deg_in(i),1)^-1/2,     s_j = max(deg_out(j),1)^-1/2
+ * Degrees are unweighted edge counts. */
+typedef enum { DR_SAGE_MEAN = 0, DR_GRAPHCONV_SYM = 1 } dr_module;
+typedef enum { DR_MERGE_MAX = 0, DR_MERGE_SUM = 1 } dr_merge;   /* Eq. 8 / Eq. 6 variant */
+
+typedef struct {
+    int32_t n_dst, n_src;
+    int64_t nnz;
+    const int64_t *row_ptr;   /* HOST [n_dst+1], row_ptr[0]=0, row_ptr[n_dst]=nnz        */
+    const int32_t *col_idx;   /* HOST [nnz], strictly increasing within a row, < n_src   */
+    const float *val;         /* HOST [nnz] edge weights a_ij > 0; NULL => all 1 */
+    dr_module module;
+} dr_rel_desc;
+
+typedef struct {
+    void *(*alloc)(void *ctx, size_t bytes, void *stream);
+    void (*free)(void *ctx, void *p, void *stream);
+    void *ctx;
+} dr_allocator;                              /* NULL => cudaMallocAsync / cudaFreeAsync */
+
+#define DR_GRAPH_SKIP_VALIDATION 1u          /* trust the CSR invariants                 */
+#define DR_GRAPH_ORDER_IDENTITY 2u           /* process rows in id order (no degree sort) */
+
+/* Build the device-resident graph: validates each CSR (sorted, unique, in
+ * range), checks rel[DR_PINNED] == rel[DR_PINS]^T, counts degrees and
+ * normalisers, builds CSC = CSR(A^T) for the backward (Alg. 2 stage 1)
+ * and the degree-binned processing orders (Alg. 1 stage 2). Host
+ * work runs on n_threads worker threads, one relation each (§3.4, P:425;
+ * 0 => 3); uploads are stream-ordered on `stream`, which this call
+ * synchronises before returning. */
+dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel_desc rel[3],
+                          const dr_allocator *a, int32_t n_threads, uint32_t flags,
+                          void *stream, dr_graph **out);
+dr_status dr_graph_destroy(dr_graph *g);
+
+typedef struct {
+    int32_t n_cell, n_net;
+    int64_t nnz[3];
+    int32_t max_deg_dst[3], max_deg_src[3];
+    int32_t hub_rows_dst[3], hub_rows_src[2];    /* rows routed to the CTA-per-row kernels */
+    size_t device_bytes;
+} dr_graph_info_t;
+dr_status dr_graph_info(const dr_graph *g, dr_graph_info_t *info);
+
+/* ------------------------------------------------------------------ CBSR
+ * Compressed Balanced Sparse Row: exactly k (value, index) pairs per
+ * row, indices strictly ascending, values copied verbatim from the dense row.
+ * val: DEVICE float [n*k]; idx: DEVICE uint8 [n*k] (idx_bytes must be 1). */
+typedef struct {
+    int64_t n;
+    int32_t dim, k, idx_bytes;
+    void *idx;
+    float *val;
+} dr_cbsr;
+
+/* D-ReLU, Eq. 2-3: th_i = min(topk(X_i,:, k)); keep X_id >= th_i,
+ * exactly k per row with ties at th_i broken towards the lowest column (Q5),
+ * -0.0 == +0.0, values verbatim including negatives (Q6). x: DEVICE [n x dim]
+ * with leading dimension ldx >= dim; out->n, dim, k set by the caller. */
+dr_status dr_drelu_topk(const float *x, int64_t n, int32_t dim, int64_t ldx, dr_cbsr *out,
+                        void *stream);
+
+/* DR-SpMM forward of one relation, Eq. 5-7, Alg. 1,
+ * W applied outside (Q9):  z[i,:] = c_i * sum_{j in N(i)} a_ij * s_j * densify(h_src[j]).
+ * h_src->n must equal the relation's n_src; z: DEVICE [n_dst x h_src->dim]. */
+dr_status dr_spmm_fwd(const dr_graph *g, dr_rel r, const dr_cbsr *h_src, float *z, void *stream);
+
+/* DR-SpMM backward (SSpMM) of one relation, Eq. 10-11, Alg. 2
+ * (P:316-345): the transposed product evaluated only at the forward-kept CBSR
+ * indices of h_src (Alg. 2 stage 1 "Reuse preserved ... CBSR indices"):
+ *   g[j,t] = sum_{i: j in N(i)} c_i * a_ij * s_j * dz[i, h_src.idx[j,t]].
+ * dz = dL/dZ: DEVICE [n_dst x dim]. Outputs (either may be NULL, not both):
+ *   g_kept: DEVICE [n_src x k];
+ *   dx:     DEVICE [n_src x dim] dense D-ReLU mask gradient: g scattered to
+ *           the kept indices, exact zeros elsewhere.
+ * accumulate != 0 adds into g_kept / into dx's kept positions (dx's other
+ * entries are then left untouched). Per-source-row ownership, no atomics (Q23). */
+dr_status dr_spmm_bwd(const dr_graph *g, dr_rel r, const float *dz, const dr_cbsr *h_src,
+                      float *g_kept, float *dx, int32_t accumulate, void *stream);
+
+/* ------------------------------------------------------------------ HeteroConv layer
+ * One HeteroConv block (Fig. 1; Eq. 4-9; reading Q1-Q3):
+ *   H_c = drelu(X_c, k_cell), H_n = drelu(X_n, k_net)
+ *   Z_psi = DR-SpMM_psi(H_src)                            (3 relations, 3 streams, §3.4)
+ *   Y_near   = Z_near Wn_near + densify(H_c) Wr_near + b_near      (SageConv mean)
+ *   Y_pinned = Z_pinned Wn_pinned + b_pinned                       (GraphConv)
+ *   Y_net    = Z_pins Wn_pins + densify(H_n) Wr_pins + b_pins      (SageConv mean)
+ *   Y_cell = max(Y_near, Y_pinned), M = [Y_near >= Y_pinned]      (Eq. 8, Eq. 14)
+ * Weights are DEVICE fp32: wn[r] is d_in(src type of r) x d_out; wr[r] is
+ * d_in(dst type of r) x d_out or NULL (no root term). wr[DR_PINNED] must be
+ * NULL (GraphConv has no root weight; DR_ERR_UNSUPPORTED otherwise). */
+typedef struct {
+    int32_t d_cell, d_net, d_out, k_cell, k_net;
+    dr_merge merge;
+    const float *wn[3];
+    const float *wr[3];
+    const float *b[3];
+} dr_layer;
+typedef struct {
+    float *wn[3];
+    float *wr[3];
+    float *b[3];
+} dr_layer_grad;                               /* same shapes; NULL where dr_layer's is NULL */
+
+#define DR_FWD_SEQUENTIAL 1u  /* run the three relations on one stream (§4.4 breakdown)    */
+#define DR_FWD_TAPS 2u        /* also keep Y_near / Y_pinned for teacher-forced parity      */
+
+/* Bytes of the caller-allocated tape (forward activations reused by the
+ * backward: CBSR of both types, Z_psi, merge-mask bits, taps) plus backward
+ * scratch. */
+dr_status dr_heteroconv_tape_bytes(const dr_graph *g, const dr_layer *L, uint32_t flags,
+                                   size_t *bytes);
+dr_status dr_heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *x_cell,
+                            const float *x_net, float *y_cell, float *y_net, void *tape,
+                            uint32_t flags, void *stream);
+/* Backward (Eq. 10-14, Alg. 2): mask routing, dW = Z^T dY, dWr = H^T dY, db,
+ * dZ = dY Wn^T, SSpMM per source type (cell: near + pins + root term; net:
+ * pinned + root term) and the D-ReLU mask scatter. dx_cell == NULL and
+ * dx_net == NULL skip the SSpMM (first layer). grads are overwritten. */
+dr_status dr_heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape,
+                            const float *dy_cell, const float *dy_net, float *dx_cell,
+                            float *dx_net, dr_layer_grad *grads, uint32_t flags, void *stream);
+/* Device views into a tape after dr_heteroconv_fwd (for teacher-forced parity
+ * tests): the CBSR of both node types, Z per relation, Y_near/Y_pinned taps
+ * (NULL unless DR_FWD_TAPS) and the merge mask (uint32 words, row-major
+ * n_cell x ceil(d_out/32), bit d%32 of word d/32 = M[i,d]). */
+typedef struct {
+    dr_cbsr h_cell, h_net;
+    float *z[3];
+    float *y_near, *y_pinned;
+    uint32_t *mask;
+} dr_tape_view;
+dr_status dr_heteroconv_tape_view(const dr_graph *g, const dr_layer *L, void *tape,
+                                  uint32_t flags, dr_tape_view *view);
+
+/* ------------------------------------------------------------------ training
+ * The 2-layer model of P:464-466: HeteroConv x n_layers -> linear head on
+ * cells -> MSE (Q14) -> backward -> [NCCL allreduce of the flat gradient] ->
+ * Adam with coupled L2 weight decay (Q15). Flat parameter layout, per layer
+ * l (d_c = d_in_cell, d_n = d_in_net for l = 0, else d_hidden; D = d_hidden):
+ *   wn_near[d_c*D] wr_near[d_c*D] b_near[D] wn_pinned[d_n*D] b_pinned[D]
+ *   wn_pins[d_c*D] wr_pins[d_n*D] b_pins[D]
+ * then the head w_h[D] b_h[1]. */
+typedef struct {
+    int32_t n_layers, d_in_cell, d_in_net, d_hidden, k_cell, k_net;
+    float lr, weight_decay, beta1, beta2, eps;
+} dr_train_cfg;
+typedef struct dr_trainer dr_trainer;         /* opaque, single-threaded use */
+
+int64_t dr_train_param_count(const dr_train_cfg *c);
+/* params: DEVICE flat buffer (caller-owned, updated in place). nccl_comm: an
+ * ncclComm_t from dr_nccl_comm_init, or NULL for one GPU. */
+dr_status dr_trainer_create(const dr_train_cfg *c, float *params, int64_t n_params,
+                            void *nccl_comm, const dr_allocator *a, dr_trainer **out);
+/* One training step on `batch` (one design, or a disjoint union of designs,
+ * Q24). x_cell/x_net/labels: DEVICE. If loss_host != NULL (pinned host float)
+ * the step's mean loss is written there when the stream reaches it. If
+ * grad_out != NULL (DEVICE [n_params]) the allreduced mean gradient is also
+ * copied there (parity tests). */
+dr_status dr_train_step(dr_trainer *t, const dr_graph *batch, const float *x_cell,
+                        const float *x_net, const float *labels, float *loss_host,
+                        float *grad_out, void *stream);
+dr_status dr_trainer_destroy(dr_trainer *t);
+
+/* NCCL bootstrap for data parallelism (north_star: one gradient allreduce per
+ * step). The unique id (128 bytes) is made on rank 0 and broadcast by the
+ * caller (e.g. through torch.distributed). NCCL is loaded at run time. */
+dr_status dr_nccl_unique_id(void *id128);
+dr_status dr_nccl_comm_init(const void *id128, int32_t nranks, int32_t rank, void **comm);
+dr_status dr_nccl_comm_destroy(void *comm);
+
+/* Number of kernels this library launched on this host thread since the last
+ * reset (evidence for bench.py's gpu_launches). */
+int64_t dr_launch_count(void);
+void dr_launch_count_reset(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DR_H_ */

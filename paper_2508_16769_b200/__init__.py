@@ -1,0 +1,349 @@
+"""B200-native DR-CircuitGNN hot path (arXiv 2508.16769) — Python binding.
+
+Thin wrappers over the C ABI in include/dr.h (libdr.so, sm_100a). They only
+marshal arguments: allocate outputs with torch on the current device, pass raw
+pointers and the current CUDA stream. Every step of the computation runs in
+libdr's kernels; there is no CPU or PyTorch fallback — if the library is
+missing or no GPU is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import (DR_FWD_SEQUENTIAL, DR_FWD_TAPS, DR_GRAPH_ORDER_IDENTITY,  # noqa: F401
+                   DR_GRAPH_SKIP_VALIDATION, DR_GRAPHCONV_SYM, DR_MERGE_MAX, DR_MERGE_SUM,
+                   DR_NEAR, DR_PINNED, DR_PINS, DR_SAGE_MEAN, DRError, EXPORTS, check,
+                   dr_cbsr, dr_layer, dr_layer_grad, dr_rel_desc, dr_tape_view, dr_train_cfg,
+                   dr_graph_info_t, lib)
+
+REL_NAMES = ("near", "pins", "pinned")
+REL_ID = {"near": DR_NEAR, "pins": DR_PINS, "pinned": DR_PINNED}
+DEFAULT_MODULES = {"near": DR_SAGE_MEAN, "pins": DR_SAGE_MEAN, "pinned": DR_GRAPHCONV_SYM}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream(stream=None):
+    torch = _torch()
+    if stream is None:
+        if not torch.cuda.is_available():
+            return C.c_void_p(0)        # host-only calls (validation) on a GPU-less host
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def version():
+    return lib().dr_version().decode()
+
+
+def launch_count():
+    return int(lib().dr_launch_count())
+
+
+def launch_count_reset():
+    lib().dr_launch_count_reset()
+
+
+# ------------------------------------------------------------------ graph
+class Graph:
+    """Device-resident heterograph (dr_graph_create). `rels` maps 'near'/'pins'/
+    'pinned' to (row_ptr int64 [n_dst+1], col_idx int32 [nnz]) host arrays."""
+
+    def __init__(self, n_cell, n_net, rels, modules=None, weights=None, n_threads=0, flags=0,
+                 stream=None):
+        modules = dict(DEFAULT_MODULES if modules is None else modules)
+        weights = dict(weights or {})
+        dims = {"near": (n_cell, n_cell), "pins": (n_net, n_cell), "pinned": (n_cell, n_net)}
+        descs = (dr_rel_desc * 3)()
+        self._keep = []
+        for name in REL_NAMES:
+            ptr, col = rels[name]
+            ptr = np.ascontiguousarray(ptr, dtype=np.int64)
+            col = np.ascontiguousarray(col, dtype=np.int32)
+            w = weights.get(name)
+            if w is not None:
+                w = np.ascontiguousarray(w, dtype=np.float32)
+            self._keep += [ptr, col, w]
+            d = descs[REL_ID[name]]
+            d.n_dst, d.n_src = int(ptr.shape[0]) - 1, dims[name][1]
+            d.nnz = int(col.shape[0])
+            d.row_ptr = ptr.ctypes.data
+            d.col_idx = col.ctypes.data if col.size else None
+            d.val = None if w is None else w.ctypes.data
+            d.module = int(modules[name])
+        out = C.c_void_p()
+        check(lib().dr_graph_create(int(n_cell), int(n_net), descs, None, int(n_threads),
+                                    int(flags), _stream(stream), C.byref(out)))
+        self._keep = None
+        self.handle = out
+        self.n_cell, self.n_net = int(n_cell), int(n_net)
+
+    @classmethod
+    def from_design(cls, d, **kw):
+        rels = {r: d.rel(r)[:2] for r in REL_NAMES}
+        return cls(d.n_cell, d.n_net, rels, **kw)
+
+    def info(self):
+        i = dr_graph_info_t()
+        check(lib().dr_graph_info(self.handle, C.byref(i)))
+        return dict(n_cell=i.n_cell, n_net=i.n_net, nnz=list(i.nnz),
+                    max_deg_dst=list(i.max_deg_dst), max_deg_src=list(i.max_deg_src),
+                    hub_rows_dst=list(i.hub_rows_dst), hub_rows_src=list(i.hub_rows_src),
+                    device_bytes=int(i.device_bytes))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().dr_graph_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------ CBSR ops
+def _cbsr(val, idx, dim):
+    n, k = val.shape
+    return dr_cbsr(n, int(dim), int(k), 1, idx.data_ptr() if n else None,
+                   val.data_ptr() if n else None)
+
+
+def drelu_topk(x, k, out=None, stream=None):
+    """Eq. 2-3: exact row top-k -> CBSR (val float32 [n,k], idx uint8 [n,k])."""
+    torch = _torch()
+    n, dim = x.shape
+    assert x.dtype == torch.float32 and x.is_cuda and x.stride(1) == 1
+    if out is None:
+        val = torch.empty((n, k), device=x.device, dtype=torch.float32)
+        idx = torch.empty((n, k), device=x.device, dtype=torch.uint8)
+    else:
+        val, idx = out
+    cb = _cbsr(val, idx, dim)
+    check(lib().dr_drelu_topk(_ptr(x), n, dim, x.stride(0), C.byref(cb), _stream(stream)))
+    return val, idx
+
+
+def spmm_fwd(g, rel, val, idx, dim, out=None, stream=None):
+    """Eq. 5-7 / Alg. 1: Z = diag(c) A diag(s) densify(H) for relation `rel`."""
+    torch = _torch()
+    r = REL_ID[rel] if isinstance(rel, str) else int(rel)
+    n_dst = g.n_cell if r in (DR_NEAR, DR_PINNED) else g.n_net
+    z = out if out is not None else torch.empty((n_dst, dim), device=val.device,
+                                                 dtype=torch.float32)
+    cb = _cbsr(val, idx, dim)
+    check(lib().dr_spmm_fwd(g.handle, r, C.byref(cb), _ptr(z), _stream(stream)))
+    return z
+
+
+def spmm_bwd(g, rel, dz, val, idx, dim, want_g=True, want_dx=False, accumulate=False,
+             g_out=None, dx_out=None, stream=None):
+    """Eq. 10-11 / Alg. 2: SSpMM at the kept CBSR indices (+ D-ReLU mask scatter)."""
+    torch = _torch()
+    r = REL_ID[rel] if isinstance(rel, str) else int(rel)
+    n, k = val.shape
+    gk = g_out if g_out is not None else (
+        torch.empty((n, k), device=dz.device, dtype=torch.float32) if want_g else None)
+    dx = dx_out if dx_out is not None else (
+        torch.empty((n, dim), device=dz.device, dtype=torch.float32) if want_dx else None)
+    cb = _cbsr(val, idx, dim)
+    check(lib().dr_spmm_bwd(g.handle, r, _ptr(dz), C.byref(cb), _ptr(gk), _ptr(dx),
+                            int(bool(accumulate)), _stream(stream)))
+    return gk, dx
+
+
+# ------------------------------------------------------------------ HeteroConv layer
+LAYER_KEYS = ("wn_near", "wr_near", "b_near", "w_pinned", "b_pinned", "wn_pins", "wr_pins",
+              "b_pins")
+
+
+class Layer:
+    """dr_layer over torch tensors W (keys as LAYER_KEYS; wr_* may be None)."""
+
+    def __init__(self, W, d_cell, d_net, d_out, k_cell, k_net, merge=DR_MERGE_MAX):
+        self.W = W
+        L = dr_layer()
+        L.d_cell, L.d_net, L.d_out, L.k_cell, L.k_net, L.merge = (
+            d_cell, d_net, d_out, k_cell, k_net, merge)
+        L.wn[DR_NEAR] = W["wn_near"].data_ptr()
+        L.wn[DR_PINNED] = W["w_pinned"].data_ptr()
+        L.wn[DR_PINS] = W["wn_pins"].data_ptr()
+        L.wr[DR_NEAR] = W["wr_near"].data_ptr() if W.get("wr_near") is not None else None
+        L.wr[DR_PINS] = W["wr_pins"].data_ptr() if W.get("wr_pins") is not None else None
+        L.wr[DR_PINNED] = None
+        L.b[DR_NEAR] = W["b_near"].data_ptr()
+        L.b[DR_PINNED] = W["b_pinned"].data_ptr()
+        L.b[DR_PINS] = W["b_pins"].data_ptr()
+        self.c = L
+
+    def tape_bytes(self, g, flags=0):
+        n = C.c_size_t()
+        check(lib().dr_heteroconv_tape_bytes(g.handle, C.byref(self.c), flags, C.byref(n)))
+        return n.value
+
+
+def heteroconv_fwd(g, layer, x_cell, x_net, flags=0, tape=None, stream=None):
+    torch = _torch()
+    dev = x_cell.device
+    D = layer.c.d_out
+    y_cell = torch.empty((g.n_cell, D), device=dev, dtype=torch.float32)
+    y_net = torch.empty((g.n_net, D), device=dev, dtype=torch.float32)
+    if tape is None:
+        tape = torch.empty(layer.tape_bytes(g, flags), device=dev, dtype=torch.uint8)
+    check(lib().dr_heteroconv_fwd(g.handle, C.byref(layer.c), _ptr(x_cell), _ptr(x_net),
+                                  _ptr(y_cell), _ptr(y_net), _ptr(tape), flags, _stream(stream)))
+    return y_cell, y_net, tape
+
+
+def tape_view(g, layer, tape, flags=0):
+    """Torch views of the forward tape (teacher-forced parity)."""
+    torch = _torch()
+    v = dr_tape_view()
+    check(lib().dr_heteroconv_tape_view(g.handle, C.byref(layer.c), _ptr(tape), flags,
+                                        C.byref(v)))
+    base = tape.data_ptr()
+    L = layer.c
+
+    def sl(ptr, shape, dtype):
+        if not ptr:
+            return None
+        nbytes = int(np.prod(shape)) * torch.tensor([], dtype=dtype).element_size()
+        off = ptr - base
+        return tape[off:off + nbytes].view(dtype).view(*shape)
+    nc, nn, D = g.n_cell, g.n_net, L.d_out
+    return dict(
+        hc_val=sl(v.h_cell.val, (nc, L.k_cell), torch.float32),
+        hc_idx=sl(v.h_cell.idx, (nc, L.k_cell), torch.uint8),
+        hn_val=sl(v.h_net.val, (nn, L.k_net), torch.float32),
+        hn_idx=sl(v.h_net.idx, (nn, L.k_net), torch.uint8),
+        z_near=sl(v.z[DR_NEAR], (nc, L.d_cell), torch.float32),
+        z_pins=sl(v.z[DR_PINS], (nn, L.d_cell), torch.float32),
+        z_pinned=sl(v.z[DR_PINNED], (nc, L.d_net), torch.float32),
+        y_near=sl(v.y_near, (nc, D), torch.float32),
+        y_pinned=sl(v.y_pinned, (nc, D), torch.float32),
+        mask=sl(v.mask, (nc, (D + 31) // 32), torch.int32),
+    )
+
+
+def heteroconv_bwd(g, layer, tape, dy_cell, dy_net, need_dx=True, flags=0, stream=None):
+    """Returns (grads dict keyed like LAYER_KEYS, dx_cell, dx_net)."""
+    torch = _torch()
+    dev = dy_cell.device
+    grads = {k: torch.empty_like(v) for k, v in layer.W.items() if v is not None}
+    G = dr_layer_grad()
+    G.wn[DR_NEAR] = grads["wn_near"].data_ptr()
+    G.wn[DR_PINNED] = grads["w_pinned"].data_ptr()
+    G.wn[DR_PINS] = grads["wn_pins"].data_ptr()
+    G.wr[DR_NEAR] = grads["wr_near"].data_ptr() if "wr_near" in grads else None
+    G.wr[DR_PINS] = grads["wr_pins"].data_ptr() if "wr_pins" in grads else None
+    G.b[DR_NEAR] = grads["b_near"].data_ptr()
+    G.b[DR_PINNED] = grads["b_pinned"].data_ptr()
+    G.b[DR_PINS] = grads["b_pins"].data_ptr()
+    dxc = dxn = None
+    if need_dx:
+        dxc = torch.empty((g.n_cell, layer.c.d_cell), device=dev, dtype=torch.float32)
+        dxn = torch.empty((g.n_net, layer.c.d_net), device=dev, dtype=torch.float32)
+    check(lib().dr_heteroconv_bwd(g.handle, C.byref(layer.c), _ptr(tape), _ptr(dy_cell),
+                                  _ptr(dy_net), _ptr(dxc), _ptr(dxn), C.byref(G), flags,
+                                  _stream(stream)))
+    return grads, dxc, dxn
+
+
+# ------------------------------------------------------------------ training
+PARAM_ORDER = ("wn_near", "wr_near", "b_near", "w_pinned", "b_pinned", "wn_pins", "wr_pins",
+               "b_pins")
+
+
+def flatten_params(P, n_layers):
+    """Named arrays (gen.make_params) -> flat float32 array in the dr.h layout."""
+    parts = []
+    for l in range(n_layers):
+        for k in PARAM_ORDER:
+            parts.append(np.asarray(P[f"l{l}.{k}"], dtype=np.float32).reshape(-1))
+    parts.append(np.asarray(P["head.w"], dtype=np.float32).reshape(-1))
+    parts.append(np.asarray(P["head.b"], dtype=np.float32).reshape(-1))
+    return np.concatenate(parts)
+
+
+def unflatten(flat, n_layers, d_cell, d_net, D):
+    """Inverse of flatten_params (shapes per dr.h)."""
+    out, o = {}, 0
+    dc, dn = d_cell, d_net
+    for l in range(n_layers):
+        shapes = {"wn_near": (dc, D), "wr_near": (dc, D), "b_near": (D,), "w_pinned": (dn, D),
+                  "b_pinned": (D,), "wn_pins": (dc, D), "wr_pins": (dn, D), "b_pins": (D,)}
+        for k in PARAM_ORDER:
+            n = int(np.prod(shapes[k]))
+            out[f"l{l}.{k}"] = flat[o:o + n].reshape(shapes[k])
+            o += n
+        dc = dn = D
+    out["head.w"] = flat[o:o + D]
+    out["head.b"] = flat[o + D:o + D + 1]
+    return out
+
+
+class Trainer:
+    """dr_trainer over a flat device parameter tensor (updated in place)."""
+
+    def __init__(self, params, n_layers, d_in_cell, d_in_net, d_hidden, k_cell, k_net,
+                 lr=2e-4, weight_decay=1e-5, beta1=0.9, beta2=0.999, eps=1e-8, nccl_comm=None):
+        torch = _torch()
+        cfg = dr_train_cfg(n_layers, d_in_cell, d_in_net, d_hidden, k_cell, k_net, lr,
+                           weight_decay, beta1, beta2, eps)
+        self.cfg = cfg
+        self.n_params = int(lib().dr_train_param_count(C.byref(cfg)))
+        assert params.numel() == self.n_params and params.dtype == torch.float32
+        self.params = params
+        out = C.c_void_p()
+        check(lib().dr_trainer_create(C.byref(cfg), _ptr(params), self.n_params,
+                                      C.c_void_p(nccl_comm) if nccl_comm else None, None,
+                                      C.byref(out)))
+        self.handle = out
+        self.loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
+
+    def step(self, g, x_cell, x_net, labels, grad_out=None, sync=True, stream=None):
+        check(lib().dr_train_step(self.handle, g.handle, _ptr(x_cell), _ptr(x_net),
+                                  _ptr(labels), C.c_void_p(self.loss_host.data_ptr()),
+                                  _ptr(grad_out), _stream(stream)))
+        if sync:
+            _torch().cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+            return float(self.loss_host[0])
+        return None
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().dr_trainer_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id():
+    buf = (C.c_char * 128)()
+    check(lib().dr_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def nccl_comm_init(uid, nranks, rank):
+    buf = (C.c_char * 128).from_buffer_copy(uid)
+    comm = C.c_void_p()
+    check(lib().dr_nccl_comm_init(buf, int(nranks), int(rank), C.byref(comm)))
+    return comm.value
+
+
+def nccl_comm_destroy(comm):
+    check(lib().dr_nccl_comm_destroy(C.c_void_p(comm)))

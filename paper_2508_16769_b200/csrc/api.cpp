@@ -1,0 +1,725 @@
+// api.cpp — the C ABI of include/dr.h: validation, the HeteroConv layer
+// orchestration over three CUDA streams (§3.4), the training step
+// and the NCCL bootstrap. Every compute step runs in this library's kernels.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "proj.h"
+
+namespace dr {
+
+// ------------------------------------------------------------------ errors & bookkeeping
+static thread_local std::string t_err;
+static thread_local int64_t t_launches = 0;
+
+void set_error(dr_status s, const std::string &msg) {
+    t_err = std::string(dr_status_str(s)) + ": " + msg;
+}
+void clear_error() { t_err.clear(); }
+void fail(dr_status s, const std::string &msg) { throw Error{s, msg}; }
+
+void note_launch(const char *name) {
+    ++t_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fail(DR_ERR_CUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
+}
+
+void ensure_smem(const void *fn, size_t bytes) {
+    static std::mutex mu;
+    static std::unordered_map<const void *, size_t> set;
+    if (bytes <= 48 * 1024) return;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t &cur = set[fn];
+    if (bytes > cur) {
+        DR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        cur = bytes;
+    }
+}
+
+// Per-host-thread helper streams/events for the 3-stream fork/join.
+struct StreamCtx {
+    int device = -1;
+    cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t fork = nullptr, ev[6] = {};
+};
+static thread_local StreamCtx t_ctx;
+
+static StreamCtx &ctx() {
+    int dev = 0;
+    DR_CUDA(cudaGetDevice(&dev));
+    if (t_ctx.device != dev) {
+        if (t_ctx.device >= 0) {
+            // previous device's objects: leave them (rare; device switches per thread)
+        }
+        for (int q = 0; q < 3; ++q) DR_CUDA(cudaStreamCreateWithFlags(&t_ctx.s[q], cudaStreamNonBlocking));
+        DR_CUDA(cudaEventCreateWithFlags(&t_ctx.fork, cudaEventDisableTiming));
+        for (int q = 0; q < 6; ++q) DR_CUDA(cudaEventCreateWithFlags(&t_ctx.ev[q], cudaEventDisableTiming));
+        t_ctx.device = dev;
+    }
+    return t_ctx;
+}
+
+static void wait_on(cudaStream_t waiter, cudaStream_t producer, cudaEvent_t ev) {
+    if (waiter == producer) return;
+    DR_CUDA(cudaEventRecord(ev, producer));
+    DR_CUDA(cudaStreamWaitEvent(waiter, ev, 0));
+}
+
+static bool is_pow2(int k) { return k > 0 && (k & (k - 1)) == 0; }
+
+static void check_k(int k, int dim, const char *what) {
+    DR_CHECK(dim >= 1 && dim <= 256 && dim % 4 == 0, DR_ERR_SHAPE_MISMATCH,
+             std::string(what) + ": dim must be a multiple of 4 in [4, 256]");
+    DR_CHECK(k >= 1 && k <= dim && k <= 128 && is_pow2(k), DR_ERR_BAD_K,
+             std::string(what) + ": k must be a power of two with 1 <= k <= min(dim, 128)");
+}
+
+static void check_cbsr(const dr_cbsr *h, const char *what) {
+    DR_CHECK(h != nullptr, DR_ERR_INVALID_ARGUMENT, std::string(what) + ": null cbsr");
+    DR_CHECK(h->idx_bytes == 1, DR_ERR_UNSUPPORTED, std::string(what) + ": idx_bytes must be 1");
+    DR_CHECK(h->n >= 0, DR_ERR_INVALID_ARGUMENT, std::string(what) + ": negative n");
+    DR_CHECK(h->n == 0 || (h->idx && h->val), DR_ERR_INVALID_ARGUMENT,
+             std::string(what) + ": null cbsr buffers");
+    check_k(h->k, h->dim, what);
+}
+
+static void check_out_width(int n, const char *what) {
+    DR_CHECK(n >= 4 && n <= 256 && n % 4 == 0 && (n % 32 == 0 || n == 4 || n == 8 || n == 16),
+             DR_ERR_SHAPE_MISMATCH,
+             std::string(what) + ": width must be 4, 8, 16 or a multiple of 32 up to 256");
+}
+
+// ------------------------------------------------------------------ tape layout
+struct TapeLayout {
+    size_t hc_val, hc_idx, hn_val, hn_idx, z[3], mask, tap_a, tap_b;
+    size_t dz[3], root_c, root_n, work[3];
+    size_t total;
+};
+
+static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static TapeLayout tape_layout(const dr_graph *g, const dr_layer *L, uint32_t flags) {
+    TapeLayout t{};
+    const size_t nc = (size_t)g->n_cell, nn = (size_t)g->n_net;
+    const size_t dc = L->d_cell, dn = L->d_net, D = L->d_out, kc = L->k_cell, kn = L->k_net;
+    size_t off = 0;
+    auto put = [&](size_t bytes) { size_t o = off; off += al(bytes); return o; };
+    t.hc_val = put(nc * kc * 4);
+    t.hc_idx = put(nc * kc);
+    t.hn_val = put(nn * kn * 4);
+    t.hn_idx = put(nn * kn);
+    t.z[DR_NEAR] = put(nc * dc * 4);
+    t.z[DR_PINS] = put(nn * dc * 4);
+    t.z[DR_PINNED] = put(nc * dn * 4);
+    t.mask = put(nc * ((D + 31) / 32) * 4);
+    t.tap_a = (flags & DR_FWD_TAPS) ? put(nc * D * 4) : (size_t)-1;
+    t.tap_b = (flags & DR_FWD_TAPS) ? put(nc * D * 4) : (size_t)-1;
+    t.dz[DR_NEAR] = put(nc * dc * 4);
+    t.dz[DR_PINS] = put(nn * dc * 4);
+    t.dz[DR_PINNED] = put(nc * dn * 4);
+    t.root_c = put(nc * kc * 4);
+    t.root_n = put(nn * kn * 4);
+    auto mx = [](size_t a, size_t b) { return a > b ? a : b; };
+    t.work[0] = put(mx(dw_part_floats(nc, (int)dc, (int)D), dw_part_floats(nc, (int)dc, (int)D)) * 4);
+    t.work[1] = put(mx(dw_part_floats(nn, (int)dc, (int)D), dw_part_floats(nn, (int)dn, (int)D)) * 4);
+    t.work[2] = put(dw_part_floats(nc, (int)dn, (int)D) * 4);
+    t.total = off;
+    return t;
+}
+
+static void check_layer(const dr_graph *g, const dr_layer *L) {
+    DR_CHECK(g && L, DR_ERR_INVALID_ARGUMENT, "null graph/layer");
+    check_k(L->k_cell, L->d_cell, "layer k_cell/d_cell");
+    check_k(L->k_net, L->d_net, "layer k_net/d_net");
+    check_out_width(L->d_out, "layer d_out");
+    check_out_width(L->d_cell, "layer d_cell");
+    check_out_width(L->d_net, "layer d_net");
+    for (int r = 0; r < 3; ++r)
+        DR_CHECK(L->wn[r] && L->b[r], DR_ERR_INVALID_ARGUMENT, "layer: null wn/b");
+    DR_CHECK(L->wr[DR_PINNED] == nullptr, DR_ERR_UNSUPPORTED, "layer: wr[PINNED] must be NULL");
+    DR_CHECK(L->merge == DR_MERGE_MAX || L->merge == DR_MERGE_SUM, DR_ERR_INVALID_ARGUMENT,
+             "layer: bad merge");
+}
+
+// ------------------------------------------------------------------ layer forward / backward
+static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc, const float *xn,
+                           float *yc, float *yn, void *tape, uint32_t flags, cudaStream_t st) {
+    const TapeLayout T = tape_layout(g, L, flags);
+    char *tp = (char *)tape;
+    float *hcv = (float *)(tp + T.hc_val), *hnv = (float *)(tp + T.hn_val);
+    uint8_t *hci = (uint8_t *)(tp + T.hc_idx), *hni = (uint8_t *)(tp + T.hn_idx);
+    float *z[3];
+    for (int r = 0; r < 3; ++r) z[r] = (float *)(tp + T.z[r]);
+    const bool seq = (flags & DR_FWD_SEQUENTIAL) != 0;
+    StreamCtx &C = ctx();
+    cudaStream_t s0 = seq ? st : C.s[0], s1 = seq ? st : C.s[1], s2 = seq ? st : C.s[2];
+    if (!seq) {
+        DR_CUDA(cudaEventRecord(C.fork, st));
+        for (int q = 0; q < 3; ++q) DR_CUDA(cudaStreamWaitEvent(C.s[q], C.fork, 0));
+    }
+    const int nc = g->n_cell, nn = g->n_net;
+    launch_drelu(xc, nc, L->d_cell, L->d_cell, L->k_cell, hcv, hci, s0);         // Eq. 2-3
+    if (!seq) DR_CUDA(cudaEventRecord(C.ev[0], s0));                               // H_c ready
+    launch_drelu(xn, nn, L->d_net, L->d_net, L->k_net, hnv, hni, s2);
+    if (!seq) DR_CUDA(cudaEventRecord(C.ev[1], s2));                               // H_n ready
+    launch_spmm_fwd(g->rel[DR_NEAR], hcv, hci, L->k_cell, L->d_cell, z[DR_NEAR], s0);   // Eq. 5-7
+    if (!seq) DR_CUDA(cudaStreamWaitEvent(s1, C.ev[0], 0));
+    launch_spmm_fwd(g->rel[DR_PINS], hcv, hci, L->k_cell, L->d_cell, z[DR_PINS], s1);
+    launch_spmm_fwd(g->rel[DR_PINNED], hnv, hni, L->k_net, L->d_net, z[DR_PINNED], s2);
+    if (!seq) DR_CUDA(cudaEventRecord(C.ev[2], s2));                               // Z_pinned ready
+    if (!seq) DR_CUDA(cudaStreamWaitEvent(s1, C.ev[1], 0));
+    {   // net: Y_net = Z_pins Wn_pins + densify(H_n) Wr_pins + b_pins   (Eq. 7, 9)
+        ProjFwdArgs a;
+        a.n = nn; a.Ka = L->d_cell; a.N = L->d_out;
+        a.Za = z[DR_PINS]; a.Wa = L->wn[DR_PINS]; a.ba = L->b[DR_PINS];
+        a.Wr = L->wr[DR_PINS]; a.hval = hnv; a.hidx = hni; a.k = L->k_net;
+        a.y = yn;
+        launch_proj_fwd(a, s1);
+    }
+    if (!seq) DR_CUDA(cudaStreamWaitEvent(s0, C.ev[2], 0));
+    {   // cell: Y_cell = max(Y_near, Y_pinned), M   (Eq. 6, 8, 14)
+        ProjFwdArgs a;
+        a.n = nc; a.Ka = L->d_cell; a.Kb = L->d_net; a.N = L->d_out;
+        a.Za = z[DR_NEAR]; a.Wa = L->wn[DR_NEAR]; a.ba = L->b[DR_NEAR];
+        a.Wr = L->wr[DR_NEAR]; a.hval = hcv; a.hidx = hci; a.k = L->k_cell;
+        a.Zb = z[DR_PINNED]; a.Wb = L->wn[DR_PINNED]; a.bb = L->b[DR_PINNED];
+        a.merge = L->merge;
+        a.y = yc;
+        a.mask = (uint32_t *)(tp + T.mask);
+        if (flags & DR_FWD_TAPS) {
+            a.tap_a = (float *)(tp + T.tap_a);
+            a.tap_b = (float *)(tp + T.tap_b);
+        }
+        launch_proj_fwd(a, s0);
+    }
+    if (!seq) {
+        wait_on(st, s0, C.ev[3]);
+        wait_on(st, s1, C.ev[4]);
+        wait_on(st, s2, C.ev[5]);
+    }
+}
+
+static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, const float *dyc,
+                           const float *dyn, float *dxc, float *dxn, dr_layer_grad *G,
+                           uint32_t flags, cudaStream_t st) {
+    const TapeLayout T = tape_layout(g, L, flags);
+    char *tp = (char *)tape;
+    const float *hcv = (float *)(tp + T.hc_val), *hnv = (float *)(tp + T.hn_val);
+    const uint8_t *hci = (uint8_t *)(tp + T.hc_idx), *hni = (uint8_t *)(tp + T.hn_idx);
+    const uint32_t *mask = (uint32_t *)(tp + T.mask);
+    float *z[3], *dz[3];
+    for (int r = 0; r < 3; ++r) {
+        z[r] = (float *)(tp + T.z[r]);
+        dz[r] = (float *)(tp + T.dz[r]);
+    }
+    float *root_c = (float *)(tp + T.root_c), *root_n = (float *)(tp + T.root_n);
+    float *work[3];
+    for (int q = 0; q < 3; ++q) work[q] = (float *)(tp + T.work[q]);
+    const int mode_near = L->merge == DR_MERGE_MAX ? kMaskM : kMaskNone;        // Eq. 12
+    const int mode_pinned = L->merge == DR_MERGE_MAX ? kMaskNotM : kMaskNone;   // Eq. 13
+    const bool seq = (flags & DR_FWD_SEQUENTIAL) != 0;
+    StreamCtx &C = ctx();
+    cudaStream_t s0 = seq ? st : C.s[0], s1 = seq ? st : C.s[1], s2 = seq ? st : C.s[2];
+    if (!seq) {
+        DR_CUDA(cudaEventRecord(C.fork, st));
+        for (int q = 0; q < 3; ++q) DR_CUDA(cudaStreamWaitEvent(C.s[q], C.fork, 0));
+    }
+    const int nc = g->n_cell, nn = g->n_net, D = L->d_out;
+    auto dw = [&](int64_t n, int K, const float *Zd, const float *hv, const uint8_t *hi, int k,
+                  const float *dy, int mode, float *gw, float *gb, float *wk, cudaStream_t s) {
+        DwArgs a;
+        a.n = n; a.K = K; a.N = D; a.Z = Zd; a.hval = hv; a.hidx = hi; a.k = k;
+        a.dy = dy; a.mask = mask; a.mask_mode = mode;
+        launch_dw(a, gw, gb, wk, s);
+    };
+    if (dxc || dxn) {
+        auto dzk = [&](int64_t n, int K, const float *dy, int mode, const float *W,
+                       const float *c, float *out, cudaStream_t s) {
+            ProjBwdArgs a;
+            a.n = n; a.N = D; a.K = K; a.dy = dy; a.mask = mask; a.mask_mode = mode;
+            a.W = W; a.c = c; a.dz = out;
+            launch_proj_bwd_dz(a, s);
+        };
+        auto rootk = [&](int64_t n, int k, const float *dy, int mode, const float *Wr,
+                         const uint8_t *hi, float *out, cudaStream_t s) {
+            RootArgs a;
+            a.n = n; a.N = D; a.k = k; a.dy = dy; a.mask = mask; a.mask_mode = mode;
+            a.Wr = Wr; a.hidx = hi; a.out = out;
+            launch_root_dots(a, s);
+        };
+        // dZ'_psi = c_psi (dY_psi Wn_psi^T)  (row-scaled by the destination normaliser)
+        dzk(nc, L->d_cell, dyc, mode_near, L->wn[DR_NEAR], g->rel[DR_NEAR].c, dz[DR_NEAR], s0);
+        if (L->wr[DR_NEAR]) rootk(nc, L->k_cell, dyc, mode_near, L->wr[DR_NEAR], hci, root_c, s0);
+        dzk(nn, L->d_cell, dyn, kMaskNone, L->wn[DR_PINS], g->rel[DR_PINS].c, dz[DR_PINS], s1);
+        if (L->wr[DR_PINS]) rootk(nn, L->k_net, dyn, kMaskNone, L->wr[DR_PINS], hni, root_n, s1);
+        if (!seq) DR_CUDA(cudaEventRecord(C.ev[0], s1));                           // dZ_pins, root_n
+        dzk(nc, L->d_net, dyc, mode_pinned, L->wn[DR_PINNED], g->rel[DR_PINNED].c,
+            dz[DR_PINNED], s2);
+        // SSpMM per source node type (Alg. 2 stage 2-3, ownership instead of atomics)
+        if (dxc) {
+            if (!seq) DR_CUDA(cudaStreamWaitEvent(s0, C.ev[0], 0));
+            BwdTerm t0{&g->rel[DR_NEAR], dz[DR_NEAR], false}, t1{&g->rel[DR_PINS], dz[DR_PINS], false};
+            launch_spmm_bwd(g->src_cell, nc, t0, t1, L->wr[DR_NEAR] ? root_c : nullptr, hci,
+                            L->k_cell, L->d_cell, nullptr, dxc, false, s0);
+        }
+        if (dxn) {
+            if (!seq) DR_CUDA(cudaStreamWaitEvent(s2, C.ev[0], 0));
+            BwdTerm t0{&g->rel[DR_PINNED], dz[DR_PINNED], false}, t1{};
+            launch_spmm_bwd(g->src_net, nn, t0, t1, L->wr[DR_PINS] ? root_n : nullptr, hni,
+                            L->k_net, L->d_net, nullptr, dxn, false, s2);
+        }
+    }
+    // weight gradients: dW = Z^T dY_psi, dWr = H^T dY_psi, db = colsum(dY_psi)
+    dw(nc, L->d_cell, z[DR_NEAR], nullptr, nullptr, 0, dyc, mode_near, G->wn[DR_NEAR],
+       G->b[DR_NEAR], work[0], s0);
+    if (L->wr[DR_NEAR])
+        dw(nc, L->d_cell, nullptr, hcv, hci, L->k_cell, dyc, mode_near, G->wr[DR_NEAR], nullptr,
+           work[0], s0);
+    dw(nc, L->d_net, z[DR_PINNED], nullptr, nullptr, 0, dyc, mode_pinned, G->wn[DR_PINNED],
+       G->b[DR_PINNED], work[2], s2);
+    dw(nn, L->d_cell, z[DR_PINS], nullptr, nullptr, 0, dyn, kMaskNone, G->wn[DR_PINS],
+       G->b[DR_PINS], work[1], s1);
+    if (L->wr[DR_PINS])
+        dw(nn, L->d_net, nullptr, hnv, hni, L->k_net, dyn, kMaskNone, G->wr[DR_PINS], nullptr,
+           work[1], s1);
+    if (!seq) {
+        wait_on(st, s0, C.ev[3]);
+        wait_on(st, s1, C.ev[4]);
+        wait_on(st, s2, C.ev[5]);
+    }
+}
+
+// ------------------------------------------------------------------ NCCL (loaded at run time)
+struct NcclApi {
+    bool ok = false;
+    std::string err;
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*commCount)(const ncclComm_t, int *) = nullptr;
+    ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
+                              ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*getErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi &nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            api.err = dlerror();
+            return;
+        }
+        api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+        api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+        api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+        api.commCount = (decltype(api.commCount))dlsym(h, "ncclCommCount");
+        api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+        api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+        api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.commCount &&
+                 api.allReduce && api.getErrorString;
+        if (!api.ok) api.err = "missing NCCL symbols";
+    });
+    if (!api.ok) fail(DR_ERR_NCCL, "cannot load NCCL: " + api.err);
+    return api;
+}
+
+#define DR_NCCL(call)                                                                        \
+    do {                                                                                     \
+        ncclResult_t r_ = (call);                                                            \
+        if (r_ != ncclSuccess) fail(DR_ERR_NCCL, std::string(#call) + ": " + nccl().getErrorString(r_)); \
+    } while (0)
+
+}  // namespace dr
+
+using namespace dr;
+
+// ------------------------------------------------------------------ trainer
+struct dr_trainer {
+    dr_train_cfg cfg{};
+    float *params = nullptr;
+    int64_t n_params = 0;
+    ncclComm_t comm = nullptr;
+    int world = 1;
+    Alloc alloc;
+    float *grad = nullptr, *m = nullptr, *v = nullptr, *scalars = nullptr;  // scalars: loss
+    int64_t step = 0;
+    char *ws = nullptr;
+    size_t ws_cap = 0;
+    std::vector<dr_layer> L;
+    std::vector<dr_layer_grad> G;
+    float *head_w = nullptr, *head_b = nullptr, *ghead_w = nullptr, *ghead_b = nullptr;
+};
+
+namespace {
+
+int64_t layer_params(int dc, int dn, int D) {
+    return (int64_t)dc * D * 3 + (int64_t)dn * D * 2 + 3 * (int64_t)D;
+}
+
+// Carve per-layer weight pointers out of a flat buffer (layout documented in dr.h).
+template <typename LayerT, typename P>
+void carve(const dr_train_cfg &c, P *base, std::vector<LayerT> &out, P **hw, P **hb) {
+    out.clear();
+    P *p = base;
+    int dc = c.d_in_cell, dn = c.d_in_net;
+    const int D = c.d_hidden;
+    for (int l = 0; l < c.n_layers; ++l) {
+        LayerT x{};
+        x.wn[DR_NEAR] = p; p += (int64_t)dc * D;
+        x.wr[DR_NEAR] = p; p += (int64_t)dc * D;
+        x.b[DR_NEAR] = p; p += D;
+        x.wn[DR_PINNED] = p; p += (int64_t)dn * D;
+        x.b[DR_PINNED] = p; p += D;
+        x.wn[DR_PINS] = p; p += (int64_t)dc * D;
+        x.wr[DR_PINS] = p; p += (int64_t)dn * D;
+        x.b[DR_PINS] = p; p += D;
+        x.wr[DR_PINNED] = nullptr;
+        out.push_back(x);
+        dc = dn = D;
+    }
+    *hw = p; p += D;
+    *hb = p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *dr_status_str(dr_status s) {
+    switch (s) {
+        case DR_OK: return "DR_OK";
+        case DR_ERR_INVALID_ARGUMENT: return "DR_ERR_INVALID_ARGUMENT";
+        case DR_ERR_BAD_K: return "DR_ERR_BAD_K";
+        case DR_ERR_SHAPE_MISMATCH: return "DR_ERR_SHAPE_MISMATCH";
+        case DR_ERR_OUT_OF_RANGE: return "DR_ERR_OUT_OF_RANGE";
+        case DR_ERR_DUPLICATE_EDGE: return "DR_ERR_DUPLICATE_EDGE";
+        case DR_ERR_TRANSPOSE_MISMATCH: return "DR_ERR_TRANSPOSE_MISMATCH";
+        case DR_ERR_NONFINITE: return "DR_ERR_NONFINITE";
+        case DR_ERR_TAPE_MISMATCH: return "DR_ERR_TAPE_MISMATCH";
+        case DR_ERR_OUT_OF_MEMORY: return "DR_ERR_OUT_OF_MEMORY";
+        case DR_ERR_CUDA: return "DR_ERR_CUDA";
+        case DR_ERR_NCCL: return "DR_ERR_NCCL";
+        case DR_ERR_UNSUPPORTED: return "DR_ERR_UNSUPPORTED";
+    }
+    return "DR_ERR_UNKNOWN";
+}
+
+const char *dr_last_error(void) { return t_err.c_str(); }
+
+const char *dr_version(void) { return "libdr 0.1 sm_100a (DR-CircuitGNN hot path, arXiv 2508.16769)"; }
+
+int64_t dr_launch_count(void) { return t_launches; }
+void dr_launch_count_reset(void) { t_launches = 0; }
+
+#define DR_API_BEGIN                                                                         \
+    clear_error();                                                                           \
+    try {
+#define DR_API_END                                                                           \
+    }                                                                                        \
+    catch (const Error &e) {                                                                 \
+        set_error(e.status, e.msg);                                                          \
+        return e.status;                                                                     \
+    }                                                                                        \
+    catch (const std::bad_alloc &) {                                                         \
+        set_error(DR_ERR_OUT_OF_MEMORY, "host allocation failed");                           \
+        return DR_ERR_OUT_OF_MEMORY;                                                         \
+    }                                                                                        \
+    return DR_OK;
+
+dr_status dr_drelu_topk(const float *x, int64_t n, int32_t dim, int64_t ldx, dr_cbsr *out,
+                        void *stream) {
+    DR_API_BEGIN
+    check_cbsr(out, "drelu out");
+    DR_CHECK(n >= 0 && out->n == n && out->dim == dim, DR_ERR_SHAPE_MISMATCH,
+             "drelu: out->n/dim must equal n/dim");
+    DR_CHECK(ldx >= dim, DR_ERR_SHAPE_MISMATCH, "drelu: ldx < dim");
+    DR_CHECK(n == 0 || x, DR_ERR_INVALID_ARGUMENT, "drelu: null x");
+    launch_drelu(x, n, dim, ldx, out->k, out->val, (uint8_t *)out->idx, (cudaStream_t)stream);
+    DR_API_END
+}
+
+dr_status dr_spmm_fwd(const dr_graph *g, dr_rel r, const dr_cbsr *h, float *z, void *stream) {
+    DR_API_BEGIN
+    DR_CHECK(g != nullptr, DR_ERR_INVALID_ARGUMENT, "spmm_fwd: null graph");
+    DR_CHECK(r >= 0 && r < 3, DR_ERR_INVALID_ARGUMENT, "spmm_fwd: bad relation");
+    check_cbsr(h, "spmm_fwd h_src");
+    const RelDev &R = g->rel[r];
+    DR_CHECK(h->n == R.n_src, DR_ERR_SHAPE_MISMATCH, "spmm_fwd: h_src->n != relation n_src");
+    DR_CHECK(R.n_dst == 0 || z, DR_ERR_INVALID_ARGUMENT, "spmm_fwd: null z");
+    launch_spmm_fwd(R, h->val, (const uint8_t *)h->idx, h->k, h->dim, z, (cudaStream_t)stream);
+    DR_API_END
+}
+
+dr_status dr_spmm_bwd(const dr_graph *g, dr_rel r, const float *dz, const dr_cbsr *h,
+                      float *g_kept, float *dx, int32_t accumulate, void *stream) {
+    DR_API_BEGIN
+    DR_CHECK(g != nullptr, DR_ERR_INVALID_ARGUMENT, "spmm_bwd: null graph");
+    DR_CHECK(r >= 0 && r < 3, DR_ERR_INVALID_ARGUMENT, "spmm_bwd: bad relation");
+    check_cbsr(h, "spmm_bwd h_src");
+    const RelDev &R = g->rel[r];
+    DR_CHECK(h->n == R.n_src, DR_ERR_SHAPE_MISMATCH, "spmm_bwd: h_src->n != relation n_src");
+    DR_CHECK(g_kept || dx, DR_ERR_INVALID_ARGUMENT, "spmm_bwd: both outputs NULL");
+    DR_CHECK(R.n_dst == 0 || dz, DR_ERR_INVALID_ARGUMENT, "spmm_bwd: null dz");
+    SrcSched sched;
+    sched.n = R.n_src;
+    sched.order = R.orderT;
+    sched.n_hub = R.n_hubT;
+    BwdTerm t0{&R, dz, true}, t1{};
+    launch_spmm_bwd(sched, R.n_src, t0, t1, nullptr, (const uint8_t *)h->idx, h->k, h->dim,
+                    g_kept, dx, accumulate != 0, (cudaStream_t)stream);
+    DR_API_END
+}
+
+dr_status dr_heteroconv_tape_bytes(const dr_graph *g, const dr_layer *L, uint32_t flags,
+                                   size_t *bytes) {
+    DR_API_BEGIN
+    check_layer(g, L);
+    DR_CHECK(bytes != nullptr, DR_ERR_INVALID_ARGUMENT, "null bytes");
+    *bytes = tape_layout(g, L, flags).total;
+    DR_API_END
+}
+
+dr_status dr_heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *x_cell,
+                            const float *x_net, float *y_cell, float *y_net, void *tape,
+                            uint32_t flags, void *stream) {
+    DR_API_BEGIN
+    check_layer(g, L);
+    DR_CHECK(tape != nullptr, DR_ERR_TAPE_MISMATCH, "null tape");
+    DR_CHECK((g->n_cell == 0 || (x_cell && y_cell)) && (g->n_net == 0 || (x_net && y_net)),
+             DR_ERR_INVALID_ARGUMENT, "heteroconv_fwd: null input/output");
+    heteroconv_fwd(g, L, x_cell, x_net, y_cell, y_net, tape, flags, (cudaStream_t)stream);
+    DR_API_END
+}
+
+dr_status dr_heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape,
+                            const float *dy_cell, const float *dy_net, float *dx_cell,
+                            float *dx_net, dr_layer_grad *grads, uint32_t flags, void *stream) {
+    DR_API_BEGIN
+    check_layer(g, L);
+    DR_CHECK(tape != nullptr, DR_ERR_TAPE_MISMATCH, "null tape");
+    DR_CHECK(grads != nullptr, DR_ERR_INVALID_ARGUMENT, "null grads");
+    for (int r = 0; r < 3; ++r) {
+        DR_CHECK(grads->wn[r] && grads->b[r], DR_ERR_INVALID_ARGUMENT, "null grad wn/b");
+        DR_CHECK(!L->wr[r] || grads->wr[r], DR_ERR_INVALID_ARGUMENT, "null grad wr");
+    }
+    DR_CHECK(dy_cell && dy_net, DR_ERR_INVALID_ARGUMENT, "null dy");
+    heteroconv_bwd(g, L, tape, dy_cell, dy_net, dx_cell, dx_net, grads, flags,
+                   (cudaStream_t)stream);
+    DR_API_END
+}
+
+dr_status dr_heteroconv_tape_view(const dr_graph *g, const dr_layer *L, void *tape,
+                                  uint32_t flags, dr_tape_view *v) {
+    DR_API_BEGIN
+    check_layer(g, L);
+    DR_CHECK(tape && v, DR_ERR_INVALID_ARGUMENT, "null tape/view");
+    const TapeLayout T = tape_layout(g, L, flags);
+    char *tp = (char *)tape;
+    std::memset(v, 0, sizeof(*v));
+    v->h_cell = dr_cbsr{g->n_cell, L->d_cell, L->k_cell, 1, tp + T.hc_idx, (float *)(tp + T.hc_val)};
+    v->h_net = dr_cbsr{g->n_net, L->d_net, L->k_net, 1, tp + T.hn_idx, (float *)(tp + T.hn_val)};
+    for (int r = 0; r < 3; ++r) v->z[r] = (float *)(tp + T.z[r]);
+    if (flags & DR_FWD_TAPS) {
+        v->y_near = (float *)(tp + T.tap_a);
+        v->y_pinned = (float *)(tp + T.tap_b);
+    }
+    v->mask = (uint32_t *)(tp + T.mask);
+    DR_API_END
+}
+
+int64_t dr_train_param_count(const dr_train_cfg *c) {
+    if (!c || c->n_layers < 1) return -1;
+    int64_t n = 0;
+    int dc = c->d_in_cell, dn = c->d_in_net;
+    for (int l = 0; l < c->n_layers; ++l) {
+        n += layer_params(dc, dn, c->d_hidden);
+        dc = dn = c->d_hidden;
+    }
+    return n + c->d_hidden + 1;
+}
+
+dr_status dr_trainer_create(const dr_train_cfg *c, float *params, int64_t n_params,
+                            void *nccl_comm, const dr_allocator *a, dr_trainer **out) {
+    dr_trainer *t = nullptr;
+    DR_API_BEGIN
+    DR_CHECK(c && params && out, DR_ERR_INVALID_ARGUMENT, "null cfg/params/out");
+    *out = nullptr;
+    DR_CHECK(c->n_layers >= 1 && c->n_layers <= 8, DR_ERR_INVALID_ARGUMENT, "n_layers in [1,8]");
+    DR_CHECK(dr_train_param_count(c) == n_params, DR_ERR_SHAPE_MISMATCH,
+             "n_params != dr_train_param_count(cfg)");
+    check_k(c->k_cell, c->d_in_cell, "cfg k_cell/d_in_cell");
+    check_k(c->k_net, c->d_in_net, "cfg k_net/d_in_net");
+    check_k(c->k_cell, c->d_hidden, "cfg k_cell/d_hidden");
+    check_k(c->k_net, c->d_hidden, "cfg k_net/d_hidden");
+    check_out_width(c->d_hidden, "cfg d_hidden");
+    check_out_width(c->d_in_cell, "cfg d_in_cell");
+    check_out_width(c->d_in_net, "cfg d_in_net");
+    t = new dr_trainer();
+    t->cfg = *c;
+    t->params = params;
+    t->n_params = n_params;
+    if (a && a->alloc && a->free) {
+        t->alloc.a = *a;
+        t->alloc.custom = true;
+    }
+    if (nccl_comm) {
+        t->comm = (ncclComm_t)nccl_comm;
+        DR_NCCL(nccl().commCount(t->comm, &t->world));
+    }
+    const size_t pb = (size_t)n_params * 4;
+    char *blk = (char *)t->alloc.get(al(pb) * 3 + 256, nullptr);
+    t->grad = (float *)blk;
+    t->m = (float *)(blk + al(pb));
+    t->v = (float *)(blk + 2 * al(pb));
+    t->scalars = (float *)(blk + 3 * al(pb));
+    DR_CUDA(cudaMemset(blk, 0, al(pb) * 3 + 256));
+    DR_CUDA(cudaDeviceSynchronize());
+    carve(t->cfg, (const float *)t->params, t->L, (const float **)&t->head_w, (const float **)&t->head_b);
+    carve(t->cfg, t->grad, t->G, &t->ghead_w, &t->ghead_b);
+    for (auto &l : t->L) {
+        l.d_out = c->d_hidden;
+        l.k_cell = c->k_cell;
+        l.k_net = c->k_net;
+        l.merge = DR_MERGE_MAX;
+    }
+    int dc = c->d_in_cell, dn = c->d_in_net;
+    for (auto &l : t->L) {
+        l.d_cell = dc;
+        l.d_net = dn;
+        dc = dn = c->d_hidden;
+    }
+    *out = t;
+    t = nullptr;
+    DR_API_END
+}
+
+dr_status dr_train_step(dr_trainer *t, const dr_graph *g, const float *x_cell, const float *x_net,
+                        const float *labels, float *loss_host, float *grad_out, void *stream) {
+    DR_API_BEGIN
+    DR_CHECK(t && g, DR_ERR_INVALID_ARGUMENT, "null trainer/graph");
+    DR_CHECK((g->n_cell == 0 || (x_cell && labels)) && (g->n_net == 0 || x_net),
+             DR_ERR_INVALID_ARGUMENT, "null inputs");
+    cudaStream_t st = (cudaStream_t)stream;
+    const dr_train_cfg &c = t->cfg;
+    const int nl = c.n_layers, D = c.d_hidden;
+    const size_t nc = (size_t)g->n_cell, nn = (size_t)g->n_net;
+    // ---- workspace (grow-only): tapes, layer outputs, gradient ping-pong
+    std::vector<size_t> tape_off(nl);
+    size_t off = 0;
+    for (int l = 0; l < nl; ++l) {
+        tape_off[l] = off;
+        off += al(tape_layout(g, &t->L[l], 0).total);
+    }
+    const size_t y_off = off;
+    off += nl * (al(nc * D * 4) + al(nn * D * 4));
+    const size_t dy_off = off;
+    off += 2 * (al(nc * D * 4) + al(nn * D * 4));
+    const size_t head_off = off;
+    off += al(head_work_floats(D) * 4);
+    const size_t dxin_off = off;
+    off += al(nc * (size_t)c.d_in_cell * 4) + al(nn * (size_t)c.d_in_net * 4);   // unused dx of layer 0
+    (void)dxin_off;
+    if (off > t->ws_cap) {
+        if (t->ws) {
+            DR_CUDA(cudaStreamSynchronize(st));
+            t->alloc.put(t->ws, st);
+        }
+        t->ws = (char *)t->alloc.get(off, st);
+        t->ws_cap = off;
+    }
+    char *ws = t->ws;
+    auto yc = [&](int l) { return (float *)(ws + y_off + l * (al(nc * D * 4) + al(nn * D * 4))); };
+    auto yn = [&](int l) { return (float *)(ws + y_off + l * (al(nc * D * 4) + al(nn * D * 4)) + al(nc * D * 4)); };
+    auto dyc = [&](int q) { return (float *)(ws + dy_off + q * (al(nc * D * 4) + al(nn * D * 4))); };
+    auto dyn = [&](int q) { return (float *)(ws + dy_off + q * (al(nc * D * 4) + al(nn * D * 4)) + al(nc * D * 4)); };
+    // ---- forward
+    const float *xc = x_cell, *xn = x_net;
+    for (int l = 0; l < nl; ++l) {
+        heteroconv_fwd(g, &t->L[l], xc, xn, yc(l), yn(l), ws + tape_off[l], 0, st);
+        xc = yc(l);
+        xn = yn(l);
+    }
+    // ---- head + MSE
+    {
+        HeadArgs h;
+        h.n = (int64_t)nc; h.N = D; h.y = yc(nl - 1); h.w = t->head_w; h.b = t->head_b;
+        h.labels = labels; h.dy = dyc(0); h.grad_w = t->ghead_w; h.grad_b = t->ghead_b;
+        h.loss = t->scalars; h.work = (float *)(ws + head_off);
+        launch_head_mse(h, st);
+    }
+    DR_CUDA(cudaMemsetAsync(dyn(0), 0, nn * D * 4, st));   // last layer's Y_net feeds nothing
+    // ---- backward
+    int cur = 0;
+    for (int l = nl - 1; l >= 0; --l) {
+        float *dxc = l > 0 ? dyc(cur ^ 1) : nullptr;
+        float *dxn = l > 0 ? dyn(cur ^ 1) : nullptr;
+        heteroconv_bwd(g, &t->L[l], ws + tape_off[l], dyc(cur), dyn(cur), dxc, dxn, &t->G[l], 0, st);
+        cur ^= 1;
+    }
+    // ---- data-parallel gradient exchange: one allreduce (sum) of the flat gradient
+    if (t->comm && t->world > 1)
+        DR_NCCL(nccl().allReduce(t->grad, t->grad, (size_t)t->n_params, ncclFloat32, ncclSum,
+                                 t->comm, st));
+    const float inv_world = 1.0f / (float)t->world;
+    if (grad_out) {
+        DR_CUDA(cudaMemcpyAsync(grad_out, t->grad, (size_t)t->n_params * 4,
+                                cudaMemcpyDeviceToDevice, st));
+        if (t->world > 1) launch_scale(grad_out, t->n_params, inv_world, st);
+    }
+    // ---- Adam (1/W mean folded in)
+    t->step += 1;
+    const double bc1 = 1.0 - std::pow((double)c.beta1, (double)t->step);
+    const double bc2 = 1.0 - std::pow((double)c.beta2, (double)t->step);
+    launch_adam(t->params, t->grad, t->m, t->v, t->n_params, c.lr, c.weight_decay, c.beta1,
+                c.beta2, c.eps, (float)bc1, (float)bc2, inv_world, st);
+    if (loss_host)
+        DR_CUDA(cudaMemcpyAsync(loss_host, t->scalars, 4, cudaMemcpyDeviceToHost, st));
+    DR_API_END
+}
+
+dr_status dr_trainer_destroy(dr_trainer *t) {
+    if (!t) return DR_OK;
+    cudaDeviceSynchronize();
+    if (t->ws) t->alloc.put(t->ws, nullptr);
+    if (t->grad) t->alloc.put(t->grad, nullptr);
+    delete t;
+    return DR_OK;
+}
+
+dr_status dr_nccl_unique_id(void *id128) {
+    DR_API_BEGIN
+    DR_CHECK(id128 != nullptr, DR_ERR_INVALID_ARGUMENT, "null id");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    DR_NCCL(nccl().getUniqueId(&id));
+    std::memcpy(id128, &id, sizeof(id));
+    DR_API_END
+}
+
+dr_status dr_nccl_comm_init(const void *id128, int32_t nranks, int32_t rank, void **comm) {
+    DR_API_BEGIN
+    DR_CHECK(id128 && comm && nranks >= 1 && rank >= 0 && rank < nranks,
+             DR_ERR_INVALID_ARGUMENT, "bad nccl init args");
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    ncclComm_t c = nullptr;
+    DR_NCCL(nccl().commInitRank(&c, nranks, id, rank));
+    *comm = (void *)c;
+    DR_API_END
+}
+
+dr_status dr_nccl_comm_destroy(void *comm) {
+    DR_API_BEGIN
+    if (comm) DR_NCCL(nccl().commDestroy((ncclComm_t)comm));
+    DR_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+// dr_internal.h — internal types of libdr (B200 / sm_100a). Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/dr.h"
+
+namespace dr {
+
+// ------------------------------------------------------------------ errors
+struct Error {
+    dr_status status;
+    std::string msg;
+};
+void set_error(dr_status s, const std::string &msg);
+void clear_error();
+[[noreturn]] void fail(dr_status s, const std::string &msg);
+
+#define DR_CUDA(call)                                                                        \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            ::dr::fail(DR_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+    } while (0)
+#define DR_CHECK(cond, status, msg)                                                          \
+    do {                                                                                     \
+        if (!(cond)) ::dr::fail(status, msg);                                                \
+    } while (0)
+
+// Launch bookkeeping: count kernels and surface launch errors immediately.
+void note_launch(const char *name);
+
+// ------------------------------------------------------------------ allocation
+struct Alloc {
+    dr_allocator a{};
+    bool custom = false;
+    void *get(size_t bytes, cudaStream_t s);
+    void put(void *p, cudaStream_t s);
+};
+
+// ------------------------------------------------------------------ device graph
+// Rows whose work exceeds this many neighbours go to the CTA-per-row kernels
+// (Alg. 1 stage 2 "high degree" class); the rest are packed several
+// rows per warp (one sub-warp of k/P lanes per row, "partition into
+// ceil(32/K) parts").
+constexpr int kHubDeg = 256;
+
+struct RelDev {
+    int32_t n_dst = 0, n_src = 0;
+    int64_t nnz = 0;
+    dr_module module = DR_SAGE_MEAN;
+    // forward: CSR rows = destinations
+    int32_t *rowptr = nullptr;   // [n_dst+1]
+    int32_t *col = nullptr;      // [nnz]
+    float *ew = nullptr;         // [nnz] a_e * s_col(e); nullptr when identically 1
+    float *c = nullptr;          // [n_dst]
+    float *s = nullptr;          // [n_src]
+    int32_t *order = nullptr;    // [n_dst] hubs first (desc degree), then desc degree
+    int32_t n_hub = 0;
+    // backward: CSC rows = sources
+    int32_t *colptr = nullptr;   // [n_src+1]
+    int32_t *row = nullptr;      // [nnz]
+    float *ewT = nullptr;        // [nnz] a_ij in CSC order; nullptr when identically 1
+    int32_t *orderT = nullptr;   // [n_src] source processing order for this relation alone
+    int32_t n_hubT = 0;
+    int32_t max_deg_dst = 0, max_deg_src = 0;
+};
+
+// Source-side schedule for the fused per-source-type SSpMM (cell sources sum
+// near + pins, net sources use pinned; Alg. 2 stage 2 "for each source node
+// type").
+struct SrcSched {
+    int32_t n = 0;
+    int32_t *order = nullptr;
+    int32_t n_hub = 0;
+};
+
+}  // namespace dr
+
+struct dr_graph {
+    int32_t n_cell = 0, n_net = 0;
+    dr::RelDev rel[3];
+    dr::SrcSched src_cell, src_net;
+    dr::Alloc alloc;
+    std::vector<void *> blocks;
+    size_t bytes = 0;
+    cudaStream_t create_stream = nullptr;
+};
+
+namespace dr {
+
+// ------------------------------------------------------------------ kernels (launchers)
+// D-ReLU (Eq. 2-3): x [n x dim] (ld ldx) -> CBSR val [n x k], idx [n x k] (uint8).
+void launch_drelu(const float *x, int64_t n, int dim, int64_t ldx, int k, float *val,
+                  uint8_t *idx, cudaStream_t s);
+
+// DR-SpMM forward of one relation: z [n_dst x dim] = diag(c) A diag(s) densify(H).
+void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
+                     float *z, cudaStream_t s);
+
+// SSpMM backward for one source node type, summing up to two relations that
+// share the source type. Term q in {0,1}: relation rel[q] (CSC), its dz, and
+// whether the kernel applies c_i per edge (standalone ABI) or dz is already
+// row-scaled (fused path). root (n_src x k) is added if non-null.
+struct BwdTerm {
+    const RelDev *rel = nullptr;
+    const float *dz = nullptr;
+    bool apply_c = false;
+};
+void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1,
+                     const float *root, const uint8_t *hidx, int k, int dim, float *g_kept,
+                     float *dx, bool accumulate, cudaStream_t s);
+
+}  // namespace dr

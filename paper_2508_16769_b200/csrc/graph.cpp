@@ -1,0 +1,375 @@
+// graph.cpp — dr_graph_create / destroy: host preprocessing of the three
+// relation subgraphs and their device upload.
+//
+// Alg. 1 stage 1: encode each adjacency as CSR (rows =
+// destinations, Eq. 4); Alg. 2 stage 1: transpose to CSC for the
+// backward; Alg. 1 stage 2: classify rows by degree (hub rows ->
+// CTA-per-row kernel, others packed by descending degree). §3.4:
+// the three subgraphs are initialised concurrently on worker threads, each
+// uploading on its own CUDA stream.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <thread>
+
+#include "dr_internal.h"
+
+namespace dr {
+namespace {
+
+struct HostRel {
+    int32_t n_dst = 0, n_src = 0;
+    int64_t nnz = 0;
+    dr_module module = DR_SAGE_MEAN;
+    std::vector<int32_t> rowptr, col, order, colptr, row, orderT;
+    std::vector<float> ew, c, s, ewT;
+    std::vector<int32_t> deg_in, deg_out;
+    int32_t n_hub = 0, n_hubT = 0, max_in = 0, max_out = 0;
+    bool weighted = false;
+    dr_status st = DR_OK;
+    std::string err;
+};
+
+// Hubs (deg > kHubDeg) first, by descending degree; then the rest by
+// descending degree (stable on id), or in id order when `identity`.
+void make_order(const std::vector<int32_t> &deg, bool identity, std::vector<int32_t> &order,
+                int32_t &n_hub) {
+    const int32_t n = (int32_t)deg.size();
+    order.resize(n);
+    if (identity) {
+        std::iota(order.begin(), order.end(), 0);
+        n_hub = 0;
+        return;
+    }
+    int32_t dmax = 0;
+    for (int32_t d : deg) dmax = std::max(dmax, d);
+    std::vector<int64_t> cnt((size_t)dmax + 2, 0);
+    for (int32_t d : deg) cnt[(size_t)(dmax - d) + 1]++;            // descending degree
+    for (size_t b = 1; b < cnt.size(); ++b) cnt[b] += cnt[b - 1];
+    for (int32_t i = 0; i < n; ++i) order[(size_t)cnt[(size_t)(dmax - deg[i])]++] = i;
+    n_hub = 0;
+    while (n_hub < n && deg[order[n_hub]] > kHubDeg) ++n_hub;
+}
+
+void build_rel(const dr_rel_desc &d, bool validate, bool identity, HostRel &h) {
+    h.n_dst = d.n_dst;
+    h.n_src = d.n_src;
+    h.nnz = d.nnz;
+    h.module = d.module;
+    const int64_t *rp = d.row_ptr;
+    const int32_t *ci = d.col_idx;
+    if (validate) {
+        if (rp[0] != 0 || rp[d.n_dst] != d.nnz) {
+            h.st = DR_ERR_OUT_OF_RANGE;
+            h.err = "row_ptr[0] != 0 or row_ptr[n_dst] != nnz";
+            return;
+        }
+        for (int32_t i = 0; i < d.n_dst; ++i) {
+            if (rp[i + 1] < rp[i]) {
+                h.st = DR_ERR_OUT_OF_RANGE;
+                h.err = "row_ptr not monotone at row " + std::to_string(i);
+                return;
+            }
+            for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+                if (ci[e] < 0 || ci[e] >= d.n_src) {
+                    h.st = DR_ERR_OUT_OF_RANGE;
+                    h.err = "col_idx out of range at row " + std::to_string(i);
+                    return;
+                }
+                if (e > rp[i] && ci[e] <= ci[e - 1]) {
+                    h.st = DR_ERR_DUPLICATE_EDGE;
+                    h.err = "row " + std::to_string(i) + " not strictly increasing";
+                    return;
+                }
+            }
+        }
+        if (d.val)
+            for (int64_t e = 0; e < d.nnz; ++e)
+                if (!std::isfinite(d.val[e])) {
+                    h.st = DR_ERR_NONFINITE;
+                    h.err = "non-finite edge weight";
+                    return;
+                }
+    }
+    h.weighted = false;
+    if (d.val)
+        for (int64_t e = 0; e < d.nnz && !h.weighted; ++e) h.weighted = d.val[e] != 1.0f;
+    // CSR (int32 offsets) and degrees
+    h.rowptr.resize((size_t)d.n_dst + 1);
+    h.deg_in.resize(d.n_dst);
+    for (int32_t i = 0; i <= d.n_dst; ++i) h.rowptr[i] = (int32_t)rp[i];
+    h.col.assign(ci, ci + d.nnz);
+    h.deg_out.assign((size_t)d.n_src, 0);
+    for (int32_t i = 0; i < d.n_dst; ++i) {
+        h.deg_in[i] = (int32_t)(rp[i + 1] - rp[i]);
+        h.max_in = std::max(h.max_in, h.deg_in[i]);
+    }
+    for (int64_t e = 0; e < d.nnz; ++e) h.deg_out[ci[e]]++;
+    for (int32_t j = 0; j < d.n_src; ++j) h.max_out = std::max(h.max_out, h.deg_out[j]);
+    // normalisers (reading Q12: unweighted counts clamped to >= 1)
+    h.c.resize(d.n_dst);
+    h.s.resize(d.n_src);
+    for (int32_t i = 0; i < d.n_dst; ++i) {
+        const double dg = std::max(h.deg_in[i], 1);
+        h.c[i] = (float)(d.module == DR_SAGE_MEAN ? 1.0 / dg : 1.0 / std::sqrt(dg));
+    }
+    for (int32_t j = 0; j < d.n_src; ++j) {
+        const double dg = std::max(h.deg_out[j], 1);
+        h.s[j] = (float)(d.module == DR_SAGE_MEAN ? 1.0 : 1.0 / std::sqrt(dg));
+    }
+    // forward per-edge weight a_e * s_j (absent when identically 1)
+    if (h.weighted || d.module != DR_SAGE_MEAN) {
+        h.ew.resize(d.nnz);
+        for (int64_t e = 0; e < d.nnz; ++e) h.ew[e] = (d.val ? d.val[e] : 1.0f) * h.s[ci[e]];
+    }
+    // CSC by counting sort (row ids ascending within each column)
+    h.colptr.assign((size_t)d.n_src + 1, 0);
+    for (int32_t j = 0; j < d.n_src; ++j) h.colptr[j + 1] = h.colptr[j] + h.deg_out[j];
+    h.row.resize(d.nnz);
+    if (h.weighted) h.ewT.resize(d.nnz);
+    std::vector<int32_t> fill(h.colptr.begin(), h.colptr.end() - 1);
+    for (int32_t i = 0; i < d.n_dst; ++i)
+        for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+            const int32_t p = fill[ci[e]]++;
+            h.row[p] = i;
+            if (h.weighted) h.ewT[p] = d.val[e];
+        }
+    make_order(h.deg_in, identity, h.order, h.n_hub);
+    make_order(h.deg_out, identity, h.orderT, h.n_hubT);
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+template <typename T>
+size_t vbytes(const std::vector<T> &v) {
+    return align_up(v.size() * sizeof(T));
+}
+
+}  // namespace
+
+void *Alloc::get(size_t bytes, cudaStream_t s) {
+    if (bytes == 0) bytes = 256;
+    void *p = nullptr;
+    if (custom) {
+        p = a.alloc(a.ctx, bytes, (void *)s);
+        if (!p) fail(DR_ERR_OUT_OF_MEMORY, "allocator returned NULL");
+        return p;
+    }
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(DR_ERR_OUT_OF_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    return p;
+}
+
+void Alloc::put(void *p, cudaStream_t s) {
+    if (!p) return;
+    if (custom) a.free(a.ctx, p, (void *)s);
+    else cudaFree(p);
+}
+
+}  // namespace dr
+
+using namespace dr;
+
+extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel_desc rel[3],
+                                     const dr_allocator *a, int32_t n_threads, uint32_t flags,
+                                     void *stream, dr_graph **out) {
+    clear_error();
+    dr_graph *g = nullptr;
+    try {
+        DR_CHECK(out && rel, DR_ERR_INVALID_ARGUMENT, "null rel/out");
+        *out = nullptr;
+        DR_CHECK(n_cell >= 0 && n_net >= 0, DR_ERR_INVALID_ARGUMENT, "negative node count");
+        const int32_t want_dst[3] = {n_cell, n_net, n_cell};
+        const int32_t want_src[3] = {n_cell, n_cell, n_net};
+        const char *names[3] = {"near", "pins", "pinned"};
+        for (int r = 0; r < 3; ++r) {
+            const dr_rel_desc &d = rel[r];
+            DR_CHECK(d.n_dst == want_dst[r] && d.n_src == want_src[r], DR_ERR_SHAPE_MISMATCH,
+                     std::string(names[r]) + ": n_dst/n_src disagree with n_cell/n_net");
+            DR_CHECK(d.nnz >= 0 && d.nnz < (int64_t)INT32_MAX, DR_ERR_UNSUPPORTED,
+                     std::string(names[r]) + ": nnz must be < 2^31");
+            DR_CHECK(d.row_ptr && (d.nnz == 0 || d.col_idx), DR_ERR_INVALID_ARGUMENT,
+                     std::string(names[r]) + ": null CSR pointer");
+            DR_CHECK(d.module == DR_SAGE_MEAN || d.module == DR_GRAPHCONV_SYM,
+                     DR_ERR_INVALID_ARGUMENT, "bad module");
+        }
+        const bool validate = !(flags & DR_GRAPH_SKIP_VALIDATION);
+        const bool identity = (flags & DR_GRAPH_ORDER_IDENTITY) != 0;
+        cudaStream_t cs = (cudaStream_t)stream;
+
+        // ---- phase 1: per-relation host preprocessing on worker threads (§3.4)
+        HostRel h[3];
+        const int nt = n_threads <= 0 ? 3 : std::min(n_threads, 3);
+        {
+            std::vector<std::thread> th;
+            for (int w = 0; w < nt; ++w)
+                th.emplace_back([&, w] {
+                    for (int r = w; r < 3; r += nt) build_rel(rel[r], validate, identity, h[r]);
+                });
+            for (auto &t : th) t.join();
+        }
+        for (int r = 0; r < 3; ++r)
+            if (h[r].st != DR_OK) fail(h[r].st, std::string(names[r]) + ": " + h[r].err);
+        // pinned == pins^T: CSR(pinned) must equal CSC(pins) exactly
+        if (validate) {
+            const bool same = h[DR_PINNED].rowptr == h[DR_PINS].colptr &&
+                              h[DR_PINNED].col == h[DR_PINS].row;
+            DR_CHECK(same, DR_ERR_TRANSPOSE_MISMATCH, "pinned is not the transpose of pins");
+        }
+        const bool pins_T = h[DR_PINNED].rowptr == h[DR_PINS].colptr &&
+                            h[DR_PINNED].col == h[DR_PINS].row;
+        const bool near_sym = h[DR_NEAR].rowptr == h[DR_NEAR].colptr &&
+                              h[DR_NEAR].col == h[DR_NEAR].row;
+
+        // source schedules for the fused per-source-type backward
+        std::vector<int32_t> degc((size_t)n_cell), degn((size_t)n_net), ord_c, ord_n;
+        for (int32_t j = 0; j < n_cell; ++j)
+            degc[j] = h[DR_NEAR].deg_out[j] + h[DR_PINS].deg_out[j];
+        for (int32_t j = 0; j < n_net; ++j) degn[j] = h[DR_PINNED].deg_out[j];
+        int32_t hub_c = 0, hub_n = 0;
+        make_order(degc, identity, ord_c, hub_c);
+        make_order(degn, identity, ord_n, hub_n);
+
+        // ---- phase 2: one device block, carved per array
+        g = new dr_graph();
+        g->n_cell = n_cell;
+        g->n_net = n_net;
+        g->create_stream = cs;
+        if (a && a->alloc && a->free) {
+            g->alloc.a = *a;
+            g->alloc.custom = true;
+        }
+        struct Up {
+            void **dst;
+            const void *src;
+            size_t bytes;
+        };
+        std::vector<Up> ups[4];            // [0..2] per relation, [3] shared
+        size_t total = 0;
+        auto plan = [&](int q, void **dst, const void *src, size_t bytes) {
+            if (bytes == 0) { *dst = nullptr; return; }
+            ups[q].push_back({dst, src, total});
+            *dst = (void *)bytes;           // temporarily the size
+            total += align_up(bytes);
+        };
+        for (int r = 0; r < 3; ++r) {
+            RelDev &d = g->rel[r];
+            HostRel &hr = h[r];
+            d.n_dst = hr.n_dst;
+            d.n_src = hr.n_src;
+            d.nnz = hr.nnz;
+            d.module = hr.module;
+            d.n_hub = hr.n_hub;
+            d.n_hubT = hr.n_hubT;
+            d.max_deg_dst = hr.max_in;
+            d.max_deg_src = hr.max_out;
+            plan(r, (void **)&d.rowptr, hr.rowptr.data(), hr.rowptr.size() * 4);
+            plan(r, (void **)&d.col, hr.col.data(), hr.col.size() * 4);
+            plan(r, (void **)&d.ew, hr.ew.data(), hr.ew.size() * 4);
+            plan(r, (void **)&d.c, hr.c.data(), hr.c.size() * 4);
+            plan(r, (void **)&d.s, hr.s.data(), hr.s.size() * 4);
+            plan(r, (void **)&d.order, hr.order.data(), hr.order.size() * 4);
+            plan(r, (void **)&d.orderT, hr.orderT.data(), hr.orderT.size() * 4);
+            plan(r, (void **)&d.ewT, hr.ewT.data(), hr.ewT.size() * 4);
+            const bool alias = (r == DR_NEAR && near_sym) || (r != DR_NEAR && pins_T);
+            if (!alias) {
+                plan(r, (void **)&d.colptr, hr.colptr.data(), hr.colptr.size() * 4);
+                plan(r, (void **)&d.row, hr.row.data(), hr.row.size() * 4);
+            }
+        }
+        g->src_cell.n = n_cell;
+        g->src_cell.n_hub = hub_c;
+        g->src_net.n = n_net;
+        g->src_net.n_hub = hub_n;
+        plan(3, (void **)&g->src_cell.order, ord_c.data(), ord_c.size() * 4);
+        plan(3, (void **)&g->src_net.order, ord_n.data(), ord_n.size() * 4);
+        char *base = (char *)g->alloc.get(total, cs);
+        g->blocks.push_back(base);
+        g->bytes = total;
+        for (int q = 0; q < 4; ++q)
+            for (Up &u : ups[q]) {
+                const size_t bytes = (size_t)reinterpret_cast<uintptr_t>(*u.dst);
+                *u.dst = base + u.bytes;
+                u.bytes = bytes;
+            }
+        // structural sharing (no second copy): CSC(near) = CSR(near) when symmetric;
+        // CSC(pins) = CSR(pinned) and CSC(pinned) = CSR(pins) when pinned == pins^T.
+        if (near_sym) {
+            g->rel[DR_NEAR].colptr = g->rel[DR_NEAR].rowptr;
+            g->rel[DR_NEAR].row = g->rel[DR_NEAR].col;
+        }
+        if (pins_T) {
+            g->rel[DR_PINNED].colptr = g->rel[DR_PINS].rowptr;
+            g->rel[DR_PINNED].row = g->rel[DR_PINS].col;
+            g->rel[DR_PINS].colptr = g->rel[DR_PINNED].rowptr;
+            g->rel[DR_PINS].row = g->rel[DR_PINNED].col;
+        }
+        // ---- phase 3: uploads, one stream per relation on the worker threads
+        DR_CUDA(cudaStreamSynchronize(cs));
+        dr_status up_st[4] = {DR_OK, DR_OK, DR_OK, DR_OK};
+        std::string up_err[4];
+        {
+            std::vector<std::thread> th;
+            for (int q = 0; q < 4; ++q)
+                th.emplace_back([&, q] {
+                    cudaStream_t s = nullptr;
+                    cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+                    for (size_t i = 0; e == cudaSuccess && i < ups[q].size(); ++i)
+                        e = cudaMemcpyAsync(*ups[q][i].dst, ups[q][i].src, ups[q][i].bytes,
+                                            cudaMemcpyHostToDevice, s);
+                    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+                    if (s) cudaStreamDestroy(s);
+                    if (e != cudaSuccess) {
+                        up_st[q] = DR_ERR_CUDA;
+                        up_err[q] = cudaGetErrorString(e);
+                    }
+                });
+            for (auto &t : th) t.join();
+        }
+        for (int q = 0; q < 4; ++q)
+            if (up_st[q] != DR_OK) fail(up_st[q], "upload: " + up_err[q]);
+        *out = g;
+        return DR_OK;
+    } catch (const Error &e) {
+        if (g) dr_graph_destroy(g);
+        set_error(e.status, e.msg);
+        return e.status;
+    } catch (const std::bad_alloc &) {
+        if (g) dr_graph_destroy(g);
+        set_error(DR_ERR_OUT_OF_MEMORY, "host allocation failed");
+        return DR_ERR_OUT_OF_MEMORY;
+    }
+}
+
+extern "C" dr_status dr_graph_destroy(dr_graph *g) {
+    if (!g) return DR_OK;
+    cudaStreamSynchronize(g->create_stream);
+    for (void *p : g->blocks) g->alloc.put(p, g->create_stream);
+    delete g;
+    return DR_OK;
+}
+
+extern "C" dr_status dr_graph_info(const dr_graph *g, dr_graph_info_t *info) {
+    clear_error();
+    if (!g || !info) {
+        set_error(DR_ERR_INVALID_ARGUMENT, "null graph/info");
+        return DR_ERR_INVALID_ARGUMENT;
+    }
+    std::memset(info, 0, sizeof(*info));
+    info->n_cell = g->n_cell;
+    info->n_net = g->n_net;
+    for (int r = 0; r < 3; ++r) {
+        info->nnz[r] = g->rel[r].nnz;
+        info->max_deg_dst[r] = g->rel[r].max_deg_dst;
+        info->max_deg_src[r] = g->rel[r].max_deg_src;
+        info->hub_rows_dst[r] = g->rel[r].n_hub;
+    }
+    info->hub_rows_src[0] = g->src_cell.n_hub;
+    info->hub_rows_src[1] = g->src_net.n_hub;
+    info->device_bytes = g->bytes;
+    return DR_OK;
+}

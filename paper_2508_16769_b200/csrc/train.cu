@@ -1,0 +1,129 @@
+// train.cu — linear head + MSE loss (reading Q14) and Adam (reading Q15, lr/wd
+// of P:466) for the training step. Reductions over rows use a fixed number of
+// per-CTA partials summed in a fixed order (deterministic, no atomics).
+#include "proj.h"
+
+namespace dr {
+namespace {
+
+constexpr int kHeadBlocks = 296;
+constexpr int kHeadThreads = 256;
+
+__global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a, float inv_n) {
+    __shared__ float wpart[kHeadThreads / 32][256 + 2];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int N = a.N;
+    float w[8], accw[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const int o = lane + 32 * s;
+        w[s] = o < N ? __ldg(a.w + o) : 0.f;
+        accw[s] = 0.f;
+    }
+    const float b = __ldg(a.b);
+    float accb = 0.f, accl = 0.f;
+    const int64_t nw = (int64_t)gridDim.x * (kHeadThreads / 32);
+    for (int64_t j = (int64_t)blockIdx.x * (kHeadThreads / 32) + wid; j < a.n; j += nw) {
+        float y[8], p = 0.f;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            const int o = lane + 32 * s;
+            y[s] = o < N ? __ldg(a.y + j * N + o) : 0.f;
+            p += y[s] * w[s];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+        const float r = p + b - __ldg(a.labels + j);
+        const float dp = 2.0f * r * inv_n;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            const int o = lane + 32 * s;
+            if (o < N) a.dy[j * N + o] = dp * w[s];
+            accw[s] += y[s] * dp;
+        }
+        accb += dp;
+        accl += r * r;
+    }
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const int o = lane + 32 * s;
+        if (o < N) wpart[wid][o] = accw[s];
+    }
+    if (lane == 0) {
+        wpart[wid][N] = accb;
+        wpart[wid][N + 1] = accl;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < N + 2; e += blockDim.x) {
+        float s = 0.f;
+        for (int q = 0; q < kHeadThreads / 32; ++q) s += wpart[q][e];
+        a.work[(int64_t)blockIdx.x * (N + 2) + e] = s;
+    }
+}
+
+__global__ void head_reduce_kernel(HeadArgs a, float inv_n) {
+    const int N = a.N;
+    for (int e = threadIdx.x; e < N + 2; e += blockDim.x) {
+        float s = 0.f;
+        for (int q = 0; q < kHeadBlocks; ++q) s += a.work[(int64_t)q * (N + 2) + e];
+        if (e < N) a.grad_w[e] = s;
+        else if (e == N) a.grad_b[0] = s;
+        else a.loss[0] = s * inv_n;
+    }
+}
+
+__global__ void adam_kernel(float *__restrict__ th, const float *__restrict__ g,
+                            float *__restrict__ m, float *__restrict__ v, int64_t n, float lr,
+                            float wd, float b1, float b2, float eps, float bc1, float bc2,
+                            float inv_world) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float t = th[i];
+        const float gi = g[i] * inv_world + wd * t;        // coupled L2 (torch.optim.Adam)
+        const float mi = b1 * m[i] + (1.f - b1) * gi;
+        const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+        m[i] = mi;
+        v[i] = vi;
+        const float denom = sqrtf(vi / bc2) + eps;
+        th[i] = t - lr * (mi / bc1) / denom;
+    }
+}
+
+__global__ void scale_kernel(float *x, int64_t n, float a) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] *= a;
+}
+
+}  // namespace
+
+size_t head_work_floats(int N) { return (size_t)kHeadBlocks * (N + 2); }
+
+void launch_head_mse(const HeadArgs &a, cudaStream_t s) {
+    const float inv_n = a.n > 0 ? 1.0f / (float)a.n : 0.f;
+    head_kernel<<<kHeadBlocks, kHeadThreads, 0, s>>>(a, inv_n);
+    note_launch("head_mse");
+    head_reduce_kernel<<<1, 256, 0, s>>>(a, inv_n);
+    note_launch("head_reduce");
+}
+
+void launch_adam(float *theta, const float *grad, float *m, float *v, int64_t n, float lr,
+                 float wd, float b1, float b2, float eps, float bc1, float bc2, float inv_world,
+                 cudaStream_t s) {
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    adam_kernel<<<(unsigned)blocks, 256, 0, s>>>(theta, grad, m, v, n, lr, wd, b1, b2, eps, bc1,
+                                                  bc2, inv_world);
+    note_launch("adam");
+}
+
+void launch_scale(float *x, int64_t n, float a, cudaStream_t s) {
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    scale_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, n, a);
+    note_launch("scale");
+}
+
+}  // namespace dr

@@ -1,0 +1,85 @@
+"""C-ABI checks that need no GPU: libdr.so loads, exports every symbol declared
+in include/dr.h, and the host-side validation of dr_graph_create (CSR
+invariants, pinned == pins^T, shapes) rejects bad graphs before any launch."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2508_16769_b200 as dr
+from paper_2508_16769_b200 import _lib
+from gen import make_config
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "dr.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(dr_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    L = _lib.lib()
+    declared = header_functions()
+    assert len(declared) >= 20
+    for name in declared:
+        assert hasattr(L, name), name
+    assert set(declared) == set(_lib.EXPORTS)
+
+
+def test_status_strings_and_version():
+    L = _lib.lib()
+    for s, name in _lib.STATUS.items():
+        assert L.dr_status_str(s).decode() == name
+    assert "sm_100a" in dr.version()
+
+
+def test_param_count_matches_survey():
+    cfg = _lib.dr_train_cfg(2, 64, 64, 64, 8, 8, 2e-4, 1e-5, 0.9, 0.999, 1e-8)
+    assert _lib.lib().dr_train_param_count(C.byref(cfg)) == 41409
+    cfg = _lib.dr_train_cfg(2, 128, 128, 128, 16, 16, 2e-4, 1e-5, 0.9, 0.999, 1e-8)
+    assert _lib.lib().dr_train_param_count(C.byref(cfg)) == 164737
+
+
+def _rels(d):
+    return {r: d.rel(r)[:2] for r in ("near", "pins", "pinned")}
+
+
+def _expect(status, fn):
+    with pytest.raises(dr.DRError) as e:
+        fn()
+    assert e.value.status == status, str(e.value)
+
+
+def test_graph_validation_errors():
+    d = make_config("C1")
+    rels = _rels(d)
+    # duplicate edge in near
+    ptr, col = rels["near"]
+    bad = col.copy()
+    r = int(np.argmax(np.diff(ptr) >= 2))
+    bad[ptr[r] + 1] = bad[ptr[r]]
+    _expect(5, lambda: dr.Graph(d.n_cell, d.n_net, dict(rels, near=(ptr, bad))))
+    # out of range column
+    bad = col.copy()
+    bad[-1] = d.n_cell + 3
+    _expect(4, lambda: dr.Graph(d.n_cell, d.n_net, dict(rels, near=(ptr, bad))))
+    # pinned is not pins^T: drop one pinned edge
+    pptr, pcol = rels["pinned"]
+    row = int(np.argmax(np.diff(pptr) >= 1))
+    keep = np.ones(pcol.size, bool)
+    keep[pptr[row]] = False
+    nptr = pptr.copy()
+    nptr[row + 1:] -= 1
+    _expect(6, lambda: dr.Graph(d.n_cell, d.n_net, dict(rels, pinned=(nptr, pcol[keep]))))
+    # shape mismatch: node counts disagree with the relations
+    _expect(3, lambda: dr.Graph(d.n_cell + 1, d.n_net, rels))
+    # non-finite weight
+    w = np.ones(col.size, np.float32)
+    w[0] = np.nan
+    _expect(7, lambda: dr.Graph(d.n_cell, d.n_net, rels, weights={"near": w}))
+    # error message is thread-local detail
+    assert "DR_ERR_NONFINITE" in _lib.lib().dr_last_error().decode()
