@@ -1,0 +1,456 @@
+"""bench.py — DR-CircuitGNN hot path on B200 (BASELINE.json metric).
+
+Default workload (N=1): BASELINE configs[1] = C2, a CircuitNet-small-shaped
+synthetic design (100k cells, 66.6k nets, hidden 64, k=8) and one full
+2-layer training step (D-ReLU -> 3x DR-SpMM -> projections/max-merge, x2 ->
+head/MSE -> backward incl. SSpMM -> [NCCL allreduce] -> Adam) per design.
+Under torchrun each rank trains on its own C2-shaped design (weak scaling), one
+NCCL allreduce per step inside dr_train_step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload C2|C4]
+
+--workload C4 is the roofline study (one HeteroConv layer fwd+bwd on the
+CircuitNet-large-shaped graph, D=128, k=16); it prints the same JSON shape with
+metric "HeteroConv fwd+bwd ms/iter".
+--impl reference times the fp64 CPU oracle (oracle/) on this box's host cores
+on the same workload (rank 0 only), as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HeteroConv fwd+bwd ms/iter and achieved HBM GB/s; train graphs/sec at 1/2/4/8 GPU"
+FALLBACK_HBM_GBS = 6650.0          # B200_PROFILING.md fallback
+FALLBACK_BF16_TFLOPS = 1590.0
+FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # SMs x FP32 lanes x FMA x max clock
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), float(j.get("bf16_tflops", FALLBACK_BF16_TFLOPS)), "measured"
+    return FALLBACK_HBM_GBS, FALLBACK_BF16_TFLOPS, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ algorithmic work per kernel tag
+def kernel_work(tag, d, D, k, n_layers):
+    """(bytes, flops) per launch for a profile tag, SURVEY §8(d) per-unit figures
+    (restated in DESIGN.md 'Algorithmic bytes'). Pair = 4 B value + 1 B index."""
+    parts = tag.split(".")
+    kind = parts[0]
+    rel = parts[-1]
+    nnz = {r: int(d.rel(r)[1].size) for r in ("near", "pins", "pinned")}
+    ndst = {"near": d.n_cell, "pins": d.n_net, "pinned": d.n_cell}
+    nsrc = {"near": d.n_cell, "pins": d.n_cell, "pinned": d.n_net}
+    if kind == "spmm_fwd":
+        ew = 4 if rel == "pinned" else 0          # GraphConv s_j folded into a per-edge weight
+        return nnz[rel] * (4 + 5 * k + ew) + ndst[rel] * (4 + 4 * D), 0.0
+    if kind == "spmm_bwd":
+        rels = ["near", "pins"] if rel == "cell" else ["pinned"]
+        n = d.n_cell if rel == "cell" else d.n_net
+        return sum(nnz[r] * (4 + 4 * k) for r in rels) + n * (k + 4 * k + 4 * D), 0.0
+    if kind == "drelu":
+        n = d.n_cell if rel == "cell" else d.n_net
+        return n * D * 4 + n * k * 5, 0.0
+    if kind in ("proj_fwd",):
+        n = d.n_cell if rel == "cell" else d.n_net
+        g = 2 if rel == "cell" else 1
+        return n * (g * D * 4 + D * 4), 2.0 * n * D * D * g
+    if kind in ("proj_bwd_dz", "dw"):
+        n = ndst.get(rel, d.n_cell)
+        return n * 8 * D, 2.0 * n * D * D
+    return 0, 0.0
+
+
+def roofline(prof, d, D, k, n_layers, steps, hbm, bf16, src):
+    """Dominant kernel tag by total device time; achieved = algorithmic bytes
+    (or FLOPs) per launch / its mean launch time."""
+    if not prof:
+        return None, {}
+    table = {}
+    for tag, (n, tot, mx) in prof.items():
+        b, f = kernel_work(tag, d, D, k, n_layers)
+        per = tot / max(n, 1)
+        table[tag] = dict(launches=n, total_ms=round(tot, 4), mean_ms=round(per, 5),
+                          gbs=round(b / (per * 1e-3) / 1e9, 1) if b and per > 0 else None,
+                          tflops=round(f / (per * 1e-3) / 1e12, 2) if f and per > 0 else None)
+    dom = max(prof, key=lambda t: prof[t][1])
+    n, tot, _ = prof[dom]
+    per_s = tot / max(n, 1) * 1e-3
+    b, f = kernel_work(dom, d, D, k, n_layers)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(dom.split(".")[0] + "." + dom.split(".")[-1])
+    kind = dom.split(".")[0]
+    if kind in ("proj_fwd", "proj_bwd_dz", "dw"):
+        ach = f / per_s / 1e12
+        rf = {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(FP32_SIMT_TFLOPS, 1),
+              "unit": "TFLOP/s", "frac": round(ach / FP32_SIMT_TFLOPS, 4), "traffic": traffic,
+              "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (SIMT FFMA)"}
+    else:
+        ach = b / per_s / 1e9
+        rf = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm,
+              "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": traffic,
+              "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})"}
+    return rf, table
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_16769_b200 as dr
+    from gen import make_config, make_params
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    hbm, bf16, src = peaks()
+    wl = args.workload
+    cfg = {"C2": dict(D=64, k=8, layers=2), "C4": dict(D=128, k=16, layers=1)}[wl]
+    D, k, nl = cfg["D"], cfg["k"], cfg["layers"]
+    t0 = time.time()
+    d = make_config(wl, seed=None if rank == 0 else 2 + 1000 * rank) if wl == "C2" else make_config(wl)
+    log(f"[rank {rank}] generated {wl}: {d.n_cell} cells, {d.n_net} nets, nnz {d.nnz()} "
+        f"in {time.time() - t0:.1f}s")
+    g = dr.Graph.from_design(d)
+    P = make_params(D, D, D, nl, seed=7)
+    dev = torch.device("cuda", local)
+    xc = torch.as_tensor(d.x_cell).to(dev)
+    xn = torch.as_tensor(d.x_net).to(dev)
+    lab = torch.as_tensor(d.labels).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+    comm = None
+    if world > 1:
+        uid = [dr.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = dr.nccl_comm_init(uid[0], world, rank)
+
+    if wl == "C2":
+        flat = torch.as_tensor(dr.flatten_params(P, nl)).to(dev)
+        tr = dr.Trainer(flat, nl, D, D, D, k, k, nccl_comm=comm)
+
+        def step():
+            tr.step(g, xc, xn, lab, sync=False)
+    else:
+        W = {kk.split(".", 1)[1]: torch.as_tensor(v).to(dev) for kk, v in P.items()
+             if kk.startswith("l0.")}
+        L = dr.Layer(W, D, D, D, k, k)
+        tape = torch.empty(L.tape_bytes(g), dtype=torch.uint8, device=dev)
+        dyc = torch.randn(d.n_cell, D, device=dev)
+        dyn = torch.randn(d.n_net, D, device=dev)
+
+        def step():
+            dr.heteroconv_fwd(g, L, xc, xn, tape=tape)
+            dr.heteroconv_bwd(g, L, tape, dyc, dyn, need_dx=True)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    dr.launch_count_reset()
+    dr.profile_begin()
+    wall0 = time.time()
+    for i in range(args.steps):
+        flush.zero_()                        # L2 flush between timed steps (outside the events)
+        ev[i][0].record()
+        step()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    wall = time.time() - wall0
+    if world > 1:
+        dist.barrier()
+    prof = dr.profile_end()
+    launches = dr.launch_count()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    time.sleep(0.2)
+    clk = clocks.stop()
+
+    # ---- end to end through the public API with host buffers (pinned), per step:
+    # H2D of the step's inputs (features + labels) and D2H of the step's loss.
+    e2e = None
+    if wl == "C2":
+        hx = torch.as_tensor(d.x_cell).pin_memory()
+        hn = torch.as_tensor(d.x_net).pin_memory()
+        hl = torch.as_tensor(d.labels).pin_memory()
+        h2d = hx.numel() * 4 + hn.numel() * 4 + hl.numel() * 4
+        dx = torch.empty_like(xc)
+        dn = torch.empty_like(xn)
+        dl = torch.empty_like(lab)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_ms = 0.0
+        for i in range(args.steps):
+            flush.zero_()
+            e0.record()
+            dx.copy_(hx, non_blocking=True)
+            dn.copy_(hn, non_blocking=True)
+            dl.copy_(hl, non_blocking=True)
+            tr.step(g, dx, dn, dl, sync=True)          # loss D2H into pinned host + sync
+            e1.record()
+            e1.synchronize()
+            e_ms += e0.elapsed_time(e1)
+        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(world * args.steps / (float(te.item()) * 1e-3), 3),
+               "unit": "graphs/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
+               "ms_per_step": round(float(te.item()) / args.steps, 4),
+               "note": "graph structure resident (created once); per step H2D x_cell, x_net, "
+                       "labels from pinned host, D2H loss"}
+
+    rf, table = roofline(prof, d, D, k, nl, args.steps, hbm, bf16, src)
+    out = None
+    if rank == 0:
+        if wl == "C2":
+            value = world * args.steps / (ms_max * 1e-3)
+            metric_unit = "graphs/s"
+            hib = True
+        else:
+            value = ms_max / args.steps
+            metric_unit = "ms/iter"
+            hib = False
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(d, P, D, k, nl, wl)
+        out = {
+            "metric": METRIC if wl == "C2" else "HeteroConv fwd+bwd ms/iter",
+            "value": round(value, 4),
+            "unit": metric_unit,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_max / args.steps, 4),
+            "higher_is_better": hib,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (seeded CircuitNet-shaped generator, random-init weights)",
+            "config": {
+                "workload": ("C2: CircuitNet-small-shaped design (BASELINE configs[1]), "
+                             "100k cells / 66.6k nets, hidden 64, D-ReLU k=8, 2 HeteroConv "
+                             "layers, full train step incl. Adam" if wl == "C2" else
+                             "C4: CircuitNet-large-shaped graph (BASELINE configs[3]), 1M "
+                             "cells / 0.7M nets, D=128, k=16, one HeteroConv layer fwd+bwd"),
+                "graphs_per_step": world,
+                "n_cell": d.n_cell, "n_net": d.n_net, "nnz": d.nnz(), "D": D, "k": k,
+                "layers": nl, "id_order": "shuffled",
+                "parallelism": f"dp{world}" if world > 1 else "single",
+                "l2": "flushed (256 MB write) before every timed step, outside the events",
+            },
+            "roofline": rf,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "wall_s_timed_loop": round(wall, 3),
+            "kernels": table,
+        }
+        print(json.dumps(out), flush=True)
+    if comm:
+        dr.nccl_comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+    return out
+
+
+# ------------------------------------------------------------------ oracle timing (CPU baseline / reference arm)
+def oracle_step_fn(d, P, D, k, nl, wl):
+    from oracle import oracle as O
+    G = O.OGraph(d)
+    if wl == "C2":
+        state = {"P": {kk: np.asarray(v, np.float64) for kk, v in P.items()}, "m": None, "t": 0}
+
+        def step():
+            loss, grads, _ = O.model_fwd_bwd(G, state["P"], nl, k, k, d.x_cell, d.x_net,
+                                             d.labels)
+            state["t"] += 1
+            for kk in state["P"]:
+                th, m, v = O.adam(state["P"][kk], grads[kk],
+                                  state.get("m_" + kk, np.zeros_like(grads[kk])),
+                                  state.get("v_" + kk, np.zeros_like(grads[kk])), state["t"])
+                state["P"][kk], state["m_" + kk], state["v_" + kk] = th, m, v
+            return loss
+    else:
+        W = O.layer_params(P, 0)
+        rng = np.random.default_rng(0)
+        dyc = rng.standard_normal((d.n_cell, D))
+        dyn = rng.standard_normal((d.n_net, D))
+
+        def step():
+            _, _, tape = O.layer_fwd(G, W, d.x_cell, d.x_net, k, k)
+            O.layer_bwd(G, W, tape, dyc, dyn, need_dx=True)
+    return step, O
+
+
+def cpu_baseline(d, P, D, k, nl, wl, budget_s=20.0):
+    step, O = oracle_step_fn(d, P, D, k, nl, wl)
+    times = []
+    t_all = time.time()
+    while True:
+        t = time.time()
+        step()
+        times.append(time.time() - t)
+        if time.time() - t_all > budget_s * 0.5 or len(times) >= 5:
+            break
+    per = float(np.mean(times))
+    if wl == "C2":
+        val, unit = 1.0 / per, "graphs/s"
+    else:
+        val, unit = per * 1e3, "ms/iter"
+    return {"value": round(val, 5), "unit": unit, "cores": O.num_threads(), "kind": "oracle",
+            "sample": f"{len(times)} full oracle steps on the same {wl} design (fp64, "
+                      f"OpenMP over rows, {O.num_threads()} threads), mean {per:.2f} s/step"}
+
+
+def run_reference(args):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return None
+    from gen import make_config, make_params
+    wl = args.workload
+    cfg = {"C2": dict(D=64, k=8, layers=2), "C4": dict(D=128, k=16, layers=1)}[wl]
+    D, k, nl = cfg["D"], cfg["k"], cfg["layers"]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    d = make_config(wl)
+    P = make_params(D, D, D, nl, seed=7)
+    step, O = oracle_step_fn(d, P, D, k, nl, wl)
+    for _ in range(min(args.warmup, 1)):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t = time.time()
+        step()
+        times.append(time.time() - t)
+    ms = float(np.sum(times)) * 1e3
+    if wl == "C2":
+        value, unit, hib = args.steps / (ms * 1e-3), "graphs/s", True
+    else:
+        value, unit, hib = ms / args.steps, "ms/iter", False
+    out = {
+        "impl": "reference",
+        "metric": METRIC if wl == "C2" else "HeteroConv fwd+bwd ms/iter",
+        "value": round(value, 5), "unit": unit, "n_gpus": world, "steps": args.steps,
+        "warmup": min(args.warmup, 1), "ms_per_step": round(ms / args.steps, 3),
+        "higher_is_better": hib, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded CircuitNet-shaped generator, random-init weights)",
+        "config": {"workload": f"{wl} (same design and parameters as our arm); fp64 CPU oracle",
+                   "n_cell": d.n_cell, "n_net": d.n_net, "D": D, "k": k, "layers": nl},
+        "cpu_baseline": {"value": round(value, 5), "unit": unit, "cores": O.num_threads(),
+                         "kind": "oracle",
+                         "sample": f"each step = one full oracle step on the {wl} design"},
+        "e2e": {"value": round(value, 5), "unit": unit, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2", choices=["C2", "C4"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

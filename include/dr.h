@@ -238,6 +238,20 @@ dr_status dr_nccl_unique_id(void *id128);
 dr_status dr_nccl_comm_init(const void *id128, int32_t nranks, int32_t rank, void **comm);
 dr_status dr_nccl_comm_destroy(void *comm);
 
+/* Per-kernel device timing: between dr_profile_begin and dr_profile_end every
+ * libdr launch issued by this host thread is bracketed by CUDA events on the
+ * stream it is launched on. dr_profile_end synchronises, aggregates by kernel
+ * tag ("<kernel>.<relation or role>") and disables profiling; *n_out is the
+ * number of distinct tags (entries beyond cap are dropped). Not for use
+ * inside CUDA-graph capture. */
+typedef struct {
+    char name[48];
+    int64_t launches;
+    double total_ms, max_ms;
+} dr_profile_entry;
+dr_status dr_profile_begin(void);
+dr_status dr_profile_end(dr_profile_entry *out, int32_t cap, int32_t *n_out);
+
 /* Number of kernels this library launched on this host thread since the last
  * reset (evidence for bench.py's gpu_launches). */
 int64_t dr_launch_count(void);

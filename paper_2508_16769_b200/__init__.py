@@ -53,6 +53,22 @@ def launch_count_reset():
     lib().dr_launch_count_reset()
 
 
+def profile_begin():
+    """Start per-kernel CUDA-event timing of libdr launches on this thread."""
+    check(lib().dr_profile_begin())
+
+
+def profile_end():
+    """Stop timing; return {tag: (launches, total_ms, max_ms)}."""
+    from ._lib import dr_profile_entry
+    cap = 256
+    buf = (dr_profile_entry * cap)()
+    n = C.c_int32()
+    check(lib().dr_profile_end(buf, cap, C.byref(n)))
+    return {buf[i].name.decode(): (int(buf[i].launches), float(buf[i].total_ms),
+                                   float(buf[i].max_ms)) for i in range(min(n.value, cap))}
+
+
 # ------------------------------------------------------------------ graph
 class Graph:
     """Device-resident heterograph (dr_graph_create). `rels` maps 'near'/'pins'/

@@ -65,6 +65,11 @@ class dr_tape_view(C.Structure):
                 ("y_pinned", P), ("mask", P)]
 
 
+class dr_profile_entry(C.Structure):
+    _fields_ = [("name", C.c_char * 48), ("launches", C.c_int64), ("total_ms", C.c_double),
+                ("max_ms", C.c_double)]
+
+
 class dr_train_cfg(C.Structure):
     _fields_ = [("n_layers", C.c_int32), ("d_in_cell", C.c_int32), ("d_in_net", C.c_int32),
                 ("d_hidden", C.c_int32), ("k_cell", C.c_int32), ("k_net", C.c_int32),
@@ -99,6 +104,8 @@ _SIGS = {
     "dr_nccl_unique_id": (C.c_int, [P]),
     "dr_nccl_comm_init": (C.c_int, [P, C.c_int32, C.c_int32, C.POINTER(P)]),
     "dr_nccl_comm_destroy": (C.c_int, [P]),
+    "dr_profile_begin": (C.c_int, []),
+    "dr_profile_end": (C.c_int, [C.POINTER(dr_profile_entry), C.c_int32, C.POINTER(C.c_int32)]),
     "dr_launch_count": (C.c_int64, []),
     "dr_launch_count_reset": (None, []),
 }

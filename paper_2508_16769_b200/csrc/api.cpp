@@ -29,6 +29,52 @@ void note_launch(const char *name) {
     if (e != cudaSuccess) fail(DR_ERR_CUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
 }
 
+// ------------------------------------------------------------------ profiling
+struct ProfRec {
+    std::string name;
+    cudaEvent_t a, b;
+};
+static thread_local bool t_prof = false;
+static thread_local std::vector<ProfRec> t_recs;
+static thread_local std::vector<cudaEvent_t> t_pool;
+static thread_local std::string t_tag;
+
+static cudaEvent_t pool_get() {
+    if (!t_pool.empty()) {
+        cudaEvent_t e = t_pool.back();
+        t_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    DR_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+ProfScope::ProfScope(const char *b, cudaStream_t st) {
+    if (!t_prof) return;
+    s = st;
+    base = b;
+    a = pool_get();
+    DR_CUDA(cudaEventRecord(a, s));
+}
+
+ProfScope::~ProfScope() {
+    if (!a) return;
+    cudaEvent_t e = nullptr;
+    try {
+        e = pool_get();
+    } catch (...) {
+        return;
+    }
+    cudaEventRecord(e, s);
+    t_recs.push_back({t_tag.empty() ? std::string(base) : std::string(base) + "." + t_tag, a, e});
+}
+
+TagScope::TagScope(const char *tag) : prev(t_tag) {
+    t_tag = prev.empty() ? std::string(tag) : prev + "." + tag;
+}
+TagScope::~TagScope() { t_tag = prev; }
+
 void ensure_smem(const void *fn, size_t bytes) {
     static std::mutex mu;
     static std::unordered_map<const void *, size_t> set;
@@ -163,14 +209,14 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
         for (int q = 0; q < 3; ++q) DR_CUDA(cudaStreamWaitEvent(C.s[q], C.fork, 0));
     }
     const int nc = g->n_cell, nn = g->n_net;
-    launch_drelu(xc, nc, L->d_cell, L->d_cell, L->k_cell, hcv, hci, s0);         // Eq. 2-3
+    { TagScope t("cell"); launch_drelu(xc, nc, L->d_cell, L->d_cell, L->k_cell, hcv, hci, s0); }  // Eq. 2-3
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[0], s0));                               // H_c ready
-    launch_drelu(xn, nn, L->d_net, L->d_net, L->k_net, hnv, hni, s2);
+    { TagScope t("net"); launch_drelu(xn, nn, L->d_net, L->d_net, L->k_net, hnv, hni, s2); }
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[1], s2));                               // H_n ready
-    launch_spmm_fwd(g->rel[DR_NEAR], hcv, hci, L->k_cell, L->d_cell, z[DR_NEAR], s0);   // Eq. 5-7
+    { TagScope t("near"); launch_spmm_fwd(g->rel[DR_NEAR], hcv, hci, L->k_cell, L->d_cell, z[DR_NEAR], s0); }  // Eq. 5-7
     if (!seq) DR_CUDA(cudaStreamWaitEvent(s1, C.ev[0], 0));
-    launch_spmm_fwd(g->rel[DR_PINS], hcv, hci, L->k_cell, L->d_cell, z[DR_PINS], s1);
-    launch_spmm_fwd(g->rel[DR_PINNED], hnv, hni, L->k_net, L->d_net, z[DR_PINNED], s2);
+    { TagScope t("pins"); launch_spmm_fwd(g->rel[DR_PINS], hcv, hci, L->k_cell, L->d_cell, z[DR_PINS], s1); }
+    { TagScope t("pinned"); launch_spmm_fwd(g->rel[DR_PINNED], hnv, hni, L->k_net, L->d_net, z[DR_PINNED], s2); }
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[2], s2));                               // Z_pinned ready
     if (!seq) DR_CUDA(cudaStreamWaitEvent(s1, C.ev[1], 0));
     {   // net: Y_net = Z_pins Wn_pins + densify(H_n) Wr_pins + b_pins   (Eq. 7, 9)
@@ -179,6 +225,7 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
         a.Za = z[DR_PINS]; a.Wa = L->wn[DR_PINS]; a.ba = L->b[DR_PINS];
         a.Wr = L->wr[DR_PINS]; a.hval = hnv; a.hidx = hni; a.k = L->k_net;
         a.y = yn;
+        TagScope t("net");
         launch_proj_fwd(a, s1);
     }
     if (!seq) DR_CUDA(cudaStreamWaitEvent(s0, C.ev[2], 0));
@@ -195,6 +242,7 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
             a.tap_a = (float *)(tp + T.tap_a);
             a.tap_b = (float *)(tp + T.tap_b);
         }
+        TagScope t("cell");
         launch_proj_fwd(a, s0);
     }
     if (!seq) {
@@ -253,40 +301,62 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
             launch_root_dots(a, s);
         };
         // dZ'_psi = c_psi (dY_psi Wn_psi^T)  (row-scaled by the destination normaliser)
-        dzk(nc, L->d_cell, dyc, mode_near, L->wn[DR_NEAR], g->rel[DR_NEAR].c, dz[DR_NEAR], s0);
-        if (L->wr[DR_NEAR]) rootk(nc, L->k_cell, dyc, mode_near, L->wr[DR_NEAR], hci, root_c, s0);
-        dzk(nn, L->d_cell, dyn, kMaskNone, L->wn[DR_PINS], g->rel[DR_PINS].c, dz[DR_PINS], s1);
-        if (L->wr[DR_PINS]) rootk(nn, L->k_net, dyn, kMaskNone, L->wr[DR_PINS], hni, root_n, s1);
+        {
+            TagScope t("near");
+            dzk(nc, L->d_cell, dyc, mode_near, L->wn[DR_NEAR], g->rel[DR_NEAR].c, dz[DR_NEAR], s0);
+            if (L->wr[DR_NEAR]) rootk(nc, L->k_cell, dyc, mode_near, L->wr[DR_NEAR], hci, root_c, s0);
+        }
+        {
+            TagScope t("pins");
+            dzk(nn, L->d_cell, dyn, kMaskNone, L->wn[DR_PINS], g->rel[DR_PINS].c, dz[DR_PINS], s1);
+            if (L->wr[DR_PINS]) rootk(nn, L->k_net, dyn, kMaskNone, L->wr[DR_PINS], hni, root_n, s1);
+        }
         if (!seq) DR_CUDA(cudaEventRecord(C.ev[0], s1));                           // dZ_pins, root_n
-        dzk(nc, L->d_net, dyc, mode_pinned, L->wn[DR_PINNED], g->rel[DR_PINNED].c,
-            dz[DR_PINNED], s2);
+        {
+            TagScope t("pinned");
+            dzk(nc, L->d_net, dyc, mode_pinned, L->wn[DR_PINNED], g->rel[DR_PINNED].c,
+                dz[DR_PINNED], s2);
+        }
         // SSpMM per source node type (Alg. 2 stage 2-3, ownership instead of atomics)
         if (dxc) {
             if (!seq) DR_CUDA(cudaStreamWaitEvent(s0, C.ev[0], 0));
             BwdTerm t0{&g->rel[DR_NEAR], dz[DR_NEAR], false}, t1{&g->rel[DR_PINS], dz[DR_PINS], false};
+            TagScope t("cell");
             launch_spmm_bwd(g->src_cell, nc, t0, t1, L->wr[DR_NEAR] ? root_c : nullptr, hci,
                             L->k_cell, L->d_cell, nullptr, dxc, false, s0);
         }
         if (dxn) {
             if (!seq) DR_CUDA(cudaStreamWaitEvent(s2, C.ev[0], 0));
             BwdTerm t0{&g->rel[DR_PINNED], dz[DR_PINNED], false}, t1{};
+            TagScope t("net");
             launch_spmm_bwd(g->src_net, nn, t0, t1, L->wr[DR_PINS] ? root_n : nullptr, hni,
                             L->k_net, L->d_net, nullptr, dxn, false, s2);
         }
     }
     // weight gradients: dW = Z^T dY_psi, dWr = H^T dY_psi, db = colsum(dY_psi)
-    dw(nc, L->d_cell, z[DR_NEAR], nullptr, nullptr, 0, dyc, mode_near, G->wn[DR_NEAR],
-       G->b[DR_NEAR], work[0], s0);
-    if (L->wr[DR_NEAR])
-        dw(nc, L->d_cell, nullptr, hcv, hci, L->k_cell, dyc, mode_near, G->wr[DR_NEAR], nullptr,
-           work[0], s0);
-    dw(nc, L->d_net, z[DR_PINNED], nullptr, nullptr, 0, dyc, mode_pinned, G->wn[DR_PINNED],
-       G->b[DR_PINNED], work[2], s2);
-    dw(nn, L->d_cell, z[DR_PINS], nullptr, nullptr, 0, dyn, kMaskNone, G->wn[DR_PINS],
-       G->b[DR_PINS], work[1], s1);
-    if (L->wr[DR_PINS])
-        dw(nn, L->d_net, nullptr, hnv, hni, L->k_net, dyn, kMaskNone, G->wr[DR_PINS], nullptr,
-           work[1], s1);
+    {
+        TagScope t("near");
+        dw(nc, L->d_cell, z[DR_NEAR], nullptr, nullptr, 0, dyc, mode_near, G->wn[DR_NEAR],
+           G->b[DR_NEAR], work[0], s0);
+        TagScope t2("root");
+        if (L->wr[DR_NEAR])
+            dw(nc, L->d_cell, nullptr, hcv, hci, L->k_cell, dyc, mode_near, G->wr[DR_NEAR],
+               nullptr, work[0], s0);
+    }
+    {
+        TagScope t("pinned");
+        dw(nc, L->d_net, z[DR_PINNED], nullptr, nullptr, 0, dyc, mode_pinned, G->wn[DR_PINNED],
+           G->b[DR_PINNED], work[2], s2);
+    }
+    {
+        TagScope t("pins");
+        dw(nn, L->d_cell, z[DR_PINS], nullptr, nullptr, 0, dyn, kMaskNone, G->wn[DR_PINS],
+           G->b[DR_PINS], work[1], s1);
+        TagScope t2("root");
+        if (L->wr[DR_PINS])
+            dw(nn, L->d_net, nullptr, hnv, hni, L->k_net, dyn, kMaskNone, G->wr[DR_PINS],
+               nullptr, work[1], s1);
+    }
     if (!seq) {
         wait_on(st, s0, C.ev[3]);
         wait_on(st, s1, C.ev[4]);
@@ -391,6 +461,21 @@ void carve(const dr_train_cfg &c, P *base, std::vector<LayerT> &out, P **hw, P *
 
 }  // namespace
 
+#define DR_API_BEGIN                                                                         \
+    clear_error();                                                                           \
+    try {
+#define DR_API_END                                                                           \
+    }                                                                                        \
+    catch (const Error &e) {                                                                 \
+        set_error(e.status, e.msg);                                                          \
+        return e.status;                                                                     \
+    }                                                                                        \
+    catch (const std::bad_alloc &) {                                                         \
+        set_error(DR_ERR_OUT_OF_MEMORY, "host allocation failed");                           \
+        return DR_ERR_OUT_OF_MEMORY;                                                         \
+    }                                                                                        \
+    return DR_OK;
+
 extern "C" {
 
 const char *dr_status_str(dr_status s) {
@@ -416,23 +501,51 @@ const char *dr_last_error(void) { return t_err.c_str(); }
 
 const char *dr_version(void) { return "libdr 0.1 sm_100a (DR-CircuitGNN hot path, arXiv 2508.16769)"; }
 
+dr_status dr_profile_begin(void) {
+    DR_API_BEGIN
+    for (auto &r : t_recs) {
+        t_pool.push_back(r.a);
+        t_pool.push_back(r.b);
+    }
+    t_recs.clear();
+    t_prof = true;
+    DR_API_END
+}
+
+dr_status dr_profile_end(dr_profile_entry *out, int32_t cap, int32_t *n_out) {
+    DR_API_BEGIN
+    t_prof = false;
+    std::vector<dr_profile_entry> agg;
+    for (auto &r : t_recs) {
+        DR_CUDA(cudaEventSynchronize(r.b));
+        float ms = 0.f;
+        DR_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        dr_profile_entry *e = nullptr;
+        for (auto &x : agg)
+            if (r.name == x.name) e = &x;
+        if (!e) {
+            agg.emplace_back();
+            e = &agg.back();
+            std::memset(e, 0, sizeof(*e));
+            std::strncpy(e->name, r.name.c_str(), sizeof(e->name) - 1);
+        }
+        e->launches += 1;
+        e->total_ms += ms;
+        if (ms > e->max_ms) e->max_ms = ms;
+    }
+    for (auto &r : t_recs) {
+        t_pool.push_back(r.a);
+        t_pool.push_back(r.b);
+    }
+    t_recs.clear();
+    if (n_out) *n_out = (int32_t)agg.size();
+    for (int32_t i = 0; out && i < cap && i < (int32_t)agg.size(); ++i) out[i] = agg[i];
+    DR_API_END
+}
+
 int64_t dr_launch_count(void) { return t_launches; }
 void dr_launch_count_reset(void) { t_launches = 0; }
 
-#define DR_API_BEGIN                                                                         \
-    clear_error();                                                                           \
-    try {
-#define DR_API_END                                                                           \
-    }                                                                                        \
-    catch (const Error &e) {                                                                 \
-        set_error(e.status, e.msg);                                                          \
-        return e.status;                                                                     \
-    }                                                                                        \
-    catch (const std::bad_alloc &) {                                                         \
-        set_error(DR_ERR_OUT_OF_MEMORY, "host allocation failed");                           \
-        return DR_ERR_OUT_OF_MEMORY;                                                         \
-    }                                                                                        \
-    return DR_OK;
 
 dr_status dr_drelu_topk(const float *x, int64_t n, int32_t dim, int64_t ldx, dr_cbsr *out,
                         void *stream) {
@@ -642,7 +755,9 @@ dr_status dr_train_step(dr_trainer *t, const dr_graph *g, const float *x_cell, c
     auto dyn = [&](int q) { return (float *)(ws + dy_off + q * (al(nc * D * 4) + al(nn * D * 4)) + al(nc * D * 4)); };
     // ---- forward
     const float *xc = x_cell, *xn = x_net;
+    static const char *ltag[8] = {"L0", "L1", "L2", "L3", "L4", "L5", "L6", "L7"};
     for (int l = 0; l < nl; ++l) {
+        TagScope tg(ltag[l]);
         heteroconv_fwd(g, &t->L[l], xc, xn, yc(l), yn(l), ws + tape_off[l], 0, st);
         xc = yc(l);
         xn = yn(l);
@@ -661,6 +776,7 @@ dr_status dr_train_step(dr_trainer *t, const dr_graph *g, const float *x_cell, c
     for (int l = nl - 1; l >= 0; --l) {
         float *dxc = l > 0 ? dyc(cur ^ 1) : nullptr;
         float *dxn = l > 0 ? dyn(cur ^ 1) : nullptr;
+        TagScope tg(ltag[l]);
         heteroconv_bwd(g, &t->L[l], ws + tape_off[l], dyc(cur), dyn(cur), dxc, dxn, &t->G[l], 0, st);
         cur ^= 1;
     }

@@ -34,6 +34,22 @@ void clear_error();
 // Launch bookkeeping: count kernels and surface launch errors immediately.
 void note_launch(const char *name);
 
+// Optional per-launch device timing (dr_profile_begin/end): events recorded on
+// the launch stream around the kernel; the name is "<base>.<current tag>".
+struct ProfScope {
+    cudaStream_t s = nullptr;
+    cudaEvent_t a = nullptr;
+    const char *base = nullptr;
+    ProfScope(const char *base, cudaStream_t s);
+    ~ProfScope();
+};
+// Tag naming the relation / role of the launches issued while it is alive.
+struct TagScope {
+    std::string prev;
+    explicit TagScope(const char *tag);
+    ~TagScope();
+};
+
 // ------------------------------------------------------------------ allocation
 struct Alloc {
     dr_allocator a{};

@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(256) drelu_kernel(const float *__restrict__ x,
 void launch_drelu(const float *x, int64_t n, int dim, int64_t ldx, int k, float *val,
                   uint8_t *idx, cudaStream_t s) {
     if (n <= 0) return;
+    ProfScope ps("drelu", s);
     const int threads = 256, rows_per_cta = threads / 32;
     int64_t blocks = (n + rows_per_cta - 1) / rows_per_cta;
     if (blocks > 148 * 16) blocks = 148 * 16;

@@ -327,6 +327,7 @@ void launch_proj_fwd(const ProjFwdArgs &a, cudaStream_t s) {
     const int TM = (int)proj_tile_rows(a.N);
     const size_t smem = ((size_t)TM * (kKC + 1) + (size_t)kKC * a.N) * 4;
     const unsigned grid = (unsigned)((a.n + TM - 1) / TM);
+    ProfScope ps("proj_fwd", s);
     if (a.Zb) {
         ensure_smem((const void *)proj_fwd_kernel<true>, smem);
         proj_fwd_kernel<true><<<grid, kThreads, smem, s>>>(a);
@@ -343,6 +344,7 @@ void launch_proj_bwd_dz(const ProjBwdArgs &a, cudaStream_t s) {
     const size_t smem = ((size_t)TM * (kKC + 1) + (size_t)kKC * a.K) * 4;
     const unsigned grid = (unsigned)((a.n + TM - 1) / TM);
     ensure_smem((const void *)proj_bwd_dz_kernel, smem);
+    ProfScope ps("proj_bwd_dz", s);
     proj_bwd_dz_kernel<<<grid, kThreads, smem, s>>>(a);
     note_launch("proj_bwd_dz");
 }
@@ -351,6 +353,7 @@ void launch_root_dots(const RootArgs &a, cudaStream_t s) {
     if (a.n <= 0) return;
     int64_t blocks = (a.n + 7) / 8;
     if (blocks > 148 * 16) blocks = 148 * 16;
+    ProfScope ps("root_dots", s);
     root_dots_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(a);
     note_launch("root_dots");
 }
@@ -368,6 +371,7 @@ size_t dw_part_floats(int64_t n, int K, int N) {
 
 // grad_w (K x N) = Z^T mask(dY); grad_b (N) = colsum(mask(dY)) if non-null.
 void launch_dw(DwArgs a, float *grad_w, float *grad_b, float *work, cudaStream_t s) {
+    ProfScope ps("dw", s);
     const int chunks = dw_num_chunks(a.n);
     a.rows_per_chunk = (int)((a.n + chunks - 1) / chunks);
     a.part = work;

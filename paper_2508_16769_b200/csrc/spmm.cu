@@ -388,6 +388,7 @@ void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, in
     const int64_t warp_ctas = (rows + (int64_t)wpc * R - 1) / ((int64_t)wpc * R);
     const unsigned grid = (unsigned)(a.hub_ctas + warp_ctas);
     if (grid == 0) return;
+    ProfScope ps("spmm_fwd", s);
     if (P == 4) {
         set_smem_attr(spmm_fwd_kernel<4>, smem);
         spmm_fwd_kernel<4><<<grid, wpc * 32, smem, s>>>(a);
@@ -443,6 +444,7 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, c
     const int64_t warp_ctas = (rows + (int64_t)wpc * R - 1) / ((int64_t)wpc * R);
     const unsigned grid = (unsigned)(a.hub_ctas + warp_ctas);
     if (grid == 0) return;
+    ProfScope ps("spmm_bwd", s);
     if (P == 4) {
         set_smem_attr(spmm_bwd_kernel<4>, smem);
         spmm_bwd_kernel<4><<<grid, wpc * 32, smem, s>>>(a);

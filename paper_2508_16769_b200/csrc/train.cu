@@ -101,6 +101,7 @@ size_t head_work_floats(int N) { return (size_t)kHeadBlocks * (N + 2); }
 
 void launch_head_mse(const HeadArgs &a, cudaStream_t s) {
     const float inv_n = a.n > 0 ? 1.0f / (float)a.n : 0.f;
+    ProfScope ps("head_mse", s);
     head_kernel<<<kHeadBlocks, kHeadThreads, 0, s>>>(a, inv_n);
     note_launch("head_mse");
     head_reduce_kernel<<<1, 256, 0, s>>>(a, inv_n);
@@ -113,6 +114,7 @@ void launch_adam(float *theta, const float *grad, float *m, float *v, int64_t n,
     int64_t blocks = (n + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
+    ProfScope ps("adam", s);
     adam_kernel<<<(unsigned)blocks, 256, 0, s>>>(theta, grad, m, v, n, lr, wd, b1, b2, eps, bc1,
                                                   bc2, inv_world);
     note_launch("adam");
