@@ -581,12 +581,8 @@ dr_status dr_spmm_bwd(const dr_graph *g, dr_rel r, const float *dz, const dr_cbs
     DR_CHECK(h->n == R.n_src, DR_ERR_SHAPE_MISMATCH, "spmm_bwd: h_src->n != relation n_src");
     DR_CHECK(g_kept || dx, DR_ERR_INVALID_ARGUMENT, "spmm_bwd: both outputs NULL");
     DR_CHECK(R.n_dst == 0 || dz, DR_ERR_INVALID_ARGUMENT, "spmm_bwd: null dz");
-    SrcSched sched;
-    sched.n = R.n_src;
-    sched.order = R.orderT;
-    sched.n_hub = R.n_hubT;
     BwdTerm t0{&R, dz, true}, t1{};
-    launch_spmm_bwd(sched, R.n_src, t0, t1, nullptr, (const uint8_t *)h->idx, h->k, h->dim,
+    launch_spmm_bwd(R.bwd, R.n_src, t0, t1, nullptr, (const uint8_t *)h->idx, h->k, h->dim,
                     g_kept, dx, accumulate != 0, (cudaStream_t)stream);
     DR_API_END
 }

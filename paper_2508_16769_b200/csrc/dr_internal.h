@@ -65,6 +65,22 @@ struct Alloc {
 // ceil(32/K) parts").
 constexpr int kHubDeg = 256;
 
+// A processing order over the rows of one kernel (destinations for the
+// forward, sources for the backward), sorted by descending degree so the row
+// classes of Alg. 1 stage 2 are contiguous: [hubs | warp rows | sub-warp rows].
+// ge[d] = number of rows with degree >= d (d <= kHubDeg + 1) lets a launch put
+// its own class boundary (it depends on k) without touching the device.
+struct Sched {
+    int32_t n = 0;
+    int32_t *order = nullptr;            // device [n]
+    int32_t n_hub = 0;                   // rows with degree > kHubDeg
+    std::vector<int32_t> ge;             // host, size kHubDeg + 2 (empty => no classes)
+    int32_t rows_above(int t) const {    // rows with t < degree <= kHubDeg
+        if (ge.empty() || t + 1 > kHubDeg + 1) return 0;
+        return ge[t + 1] - n_hub;
+    }
+};
+
 struct RelDev {
     int32_t n_dst = 0, n_src = 0;
     int64_t nnz = 0;
@@ -75,25 +91,19 @@ struct RelDev {
     float *ew = nullptr;         // [nnz] a_e * s_col(e); nullptr when identically 1
     float *c = nullptr;          // [n_dst]
     float *s = nullptr;          // [n_src]
-    int32_t *order = nullptr;    // [n_dst] hubs first (desc degree), then desc degree
-    int32_t n_hub = 0;
+    Sched fwd;                   // destination rows
     // backward: CSC rows = sources
     int32_t *colptr = nullptr;   // [n_src+1]
     int32_t *row = nullptr;      // [nnz]
     float *ewT = nullptr;        // [nnz] a_ij in CSC order; nullptr when identically 1
-    int32_t *orderT = nullptr;   // [n_src] source processing order for this relation alone
-    int32_t n_hubT = 0;
+    Sched bwd;                   // source rows of this relation alone (standalone dr_spmm_bwd)
     int32_t max_deg_dst = 0, max_deg_src = 0;
 };
 
-// Source-side schedule for the fused per-source-type SSpMM (cell sources sum
+// Source-side schedules for the fused per-source-type SSpMM (cell sources sum
 // near + pins, net sources use pinned; Alg. 2 stage 2 "for each source node
-// type").
-struct SrcSched {
-    int32_t n = 0;
-    int32_t *order = nullptr;
-    int32_t n_hub = 0;
-};
+// type") are plain Scheds over the combined CSC degree.
+using SrcSched = Sched;
 
 }  // namespace dr
 

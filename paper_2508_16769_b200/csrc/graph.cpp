@@ -22,7 +22,7 @@ struct HostRel {
     int32_t n_dst = 0, n_src = 0;
     int64_t nnz = 0;
     dr_module module = DR_SAGE_MEAN;
-    std::vector<int32_t> rowptr, col, order, colptr, row, orderT;
+    std::vector<int32_t> rowptr, col, order, colptr, row, orderT, ge, geT;
     std::vector<float> ew, c, s, ewT;
     std::vector<int32_t> deg_in, deg_out;
     int32_t n_hub = 0, n_hubT = 0, max_in = 0, max_out = 0;
@@ -31,17 +31,22 @@ struct HostRel {
     std::string err;
 };
 
-// Hubs (deg > kHubDeg) first, by descending degree; then the rest by
-// descending degree (stable on id), or in id order when `identity`.
+// Rows by descending degree (stable on id): hubs (deg > kHubDeg) first, then
+// the warp-row and sub-warp-row classes whose boundary a launch picks from
+// ge[] (rows with degree >= d). In id order, with no classes, when `identity`.
 void make_order(const std::vector<int32_t> &deg, bool identity, std::vector<int32_t> &order,
-                int32_t &n_hub) {
+                int32_t &n_hub, std::vector<int32_t> &ge) {
     const int32_t n = (int32_t)deg.size();
     order.resize(n);
+    ge.clear();
     if (identity) {
         std::iota(order.begin(), order.end(), 0);
         n_hub = 0;
         return;
     }
+    ge.assign(kHubDeg + 2, 0);
+    for (int32_t d : deg) ge[std::min(d, kHubDeg + 1)]++;
+    for (int dd = kHubDeg; dd >= 0; --dd) ge[dd] += ge[dd + 1];
     int32_t dmax = 0;
     for (int32_t d : deg) dmax = std::max(dmax, d);
     std::vector<int64_t> cnt((size_t)dmax + 2, 0);
@@ -135,8 +140,8 @@ void build_rel(const dr_rel_desc &d, bool validate, bool identity, HostRel &h) {
             h.row[p] = i;
             if (h.weighted) h.ewT[p] = d.val[e];
         }
-    make_order(h.deg_in, identity, h.order, h.n_hub);
-    make_order(h.deg_out, identity, h.orderT, h.n_hubT);
+    make_order(h.deg_in, identity, h.order, h.n_hub, h.ge);
+    make_order(h.deg_out, identity, h.orderT, h.n_hubT, h.geT);
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -231,8 +236,9 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
             degc[j] = h[DR_NEAR].deg_out[j] + h[DR_PINS].deg_out[j];
         for (int32_t j = 0; j < n_net; ++j) degn[j] = h[DR_PINNED].deg_out[j];
         int32_t hub_c = 0, hub_n = 0;
-        make_order(degc, identity, ord_c, hub_c);
-        make_order(degn, identity, ord_n, hub_n);
+        std::vector<int32_t> ge_c, ge_n;
+        make_order(degc, identity, ord_c, hub_c, ge_c);
+        make_order(degn, identity, ord_n, hub_n, ge_n);
 
         // ---- phase 2: one device block, carved per array
         g = new dr_graph();
@@ -263,8 +269,12 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
             d.n_src = hr.n_src;
             d.nnz = hr.nnz;
             d.module = hr.module;
-            d.n_hub = hr.n_hub;
-            d.n_hubT = hr.n_hubT;
+            d.fwd.n = hr.n_dst;
+            d.fwd.n_hub = hr.n_hub;
+            d.fwd.ge = hr.ge;
+            d.bwd.n = hr.n_src;
+            d.bwd.n_hub = hr.n_hubT;
+            d.bwd.ge = hr.geT;
             d.max_deg_dst = hr.max_in;
             d.max_deg_src = hr.max_out;
             plan(r, (void **)&d.rowptr, hr.rowptr.data(), hr.rowptr.size() * 4);
@@ -272,8 +282,8 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
             plan(r, (void **)&d.ew, hr.ew.data(), hr.ew.size() * 4);
             plan(r, (void **)&d.c, hr.c.data(), hr.c.size() * 4);
             plan(r, (void **)&d.s, hr.s.data(), hr.s.size() * 4);
-            plan(r, (void **)&d.order, hr.order.data(), hr.order.size() * 4);
-            plan(r, (void **)&d.orderT, hr.orderT.data(), hr.orderT.size() * 4);
+            plan(r, (void **)&d.fwd.order, hr.order.data(), hr.order.size() * 4);
+            plan(r, (void **)&d.bwd.order, hr.orderT.data(), hr.orderT.size() * 4);
             plan(r, (void **)&d.ewT, hr.ewT.data(), hr.ewT.size() * 4);
             const bool alias = (r == DR_NEAR && near_sym) || (r != DR_NEAR && pins_T);
             if (!alias) {
@@ -283,8 +293,10 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
         }
         g->src_cell.n = n_cell;
         g->src_cell.n_hub = hub_c;
+        g->src_cell.ge = ge_c;
         g->src_net.n = n_net;
         g->src_net.n_hub = hub_n;
+        g->src_net.ge = ge_n;
         plan(3, (void **)&g->src_cell.order, ord_c.data(), ord_c.size() * 4);
         plan(3, (void **)&g->src_net.order, ord_n.data(), ord_n.size() * 4);
         char *base = (char *)g->alloc.get(total, cs);
@@ -366,7 +378,7 @@ extern "C" dr_status dr_graph_info(const dr_graph *g, dr_graph_info_t *info) {
         info->nnz[r] = g->rel[r].nnz;
         info->max_deg_dst[r] = g->rel[r].max_deg_dst;
         info->max_deg_src[r] = g->rel[r].max_deg_src;
-        info->hub_rows_dst[r] = g->rel[r].n_hub;
+        info->hub_rows_dst[r] = g->rel[r].fwd.n_hub;
     }
     info->hub_rows_src[0] = g->src_cell.n_hub;
     info->hub_rows_src[1] = g->src_net.n_hub;

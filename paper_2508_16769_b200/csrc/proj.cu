@@ -227,15 +227,20 @@ __global__ void __launch_bounds__(kThreads) root_dots_kernel(RootArgs a) {
 }
 
 // ------------------------------------------------------------------ dW partials: Z^T mask(dY), colsum
+// One CTA per contiguous row chunk; the K x N accumulator is split into 4x4
+// blocks owned by threads (<= 4 blocks each, grid.y slices beyond). Rows are
+// staged 32 at a time with 128-bit loads; the merge mask is applied per
+// 4-column group from one 32-bit word. Partials go to part[chunk][K*N (+N)].
 __global__ void __launch_bounds__(kThreads) dw_partial_kernel(DwArgs a) {
     extern __shared__ __align__(16) float sm[];
     constexpr int RS = 32;
-    const int K = a.K, N = a.N, mw = (N + 31) >> 5;
+    const int K = a.K, N = a.N, mw = (N + 31) >> 5, K4 = K >> 2, N4 = N >> 2;
     float *Zs = sm;                                   // [RS][K]
     float *Ys = sm + RS * K;                          // [RS][N]
     const int tid = threadIdx.x;
-    const int nbk = K >> 2, nbo = N >> 2, NB = nbk * nbo;
+    const int NB = K4 * N4;
     const int blk0 = blockIdx.y * (4 * kThreads);     // this CTA's slice of 4x4 blocks
+    const int64_t len = (int64_t)K * N + (a.part_b ? N : 0);
     float acc[4][4][4];
 #pragma unroll
     for (int b = 0; b < 4; ++b)
@@ -247,34 +252,49 @@ __global__ void __launch_bounds__(kThreads) dw_partial_kernel(DwArgs a) {
     const int64_t rbeg = (int64_t)blockIdx.x * a.rows_per_chunk;
     const int64_t rend = min((int64_t)a.n, rbeg + a.rows_per_chunk);
     for (int64_t rb = rbeg; rb < rend; rb += RS) {
-        // stage Z (dense, or densified CBSR) and masked dY
         if (a.Z) {
-            for (int e = tid; e < RS * K; e += kThreads) {
-                const int rr = e / K, cc = e % K;
+            for (int e = tid; e < RS * K4; e += kThreads) {
+                const int rr = e / K4, c4 = e % K4;
                 const int64_t row = rb + rr;
-                Zs[e] = row < rend ? __ldg(a.Z + row * K + cc) : 0.f;
+                reinterpret_cast<float4 *>(Zs)[e] =
+                    row < rend ? __ldg(reinterpret_cast<const float4 *>(a.Z + row * K) + c4)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-        } else {
-            for (int e = tid; e < RS * K; e += kThreads) Zs[e] = 0.f;
+        } else {                                      // densify the CBSR rows
+            for (int e = tid; e < RS * K4; e += kThreads)
+                reinterpret_cast<float4 *>(Zs)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
             __syncthreads();
             for (int e = tid; e < RS * a.k; e += kThreads) {
                 const int rr = e / a.k, t = e % a.k;
                 const int64_t row = rb + rr;
-                if (row < rend) Zs[rr * K + __ldg(a.hidx + row * a.k + t)] = __ldg(a.hval + row * a.k + t);
+                if (row < rend)
+                    Zs[rr * K + __ldg(a.hidx + row * a.k + t)] = __ldg(a.hval + row * a.k + t);
             }
         }
-        for (int e = tid; e < RS * N; e += kThreads) {
-            const int rr = e / N, cc = e % N;
+        for (int e = tid; e < RS * N4; e += kThreads) {
+            const int rr = e / N4, c4 = e % N4;
             const int64_t row = rb + rr;
-            Ys[e] = (row < rend && mask_keep(a.mask, mw, row, cc, a.mask_mode))
-                        ? __ldg(a.dy + row * N + cc) : 0.f;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (row < rend) {
+                v = __ldg(reinterpret_cast<const float4 *>(a.dy + row * N) + c4);
+                if (a.mask_mode != kMaskNone) {
+                    uint32_t bits = (__ldg(a.mask + row * mw + (c4 >> 3)) >> (4 * (c4 & 7))) & 0xfu;
+                    if (a.mask_mode == kMaskNotM) bits = ~bits;
+                    if (!(bits & 1u)) v.x = 0.f;
+                    if (!(bits & 2u)) v.y = 0.f;
+                    if (!(bits & 4u)) v.z = 0.f;
+                    if (!(bits & 8u)) v.w = 0.f;
+                }
+            }
+            reinterpret_cast<float4 *>(Ys)[e] = v;
         }
         __syncthreads();
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const int blk = blk0 + tid + b * kThreads;
             if (blk >= NB) break;
-            const int bk = blk / nbo, bo = blk % nbo;
+            const int bk = blk / N4, bo = blk % N4;
+#pragma unroll 4
             for (int rr = 0; rr < RS; ++rr) {
                 const float4 z = reinterpret_cast<const float4 *>(Zs + rr * K)[bk];
                 const float4 y = reinterpret_cast<const float4 *>(Ys + rr * N)[bo];
@@ -292,28 +312,38 @@ __global__ void __launch_bounds__(kThreads) dw_partial_kernel(DwArgs a) {
             for (int rr = 0; rr < RS; ++rr) bsum += Ys[rr * N + tid];
         __syncthreads();
     }
-    float *out = a.part + (int64_t)blockIdx.x * K * N;
+    float *out = a.part + (int64_t)blockIdx.x * len;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
         const int blk = blk0 + tid + b * kThreads;
         if (blk >= NB) break;
-        const int bk = blk / nbo, bo = blk % nbo;
+        const int bk = blk / N4, bo = blk % N4;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
             reinterpret_cast<float4 *>(out + (int64_t)(bk * 4 + i) * N)[bo] =
                 make_float4(acc[b][i][0], acc[b][i][1], acc[b][i][2], acc[b][i][3]);
     }
-    if (a.part_b && blockIdx.y == 0 && tid < N) a.part_b[(int64_t)blockIdx.x * N + tid] = bsum;
+    if (a.part_b && blockIdx.y == 0 && tid < N) out[(int64_t)K * N + tid] = bsum;
 }
 
-// out[e] (+)= sum_{c < n_chunks} part[c*len + e], fixed order
-__global__ void reduce_chunks_kernel(const float *__restrict__ part, int n_chunks, int64_t len,
-                                     float *__restrict__ out) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len;
-         e += (int64_t)gridDim.x * blockDim.x) {
+// out[e] = sum_{c < n_parts} part[c*len + e] in a fixed order: block (32 x 8),
+// thread (e, s) sums chunks c = s, s+8, ..., then the 8 slices are added in order.
+__global__ void reduce_parts_kernel(const float *__restrict__ part, int n_parts, int64_t len,
+                                    int64_t len_w, float *__restrict__ out_w,
+                                    float *__restrict__ out_b) {
+    __shared__ float red[8][33];
+    const int64_t e = (int64_t)blockIdx.x * 32 + threadIdx.x;
+    float acc = 0.f;
+    if (e < len)
+        for (int c = threadIdx.y; c < n_parts; c += 8) acc += __ldg(part + (int64_t)c * len + e);
+    red[threadIdx.y][threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.y == 0 && e < len) {
         float s = 0.f;
-        for (int c = 0; c < n_chunks; ++c) s += part[(int64_t)c * len + e];
-        out[e] = s;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s += red[q][threadIdx.x];
+        if (e < len_w) out_w[e] = s;
+        else if (out_b) out_b[e - len_w] = s;
     }
 }
 
@@ -359,8 +389,8 @@ void launch_root_dots(const RootArgs &a, cudaStream_t s) {
 }
 
 int dw_num_chunks(int64_t n) {
-    int64_t c = (n + 255) / 256;
-    if (c > 296) c = 296;
+    int64_t c = (n + 511) / 512;
+    if (c > 148) c = 148;
     if (c < 1) c = 1;
     return (int)c;
 }
@@ -372,27 +402,22 @@ size_t dw_part_floats(int64_t n, int K, int N) {
 // grad_w (K x N) = Z^T mask(dY); grad_b (N) = colsum(mask(dY)) if non-null.
 void launch_dw(DwArgs a, float *grad_w, float *grad_b, float *work, cudaStream_t s) {
     ProfScope ps("dw", s);
-    const int chunks = dw_num_chunks(a.n);
-    a.rows_per_chunk = (int)((a.n + chunks - 1) / chunks);
+    const int chunks = a.n > 0 ? dw_num_chunks(a.n) : 0;
+    a.rows_per_chunk = chunks ? (int)((a.n + chunks - 1) / chunks) : 0;
     a.part = work;
-    a.part_b = grad_b ? work + (size_t)chunks * a.K * a.N : nullptr;
-    const size_t smem = (size_t)32 * (a.K + a.N) * 4;
-    const int NB = (a.K / 4) * (a.N / 4);
-    dim3 grid((unsigned)chunks, (unsigned)((NB + 4 * kThreads - 1) / (4 * kThreads)));
-    if (a.n > 0) {
+    a.part_b = grad_b ? work : nullptr;             // flag only: bias lives after K*N per chunk
+    const int64_t len_w = (int64_t)a.K * a.N, len = len_w + (grad_b ? a.N : 0);
+    if (chunks) {
+        const size_t smem = (size_t)32 * (a.K + a.N) * 4;
+        const int NB = (a.K / 4) * (a.N / 4);
+        dim3 grid((unsigned)chunks, (unsigned)((NB + 4 * kThreads - 1) / (4 * kThreads)));
         ensure_smem((const void *)dw_partial_kernel, smem);
         dw_partial_kernel<<<grid, kThreads, smem, s>>>(a);
         note_launch("dw_partial");
     }
-    const int64_t len = (int64_t)a.K * a.N;
-    const int nchunks = a.n > 0 ? chunks : 0;
-    reduce_chunks_kernel<<<(unsigned)((len + 255) / 256 < 592 ? (len + 255) / 256 : 592), 256, 0,
-                           s>>>(work, nchunks, len, grad_w);
-    note_launch("reduce_chunks");
-    if (grad_b) {
-        reduce_chunks_kernel<<<1, 256, 0, s>>>(a.part_b ? a.part_b : work, nchunks, a.N, grad_b);
-        note_launch("reduce_chunks");
-    }
+    reduce_parts_kernel<<<(unsigned)((len + 31) / 32), dim3(32, 8), 0, s>>>(work, chunks, len, len_w,
+                                                                             grad_w, grad_b);
+    note_launch("reduce_parts");
 }
 
 }  // namespace dr

@@ -1,30 +1,35 @@
 // spmm.cu — DR-SpMM forward (Alg. 1, Eq. 5-7) and SSpMM backward (Alg. 2,
 // Eq. 10-11) over CBSR operands, for sm_100a.
 //
-// Mapping (Alg. 1 stage 2, "partition into ceil(32/K) parts"):
-// a warp is split into R = 32/L sub-warps of L = k/P lanes; each sub-warp owns
-// one row, each lane owns P of the row's k CBSR pairs (P = 4 -> one 128-bit
-// value load + one 32-bit index load per neighbour). Rows are processed in the
-// graph's degree-descending order so the R rows of a warp have similar work and
-// the heaviest rows start first. Rows with more than kHubDeg neighbours
-// ("evil rows", §2.3) are handled by one CTA each: its sub-warps
-// split the neighbour list into contiguous chunks and their partials are
-// summed in a fixed order. Every output element therefore has one owner and a
-// fixed summation order: no atomics anywhere (reading Q23), results are
-// bit-reproducible run to run.
+// Lane mapping (Alg. 1 stage 2, "partition into ceil(32/K) parts"):
+// a warp is split into R = 32/L sub-warps of L = k/P lanes; each lane owns P of
+// a CBSR row's k pairs (P = 4: one 128-bit value load + one 32-bit index load
+// per neighbour). Rows are processed in the graph's degree-descending order and
+// split into the three degree classes of stage 2:
+//   sub rows  (deg <= R):          R rows per warp, one sub-warp per row;
+//   warp rows (R < deg <= 256):    one row per warp, the R sub-warps take every
+//                                  R-th neighbour, private partial rows are summed
+//                                  in a fixed order at the end;
+//   hub rows  (deg > 256, "evil rows" §2.3): one CTA per row, its
+//                                  sub-warps take contiguous neighbour chunks,
+//                                  partials summed in a fixed order.
+// Every output element has one owner and a fixed summation order: no atomics
+// anywhere (reading Q23), bit-reproducible results.
 //
-// Forward: the sub-warp accumulates densify(H_j) for its row into a D-float
-// shared-memory row (the k indices of one CBSR row are distinct, so the lanes
-// of a sub-warp never collide), then writes c_i * acc with 128-bit stores.
-// Backward: the sub-warp of source row j keeps its k CBSR indices in registers
-// and pulls dz[i, idx_j,t] over j's CSC list (sampled gather), accumulating in
-// registers; the D-ReLU mask gradient is the scatter of those k values.
+// Forward: sub-warps accumulate densify(H_j) into D-float shared-memory rows.
+// The k indices of one CBSR row are distinct, so a sub-warp's lanes never
+// collide; each neighbour's P read-modify-writes are issued loads-first.
+// Backward: each lane keeps P of the source row's k CBSR indices in registers
+// and pulls dz[i, idx] over the CSC list (sampled gather) into registers;
+// warp rows reduce across sub-warps with a shuffle butterfly. The D-ReLU mask
+// gradient is the scatter of those k values into a zero row.
 #include "dr_internal.h"
 
 namespace dr {
 namespace {
 
 constexpr int kU = 4;           // neighbours in flight per lane (memory-level parallelism)
+constexpr int kHubCtas = 296;   // 2 per SM
 
 template <int P>
 struct Pairs {
@@ -52,39 +57,56 @@ __device__ __forceinline__ void load_pairs(const float *__restrict__ hval,
     }
 }
 
-// Accumulate the neighbours [e0, e1) of one row into `acc` (shared, D floats).
+// Accumulate neighbours e0, e0+stride, ... < e1 of one row into `acc` (shared,
+// D floats). Column ids and weights are prefetched one iteration ahead.
 template <int P>
-__device__ __forceinline__ void fwd_accumulate(int e0, int e1, const int32_t *__restrict__ col,
+__device__ __forceinline__ void fwd_accumulate(int e0, int e1, int stride,
+                                               const int32_t *__restrict__ col,
                                                const float *__restrict__ ew,
                                                const float *__restrict__ hval,
                                                const uint8_t *__restrict__ hidx, int k, int ll,
                                                float *acc) {
-    for (int e = e0; e < e1; e += kU) {
+    int jn[kU];
+    float wn[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+        const int ee = e0 + u * stride;
+        const bool ok = ee < e1;
+        jn[u] = ok ? __ldg(col + ee) : -1;
+        wn[u] = (ok && ew) ? __ldg(ew + ee) : 1.0f;
+    }
+    for (int e = e0; e < e1; e += kU * stride) {
         int j[kU];
         float w[kU];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const bool ok = e + u < e1;
-            j[u] = ok ? __ldg(col + e + u) : -1;
-            w[u] = (ok && ew) ? __ldg(ew + e + u) : 1.0f;
-        }
+        for (int u = 0; u < kU; ++u) { j[u] = jn[u]; w[u] = wn[u]; }
         Pairs<P> pr[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u)
             if (j[u] >= 0) load_pairs<P>(hval, hidx, (int64_t)j[u] * k + ll * P, pr[u]);
 #pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int ee = e + (kU + u) * stride;
+            const bool ok = ee < e1;
+            jn[u] = ok ? __ldg(col + ee) : -1;
+            wn[u] = (ok && ew) ? __ldg(ew + ee) : 1.0f;
+        }
+#pragma unroll
         for (int u = 0; u < kU; ++u)
             if (j[u] >= 0) {
+                float old[P];
 #pragma unroll
-                for (int p = 0; p < P; ++p) acc[pr[u].id[p]] += w[u] * pr[u].v[p];
+                for (int p = 0; p < P; ++p) old[p] = acc[pr[u].id[p]];
+#pragma unroll
+                for (int p = 0; p < P; ++p) acc[pr[u].id[p]] = old[p] + w[u] * pr[u].v[p];
             }
     }
 }
 
 struct FwdArgs {
     const int32_t *order;
-    int32_t n_hub, n_rows;       // order[0..n_hub) hubs, order[n_hub..n_rows) warp rows
-    int32_t hub_ctas;            // blocks [0, hub_ctas) serve hubs
+    int32_t n_hub, n_warp, n_rows;   // [0,n_hub) hubs, [n_hub,n_hub+n_warp) warp rows, rest sub
+    int32_t hub_ctas, warp_ctas;     // block ranges: hubs, warp rows, then sub rows
     const int32_t *rowptr, *col;
     const float *ew, *c;
     const float *hval;
@@ -94,51 +116,78 @@ struct FwdArgs {
 };
 
 template <int P>
-__global__ void __launch_bounds__(256) spmm_fwd_kernel(FwdArgs a) {
+__global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
     extern __shared__ __align__(16) float sm[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
     const int L = a.L, R = 32 / L, sub = lane / L, ll = lane % L, D = a.D, D4 = D >> 2;
     float *acc = sm + (size_t)(wid * R + sub) * D;
     float4 *acc4 = reinterpret_cast<float4 *>(acc);
+    const int b = blockIdx.x;
 
-    if ((int)blockIdx.x < a.hub_ctas) {
-        // ---- CTA per hub row: S sub-warps split the neighbour list, fixed-order reduce
+    if (b < a.hub_ctas) {
+        // ---- hub rows: CTA per row, contiguous chunks per sub-warp, fixed-order sum
         const int S = wpc * R, sidx = wid * R + sub;
-        for (int h = blockIdx.x; h < a.n_hub; h += a.hub_ctas) {
+        for (int h = b; h < a.n_hub; h += a.hub_ctas) {
             const int row = __ldg(a.order + h);
             const int e0 = __ldg(a.rowptr + row), e1 = __ldg(a.rowptr + row + 1);
             for (int c4 = ll; c4 < D4; c4 += L) acc4[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
             __syncwarp();
             const int chunk = (e1 - e0 + S - 1) / S;
             const int b0 = min(e1, e0 + sidx * chunk), b1 = min(e1, b0 + chunk);
-            fwd_accumulate<P>(b0, b1, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc);
+            fwd_accumulate<P>(b0, b1, 1, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc);
             __syncthreads();
             const float cr = __ldg(a.c + row);
             for (int cc = threadIdx.x; cc < D; cc += blockDim.x) {
-                float sacc = 0.f;
-                for (int q = 0; q < S; ++q) sacc += sm[(size_t)q * D + cc];
-                a.z[(int64_t)row * D + cc] = cr * sacc;
+                float s = 0.f;
+                for (int q = 0; q < S; ++q) s += sm[(size_t)q * D + cc];
+                a.z[(int64_t)row * D + cc] = cr * s;
             }
             __syncthreads();
         }
         return;
     }
-    // ---- sub-warp per row
-    const int64_t gw = (int64_t)(blockIdx.x - a.hub_ctas) * wpc + wid;
-    const int pos = a.n_hub + (int)(gw * R) + sub;
+    if (b < a.hub_ctas + a.warp_ctas) {
+        // ---- warp rows: R sub-warps interleave the neighbour list
+        const int pos = a.n_hub + (b - a.hub_ctas) * wpc + wid;
+        const bool valid = pos < a.n_hub + a.n_warp;
+        const int row = valid ? __ldg(a.order + pos) : 0;
+        for (int c4 = ll; c4 < D4; c4 += L) acc4[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncwarp();
+        if (valid)
+            fwd_accumulate<P>(__ldg(a.rowptr + row) + sub, __ldg(a.rowptr + row + 1), R, a.col,
+                              a.ew, a.hval, a.hidx, a.k, ll, acc);
+        __syncwarp();
+        if (valid) {
+            const float cr = __ldg(a.c + row);
+            const float4 *w4 = reinterpret_cast<const float4 *>(sm + (size_t)wid * R * D);
+            float4 *zr = reinterpret_cast<float4 *>(a.z + (int64_t)row * D);
+            for (int c4 = lane; c4 < D4; c4 += 32) {
+                float4 s = w4[c4];
+                for (int q = 1; q < R; ++q) {
+                    const float4 t = w4[(size_t)q * D4 + c4];
+                    s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
+                }
+                __stcs(zr + c4, make_float4(cr * s.x, cr * s.y, cr * s.z, cr * s.w));
+            }
+        }
+        return;
+    }
+    // ---- sub rows: R rows per warp
+    const int64_t gw = (int64_t)(b - a.hub_ctas - a.warp_ctas) * wpc + wid;
+    const int64_t pos = (int64_t)a.n_hub + a.n_warp + gw * R + sub;
     const bool valid = pos < a.n_rows;
     const int row = valid ? __ldg(a.order + pos) : 0;
     for (int c4 = ll; c4 < D4; c4 += L) acc4[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncwarp();
     if (valid)
-        fwd_accumulate<P>(__ldg(a.rowptr + row), __ldg(a.rowptr + row + 1), a.col, a.ew, a.hval,
-                          a.hidx, a.k, ll, acc);
+        fwd_accumulate<P>(__ldg(a.rowptr + row), __ldg(a.rowptr + row + 1), 1, a.col, a.ew,
+                          a.hval, a.hidx, a.k, ll, acc);
     __syncwarp();
     if (valid) {
         const float cr = __ldg(a.c + row);
         float4 *zr = reinterpret_cast<float4 *>(a.z + (int64_t)row * D);
         for (int c4 = ll; c4 < D4; c4 += L) {
-            float4 v = acc4[c4];
+            const float4 v = acc4[c4];
             __stcs(zr + c4, make_float4(cr * v.x, cr * v.y, cr * v.z, cr * v.w));
         }
     }
@@ -147,13 +196,13 @@ __global__ void __launch_bounds__(256) spmm_fwd_kernel(FwdArgs a) {
 // ------------------------------------------------------------------ backward
 struct TermDev {
     const int32_t *colptr, *row;
-    const float *ewT, *s, *c;    // c != nullptr: apply c_i per edge
+    const float *ewT, *s, *c;    // c != nullptr: apply c_i per edge (standalone ABI)
     const float *dz;
 };
 
 struct BwdArgs {
     const int32_t *order;
-    int32_t n_hub, n_rows, hub_ctas;
+    int32_t n_hub, n_warp, n_rows, hub_ctas, warp_ctas;
     TermDev t[2];
     int n_terms;
     const float *root;
@@ -163,18 +212,24 @@ struct BwdArgs {
     int accumulate;
 };
 
+// Pull dz[i, id[p]] over CSC entries e0, e0+stride, ... < e1 into a[p].
 template <int P>
-__device__ __forceinline__ void bwd_term(const TermDev &t, int e0, int e1, const uint32_t *id,
-                                         int D, float *a) {
-    for (int e = e0; e < e1; e += kU) {
+__device__ __forceinline__ void bwd_term(const TermDev &t, int e0, int e1, int stride,
+                                         const uint32_t *id, int D, float *a) {
+    int in[kU];
+    float wn[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+        const int ee = e0 + u * stride;
+        const bool ok = ee < e1;
+        in[u] = ok ? __ldg(t.row + ee) : -1;
+        wn[u] = (ok && t.ewT) ? __ldg(t.ewT + ee) : 1.0f;
+    }
+    for (int e = e0; e < e1; e += kU * stride) {
         int i[kU];
         float w[kU];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const bool ok = e + u < e1;
-            i[u] = ok ? __ldg(t.row + e + u) : -1;
-            w[u] = (ok && t.ewT) ? __ldg(t.ewT + e + u) : 1.0f;
-        }
+        for (int u = 0; u < kU; ++u) { i[u] = in[u]; w[u] = wn[u]; }
         float v[kU][P];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
@@ -184,6 +239,13 @@ __device__ __forceinline__ void bwd_term(const TermDev &t, int e0, int e1, const
                 for (int p = 0; p < P; ++p) v[u][p] = __ldg(dzr + id[p]);
                 if (t.c) w[u] *= __ldg(t.c + i[u]);
             }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int ee = e + (kU + u) * stride;
+            const bool ok = ee < e1;
+            in[u] = ok ? __ldg(t.row + ee) : -1;
+            wn[u] = (ok && t.ewT) ? __ldg(t.ewT + ee) : 1.0f;
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u)
@@ -208,8 +270,8 @@ __device__ __forceinline__ void load_idx(const uint8_t *__restrict__ hidx, int64
     }
 }
 
-// Write the P values of lane ll for source row j (g_kept and/or dense dx via
-// the sub-warp's shared staging row `srow`). Must be reached by the whole warp.
+// Write lane ll's P values of source row j: g_kept and/or the dense dX row
+// (zeros + k values, staged in the sub-warp's shared row). Whole warp calls it.
 template <int P>
 __device__ __forceinline__ void bwd_store(const BwdArgs &a, bool valid, int j, int ll,
                                           const uint32_t *id, const float *g, float *srow) {
@@ -229,7 +291,8 @@ __device__ __forceinline__ void bwd_store(const BwdArgs &a, bool valid, int j, i
         return;
     }
     float4 *s4 = reinterpret_cast<float4 *>(srow);
-    for (int c4 = ll; c4 < D4; c4 += L) s4[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid)
+        for (int c4 = ll; c4 < D4; c4 += L) s4[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncwarp();
     if (valid) {
 #pragma unroll
@@ -244,17 +307,18 @@ __device__ __forceinline__ void bwd_store(const BwdArgs &a, bool valid, int j, i
 }
 
 template <int P>
-__global__ void __launch_bounds__(256) spmm_bwd_kernel(BwdArgs a) {
+__global__ void __launch_bounds__(256, 4) spmm_bwd_kernel(BwdArgs a) {
     extern __shared__ __align__(16) float sm[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
     const int L = a.L, R = 32 / L, sub = lane / L, ll = lane % L;
     float *srow = sm + (size_t)(wid * R + sub) * a.D;
+    const int b = blockIdx.x;
 
-    if ((int)blockIdx.x < a.hub_ctas) {
-        // ---- CTA per hub source row: partials over contiguous chunks, fixed-order sum
+    if (b < a.hub_ctas) {
+        // ---- hub source rows: partials over contiguous chunks, fixed-order sum
         const int S = wpc * R, sidx = wid * R + sub;
-        float *part = sm;                            // [S][k] partials (reuses staging area)
-        for (int h = blockIdx.x; h < a.n_hub; h += a.hub_ctas) {
+        float *part = sm;                            // [S][k] partials + final row
+        for (int h = b; h < a.n_hub; h += a.hub_ctas) {
             const int j = __ldg(a.order + h);
             uint32_t id[P];
             load_idx<P>(a.hidx, (int64_t)j * a.k + ll * P, id);
@@ -269,7 +333,7 @@ __global__ void __launch_bounds__(256) spmm_bwd_kernel(BwdArgs a) {
                 float acc[P];
 #pragma unroll
                 for (int p = 0; p < P; ++p) acc[p] = 0.f;
-                bwd_term<P>(t, b0, b1, id, a.D, acc);
+                bwd_term<P>(t, b0, b1, 1, id, a.D, acc);
                 const float sj = __ldg(t.s + j);
 #pragma unroll
                 for (int p = 0; p < P; ++p) g[p] += sj * acc[p];
@@ -280,13 +344,13 @@ __global__ void __launch_bounds__(256) spmm_bwd_kernel(BwdArgs a) {
             __syncthreads();
             if (threadIdx.x < a.k) {
                 const int t = threadIdx.x;
-                float sacc = 0.f;
-                for (int q = 0; q < S; ++q) sacc += part[(size_t)q * a.k + t];
-                if (a.root) sacc += __ldg(a.root + (int64_t)j * a.k + t);
-                part[(size_t)S * a.k + t] = sacc;    // final values after the partials
+                float s = 0.f;
+                for (int q = 0; q < S; ++q) s += part[(size_t)q * a.k + t];
+                if (a.root) s += __ldg(a.root + (int64_t)j * a.k + t);
+                part[(size_t)S * a.k + t] = s;
             }
             __syncthreads();
-            if (wid == 0 && sub == 0) {              // sub-warp 0 stores the row
+            if (wid == 0 && sub == 0) {
                 float gf[P];
 #pragma unroll
                 for (int p = 0; p < P; ++p) gf[p] = part[(size_t)S * a.k + ll * P + p];
@@ -299,7 +363,7 @@ __global__ void __launch_bounds__(256) spmm_bwd_kernel(BwdArgs a) {
                     float *dr = a.dx + (int64_t)j * a.D;
                     if (!a.accumulate)
                         for (int cc = ll; cc < a.D; cc += L) dr[cc] = 0.f;
-                    __syncwarp((1u << L) - 1u);
+                    __syncwarp(L == 32 ? 0xffffffffu : ((1u << L) - 1u));
 #pragma unroll
                     for (int p = 0; p < P; ++p) {
                         if (a.accumulate) dr[id[p]] += gf[p];
@@ -310,10 +374,12 @@ __global__ void __launch_bounds__(256) spmm_bwd_kernel(BwdArgs a) {
         }
         return;
     }
-    // ---- sub-warp per source row
-    const int64_t gw = (int64_t)(blockIdx.x - a.hub_ctas) * wpc + wid;
-    const int pos = a.n_hub + (int)(gw * R) + sub;
-    const bool valid = pos < a.n_rows;
+    const bool warp_rows = b < a.hub_ctas + a.warp_ctas;
+    int64_t pos;
+    if (warp_rows) pos = (int64_t)a.n_hub + (int64_t)(b - a.hub_ctas) * wpc + wid;
+    else pos = (int64_t)a.n_hub + a.n_warp + ((int64_t)(b - a.hub_ctas - a.warp_ctas) * wpc + wid) * R + sub;
+    const int64_t end = warp_rows ? (int64_t)a.n_hub + a.n_warp : (int64_t)a.n_rows;
+    const bool valid = pos < end;
     const int j = valid ? __ldg(a.order + pos) : 0;
     uint32_t id[P];
     float g[P];
@@ -321,22 +387,33 @@ __global__ void __launch_bounds__(256) spmm_bwd_kernel(BwdArgs a) {
     for (int p = 0; p < P; ++p) { g[p] = 0.f; id[p] = 0; }
     if (valid) {
         load_idx<P>(a.hidx, (int64_t)j * a.k + ll * P, id);
+        const int first = warp_rows ? sub : 0, stride = warp_rows ? R : 1;
         for (int q = 0; q < a.n_terms; ++q) {
             const TermDev &t = a.t[q];
             float acc[P];
 #pragma unroll
             for (int p = 0; p < P; ++p) acc[p] = 0.f;
-            bwd_term<P>(t, __ldg(t.colptr + j), __ldg(t.colptr + j + 1), id, a.D, acc);
+            bwd_term<P>(t, __ldg(t.colptr + j) + first, __ldg(t.colptr + j + 1), stride, id, a.D,
+                        acc);
             const float sj = __ldg(t.s + j);
 #pragma unroll
             for (int p = 0; p < P; ++p) g[p] += sj * acc[p];
         }
-        if (a.root) {
+    }
+    if (warp_rows) {
+        // butterfly over the R sub-warps (lanes with equal ll hold the same positions);
+        // every lane ends with the identical, order-fixed total
+        for (int off = L; off < 32; off <<= 1) {
 #pragma unroll
-            for (int p = 0; p < P; ++p) g[p] += __ldg(a.root + (int64_t)j * a.k + ll * P + p);
+            for (int p = 0; p < P; ++p) g[p] += __shfl_xor_sync(0xffffffffu, g[p], off);
         }
     }
-    bwd_store<P>(a, valid, j, ll, id, g, srow);
+    if (valid && a.root) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) g[p] += __ldg(a.root + (int64_t)j * a.k + ll * P + p);
+    }
+    bwd_store<P>(a, valid && (!warp_rows || sub == 0), j, ll, id, g,
+                 warp_rows ? sm + (size_t)wid * R * a.D : srow);
 }
 
 // ------------------------------------------------------------------ host helpers
@@ -349,16 +426,9 @@ int choose_P(int k, int D) {
     return -1;
 }
 
-template <typename K>
-void set_smem_attr(K kernel, size_t bytes) {
-    static thread_local size_t done = 0;
-    (void)done;
-    if (bytes > 48 * 1024)
-        DR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)bytes));
-}
-
 }  // namespace
+
+void ensure_smem(const void *fn, size_t bytes);
 
 void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
                      float *z, cudaStream_t s) {
@@ -366,8 +436,11 @@ void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, in
     const int P = choose_P(k, dim);
     DR_CHECK(P > 0, DR_ERR_BAD_K, "spmm_fwd: unsupported k");
     FwdArgs a{};
-    a.order = r.order;
-    a.n_hub = r.n_hub;
+    a.order = r.fwd.order;
+    a.L = k / P;
+    const int R = 32 / a.L;
+    a.n_hub = r.fwd.n_hub;
+    a.n_warp = r.fwd.rows_above(R);
     a.n_rows = r.n_dst;
     a.rowptr = r.rowptr;
     a.col = r.col;
@@ -377,26 +450,25 @@ void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, in
     a.hidx = hidx;
     a.k = k;
     a.D = dim;
-    a.L = k / P;
     a.z = z;
-    const int R = 32 / a.L;
     int wpc = 8;
     while (wpc > 1 && (size_t)wpc * R * dim * 4 > 96 * 1024) wpc >>= 1;
     const size_t smem = (size_t)wpc * R * dim * 4;
-    a.hub_ctas = r.n_hub > 0 ? (r.n_hub < 296 ? r.n_hub : 296) : 0;
-    const int64_t rows = (int64_t)r.n_dst - r.n_hub;
-    const int64_t warp_ctas = (rows + (int64_t)wpc * R - 1) / ((int64_t)wpc * R);
-    const unsigned grid = (unsigned)(a.hub_ctas + warp_ctas);
+    a.hub_ctas = a.n_hub > 0 ? (a.n_hub < kHubCtas ? a.n_hub : kHubCtas) : 0;
+    a.warp_ctas = (a.n_warp + wpc - 1) / wpc;
+    const int64_t n_sub = (int64_t)r.n_dst - a.n_hub - a.n_warp;
+    const int64_t sub_ctas = (n_sub + (int64_t)wpc * R - 1) / ((int64_t)wpc * R);
+    const unsigned grid = (unsigned)(a.hub_ctas + a.warp_ctas + sub_ctas);
     if (grid == 0) return;
     ProfScope ps("spmm_fwd", s);
     if (P == 4) {
-        set_smem_attr(spmm_fwd_kernel<4>, smem);
+        ensure_smem((const void *)spmm_fwd_kernel<4>, smem);
         spmm_fwd_kernel<4><<<grid, wpc * 32, smem, s>>>(a);
     } else if (P == 2) {
-        set_smem_attr(spmm_fwd_kernel<2>, smem);
+        ensure_smem((const void *)spmm_fwd_kernel<2>, smem);
         spmm_fwd_kernel<2><<<grid, wpc * 32, smem, s>>>(a);
     } else {
-        set_smem_attr(spmm_fwd_kernel<1>, smem);
+        ensure_smem((const void *)spmm_fwd_kernel<1>, smem);
         spmm_fwd_kernel<1><<<grid, wpc * 32, smem, s>>>(a);
     }
     note_launch("spmm_fwd");
@@ -410,7 +482,10 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, c
     DR_CHECK(P > 0, DR_ERR_BAD_K, "spmm_bwd: unsupported k");
     BwdArgs a{};
     a.order = sched.order;
+    a.L = k / P;
+    const int R = 32 / a.L;
     a.n_hub = sched.n_hub;
+    a.n_warp = sched.rows_above(R);
     a.n_rows = n_src;
     BwdTerm terms[2] = {t0, t1};
     a.n_terms = 0;
@@ -429,30 +504,29 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, c
     a.hidx = hidx;
     a.k = k;
     a.D = dim;
-    a.L = k / P;
     a.g_kept = g_kept;
     a.dx = dx;
     a.accumulate = accumulate ? 1 : 0;
-    const int R = 32 / a.L;
     int wpc = 8;
     while (wpc > 1 && (size_t)wpc * R * dim * 4 > 96 * 1024) wpc >>= 1;
     size_t smem = (size_t)wpc * R * dim * 4;
     const size_t hub_need = ((size_t)wpc * R + 1) * k * 4;    // partials + final row
     if (hub_need > smem) smem = hub_need;
-    a.hub_ctas = sched.n_hub > 0 ? (sched.n_hub < 296 ? sched.n_hub : 296) : 0;
-    const int64_t rows = (int64_t)n_src - sched.n_hub;
-    const int64_t warp_ctas = (rows + (int64_t)wpc * R - 1) / ((int64_t)wpc * R);
-    const unsigned grid = (unsigned)(a.hub_ctas + warp_ctas);
+    a.hub_ctas = a.n_hub > 0 ? (a.n_hub < kHubCtas ? a.n_hub : kHubCtas) : 0;
+    a.warp_ctas = (a.n_warp + wpc - 1) / wpc;
+    const int64_t n_sub = (int64_t)n_src - a.n_hub - a.n_warp;
+    const int64_t sub_ctas = (n_sub + (int64_t)wpc * R - 1) / ((int64_t)wpc * R);
+    const unsigned grid = (unsigned)(a.hub_ctas + a.warp_ctas + sub_ctas);
     if (grid == 0) return;
     ProfScope ps("spmm_bwd", s);
     if (P == 4) {
-        set_smem_attr(spmm_bwd_kernel<4>, smem);
+        ensure_smem((const void *)spmm_bwd_kernel<4>, smem);
         spmm_bwd_kernel<4><<<grid, wpc * 32, smem, s>>>(a);
     } else if (P == 2) {
-        set_smem_attr(spmm_bwd_kernel<2>, smem);
+        ensure_smem((const void *)spmm_bwd_kernel<2>, smem);
         spmm_bwd_kernel<2><<<grid, wpc * 32, smem, s>>>(a);
     } else {
-        set_smem_attr(spmm_bwd_kernel<1>, smem);
+        ensure_smem((const void *)spmm_bwd_kernel<1>, smem);
         spmm_bwd_kernel<1><<<grid, wpc * 32, smem, s>>>(a);
     }
     note_launch("spmm_bwd");
