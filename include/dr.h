@@ -88,7 +88,7 @@ typedef struct {
 } dr_allocator;                              /* NULL => cudaMallocAsync / cudaFreeAsync */
 
 #define DR_GRAPH_SKIP_VALIDATION 1u          /* trust the CSR invariants                 */
-#define DR_GRAPH_ORDER_IDENTITY 2u           /* process rows in id order (no degree sort) */
+#define DR_GRAPH_ORDER_IDENTITY 2u           /* process rows in id order (no degree classes) */
 
 /* Build the device-resident graph: validates each CSR (sorted, unique, in
  * range), checks rel[DR_PINNED] == rel[DR_PINS]^T, counts degrees and

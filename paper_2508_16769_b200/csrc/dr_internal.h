@@ -66,20 +66,25 @@ struct Alloc {
 constexpr int kHubDeg = 256;
 
 // A processing order over the rows of one kernel (destinations for the
-// forward, sources for the backward), sorted by descending degree so the row
-// classes of Alg. 1 stage 2 are contiguous: [hubs | warp rows | sub-warp rows].
-// ge[d] = number of rows with degree >= d (d <= kHubDeg + 1) lets a launch put
-// its own class boundary (it depends on k) without touching the device.
+// forward, sources for the backward), by descending degree so the degree
+// classes of Alg. 1 stage 2 are contiguous: [hubs | warp rows |
+// sub-warp rows]. Hubs (deg > kHubDeg) get a CTA each; the warp/sub-warp
+// boundary depends on k and D, so a launch picks it from ge[] (rows with
+// degree >= d, d <= kHubDeg + 1) without touching the device.
 struct Sched {
     int32_t n = 0;
     int32_t *order = nullptr;            // device [n]
-    int32_t n_hub = 0;                   // rows with degree > kHubDeg
-    std::vector<int32_t> ge;             // host, size kHubDeg + 2 (empty => no classes)
+    int32_t n_hub = 0;
+    std::vector<int32_t> ge;             // host; empty => no classes (identity order)
     int32_t rows_above(int t) const {    // rows with t < degree <= kHubDeg
-        if (ge.empty() || t + 1 > kHubDeg + 1) return 0;
-        return ge[t + 1] - n_hub;
+        if (ge.empty() || t >= kHubDeg) return 0;
+        return ge[t < 0 ? 0 : t + 1] - n_hub;
     }
 };
+// Degree above which a non-hub row gets a whole warp (its R sub-warps take
+// every R-th neighbour): enough neighbours for >= 2 loads in flight per
+// sub-warp; overridable with DR_WARP_ROW_DEG for experiments.
+int warp_row_threshold(int R, int D);
 
 struct RelDev {
     int32_t n_dst = 0, n_src = 0;

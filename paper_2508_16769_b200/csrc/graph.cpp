@@ -22,10 +22,11 @@ struct HostRel {
     int32_t n_dst = 0, n_src = 0;
     int64_t nnz = 0;
     dr_module module = DR_SAGE_MEAN;
-    std::vector<int32_t> rowptr, col, order, colptr, row, orderT, ge, geT;
+    std::vector<int32_t> rowptr, col, order, colptr, row, orderT;
     std::vector<float> ew, c, s, ewT;
     std::vector<int32_t> deg_in, deg_out;
     int32_t n_hub = 0, n_hubT = 0, max_in = 0, max_out = 0;
+    std::vector<int32_t> ge, geT;
     bool weighted = false;
     dr_status st = DR_OK;
     std::string err;
@@ -39,25 +40,69 @@ void make_order(const std::vector<int32_t> &deg, bool identity, std::vector<int3
     const int32_t n = (int32_t)deg.size();
     order.resize(n);
     ge.clear();
+    n_hub = 0;
     if (identity) {
         std::iota(order.begin(), order.end(), 0);
-        n_hub = 0;
         return;
     }
-    ge.assign(kHubDeg + 2, 0);
-    for (int32_t d : deg) ge[std::min(d, kHubDeg + 1)]++;
-    for (int dd = kHubDeg; dd >= 0; --dd) ge[dd] += ge[dd + 1];
     int32_t dmax = 0;
     for (int32_t d : deg) dmax = std::max(dmax, d);
     std::vector<int64_t> cnt((size_t)dmax + 2, 0);
     for (int32_t d : deg) cnt[(size_t)(dmax - d) + 1]++;            // descending degree
     for (size_t b = 1; b < cnt.size(); ++b) cnt[b] += cnt[b - 1];
     for (int32_t i = 0; i < n; ++i) order[(size_t)cnt[(size_t)(dmax - deg[i])]++] = i;
-    n_hub = 0;
     while (n_hub < n && deg[order[n_hub]] > kHubDeg) ++n_hub;
+    ge.assign(kHubDeg + 2, 0);
+    for (int32_t d : deg) ge[std::min(d, kHubDeg + 1)]++;
+    for (int dd = kHubDeg; dd >= 0; --dd) ge[dd] += ge[dd + 1];
 }
 
-void build_rel(const dr_rel_desc &d, bool validate, bool identity, HostRel &h) {
+// Locality rank of the cells: breadth-first order over the near graph (each
+// component from a pseudo-peripheral start found by a first BFS). On a
+// geometric graph consecutive ranks are spatial neighbours, so rows processed
+// together touch overlapping neighbour sets (L2 reuse of gathered rows).
+[[maybe_unused]] std::vector<int64_t> bfs_rank(int32_t n, const std::vector<int32_t> &rp,
+                              const std::vector<int32_t> &col) {
+    std::vector<int64_t> rank((size_t)n, -1);
+    std::vector<int32_t> queue((size_t)n), mark((size_t)n, -1);
+    int64_t next = 0;
+    for (int32_t s = 0; s < n; ++s) {
+        if (rank[s] >= 0) continue;
+        // first sweep: farthest node from s within its component
+        size_t qh = 0, qt = 0;
+        queue[qt++] = s;
+        mark[s] = s;
+        int32_t last = s;
+        while (qh < qt) {
+            const int32_t u = queue[qh++];
+            last = u;
+            for (int32_t e = rp[u]; e < rp[u + 1]; ++e) {
+                const int32_t v = col[e];
+                if (mark[v] != s && rank[v] < 0) {
+                    mark[v] = s;
+                    queue[qt++] = v;
+                }
+            }
+        }
+        // second sweep from the pseudo-peripheral node assigns the ranks
+        qh = qt = 0;
+        queue[qt++] = last;
+        rank[last] = next++;
+        while (qh < qt) {
+            const int32_t u = queue[qh++];
+            for (int32_t e = rp[u]; e < rp[u + 1]; ++e) {
+                const int32_t v = col[e];
+                if (rank[v] < 0) {
+                    rank[v] = next++;
+                    queue[qt++] = v;
+                }
+            }
+        }
+    }
+    return rank;
+}
+
+void build_rel(const dr_rel_desc &d, bool validate, HostRel &h) {
     h.n_dst = d.n_dst;
     h.n_src = d.n_src;
     h.nnz = d.nnz;
@@ -140,8 +185,6 @@ void build_rel(const dr_rel_desc &d, bool validate, bool identity, HostRel &h) {
             h.row[p] = i;
             if (h.weighted) h.ewT[p] = d.val[e];
         }
-    make_order(h.deg_in, identity, h.order, h.n_hub, h.ge);
-    make_order(h.deg_out, identity, h.orderT, h.n_hubT, h.geT);
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -213,7 +256,7 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
             std::vector<std::thread> th;
             for (int w = 0; w < nt; ++w)
                 th.emplace_back([&, w] {
-                    for (int r = w; r < 3; r += nt) build_rel(rel[r], validate, identity, h[r]);
+                    for (int r = w; r < 3; r += nt) build_rel(rel[r], validate, h[r]);
                 });
             for (auto &t : th) t.join();
         }
@@ -230,6 +273,15 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
         const bool near_sym = h[DR_NEAR].rowptr == h[DR_NEAR].colptr &&
                               h[DR_NEAR].col == h[DR_NEAR].row;
 
+        {
+            std::vector<std::thread> th;
+            for (int r = 0; r < 3; ++r)
+                th.emplace_back([&, r] {
+                    make_order(h[r].deg_in, identity, h[r].order, h[r].n_hub, h[r].ge);
+                    make_order(h[r].deg_out, identity, h[r].orderT, h[r].n_hubT, h[r].geT);
+                });
+            for (auto &t : th) t.join();
+        }
         // source schedules for the fused per-source-type backward
         std::vector<int32_t> degc((size_t)n_cell), degn((size_t)n_net), ord_c, ord_n;
         for (int32_t j = 0; j < n_cell; ++j)

@@ -6,8 +6,8 @@
 // a CBSR row's k pairs (P = 4: one 128-bit value load + one 32-bit index load
 // per neighbour). Rows are processed in the graph's degree-descending order and
 // split into the three degree classes of stage 2:
-//   sub rows  (deg <= R):          R rows per warp, one sub-warp per row;
-//   warp rows (R < deg <= 256):    one row per warp, the R sub-warps take every
+//   sub rows  (deg <= 2*4*R):      R rows per warp, one sub-warp per row;
+//   warp rows (2*4*R < deg <= 256): one row per warp, the R sub-warps take every
 //                                  R-th neighbour, private partial rows are summed
 //                                  in a fixed order at the end;
 //   hub rows  (deg > 256, "evil rows" §2.3): one CTA per row, its
@@ -23,6 +23,8 @@
 // and pulls dz[i, idx] over the CSC list (sampled gather) into registers;
 // warp rows reduce across sub-warps with a shuffle butterfly. The D-ReLU mask
 // gradient is the scatter of those k values into a zero row.
+#include <cstdlib>
+
 #include "dr_internal.h"
 
 namespace dr {
@@ -430,6 +432,13 @@ int choose_P(int k, int D) {
 
 void ensure_smem(const void *fn, size_t bytes);
 
+int warp_row_threshold(int R, int D) {
+    const char *e = getenv("DR_WARP_ROW_DEG");     // experiments only
+    const int env = e ? atoi(e) : -1;
+    (void)D;
+    return env >= 0 ? env : 2 * kU * R;
+}
+
 void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
                      float *z, cudaStream_t s) {
     if (r.n_dst <= 0) return;
@@ -440,7 +449,7 @@ void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, in
     a.L = k / P;
     const int R = 32 / a.L;
     a.n_hub = r.fwd.n_hub;
-    a.n_warp = r.fwd.rows_above(R);
+    a.n_warp = r.fwd.rows_above(warp_row_threshold(R, dim));
     a.n_rows = r.n_dst;
     a.rowptr = r.rowptr;
     a.col = r.col;
@@ -485,7 +494,7 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, c
     a.L = k / P;
     const int R = 32 / a.L;
     a.n_hub = sched.n_hub;
-    a.n_warp = sched.rows_above(R);
+    a.n_warp = sched.rows_above(warp_row_threshold(R, dim));
     a.n_rows = n_src;
     BwdTerm terms[2] = {t0, t1};
     a.n_terms = 0;
