@@ -195,11 +195,8 @@ def run_ours(args):
     xn = torch.as_tensor(d.x_net).to(dev)
     lab = torch.as_tensor(d.labels).to(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
-    comm = None
-    if world > 1:
-        uid = [dr.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = dr.nccl_comm_init(uid[0], world, rank)
+    from paper_2508_16769_b200 import dist as ddp
+    comm = ddp.setup_nccl(dr, rank, world)
 
     if wl == "C2":
         flat = torch.as_tensor(dr.flatten_params(P, nl)).to(dev)

@@ -7,6 +7,7 @@ features, labels and parameters (SURVEY.md §8(d) recipe, restated in DESIGN.md
 """
 from .circuit import (  # noqa: F401
     Design,
+    disjoint_union,
     CONFIGS,
     make_design,
     make_config,

@@ -194,6 +194,31 @@ def _nets(rng, pos, n_net, pins_mean, d_max):
     return ptr, col, alpha
 
 
+def disjoint_union(designs, name="union"):
+    """Block-diagonal union of designs (a per-rank batch of graphs, reading Q24):
+    ids of design q are offset by the node counts of designs < q. Data layout only."""
+    def cat(ptrs, cols, offs):
+        ptr = [np.zeros(1, np.int64)]
+        base = 0
+        for p in ptrs:
+            ptr.append(p[1:] + base)
+            base += int(p[-1])
+        col = np.concatenate([c.astype(np.int64) + o for c, o in zip(cols, offs)]) if cols else \
+            np.zeros(0, np.int64)
+        return np.concatenate(ptr), col.astype(np.int32)
+    oc = np.cumsum([0] + [d.n_cell for d in designs])[:-1]
+    on = np.cumsum([0] + [d.n_net for d in designs])[:-1]
+    near = cat([d.near_ptr for d in designs], [d.near_col for d in designs], oc)
+    pins = cat([d.pins_ptr for d in designs], [d.pins_col for d in designs], oc)
+    pinned = cat([d.pinned_ptr for d in designs], [d.pinned_col for d in designs], on)
+    return Design(name, int(sum(d.n_cell for d in designs)), int(sum(d.n_net for d in designs)),
+                  near[0], near[1], pins[0], pins[1], pinned[0], pinned[1],
+                  np.concatenate([d.x_cell for d in designs]),
+                  np.concatenate([d.x_net for d in designs]),
+                  np.concatenate([d.labels for d in designs]),
+                  meta=dict(parts=[d.name for d in designs]))
+
+
 def _permute_csr(ptr, col, row_perm, col_perm):
     """Relabel rows by row_perm[old]=new and cols by col_perm[old]=new."""
     n = ptr.size - 1

@@ -82,8 +82,8 @@ struct Sched {
     }
 };
 // Degree above which a non-hub row gets a whole warp (its R sub-warps take
-// every R-th neighbour): enough neighbours for >= 2 loads in flight per
-// sub-warp; overridable with DR_WARP_ROW_DEG for experiments.
+// every R-th neighbour); 32 measured best for k = 8 and 16 (profiles/r01);
+// overridable with DR_WARP_ROW_DEG for experiments.
 int warp_row_threshold(int R, int D);
 
 struct RelDev {

@@ -6,8 +6,8 @@
 // a CBSR row's k pairs (P = 4: one 128-bit value load + one 32-bit index load
 // per neighbour). Rows are processed in the graph's degree-descending order and
 // split into the three degree classes of stage 2:
-//   sub rows  (deg <= 2*4*R):      R rows per warp, one sub-warp per row;
-//   warp rows (2*4*R < deg <= 256): one row per warp, the R sub-warps take every
+//   sub rows  (deg <= 32):         R rows per warp, one sub-warp per row;
+//   warp rows (32 < deg <= 256):   one row per warp, the R sub-warps take every
 //                                  R-th neighbour, private partial rows are summed
 //                                  in a fixed order at the end;
 //   hub rows  (deg > 256, "evil rows" §2.3): one CTA per row, its
@@ -436,7 +436,8 @@ int warp_row_threshold(int R, int D) {
     const char *e = getenv("DR_WARP_ROW_DEG");     // experiments only
     const int env = e ? atoi(e) : -1;
     (void)D;
-    return env >= 0 ? env : 2 * kU * R;
+    (void)R;
+    return env >= 0 ? env : 32;   // measured best on C2 (k=8) and C4 (k=16): profiles/r01/ab_*.txt
 }
 
 void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,

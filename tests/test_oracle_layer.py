@@ -14,8 +14,7 @@ import numpy as np
 import pytest
 import torch
 
-from gen import make_config, make_design, make_params
-from gen.circuit import Design
+from gen import disjoint_union, make_config, make_design, make_params
 from oracle import oracle as O
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_vectors.json")))
@@ -196,20 +195,6 @@ def test_adam_matches_torch_and_closed_form():
     assert np.array_equal(th0, theta0)
 
 
-def disjoint_union(a: Design, b: Design):
-    """Test-side data layout only: block-diagonal union of two designs."""
-    def cat(pa, ca, pb, cb, off):
-        return (np.concatenate([pa, pb[1:] + pa[-1]]),
-                np.concatenate([ca, cb + off]).astype(np.int32))
-    near = cat(a.near_ptr, a.near_col, b.near_ptr, b.near_col, a.n_cell)
-    pins = cat(a.pins_ptr, a.pins_col, b.pins_ptr, b.pins_col, a.n_cell)
-    pinned = cat(a.pinned_ptr, a.pinned_col, b.pinned_ptr, b.pinned_col, a.n_net)
-    return Design("union", a.n_cell + b.n_cell, a.n_net + b.n_net, near[0], near[1],
-                  pins[0], pins[1], pinned[0], pinned[1],
-                  np.concatenate([a.x_cell, b.x_cell]), np.concatenate([a.x_net, b.x_net]),
-                  np.concatenate([a.labels, b.labels]))
-
-
 def test_dp_mean_equals_union_gradient():
     a = make_design("a", 48, 11, d_cell=16, d_net=16, near_mean=5, near_cap=16, pins_mean=2.5,
                     pins_dmax=10, n_net=20)
@@ -218,7 +203,7 @@ def test_dp_mean_equals_union_gradient():
     P = make_params(16, 16, 16, 2, seed=2)
     ga = O.model_fwd_bwd(O.OGraph(a), P, 2, 4, 4, a.x_cell, a.x_net, a.labels)[1]
     gb = O.model_fwd_bwd(O.OGraph(b), P, 2, 4, 4, b.x_cell, b.x_net, b.labels)[1]
-    u = disjoint_union(a, b)
+    u = disjoint_union([a, b])
     gu = O.model_fwd_bwd(O.OGraph(u), P, 2, 4, 4, u.x_cell, u.x_net, u.labels)[1]
     gm = O.dp_mean([ga, gb])
     for k in gu:
