@@ -10,6 +10,7 @@
 #include <unordered_map>
 
 #include "proj.h"
+#include "tc_gemm.h"
 
 namespace dr {
 
@@ -144,6 +145,7 @@ static void check_out_width(int n, const char *what) {
 struct TapeLayout {
     size_t hc_val, hc_idx, hn_val, hn_idx, z[3], mask, tap_a, tap_b;
     size_t dz[3], root_c, root_n, work[3];
+    size_t img_fa, img_fb, img_fn, img_dz[3];     // packed tcgen05 B operands
     size_t total;
 };
 
@@ -174,6 +176,12 @@ static TapeLayout tape_layout(const dr_graph *g, const dr_layer *L, uint32_t fla
     t.work[0] = put(mx(dw_part_floats(nc, (int)dc, (int)D), dw_part_floats(nc, (int)dc, (int)D)) * 4);
     t.work[1] = put(mx(dw_part_floats(nn, (int)dc, (int)D), dw_part_floats(nn, (int)dn, (int)D)) * 4);
     t.work[2] = put(dw_part_floats(nc, (int)dn, (int)D) * 4);
+    t.img_fa = put(2 * tc_bimg_bytes((int)dc, (int)D));
+    t.img_fb = put(tc_bimg_bytes((int)dn, (int)D));
+    t.img_fn = put(tc_bimg_bytes((int)dc, (int)D) + tc_bimg_bytes((int)dn, (int)D));
+    t.img_dz[DR_NEAR] = put(tc_bimg_bytes((int)D, (int)dc));
+    t.img_dz[DR_PINS] = put(tc_bimg_bytes((int)D, (int)dc));
+    t.img_dz[DR_PINNED] = put(tc_bimg_bytes((int)D, (int)dn));
     t.total = off;
     return t;
 }
@@ -219,31 +227,72 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
     { TagScope t("pinned"); launch_spmm_fwd(g->rel[DR_PINNED], hnv, hni, L->k_net, L->d_net, z[DR_PINNED], s2); }
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[2], s2));                               // Z_pinned ready
     if (!seq) DR_CUDA(cudaStreamWaitEvent(s1, C.ev[1], 0));
+    const bool tc = tc_supported(L->d_out);
     {   // net: Y_net = Z_pins Wn_pins + densify(H_n) Wr_pins + b_pins   (Eq. 7, 9)
-        ProjFwdArgs a;
-        a.n = nn; a.Ka = L->d_cell; a.N = L->d_out;
-        a.Za = z[DR_PINS]; a.Wa = L->wn[DR_PINS]; a.ba = L->b[DR_PINS];
-        a.Wr = L->wr[DR_PINS]; a.hval = hnv; a.hidx = hni; a.k = L->k_net;
-        a.y = yn;
         TagScope t("net");
-        launch_proj_fwd(a, s1);
+        if (tc) {
+            uint8_t *img = (uint8_t *)(tp + T.img_fn);
+            launch_pack_b(L->wn[DR_PINS], L->d_out, L->d_cell, L->d_out, true, img, s1);
+            if (L->wr[DR_PINS])
+                launch_pack_b(L->wr[DR_PINS], L->d_out, L->d_net, L->d_out, true,
+                              img + tc_bimg_bytes(L->d_cell, L->d_out), s1);
+            TcRowsDesc d;
+            d.n = nn; d.N = L->d_out; d.G = 1; d.epi = kEpiFwd;
+            d.nseg[0] = L->wr[DR_PINS] ? 2 : 1;
+            d.seg[0][0].A = z[DR_PINS]; d.seg[0][0].K = L->d_cell;
+            d.seg[0][1].hval = hnv; d.seg[0][1].hidx = hni; d.seg[0][1].k = L->k_net;
+            d.seg[0][1].K = L->d_net;
+            d.bimg[0] = img; d.bias[0] = L->b[DR_PINS];
+            d.y = yn;
+            launch_tc_rows(d, s1);
+        } else {
+            ProjFwdArgs a;
+            a.n = nn; a.Ka = L->d_cell; a.N = L->d_out;
+            a.Za = z[DR_PINS]; a.Wa = L->wn[DR_PINS]; a.ba = L->b[DR_PINS];
+            a.Wr = L->wr[DR_PINS]; a.hval = hnv; a.hidx = hni; a.k = L->k_net;
+            a.y = yn;
+            launch_proj_fwd(a, s1);
+        }
     }
     if (!seq) DR_CUDA(cudaStreamWaitEvent(s0, C.ev[2], 0));
     {   // cell: Y_cell = max(Y_near, Y_pinned), M   (Eq. 6, 8, 14)
-        ProjFwdArgs a;
-        a.n = nc; a.Ka = L->d_cell; a.Kb = L->d_net; a.N = L->d_out;
-        a.Za = z[DR_NEAR]; a.Wa = L->wn[DR_NEAR]; a.ba = L->b[DR_NEAR];
-        a.Wr = L->wr[DR_NEAR]; a.hval = hcv; a.hidx = hci; a.k = L->k_cell;
-        a.Zb = z[DR_PINNED]; a.Wb = L->wn[DR_PINNED]; a.bb = L->b[DR_PINNED];
-        a.merge = L->merge;
-        a.y = yc;
-        a.mask = (uint32_t *)(tp + T.mask);
-        if (flags & DR_FWD_TAPS) {
-            a.tap_a = (float *)(tp + T.tap_a);
-            a.tap_b = (float *)(tp + T.tap_b);
-        }
         TagScope t("cell");
-        launch_proj_fwd(a, s0);
+        float *tap_a = (flags & DR_FWD_TAPS) ? (float *)(tp + T.tap_a) : nullptr;
+        float *tap_b = (flags & DR_FWD_TAPS) ? (float *)(tp + T.tap_b) : nullptr;
+        if (tc) {
+            uint8_t *ia = (uint8_t *)(tp + T.img_fa), *ib = (uint8_t *)(tp + T.img_fb);
+            launch_pack_b(L->wn[DR_NEAR], L->d_out, L->d_cell, L->d_out, true, ia, s0);
+            if (L->wr[DR_NEAR])
+                launch_pack_b(L->wr[DR_NEAR], L->d_out, L->d_cell, L->d_out, true,
+                              ia + tc_bimg_bytes(L->d_cell, L->d_out), s0);
+            launch_pack_b(L->wn[DR_PINNED], L->d_out, L->d_net, L->d_out, true, ib, s0);
+            TcRowsDesc d;
+            d.n = nc; d.N = L->d_out; d.G = 2; d.epi = kEpiFwd;
+            d.nseg[0] = L->wr[DR_NEAR] ? 2 : 1;
+            d.seg[0][0].A = z[DR_NEAR]; d.seg[0][0].K = L->d_cell;
+            d.seg[0][1].hval = hcv; d.seg[0][1].hidx = hci; d.seg[0][1].k = L->k_cell;
+            d.seg[0][1].K = L->d_cell;
+            d.nseg[1] = 1;
+            d.seg[1][0].A = z[DR_PINNED]; d.seg[1][0].K = L->d_net;
+            d.bimg[0] = ia; d.bimg[1] = ib;
+            d.bias[0] = L->b[DR_NEAR]; d.bias[1] = L->b[DR_PINNED];
+            d.merge = L->merge;
+            d.y = yc; d.mask_out = (uint32_t *)(tp + T.mask);
+            d.tap_a = tap_a; d.tap_b = tap_b;
+            launch_tc_rows(d, s0);
+        } else {
+            ProjFwdArgs a;
+            a.n = nc; a.Ka = L->d_cell; a.Kb = L->d_net; a.N = L->d_out;
+            a.Za = z[DR_NEAR]; a.Wa = L->wn[DR_NEAR]; a.ba = L->b[DR_NEAR];
+            a.Wr = L->wr[DR_NEAR]; a.hval = hcv; a.hidx = hci; a.k = L->k_cell;
+            a.Zb = z[DR_PINNED]; a.Wb = L->wn[DR_PINNED]; a.bb = L->b[DR_PINNED];
+            a.merge = L->merge;
+            a.y = yc;
+            a.mask = (uint32_t *)(tp + T.mask);
+            a.tap_a = tap_a;
+            a.tap_b = tap_b;
+            launch_proj_fwd(a, s0);
+        }
     }
     if (!seq) {
         wait_on(st, s0, C.ev[3]);
@@ -287,7 +336,18 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
     };
     if (dxc || dxn) {
         auto dzk = [&](int64_t n, int K, const float *dy, int mode, const float *W,
-                       const float *c, float *out, cudaStream_t s) {
+                       const float *c, float *out, uint8_t *img, cudaStream_t s) {
+            if (tc_supported(K)) {       // dZ = c (mask(dY) W^T): B_op[n][kk] = W[n][kk]
+                launch_pack_b(W, D, D, K, false, img, s);
+                TcRowsDesc d;
+                d.n = n; d.N = K; d.G = 1; d.epi = kEpiDz;
+                d.nseg[0] = 1;
+                d.seg[0][0].A = dy; d.seg[0][0].K = D; d.seg[0][0].mask_mode = mode;
+                d.mask_in = mask; d.mask_in_width = D;
+                d.bimg[0] = img; d.crow = c; d.dz = out;
+                launch_tc_rows(d, s);
+                return;
+            }
             ProjBwdArgs a;
             a.n = n; a.N = D; a.K = K; a.dy = dy; a.mask = mask; a.mask_mode = mode;
             a.W = W; a.c = c; a.dz = out;
@@ -303,19 +363,21 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
         // dZ'_psi = c_psi (dY_psi Wn_psi^T)  (row-scaled by the destination normaliser)
         {
             TagScope t("near");
-            dzk(nc, L->d_cell, dyc, mode_near, L->wn[DR_NEAR], g->rel[DR_NEAR].c, dz[DR_NEAR], s0);
+            dzk(nc, L->d_cell, dyc, mode_near, L->wn[DR_NEAR], g->rel[DR_NEAR].c, dz[DR_NEAR],
+                (uint8_t *)(tp + T.img_dz[DR_NEAR]), s0);
             if (L->wr[DR_NEAR]) rootk(nc, L->k_cell, dyc, mode_near, L->wr[DR_NEAR], hci, root_c, s0);
         }
         {
             TagScope t("pins");
-            dzk(nn, L->d_cell, dyn, kMaskNone, L->wn[DR_PINS], g->rel[DR_PINS].c, dz[DR_PINS], s1);
+            dzk(nn, L->d_cell, dyn, kMaskNone, L->wn[DR_PINS], g->rel[DR_PINS].c, dz[DR_PINS],
+                (uint8_t *)(tp + T.img_dz[DR_PINS]), s1);
             if (L->wr[DR_PINS]) rootk(nn, L->k_net, dyn, kMaskNone, L->wr[DR_PINS], hni, root_n, s1);
         }
         if (!seq) DR_CUDA(cudaEventRecord(C.ev[0], s1));                           // dZ_pins, root_n
         {
             TagScope t("pinned");
             dzk(nc, L->d_net, dyc, mode_pinned, L->wn[DR_PINNED], g->rel[DR_PINNED].c,
-                dz[DR_PINNED], s2);
+                dz[DR_PINNED], (uint8_t *)(tp + T.img_dz[DR_PINNED]), s2);
         }
         // SSpMM per source node type (Alg. 2 stage 2-3, ownership instead of atomics)
         if (dxc) {

@@ -338,3 +338,31 @@ def test_train_step_c2_runs_and_loss_decreases():
     losses = [tr.step(g, xc, xn, y) for _ in range(30)]
     assert np.all(np.isfinite(losses))
     assert losses[-1] < losses[0]
+
+
+# ------------------------------------------------------------------ tensor-core dense path
+@pytest.mark.parametrize("name,D,k", [("C1", 16, 4), ("C2s", 64, 8), ("C4s", 128, 16)])
+def test_dense_tcgen05_matches_simt(designs, name, D, k, monkeypatch):
+    """The tcgen05 3xTF32 projections/dZ agree with the SIMT fp32 kernels (both
+    are separately pinned to the oracle above) to 1e-5 row-normalised."""
+    d = designs[name]
+    g = _graph(d)
+    P = make_params(D, D, D, 1, seed=8)
+    L, W = _layer(P, 0, D, D, D, k, k)
+    rng = np.random.default_rng(12)
+    xc = cuda(rng.standard_normal((d.n_cell, D)).astype(np.float32))
+    xn = cuda(rng.standard_normal((d.n_net, D)).astype(np.float32))
+    dyc = cuda(rng.standard_normal((d.n_cell, D)).astype(np.float32))
+    dyn = cuda(rng.standard_normal((d.n_net, D)).astype(np.float32))
+    outs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("DR_DENSE_SIMT", mode)
+        yc, yn, tape = dr.heteroconv_fwd(g, L, xc, xn, flags=dr.DR_FWD_TAPS)
+        v = dr.tape_view(g, L, tape, dr.DR_FWD_TAPS)
+        grads, dxc, dxn = dr.heteroconv_bwd(g, L, tape, dyc, dyn, flags=dr.DR_FWD_TAPS)
+        torch.cuda.synchronize()
+        outs[mode] = dict(yc=to_np(yc), yn=to_np(yn), ya=to_np(v["y_near"]),
+                          yb=to_np(v["y_pinned"]), dxc=to_np(dxc), dxn=to_np(dxn),
+                          **{kk: to_np(vv) for kk, vv in grads.items()})
+    for key in outs["0"]:
+        assert row_err(outs["0"][key], outs["1"][key]) <= 1e-5, key
