@@ -126,9 +126,18 @@ def kernel_work(tag, d, D, k, n_layers):
         n = d.n_cell if rel == "cell" else d.n_net
         g = 2 if rel == "cell" else 1
         return n * (g * D * 4 + D * 4), 2.0 * n * D * D * g
-    if kind in ("proj_bwd_dz", "dw"):
+    if kind in ("proj_bwd_dz", "dw", "tc_dz"):
         n = ndst.get(rel, d.n_cell)
         return n * 8 * D, 2.0 * n * D * D
+    if kind == "tc_proj":
+        n = d.n_cell if rel == "cell" else d.n_net
+        if rel == "cell":       # Z_near, Z_pinned read, CBSR root input, Y written
+            return n * (2 * D * 4 + 5 * k + 4 * D), 2.0 * n * D * (3 * D)
+        return n * (D * 4 + 5 * k + 4 * D), 2.0 * n * D * (2 * D)
+    if kind == "tc_dw":
+        n = ndst.get(rel, d.n_cell)
+        kin = 2 * D if rel in ("near", "pins") else D
+        return n * (kin * 4 + D * 4), 2.0 * n * kin * D
     return 0, 0.0
 
 
@@ -153,6 +162,22 @@ def roofline(prof, d, D, k, n_layers, steps, hbm, bf16, src):
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(dom.split(".")[0] + "." + dom.split(".")[-1])
     kind = dom.split(".")[0]
+    if kind.startswith("tc_"):
+        # tcgen05 3xTF32: tensor peak = measured bf16 x nominal tf32/bf16 ratio (1.1/2.25),
+        # useful flops are 1/3 of issued; report whichever roofline binds
+        tf32 = bf16 * (1.1 / 2.25)
+        t_hbm, t_tc = b / (hbm * 1e9), 3.0 * f / (tf32 * 1e12)
+        if t_tc > t_hbm:
+            ach = 3.0 * f / per_s / 1e12
+            rf = {"kernel": dom, "bound": "tensor", "achieved": round(ach, 2), "peak": round(tf32, 1),
+                  "unit": "TFLOP/s", "frac": round(ach / tf32, 4), "traffic": traffic,
+                  "peak_source": "MEASURED_PEAKS.json bf16 x 1.1/2.25 (tf32, issued 3xTF32 flops)"}
+        else:
+            ach = b / per_s / 1e9
+            rf = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm,
+                  "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": traffic,
+                  "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})"}
+        return rf, table
     if kind in ("proj_fwd", "proj_bwd_dz", "dw"):
         ach = f / per_s / 1e12
         rf = {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(FP32_SIMT_TFLOPS, 1),

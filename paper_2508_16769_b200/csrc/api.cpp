@@ -173,9 +173,11 @@ static TapeLayout tape_layout(const dr_graph *g, const dr_layer *L, uint32_t fla
     t.root_c = put(nc * kc * 4);
     t.root_n = put(nn * kn * 4);
     auto mx = [](size_t a, size_t b) { return a > b ? a : b; };
-    t.work[0] = put(mx(dw_part_floats(nc, (int)dc, (int)D), dw_part_floats(nc, (int)dc, (int)D)) * 4);
-    t.work[1] = put(mx(dw_part_floats(nn, (int)dc, (int)D), dw_part_floats(nn, (int)dn, (int)D)) * 4);
-    t.work[2] = put(dw_part_floats(nc, (int)dn, (int)D) * 4);
+    const int gc = dc + dc <= 128 ? 1 : 2, gn = dc + dn <= 128 ? 1 : 2;
+    t.work[0] = put(mx(dw_part_floats(nc, (int)dc, (int)D), tc_reduce_work_floats(nc, gc, (int)D)) * 4);
+    t.work[1] = put(mx(mx(dw_part_floats(nn, (int)dc, (int)D), dw_part_floats(nn, (int)dn, (int)D)),
+                       tc_reduce_work_floats(nn, gn, (int)D)) * 4);
+    t.work[2] = put(mx(dw_part_floats(nc, (int)dn, (int)D), tc_reduce_work_floats(nc, 1, (int)D)) * 4);
     t.img_fa = put(2 * tc_bimg_bytes((int)dc, (int)D));
     t.img_fb = put(tc_bimg_bytes((int)dn, (int)D));
     t.img_fn = put(tc_bimg_bytes((int)dc, (int)D) + tc_bimg_bytes((int)dn, (int)D));
@@ -396,28 +398,63 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
         }
     }
     // weight gradients: dW = Z^T dY_psi, dWr = H^T dY_psi, db = colsum(dY_psi)
+    // weight gradients on tensor cores when the shapes allow (tcgen05, 3xTF32)
+    auto dwt = [&](int64_t n, const float *Za, int wa, float *ga, const float *hv,
+                   const uint8_t *hi, int k, int wb, float *gb, const float *dy, int mode,
+                   float *db, float *wk, cudaStream_t s) {
+        TcReduceDesc d;
+        d.n = n; d.N = D; d.dy = dy; d.mask = mask; d.mask_mode = mode; d.db = db;
+        TcRedSegDesc sa, sb;
+        sa.Z = Za; sa.w = wa; sa.grad = ga;
+        sb.hval = hv; sb.hidx = hi; sb.k = k; sb.w = wb; sb.grad = gb;
+        if (!gb) {
+            d.G = 1; d.nseg[0] = 1; d.seg[0][0] = sa;
+        } else if (wa + wb <= 128) {
+            d.G = 1; d.nseg[0] = 2; d.seg[0][0] = sa; d.seg[0][1] = sb;
+        } else {
+            d.G = 2; d.nseg[0] = 1; d.nseg[1] = 1; d.seg[0][0] = sa; d.seg[1][0] = sb;
+        }
+        launch_tc_reduce(d, wk, s);
+    };
+    const bool tcw = tc_supported(D) && L->d_cell <= 128 && L->d_net <= 128;
     {
         TagScope t("near");
-        dw(nc, L->d_cell, z[DR_NEAR], nullptr, nullptr, 0, dyc, mode_near, G->wn[DR_NEAR],
-           G->b[DR_NEAR], work[0], s0);
-        TagScope t2("root");
-        if (L->wr[DR_NEAR])
-            dw(nc, L->d_cell, nullptr, hcv, hci, L->k_cell, dyc, mode_near, G->wr[DR_NEAR],
-               nullptr, work[0], s0);
+        if (tcw) {
+            dwt(nc, z[DR_NEAR], L->d_cell, G->wn[DR_NEAR], hcv, hci, L->k_cell, L->d_cell,
+                L->wr[DR_NEAR] ? G->wr[DR_NEAR] : nullptr, dyc, mode_near, G->b[DR_NEAR],
+                work[0], s0);
+        } else {
+            dw(nc, L->d_cell, z[DR_NEAR], nullptr, nullptr, 0, dyc, mode_near, G->wn[DR_NEAR],
+               G->b[DR_NEAR], work[0], s0);
+            TagScope t2("root");
+            if (L->wr[DR_NEAR])
+                dw(nc, L->d_cell, nullptr, hcv, hci, L->k_cell, dyc, mode_near, G->wr[DR_NEAR],
+                   nullptr, work[0], s0);
+        }
     }
     {
         TagScope t("pinned");
-        dw(nc, L->d_net, z[DR_PINNED], nullptr, nullptr, 0, dyc, mode_pinned, G->wn[DR_PINNED],
-           G->b[DR_PINNED], work[2], s2);
+        if (tcw)
+            dwt(nc, z[DR_PINNED], L->d_net, G->wn[DR_PINNED], nullptr, nullptr, 0, 0, nullptr,
+                dyc, mode_pinned, G->b[DR_PINNED], work[2], s2);
+        else
+            dw(nc, L->d_net, z[DR_PINNED], nullptr, nullptr, 0, dyc, mode_pinned,
+               G->wn[DR_PINNED], G->b[DR_PINNED], work[2], s2);
     }
     {
         TagScope t("pins");
-        dw(nn, L->d_cell, z[DR_PINS], nullptr, nullptr, 0, dyn, kMaskNone, G->wn[DR_PINS],
-           G->b[DR_PINS], work[1], s1);
-        TagScope t2("root");
-        if (L->wr[DR_PINS])
-            dw(nn, L->d_net, nullptr, hnv, hni, L->k_net, dyn, kMaskNone, G->wr[DR_PINS],
-               nullptr, work[1], s1);
+        if (tcw) {
+            dwt(nn, z[DR_PINS], L->d_cell, G->wn[DR_PINS], hnv, hni, L->k_net, L->d_net,
+                L->wr[DR_PINS] ? G->wr[DR_PINS] : nullptr, dyn, kMaskNone, G->b[DR_PINS],
+                work[1], s1);
+        } else {
+            dw(nn, L->d_cell, z[DR_PINS], nullptr, nullptr, 0, dyn, kMaskNone, G->wn[DR_PINS],
+               G->b[DR_PINS], work[1], s1);
+            TagScope t2("root");
+            if (L->wr[DR_PINS])
+                dw(nn, L->d_net, nullptr, hnv, hni, L->k_net, dyn, kMaskNone, G->wr[DR_PINS],
+                   nullptr, work[1], s1);
+        }
     }
     if (!seq) {
         wait_on(st, s0, C.ev[3]);

@@ -40,6 +40,29 @@ size_t tc_bimg_bytes(int K, int NB);
 void launch_pack_b(const float *W, int ldw, int K, int NB, bool transpose, uint8_t *img,
                    cudaStream_t s);
 bool tc_supported(int N);
+
+// dW = Z^T mask(dY) over all rows, up to 2 accumulator groups of M=128 feature
+// rows, each stacking up to 2 segments (dense Z or densified CBSR). grad of a
+// segment is a w x N row-major matrix; db (N) = colsum(mask(dY)) if non-null.
+struct TcRedSegDesc {
+    const float *Z = nullptr;
+    const float *hval = nullptr;
+    const uint8_t *hidx = nullptr;
+    int k = 0, w = 0;
+    float *grad = nullptr;
+};
+struct TcReduceDesc {
+    int64_t n = 0;
+    int N = 0, G = 1;
+    int nseg[2] = {0, 0};
+    TcRedSegDesc seg[2][2];
+    const float *dy = nullptr;
+    const uint32_t *mask = nullptr;
+    int mask_mode = 0;
+    float *db = nullptr;
+};
+size_t tc_reduce_work_floats(int64_t n, int G, int N);
+void launch_tc_reduce(const TcReduceDesc &d, float *work, cudaStream_t s);
 void launch_tc_rows(const TcRowsDesc &d, cudaStream_t s);
 
 }  // namespace dr
