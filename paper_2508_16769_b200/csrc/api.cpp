@@ -173,7 +173,7 @@ static TapeLayout tape_layout(const dr_graph *g, const dr_layer *L, uint32_t fla
     t.root_c = put(nc * kc * 4);
     t.root_n = put(nn * kn * 4);
     auto mx = [](size_t a, size_t b) { return a > b ? a : b; };
-    const int gc = dc + dc <= 128 ? 1 : 2, gn = dc + dn <= 128 ? 1 : 2;
+    const int gc = 1, gn = 1;
     t.work[0] = put(mx(dw_part_floats(nc, (int)dc, (int)D), tc_reduce_work_floats(nc, gc, (int)D)) * 4);
     t.work[1] = put(mx(mx(dw_part_floats(nn, (int)dc, (int)D), dw_part_floats(nn, (int)dn, (int)D)),
                        tc_reduce_work_floats(nn, gn, (int)D)) * 4);
@@ -407,12 +407,15 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
         TcRedSegDesc sa, sb;
         sa.Z = Za; sa.w = wa; sa.grad = ga;
         sb.hval = hv; sb.hidx = hi; sb.k = k; sb.w = wb; sb.grad = gb;
+        d.G = 1;
         if (!gb) {
-            d.G = 1; d.nseg[0] = 1; d.seg[0][0] = sa;
+            d.nseg[0] = 1; d.seg[0][0] = sa;
         } else if (wa + wb <= 128) {
-            d.G = 1; d.nseg[0] = 2; d.seg[0][0] = sa; d.seg[0][1] = sb;
-        } else {
-            d.G = 2; d.nseg[0] = 1; d.nseg[1] = 1; d.seg[0][0] = sa; d.seg[1][0] = sb;
+            d.nseg[0] = 2; d.seg[0][0] = sa; d.seg[0][1] = sb;
+        } else {                                   // two passes over dY (M = 128 each)
+            d.nseg[0] = 1; d.seg[0][0] = sa;
+            launch_tc_reduce(d, wk, s);
+            d.seg[0][0] = sb; d.db = nullptr;
         }
         launch_tc_reduce(d, wk, s);
     };
