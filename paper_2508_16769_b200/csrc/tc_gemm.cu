@@ -29,7 +29,7 @@ namespace {
 constexpr int kTM = 128;             // MMA M (rows of a tile / feature rows of dW)
 constexpr int kKC = 32;              // K per chunk (one 128-B swizzle atom of fp32)
 constexpr int kThreadsTC = 128;
-constexpr int kSmemMax = 227 * 1024;
+constexpr int kSmemMax = 227 * 1024 - 2048;   // opt-in limit minus static smem
 
 // ---------------------------------------------------------------- B packing
 // img[c] = { hi: NB rows x 128 B (swizzled), lo: NB rows x 128 B } for chunk c of
