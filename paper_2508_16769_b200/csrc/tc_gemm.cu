@@ -28,7 +28,7 @@ namespace {
 
 constexpr int kTM = 128;             // MMA M (rows of a tile / feature rows of dW)
 constexpr int kKC = 32;              // K per chunk (one 128-B swizzle atom of fp32)
-constexpr int kThreadsTC = 128;
+constexpr int kThreadsTC = 256;   // 8 warps: warps w and w+4 share TMEM lane quarter w%4
 constexpr int kSmemMax = 227 * 1024 - 2048;   // opt-in limit minus static smem
 
 // ---------------------------------------------------------------- B packing
@@ -119,7 +119,7 @@ __device__ __forceinline__ void rows_issue_raw(const TcRowsArgs &a, const Step &
     const int tid = threadIdx.x;
     if (s.A) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < 1024 / kThreadsTC; ++i) {
             const int p = tid + kThreadsTC * i, r = p >> 3, q = p & 7;
             const int64_t row = r0 + r;
             const int col = st.c * kKC + q * 4;
@@ -127,7 +127,7 @@ __device__ __forceinline__ void rows_issue_raw(const TcRowsArgs &a, const Step &
             tc::cp_async16(raw + r * 128 + q * 16, ok ? (const void *)(s.A + row * s.K + col)
                                                       : (const void *)s.A, ok ? 16u : 0u);
         }
-        if (s.mask_mode != kMaskNone) {
+        if (s.mask_mode != kMaskNone && tid < kTM) {
             const int64_t row = r0 + tid;
             const bool ok = row < a.n;
             tc::cp_async4(raw + 16384 + tid * 4,
@@ -148,9 +148,10 @@ __device__ __forceinline__ void rows_convert(const TcRowsArgs &a, const Step &st
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (s.A) {
         const int q = lane & 7;
+        constexpr int RPW = kTM / (kThreadsTC / 32);          // rows per warp
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int r = warp * 32 + i * 4 + (lane >> 3);
+        for (int i = 0; i < RPW / 4; ++i) {
+            const int r = warp * RPW + i * 4 + (lane >> 3);
             float4 v = *reinterpret_cast<const float4 *>(raw + r * 128 + q * 16);
             if (s.mask_mode != kMaskNone) {
                 const uint32_t w = *reinterpret_cast<const uint32_t *>(raw + 16384 + r * 4);
@@ -164,17 +165,20 @@ __device__ __forceinline__ void rows_convert(const TcRowsArgs &a, const Step &st
             store_split4(hi, lo, tc::sw128_off(r, q * 4), v);
         }
     } else {
-        const int r = tid;                         // one row per thread
+        // two threads per row: each zeroes half of the row, then (after a barrier)
+        // scatters every other CBSR pair of the row
+        const int r = tid & (kTM - 1), half = tid / kTM;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 4; ++q) {
             const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-            *reinterpret_cast<float4 *>(hi + r * 128 + q * 16) = z;
-            *reinterpret_cast<float4 *>(lo + r * 128 + q * 16) = z;
+            *reinterpret_cast<float4 *>(hi + r * 128 + (half * 4 + q) * 16) = z;
+            *reinterpret_cast<float4 *>(lo + r * 128 + (half * 4 + q) * 16) = z;
         }
+        __syncthreads();
         const float *vals = reinterpret_cast<const float *>(raw) + r * s.k;
         const uint8_t *idx = raw + kTM * s.k * 4 + r * s.k;
         const int lo_c = st.c * kKC;
-        for (int t = 0; t < s.k; ++t) {
+        for (int t = half; t < s.k; t += 2) {
             const int c = (int)idx[t] - lo_c;
             if (c >= 0 && c < kKC) store_split1(hi, lo, tc::sw128_off(r, c), vals[t]);
         }
@@ -184,12 +188,15 @@ __device__ __forceinline__ void rows_convert(const TcRowsArgs &a, const Step &st
 __device__ __forceinline__ void rows_epilogue(const TcRowsArgs &a, uint32_t tmem, int64_t r0) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int N = a.N;
-    const int64_t row = r0 + warp * 32 + lane;
+    const int quarter = warp & 3, half = warp >> 2;
+    const int64_t row = r0 + quarter * 32 + lane;
     const bool ok = row < a.n;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    // column range of this warp: halves of N when both halves hold whole 32-col words
+    const int jb = N >= 64 ? half * (N / 2) : 0, je = N >= 64 ? jb + N / 2 : (half ? 0 : N);
     if (a.epi == kEpiDz) {
         const float cr = (ok && a.crow) ? __ldg(a.crow + row) : 1.f;
-        for (int j = 0; j < N; j += 16) {
+        for (int j = jb; j < je; j += 16) {
             float v[16];
             tc::tmem_ld16(tmem + lane_base + (uint32_t)j, v);
             if (ok) {
@@ -204,19 +211,30 @@ __device__ __forceinline__ void rows_epilogue(const TcRowsArgs &a, uint32_t tmem
     }
     const int mw = (N + 31) >> 5;
     uint32_t word = 0;
-    for (int j = 0; j < N; j += 16) {
+    for (int j = jb; j < je; j += 16) {
         float ya[16], yb[16];
         tc::tmem_ld16(tmem + lane_base + (uint32_t)j, ya);
         if (a.G == 2) tc::tmem_ld16(tmem + lane_base + (uint32_t)(N + j), yb);
         if (!ok) continue;
+        float bias[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) ya[q] += __ldg(a.bias[0] + j + q);
+        for (int q = 0; q < 4; ++q) {
+            const float4 b = __ldg(reinterpret_cast<const float4 *>(a.bias[0] + j) + q);
+            bias[4 * q] = b.x; bias[4 * q + 1] = b.y; bias[4 * q + 2] = b.z; bias[4 * q + 3] = b.w;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) ya[q] += bias[q];
         float y[16];
         uint32_t bits = 0;
         if (a.G == 2) {
 #pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 b = __ldg(reinterpret_cast<const float4 *>(a.bias[1] + j) + q);
+                bias[4 * q] = b.x; bias[4 * q + 1] = b.y; bias[4 * q + 2] = b.z; bias[4 * q + 3] = b.w;
+            }
+#pragma unroll
             for (int q = 0; q < 16; ++q) {
-                yb[q] += __ldg(a.bias[1] + j + q);
+                yb[q] += bias[q];
                 if (a.merge == DR_MERGE_MAX) {
                     const bool m = ya[q] >= yb[q];          // Eq. 14: ties -> near
                     y[q] = m ? ya[q] : yb[q];
@@ -249,7 +267,7 @@ __device__ __forceinline__ void rows_epilogue(const TcRowsArgs &a, uint32_t tmem
         }
         if (a.G == 2 && a.mask_out) {
             word |= bits << (j & 16);
-            if ((j & 16) || j + 16 >= N) {
+            if ((j & 16) || j + 16 >= je) {
                 a.mask_out[row * mw + (j >> 5)] = word;
                 word = 0;
             }
@@ -406,10 +424,12 @@ __device__ __forceinline__ void red_convert(const TcReduceArgs &a, const uint8_t
                                             uint8_t *op, float *dbacc) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t a_bytes = kTM * 128;
-    // A groups: warp w owns feature rows [32w, 32w+32); lane = feature
+    // A groups: warp w owns feature rows [32(w%4), +32) and graph rows [16(w/4), +16);
+    // lane = feature
+    const int quarter = warp & 3, half = warp >> 2;
     for (int g = 0; g < a.G; ++g) {
         char *hi = reinterpret_cast<char *>(op + g * 2 * a_bytes), *lo = hi + a_bytes;
-        const int f = warp * 32 + lane;
+        const int f = quarter * 32 + lane;
         for (int q = 0; q < a.nseg[g]; ++q) {
             const RSeg &s = a.seg[g][q];
             if (f < s.m0 || f >= s.m0 + s.w) continue;
@@ -417,11 +437,12 @@ __device__ __forceinline__ void red_convert(const TcReduceArgs &a, const uint8_t
             if (s.Z) {
                 const float *z = reinterpret_cast<const float *>(raw + s.raw_off);
 #pragma unroll 8
-                for (int rr = 0; rr < 32; ++rr)
+                for (int rr = half * 16; rr < half * 16 + 16; ++rr)
                     store_split1(hi, lo, tc::sw128_off(f, rr), z[rr * s.w + fl]);
             } else {
 #pragma unroll 8
-                for (int rr = 0; rr < 32; ++rr) store_split1(hi, lo, tc::sw128_off(f, rr), 0.f);
+                for (int rr = half * 16; rr < half * 16 + 16; ++rr)
+                    store_split1(hi, lo, tc::sw128_off(f, rr), 0.f);
             }
         }
     }
@@ -445,11 +466,11 @@ __device__ __forceinline__ void red_convert(const TcReduceArgs &a, const uint8_t
         const uint32_t *mk = reinterpret_cast<const uint32_t *>(raw + a.raw_mask);
         const int mw = (a.N + 31) >> 5;
         for (int i = 0; i < 2; ++i) {
-            const int c = (warp + 4 * i) * 32 + lane;  // columns covered by this thread
+            const int c = (quarter + 4 * i) * 32 + lane;  // columns covered by this thread
             if (c >= a.N) break;
             float s = 0.f;
 #pragma unroll 8
-            for (int rr = 0; rr < 32; ++rr) {
+            for (int rr = half * 16; rr < half * 16 + 16; ++rr) {
                 float v = dy[rr * a.N + c];
                 if (a.mask_mode != kMaskNone) {
                     const uint32_t b = (mk[rr * mw + (c >> 5)] >> (c & 31)) & 1u;
@@ -541,14 +562,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_reduce_kernel(TcReduceArgs a
     }
     tc::cp_async_wait<0>();
     float *out = a.part + (int64_t)blockIdx.x * ((int64_t)G * kTM * N + N);
+    const int quarter = warp & 3, half = warp >> 2;
     if (total > 0) {
         const uint32_t last = (uint32_t)((total - 1) & 1), luse = (uint32_t)((total - 1) >> 1);
         tc::mbar_wait(&mma_done[last], luse & 1u);
         tc::fence_after();
-        const int m = warp * 32 + lane;
-        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        const int m = quarter * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+        const int jb = N >= 32 ? half * (N / 2) : 0, je = N >= 32 ? jb + N / 2 : (half ? 0 : N);
         for (int g = 0; g < G; ++g)
-            for (int j = 0; j < N; j += 16) {
+            for (int j = jb; j < je; j += 16) {
                 float v[16];
                 tc::tmem_ld16(tmem + lane_base + (uint32_t)(g * N + j), v);
                 float4 *o = reinterpret_cast<float4 *>(out + ((int64_t)g * kTM + m) * N + j);
@@ -559,9 +582,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_reduce_kernel(TcReduceArgs a
     } else {
         for (int64_t e = tid; e < (int64_t)G * kTM * N; e += kThreadsTC) out[e] = 0.f;
     }
-    for (int i = 0; i < 2; ++i) {
-        const int c = (warp + 4 * i) * 32 + lane;
-        if (c < N) out[(int64_t)G * kTM * N + c] = dbacc[i];
+    {   // db partial: the two row halves of each column, added in a fixed order
+        __shared__ float dbs[2][256];
+        for (int i = 0; i < 2; ++i) {
+            const int c = (quarter + 4 * i) * 32 + lane;
+            if (c < N) dbs[half][c] = dbacc[i];
+        }
+        __syncthreads();
+        for (int c = tid; c < N; c += kThreadsTC) out[(int64_t)G * kTM * N + c] = dbs[0][c] + dbs[1][c];
     }
     tc::fence_before();
     __syncthreads();
