@@ -66,25 +66,23 @@ struct Alloc {
 constexpr int kHubDeg = 256;
 
 // A processing order over the rows of one kernel (destinations for the
-// forward, sources for the backward), by descending degree so the degree
-// classes of Alg. 1 stage 2 are contiguous: [hubs | warp rows |
-// sub-warp rows]. Hubs (deg > kHubDeg) get a CTA each; the warp/sub-warp
-// boundary depends on k and D, so a launch picks it from ge[] (rows with
-// degree >= d, d <= kHubDeg + 1) without touching the device.
+// forward, sources for the backward), split into the degree classes of Alg. 1
+// stage 2: [hubs | warp rows | sub-warp rows]. Hubs (deg >
+// kHubDeg) get a CTA each, warp rows (warp_deg < deg <= kHubDeg) a warp each,
+// sub-warp rows (deg <= warp_deg) share a warp. Inside the warp and sub-warp
+// classes rows are grouped by power-of-two degree bucket (descending, so a warp
+// holds rows of similar work) and ordered by a locality rank inside a bucket
+// (BFS over the near graph), so rows processed at the same time share
+// neighbours and their gathers hit L2. Fixed at graph creation.
 struct Sched {
     int32_t n = 0;
     int32_t *order = nullptr;            // device [n]
-    int32_t n_hub = 0;
-    std::vector<int32_t> ge;             // host; empty => no classes (identity order)
-    int32_t rows_above(int t) const {    // rows with t < degree <= kHubDeg
-        if (ge.empty() || t >= kHubDeg) return 0;
-        return ge[t < 0 ? 0 : t + 1] - n_hub;
-    }
+    int32_t n_hub = 0, n_warp = 0;
 };
 // Degree above which a non-hub row gets a whole warp (its R sub-warps take
 // every R-th neighbour); 32 measured best for k = 8 and 16 (profiles/r01);
-// overridable with DR_WARP_ROW_DEG for experiments.
-int warp_row_threshold(int R, int D);
+// DR_WARP_ROW_DEG overrides it at graph creation (experiments only).
+int warp_row_threshold();
 
 struct RelDev {
     int32_t n_dst = 0, n_src = 0;

@@ -9,6 +9,7 @@
 // uploading on its own CUDA stream.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <thread>
@@ -25,43 +26,50 @@ struct HostRel {
     std::vector<int32_t> rowptr, col, order, colptr, row, orderT;
     std::vector<float> ew, c, s, ewT;
     std::vector<int32_t> deg_in, deg_out;
-    int32_t n_hub = 0, n_hubT = 0, max_in = 0, max_out = 0;
-    std::vector<int32_t> ge, geT;
+    int32_t n_hub = 0, n_hubT = 0, n_warp = 0, n_warpT = 0, max_in = 0, max_out = 0;
     bool weighted = false;
     dr_status st = DR_OK;
     std::string err;
 };
 
-// Rows by descending degree (stable on id): hubs (deg > kHubDeg) first, then
-// the warp-row and sub-warp-row classes whose boundary a launch picks from
-// ge[] (rows with degree >= d). In id order, with no classes, when `identity`.
-void make_order(const std::vector<int32_t> &deg, bool identity, std::vector<int32_t> &order,
-                int32_t &n_hub, std::vector<int32_t> &ge) {
+// Processing order (see Sched in dr_internal.h): hubs by descending degree,
+// then the warp and sub-warp classes, each grouped by power-of-two degree bucket
+// (descending) and ordered by `loc` inside a bucket (by id when `loc` is empty).
+// `identity` keeps plain id order with no classes (pure-DRAM measurement flag).
+void make_order(const std::vector<int32_t> &deg, bool identity, const std::vector<int64_t> &loc,
+                int warp_deg, std::vector<int32_t> &order, int32_t &n_hub, int32_t &n_warp) {
     const int32_t n = (int32_t)deg.size();
     order.resize(n);
-    ge.clear();
-    n_hub = 0;
-    if (identity) {
-        std::iota(order.begin(), order.end(), 0);
-        return;
+    std::iota(order.begin(), order.end(), 0);
+    n_hub = n_warp = 0;
+    if (identity) return;
+    auto bucket = [&](int32_t i) -> int {          // 0 = hub; smaller = heavier
+        const int32_t d = deg[i];
+        if (d > kHubDeg) return 0;
+        int lg = 0;
+        while ((1 << lg) < d) ++lg;                 // ceil(log2(d)), 0 for d <= 1
+        return 1 + (9 - lg);
+    };
+    std::vector<int64_t> key((size_t)n);
+    for (int32_t i = 0; i < n; ++i) {
+        const int b = bucket(i);
+        const int64_t inner = b == 0 ? (int64_t)(INT32_MAX - deg[i])
+                                     : (loc.empty() ? (int64_t)i : loc[i]);
+        key[i] = ((int64_t)b << 40) | inner;
     }
-    int32_t dmax = 0;
-    for (int32_t d : deg) dmax = std::max(dmax, d);
-    std::vector<int64_t> cnt((size_t)dmax + 2, 0);
-    for (int32_t d : deg) cnt[(size_t)(dmax - d) + 1]++;            // descending degree
-    for (size_t b = 1; b < cnt.size(); ++b) cnt[b] += cnt[b - 1];
-    for (int32_t i = 0; i < n; ++i) order[(size_t)cnt[(size_t)(dmax - deg[i])]++] = i;
-    while (n_hub < n && deg[order[n_hub]] > kHubDeg) ++n_hub;
-    ge.assign(kHubDeg + 2, 0);
-    for (int32_t d : deg) ge[std::min(d, kHubDeg + 1)]++;
-    for (int dd = kHubDeg; dd >= 0; --dd) ge[dd] += ge[dd + 1];
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t x, int32_t y) { return key[x] < key[y]; });
+    for (int32_t i = 0; i < n; ++i) {
+        if (deg[i] > kHubDeg) ++n_hub;
+        else if (deg[i] > warp_deg) ++n_warp;
+    }
 }
 
 // Locality rank of the cells: breadth-first order over the near graph (each
 // component from a pseudo-peripheral start found by a first BFS). On a
 // geometric graph consecutive ranks are spatial neighbours, so rows processed
 // together touch overlapping neighbour sets (L2 reuse of gathered rows).
-[[maybe_unused]] std::vector<int64_t> bfs_rank(int32_t n, const std::vector<int32_t> &rp,
+std::vector<int64_t> bfs_rank(int32_t n, const std::vector<int32_t> &rp,
                               const std::vector<int32_t> &col) {
     std::vector<int64_t> rank((size_t)n, -1);
     std::vector<int32_t> queue((size_t)n), mark((size_t)n, -1);
@@ -196,6 +204,12 @@ size_t vbytes(const std::vector<T> &v) {
 
 }  // namespace
 
+int warp_row_threshold() {
+    const char *e = getenv("DR_WARP_ROW_DEG");     // experiments only
+    const int env = e ? atoi(e) : -1;
+    return env >= 0 ? env : 32;   // measured best on C2 (k=8) and C4 (k=16): profiles/r01/ab_*.txt
+}
+
 void *Alloc::get(size_t bytes, cudaStream_t s) {
     if (bytes == 0) bytes = 256;
     void *p = nullptr;
@@ -273,12 +287,33 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
         const bool near_sym = h[DR_NEAR].rowptr == h[DR_NEAR].colptr &&
                               h[DR_NEAR].col == h[DR_NEAR].row;
 
+        // locality ranks: cells by BFS over the near graph,
+        // nets by their lowest-ranked member cell; DR_ORDER=degree drops them
+        std::vector<int64_t> rank_c, rank_n;
+        const char *ord_env = getenv("DR_ORDER");
+        const bool use_loc = !identity && !(ord_env && std::string(ord_env) == "degree");
+        if (use_loc) {
+            rank_c = bfs_rank(n_cell, h[DR_NEAR].rowptr, h[DR_NEAR].col);
+            rank_n.assign((size_t)n_net, 0);
+            const HostRel &pn = h[DR_PINS];         // rows = nets, cols = member cells
+            for (int32_t j = 0; j < n_net; ++j) {
+                int64_t m = (int64_t)n_cell + j;
+                for (int32_t e = pn.rowptr[j]; e < pn.rowptr[j + 1]; ++e)
+                    m = std::min(m, rank_c[pn.col[e]]);
+                rank_n[j] = m;
+            }
+        }
+        const int wdeg = warp_row_threshold();
         {
+            const std::vector<int64_t> *dst_loc[3] = {&rank_c, &rank_n, &rank_c};
+            const std::vector<int64_t> *src_loc[3] = {&rank_c, &rank_c, &rank_n};
             std::vector<std::thread> th;
             for (int r = 0; r < 3; ++r)
                 th.emplace_back([&, r] {
-                    make_order(h[r].deg_in, identity, h[r].order, h[r].n_hub, h[r].ge);
-                    make_order(h[r].deg_out, identity, h[r].orderT, h[r].n_hubT, h[r].geT);
+                    make_order(h[r].deg_in, identity, *dst_loc[r], wdeg, h[r].order, h[r].n_hub,
+                               h[r].n_warp);
+                    make_order(h[r].deg_out, identity, *src_loc[r], wdeg, h[r].orderT,
+                               h[r].n_hubT, h[r].n_warpT);
                 });
             for (auto &t : th) t.join();
         }
@@ -287,10 +322,9 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
         for (int32_t j = 0; j < n_cell; ++j)
             degc[j] = h[DR_NEAR].deg_out[j] + h[DR_PINS].deg_out[j];
         for (int32_t j = 0; j < n_net; ++j) degn[j] = h[DR_PINNED].deg_out[j];
-        int32_t hub_c = 0, hub_n = 0;
-        std::vector<int32_t> ge_c, ge_n;
-        make_order(degc, identity, ord_c, hub_c, ge_c);
-        make_order(degn, identity, ord_n, hub_n, ge_n);
+        int32_t hub_c = 0, hub_n = 0, warp_c = 0, warp_n = 0;
+        make_order(degc, identity, rank_c, wdeg, ord_c, hub_c, warp_c);
+        make_order(degn, identity, rank_n, wdeg, ord_n, hub_n, warp_n);
 
         // ---- phase 2: one device block, carved per array
         g = new dr_graph();
@@ -323,10 +357,10 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
             d.module = hr.module;
             d.fwd.n = hr.n_dst;
             d.fwd.n_hub = hr.n_hub;
-            d.fwd.ge = hr.ge;
+            d.fwd.n_warp = hr.n_warp;
             d.bwd.n = hr.n_src;
             d.bwd.n_hub = hr.n_hubT;
-            d.bwd.ge = hr.geT;
+            d.bwd.n_warp = hr.n_warpT;
             d.max_deg_dst = hr.max_in;
             d.max_deg_src = hr.max_out;
             plan(r, (void **)&d.rowptr, hr.rowptr.data(), hr.rowptr.size() * 4);
@@ -345,10 +379,10 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
         }
         g->src_cell.n = n_cell;
         g->src_cell.n_hub = hub_c;
-        g->src_cell.ge = ge_c;
+        g->src_cell.n_warp = warp_c;
         g->src_net.n = n_net;
         g->src_net.n_hub = hub_n;
-        g->src_net.ge = ge_n;
+        g->src_net.n_warp = warp_n;
         plan(3, (void **)&g->src_cell.order, ord_c.data(), ord_c.size() * 4);
         plan(3, (void **)&g->src_net.order, ord_n.data(), ord_n.size() * 4);
         char *base = (char *)g->alloc.get(total, cs);

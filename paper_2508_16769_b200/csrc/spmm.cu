@@ -432,14 +432,6 @@ int choose_P(int k, int D) {
 
 void ensure_smem(const void *fn, size_t bytes);
 
-int warp_row_threshold(int R, int D) {
-    const char *e = getenv("DR_WARP_ROW_DEG");     // experiments only
-    const int env = e ? atoi(e) : -1;
-    (void)D;
-    (void)R;
-    return env >= 0 ? env : 32;   // measured best on C2 (k=8) and C4 (k=16): profiles/r01/ab_*.txt
-}
-
 void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
                      float *z, cudaStream_t s) {
     if (r.n_dst <= 0) return;
@@ -450,7 +442,7 @@ void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, in
     a.L = k / P;
     const int R = 32 / a.L;
     a.n_hub = r.fwd.n_hub;
-    a.n_warp = r.fwd.rows_above(warp_row_threshold(R, dim));
+    a.n_warp = r.fwd.n_warp;
     a.n_rows = r.n_dst;
     a.rowptr = r.rowptr;
     a.col = r.col;
@@ -495,7 +487,7 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, c
     a.L = k / P;
     const int R = 32 / a.L;
     a.n_hub = sched.n_hub;
-    a.n_warp = sched.rows_above(warp_row_threshold(R, dim));
+    a.n_warp = sched.n_warp;
     a.n_rows = n_src;
     BwdTerm terms[2] = {t0, t1};
     a.n_terms = 0;
