@@ -10,7 +10,7 @@
 #include <unordered_map>
 
 #include "proj.h"
-#include "tc_gemm.h"
+#include "tc2.h"
 
 namespace dr {
 
@@ -173,17 +173,17 @@ static TapeLayout tape_layout(const dr_graph *g, const dr_layer *L, uint32_t fla
     t.root_c = put(nc * kc * 4);
     t.root_n = put(nn * kn * 4);
     auto mx = [](size_t a, size_t b) { return a > b ? a : b; };
-    const int gc = 1, gn = 1;
-    t.work[0] = put(mx(dw_part_floats(nc, (int)dc, (int)D), tc_reduce_work_floats(nc, gc, (int)D)) * 4);
-    t.work[1] = put(mx(mx(dw_part_floats(nn, (int)dc, (int)D), dw_part_floats(nn, (int)dn, (int)D)),
-                       tc_reduce_work_floats(nn, gn, (int)D)) * 4);
-    t.work[2] = put(mx(dw_part_floats(nc, (int)dn, (int)D), tc_reduce_work_floats(nc, 1, (int)D)) * 4);
-    t.img_fa = put(2 * tc_bimg_bytes((int)dc, (int)D));
-    t.img_fb = put(tc_bimg_bytes((int)dn, (int)D));
-    t.img_fn = put(tc_bimg_bytes((int)dc, (int)D) + tc_bimg_bytes((int)dn, (int)D));
-    t.img_dz[DR_NEAR] = put(tc_bimg_bytes((int)D, (int)dc));
-    t.img_dz[DR_PINS] = put(tc_bimg_bytes((int)D, (int)dc));
-    t.img_dz[DR_PINNED] = put(tc_bimg_bytes((int)D, (int)dn));
+    const size_t red = tc2_reduce_work_floats(2, (int)D);
+    t.work[0] = put(mx(dw_part_floats(nc, (int)dc, (int)D), red) * 4);
+    t.work[1] = put(mx(mx(dw_part_floats(nn, (int)dc, (int)D), dw_part_floats(nn, (int)dn, (int)D)), red) * 4);
+    t.work[2] = put(mx(dw_part_floats(nc, (int)dn, (int)D), red) * 4);
+    // packed B operands of the tensor-core GEMMs (tc2.h)
+    t.img_fa = put(tc2_bimg_bytes((int)dc, (int)D) * 2);
+    t.img_fb = put(tc2_bimg_bytes((int)dn, (int)D));
+    t.img_fn = put(tc2_bimg_bytes((int)dc, (int)D) + tc2_bimg_bytes((int)dn, (int)D));
+    t.img_dz[DR_NEAR] = put(tc2_bimg_bytes((int)D, (int)(2 * dc)));
+    t.img_dz[DR_PINS] = put(tc2_bimg_bytes((int)D, (int)(dc + dn)));
+    t.img_dz[DR_PINNED] = put(tc2_bimg_bytes((int)D, (int)dn));
     t.total = off;
     return t;
 }
@@ -229,24 +229,23 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
     { TagScope t("pinned"); launch_spmm_fwd(g->rel[DR_PINNED], hnv, hni, L->k_net, L->d_net, z[DR_PINNED], s2); }
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[2], s2));                               // Z_pinned ready
     if (!seq) DR_CUDA(cudaStreamWaitEvent(s1, C.ev[1], 0));
-    const bool tc = tc_supported(L->d_out);
     {   // net: Y_net = Z_pins Wn_pins + densify(H_n) Wr_pins + b_pins   (Eq. 7, 9)
         TagScope t("net");
-        if (tc) {
-            uint8_t *img = (uint8_t *)(tp + T.img_fn);
-            launch_pack_b(L->wn[DR_PINS], L->d_out, L->d_cell, L->d_out, true, img, s1);
+        Tc2RowsDesc d;
+        uint8_t *img = (uint8_t *)(tp + T.img_fn);
+        d.n = nn; d.N = L->d_out; d.G = 1; d.epi = kEpi2Fwd;
+        d.nseg[0] = L->wr[DR_PINS] ? 2 : 1;
+        d.seg[0][0].A = z[DR_PINS]; d.seg[0][0].K = L->d_cell;
+        d.seg[0][1].hval = hnv; d.seg[0][1].hidx = hni; d.seg[0][1].k = L->k_net;
+        d.seg[0][1].K = L->d_net;
+        d.bimg[0] = img; d.bias[0] = L->b[DR_PINS];
+        d.y = yn;
+        if (tc2_rows_supported(d)) {
+            launch_tc2_pack_b(L->wn[DR_PINS], L->d_out, L->d_cell, L->d_out, 0, L->d_out, true, img, s1);
             if (L->wr[DR_PINS])
-                launch_pack_b(L->wr[DR_PINS], L->d_out, L->d_net, L->d_out, true,
-                              img + tc_bimg_bytes(L->d_cell, L->d_out), s1);
-            TcRowsDesc d;
-            d.n = nn; d.N = L->d_out; d.G = 1; d.epi = kEpiFwd;
-            d.nseg[0] = L->wr[DR_PINS] ? 2 : 1;
-            d.seg[0][0].A = z[DR_PINS]; d.seg[0][0].K = L->d_cell;
-            d.seg[0][1].hval = hnv; d.seg[0][1].hidx = hni; d.seg[0][1].k = L->k_net;
-            d.seg[0][1].K = L->d_net;
-            d.bimg[0] = img; d.bias[0] = L->b[DR_PINS];
-            d.y = yn;
-            launch_tc_rows(d, s1);
+                launch_tc2_pack_b(L->wr[DR_PINS], L->d_out, L->d_net, L->d_out, 0, L->d_out, true,
+                                  img + tc2_bimg_bytes(L->d_cell, L->d_out), s1);
+            launch_tc2_rows(d, s1);
         } else {
             ProjFwdArgs a;
             a.n = nn; a.Ka = L->d_cell; a.N = L->d_out;
@@ -261,27 +260,27 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
         TagScope t("cell");
         float *tap_a = (flags & DR_FWD_TAPS) ? (float *)(tp + T.tap_a) : nullptr;
         float *tap_b = (flags & DR_FWD_TAPS) ? (float *)(tp + T.tap_b) : nullptr;
-        if (tc) {
-            uint8_t *ia = (uint8_t *)(tp + T.img_fa), *ib = (uint8_t *)(tp + T.img_fb);
-            launch_pack_b(L->wn[DR_NEAR], L->d_out, L->d_cell, L->d_out, true, ia, s0);
+        uint8_t *ia = (uint8_t *)(tp + T.img_fa), *ib = (uint8_t *)(tp + T.img_fb);
+        Tc2RowsDesc d;
+        d.n = nc; d.N = L->d_out; d.G = 2; d.epi = kEpi2Fwd;
+        d.nseg[0] = L->wr[DR_NEAR] ? 2 : 1;
+        d.seg[0][0].A = z[DR_NEAR]; d.seg[0][0].K = L->d_cell;
+        d.seg[0][1].hval = hcv; d.seg[0][1].hidx = hci; d.seg[0][1].k = L->k_cell;
+        d.seg[0][1].K = L->d_cell;
+        d.nseg[1] = 1;
+        d.seg[1][0].A = z[DR_PINNED]; d.seg[1][0].K = L->d_net;
+        d.bimg[0] = ia; d.bimg[1] = ib;
+        d.bias[0] = L->b[DR_NEAR]; d.bias[1] = L->b[DR_PINNED];
+        d.merge = L->merge;
+        d.y = yc; d.mask_out = (uint32_t *)(tp + T.mask);
+        d.tap_a = tap_a; d.tap_b = tap_b;
+        if (tc2_rows_supported(d)) {
+            launch_tc2_pack_b(L->wn[DR_NEAR], L->d_out, L->d_cell, L->d_out, 0, L->d_out, true, ia, s0);
             if (L->wr[DR_NEAR])
-                launch_pack_b(L->wr[DR_NEAR], L->d_out, L->d_cell, L->d_out, true,
-                              ia + tc_bimg_bytes(L->d_cell, L->d_out), s0);
-            launch_pack_b(L->wn[DR_PINNED], L->d_out, L->d_net, L->d_out, true, ib, s0);
-            TcRowsDesc d;
-            d.n = nc; d.N = L->d_out; d.G = 2; d.epi = kEpiFwd;
-            d.nseg[0] = L->wr[DR_NEAR] ? 2 : 1;
-            d.seg[0][0].A = z[DR_NEAR]; d.seg[0][0].K = L->d_cell;
-            d.seg[0][1].hval = hcv; d.seg[0][1].hidx = hci; d.seg[0][1].k = L->k_cell;
-            d.seg[0][1].K = L->d_cell;
-            d.nseg[1] = 1;
-            d.seg[1][0].A = z[DR_PINNED]; d.seg[1][0].K = L->d_net;
-            d.bimg[0] = ia; d.bimg[1] = ib;
-            d.bias[0] = L->b[DR_NEAR]; d.bias[1] = L->b[DR_PINNED];
-            d.merge = L->merge;
-            d.y = yc; d.mask_out = (uint32_t *)(tp + T.mask);
-            d.tap_a = tap_a; d.tap_b = tap_b;
-            launch_tc_rows(d, s0);
+                launch_tc2_pack_b(L->wr[DR_NEAR], L->d_out, L->d_cell, L->d_out, 0, L->d_out, true,
+                                  ia + tc2_bimg_bytes(L->d_cell, L->d_out), s0);
+            launch_tc2_pack_b(L->wn[DR_PINNED], L->d_out, L->d_net, L->d_out, 0, L->d_out, true, ib, s0);
+            launch_tc2_rows(d, s0);
         } else {
             ProjFwdArgs a;
             a.n = nc; a.Ka = L->d_cell; a.Kb = L->d_net; a.N = L->d_out;
@@ -337,49 +336,52 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
         launch_dw(a, gw, gb, wk, s);
     };
     if (dxc || dxn) {
-        auto dzk = [&](int64_t n, int K, const float *dy, int mode, const float *W,
+        // dZ'_psi = c_psi (dY_psi Wn_psi^T) (row-scaled by the destination normaliser),
+        // with the Sage root term (dY_psi Wr_psi^T) at the kept indices as extra columns
+        auto dzk = [&](int64_t n, int Kd, const float *dy, int mode, const float *W,
+                       const float *Wr, int Kr, const uint8_t *ridx, int rk, float *root,
                        const float *c, float *out, uint8_t *img, cudaStream_t s) {
-            if (tc_supported(K)) {       // dZ = c (mask(dY) W^T): B_op[n][kk] = W[n][kk]
-                launch_pack_b(W, D, D, K, false, img, s);
-                TcRowsDesc d;
-                d.n = n; d.N = K; d.G = 1; d.epi = kEpiDz;
-                d.nseg[0] = 1;
-                d.seg[0][0].A = dy; d.seg[0][0].K = D; d.seg[0][0].mask_mode = mode;
-                d.mask_in = mask; d.mask_in_width = D;
-                d.bimg[0] = img; d.crow = c; d.dz = out;
-                launch_tc_rows(d, s);
+            Tc2RowsDesc d;
+            d.n = n; d.N = Kd + (Wr ? Kr : 0); d.G = 1; d.epi = kEpi2Dz;
+            d.nseg[0] = 1;
+            d.seg[0][0].A = dy; d.seg[0][0].K = D; d.seg[0][0].mask_mode = mode;
+            d.mask_in = mask; d.mask_width = D;
+            d.bimg[0] = img; d.n_dz = Kd; d.crow = c; d.dz = out;
+            if (Wr) { d.root_idx = ridx; d.root_k = rk; d.root = root; }
+            if (tc2_rows_supported(d)) {       // B_op[n][kk] = W[n][kk]
+                launch_tc2_pack_b(W, D, D, Kd, 0, d.N, false, img, s);
+                if (Wr) launch_tc2_pack_b(Wr, D, D, Kr, Kd, d.N, false, img, s);
+                launch_tc2_rows(d, s);
                 return;
             }
             ProjBwdArgs a;
-            a.n = n; a.N = D; a.K = K; a.dy = dy; a.mask = mask; a.mask_mode = mode;
+            a.n = n; a.N = D; a.K = Kd; a.dy = dy; a.mask = mask; a.mask_mode = mode;
             a.W = W; a.c = c; a.dz = out;
             launch_proj_bwd_dz(a, s);
+            if (Wr) {
+                RootArgs r;
+                r.n = n; r.N = D; r.k = rk; r.dy = dy; r.mask = mask; r.mask_mode = mode;
+                r.Wr = Wr; r.hidx = ridx; r.out = root;
+                launch_root_dots(r, s);
+            }
         };
-        auto rootk = [&](int64_t n, int k, const float *dy, int mode, const float *Wr,
-                         const uint8_t *hi, float *out, cudaStream_t s) {
-            RootArgs a;
-            a.n = n; a.N = D; a.k = k; a.dy = dy; a.mask = mask; a.mask_mode = mode;
-            a.Wr = Wr; a.hidx = hi; a.out = out;
-            launch_root_dots(a, s);
-        };
-        // dZ'_psi = c_psi (dY_psi Wn_psi^T)  (row-scaled by the destination normaliser)
         {
             TagScope t("near");
-            dzk(nc, L->d_cell, dyc, mode_near, L->wn[DR_NEAR], g->rel[DR_NEAR].c, dz[DR_NEAR],
+            dzk(nc, L->d_cell, dyc, mode_near, L->wn[DR_NEAR], L->wr[DR_NEAR], L->d_cell, hci,
+                L->k_cell, root_c, g->rel[DR_NEAR].c, dz[DR_NEAR],
                 (uint8_t *)(tp + T.img_dz[DR_NEAR]), s0);
-            if (L->wr[DR_NEAR]) rootk(nc, L->k_cell, dyc, mode_near, L->wr[DR_NEAR], hci, root_c, s0);
         }
         {
             TagScope t("pins");
-            dzk(nn, L->d_cell, dyn, kMaskNone, L->wn[DR_PINS], g->rel[DR_PINS].c, dz[DR_PINS],
+            dzk(nn, L->d_cell, dyn, kMaskNone, L->wn[DR_PINS], L->wr[DR_PINS], L->d_net, hni,
+                L->k_net, root_n, g->rel[DR_PINS].c, dz[DR_PINS],
                 (uint8_t *)(tp + T.img_dz[DR_PINS]), s1);
-            if (L->wr[DR_PINS]) rootk(nn, L->k_net, dyn, kMaskNone, L->wr[DR_PINS], hni, root_n, s1);
         }
         if (!seq) DR_CUDA(cudaEventRecord(C.ev[0], s1));                           // dZ_pins, root_n
         {
             TagScope t("pinned");
-            dzk(nc, L->d_net, dyc, mode_pinned, L->wn[DR_PINNED], g->rel[DR_PINNED].c,
-                dz[DR_PINNED], (uint8_t *)(tp + T.img_dz[DR_PINNED]), s2);
+            dzk(nc, L->d_net, dyc, mode_pinned, L->wn[DR_PINNED], nullptr, 0, nullptr, 0, nullptr,
+                g->rel[DR_PINNED].c, dz[DR_PINNED], (uint8_t *)(tp + T.img_dz[DR_PINNED]), s2);
         }
         // SSpMM per source node type (Alg. 2 stage 2-3, ownership instead of atomics)
         if (dxc) {
@@ -397,36 +399,31 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
                             L->k_net, L->d_net, nullptr, dxn, false, s2);
         }
     }
-    // weight gradients: dW = Z^T dY_psi, dWr = H^T dY_psi, db = colsum(dY_psi)
-    // weight gradients on tensor cores when the shapes allow (tcgen05, 3xTF32)
+    // weight gradients: dW = Z^T dY_psi, dWr = H^T dY_psi, db = colsum(dY_psi), on the
+    // tensor cores when the shapes allow (tc2 reduce GEMM), else the SIMT kernels
     auto dwt = [&](int64_t n, const float *Za, int wa, float *ga, const float *hv,
                    const uint8_t *hi, int k, int wb, float *gb, const float *dy, int mode,
-                   float *db, float *wk, cudaStream_t s) {
-        TcReduceDesc d;
+                   float *db, float *wk, cudaStream_t s) -> bool {
+        Tc2ReduceDesc d;
         d.n = n; d.N = D; d.dy = dy; d.mask = mask; d.mask_mode = mode; d.db = db;
-        TcRedSegDesc sa, sb;
+        Tc2RedSeg sa, sb;
         sa.Z = Za; sa.w = wa; sa.grad = ga;
         sb.hval = hv; sb.hidx = hi; sb.k = k; sb.w = wb; sb.grad = gb;
-        d.G = 1;
-        if (!gb) {
-            d.nseg[0] = 1; d.seg[0][0] = sa;
-        } else if (wa + wb <= 128) {
-            d.nseg[0] = 2; d.seg[0][0] = sa; d.seg[0][1] = sb;
-        } else {                                   // two passes over dY (M = 128 each)
-            d.nseg[0] = 1; d.seg[0][0] = sa;
-            launch_tc_reduce(d, wk, s);
-            d.seg[0][0] = sb; d.db = nullptr;
+        d.G = 1; d.nseg[0] = 1; d.seg[0][0] = sa;
+        if (gb && wa + wb <= 128) {
+            d.nseg[0] = 2; d.seg[0][1] = sb;
+        } else if (gb) {                           // two groups of 128 feature rows
+            d.G = 2; d.nseg[1] = 1; d.seg[1][0] = sb;
         }
-        launch_tc_reduce(d, wk, s);
+        if (!tc2_reduce_supported(d)) return false;
+        launch_tc2_reduce(d, wk, s);
+        return true;
     };
-    const bool tcw = tc_supported(D) && L->d_cell <= 128 && L->d_net <= 128;
     {
         TagScope t("near");
-        if (tcw) {
-            dwt(nc, z[DR_NEAR], L->d_cell, G->wn[DR_NEAR], hcv, hci, L->k_cell, L->d_cell,
-                L->wr[DR_NEAR] ? G->wr[DR_NEAR] : nullptr, dyc, mode_near, G->b[DR_NEAR],
-                work[0], s0);
-        } else {
+        if (!dwt(nc, z[DR_NEAR], L->d_cell, G->wn[DR_NEAR], hcv, hci, L->k_cell, L->d_cell,
+                 L->wr[DR_NEAR] ? G->wr[DR_NEAR] : nullptr, dyc, mode_near, G->b[DR_NEAR],
+                 work[0], s0)) {
             dw(nc, L->d_cell, z[DR_NEAR], nullptr, nullptr, 0, dyc, mode_near, G->wn[DR_NEAR],
                G->b[DR_NEAR], work[0], s0);
             TagScope t2("root");
@@ -437,20 +434,16 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
     }
     {
         TagScope t("pinned");
-        if (tcw)
-            dwt(nc, z[DR_PINNED], L->d_net, G->wn[DR_PINNED], nullptr, nullptr, 0, 0, nullptr,
-                dyc, mode_pinned, G->b[DR_PINNED], work[2], s2);
-        else
+        if (!dwt(nc, z[DR_PINNED], L->d_net, G->wn[DR_PINNED], nullptr, nullptr, 0, 0, nullptr,
+                 dyc, mode_pinned, G->b[DR_PINNED], work[2], s2))
             dw(nc, L->d_net, z[DR_PINNED], nullptr, nullptr, 0, dyc, mode_pinned,
                G->wn[DR_PINNED], G->b[DR_PINNED], work[2], s2);
     }
     {
         TagScope t("pins");
-        if (tcw) {
-            dwt(nn, z[DR_PINS], L->d_cell, G->wn[DR_PINS], hnv, hni, L->k_net, L->d_net,
-                L->wr[DR_PINS] ? G->wr[DR_PINS] : nullptr, dyn, kMaskNone, G->b[DR_PINS],
-                work[1], s1);
-        } else {
+        if (!dwt(nn, z[DR_PINS], L->d_cell, G->wn[DR_PINS], hnv, hni, L->k_net, L->d_net,
+                 L->wr[DR_PINS] ? G->wr[DR_PINS] : nullptr, dyn, kMaskNone, G->b[DR_PINS],
+                 work[1], s1)) {
             dw(nn, L->d_cell, z[DR_PINS], nullptr, nullptr, 0, dyn, kMaskNone, G->wn[DR_PINS],
                G->b[DR_PINS], work[1], s1);
             TagScope t2("root");

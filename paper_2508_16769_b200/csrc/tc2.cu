@@ -1,0 +1,1044 @@
+// tc2.cu — warp-specialised tcgen05 GEMMs for the dense parts of a HeteroConv
+// layer (see tc2.h for the math and the precision argument).
+//
+// Row GEMM (one persistent CTA per SM, 10 warps):
+//   warp 0      producer : per (tile, K chunk) step, 1-D bulk copies (TMA engine) of
+//                          the 128 rows x 64 fp32 of the chunk (or the tile's CBSR
+//                          rows) and the merge-mask words into a stage; packed B
+//                          chunks into a ring (or once, when all fit: resident B);
+//   warps 2-5   converters: split the raw fp32 stage IN PLACE into the bf16 hi / lo
+//                          K-major SW128 operand tiles (masking, zero-padding,
+//                          densifying CBSR rows on the way);
+//   warp 1      MMA      : one thread issues 3 kind::f16 MMAs per K=16 step into a
+//                          double-buffered TMEM accumulator, commits to the stage /
+//                          B slot / accumulator barriers;
+//   warps 6-9   epilogue : TMEM -> registers (one row per thread), bias, max-merge
+//                          + mask bits (Eq. 8, 14), taps, or the dz row scale and the
+//                          root-term sampling, then global stores.
+// Reduce GEMM (dW = A^T mask(dY)): 6 warps, same producer / MMA roles; the four
+// converter warps transpose 64-row stages into [feature][row] and [col][row]
+// operands, accumulate db, and read the final TMEM accumulator out as per-CTA
+// partials that a second kernel sums in a fixed order (deterministic, no atomics).
+#include "dr_internal.h"
+#include "proj.h"
+#include "tc.cuh"
+#include "tc2.h"
+
+namespace dr {
+namespace {
+
+constexpr int kTile = 128;             // rows per tile = MMA M
+constexpr int kChunk = 64;             // bf16 K per chunk (one 128-B swizzle atom)
+constexpr uint32_t kStage = 32768;     // 128 x 64 fp32 raw == bf16 hi + lo tiles
+constexpr uint32_t kHalf = 16384;      // one bf16 128 x 64 tile
+constexpr int kMaskStage = 4096;       // 128 rows x up to 8 mask words
+constexpr int kRowsThreads = 320;
+constexpr int kRedThreads = 192;
+constexpr int kSmemBudget = 227 * 1024 - 1024 - 1024;   // opt-in max minus alignment/static (rows)
+constexpr int kSmemBudgetRed = 227 * 1024 - 1024 - 6144;   // reduce kernel: 5 KB static
+constexpr int kMaxSteps = 16;
+constexpr int kMaxSA = 4, kMaxSB = 16;
+
+__device__ __forceinline__ float4 lds4(const uint8_t *p) { return *reinterpret_cast<const float4 *>(p); }
+
+// ================================================================= B packing
+// chunk c of the image: hi = Ntot rows x 128 B, then lo; element (n, kk) of the
+// operand at sw128_off_h(n, kk - 64c).
+__global__ void tc2_pack_b_kernel(const float *__restrict__ W, int ldw, int K, int NB, int n0,
+                                  int Ntot, int transpose, uint8_t *__restrict__ img) {
+    const int chunks = (K + kChunk - 1) / kChunk;
+    const int64_t total = (int64_t)chunks * NB * (kChunk / 2);      // element pairs
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int kp = (int)(e % (kChunk / 2));
+        const int n = (int)((e / (kChunk / 2)) % NB);
+        const int c = (int)(e / ((int64_t)(kChunk / 2) * NB));
+        const int k0 = c * kChunk + 2 * kp;
+        float v[2];
+        for (int q = 0; q < 2; ++q) {
+            const int k = k0 + q;
+            v[q] = k < K ? (transpose ? W[(int64_t)k * ldw + n] : W[(int64_t)n * ldw + k]) : 0.f;
+        }
+        uint32_t hi, lo;
+        tc::split_bf16x2(v[0], v[1], hi, lo);
+        uint8_t *base = img + (size_t)c * 2 * Ntot * 128;
+        const uint32_t off = tc::sw128_off_h((uint32_t)(n0 + n), (uint32_t)(2 * kp));
+        *reinterpret_cast<uint32_t *>(base + off) = hi;
+        *reinterpret_cast<uint32_t *>(base + (size_t)Ntot * 128 + off) = lo;
+    }
+}
+
+// ================================================================= row GEMM
+struct R2Step {
+    int8_t g, s, c, bc, first;     // group, segment, chunk in segment, chunk in group image, first of group
+};
+struct R2Seg {
+    const float *A;
+    const float *hval;
+    const uint8_t *hidx;
+    int k, K, mask_mode;
+};
+struct R2Args {
+    int64_t n;
+    int N, G, S;
+    R2Step step[kMaxSteps];
+    R2Seg seg[2][2];
+    const uint8_t *bimg[2];
+    const uint32_t *mask_in;
+    int mw;
+    int SA, SB, b_resident;
+    uint32_t bchunk;               // bytes of one packed B chunk (hi + lo)
+    int epi;
+    const float *bias[2];
+    int merge;
+    float *y;
+    uint32_t *mask_out;
+    float *tap_a, *tap_b;
+    int n_dz;
+    const float *crow;
+    float *dz;
+    const uint8_t *root_idx;
+    int root_k;
+    float *root;
+};
+
+__host__ __device__ __forceinline__ uint32_t rup16(uint32_t x) { return (x + 15u) & ~15u; }
+
+// producer: one step's raw data into stage `st`, signalled on `full`
+__device__ __forceinline__ void rows_produce(const R2Args &a, const R2Step &sp, int64_t r0,
+                                             uint8_t *st, uint8_t *mk, uint64_t *full, int lane) {
+    const R2Seg &s = a.seg[sp.g][sp.s];
+    const int rows = (int)(a.n - r0 < kTile ? a.n - r0 : kTile);
+    if (s.A) {
+        const int Kc = min(kChunk, s.K - sp.c * kChunk);
+        const uint32_t row_bytes = (uint32_t)Kc * 4;
+        const uint32_t mbytes = s.mask_mode != kMask2None ? rup16((uint32_t)rows * a.mw * 4) : 0u;
+        if (lane == 0) tc::mbar_arrive_expect_tx(full, row_bytes * rows + mbytes);
+        __syncwarp();
+        const float *src = s.A + r0 * s.K + sp.c * kChunk;
+        for (int r = lane; r < rows; r += 32)
+            tc::bulk_g2s(st + r * 256, src + (int64_t)r * s.K, row_bytes, full);
+        if (mbytes && lane == 0) tc::bulk_g2s(mk, a.mask_in + r0 * a.mw, mbytes, full);
+    } else {
+        // CBSR rows of the tile: values at +0, indices at +kHalf (both contiguous);
+        // sizes rounded up to 16 B (the tape pads every buffer)
+        const uint32_t vb = rup16((uint32_t)rows * s.k * 4), ib = rup16((uint32_t)rows * s.k);
+        if (lane == 0) {
+            tc::mbar_arrive_expect_tx(full, vb + ib);
+            tc::bulk_g2s(st, s.hval + r0 * s.k, vb, full);
+            tc::bulk_g2s(st + kHalf, s.hidx + r0 * s.k, ib, full);
+        }
+    }
+}
+
+// converters (128 threads, ct = 0..127): raw stage -> hi (+0) / lo (+kHalf) in place
+__device__ __forceinline__ void rows_convert(const R2Args &a, const R2Step &sp, int64_t r0,
+                                             uint8_t *st, const uint8_t *mk, int ct) {
+    const R2Seg &s = a.seg[sp.g][sp.s];
+    const int lane = ct & 31, cw = ct >> 5;
+    if (s.A) {
+        const int Kc = min(kChunk, s.K - sp.c * kChunk);
+        const int q = lane & 15;                       // float4 column group of the chunk
+        float4 v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int r = cw * 32 + 2 * i + (lane >> 4);
+            v[i] = lds4(st + r * 256 + q * 16);
+        }
+        uint32_t mbits[16];
+        if (s.mask_mode != kMask2None) {
+            const int col = sp.c * kChunk + 4 * q;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int r = cw * 32 + 2 * i + (lane >> 4);
+                const uint32_t w = *reinterpret_cast<const uint32_t *>(mk + (r * a.mw + (col >> 5)) * 4);
+                uint32_t b = (w >> (col & 31)) & 0xfu;
+                if (s.mask_mode == kMask2NotM) b = ~b & 0xfu;
+                mbits[i] = b;
+            }
+        }
+        tc::named_bar(1, 128);                         // every raw read precedes any write
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int r = cw * 32 + 2 * i + (lane >> 4);
+            float4 x = v[i];
+            const bool ok = (r0 + r < a.n) && (4 * q < Kc);
+            if (!ok) x = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (s.mask_mode != kMask2None) {
+                const uint32_t b = mbits[i];
+                if (!(b & 1u)) x.x = 0.f;
+                if (!(b & 2u)) x.y = 0.f;
+                if (!(b & 4u)) x.z = 0.f;
+                if (!(b & 8u)) x.w = 0.f;
+            }
+            uint2 h, l;
+            tc::split_bf16x2(x.x, x.y, h.x, l.x);
+            tc::split_bf16x2(x.z, x.w, h.y, l.y);
+            const uint32_t off = tc::sw128_off_h((uint32_t)r, (uint32_t)(4 * q));
+            *reinterpret_cast<uint2 *>(st + off) = h;
+            *reinterpret_cast<uint2 *>(st + kHalf + off) = l;
+        }
+    } else {
+        // one row per thread: read its k pairs, then zero the row and scatter
+        const int r = ct, k = s.k;
+        const bool ok = r0 + r < a.n;
+        float vv[32];
+        uint32_t iw[8];
+        const float *vals = reinterpret_cast<const float *>(st) + r * k;
+        const uint8_t *idx = st + kHalf + r * k;
+#pragma unroll
+        for (int t = 0; t < 32; ++t)
+            if (t < k) vv[t] = vals[t];
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            if (4 * t < k) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    if (4 * t + b < k) w |= (uint32_t)idx[4 * t + b] << (8 * b);
+                iw[t] = w;
+            }
+        tc::named_bar(1, 128);
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            *reinterpret_cast<float4 *>(st + r * 128 + c * 16) = z;
+            *reinterpret_cast<float4 *>(st + kHalf + r * 128 + c * 16) = z;
+        }
+        if (ok) {
+            const int lo_c = sp.c * kChunk;
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+                if (t < k) {
+                    const int cc = (int)((iw[t >> 2] >> (8 * (t & 3))) & 0xffu) - lo_c;
+                    if (cc >= 0 && cc < kChunk) {
+                        uint32_t h, l;
+                        tc::split_bf16x2(vv[t], 0.f, h, l);
+                        const uint32_t off = tc::sw128_off_h((uint32_t)r, (uint32_t)cc);
+                        *reinterpret_cast<uint16_t *>(st + off) = (uint16_t)(h & 0xffffu);
+                        *reinterpret_cast<uint16_t *>(st + kHalf + off) = (uint16_t)(l & 0xffffu);
+                    }
+                }
+        }
+    }
+}
+
+__device__ __forceinline__ float pick16(const float *v, int i) {
+    float r = v[0];
+#pragma unroll
+    for (int q = 1; q < 16; ++q) r = (i == q) ? v[q] : r;
+    return r;
+}
+
+// epilogue warp (quarter qd): rows r0 + 32 qd + lane of accumulator columns at `acc`
+__device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int64_t r0, int qd,
+                                              int lane) {
+    const int N = a.N;
+    const int64_t row = r0 + qd * 32 + lane;
+    const bool ok = row < a.n;
+    const uint32_t lb = acc + ((uint32_t)(qd * 32) << 16);
+    if (a.epi == kEpi2Dz) {
+        const float cr = (ok && a.crow) ? __ldg(a.crow + row) : 1.f;
+        uint32_t iw[8];
+        const int rk = a.root_k;
+        if (a.root && ok) {
+            const uint8_t *ip = a.root_idx + row * rk;
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                if (4 * t < rk) {
+                    uint32_t w = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        if (4 * t + b < rk) w |= (uint32_t)__ldg(ip + 4 * t + b) << (8 * b);
+                    iw[t] = w;
+                }
+        }
+        int p = 0;                                     // next root index (ascending)
+        for (int j = 0; j < N; j += 16) {
+            float v[16];
+            tc::tmem_ld16(lb + (uint32_t)j, v);
+            if (!ok) continue;
+            if (j < a.n_dz) {
+                float4 *o = reinterpret_cast<float4 *>(a.dz + row * a.n_dz + j);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    o[q] = make_float4(cr * v[4 * q], cr * v[4 * q + 1], cr * v[4 * q + 2],
+                                       cr * v[4 * q + 3]);
+            } else if (a.root) {
+                const int j0 = j - a.n_dz;
+                while (p < rk) {
+                    const int id = (int)((iw[p >> 2] >> (8 * (p & 3))) & 0xffu);
+                    if (id >= j0 + 16) break;
+                    a.root[row * rk + p] = pick16(v, id - j0);
+                    ++p;
+                }
+            }
+        }
+        return;
+    }
+    const int mw = (N + 31) >> 5;
+    uint32_t word = 0;
+    for (int j = 0; j < N; j += 16) {
+        float ya[16], yb[16];
+        tc::tmem_ld16(lb + (uint32_t)j, ya);
+        if (a.G == 2) tc::tmem_ld16(lb + (uint32_t)(N + j), yb);
+        if (!ok) continue;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float4 b = __ldg(reinterpret_cast<const float4 *>(a.bias[0] + j) + q);
+            ya[4 * q] += b.x; ya[4 * q + 1] += b.y; ya[4 * q + 2] += b.z; ya[4 * q + 3] += b.w;
+        }
+        float y[16];
+        uint32_t bits = 0;
+        if (a.G == 2) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 b = __ldg(reinterpret_cast<const float4 *>(a.bias[1] + j) + q);
+                yb[4 * q] += b.x; yb[4 * q + 1] += b.y; yb[4 * q + 2] += b.z; yb[4 * q + 3] += b.w;
+            }
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                if (a.merge == DR_MERGE_MAX) {
+                    const bool m = ya[q] >= yb[q];          // Eq. 14: ties -> near
+                    y[q] = m ? ya[q] : yb[q];
+                    bits |= (uint32_t)m << q;
+                } else {
+                    y[q] = ya[q] + yb[q];
+                }
+            }
+            if (a.tap_a) {
+                float4 *o = reinterpret_cast<float4 *>(a.tap_a + row * N + j);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) o[q] = make_float4(ya[4 * q], ya[4 * q + 1], ya[4 * q + 2], ya[4 * q + 3]);
+            }
+            if (a.tap_b) {
+                float4 *o = reinterpret_cast<float4 *>(a.tap_b + row * N + j);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) o[q] = make_float4(yb[4 * q], yb[4 * q + 1], yb[4 * q + 2], yb[4 * q + 3]);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) y[q] = ya[q];
+        }
+        float4 *o = reinterpret_cast<float4 *>(a.y + row * N + j);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) __stcs(o + q, make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]));
+        if (a.G == 2 && a.mask_out) {
+            word |= bits << (j & 16);
+            if ((j & 16) || j + 16 >= N) {
+                a.mask_out[row * mw + (j >> 5)] = word;
+                word = 0;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_constant__ R2Args a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t full[kMaxSA], conv[kMaxSA], empty[kMaxSA];
+    __shared__ __align__(8) uint64_t bfull[kMaxSB], bempty[kMaxSB], accf[2], acce[2];
+    __shared__ uint32_t tmem_slot;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int SA = a.SA, SB = a.SB, S = a.S;
+    uint8_t *stages = sm;
+    uint8_t *bslots = sm + (size_t)SA * kStage;
+    uint8_t *masks = bslots + (size_t)SB * a.bchunk;
+    const uint32_t GN = (uint32_t)(a.G * a.N);
+    uint32_t ncols = 32;
+    while (ncols < 2 * GN) ncols <<= 1;
+    if (tid == 0) {
+        for (int i = 0; i < SA; ++i) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&conv[i], 4);
+            tc::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < SB; ++i) {
+            tc::mbar_init(&bfull[i], 1);
+            tc::mbar_init(&bempty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&accf[i], 1);
+            tc::mbar_init(&acce[i], 4);
+        }
+        tc::fence_mbar_init();
+    }
+    if (warp == 1) {
+        tc::tmem_alloc(&tmem_slot, ncols);
+        tc::tmem_relinquish();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_slot;
+    const int64_t n_tiles = (a.n + kTile - 1) / kTile;
+    const int64_t my_tiles = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    if (warp == 0) {
+        // ---------------- producer
+        if (a.b_resident) {
+            if (lane == 0)
+                for (int j = 0; j < S; ++j) {
+                    const R2Step sp = a.step[j];
+                    tc::mbar_arrive_expect_tx(&bfull[j], a.bchunk);
+                    tc::bulk_g2s(bslots + (size_t)j * a.bchunk, a.bimg[sp.g] + (size_t)sp.bc * a.bchunk,
+                                 a.bchunk, &bfull[j]);
+                }
+        }
+        uint32_t it = 0, bt = 0;
+        for (int64_t t = 0; t < my_tiles; ++t) {
+            const int64_t r0 = ((int64_t)blockIdx.x + t * gridDim.x) * kTile;
+            for (int j = 0; j < S; ++j, ++it) {
+                const int slot = (int)(it % SA);
+                const uint32_t u = it / SA;
+                if (u > 0) tc::mbar_wait(&empty[slot], (u - 1) & 1u);
+                const R2Step sp = a.step[j];
+                rows_produce(a, sp, r0, stages + (size_t)slot * kStage, masks + (size_t)slot * kMaskStage,
+                             &full[slot], lane);
+                if (!a.b_resident) {
+                    const int bs = (int)(bt % SB);
+                    const uint32_t bu = bt / SB;
+                    if (lane == 0) {
+                        if (bu > 0) tc::mbar_wait(&bempty[bs], (bu - 1) & 1u);
+                        tc::mbar_arrive_expect_tx(&bfull[bs], a.bchunk);
+                        tc::bulk_g2s(bslots + (size_t)bs * a.bchunk,
+                                     a.bimg[sp.g] + (size_t)sp.bc * a.bchunk, a.bchunk, &bfull[bs]);
+                    }
+                    ++bt;
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = tc::idesc_bf16(kTile, a.N);
+            uint32_t it = 0, bt = 0;
+            for (int64_t t = 0; t < my_tiles; ++t) {
+                const uint32_t ab = (uint32_t)(t & 1);
+                if (t >= 2) tc::mbar_wait(&acce[ab], (uint32_t)(((t >> 1) - 1) & 1));
+                tc::fence_after();
+                const uint32_t dbase = tmem + ab * GN;
+                for (int j = 0; j < S; ++j, ++it) {
+                    const int slot = (int)(it % SA);
+                    tc::mbar_wait(&conv[slot], (it / SA) & 1u);
+                    const R2Step sp = a.step[j];
+                    int bs;
+                    if (a.b_resident) {
+                        bs = j;
+                        tc::mbar_wait(&bfull[bs], 0u);
+                    } else {
+                        bs = (int)(bt % SB);
+                        tc::mbar_wait(&bfull[bs], (bt / SB) & 1u);
+                    }
+                    tc::fence_after();
+                    const R2Seg &sg = a.seg[sp.g][sp.s];
+                    const int Kc = min(kChunk, sg.K - sp.c * kChunk);
+                    const int nks = (Kc + 15) >> 4;
+                    const uint32_t sa = tc::smem_u32(stages + (size_t)slot * kStage);
+                    const uint32_t sb = tc::smem_u32(bslots + (size_t)bs * a.bchunk);
+                    const uint32_t blo = (uint32_t)a.N * 128u;
+                    const uint32_t d = dbase + (uint32_t)(sp.g * a.N);
+                    for (int ks = 0; ks < nks; ++ks) {
+                        const uint32_t ko = ks * 32;
+                        const uint64_t ah = tc::desc_sw128(sa + ko), al = tc::desc_sw128(sa + kHalf + ko);
+                        const uint64_t bh = tc::desc_sw128(sb + ko), bl = tc::desc_sw128(sb + blo + ko);
+                        tc::mma_bf16(d, ah, bh, idesc, (sp.first && ks == 0) ? 0u : 1u);
+                        tc::mma_bf16(d, ah, bl, idesc, 1u);
+                        tc::mma_bf16(d, al, bh, idesc, 1u);
+                    }
+                    tc::mma_commit(&empty[slot]);
+                    if (!a.b_resident) {
+                        tc::mma_commit(&bempty[bs]);
+                        ++bt;
+                    }
+                }
+                tc::mma_commit(&accf[ab]);
+            }
+        }
+        __syncwarp();
+    } else if (warp < 6) {
+        // ---------------- converters
+        const int ct = tid - 64;
+        uint32_t it = 0;
+        for (int64_t t = 0; t < my_tiles; ++t) {
+            const int64_t r0 = ((int64_t)blockIdx.x + t * gridDim.x) * kTile;
+            for (int j = 0; j < S; ++j, ++it) {
+                const int slot = (int)(it % SA);
+                tc::mbar_wait(&full[slot], (it / SA) & 1u);
+                rows_convert(a, a.step[j], r0, stages + (size_t)slot * kStage,
+                             masks + (size_t)slot * kMaskStage, ct);
+                tc::fence_async_smem();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&conv[slot]);
+            }
+        }
+    } else {
+        // ---------------- epilogue
+        const int qd = warp & 3;
+        for (int64_t t = 0; t < my_tiles; ++t) {
+            const int64_t r0 = ((int64_t)blockIdx.x + t * gridDim.x) * kTile;
+            const uint32_t ab = (uint32_t)(t & 1);
+            tc::mbar_wait(&accf[ab], (uint32_t)((t >> 1) & 1));
+            tc::fence_after();
+            rows_epilogue(a, tmem + ab * GN, r0, qd, lane);
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&acce[ab]);
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem, ncols);
+    }
+}
+
+// ================================================================= reduce GEMM
+// Stage (64 graph rows): per group g an A' operand [128 features][64 rows]
+// (hi + lo, 32 KB; the dense segment's raw rows land in it and are transposed
+// in place), B' = mask(dY)^T [N][64 rows] (hi + lo, 256 N bytes; dY rows land in
+// it), CBSR rows and mask words in small side areas.
+struct RdSeg {
+    const float *Z;
+    const float *hval;
+    const uint8_t *hidx;
+    int k, w, m0;
+};
+struct RdArgs {
+    int64_t n;
+    int N, G;
+    int nseg[2];
+    RdSeg seg[2][2];
+    const float *dy;
+    const uint32_t *mask;
+    int mw, mask_mode;
+    int SA;
+    uint32_t stage_bytes, off_b, off_cbsr, off_mask;   // within a stage
+    uint32_t cbsr_seg_bytes;                            // per CBSR segment: vals (64k*4) + idx (64k)
+    int64_t rows_per_cta;
+    float *part;                                        // [grid][G*128*N + N]
+};
+
+constexpr int kRRows = 64;     // graph rows per reduce step (= MMA K of 4 kind::f16 steps)
+
+__device__ __forceinline__ void red_produce(const RdArgs &a, int64_t rb, int64_t re, uint8_t *st,
+                                            uint64_t *full, int lane) {
+    const int rows = (int)(re - rb < kRRows ? re - rb : kRRows);
+    uint32_t bytes = 0;
+    int ci = 0;
+    for (int g = 0; g < a.G; ++g)
+        for (int q = 0; q < a.nseg[g]; ++q) {
+            const RdSeg &s = a.seg[g][q];
+            if (s.Z) bytes += (uint32_t)rows * s.w * 4;
+            else bytes += rup16((uint32_t)rows * s.k * 4) + rup16((uint32_t)rows * s.k);
+        }
+    bytes += (uint32_t)rows * a.N * 4;
+    const uint32_t mb = a.mask_mode != kMask2None ? rup16((uint32_t)rows * a.mw * 4) : 0u;
+    bytes += mb;
+    if (lane == 0) {
+        tc::mbar_arrive_expect_tx(full, bytes);
+        for (int g = 0; g < a.G; ++g)
+            for (int q = 0; q < a.nseg[g]; ++q) {
+                const RdSeg &s = a.seg[g][q];
+                if (s.Z) {
+                    tc::bulk_g2s(st + (size_t)g * kStage, s.Z + rb * s.w, (uint32_t)rows * s.w * 4, full);
+                } else {
+                    uint8_t *cb = st + a.off_cbsr + (size_t)ci * a.cbsr_seg_bytes;
+                    tc::bulk_g2s(cb, s.hval + rb * s.k, rup16((uint32_t)rows * s.k * 4), full);
+                    tc::bulk_g2s(cb + (size_t)kRRows * s.k * 4, s.hidx + rb * s.k,
+                                 rup16((uint32_t)rows * s.k), full);
+                    ++ci;
+                }
+            }
+        tc::bulk_g2s(st + a.off_b, a.dy + rb * a.N, (uint32_t)rows * a.N * 4, full);
+        if (mb) tc::bulk_g2s(st + a.off_mask, a.mask + rb * a.mw, mb, full);
+    }
+}
+
+// Transposing split, read phase: unit u = (m, j) is column m (< W) of graph rows
+// 8j..8j+7 of a [64][W] fp32 block (row stride W), masked by the merge mask
+// when asked; rows >= valid read as 0. Optionally accumulates the unit's sum.
+template <int MAXU>
+__device__ __forceinline__ void red_read(const float *raw, int W, int valid, int ct,
+                                         const uint8_t *mkraw, int mw, int mask_mode,
+                                         float (&v)[MAXU][8], float *colsum) {
+    const int units = W * 8;
+#pragma unroll
+    for (int i = 0; i < MAXU; ++i) {
+        const int u = ct + 128 * i;
+        if (u < units) {
+            const int m = u % W, j = u / W;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int rr = 8 * j + r;
+                float x = rr < valid ? raw[rr * W + m] : 0.f;
+                if (mask_mode != kMask2None) {
+                    const uint32_t w =
+                        *reinterpret_cast<const uint32_t *>(mkraw + (rr * mw + (m >> 5)) * 4);
+                    const bool bit = (w >> (m & 31)) & 1u;
+                    if (bit != (mask_mode == kMask2M)) x = 0.f;
+                }
+                v[i][r] = x;
+            }
+            if (colsum) {
+                float s = 0.f;
+#pragma unroll
+                for (int r = 0; r < 8; ++r) s += v[i][r];
+                colsum[i] += s;
+            }
+        }
+    }
+}
+// write phase: unit (m, j) -> operand row m0 + m, K positions 8j..8j+7 (hi at
+// +0, lo at +lo_off)
+template <int MAXU>
+__device__ __forceinline__ void red_write(uint8_t *tile, uint32_t lo_off, int W, int m0, int ct,
+                                          const float (&v)[MAXU][8]) {
+    const int units = W * 8;
+#pragma unroll
+    for (int i = 0; i < MAXU; ++i) {
+        const int u = ct + 128 * i;
+        if (u < units) {
+            const int m = u % W, j = u / W;
+            uint4 h, l;
+            tc::split_bf16x2(v[i][0], v[i][1], h.x, l.x);
+            tc::split_bf16x2(v[i][2], v[i][3], h.y, l.y);
+            tc::split_bf16x2(v[i][4], v[i][5], h.z, l.z);
+            tc::split_bf16x2(v[i][6], v[i][7], h.w, l.w);
+            const uint32_t off = tc::sw128_off_h((uint32_t)(m0 + m), (uint32_t)(8 * j));
+            *reinterpret_cast<uint4 *>(tile + off) = h;
+            *reinterpret_cast<uint4 *>(tile + lo_off + off) = l;
+        }
+    }
+}
+
+// converters: one stage -> A'_g (per group) and B' operands; db unit sums in colsum
+__device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int valid, int ct,
+                                            float (&colsum)[8]) {
+    const uint8_t *mk = st + a.off_mask;
+    int ci = 0;
+    for (int g = 0; g < a.G; ++g) {
+        uint8_t *tile = st + (size_t)g * kStage;
+        float v[8][8];
+        int wd = 0, wtot = 0;
+        const RdSeg *dseg = nullptr;
+        for (int q = 0; q < a.nseg[g]; ++q) {
+            wtot += a.seg[g][q].w;
+            if (a.seg[g][q].Z) { dseg = &a.seg[g][q]; wd = dseg->w; }
+        }
+        if (dseg) red_read<8>(reinterpret_cast<const float *>(tile), wd, valid, ct, mk, 0,
+                              kMask2None, v, nullptr);
+        // CBSR entries of this group: thread -> graph row ct/2, half ct&1 of its k pairs
+        float cv[16];
+        uint32_t cid[16];
+        int cm0 = 0, ck = 0;
+        bool has_cbsr = false;
+        for (int q = 0; q < a.nseg[g]; ++q) {
+            const RdSeg &s = a.seg[g][q];
+            if (s.Z) continue;
+            has_cbsr = true;
+            cm0 = s.m0;
+            ck = s.k;
+            const uint8_t *cb = st + a.off_cbsr + (size_t)ci * a.cbsr_seg_bytes;
+            const int r = ct >> 1, h = ct & 1;
+            const float *vals = reinterpret_cast<const float *>(cb) + r * s.k;
+            const uint8_t *ids = cb + (size_t)kRRows * s.k * 4 + r * s.k;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                const int tt = 2 * t + h;
+                const bool ok = tt < s.k && r < valid;
+                cv[t] = ok ? vals[tt] : 0.f;
+                cid[t] = ok ? (uint32_t)ids[tt] : 0xffffffffu;
+            }
+            ++ci;
+        }
+        tc::named_bar(1, 128);                      // raw reads done before writes
+        if (dseg) red_write<8>(tile, kHalf, wd, dseg->m0, ct, v);
+        {   // zero the CBSR rows and the unused rows [wtot, 128)
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < a.nseg[g]; ++q) {
+                const RdSeg &s = a.seg[g][q];
+                if (s.Z) continue;
+                for (int e = ct; e < s.w * 8; e += 128) {
+                    const int m = s.m0 + e / 8, c = e % 8;
+                    *reinterpret_cast<float4 *>(tile + m * 128 + c * 16) = z;
+                    *reinterpret_cast<float4 *>(tile + kHalf + m * 128 + c * 16) = z;
+                }
+            }
+            for (int e = wtot * 8 + ct; e < kTile * 8; e += 128) {
+                const int m = e / 8, c = e % 8;
+                *reinterpret_cast<float4 *>(tile + m * 128 + c * 16) = z;
+                *reinterpret_cast<float4 *>(tile + kHalf + m * 128 + c * 16) = z;
+            }
+        }
+        if (has_cbsr) {
+            tc::named_bar(1, 128);                  // zeros before the scatter
+            const int r = ct >> 1;
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+                if (2 * t + (ct & 1) < ck && cid[t] != 0xffffffffu) {
+                    uint32_t h, l;
+                    tc::split_bf16x2(cv[t], 0.f, h, l);
+                    const uint32_t off = tc::sw128_off_h((uint32_t)(cm0 + (int)cid[t]), (uint32_t)r);
+                    *reinterpret_cast<uint16_t *>(tile + off) = (uint16_t)(h & 0xffffu);
+                    *reinterpret_cast<uint16_t *>(tile + kHalf + off) = (uint16_t)(l & 0xffffu);
+                }
+        }
+    }
+    {   // B' = mask(dY)^T
+        uint8_t *tile = st + a.off_b;
+        float v[8][8];
+        red_read<8>(reinterpret_cast<const float *>(tile), a.N, valid, ct, mk, a.mw, a.mask_mode, v,
+                    colsum);
+        tc::named_bar(1, 128);
+        red_write<8>(tile, (uint32_t)a.N * 128u, a.N, 0, ct, v);
+    }
+}
+
+__global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid_constant__ RdArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t full[kMaxSA], conv[kMaxSA], empty[kMaxSA], accf;
+    __shared__ uint32_t tmem_slot;
+    __shared__ float dbs[8][128];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int SA = a.SA, G = a.G, N = a.N;
+    uint32_t ncols = 32;
+    while (ncols < (uint32_t)(G * N)) ncols <<= 1;
+    if (tid == 0) {
+        for (int i = 0; i < SA; ++i) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&conv[i], 4);
+            tc::mbar_init(&empty[i], 1);
+        }
+        tc::mbar_init(&accf, 1);
+        tc::fence_mbar_init();
+    }
+    if (warp == 1) {
+        tc::tmem_alloc(&tmem_slot, ncols);
+        tc::tmem_relinquish();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_slot;
+    const int64_t rbeg = (int64_t)blockIdx.x * a.rows_per_cta;
+    const int64_t rend = a.n < rbeg + a.rows_per_cta ? a.n : rbeg + a.rows_per_cta;
+    const int64_t total = rend > rbeg ? (rend - rbeg + kRRows - 1) / kRRows : 0;
+    float *out = a.part + (int64_t)blockIdx.x * ((int64_t)G * kTile * N + N);
+
+    if (warp == 0) {
+        for (int64_t it = 0; it < total; ++it) {
+            const int slot = (int)(it % SA);
+            const uint32_t u = (uint32_t)(it / SA);
+            if (u > 0) tc::mbar_wait(&empty[slot], (u - 1) & 1u);
+            red_produce(a, rbeg + it * kRRows, rend, sm + (size_t)slot * a.stage_bytes, &full[slot], lane);
+            __syncwarp();
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && total > 0) {
+            const uint32_t idesc = tc::idesc_bf16(kTile, N);
+            for (int64_t it = 0; it < total; ++it) {
+                const int slot = (int)(it % SA);
+                tc::mbar_wait(&conv[slot], (uint32_t)((it / SA) & 1));
+                tc::fence_after();
+                uint8_t *st = sm + (size_t)slot * a.stage_bytes;
+                const uint32_t sb = tc::smem_u32(st + a.off_b), blo = (uint32_t)N * 128u;
+                for (int g = 0; g < G; ++g) {
+                    const uint32_t sa = tc::smem_u32(st + (size_t)g * kStage);
+                    const uint32_t d = tmem + (uint32_t)(g * N);
+#pragma unroll
+                    for (int ks = 0; ks < kRRows / 16; ++ks) {
+                        const uint32_t ko = ks * 32;
+                        const uint64_t ah = tc::desc_sw128(sa + ko), al = tc::desc_sw128(sa + kHalf + ko);
+                        const uint64_t bh = tc::desc_sw128(sb + ko), bl = tc::desc_sw128(sb + blo + ko);
+                        tc::mma_bf16(d, ah, bh, idesc, (it == 0 && ks == 0) ? 0u : 1u);
+                        tc::mma_bf16(d, ah, bl, idesc, 1u);
+                        tc::mma_bf16(d, al, bh, idesc, 1u);
+                    }
+                }
+                tc::mma_commit(&empty[slot]);
+            }
+            tc::mma_commit(&accf);
+        }
+        __syncwarp();
+    } else {
+        const int ct = tid - 64;
+        float colsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int64_t it = 0; it < total; ++it) {
+            const int slot = (int)(it % SA);
+            tc::mbar_wait(&full[slot], (uint32_t)((it / SA) & 1));
+            const int64_t rb = rbeg + it * kRRows;
+            const int valid = (int)(rend - rb < kRRows ? rend - rb : kRRows);
+            red_convert(a, sm + (size_t)slot * a.stage_bytes, valid, ct, colsum);
+            tc::fence_async_smem();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&conv[slot]);
+        }
+        // db partials: unit (n, j) of thread ct, summed over j in a fixed order
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int u = ct + 128 * i;
+            if (u < N * 8) dbs[u / N][u % N] = colsum[i];
+        }
+        tc::named_bar(1, 128);
+        for (int c = ct; c < N; c += 128) {
+            float s = 0.f;
+            for (int j = 0; j < 8; ++j) s += dbs[j][c];
+            out[(int64_t)G * kTile * N + c] = s;
+        }
+        // accumulator -> per-CTA partial (lane = feature row)
+        const int qd = warp & 3;
+        if (total > 0) {
+            tc::mbar_wait(&accf, 0u);
+            tc::fence_after();
+        }
+        const int m = qd * 32 + lane;
+        const uint32_t lb = tmem + ((uint32_t)(qd * 32) << 16);
+        for (int g = 0; g < G; ++g)
+            for (int j = 0; j < N; j += 16) {
+                float v[16];
+                if (total > 0) tc::tmem_ld16(lb + (uint32_t)(g * N + j), v);
+                else
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) v[q] = 0.f;
+                float4 *o = reinterpret_cast<float4 *>(out + ((int64_t)g * kTile + m) * N + j);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem, ncols);
+    }
+}
+
+// Sum per-CTA partials in a fixed order and scatter to the segment outputs.
+struct RdOut {
+    int nout;
+    int g[4], m0[4], w[4];
+    float *dst[4];
+    float *db;
+};
+__global__ void tc2_reduce_parts_kernel(const float *__restrict__ part, int nparts, int G, int N,
+                                        RdOut o) {
+    __shared__ float red[8][33];
+    const int64_t len = (int64_t)G * kTile * N + N;
+    const int64_t e = (int64_t)blockIdx.x * 32 + threadIdx.x;
+    float acc = 0.f;
+    if (e < len)
+        for (int c = threadIdx.y; c < nparts; c += 8) acc += __ldg(part + (int64_t)c * len + e);
+    red[threadIdx.y][threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.y != 0 || e >= len) return;
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += red[q][threadIdx.x];
+    if (e >= (int64_t)G * kTile * N) {
+        if (o.db) o.db[e - (int64_t)G * kTile * N] = s;
+        return;
+    }
+    const int g = (int)(e / ((int64_t)kTile * N));
+    const int m = (int)((e / N) % kTile), c = (int)(e % N);
+    for (int i = 0; i < o.nout; ++i)
+        if (o.g[i] == g && m >= o.m0[i] && m < o.m0[i] + o.w[i])
+            o.dst[i][(int64_t)(m - o.m0[i]) * N + c] = s;
+}
+
+}  // namespace
+
+// ================================================================= host side
+size_t tc2_bimg_bytes(int K, int Ntot) {
+    return (size_t)((K + kChunk - 1) / kChunk) * 2 * (size_t)Ntot * 128;
+}
+
+void launch_tc2_pack_b(const float *W, int ldw, int K, int NB, int n0, int Ntot, bool transpose,
+                       uint8_t *img, cudaStream_t s) {
+    const int64_t total = (int64_t)((K + kChunk - 1) / kChunk) * NB * (kChunk / 2);
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 592) blocks = 592;
+    if (blocks < 1) blocks = 1;
+    tc2_pack_b_kernel<<<(unsigned)blocks, 256, 0, s>>>(W, ldw, K, NB, n0, Ntot, transpose ? 1 : 0, img);
+    note_launch("tc2_pack_b");
+}
+
+static bool seg_ok(const Tc2Seg &s) {
+    if (s.K < 4 || s.K > 256 || s.K % 4) return false;
+    if (!s.A && (s.k < 1 || s.k > 32 || s.k > s.K)) return false;
+    return true;
+}
+
+bool tc2_rows_supported(const Tc2RowsDesc &d) {
+    const char *e = getenv("DR_DENSE_SIMT");      // A/B switch for tests and profiling
+    if (e && atoi(e)) return false;
+    if (d.N < 16 || d.N > 256 || d.N % 16) return false;
+    if (d.G < 1 || d.G > 2 || 2 * d.G * d.N > 512) return false;
+    int steps = 0;
+    for (int g = 0; g < d.G; ++g) {
+        if (d.nseg[g] < 1 || d.nseg[g] > 2) return false;
+        for (int q = 0; q < d.nseg[g]; ++q) {
+            if (!seg_ok(d.seg[g][q])) return false;
+            if (d.seg[g][q].mask_mode != kMask2None && (d.mask_width + 31) / 32 > 8) return false;
+            steps += (d.seg[g][q].K + kChunk - 1) / kChunk;
+        }
+    }
+    if (steps > kMaxSteps) return false;
+    if (d.epi == kEpi2Dz && d.root && (d.root_k < 1 || d.root_k > 32 || (d.N - d.n_dz) % 16)) return false;
+    if (d.epi == kEpi2Dz && d.n_dz % 16) return false;
+    const size_t bchunk = (size_t)256 * d.N;
+    return 2 * kStage + 2 * kMaskStage + 2 * bchunk <= (size_t)kSmemBudget;
+}
+
+void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
+    if (d.n <= 0) return;
+    DR_CHECK(tc2_rows_supported(d), DR_ERR_UNSUPPORTED, "tc2_rows: unsupported shape");
+    R2Args a{};
+    a.n = d.n;
+    a.N = d.N;
+    a.G = d.G;
+    a.S = 0;
+    for (int g = 0; g < d.G; ++g) {
+        a.bimg[g] = d.bimg[g];
+        a.bias[g] = d.bias[g];
+        int bc = 0;
+        for (int q = 0; q < d.nseg[g]; ++q) {
+            const Tc2Seg &sd = d.seg[g][q];
+            a.seg[g][q] = R2Seg{sd.A, sd.hval, sd.hidx, sd.k, sd.K, sd.A ? sd.mask_mode : kMask2None};
+            const int chunks = (sd.K + kChunk - 1) / kChunk;
+            for (int c = 0; c < chunks; ++c)
+                a.step[a.S++] = R2Step{(int8_t)g, (int8_t)q, (int8_t)c, (int8_t)bc++,
+                                       (int8_t)(q == 0 && c == 0)};
+        }
+    }
+    a.mask_in = d.mask_in;
+    a.mw = (d.mask_width + 31) / 32;
+    a.bchunk = (uint32_t)(256 * d.N);
+    a.epi = d.epi;
+    a.merge = d.merge;
+    a.y = d.y;
+    a.mask_out = d.mask_out;
+    a.tap_a = d.tap_a;
+    a.tap_b = d.tap_b;
+    a.n_dz = d.n_dz;
+    a.crow = d.crow;
+    a.dz = d.dz;
+    a.root_idx = d.root_idx;
+    a.root_k = d.root_k;
+    a.root = d.root;
+    // stages: B resident when every chunk fits beside >= 2 A stages, else a ring
+    const size_t st_bytes = kStage + kMaskStage;
+    const size_t budget = kSmemBudget;
+    if ((size_t)a.S * a.bchunk + 2 * st_bytes <= budget && a.S <= kMaxSB) {
+        a.b_resident = 1;
+        a.SB = a.S;
+        a.SA = (int)std::min<size_t>(kMaxSA, (budget - (size_t)a.S * a.bchunk) / st_bytes);
+    } else {
+        a.b_resident = 0;
+        a.SA = 3;
+        if (3 * st_bytes + 2 * (size_t)a.bchunk > budget) a.SA = 2;
+        a.SB = (int)std::min<size_t>(4, (budget - a.SA * st_bytes) / a.bchunk);
+    }
+    const size_t smem = (size_t)a.SA * st_bytes + (size_t)a.SB * a.bchunk + 1024;
+    const int64_t tiles = (d.n + kTile - 1) / kTile;
+    const int64_t grid = tiles < 148 ? tiles : 148;
+    ProfScope ps(d.epi == kEpi2Dz ? "tc_dz" : "tc_proj", s);
+    ensure_smem((const void *)tc2_rows_kernel, smem);
+    tc2_rows_kernel<<<(unsigned)grid, kRowsThreads, smem, s>>>(a);
+    note_launch("tc2_rows");
+}
+
+bool tc2_reduce_supported(const Tc2ReduceDesc &d) {
+    const char *e = getenv("DR_DENSE_SIMT");
+    if (e && atoi(e)) return false;
+    if (d.N < 16 || d.N > 128 || d.N % 16) return false;
+    if (d.G < 1 || d.G > 2) return false;
+    for (int g = 0; g < d.G; ++g) {
+        if (d.nseg[g] < 1 || d.nseg[g] > 2) return false;
+        int w = 0, dense = 0, cb = 0;
+        for (int q = 0; q < d.nseg[g]; ++q) {
+            const Tc2RedSeg &s = d.seg[g][q];
+            if (s.w < 4 || s.w % 4) return false;
+            w += s.w;
+            if (s.Z) ++dense;
+            else {
+                ++cb;
+                if (s.k < 1 || s.k > 32 || s.k > s.w) return false;
+            }
+        }
+        if (w > 128 || dense > 1 || cb > 1) return false;
+    }
+    if (d.mask_mode != kMask2None && (d.N + 31) / 32 > 8) return false;
+    return true;
+}
+
+size_t tc2_reduce_work_floats(int G, int N) {
+    return (size_t)148 * ((size_t)G * kTile * N + N);
+}
+
+void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s) {
+    DR_CHECK(tc2_reduce_supported(d), DR_ERR_UNSUPPORTED, "tc2_reduce: unsupported shape");
+    RdArgs a{};
+    a.n = d.n;
+    a.N = d.N;
+    a.G = d.G;
+    RdOut o{};
+    int ncb = 0, maxk = 0;
+    for (int g = 0; g < d.G; ++g) {
+        a.nseg[g] = d.nseg[g];
+        int m0 = 0;
+        for (int q = 0; q < d.nseg[g]; ++q) {
+            const Tc2RedSeg &sd = d.seg[g][q];
+            a.seg[g][q] = RdSeg{sd.Z, sd.hval, sd.hidx, sd.k, sd.w, m0};
+            if (!sd.Z) {
+                ++ncb;
+                maxk = std::max(maxk, sd.k);
+            }
+            o.g[o.nout] = g;
+            o.m0[o.nout] = m0;
+            o.w[o.nout] = sd.w;
+            o.dst[o.nout] = sd.grad;
+            ++o.nout;
+            m0 += sd.w;
+        }
+    }
+    o.db = d.db;
+    a.dy = d.dy;
+    a.mask = d.mask;
+    a.mask_mode = d.mask_mode;
+    a.mw = (d.N + 31) / 32;
+    auto r1k = [](uint32_t x) { return (x + 1023u) & ~1023u; };
+    uint32_t off = (uint32_t)d.G * kStage;
+    a.off_b = off;
+    off += r1k((uint32_t)256 * d.N);
+    a.off_cbsr = off;
+    a.cbsr_seg_bytes = (uint32_t)(kRRows * maxk * 4 + rup16((uint32_t)kRRows * maxk) + 16);
+    a.cbsr_seg_bytes = (a.cbsr_seg_bytes + 127u) & ~127u;
+    off += r1k(a.cbsr_seg_bytes * (uint32_t)ncb);
+    a.off_mask = off;
+    off += r1k(kRRows * 8 * 4 + 16);
+    a.stage_bytes = off;
+    a.SA = (int)std::min<size_t>(kMaxSA, (size_t)kSmemBudgetRed / a.stage_bytes);
+    DR_CHECK(a.SA >= 2, DR_ERR_UNSUPPORTED, "tc2_reduce: shared memory budget");
+    const size_t smem = (size_t)a.SA * a.stage_bytes + 1024;
+    int64_t grid = (d.n + 4 * kRRows - 1) / (4 * kRRows);
+    if (grid > 148) grid = 148;
+    if (grid < 1) grid = 1;
+    a.rows_per_cta = ((d.n + grid - 1) / grid + kRRows - 1) / kRRows * kRRows;
+    a.part = work;
+    ProfScope ps("tc_dw", s);
+    ensure_smem((const void *)tc2_reduce_kernel, smem);
+    tc2_reduce_kernel<<<(unsigned)grid, kRedThreads, smem, s>>>(a);
+    note_launch("tc2_reduce");
+    const int64_t stride = (int64_t)d.G * kTile * d.N + d.N;
+    tc2_reduce_parts_kernel<<<(unsigned)((stride + 31) / 32), dim3(32, 8), 0, s>>>(work, (int)grid,
+                                                                                   d.G, d.N, o);
+    note_launch("tc2_reduce_parts");
+}
+
+}  // namespace dr

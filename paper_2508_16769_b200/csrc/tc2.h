@@ -1,0 +1,87 @@
+// tc2.h — host interface of the warp-specialised tcgen05 GEMMs (internal).
+//
+// Every dense contraction of a HeteroConv layer is one of two shapes:
+//   row GEMM  : Y[n x N] = sum_g-segments A_seg[n x K_seg] B_seg[K_seg x N]   (+ epilogue)
+//               the forward projections (Eq. 4 W^psi) with the max-merge
+//               epilogue (Eq. 8 / Eq. 14), and the backward dZ' = c (mask(dY) Wn^T)
+//               (Eq. 10-13) with the Sage root term (mask(dY) Wr^T) sampled at the
+//               CBSR indices fused as extra output columns;
+//   reduce GEMM: dW[K_seg x N] = A_seg^T mask(dY) over all n rows, db = colsum(mask(dY)).
+// Precision (north_star 1e-4): each fp32 operand is split x = hi + lo with hi, lo
+// bf16 (hi = rn(x), lo = rn(x - hi); |x - hi - lo| <= 2^-17 |x|), and every
+// product is hi*hi + hi*lo + lo*hi: 3 kind::f16 MMAs, fp32 accumulation in TMEM.
+#pragma once
+#include "dr_internal.h"
+
+namespace dr {
+
+enum { kMask2None = 0, kMask2M = 1, kMask2NotM = 2 };   // = kMaskNone/kMaskM/kMaskNotM
+enum { kEpi2Fwd = 0, kEpi2Dz = 1 };
+
+struct Tc2Seg {
+    const float *A = nullptr;          // dense n x K row-major, or nullptr => CBSR
+    const float *hval = nullptr;       // CBSR n x k (values), idx n x k (uint8)
+    const uint8_t *hidx = nullptr;
+    int k = 0;
+    int K = 0;                         // width of the segment (dense K, or CBSR dim)
+    int mask_mode = kMask2None;        // dense only: route dY_cell by the merge mask
+};
+
+struct Tc2RowsDesc {
+    int64_t n = 0;
+    int N = 0;                         // output columns of one accumulator group
+    int G = 1;                         // accumulator groups (2: near | pinned for the merge)
+    int nseg[2] = {0, 0};
+    Tc2Seg seg[2][2];
+    const uint8_t *bimg[2] = {nullptr, nullptr};   // packed B per group (tc2_bimg_bytes)
+    const uint32_t *mask_in = nullptr;             // n x ceil(mask_width/32) merge-mask words
+    int mask_width = 0;
+    int epi = kEpi2Fwd;
+    // forward epilogue
+    const float *bias[2] = {nullptr, nullptr};
+    int merge = DR_MERGE_MAX;
+    float *y = nullptr;
+    uint32_t *mask_out = nullptr;
+    float *tap_a = nullptr, *tap_b = nullptr;
+    // dz epilogue: columns [0, n_dz) -> dz (n x n_dz) scaled by crow; columns
+    // [n_dz, N) -> the root row, sampled at root_idx (n x root_k) -> root (n x root_k)
+    int n_dz = 0;
+    const float *crow = nullptr;
+    float *dz = nullptr;
+    const uint8_t *root_idx = nullptr;
+    int root_k = 0;
+    float *root = nullptr;
+};
+
+// Packed B image: per 64-wide K chunk, hi then lo, each Ntot rows x 128 B
+// (bf16, K-major, 128-B swizzle).
+size_t tc2_bimg_bytes(int K, int Ntot);
+// rows [n0, n0 + NB) of the image of a K x Ntot operand:
+// B_op[n0 + n][kk] = transpose ? W[kk*ldw + n] : W[n*ldw + kk].
+void launch_tc2_pack_b(const float *W, int ldw, int K, int NB, int n0, int Ntot, bool transpose,
+                       uint8_t *img, cudaStream_t s);
+bool tc2_rows_supported(const Tc2RowsDesc &d);
+void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s);
+
+struct Tc2RedSeg {
+    const float *Z = nullptr;          // dense n x w, or nullptr => CBSR (hval/hidx/k, width w)
+    const float *hval = nullptr;
+    const uint8_t *hidx = nullptr;
+    int k = 0, w = 0;
+    float *grad = nullptr;             // w x N row-major
+};
+struct Tc2ReduceDesc {
+    int64_t n = 0;
+    int N = 0, G = 1;                  // G accumulator groups of 128 feature rows
+    int nseg[2] = {0, 0};              // segments stacked inside a group (widths sum <= 128)
+    Tc2RedSeg seg[2][2];
+    const float *dy = nullptr;
+    const uint32_t *mask = nullptr;
+    int mask_mode = kMask2None;
+    float *db = nullptr;
+};
+bool tc2_reduce_supported(const Tc2ReduceDesc &d);
+size_t tc2_reduce_work_floats(int G, int N);
+void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s);
+
+}  // namespace dr
