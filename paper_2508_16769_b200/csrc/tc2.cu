@@ -19,6 +19,12 @@
 // converter warps transpose 64-row stages into [feature][row] and [col][row]
 // operands, accumulate db, and read the final TMEM accumulator out as per-CTA
 // partials that a second kernel sums in a fixed order (deterministic, no atomics).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
 #include "dr_internal.h"
 #include "proj.h"
 #include "tc.cuh"
@@ -34,8 +40,8 @@ constexpr uint32_t kHalf = 16384;      // one bf16 128 x 64 tile
 constexpr int kMaskStage = 4096;       // 128 rows x up to 8 mask words
 constexpr int kRowsThreads = 320;
 constexpr int kRedThreads = 192;
-constexpr int kSmemBudget = 227 * 1024 - 1024 - 1024;   // opt-in max minus alignment/static (rows)
-constexpr int kSmemBudgetRed = 227 * 1024 - 1024 - 6144;   // reduce kernel: 5 KB static
+constexpr int kSmemBudget = 227 * 1024 - 1024 - 4096;   // opt-in max minus alignment and static smem (rows)
+constexpr int kSmemBudgetRed = 227 * 1024 - 1024 - 6144 - 1024;   // reduce kernel: 6 KB static
 constexpr int kMaxSteps = 16;
 constexpr int kMaxSA = 4, kMaxSB = 16;
 
@@ -79,6 +85,7 @@ struct R2Seg {
     int k, K, mask_mode;
 };
 struct R2Args {
+    CUtensorMap tmap[2][2];        // dense segments: [n x K] fp32, box 64 cols x 128 rows
     int64_t n;
     int N, G, S;
     R2Step step[kMaxSteps];
@@ -110,15 +117,14 @@ __device__ __forceinline__ void rows_produce(const R2Args &a, const R2Step &sp, 
     const R2Seg &s = a.seg[sp.g][sp.s];
     const int rows = (int)(a.n - r0 < kTile ? a.n - r0 : kTile);
     if (s.A) {
-        const int Kc = min(kChunk, s.K - sp.c * kChunk);
-        const uint32_t row_bytes = (uint32_t)Kc * 4;
+        // one TMA box: rows r0..r0+127, columns 64c..64c+63 (out-of-range rows and
+        // columns arrive as zeros), plus the tile's merge-mask words
         const uint32_t mbytes = s.mask_mode != kMask2None ? rup16((uint32_t)rows * a.mw * 4) : 0u;
-        if (lane == 0) tc::mbar_arrive_expect_tx(full, row_bytes * rows + mbytes);
-        __syncwarp();
-        const float *src = s.A + r0 * s.K + sp.c * kChunk;
-        for (int r = lane; r < rows; r += 32)
-            tc::bulk_g2s(st + r * 256, src + (int64_t)r * s.K, row_bytes, full);
-        if (mbytes && lane == 0) tc::bulk_g2s(mk, a.mask_in + r0 * a.mw, mbytes, full);
+        if (lane == 0) {
+            tc::mbar_arrive_expect_tx(full, kStage + mbytes);
+            tc::tma_load_2d(st, &a.tmap[sp.g][sp.s], sp.c * kChunk, (int)r0, full);
+            if (mbytes) tc::bulk_g2s(mk, a.mask_in + r0 * a.mw, mbytes, full);
+        }
     } else {
         // CBSR rows of the tile: values at +0, indices at +kHalf (both contiguous);
         // sizes rounded up to 16 B (the tape pads every buffer)
@@ -137,7 +143,6 @@ __device__ __forceinline__ void rows_convert(const R2Args &a, const R2Step &sp, 
     const R2Seg &s = a.seg[sp.g][sp.s];
     const int lane = ct & 31, cw = ct >> 5;
     if (s.A) {
-        const int Kc = min(kChunk, s.K - sp.c * kChunk);
         const int q = lane & 15;                       // float4 column group of the chunk
         float4 v[16];
 #pragma unroll
@@ -161,9 +166,7 @@ __device__ __forceinline__ void rows_convert(const R2Args &a, const R2Step &sp, 
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
             const int r = cw * 32 + 2 * i + (lane >> 4);
-            float4 x = v[i];
-            const bool ok = (r0 + r < a.n) && (4 * q < Kc);
-            if (!ok) x = make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 x = v[i];                           // TMA zero-filled rows >= n, cols >= K
             if (s.mask_mode != kMask2None) {
                 const uint32_t b = mbits[i];
                 if (!(b & 1u)) x.x = 0.f;
@@ -179,46 +182,47 @@ __device__ __forceinline__ void rows_convert(const R2Args &a, const R2Step &sp, 
             *reinterpret_cast<uint2 *>(st + kHalf + off) = l;
         }
     } else {
-        // one row per thread: read its k pairs, then zero the row and scatter
-        const int r = ct, k = s.k;
-        const bool ok = r0 + r < a.n;
-        float vv[32];
-        uint32_t iw[8];
-        const float *vals = reinterpret_cast<const float *>(st) + r * k;
-        const uint8_t *idx = st + kHalf + r * k;
+        // CBSR chunk: thread ct reads float4 groups e4 = ct + 128 i of the tile's
+        // contiguous values (and the 4 matching index bytes), conflict-free; after
+        // a barrier the whole operand is zeroed, after a second one each thread
+        // scatters its entries whose index falls in this chunk's 64 columns
+        const int k = s.k, nv4 = 32 * k;               // 128 k entries / 4
+        int lk = 0;
+        while ((1 << lk) < k) ++lk;
+        float4 vq[8];
+        uint32_t iq[8];
 #pragma unroll
-        for (int t = 0; t < 32; ++t)
-            if (t < k) vv[t] = vals[t];
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-            if (4 * t < k) {
-                uint32_t w = 0;
-#pragma unroll
-                for (int b = 0; b < 4; ++b)
-                    if (4 * t + b < k) w |= (uint32_t)idx[4 * t + b] << (8 * b);
-                iw[t] = w;
+        for (int i = 0; i < 8; ++i) {
+            const int e4 = ct + 128 * i;
+            if (e4 < nv4) {
+                vq[i] = lds4(st + 16 * e4);
+                iq[i] = *reinterpret_cast<const uint32_t *>(st + kHalf + 4 * e4);
             }
+        }
         tc::named_bar(1, 128);
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            *reinterpret_cast<float4 *>(st + r * 128 + c * 16) = z;
-            *reinterpret_cast<float4 *>(st + kHalf + r * 128 + c * 16) = z;
-        }
-        if (ok) {
-            const int lo_c = sp.c * kChunk;
+        for (int i = 0; i < 16; ++i) *reinterpret_cast<float4 *>(st + 16 * (ct + 128 * i)) = z;
+        tc::named_bar(1, 128);
+        const int lo_c = sp.c * kChunk;
+        const int rows = (int)(a.n - r0 < kTile ? a.n - r0 : kTile);
 #pragma unroll
-            for (int t = 0; t < 32; ++t)
-                if (t < k) {
-                    const int cc = (int)((iw[t >> 2] >> (8 * (t & 3))) & 0xffu) - lo_c;
-                    if (cc >= 0 && cc < kChunk) {
-                        uint32_t h, l;
-                        tc::split_bf16x2(vv[t], 0.f, h, l);
-                        const uint32_t off = tc::sw128_off_h((uint32_t)r, (uint32_t)cc);
-                        *reinterpret_cast<uint16_t *>(st + off) = (uint16_t)(h & 0xffffu);
-                        *reinterpret_cast<uint16_t *>(st + kHalf + off) = (uint16_t)(l & 0xffffu);
-                    }
+        for (int i = 0; i < 8; ++i) {
+            const int e4 = ct + 128 * i;
+            if (e4 >= nv4) continue;
+            const float vv[4] = {vq[i].x, vq[i].y, vq[i].z, vq[i].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int e = 4 * e4 + q, r = e >> lk;
+                const int col = (int)((iq[i] >> (8 * q)) & 0xffu) - lo_c;
+                if (r < rows && col >= 0 && col < kChunk) {
+                    uint32_t h, l;
+                    tc::split_bf16x2(vv[q], 0.f, h, l);
+                    const uint32_t off = tc::sw128_off_h((uint32_t)r, (uint32_t)col);
+                    *reinterpret_cast<uint16_t *>(st + off) = (uint16_t)(h & 0xffffu);
+                    *reinterpret_cast<uint16_t *>(st + kHalf + off) = (uint16_t)(l & 0xffffu);
                 }
+            }
         }
     }
 }
@@ -232,7 +236,7 @@ __device__ __forceinline__ float pick16(const float *v, int i) {
 
 // epilogue warp (quarter qd): rows r0 + 32 qd + lane of accumulator columns at `acc`
 __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int64_t r0, int qd,
-                                              int lane) {
+                                              int lane, const float *bias_s) {
     const int N = a.N;
     const int64_t row = r0 + qd * 32 + lane;
     const bool ok = row < a.n;
@@ -280,22 +284,21 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
     uint32_t word = 0;
     for (int j = 0; j < N; j += 16) {
         float ya[16], yb[16];
-        tc::tmem_ld16(lb + (uint32_t)j, ya);
-        if (a.G == 2) tc::tmem_ld16(lb + (uint32_t)(N + j), yb);
-        if (!ok) continue;
+        {
+            uint32_t ra[16], rb[16];
+            tc::tmem_ld16_nw(lb + (uint32_t)j, ra);
+            if (a.G == 2) tc::tmem_ld16_nw(lb + (uint32_t)(N + j), rb);
+            tc::tmem_wait_ld();
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const float4 b = __ldg(reinterpret_cast<const float4 *>(a.bias[0] + j) + q);
-            ya[4 * q] += b.x; ya[4 * q + 1] += b.y; ya[4 * q + 2] += b.z; ya[4 * q + 3] += b.w;
+            for (int q = 0; q < 16; ++q) {
+                ya[q] = __uint_as_float(ra[q]) + bias_s[j + q];
+                yb[q] = a.G == 2 ? __uint_as_float(rb[q]) + bias_s[256 + j + q] : 0.f;
+            }
         }
+        if (!ok) continue;
         float y[16];
         uint32_t bits = 0;
         if (a.G == 2) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const float4 b = __ldg(reinterpret_cast<const float4 *>(a.bias[1] + j) + q);
-                yb[4 * q] += b.x; yb[4 * q + 1] += b.y; yb[4 * q + 2] += b.z; yb[4 * q + 3] += b.w;
-            }
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
                 if (a.merge == DR_MERGE_MAX) {
@@ -322,7 +325,7 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
         }
         float4 *o = reinterpret_cast<float4 *>(a.y + row * N + j);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) __stcs(o + q, make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]));
+        for (int q = 0; q < 4; ++q) o[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
         if (a.G == 2 && a.mask_out) {
             word |= bits << (j & 16);
             if ((j & 16) || j + 16 >= N) {
@@ -340,8 +343,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
     __shared__ __align__(8) uint64_t full[kMaxSA], conv[kMaxSA], empty[kMaxSA];
     __shared__ __align__(8) uint64_t bfull[kMaxSB], bempty[kMaxSB], accf[2], acce[2];
     __shared__ uint32_t tmem_slot;
+    __shared__ float bias_s[512];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int SA = a.SA, SB = a.SB, S = a.S;
+    for (int e = tid; e < 512; e += kRowsThreads) {
+        const int g = e >> 8, j = e & 255;
+        bias_s[e] = (a.epi == kEpi2Fwd && g < a.G && j < a.N && a.bias[g]) ? a.bias[g][j] : 0.f;
+    }
     uint8_t *stages = sm;
     uint8_t *bslots = sm + (size_t)SA * kStage;
     uint8_t *masks = bslots + (size_t)SB * a.bchunk;
@@ -482,7 +490,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
             const uint32_t ab = (uint32_t)(t & 1);
             tc::mbar_wait(&accf[ab], (uint32_t)((t >> 1) & 1));
             tc::fence_after();
-            rows_epilogue(a, tmem + ab * GN, r0, qd, lane);
+            rows_epilogue(a, tmem + ab * GN, r0, qd, lane, bias_s);
             tc::fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&acce[ab]);
@@ -558,78 +566,111 @@ __device__ __forceinline__ void red_produce(const RdArgs &a, int64_t rb, int64_t
     }
 }
 
-// Transposing split, read phase: unit u = (m, j) is column m (< W) of graph rows
-// 8j..8j+7 of a [64][W] fp32 block (row stride W), masked by the merge mask
-// when asked; rows >= valid read as 0. Optionally accumulates the unit's sum.
+// Transposing split of a [64 rows][W] fp32 block (row stride W) into operand
+// rows m0 .. m0+W-1 of a K-major [rows][64] bf16 hi/lo tile pair. A unit is a
+// feature quad fq (4 columns) x a row octet j (8 graph rows): 8 float4 reads,
+// 4 x (16-B hi + 16-B lo) writes. Lane l of a warp takes fq low bits from l%8
+// and j low bits from l/8, so both the row reads (8 lanes = 128 contiguous B)
+// and the swizzled writes (8 distinct 16-B bank groups per warp) are
+// conflict-free. Rows >= valid read as 0; the merge mask is applied when asked.
+struct Unit {
+    int fq, j;
+    bool ok;
+};
+__device__ __forceinline__ Unit red_unit(int W, int ct, int it) {
+    const int W4 = W >> 2, fh = (W4 + 7) >> 3;
+    const int u = ct + 128 * it;
+    const int i = u & 7, gq = (u >> 3) & 3, rest = u >> 5;
+    Unit x;
+    x.fq = i + 8 * (rest % fh);
+    x.j = gq + 4 * (rest / fh);
+    x.ok = x.fq < W4 && x.j < 8;
+    return x;
+}
 template <int MAXU>
 __device__ __forceinline__ void red_read(const float *raw, int W, int valid, int ct,
                                          const uint8_t *mkraw, int mw, int mask_mode,
-                                         float (&v)[MAXU][8], float *colsum) {
-    const int units = W * 8;
+                                         float4 (&v)[MAXU][8], float (*colsum)[4]) {
+    const float4 *raw4 = reinterpret_cast<const float4 *>(raw);
+    const int W4 = W >> 2;
 #pragma unroll
     for (int i = 0; i < MAXU; ++i) {
-        const int u = ct + 128 * i;
-        if (u < units) {
-            const int m = u % W, j = u / W;
+        const Unit x = red_unit(W, ct, i);
+        if (!x.ok) continue;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int rr = 8 * x.j + r;
+            float4 q = rr < valid ? raw4[rr * W4 + x.fq] : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (mask_mode != kMask2None) {
+                const int col = 4 * x.fq;
+                const uint32_t w =
+                    *reinterpret_cast<const uint32_t *>(mkraw + (rr * mw + (col >> 5)) * 4);
+                uint32_t b = (w >> (col & 31)) & 0xfu;
+                if (mask_mode == kMask2NotM) b = ~b & 0xfu;
+                if (!(b & 1u)) q.x = 0.f;
+                if (!(b & 2u)) q.y = 0.f;
+                if (!(b & 4u)) q.z = 0.f;
+                if (!(b & 8u)) q.w = 0.f;
+            }
+            v[i][r] = q;
+        }
+        if (colsum) {
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
-                const int rr = 8 * j + r;
-                float x = rr < valid ? raw[rr * W + m] : 0.f;
-                if (mask_mode != kMask2None) {
-                    const uint32_t w =
-                        *reinterpret_cast<const uint32_t *>(mkraw + (rr * mw + (m >> 5)) * 4);
-                    const bool bit = (w >> (m & 31)) & 1u;
-                    if (bit != (mask_mode == kMask2M)) x = 0.f;
-                }
-                v[i][r] = x;
-            }
-            if (colsum) {
-                float s = 0.f;
-#pragma unroll
-                for (int r = 0; r < 8; ++r) s += v[i][r];
-                colsum[i] += s;
+                colsum[i][0] += v[i][r].x;
+                colsum[i][1] += v[i][r].y;
+                colsum[i][2] += v[i][r].z;
+                colsum[i][3] += v[i][r].w;
             }
         }
     }
 }
-// write phase: unit (m, j) -> operand row m0 + m, K positions 8j..8j+7 (hi at
-// +0, lo at +lo_off)
+__device__ __forceinline__ void store_col8(uint8_t *tile, uint32_t lo_off, int m, int j,
+                                           float a0, float a1, float a2, float a3, float a4,
+                                           float a5, float a6, float a7) {
+    uint4 h, l;
+    tc::split_bf16x2(a0, a1, h.x, l.x);
+    tc::split_bf16x2(a2, a3, h.y, l.y);
+    tc::split_bf16x2(a4, a5, h.z, l.z);
+    tc::split_bf16x2(a6, a7, h.w, l.w);
+    const uint32_t off = tc::sw128_off_h((uint32_t)m, (uint32_t)(8 * j));
+    *reinterpret_cast<uint4 *>(tile + off) = h;
+    *reinterpret_cast<uint4 *>(tile + lo_off + off) = l;
+}
 template <int MAXU>
 __device__ __forceinline__ void red_write(uint8_t *tile, uint32_t lo_off, int W, int m0, int ct,
-                                          const float (&v)[MAXU][8]) {
-    const int units = W * 8;
+                                          const float4 (&v)[MAXU][8]) {
 #pragma unroll
     for (int i = 0; i < MAXU; ++i) {
-        const int u = ct + 128 * i;
-        if (u < units) {
-            const int m = u % W, j = u / W;
-            uint4 h, l;
-            tc::split_bf16x2(v[i][0], v[i][1], h.x, l.x);
-            tc::split_bf16x2(v[i][2], v[i][3], h.y, l.y);
-            tc::split_bf16x2(v[i][4], v[i][5], h.z, l.z);
-            tc::split_bf16x2(v[i][6], v[i][7], h.w, l.w);
-            const uint32_t off = tc::sw128_off_h((uint32_t)(m0 + m), (uint32_t)(8 * j));
-            *reinterpret_cast<uint4 *>(tile + off) = h;
-            *reinterpret_cast<uint4 *>(tile + lo_off + off) = l;
-        }
+        const Unit x = red_unit(W, ct, i);
+        if (!x.ok) continue;
+        const int m = m0 + 4 * x.fq;
+        store_col8(tile, lo_off, m + 0, x.j, v[i][0].x, v[i][1].x, v[i][2].x, v[i][3].x,
+                   v[i][4].x, v[i][5].x, v[i][6].x, v[i][7].x);
+        store_col8(tile, lo_off, m + 1, x.j, v[i][0].y, v[i][1].y, v[i][2].y, v[i][3].y,
+                   v[i][4].y, v[i][5].y, v[i][6].y, v[i][7].y);
+        store_col8(tile, lo_off, m + 2, x.j, v[i][0].z, v[i][1].z, v[i][2].z, v[i][3].z,
+                   v[i][4].z, v[i][5].z, v[i][6].z, v[i][7].z);
+        store_col8(tile, lo_off, m + 3, x.j, v[i][0].w, v[i][1].w, v[i][2].w, v[i][3].w,
+                   v[i][4].w, v[i][5].w, v[i][6].w, v[i][7].w);
     }
 }
 
 // converters: one stage -> A'_g (per group) and B' operands; db unit sums in colsum
 __device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int valid, int ct,
-                                            float (&colsum)[8]) {
+                                            float (&colsum)[2][4]) {
     const uint8_t *mk = st + a.off_mask;
     int ci = 0;
     for (int g = 0; g < a.G; ++g) {
         uint8_t *tile = st + (size_t)g * kStage;
-        float v[8][8];
+        float4 v[2][8];
         int wd = 0, wtot = 0;
         const RdSeg *dseg = nullptr;
         for (int q = 0; q < a.nseg[g]; ++q) {
             wtot += a.seg[g][q].w;
             if (a.seg[g][q].Z) { dseg = &a.seg[g][q]; wd = dseg->w; }
         }
-        if (dseg) red_read<8>(reinterpret_cast<const float *>(tile), wd, valid, ct, mk, 0,
+        if (dseg) red_read<2>(reinterpret_cast<const float *>(tile), wd, valid, ct, mk, 0,
                               kMask2None, v, nullptr);
         // CBSR entries of this group: thread -> graph row ct/2, half ct&1 of its k pairs
         float cv[16];
@@ -656,7 +697,7 @@ __device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int va
             ++ci;
         }
         tc::named_bar(1, 128);                      // raw reads done before writes
-        if (dseg) red_write<8>(tile, kHalf, wd, dseg->m0, ct, v);
+        if (dseg) red_write<2>(tile, kHalf, wd, dseg->m0, ct, v);
         {   // zero the CBSR rows and the unused rows [wtot, 128)
             const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int q = 0; q < a.nseg[g]; ++q) {
@@ -690,11 +731,11 @@ __device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int va
     }
     {   // B' = mask(dY)^T
         uint8_t *tile = st + a.off_b;
-        float v[8][8];
-        red_read<8>(reinterpret_cast<const float *>(tile), a.N, valid, ct, mk, a.mw, a.mask_mode, v,
+        float4 v[2][8];
+        red_read<2>(reinterpret_cast<const float *>(tile), a.N, valid, ct, mk, a.mw, a.mask_mode, v,
                     colsum);
         tc::named_bar(1, 128);
-        red_write<8>(tile, (uint32_t)a.N * 128u, a.N, 0, ct, v);
+        red_write<2>(tile, (uint32_t)a.N * 128u, a.N, 0, ct, v);
     }
 }
 
@@ -768,7 +809,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
         __syncwarp();
     } else {
         const int ct = tid - 64;
-        float colsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        float colsum[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
         for (int64_t it = 0; it < total; ++it) {
             const int slot = (int)(it % SA);
             tc::mbar_wait(&full[slot], (uint32_t)((it / SA) & 1));
@@ -779,11 +820,13 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&conv[slot]);
         }
-        // db partials: unit (n, j) of thread ct, summed over j in a fixed order
+        // db partials: unit (column quad, row octet j) of thread ct, summed over j in a
+        // fixed order
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int u = ct + 128 * i;
-            if (u < N * 8) dbs[u / N][u % N] = colsum[i];
+        for (int i = 0; i < 2; ++i) {
+            const Unit x = red_unit(N, ct, i);
+            if (x.ok)
+                for (int e = 0; e < 4; ++e) dbs[x.j][4 * x.fq + e] = colsum[i][e];
         }
         tc::named_bar(1, 128);
         for (int c = ct; c < N; c += 128) {
@@ -868,6 +911,34 @@ void launch_tc2_pack_b(const float *W, int ldw, int K, int NB, int n0, int Ntot,
     note_launch("tc2_pack_b");
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    });
+    DR_CHECK(fn != nullptr, DR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// [n x K] fp32 row-major, box = 64 columns x 128 rows, no swizzle (row-major
+// [128][64] landing tile), zero fill out of range
+static void make_tmap(CUtensorMap *m, const float *A, int64_t n, int K) {
+    const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)K * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)kChunk, (cuuint32_t)kTile};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)A, dims, strides, box,
+                                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DR_CHECK(r == CUDA_SUCCESS, DR_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+}
+
 static bool seg_ok(const Tc2Seg &s) {
     if (s.K < 4 || s.K > 256 || s.K % 4) return false;
     if (!s.A && (s.k < 1 || s.k > 32 || s.k > s.K)) return false;
@@ -910,6 +981,7 @@ void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
         for (int q = 0; q < d.nseg[g]; ++q) {
             const Tc2Seg &sd = d.seg[g][q];
             a.seg[g][q] = R2Seg{sd.A, sd.hval, sd.hidx, sd.k, sd.K, sd.A ? sd.mask_mode : kMask2None};
+            if (sd.A) make_tmap(&a.tmap[g][q], sd.A, d.n, sd.K);
             const int chunks = (sd.K + kChunk - 1) / kChunk;
             for (int c = 0; c < chunks; ++c)
                 a.step[a.S++] = R2Step{(int8_t)g, (int8_t)q, (int8_t)c, (int8_t)bc++,
@@ -953,6 +1025,22 @@ void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
     note_launch("tc2_rows");
 }
 
+// stage layout of the reduce kernel: [A'_g 32 KB each][B' 256 N][CBSR raw][mask words]
+static void red_layout(const Tc2ReduceDesc &d, int ncb, int maxk, RdArgs &a) {
+    auto r1k = [](uint32_t x) { return (x + 1023u) & ~1023u; };
+    uint32_t off = (uint32_t)d.G * kStage;
+    a.off_b = off;
+    off += r1k((uint32_t)256 * d.N);
+    a.off_cbsr = off;
+    a.cbsr_seg_bytes = (uint32_t)(kRRows * maxk * 4 + rup16((uint32_t)kRRows * maxk) + 16);
+    a.cbsr_seg_bytes = (a.cbsr_seg_bytes + 127u) & ~127u;
+    off += r1k(a.cbsr_seg_bytes * (uint32_t)ncb);
+    a.off_mask = off;
+    off += r1k(kRRows * 8 * 4 + 16);
+    a.stage_bytes = off;
+    a.SA = (int)std::min<size_t>(kMaxSA, (size_t)kSmemBudgetRed / a.stage_bytes);
+}
+
 bool tc2_reduce_supported(const Tc2ReduceDesc &d) {
     const char *e = getenv("DR_DENSE_SIMT");
     if (e && atoi(e)) return false;
@@ -974,7 +1062,16 @@ bool tc2_reduce_supported(const Tc2ReduceDesc &d) {
         if (w > 128 || dense > 1 || cb > 1) return false;
     }
     if (d.mask_mode != kMask2None && (d.N + 31) / 32 > 8) return false;
-    return true;
+    int ncb = 0, maxk = 0;
+    for (int g = 0; g < d.G; ++g)
+        for (int q = 0; q < d.nseg[g]; ++q)
+            if (!d.seg[g][q].Z) {
+                ++ncb;
+                maxk = std::max(maxk, d.seg[g][q].k);
+            }
+    RdArgs a{};
+    red_layout(d, ncb, maxk, a);
+    return a.SA >= 2;
 }
 
 size_t tc2_reduce_work_floats(int G, int N) {
@@ -1012,18 +1109,7 @@ void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s) {
     a.mask = d.mask;
     a.mask_mode = d.mask_mode;
     a.mw = (d.N + 31) / 32;
-    auto r1k = [](uint32_t x) { return (x + 1023u) & ~1023u; };
-    uint32_t off = (uint32_t)d.G * kStage;
-    a.off_b = off;
-    off += r1k((uint32_t)256 * d.N);
-    a.off_cbsr = off;
-    a.cbsr_seg_bytes = (uint32_t)(kRRows * maxk * 4 + rup16((uint32_t)kRRows * maxk) + 16);
-    a.cbsr_seg_bytes = (a.cbsr_seg_bytes + 127u) & ~127u;
-    off += r1k(a.cbsr_seg_bytes * (uint32_t)ncb);
-    a.off_mask = off;
-    off += r1k(kRRows * 8 * 4 + 16);
-    a.stage_bytes = off;
-    a.SA = (int)std::min<size_t>(kMaxSA, (size_t)kSmemBudgetRed / a.stage_bytes);
+    red_layout(d, ncb, maxk, a);
     DR_CHECK(a.SA >= 2, DR_ERR_UNSUPPORTED, "tc2_reduce: shared memory budget");
     const size_t smem = (size_t)a.SA * a.stage_bytes + 1024;
     int64_t grid = (d.n + 4 * kRRows - 1) / (4 * kRRows);
