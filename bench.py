@@ -255,7 +255,6 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     dr.launch_count_reset()
-    dr.profile_begin()
     wall0 = time.time()
     for i in range(args.steps):
         flush.zero_()                        # L2 flush between timed steps (outside the events)
@@ -266,7 +265,6 @@ def run_ours(args):
     wall = time.time() - wall0
     if world > 1:
         dist.barrier()
-    prof = dr.profile_end()
     launches = dr.launch_count()
     ms = sum(a.elapsed_time(b) for a, b in ev)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -275,6 +273,18 @@ def run_ours(args):
     ms_max = float(t.item())
     time.sleep(0.2)
     clk = clocks.stop()
+
+    # ---- per-kernel device times for the roofline: the same steps again, eagerly
+    # (the timed region replays a captured CUDA graph, whose kernels cannot carry
+    # per-launch events), CUDA events around every launch on its own stream
+    os.environ["DR_FORCE_SEQUENTIAL"] = "1"   # isolated kernels: no cross-stream overlap in the events
+    dr.profile_begin()
+    for i in range(args.steps):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    prof = dr.profile_end()
+    os.environ.pop("DR_FORCE_SEQUENTIAL", None)
 
     # ---- end to end through the public API with host buffers (pinned), per step:
     # H2D of the step's inputs (features + labels) and D2H of the step's loss.
@@ -287,6 +297,11 @@ def run_ours(args):
         dx = torch.empty_like(xc)
         dn = torch.empty_like(xn)
         dl = torch.empty_like(lab)
+        for _ in range(2):                   # warm the e2e buffers' captured graph
+            dx.copy_(hx, non_blocking=True)
+            dn.copy_(hn, non_blocking=True)
+            dl.copy_(hl, non_blocking=True)
+            tr.step(g, dx, dn, dl, sync=True)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -349,6 +364,11 @@ def run_ours(args):
                 "layers": nl, "id_order": "shuffled",
                 "parallelism": f"dp{world}" if world > 1 else "single",
                 "l2": "flushed (256 MB write) before every timed step, outside the events",
+                "kernel_times": "per-launch CUDA events in an eager, single-stream pass of the "
+                                "same steps right after the timed region (the timed region "
+                                "replays the step's CUDA graph on 3 streams)" if wl == "C2" else
+                                "per-launch CUDA events in a single-stream pass of the same "
+                                "steps right after the timed region",
             },
             "roofline": rf,
             "cpu_baseline": cpu,

@@ -92,6 +92,7 @@ void ensure_smem(const void *fn, size_t bytes) {
 struct StreamCtx {
     int device = -1;
     cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t cap = nullptr;                  // private capture stream (CUDA graphs)
     cudaEvent_t fork = nullptr, ev[6] = {};
 };
 static thread_local StreamCtx t_ctx;
@@ -104,6 +105,7 @@ static StreamCtx &ctx() {
             // previous device's objects: leave them (rare; device switches per thread)
         }
         for (int q = 0; q < 3; ++q) DR_CUDA(cudaStreamCreateWithFlags(&t_ctx.s[q], cudaStreamNonBlocking));
+        DR_CUDA(cudaStreamCreateWithFlags(&t_ctx.cap, cudaStreamNonBlocking));
         DR_CUDA(cudaEventCreateWithFlags(&t_ctx.fork, cudaEventDisableTiming));
         for (int q = 0; q < 6; ++q) DR_CUDA(cudaEventCreateWithFlags(&t_ctx.ev[q], cudaEventDisableTiming));
         t_ctx.device = dev;
@@ -115,6 +117,13 @@ static void wait_on(cudaStream_t waiter, cudaStream_t producer, cudaEvent_t ev) 
     if (waiter == producer) return;
     DR_CUDA(cudaEventRecord(ev, producer));
     DR_CUDA(cudaStreamWaitEvent(waiter, ev, 0));
+}
+
+// DR_FORCE_SEQUENTIAL=1: every layer runs on the caller's stream (per-kernel
+// timing passes of bench.py; results are bit-identical either way).
+static bool force_sequential() {
+    const char *e = getenv("DR_FORCE_SEQUENTIAL");
+    return e && atoi(e);
 }
 
 static bool is_pow2(int k) { return k > 0 && (k & (k - 1)) == 0; }
@@ -211,7 +220,7 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
     uint8_t *hci = (uint8_t *)(tp + T.hc_idx), *hni = (uint8_t *)(tp + T.hn_idx);
     float *z[3];
     for (int r = 0; r < 3; ++r) z[r] = (float *)(tp + T.z[r]);
-    const bool seq = (flags & DR_FWD_SEQUENTIAL) != 0;
+    const bool seq = (flags & DR_FWD_SEQUENTIAL) != 0 || force_sequential();
     StreamCtx &C = ctx();
     cudaStream_t s0 = seq ? st : C.s[0], s1 = seq ? st : C.s[1], s2 = seq ? st : C.s[2];
     if (!seq) {
@@ -320,7 +329,7 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
     for (int q = 0; q < 3; ++q) work[q] = (float *)(tp + T.work[q]);
     const int mode_near = L->merge == DR_MERGE_MAX ? kMaskM : kMaskNone;        // Eq. 12
     const int mode_pinned = L->merge == DR_MERGE_MAX ? kMaskNotM : kMaskNone;   // Eq. 13
-    const bool seq = (flags & DR_FWD_SEQUENTIAL) != 0;
+    const bool seq = (flags & DR_FWD_SEQUENTIAL) != 0 || force_sequential();
     StreamCtx &C = ctx();
     cudaStream_t s0 = seq ? st : C.s[0], s1 = seq ? st : C.s[1], s2 = seq ? st : C.s[2];
     if (!seq) {
@@ -521,6 +530,17 @@ struct dr_trainer {
     std::vector<dr_layer> L;
     std::vector<dr_layer_grad> G;
     float *head_w = nullptr, *head_b = nullptr, *ghead_w = nullptr, *ghead_b = nullptr;
+    int64_t *step_dev = nullptr;             // Adam step counter (device, inside scalars)
+    // CUDA graphs of the whole step (§3.2 "CUDA-graph captured per batch shape"),
+    // keyed by the call's graph and buffers; a key runs eagerly once, then is captured
+    struct GraphEntry {
+        uint64_t graph_uid = 0;
+        const void *xc = nullptr, *xn = nullptr, *lab = nullptr, *loss = nullptr, *gout = nullptr;
+        int runs = 0;
+        int64_t kernels = 0;                 // kernel nodes (counted as launches per replay)
+        cudaGraphExec_t exec = nullptr;
+    };
+    std::vector<GraphEntry> graphs;
 };
 
 namespace {
@@ -784,6 +804,7 @@ dr_status dr_trainer_create(const dr_train_cfg *c, float *params, int64_t n_para
     t->m = (float *)(blk + al(pb));
     t->v = (float *)(blk + 2 * al(pb));
     t->scalars = (float *)(blk + 3 * al(pb));
+    t->step_dev = (int64_t *)(blk + 3 * al(pb) + 64);
     DR_CUDA(cudaMemset(blk, 0, al(pb) * 3 + 256));
     DR_CUDA(cudaDeviceSynchronize());
     carve(t->cfg, (const float *)t->params, t->L, (const float **)&t->head_w, (const float **)&t->head_b);
@@ -805,17 +826,13 @@ dr_status dr_trainer_create(const dr_train_cfg *c, float *params, int64_t n_para
     DR_API_END
 }
 
-dr_status dr_train_step(dr_trainer *t, const dr_graph *g, const float *x_cell, const float *x_net,
-                        const float *labels, float *loss_host, float *grad_out, void *stream) {
-    DR_API_BEGIN
-    DR_CHECK(t && g, DR_ERR_INVALID_ARGUMENT, "null trainer/graph");
-    DR_CHECK((g->n_cell == 0 || (x_cell && labels)) && (g->n_net == 0 || x_net),
-             DR_ERR_INVALID_ARGUMENT, "null inputs");
-    cudaStream_t st = (cudaStream_t)stream;
+// One training step (forward, head/MSE, backward, allreduce, Adam), enqueued on st.
+static void train_step_body(dr_trainer *t, const dr_graph *g, const float *x_cell,
+                            const float *x_net, const float *labels, float *loss_host,
+                            float *grad_out, char *ws, cudaStream_t st) {
     const dr_train_cfg &c = t->cfg;
     const int nl = c.n_layers, D = c.d_hidden;
     const size_t nc = (size_t)g->n_cell, nn = (size_t)g->n_net;
-    // ---- workspace (grow-only): tapes, layer outputs, gradient ping-pong
     std::vector<size_t> tape_off(nl);
     size_t off = 0;
     for (int l = 0; l < nl; ++l) {
@@ -827,19 +844,6 @@ dr_status dr_train_step(dr_trainer *t, const dr_graph *g, const float *x_cell, c
     const size_t dy_off = off;
     off += 2 * (al(nc * D * 4) + al(nn * D * 4));
     const size_t head_off = off;
-    off += al(head_work_floats(D) * 4);
-    const size_t dxin_off = off;
-    off += al(nc * (size_t)c.d_in_cell * 4) + al(nn * (size_t)c.d_in_net * 4);   // unused dx of layer 0
-    (void)dxin_off;
-    if (off > t->ws_cap) {
-        if (t->ws) {
-            DR_CUDA(cudaStreamSynchronize(st));
-            t->alloc.put(t->ws, st);
-        }
-        t->ws = (char *)t->alloc.get(off, st);
-        t->ws_cap = off;
-    }
-    char *ws = t->ws;
     auto yc = [&](int l) { return (float *)(ws + y_off + l * (al(nc * D * 4) + al(nn * D * 4))); };
     auto yn = [&](int l) { return (float *)(ws + y_off + l * (al(nc * D * 4) + al(nn * D * 4)) + al(nc * D * 4)); };
     auto dyc = [&](int q) { return (float *)(ws + dy_off + q * (al(nc * D * 4) + al(nn * D * 4))); };
@@ -881,20 +885,98 @@ dr_status dr_train_step(dr_trainer *t, const dr_graph *g, const float *x_cell, c
                                 cudaMemcpyDeviceToDevice, st));
         if (t->world > 1) launch_scale(grad_out, t->n_params, inv_world, st);
     }
-    // ---- Adam (1/W mean folded in)
-    t->step += 1;
-    const double bc1 = 1.0 - std::pow((double)c.beta1, (double)t->step);
-    const double bc2 = 1.0 - std::pow((double)c.beta2, (double)t->step);
+    // ---- Adam (1/W mean folded in; step counter and bias corrections on the device)
     launch_adam(t->params, t->grad, t->m, t->v, t->n_params, c.lr, c.weight_decay, c.beta1,
-                c.beta2, c.eps, (float)bc1, (float)bc2, inv_world, st);
+                c.beta2, c.eps, t->step_dev, inv_world, st);
     if (loss_host)
         DR_CUDA(cudaMemcpyAsync(loss_host, t->scalars, 4, cudaMemcpyDeviceToHost, st));
+}
+
+dr_status dr_train_step(dr_trainer *t, const dr_graph *g, const float *x_cell, const float *x_net,
+                        const float *labels, float *loss_host, float *grad_out, void *stream) {
+    DR_API_BEGIN
+    DR_CHECK(t && g, DR_ERR_INVALID_ARGUMENT, "null trainer/graph");
+    DR_CHECK((g->n_cell == 0 || (x_cell && labels)) && (g->n_net == 0 || x_net),
+             DR_ERR_INVALID_ARGUMENT, "null inputs");
+    cudaStream_t st = (cudaStream_t)stream;
+    const dr_train_cfg &c = t->cfg;
+    const int nl = c.n_layers, D = c.d_hidden;
+    const size_t nc = (size_t)g->n_cell, nn = (size_t)g->n_net;
+    // ---- workspace (grow-only): tapes, layer outputs, gradient ping-pong, head partials
+    size_t off = 0;
+    for (int l = 0; l < nl; ++l) off += al(tape_layout(g, &t->L[l], 0).total);
+    off += nl * (al(nc * D * 4) + al(nn * D * 4));
+    off += 2 * (al(nc * D * 4) + al(nn * D * 4));
+    off += al(head_work_floats(D) * 4);
+    if (off > t->ws_cap) {
+        DR_CUDA(cudaStreamSynchronize(st));
+        for (auto &e : t->graphs)
+            if (e.exec) cudaGraphExecDestroy(e.exec);
+        t->graphs.clear();                     // captured graphs point at the old workspace
+        if (t->ws) t->alloc.put(t->ws, st);
+        t->ws = (char *)t->alloc.get(off, st);
+        t->ws_cap = off;
+    }
+    t->step += 1;
+    const char *ng = getenv("DR_NO_GRAPH");
+    if (t_prof || (ng && atoi(ng))) {          // per-kernel profiling runs eagerly
+        train_step_body(t, g, x_cell, x_net, labels, loss_host, grad_out, t->ws, st);
+    } else {
+        dr_trainer::GraphEntry *ge = nullptr;
+        for (auto &e : t->graphs)
+            if (e.graph_uid == g->uid && e.xc == x_cell && e.xn == x_net && e.lab == labels &&
+                e.loss == loss_host && e.gout == grad_out)
+                ge = &e;
+        if (!ge) {
+            t->graphs.push_back({});
+            ge = &t->graphs.back();
+            ge->graph_uid = g->uid; ge->xc = x_cell; ge->xn = x_net; ge->lab = labels;
+            ge->loss = loss_host; ge->gout = grad_out;
+        }
+        if (ge->exec) {
+            DR_CUDA(cudaGraphLaunch(ge->exec, st));
+            t_launches += ge->kernels;
+        } else if (ge->runs++ == 0) {          // first use: eager (attributes, caches)
+            train_step_body(t, g, x_cell, x_net, labels, loss_host, grad_out, t->ws, st);
+        } else {                               // capture on a private stream, replay on st
+            StreamCtx &C = ctx();
+            cudaGraph_t graph = nullptr;
+            DR_CUDA(cudaStreamBeginCapture(C.cap, cudaStreamCaptureModeThreadLocal));
+            try {
+                train_step_body(t, g, x_cell, x_net, labels, loss_host, grad_out, t->ws, C.cap);
+            } catch (...) {
+                cudaStreamEndCapture(C.cap, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                cudaGetLastError();
+                throw;
+            }
+            DR_CUDA(cudaStreamEndCapture(C.cap, &graph));
+            size_t nn_nodes = 0;
+            cudaGraphGetNodes(graph, nullptr, &nn_nodes);
+            std::vector<cudaGraphNode_t> nodes(nn_nodes);
+            cudaGraphGetNodes(graph, nodes.data(), &nn_nodes);
+            ge->kernels = 0;
+            for (auto nd : nodes) {
+                cudaGraphNodeType ty;
+                if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel)
+                    ++ge->kernels;
+            }
+            t_launches -= ge->kernels;         // the capture counted them; the replay below counts
+            const cudaError_t ie = cudaGraphInstantiate(&ge->exec, graph, 0);
+            cudaGraphDestroy(graph);
+            DR_CUDA(ie);
+            DR_CUDA(cudaGraphLaunch(ge->exec, st));
+            t_launches += ge->kernels;
+        }
+    }
     DR_API_END
 }
 
 dr_status dr_trainer_destroy(dr_trainer *t) {
     if (!t) return DR_OK;
     cudaDeviceSynchronize();
+    for (auto &e : t->graphs)
+        if (e.exec) cudaGraphExecDestroy(e.exec);
     if (t->ws) t->alloc.put(t->ws, nullptr);
     if (t->grad) t->alloc.put(t->grad, nullptr);
     delete t;

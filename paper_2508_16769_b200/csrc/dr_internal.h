@@ -111,6 +111,7 @@ using SrcSched = Sched;
 }  // namespace dr
 
 struct dr_graph {
+    uint64_t uid = 0;                    // unique per created graph (CUDA-graph cache key)
     int32_t n_cell = 0, n_net = 0;
     dr::RelDev rel[3];
     dr::SrcSched src_cell, src_net;

@@ -8,6 +8,7 @@
 // the three subgraphs are initialised concurrently on worker threads, each
 // uploading on its own CUDA stream.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -328,6 +329,8 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
 
         // ---- phase 2: one device block, carved per array
         g = new dr_graph();
+        static std::atomic<uint64_t> next_uid{1};
+        g->uid = next_uid++;
         g->n_cell = n_cell;
         g->n_net = n_net;
         g->create_stream = cs;

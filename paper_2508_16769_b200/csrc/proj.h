@@ -80,7 +80,7 @@ void launch_head_mse(const HeadArgs &a, cudaStream_t s);
 
 // Adam with coupled L2 weight decay (reading Q15); grad is scaled by inv_world first.
 void launch_adam(float *theta, const float *grad, float *m, float *v, int64_t n, float lr,
-                 float wd, float b1, float b2, float eps, float bc1, float bc2, float inv_world,
+                 float wd, float b1, float b2, float eps, int64_t *step_dev, float inv_world,
                  cudaStream_t s);
 void launch_scale(float *x, int64_t n, float a, cudaStream_t s);
 

@@ -72,10 +72,18 @@ __global__ void head_reduce_kernel(HeadArgs a, float inv_n) {
     }
 }
 
+// Adam step counter lives on the device (so a captured CUDA graph of the whole
+// training step replays correctly): bump it, then every thread derives the bias
+// corrections 1 - beta^t in double, exactly as the host formula did.
+__global__ void step_bump_kernel(int64_t *step) { *step += 1; }
+
 __global__ void adam_kernel(float *__restrict__ th, const float *__restrict__ g,
                             float *__restrict__ m, float *__restrict__ v, int64_t n, float lr,
-                            float wd, float b1, float b2, float eps, float bc1, float bc2,
+                            float wd, float b1, float b2, float eps, const int64_t *step_dev,
                             float inv_world) {
+    const double st = (double)*step_dev;
+    const float bc1 = (float)(1.0 - pow((double)b1, st));
+    const float bc2 = (float)(1.0 - pow((double)b2, st));
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const float t = th[i];
@@ -109,14 +117,16 @@ void launch_head_mse(const HeadArgs &a, cudaStream_t s) {
 }
 
 void launch_adam(float *theta, const float *grad, float *m, float *v, int64_t n, float lr,
-                 float wd, float b1, float b2, float eps, float bc1, float bc2, float inv_world,
+                 float wd, float b1, float b2, float eps, int64_t *step_dev, float inv_world,
                  cudaStream_t s) {
     int64_t blocks = (n + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
+    step_bump_kernel<<<1, 1, 0, s>>>(step_dev);
+    note_launch("step_bump");
     ProfScope ps("adam", s);
-    adam_kernel<<<(unsigned)blocks, 256, 0, s>>>(theta, grad, m, v, n, lr, wd, b1, b2, eps, bc1,
-                                                  bc2, inv_world);
+    adam_kernel<<<(unsigned)blocks, 256, 0, s>>>(theta, grad, m, v, n, lr, wd, b1, b2, eps,
+                                                  step_dev, inv_world);
     note_launch("adam");
 }
 
