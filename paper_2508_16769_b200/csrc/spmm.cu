@@ -476,11 +476,23 @@ void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, in
     note_launch("spmm_fwd");
 }
 
+// Backward lane mapping: two CBSR positions per lane (P = 2, L = k/2 lanes per
+// row): the sampled gathers of one warp instruction then touch fewer neighbour
+// rows of dZ (fewer distinct cache lines per request) than with P = 4, while
+// keeping two independent loads per lane; measured best at C2 (k=8) and C4
+// (k=16) against P = 1 and 4 (profiles/r01/ab_bwdP.txt). Row sums stay in registers.
+static int choose_P_bwd(int k) {
+    const char *e = getenv("DR_BWD_P");              // experiments only
+    if (e && atoi(e) > 0 && k % atoi(e) == 0 && k / atoi(e) <= 32) return atoi(e);
+    if (k == 1) return 1;
+    return k / 2 <= 32 ? 2 : k / 32;
+}
+
 void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, const float *root,
                      const uint8_t *hidx, int k, int dim, float *g_kept, float *dx,
                      bool accumulate, cudaStream_t s) {
     if (n_src <= 0) return;
-    const int P = choose_P(k, dim);
+    const int P = choose_P_bwd(k);
     DR_CHECK(P > 0, DR_ERR_BAD_K, "spmm_bwd: unsupported k");
     BwdArgs a{};
     a.order = sched.order;
