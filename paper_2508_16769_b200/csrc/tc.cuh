@@ -69,6 +69,25 @@ __device__ __forceinline__ void tma_load_2d(void *sdst, const void *tmap, int c0
         : "memory");
 }
 
+// 2-D tensor store (TMA) of a shared-memory box to (c0, c1) of the tensor map,
+// tracked by the issuing thread's bulk async-groups.
+__device__ __forceinline__ void tma_store_2d(const void *tmap, int c0, int c1, const void *ssrc) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+            reinterpret_cast<uint64_t>(tmap)),
+        "r"(c0), "r"(c1), "r"(smem_u32(ssrc))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ---------------------------------------------------------------- cp.async (LDGSTS)
 // 16-byte global -> shared copy; `bytes` < 16 zero-fills the rest (0 => all zero).
 __device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc, uint32_t bytes) {

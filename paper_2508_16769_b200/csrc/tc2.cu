@@ -40,7 +40,8 @@ constexpr uint32_t kHalf = 16384;      // one bf16 128 x 64 tile
 constexpr int kMaskStage = 4096;       // 128 rows x up to 8 mask words
 constexpr int kRowsThreads = 320;
 constexpr int kRedThreads = 192;
-constexpr int kSmemBudget = 227 * 1024 - 1024 - 4096;   // opt-in max minus alignment and static smem (rows)
+constexpr int kEpiStage = 4 * 4096;   // epilogue TMA-store staging (4 warps x 2 x 2 KB)
+constexpr int kSmemBudget = 227 * 1024 - 1024 - 4096 - kEpiStage;   // opt-in max minus alignment, static smem, staging (rows)
 constexpr int kSmemBudgetRed = 227 * 1024 - 1024 - 6144 - 1024;   // reduce kernel: 6 KB static
 constexpr int kMaxSteps = 16;
 constexpr int kMaxSA = 4, kMaxSB = 16;
@@ -86,6 +87,7 @@ struct R2Seg {
 };
 struct R2Args {
     CUtensorMap tmap[2][2];        // dense segments: [n x K] fp32, box 64 cols x 128 rows
+    CUtensorMap tmap_out;          // y (n x N) or dz (n x n_dz) fp32, box 16 cols x 32 rows, SW64
     int64_t n;
     int N, G, S;
     R2Step step[kMaxSteps];
@@ -95,6 +97,7 @@ struct R2Args {
     int mw;
     int SA, SB, b_resident;
     uint32_t bchunk;               // bytes of one packed B chunk (hi + lo)
+    uint32_t epi_off;              // byte offset of the epilogue staging boxes
     int epi;
     const float *bias[2];
     int merge;
@@ -235,10 +238,36 @@ __device__ __forceinline__ float pick16(const float *v, int i) {
 }
 
 // epilogue warp (quarter qd): rows r0 + 32 qd + lane of accumulator columns at `acc`
+// Stage 16 columns of this warp's 32 rows (lane = row) in a 2-KB SW64 box and
+// TMA-store it to (col, row0) of the output map: coalesced, sector-complete
+// writes instead of 32 row-strided 16-B stores per instruction. Two buffers
+// per warp; a buffer is rewritten once the store issued two calls ago has
+// finished reading it.
+__device__ __forceinline__ void epi_store16(const CUtensorMap *map, int col, int64_t row0,
+                                            const float *v, uint8_t *stage, int &sb, int lane) {
+    uint8_t *buf = stage + sb * 2048;
+    if (lane == 0) tc::bulk_wait_read<1>();
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const uint32_t off = (uint32_t)lane * 64u + ((((uint32_t)c ^ ((uint32_t)lane >> 1)) & 3u) << 4);
+        *reinterpret_cast<float4 *>(buf + off) = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+    }
+    tc::fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+        tc::tma_store_2d(map, col, (int)row0, buf);
+        tc::bulk_commit();
+    }
+    sb ^= 1;
+}
+
+// epilogue warp (quarter qd): rows r0 + 32 qd + lane of accumulator columns at `acc`
 __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int64_t r0, int qd,
-                                              int lane, const float *bias_s) {
+                                              int lane, const float *bias_s, uint8_t *stage,
+                                              int &sb) {
     const int N = a.N;
-    const int64_t row = r0 + qd * 32 + lane;
+    const int64_t row0 = r0 + qd * 32, row = row0 + lane;
     const bool ok = row < a.n;
     const uint32_t lb = acc + ((uint32_t)(qd * 32) << 16);
     if (a.epi == kEpi2Dz) {
@@ -258,81 +287,84 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
                 }
         }
         int p = 0;                                     // next root index (ascending)
-        for (int j = 0; j < N; j += 16) {
-            float v[16];
-            tc::tmem_ld16(lb + (uint32_t)j, v);
-            if (!ok) continue;
-            if (j < a.n_dz) {
-                float4 *o = reinterpret_cast<float4 *>(a.dz + row * a.n_dz + j);
+        for (int j = 0; j < N; j += 32) {
+            uint32_t r[2][16];
+            tc::tmem_ld16_nw(lb + (uint32_t)j, r[0]);
+            if (j + 16 < N) tc::tmem_ld16_nw(lb + (uint32_t)(j + 16), r[1]);
+            tc::tmem_wait_ld();
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    o[q] = make_float4(cr * v[4 * q], cr * v[4 * q + 1], cr * v[4 * q + 2],
-                                       cr * v[4 * q + 3]);
-            } else if (a.root) {
-                const int j0 = j - a.n_dz;
-                while (p < rk) {
-                    const int id = (int)((iw[p >> 2] >> (8 * (p & 3))) & 0xffu);
-                    if (id >= j0 + 16) break;
-                    a.root[row * rk + p] = pick16(v, id - j0);
-                    ++p;
+            for (int h = 0; h < 2; ++h) {
+                const int jj = j + 16 * h;
+                if (jj >= N) break;
+                float v[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[h][q]);
+                if (jj < a.n_dz) {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) v[q] *= cr;
+                    epi_store16(&a.tmap_out, jj, row0, v, stage, sb, lane);
+                } else if (a.root && ok) {
+                    const int j0 = jj - a.n_dz;
+                    while (p < rk) {
+                        const int id = (int)((iw[p >> 2] >> (8 * (p & 3))) & 0xffu);
+                        if (id >= j0 + 16) break;
+                        a.root[row * rk + p] = pick16(v, id - j0);
+                        ++p;
+                    }
                 }
             }
         }
         return;
     }
     const int mw = (N + 31) >> 5;
-    uint32_t word = 0;
-    for (int j = 0; j < N; j += 16) {
-        float ya[16], yb[16];
-        {
-            uint32_t ra[16], rb[16];
-            tc::tmem_ld16_nw(lb + (uint32_t)j, ra);
-            if (a.G == 2) tc::tmem_ld16_nw(lb + (uint32_t)(N + j), rb);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                ya[q] = __uint_as_float(ra[q]) + bias_s[j + q];
-                yb[q] = a.G == 2 ? __uint_as_float(rb[q]) + bias_s[256 + j + q] : 0.f;
-            }
-        }
-        if (!ok) continue;
-        float y[16];
-        uint32_t bits = 0;
+    for (int j = 0; j < N; j += 32) {
+        uint32_t ra[2][16], rb[2][16];
+        tc::tmem_ld16_nw(lb + (uint32_t)j, ra[0]);
+        if (j + 16 < N) tc::tmem_ld16_nw(lb + (uint32_t)(j + 16), ra[1]);
         if (a.G == 2) {
+            tc::tmem_ld16_nw(lb + (uint32_t)(N + j), rb[0]);
+            if (j + 16 < N) tc::tmem_ld16_nw(lb + (uint32_t)(N + j + 16), rb[1]);
+        }
+        tc::tmem_wait_ld();
+        uint32_t word = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int jj = j + 16 * h;
+            if (jj >= N) break;
+            float ya[16], yb[16], y[16];
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-                if (a.merge == DR_MERGE_MAX) {
-                    const bool m = ya[q] >= yb[q];          // Eq. 14: ties -> near
-                    y[q] = m ? ya[q] : yb[q];
-                    bits |= (uint32_t)m << q;
-                } else {
-                    y[q] = ya[q] + yb[q];
+                ya[q] = __uint_as_float(ra[h][q]) + bias_s[jj + q];
+                yb[q] = a.G == 2 ? __uint_as_float(rb[h][q]) + bias_s[256 + jj + q] : 0.f;
+            }
+            if (a.G == 2) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    if (a.merge == DR_MERGE_MAX) {
+                        const bool m = ya[q] >= yb[q];          // Eq. 14: ties -> near
+                        y[q] = m ? ya[q] : yb[q];
+                        word |= (uint32_t)m << (16 * h + q);
+                    } else {
+                        y[q] = ya[q] + yb[q];
+                    }
                 }
-            }
-            if (a.tap_a) {
-                float4 *o = reinterpret_cast<float4 *>(a.tap_a + row * N + j);
+                if (ok && a.tap_a) {
+                    float4 *o = reinterpret_cast<float4 *>(a.tap_a + row * N + jj);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) o[q] = make_float4(ya[4 * q], ya[4 * q + 1], ya[4 * q + 2], ya[4 * q + 3]);
-            }
-            if (a.tap_b) {
-                float4 *o = reinterpret_cast<float4 *>(a.tap_b + row * N + j);
+                    for (int q = 0; q < 4; ++q) o[q] = make_float4(ya[4 * q], ya[4 * q + 1], ya[4 * q + 2], ya[4 * q + 3]);
+                }
+                if (ok && a.tap_b) {
+                    float4 *o = reinterpret_cast<float4 *>(a.tap_b + row * N + jj);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) o[q] = make_float4(yb[4 * q], yb[4 * q + 1], yb[4 * q + 2], yb[4 * q + 3]);
-            }
-        } else {
+                    for (int q = 0; q < 4; ++q) o[q] = make_float4(yb[4 * q], yb[4 * q + 1], yb[4 * q + 2], yb[4 * q + 3]);
+                }
+            } else {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) y[q] = ya[q];
+                for (int q = 0; q < 16; ++q) y[q] = ya[q];
+            }
+            epi_store16(&a.tmap_out, jj, row0, y, stage, sb, lane);
         }
-        float4 *o = reinterpret_cast<float4 *>(a.y + row * N + j);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) o[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
-        if (a.G == 2 && a.mask_out) {
-            word |= bits << (j & 16);
-            if ((j & 16) || j + 16 >= N) {
-                a.mask_out[row * mw + (j >> 5)] = word;
-                word = 0;
-            }
-        }
+        if (ok && a.G == 2 && a.mask_out) a.mask_out[row * mw + (j >> 5)] = word;
     }
 }
 
@@ -353,6 +385,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
     uint8_t *stages = sm;
     uint8_t *bslots = sm + (size_t)SA * kStage;
     uint8_t *masks = bslots + (size_t)SB * a.bchunk;
+    uint8_t *epi_stage = sm + a.epi_off;        // 4 epilogue warps x 2 x 2 KB (1024-aligned)
     const uint32_t GN = (uint32_t)(a.G * a.N);
     uint32_t ncols = 32;
     while (ncols < 2 * GN) ncols <<= 1;
@@ -485,16 +518,20 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
     } else {
         // ---------------- epilogue
         const int qd = warp & 3;
+        uint8_t *stage = epi_stage + (size_t)(warp - 6) * 4096;
+        int sb = 0;
         for (int64_t t = 0; t < my_tiles; ++t) {
             const int64_t r0 = ((int64_t)blockIdx.x + t * gridDim.x) * kTile;
             const uint32_t ab = (uint32_t)(t & 1);
             tc::mbar_wait(&accf[ab], (uint32_t)((t >> 1) & 1));
             tc::fence_after();
-            rows_epilogue(a, tmem + ab * GN, r0, qd, lane, bias_s);
+            rows_epilogue(a, tmem + ab * GN, r0, qd, lane, bias_s, stage, sb);
             tc::fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&acce[ab]);
         }
+        if (lane == 0) tc::bulk_wait<0>();             // stores done before smem is released
+        __syncwarp();
     }
     tc::fence_before();
     __syncthreads();
@@ -925,6 +962,18 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+// output map: [n x W] fp32 row-major, box = 16 columns x 32 rows, SWIZZLE_64B
+static void make_out_tmap(CUtensorMap *m, float *Y, int64_t n, int W) {
+    const cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)W * 4};
+    const cuuint32_t box[2] = {16, 32};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)Y, dims, strides, box,
+                                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DR_CHECK(r == CUDA_SUCCESS, DR_ERR_CUDA, "cuTensorMapEncodeTiled (out) failed");
+}
+
 // [n x K] fp32 row-major, box = 64 columns x 128 rows, no swizzle (row-major
 // [128][64] landing tile), zero fill out of range
 static void make_tmap(CUtensorMap *m, const float *A, int64_t n, int K) {
@@ -1016,7 +1065,10 @@ void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
         if (3 * st_bytes + 2 * (size_t)a.bchunk > budget) a.SA = 2;
         a.SB = (int)std::min<size_t>(4, (budget - a.SA * st_bytes) / a.bchunk);
     }
-    const size_t smem = (size_t)a.SA * st_bytes + (size_t)a.SB * a.bchunk + 1024;
+    a.epi_off = (uint32_t)((a.SA * st_bytes + (size_t)a.SB * a.bchunk + 1023) / 1024 * 1024);
+    const size_t smem = (size_t)a.epi_off + kEpiStage + 1024;
+    if (d.epi == kEpi2Dz) make_out_tmap(&a.tmap_out, d.dz, d.n, d.n_dz);
+    else make_out_tmap(&a.tmap_out, d.y, d.n, d.N);
     const int64_t tiles = (d.n + kTile - 1) / kTile;
     const int64_t grid = tiles < 148 ? tiles : 148;
     ProfScope ps(d.epi == kEpi2Dz ? "tc_dz" : "tc_proj", s);
