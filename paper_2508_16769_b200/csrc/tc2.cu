@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <mutex>
 
 #include "dr_internal.h"
@@ -565,7 +566,11 @@ struct RdArgs {
     uint32_t cbsr_seg_bytes;                            // per CBSR segment: vals (64k*4) + idx (64k)
     int64_t rows_per_cta;
     float *part;                                        // [grid][G*128*N + N]
+    unsigned long long *dbg;                            // DR_TC2_DEBUG role timers, else null
 };
+
+#define RDBG_T0 const long long dbg_t0 = a.dbg ? clock64() : 0
+#define RDBG_ADD(slot) do { if (a.dbg) atomicAdd(a.dbg + blockIdx.x * 16 + (slot), (unsigned long long)(clock64() - dbg_t0)); } while (0)
 
 constexpr int kRRows = 64;     // graph rows per reduce step (= MMA K of 4 kind::f16 steps)
 
@@ -776,6 +781,147 @@ __device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int va
     }
 }
 
+// ---- specialised converter: compile-time layout (G groups, dense width WD, CBSR
+// width WC, N output columns), for the square-layer shapes of the workloads:
+//   G = 1: group 0 = [Z (WD) | densify(H) (WC)], G = 2: group 0 = Z, group 1 = H.
+template <int W>
+__device__ __forceinline__ Unit red_unit_t(int ct, int it) {
+    constexpr int W4 = W / 4, fh = (W4 + 7) / 8;
+    const int u = ct + 128 * it;
+    const int i = u & 7, gq = (u >> 3) & 3, rest = u >> 5;
+    Unit x;
+    x.fq = i + 8 * (rest % fh);
+    x.j = gq + 4 * (rest / fh);
+    x.ok = x.fq < W4 && x.j < 8;
+    return x;
+}
+template <int W>
+__device__ __forceinline__ void red_read_t(const float *raw, int valid, int ct, const uint8_t *mkraw,
+                                           int mw, int mask_mode, float4 (&v)[2][8],
+                                           float (*colsum)[4]) {
+    const float4 *raw4 = reinterpret_cast<const float4 *>(raw);
+    constexpr int W4 = W / 4;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const Unit x = red_unit_t<W>(ct, i);
+        if (!x.ok) continue;
+        const int col = 4 * x.fq;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int rr = 8 * x.j + r;
+            float4 q = raw4[rr * W4 + x.fq];
+            if (rr >= valid) q = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (mask_mode != kMask2None) {
+                const uint32_t w = *reinterpret_cast<const uint32_t *>(mkraw + (rr * mw + (col >> 5)) * 4);
+                uint32_t b = (w >> (col & 31)) & 0xfu;
+                if (mask_mode == kMask2NotM) b = ~b & 0xfu;
+                if (!(b & 1u)) q.x = 0.f;
+                if (!(b & 2u)) q.y = 0.f;
+                if (!(b & 4u)) q.z = 0.f;
+                if (!(b & 8u)) q.w = 0.f;
+            }
+            v[i][r] = q;
+            if (colsum) {
+                colsum[i][0] += q.x;
+                colsum[i][1] += q.y;
+                colsum[i][2] += q.z;
+                colsum[i][3] += q.w;
+            }
+        }
+    }
+}
+template <int W>
+__device__ __forceinline__ void red_write_t(uint8_t *tile, uint32_t lo_off, int m0, int ct,
+                                            const float4 (&v)[2][8]) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const Unit x = red_unit_t<W>(ct, i);
+        if (!x.ok) continue;
+        const int m = m0 + 4 * x.fq;
+        store_col8(tile, lo_off, m + 0, x.j, v[i][0].x, v[i][1].x, v[i][2].x, v[i][3].x,
+                   v[i][4].x, v[i][5].x, v[i][6].x, v[i][7].x);
+        store_col8(tile, lo_off, m + 1, x.j, v[i][0].y, v[i][1].y, v[i][2].y, v[i][3].y,
+                   v[i][4].y, v[i][5].y, v[i][6].y, v[i][7].y);
+        store_col8(tile, lo_off, m + 2, x.j, v[i][0].z, v[i][1].z, v[i][2].z, v[i][3].z,
+                   v[i][4].z, v[i][5].z, v[i][6].z, v[i][7].z);
+        store_col8(tile, lo_off, m + 3, x.j, v[i][0].w, v[i][1].w, v[i][2].w, v[i][3].w,
+                   v[i][4].w, v[i][5].w, v[i][6].w, v[i][7].w);
+    }
+}
+template <int G, int WD, int WC, int N>
+__device__ __forceinline__ void red_convert_t(const RdArgs &a, uint8_t *st, int valid, int ct,
+                                              float (&colsum)[2][4]) {
+    const uint8_t *mk = st + a.off_mask;
+    uint8_t *tz = st;                                   // group 0: dense rows [0, WD)
+    uint8_t *th = G == 2 ? st + kStage : st;            // CBSR rows [hm0, hm0 + WC)
+    constexpr int hm0 = G == 2 ? 0 : WD;
+    float4 v[2][8];
+    red_read_t<WD>(reinterpret_cast<const float *>(tz), valid, ct, mk, 0, kMask2None, v, nullptr);
+    // CBSR: thread -> graph row r = ct & 63, contiguous half h = ct >> 6 of its k pairs
+    const int kc = a.seg[G == 2 ? 1 : 0][G == 2 ? 0 : 1].k;
+    const int r = ct & 63, h = ct >> 6, kh = kc >> 1;
+    float cv[16];
+    uint32_t cw[4];
+    if constexpr (WC > 0) {
+        const uint8_t *cb = st + a.off_cbsr;
+        const float *vals = reinterpret_cast<const float *>(cb) + r * kc + h * kh;
+        const uint8_t *ids = cb + (size_t)kRRows * kc * 4 + r * kc + h * kh;
+        const bool okr = r < valid;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) cv[t] = (t < kh && okr) ? vals[t] : 0.f;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            uint32_t w = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (4 * t + b < kh) w |= (uint32_t)ids[4 * t + b] << (8 * b);
+            cw[t] = okr ? w : 0u;
+        }
+    }
+    tc::named_bar(1, 128);                              // raw reads done before writes
+    red_write_t<WD>(tz, kHalf, 0, ct, v);
+    {
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        if constexpr (WC > 0) {
+#pragma unroll
+            for (int e0 = 0; e0 < WC * 8; e0 += 128) {
+                const int e = e0 + ct, m = hm0 + e / 8, c = e % 8;
+                *reinterpret_cast<float4 *>(th + m * 128 + c * 16) = z;
+                *reinterpret_cast<float4 *>(th + kHalf + m * 128 + c * 16) = z;
+            }
+        }
+        if constexpr (G == 1 && WD + WC < kTile) {
+            for (int e = (WD + WC) * 8 + ct; e < kTile * 8; e += 128) {
+                const int m = e / 8, c = e % 8;
+                *reinterpret_cast<float4 *>(tz + m * 128 + c * 16) = z;
+                *reinterpret_cast<float4 *>(tz + kHalf + m * 128 + c * 16) = z;
+            }
+        }
+    }
+    if constexpr (WC > 0) {
+        tc::named_bar(1, 128);                          // zeros before the scatter
+        if (r < valid) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+                if (t < kh) {
+                    const int id = (int)((cw[t >> 2] >> (8 * (t & 3))) & 0xffu);
+                    uint32_t hh, ll;
+                    tc::split_bf16x2(cv[t], 0.f, hh, ll);
+                    const uint32_t off = tc::sw128_off_h((uint32_t)(hm0 + id), (uint32_t)r);
+                    *reinterpret_cast<uint16_t *>(th + off) = (uint16_t)(hh & 0xffffu);
+                    *reinterpret_cast<uint16_t *>(th + kHalf + off) = (uint16_t)(ll & 0xffffu);
+                }
+        }
+    }
+    {   // B' = mask(dY)^T
+        uint8_t *tile = st + a.off_b;
+        red_read_t<N>(reinterpret_cast<const float *>(tile), valid, ct, mk, a.mw, a.mask_mode, v, colsum);
+        tc::named_bar(1, 128);
+        red_write_t<N>(tile, (uint32_t)N * 128u, 0, ct, v);
+    }
+}
+
+template <int G_, int WD_, int WC_, int N_>
 __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid_constant__ RdArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -783,6 +929,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
     __shared__ __align__(8) uint64_t full[kMaxSA], conv[kMaxSA], empty[kMaxSA], accf;
     __shared__ uint32_t tmem_slot;
     __shared__ float dbs[8][128];
+    const long long kt0 = clock64();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int SA = a.SA, G = a.G, N = a.N;
     uint32_t ncols = 32;
@@ -813,7 +960,11 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
         for (int64_t it = 0; it < total; ++it) {
             const int slot = (int)(it % SA);
             const uint32_t u = (uint32_t)(it / SA);
-            if (u > 0) tc::mbar_wait(&empty[slot], (u - 1) & 1u);
+            if (u > 0) {
+                RDBG_T0;
+                tc::mbar_wait(&empty[slot], (u - 1) & 1u);
+                if (lane == 0) RDBG_ADD(0);
+            }
             red_produce(a, rbeg + it * kRRows, rend, sm + (size_t)slot * a.stage_bytes, &full[slot], lane);
             __syncwarp();
         }
@@ -822,7 +973,11 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
             const uint32_t idesc = tc::idesc_bf16(kTile, N);
             for (int64_t it = 0; it < total; ++it) {
                 const int slot = (int)(it % SA);
-                tc::mbar_wait(&conv[slot], (uint32_t)((it / SA) & 1));
+                {
+                    RDBG_T0;
+                    tc::mbar_wait(&conv[slot], (uint32_t)((it / SA) & 1));
+                    RDBG_ADD(1);
+                }
                 tc::fence_after();
                 uint8_t *st = sm + (size_t)slot * a.stage_bytes;
                 const uint32_t sb = tc::smem_u32(st + a.off_b), blo = (uint32_t)N * 128u;
@@ -849,10 +1004,21 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
         float colsum[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
         for (int64_t it = 0; it < total; ++it) {
             const int slot = (int)(it % SA);
-            tc::mbar_wait(&full[slot], (uint32_t)((it / SA) & 1));
+            {
+                RDBG_T0;
+                tc::mbar_wait(&full[slot], (uint32_t)((it / SA) & 1));
+                if (ct == 0) RDBG_ADD(2);
+            }
             const int64_t rb = rbeg + it * kRRows;
             const int valid = (int)(rend - rb < kRRows ? rend - rb : kRRows);
-            red_convert(a, sm + (size_t)slot * a.stage_bytes, valid, ct, colsum);
+            {
+                RDBG_T0;
+                if constexpr (G_ > 0)
+                    red_convert_t<G_, WD_, WC_, N_>(a, sm + (size_t)slot * a.stage_bytes, valid, ct, colsum);
+                else
+                    red_convert(a, sm + (size_t)slot * a.stage_bytes, valid, ct, colsum);
+                if (ct == 0) RDBG_ADD(3);
+            }
             tc::fence_async_smem();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&conv[slot]);
@@ -893,6 +1059,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
     }
     tc::fence_before();
     __syncthreads();
+    if (a.dbg && tid == 0) atomicAdd(a.dbg + blockIdx.x * 16 + 8, (unsigned long long)(clock64() - kt0));
     if (warp == 1) {
         tc::fence_after();
         tc::tmem_dealloc(tmem, ncols);
@@ -1170,9 +1337,46 @@ void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s) {
     a.rows_per_cta = ((d.n + grid - 1) / grid + kRRows - 1) / kRRows * kRRows;
     a.part = work;
     ProfScope ps("tc_dw", s);
-    ensure_smem((const void *)tc2_reduce_kernel, smem);
-    tc2_reduce_kernel<<<(unsigned)grid, kRedThreads, smem, s>>>(a);
+    static unsigned long long *dbg_buf = nullptr;
+    const char *dbe = getenv("DR_TC2_DEBUG");
+    if (dbe && atoi(dbe)) {
+        if (!dbg_buf) DR_CUDA(cudaMalloc(&dbg_buf, 148 * 16 * 8));
+        DR_CUDA(cudaMemsetAsync(dbg_buf, 0, 148 * 16 * 8, s));
+        a.dbg = dbg_buf;
+    }
+    // specialised converters for the square-layer shapes; generic otherwise
+    auto is_seg = [&](int g, int q, bool dense, int w) {
+        return d.seg[g][q].w == w && (d.seg[g][q].Z != nullptr) == dense && (dense || d.seg[g][q].k <= 32);
+    };
+    const void *fn = (const void *)tc2_reduce_kernel<0, 0, 0, 0>;
+    if (d.G == 1 && d.nseg[0] == 2 && d.N == 64 && is_seg(0, 0, true, 64) && is_seg(0, 1, false, 64))
+        fn = (const void *)tc2_reduce_kernel<1, 64, 64, 64>;
+    else if (d.G == 2 && d.nseg[0] == 1 && d.nseg[1] == 1 && d.N == 128 && is_seg(0, 0, true, 128) &&
+             is_seg(1, 0, false, 128))
+        fn = (const void *)tc2_reduce_kernel<2, 128, 128, 128>;
+    else if (d.G == 1 && d.nseg[0] == 1 && d.N == 64 && is_seg(0, 0, true, 64))
+        fn = (const void *)tc2_reduce_kernel<1, 64, 0, 64>;
+    else if (d.G == 1 && d.nseg[0] == 1 && d.N == 128 && is_seg(0, 0, true, 128))
+        fn = (const void *)tc2_reduce_kernel<1, 128, 0, 128>;
+    ensure_smem(fn, smem);
+    {
+        void *args[] = {(void *)&a};
+        DR_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(kRedThreads), args, smem, s));
+    }
     note_launch("tc2_reduce");
+    if (a.dbg) {
+        unsigned long long h[148 * 16];
+        DR_CUDA(cudaStreamSynchronize(s));
+        DR_CUDA(cudaMemcpy(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost));
+        double t[16] = {0};
+        for (int b = 0; b < grid; ++b)
+            for (int q = 0; q < 16; ++q) t[q] += (double)h[b * 16 + q] / grid;
+        fprintf(stderr,
+                "[tc2_reduce n=%lld N=%d G=%d SA=%d stage=%u rows/cta=%lld] kcycles/CTA: total %.1f | "
+                "prod wait empty %.1f | mma wait conv %.1f | conv wait full %.1f work %.1f\n",
+                (long long)d.n, a.N, a.G, a.SA, a.stage_bytes, (long long)a.rows_per_cta, t[8] / 1e3,
+                t[0] / 1e3, t[1] / 1e3, t[2] / 1e3, t[3] / 1e3);
+    }
     const int64_t stride = (int64_t)d.G * kTile * d.N + d.N;
     tc2_reduce_parts_kernel<<<(unsigned)((stride + 31) / 32), dim3(32, 8), 0, s>>>(work, (int)grid,
                                                                                    d.G, d.N, o);
