@@ -108,6 +108,10 @@ typedef struct {
     int32_t max_deg_dst[3], max_deg_src[3];
     int32_t hub_rows_dst[3], hub_rows_src[2];    /* rows routed to the CTA-per-row kernels */
     size_t device_bytes;
+    /* tensor-core tiled SpMM (near only, unit weights, mean degree >= 8): tiles of
+     * <= 128 rows and 64-id halo chunks of the CSR / CSC form; 0 => SIMT kernels */
+    int32_t tiles[3], tiles_T[3];
+    int64_t chunks[3], chunks_T[3];
 } dr_graph_info_t;
 dr_status dr_graph_info(const dr_graph *g, dr_graph_info_t *info);
 

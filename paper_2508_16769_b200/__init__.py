@@ -114,7 +114,8 @@ class Graph:
         return dict(n_cell=i.n_cell, n_net=i.n_net, nnz=list(i.nnz),
                     max_deg_dst=list(i.max_deg_dst), max_deg_src=list(i.max_deg_src),
                     hub_rows_dst=list(i.hub_rows_dst), hub_rows_src=list(i.hub_rows_src),
-                    device_bytes=int(i.device_bytes))
+                    device_bytes=int(i.device_bytes), tiles=list(i.tiles),
+                    tiles_T=list(i.tiles_T), chunks=list(i.chunks), chunks_T=list(i.chunks_T))
 
     def close(self):
         if getattr(self, "handle", None):

@@ -42,7 +42,8 @@ class dr_graph_info_t(C.Structure):
     _fields_ = [("n_cell", C.c_int32), ("n_net", C.c_int32), ("nnz", C.c_int64 * 3),
                 ("max_deg_dst", C.c_int32 * 3), ("max_deg_src", C.c_int32 * 3),
                 ("hub_rows_dst", C.c_int32 * 3), ("hub_rows_src", C.c_int32 * 2),
-                ("device_bytes", C.c_size_t)]
+                ("device_bytes", C.c_size_t), ("tiles", C.c_int32 * 3), ("tiles_T", C.c_int32 * 3),
+                ("chunks", C.c_int64 * 3), ("chunks_T", C.c_int64 * 3)]
 
 
 class dr_cbsr(C.Structure):

@@ -111,6 +111,111 @@ std::vector<int64_t> bfs_rank(int32_t n, const std::vector<int32_t> &rp,
     return rank;
 }
 
+// Host form of a TileSet (see dr_internal.h).
+struct HostTiles {
+    std::vector<int32_t> rows, chunk_beg, halo, eptr;
+    std::vector<uint16_t> cedge;
+    std::vector<int32_t> cta_beg;
+    int32_t n_tiles = 0, grid = 0;
+    int64_t n_chunks = 0;
+};
+
+// Tiles of <= 128 rows of a square relation (rp, col over n rows), grown as BFS
+// balls over the relation from the lowest-ranked unassigned row (rank = the
+// locality order), so a tile is a compact neighbourhood and its halo small;
+// then per tile the sorted distinct column ids (the halo, padded to 64-id
+// chunks with -1) and, per chunk, its edges as (m << 6 | u).
+void build_tiles(int32_t n, const std::vector<int32_t> &rp, const std::vector<int32_t> &col,
+                 const std::vector<int64_t> &rank, HostTiles &T) {
+    std::vector<int32_t> seq((size_t)n);
+    if (rank.empty()) std::iota(seq.begin(), seq.end(), 0);
+    else
+        for (int32_t i = 0; i < n; ++i) seq[(size_t)rank[i]] = i;
+    std::vector<char> assigned((size_t)n, 0);
+    std::vector<int32_t> queue;
+    queue.reserve(kTsRows * 8);
+    std::vector<int32_t> local((size_t)n, -1);
+    std::vector<int32_t> tile, hl, cnt;
+    T.chunk_beg.push_back(0);
+    T.eptr.push_back(0);
+    T.cedge.reserve(col.size());
+    size_t pos = 0;
+    while (true) {
+        while (pos < (size_t)n && assigned[seq[pos]]) ++pos;
+        if (pos >= (size_t)n) break;
+        tile.clear();
+        queue.clear();
+        const int32_t s0 = seq[pos];
+        assigned[s0] = 1;
+        tile.push_back(s0);
+        queue.push_back(s0);
+        for (size_t qh = 0; qh < queue.size() && (int)tile.size() < kTsRows; ++qh) {
+            const int32_t u = queue[qh];
+            for (int32_t e = rp[u]; e < rp[u + 1] && (int)tile.size() < kTsRows; ++e) {
+                const int32_t v = col[e];
+                if (!assigned[v]) {
+                    assigned[v] = 1;
+                    tile.push_back(v);
+                    queue.push_back(v);
+                }
+            }
+        }
+        // halo: sorted distinct columns of the tile's rows
+        hl.clear();
+        for (int32_t i : tile)
+            for (int32_t e = rp[i]; e < rp[i + 1]; ++e)
+                if (local[col[e]] < 0) {
+                    local[col[e]] = 0;
+                    hl.push_back(col[e]);
+                }
+        std::sort(hl.begin(), hl.end());
+        for (size_t u = 0; u < hl.size(); ++u) local[hl[u]] = (int32_t)u;
+        const int64_t nch = std::max<int64_t>(1, ((int64_t)hl.size() + kTsChunk - 1) / kTsChunk);
+        for (int m = 0; m < kTsRows; ++m) T.rows.push_back(m < (int)tile.size() ? tile[m] : -1);
+        for (int64_t u = 0; u < nch * kTsChunk; ++u)
+            T.halo.push_back(u < (int64_t)hl.size() ? hl[(size_t)u] : -1);
+        // edges bucketed by chunk (counting sort), row-major inside a chunk
+        cnt.assign((size_t)nch + 1, 0);
+        for (int32_t i : tile)
+            for (int32_t e = rp[i]; e < rp[i + 1]; ++e) cnt[local[col[e]] / kTsChunk + 1]++;
+        // each chunk's list is padded to a multiple of 8 entries (16 B, for the
+        // converters' 16-B async copies) with 0xFFFF (row slot 1023: skipped)
+        for (int64_t q = 1; q <= nch; ++q) cnt[q] = (cnt[q] + 7) & ~7;
+        for (int64_t q = 0; q < nch; ++q) cnt[q + 1] += cnt[q];
+        const size_t base = T.cedge.size();
+        T.cedge.resize(base + (size_t)cnt[nch], (uint16_t)0xFFFF);
+        std::vector<int32_t> cur(cnt.begin(), cnt.end() - 1);
+        for (int m = 0; m < (int)tile.size(); ++m) {
+            const int32_t i = tile[m];
+            for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
+                const int32_t u = local[col[e]];
+                // stored as the halfword index of A[m][u] in the K-major SW128 bf16
+                // tile the converters build (16-B chunk (u/8) ^ (m%8) of row m)
+                const int uu = u % kTsChunk;
+                const int off = m * 128 + ((((uu >> 3) ^ (m & 7)) & 7) << 4) + ((uu & 7) << 1);
+                T.cedge[base + cur[u / kTsChunk]++] = (uint16_t)(off >> 1);
+            }
+        }
+        for (int64_t q = 0; q < nch; ++q) T.eptr.push_back((int32_t)(base + cnt[q + 1]));
+        for (int32_t h : hl) local[h] = -1;
+        T.n_chunks += nch;
+        T.chunk_beg.push_back((int32_t)T.n_chunks);
+        ++T.n_tiles;
+    }
+    // persistent-kernel work split: CTA b takes the tiles whose first chunk lies in
+    // [b C / grid, (b+1) C / grid) -- contiguous (neighbouring balls share halo
+    // rows in L2) and balanced by chunk count
+    T.grid = std::min<int32_t>(T.n_tiles, 148);
+    T.cta_beg.assign((size_t)T.grid + 1, T.n_tiles);
+    int32_t t = 0;
+    for (int32_t b = 0; b < T.grid; ++b) {
+        const int64_t c0 = T.n_chunks * b / T.grid;
+        while (t < T.n_tiles && T.chunk_beg[t] < c0) ++t;
+        T.cta_beg[b] = t;
+    }
+    T.cta_beg[0] = 0;
+}
+
 void build_rel(const dr_rel_desc &d, bool validate, HostRel &h) {
     h.n_dst = d.n_dst;
     h.n_src = d.n_src;
@@ -305,6 +410,19 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
             }
         }
         const int wdeg = warp_row_threshold();
+        // tiled form of near for the tensor-core SpMM (tspmm.cu): unit weights,
+        // dense enough neighbourhoods (mean degree >= 8); DR_TILES=0 disables
+        HostTiles tl, tlT;
+        const char *tenv = getenv("DR_TILES");
+        const HostRel &hn = h[DR_NEAR];
+        const bool want_tiles = !identity && !(tenv && atoi(tenv) == 0) && hn.ew.empty() &&
+                                hn.ewT.empty() && hn.n_dst > 0 && hn.nnz >= 8LL * hn.n_dst;
+        std::thread tile_th;
+        if (want_tiles)
+            tile_th = std::thread([&] {
+                build_tiles(hn.n_dst, hn.rowptr, hn.col, rank_c, tl);
+                if (!near_sym) build_tiles(hn.n_src, hn.colptr, hn.row, rank_c, tlT);
+            });
         {
             const std::vector<int64_t> *dst_loc[3] = {&rank_c, &rank_n, &rank_c};
             const std::vector<int64_t> *src_loc[3] = {&rank_c, &rank_c, &rank_n};
@@ -326,6 +444,7 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
         int32_t hub_c = 0, hub_n = 0, warp_c = 0, warp_n = 0;
         make_order(degc, identity, rank_c, wdeg, ord_c, hub_c, warp_c);
         make_order(degn, identity, rank_n, wdeg, ord_n, hub_n, warp_n);
+        if (tile_th.joinable()) tile_th.join();
 
         // ---- phase 2: one device block, carved per array
         g = new dr_graph();
@@ -380,6 +499,21 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
                 plan(r, (void **)&d.row, hr.row.data(), hr.row.size() * 4);
             }
         }
+        auto plan_tiles = [&](TileSet &ts, HostTiles &ht) {
+            ts.n_tiles = ht.n_tiles;
+            ts.n_chunks = ht.n_chunks;
+            plan(0, (void **)&ts.rows, ht.rows.data(), ht.rows.size() * 4);
+            plan(0, (void **)&ts.chunk_beg, ht.chunk_beg.data(), ht.chunk_beg.size() * 4);
+            plan(0, (void **)&ts.halo, ht.halo.data(), ht.halo.size() * 4);
+            plan(0, (void **)&ts.eptr, ht.eptr.data(), ht.eptr.size() * 4);
+            plan(0, (void **)&ts.cedge, ht.cedge.data(), ht.cedge.size() * 2);
+            ts.grid = ht.grid;
+            plan(0, (void **)&ts.cta_beg, ht.cta_beg.data(), ht.cta_beg.size() * 4);
+        };
+        if (want_tiles) {
+            plan_tiles(g->rel[DR_NEAR].tiles, tl);
+            if (!near_sym) plan_tiles(g->rel[DR_NEAR].tilesT, tlT);
+        }
         g->src_cell.n = n_cell;
         g->src_cell.n_hub = hub_c;
         g->src_cell.n_warp = warp_c;
@@ -399,6 +533,7 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
             }
         // structural sharing (no second copy): CSC(near) = CSR(near) when symmetric;
         // CSC(pins) = CSR(pinned) and CSC(pinned) = CSR(pins) when pinned == pins^T.
+        if (want_tiles && near_sym) g->rel[DR_NEAR].tilesT = g->rel[DR_NEAR].tiles;
         if (near_sym) {
             g->rel[DR_NEAR].colptr = g->rel[DR_NEAR].rowptr;
             g->rel[DR_NEAR].row = g->rel[DR_NEAR].col;
@@ -468,6 +603,10 @@ extern "C" dr_status dr_graph_info(const dr_graph *g, dr_graph_info_t *info) {
         info->max_deg_dst[r] = g->rel[r].max_deg_dst;
         info->max_deg_src[r] = g->rel[r].max_deg_src;
         info->hub_rows_dst[r] = g->rel[r].fwd.n_hub;
+        info->tiles[r] = g->rel[r].tiles.n_tiles;
+        info->tiles_T[r] = g->rel[r].tilesT.n_tiles;
+        info->chunks[r] = g->rel[r].tiles.n_chunks;
+        info->chunks_T[r] = g->rel[r].tilesT.n_chunks;
     }
     info->hub_rows_src[0] = g->src_cell.n_hub;
     info->hub_rows_src[1] = g->src_net.n_hub;

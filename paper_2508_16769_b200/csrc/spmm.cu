@@ -435,6 +435,10 @@ void ensure_smem(const void *fn, size_t bytes);
 void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
                      float *z, cudaStream_t s) {
     if (r.n_dst <= 0) return;
+    if (!r.ew && tspmm_supported(r.tiles, dim, k)) {      // tensor-core tiled path
+        launch_tspmm_fwd(r, hval, hidx, k, dim, z, s);
+        return;
+    }
     const int P = choose_P(k, dim);
     DR_CHECK(P > 0, DR_ERR_BAD_K, "spmm_fwd: unsupported k");
     FwdArgs a{};
@@ -492,6 +496,12 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, c
                      const uint8_t *hidx, int k, int dim, float *g_kept, float *dx,
                      bool accumulate, cudaStream_t s) {
     if (n_src <= 0) return;
+    if (t0.rel && !t0.rel->ewT && !accumulate && tspmm_supported(t0.rel->tilesT, dim, k) &&
+        t0.rel->n_src == n_src) {                           // tensor-core tiled path
+        launch_tspmm_bwd(*t0.rel, t0.dz, t0.apply_c, t1.rel, t1.dz, t1.apply_c, root, hidx, k,
+                         dim, g_kept, dx, s);
+        return;
+    }
     const int P = choose_P_bwd(k);
     DR_CHECK(P > 0, DR_ERR_BAD_K, "spmm_bwd: unsupported k");
     BwdArgs a{};

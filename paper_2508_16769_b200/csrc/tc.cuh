@@ -95,6 +95,10 @@ __device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc, uint32_
                  "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sdst)), "l"(gsrc)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async4(void *sdst, const void *gsrc, uint32_t bytes) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc),
                  "r"(bytes)

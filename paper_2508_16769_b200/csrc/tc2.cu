@@ -77,6 +77,8 @@ __global__ void tc2_pack_b_kernel(const float *__restrict__ W, int ldw, int K, i
 }
 
 // ================================================================= row GEMM
+#define RDBG_T0 const long long dbg_t0 = a.dbg ? clock64() : 0
+#define RDBG_ADD(slot) do { if (a.dbg) atomicAdd(a.dbg + blockIdx.x * 16 + (slot), (unsigned long long)(clock64() - dbg_t0)); } while (0)
 struct R2Step {
     int8_t g, s, c, bc, first;     // group, segment, chunk in segment, chunk in group image, first of group
 };
@@ -111,6 +113,7 @@ struct R2Args {
     const uint8_t *root_idx;
     int root_k;
     float *root;
+    unsigned long long *dbg;       // DR_TC2_DEBUG role timers, else null
 };
 
 __host__ __device__ __forceinline__ uint32_t rup16(uint32_t x) { return (x + 15u) & ~15u; }
@@ -414,6 +417,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = tmem_slot;
+    const long long kt0 = clock64();
     const int64_t n_tiles = (a.n + kTile - 1) / kTile;
     const int64_t my_tiles = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
@@ -434,7 +438,11 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
             for (int j = 0; j < S; ++j, ++it) {
                 const int slot = (int)(it % SA);
                 const uint32_t u = it / SA;
-                if (u > 0) tc::mbar_wait(&empty[slot], (u - 1) & 1u);
+                if (u > 0) {
+                    RDBG_T0;
+                    tc::mbar_wait(&empty[slot], (u - 1) & 1u);
+                    if (lane == 0) RDBG_ADD(0);
+                }
                 const R2Step sp = a.step[j];
                 rows_produce(a, sp, r0, stages + (size_t)slot * kStage, masks + (size_t)slot * kMaskStage,
                              &full[slot], lane);
@@ -459,12 +467,20 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
             uint32_t it = 0, bt = 0;
             for (int64_t t = 0; t < my_tiles; ++t) {
                 const uint32_t ab = (uint32_t)(t & 1);
-                if (t >= 2) tc::mbar_wait(&acce[ab], (uint32_t)(((t >> 1) - 1) & 1));
+                if (t >= 2) {
+                    RDBG_T0;
+                    tc::mbar_wait(&acce[ab], (uint32_t)(((t >> 1) - 1) & 1));
+                    RDBG_ADD(2);
+                }
                 tc::fence_after();
                 const uint32_t dbase = tmem + ab * GN;
                 for (int j = 0; j < S; ++j, ++it) {
                     const int slot = (int)(it % SA);
-                    tc::mbar_wait(&conv[slot], (it / SA) & 1u);
+                    {
+                        RDBG_T0;
+                        tc::mbar_wait(&conv[slot], (it / SA) & 1u);
+                        RDBG_ADD(1);
+                    }
                     const R2Step sp = a.step[j];
                     int bs;
                     if (a.b_resident) {
@@ -508,9 +524,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
             const int64_t r0 = ((int64_t)blockIdx.x + t * gridDim.x) * kTile;
             for (int j = 0; j < S; ++j, ++it) {
                 const int slot = (int)(it % SA);
-                tc::mbar_wait(&full[slot], (it / SA) & 1u);
+                {
+                    RDBG_T0;
+                    tc::mbar_wait(&full[slot], (it / SA) & 1u);
+                    if (ct == 0) RDBG_ADD(3);
+                }
+                RDBG_T0;
                 rows_convert(a, a.step[j], r0, stages + (size_t)slot * kStage,
                              masks + (size_t)slot * kMaskStage, ct);
+                if (ct == 0) RDBG_ADD(4);
                 tc::fence_async_smem();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&conv[slot]);
@@ -524,9 +546,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
         for (int64_t t = 0; t < my_tiles; ++t) {
             const int64_t r0 = ((int64_t)blockIdx.x + t * gridDim.x) * kTile;
             const uint32_t ab = (uint32_t)(t & 1);
-            tc::mbar_wait(&accf[ab], (uint32_t)((t >> 1) & 1));
+            {
+                RDBG_T0;
+                tc::mbar_wait(&accf[ab], (uint32_t)((t >> 1) & 1));
+                if (warp == 6 && lane == 0) RDBG_ADD(5);
+            }
             tc::fence_after();
+            RDBG_T0;
             rows_epilogue(a, tmem + ab * GN, r0, qd, lane, bias_s, stage, sb);
+            if (warp == 6 && lane == 0) RDBG_ADD(6);
             tc::fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&acce[ab]);
@@ -536,6 +564,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
     }
     tc::fence_before();
     __syncthreads();
+    if (a.dbg && tid == 0) atomicAdd(a.dbg + blockIdx.x * 16 + 8, (unsigned long long)(clock64() - kt0));
     if (warp == 1) {
         tc::fence_after();
         tc::tmem_dealloc(tmem, ncols);
@@ -569,8 +598,6 @@ struct RdArgs {
     unsigned long long *dbg;                            // DR_TC2_DEBUG role timers, else null
 };
 
-#define RDBG_T0 const long long dbg_t0 = a.dbg ? clock64() : 0
-#define RDBG_ADD(slot) do { if (a.dbg) atomicAdd(a.dbg + blockIdx.x * 16 + (slot), (unsigned long long)(clock64() - dbg_t0)); } while (0)
 
 constexpr int kRRows = 64;     // graph rows per reduce step (= MMA K of 4 kind::f16 steps)
 
@@ -1080,6 +1107,7 @@ __global__ void tc2_reduce_parts_kernel(const float *__restrict__ part, int npar
     const int64_t e = (int64_t)blockIdx.x * 32 + threadIdx.x;
     float acc = 0.f;
     if (e < len)
+#pragma unroll 8
         for (int c = threadIdx.y; c < nparts; c += 8) acc += __ldg(part + (int64_t)c * len + e);
     red[threadIdx.y][threadIdx.x] = acc;
     __syncthreads();
@@ -1240,8 +1268,29 @@ void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
     const int64_t grid = tiles < 148 ? tiles : 148;
     ProfScope ps(d.epi == kEpi2Dz ? "tc_dz" : "tc_proj", s);
     ensure_smem((const void *)tc2_rows_kernel, smem);
+    static unsigned long long *dbg_buf = nullptr;
+    const char *dbe = getenv("DR_TC2_DEBUG");
+    if (dbe && atoi(dbe)) {
+        if (!dbg_buf) DR_CUDA(cudaMalloc(&dbg_buf, 148 * 16 * 8));
+        DR_CUDA(cudaMemsetAsync(dbg_buf, 0, 148 * 16 * 8, s));
+        a.dbg = dbg_buf;
+    }
     tc2_rows_kernel<<<(unsigned)grid, kRowsThreads, smem, s>>>(a);
     note_launch("tc2_rows");
+    if (a.dbg) {
+        unsigned long long h[148 * 16];
+        DR_CUDA(cudaStreamSynchronize(s));
+        DR_CUDA(cudaMemcpy(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost));
+        double t[16] = {0};
+        for (int b = 0; b < grid; ++b)
+            for (int q = 0; q < 16; ++q) t[q] += (double)h[b * 16 + q] / grid;
+        fprintf(stderr,
+                "[tc2_rows n=%lld N=%d G=%d S=%d SA=%d SB=%d res=%d epi=%d] kcycles/CTA: total %.1f | "
+                "prod wait %.1f | mma wait conv %.1f acc %.1f | conv wait %.1f work %.1f | epi wait "
+                "%.1f work %.1f\n",
+                (long long)d.n, a.N, a.G, a.S, a.SA, a.SB, a.b_resident, a.epi, t[8] / 1e3,
+                t[0] / 1e3, t[1] / 1e3, t[2] / 1e3, t[3] / 1e3, t[4] / 1e3, t[5] / 1e3, t[6] / 1e3);
+    }
 }
 
 // stage layout of the reduce kernel: [A'_g 32 KB each][B' 256 N][CBSR raw][mask words]

@@ -8,6 +8,7 @@ namespace {
 
 constexpr int kHeadBlocks = 296;
 constexpr int kHeadThreads = 256;
+constexpr int kHeadU = 4;          // rows in flight per warp
 
 __global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a, float inv_n) {
     __shared__ float wpart[kHeadThreads / 32][256 + 2];
@@ -23,26 +24,47 @@ __global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a, float in
     const float b = __ldg(a.b);
     float accb = 0.f, accl = 0.f;
     const int64_t nw = (int64_t)gridDim.x * (kHeadThreads / 32);
-    for (int64_t j = (int64_t)blockIdx.x * (kHeadThreads / 32) + wid; j < a.n; j += nw) {
-        float y[8], p = 0.f;
+    // kHeadU rows per warp iteration, all loads issued before the reductions
+    // (the row loop is latency-bound otherwise: one dependent shuffle chain per row)
+    for (int64_t j0 = ((int64_t)blockIdx.x * (kHeadThreads / 32) + wid) * kHeadU; j0 < a.n;
+         j0 += nw * kHeadU) {
+        float y[kHeadU][8], p[kHeadU], lab[kHeadU];
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
-            const int o = lane + 32 * s;
-            y[s] = o < N ? __ldg(a.y + j * N + o) : 0.f;
-            p += y[s] * w[s];
+        for (int u = 0; u < kHeadU; ++u) {
+            const int64_t j = j0 + u;
+            const bool ok = j < a.n;
+            lab[u] = ok ? __ldg(a.labels + j) : 0.f;
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+                const int o = lane + 32 * s;
+                y[u][s] = (ok && o < N) ? __ldg(a.y + j * N + o) : 0.f;
+            }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-        const float r = p + b - __ldg(a.labels + j);
-        const float dp = 2.0f * r * inv_n;
+        for (int u = 0; u < kHeadU; ++u) {
+            p[u] = 0.f;
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
-            const int o = lane + 32 * s;
-            if (o < N) a.dy[j * N + o] = dp * w[s];
-            accw[s] += y[s] * dp;
+            for (int s = 0; s < 8; ++s) p[u] += y[u][s] * w[s];
         }
-        accb += dp;
-        accl += r * r;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < kHeadU; ++u) p[u] += __shfl_xor_sync(0xffffffffu, p[u], o);
+#pragma unroll
+        for (int u = 0; u < kHeadU; ++u) {
+            const int64_t j = j0 + u;
+            if (j >= a.n) break;
+            const float r = p[u] + b - lab[u];
+            const float dp = 2.0f * r * inv_n;
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+                const int o = lane + 32 * s;
+                if (o < N) a.dy[j * N + o] = dp * w[s];
+                accw[s] += y[u][s] * dp;
+            }
+            accb += dp;
+            accl += r * r;
+        }
     }
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
@@ -61,15 +83,22 @@ __global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a, float in
     }
 }
 
+// One warp per output element: lanes take every 32nd block partial, then a
+// fixed butterfly (deterministic; a single-thread loop over 296 dependent loads
+// was latency-bound).
 __global__ void head_reduce_kernel(HeadArgs a, float inv_n) {
-    const int N = a.N;
-    for (int e = threadIdx.x; e < N + 2; e += blockDim.x) {
-        float s = 0.f;
-        for (int q = 0; q < kHeadBlocks; ++q) s += a.work[(int64_t)q * (N + 2) + e];
-        if (e < N) a.grad_w[e] = s;
-        else if (e == N) a.grad_b[0] = s;
-        else a.loss[0] = s * inv_n;
-    }
+    const int N = a.N, lane = threadIdx.x & 31;
+    const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (e >= N + 2) return;
+    float s = 0.f;
+#pragma unroll
+    for (int q = lane; q < kHeadBlocks; q += 32) s += a.work[(int64_t)q * (N + 2) + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane) return;
+    if (e < N) a.grad_w[e] = s;
+    else if (e == N) a.grad_b[0] = s;
+    else a.loss[0] = s * inv_n;
 }
 
 // Adam step counter lives on the device (so a captured CUDA graph of the whole
@@ -112,7 +141,7 @@ void launch_head_mse(const HeadArgs &a, cudaStream_t s) {
     ProfScope ps("head_mse", s);
     head_kernel<<<kHeadBlocks, kHeadThreads, 0, s>>>(a, inv_n);
     note_launch("head_mse");
-    head_reduce_kernel<<<1, 256, 0, s>>>(a, inv_n);
+    head_reduce_kernel<<<(unsigned)((a.N + 2 + 7) / 8), 256, 0, s>>>(a, inv_n);
     note_launch("head_reduce");
 }
 

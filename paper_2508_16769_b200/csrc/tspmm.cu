@@ -1,0 +1,734 @@
+// tspmm.cu — tiled DR-SpMM forward (Alg. 1, Eq. 5-7) and SSpMM backward (Alg. 2,
+// Eq. 10-11) of a square unit-weight relation (near) on the tcgen05 tensor cores.
+//
+// The relation is cut into tiles of <= 128 rows with compact neighbourhoods
+// (TileSet, graph.cpp). For a tile T with halo H (the distinct ids its rows
+// touch), the aggregation of all its rows is one dense product
+//     forward : Z_T  = diag(c_T)  Adj[T x H] densify(H_src[H])      (Eq. 5)
+//     backward: G_T  = diag(s_T)  Adj^T[T x H] dZ'[H]               (Eq. 10)
+// with the 0/1 adjacency tile as the A operand (exact in bf16) and the halo's
+// feature rows as the B operand, split x = hi + lo in bf16 (|x - hi - lo| <=
+// 2^-17 |x|; two kind::f16 MMAs per K step, fp32 accumulation in TMEM). The
+// backward then samples G at the source row's own CBSR indices (the D-ReLU mask
+// gradient, Eq. 11), adds the second relation of the source type (pins) and the
+// Sage root term, and writes the dense dX row. Every halo row is read once per
+// tile (compulsory bytes) instead of once per edge, and the per-edge work moves
+// from the L1/shared-memory scatter pipes to the tensor cores.
+//
+// Roles (one persistent CTA per SM, 14 warps; CTA b owns a contiguous range of
+// tiles balanced by chunk count, TileSet::cta_beg):
+//   warp 0     producer  (backward): bulk copies (TMA engine) of the chunk's 64
+//                         dZ' halo rows into the stage;
+//   warps 2-9  converters: zero + scatter the 0/1 adjacency chunk [128 x 64];
+//                         forward: densify the halo's CBSR rows straight into the
+//                         K-major hi/lo B tiles; backward: transposing hi/lo split
+//                         of the landed dZ' rows (in place). Their global reads
+//                         are cp.async copies into side slots two chunks ahead;
+//   warp 1     MMA      : one thread, 2 MMAs per K = 16 step into a double-
+//                         buffered TMEM accumulator;
+//   warps 10-13 epilogue: TMEM -> registers (lane = tile row) -> a per-warp
+//                         [32 rows x 32 cols] staging tile -> 128-bit coalesced
+//                         row stores (4 rows x 128 B per instruction).
+// Fixed summation order everywhere: deterministic, no atomics (reading Q23).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "dr_internal.h"
+#include "tc.cuh"
+
+namespace dr {
+
+void ensure_smem(const void *fn, size_t bytes);
+
+namespace {
+
+constexpr int kThreads = 448;
+constexpr int kConv = 256;                     // converter threads (warps 2-9)
+constexpr int kEpiWarp0 = 10;
+constexpr int kMaxSA = 4;
+constexpr int kStg = 36;                       // epilogue staging row stride (floats, 144 B)
+constexpr uint32_t kATile = 16384;             // 128 x 64 bf16
+constexpr uint32_t kEpiWarpBytes = 32 * kStg * 4 + 32 * 32 + 2 * 32 * 4 * 4;   // staging, ids, nets, weights
+constexpr uint32_t kStgBytes = 4 * kEpiWarpBytes;
+constexpr uint16_t kBf16One = 0x3F80;
+
+struct TsArgs {
+    const int32_t *rows, *chunk_beg, *halo, *eptr, *cta_beg;
+    const uint16_t *cedge;
+    int k, SA;
+    uint32_t stage_bytes, side_bytes;
+    // forward: CBSR of the halo (source) rows, per-row output scale, output
+    const float *hval;
+    const uint8_t *hidx;
+    const float *c;
+    float *z;
+    // backward: dZ' rows of the halo (destinations), optional per-halo-row scale
+    // (standalone ABI: dz not yet row-scaled), s_j of the tiled relation, and an
+    // optional second relation term for the same source type (pins CSC)
+    const float *dz, *dzc, *s;
+    const int32_t *p_colptr, *p_row;
+    const float *p_ewT, *p_s, *p_c, *p_dz;
+    const float *root;
+    float *dx, *g_kept;
+    unsigned long long *dbg;          // DR_TS_DEBUG role timers (cycles per CTA), else null
+};
+
+// mbarrier wait with a short sleep between probes: for the roles that are not
+// on the critical path (MMA issuer, epilogue, producer), so their polling does
+// not take issue slots from the converter warps sharing their SM sub-partition
+__device__ __forceinline__ void wait_sleep(uint64_t *bar, uint32_t phase) {
+    while (!tc::mbar_try_wait(bar, phase)) __nanosleep(64);
+}
+
+#define TDBG_T0 const long long dbg_t0 = a.dbg ? clock64() : 0
+#define TDBG_ADD(slot) do { if (a.dbg) atomicAdd(a.dbg + blockIdx.x * 16 + (slot), (unsigned long long)(clock64() - dbg_t0)); } while (0)
+
+// ---- transposing split unit (backward B operand): feature quad fq x row octet j
+struct Unit {
+    int fq, j;
+    bool ok;
+};
+template <int D>
+__device__ __forceinline__ Unit unit_of(int ct) {
+    constexpr int W4 = D / 4, fh = (W4 + 7) / 8;
+    const int i = ct & 7, gq = (ct >> 3) & 3, rest = ct >> 5;
+    Unit x;
+    x.fq = i + 8 * (rest % fh);
+    x.j = gq + 4 * (rest / fh);
+    x.ok = x.fq < W4 && x.j < 8;
+    return x;
+}
+__device__ __forceinline__ void store_col8(uint8_t *B, uint32_t lo_off, int f, int j, const float *a) {
+    uint4 h, l;
+    tc::split_bf16x2(a[0], a[1], h.x, l.x);
+    tc::split_bf16x2(a[2], a[3], h.y, l.y);
+    tc::split_bf16x2(a[4], a[5], h.z, l.z);
+    tc::split_bf16x2(a[6], a[7], h.w, l.w);
+    const uint32_t off = tc::sw128_off_h((uint32_t)f, (uint32_t)(8 * j));
+    *reinterpret_cast<uint4 *>(B + off) = h;
+    *reinterpret_cast<uint4 *>(B + lo_off + off) = l;
+}
+
+// ---- converter side buffers
+// The converters' global reads for chunk ch are 16/8/4-B async copies
+// (cp.async) into a side slot issued two chunks ahead: the chunk's adjacency
+// entries (padded to 16 B per chunk at graph creation) and, forward, the CBSR
+// rows of its 64 halo ids (thread ct copies its quarter u = ct / 4, h = ct % 4).
+// Addresses (eptr, halo ids) are loaded into registers three chunks ahead.
+constexpr int kSideSlots = 3;
+constexpr int kSideE = 2048;                   // adjacency entries per slot (4 KB), forward
+constexpr int kSideEB = 2048;                  // backward
+struct CInfo {
+    int e0, e1;      // adjacency entries [e0, e1) of the chunk
+    int id;          // forward: halo id of row u = ct / 4
+    int h0, h1;      // backward: halo ids of rows lane, lane + 32 (valid-row count)
+};
+template <bool BWD>
+__device__ __forceinline__ void info_load(const TsArgs &a, int64_t ch, int ct, CInfo &p) {
+    p.e0 = __ldg(a.eptr + ch);
+    p.e1 = __ldg(a.eptr + ch + 1);
+    if constexpr (!BWD) {
+        p.id = __ldg(a.halo + ch * kTsChunk + (ct >> 2));
+    } else {
+        p.h0 = __ldg(a.halo + ch * kTsChunk + (ct & 31));
+        p.h1 = __ldg(a.halo + ch * kTsChunk + 32 + (ct & 31));
+    }
+}
+template <bool BWD, int QH>
+__device__ __forceinline__ void side_issue(const TsArgs &a, const CInfo &p, uint8_t *sd, int ct) {
+    constexpr int SE = BWD ? kSideEB : kSideE;
+    const int n = min(p.e1 - p.e0, SE);
+    if (8 * ct < n) tc::cp_async16(sd + 16 * ct, a.cedge + p.e0 + 8 * ct, 16);
+    if constexpr (!BWD) {
+        if (p.id >= 0) {
+            constexpr int K = 4 * QH;
+            const int u = ct >> 2, h = ct & 3;
+            uint8_t *sv = sd + 2 * kSideE + u * K * 4 + h * QH * 4;
+            const float *gv = a.hval + (int64_t)p.id * K + h * QH;
+            if constexpr (QH == 8) {
+                tc::cp_async16(sv, gv, 16);
+                tc::cp_async16(sv + 16, gv + 4, 16);
+            } else if constexpr (QH == 4) {
+                tc::cp_async16(sv, gv, 16);
+            } else if constexpr (QH == 2) {
+                tc::cp_async8(sv, gv);
+            } else {
+                tc::cp_async4(sv, gv, 4);
+            }
+            if (h == 0) {
+                uint8_t *si = sd + 2 * kSideE + 64 * K * 4 + u * K;
+                const uint8_t *gi = a.hidx + (int64_t)p.id * K;
+                if constexpr (QH == 8) {
+                    tc::cp_async16(si, gi, 16);
+                    tc::cp_async16(si + 16, gi + 16, 16);
+                } else if constexpr (QH == 4) {
+                    tc::cp_async16(si, gi, 16);
+                } else if constexpr (QH == 2) {
+                    tc::cp_async8(si, gi);
+                } else {
+                    tc::cp_async4(si, gi, 4);
+                }
+            }
+        }
+    }
+}
+
+// Zero the [128 x 64] A tile (256 converter threads).
+__device__ __forceinline__ void zero_a(uint8_t *A, int ct) {
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) reinterpret_cast<uint4 *>(A)[ct + kConv * i] = z;
+}
+__device__ __forceinline__ void put_edge(uint8_t *A, uint32_t v) {   // v = halfword offset
+    if (v != 0xFFFFu) reinterpret_cast<uint16_t *>(A)[v] = kBf16One;
+}
+// edges of the chunk -> 1.0 at A[m][u]: 8 entries per thread from the side slot,
+// any beyond kSideE straight from global
+template <int SE>
+__device__ __forceinline__ void scatter_edges(const TsArgs &a, const CInfo &p, const uint8_t *sd,
+                                              uint8_t *A, int ct) {
+    const int n = p.e1 - p.e0;
+    if (8 * ct < min(n, SE)) {
+        const uint4 w = *reinterpret_cast<const uint4 *>(sd + 16 * ct);
+        put_edge(A, w.x & 0xffffu); put_edge(A, w.x >> 16);
+        put_edge(A, w.y & 0xffffu); put_edge(A, w.y >> 16);
+        put_edge(A, w.z & 0xffffu); put_edge(A, w.z >> 16);
+        put_edge(A, w.w & 0xffffu); put_edge(A, w.w >> 16);
+    }
+    for (int e = SE + ct; e < n; e += kConv) put_edge(A, __ldg(a.cedge + p.e0 + e));
+}
+
+template <int D, int QH>
+__device__ __forceinline__ void convert_fwd(const TsArgs &a, const CInfo &p, const uint8_t *sd,
+                                            uint8_t *st, int ct, int ch, int cb) {
+    uint8_t *A = st, *B = st + kATile;
+    constexpr uint32_t lo = (uint32_t)D * 128u;
+    constexpr int K = 4 * QH;
+    zero_a(A, ct);
+    {
+        const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int i = 0; i < (2 * D * 128) / (16 * kConv); ++i)
+            reinterpret_cast<uint4 *>(B)[ct + kConv * i] = z;
+    }
+    tc::cp_async_wait<1>();                 // this chunk's side copies (ch + 1's may fly)
+    tc::named_bar(1, kConv);                // zeros + everyone's side data
+    scatter_edges<kSideE>(a, p, sd, A, ct);
+    if (p.id >= 0) {
+        const int u = ct >> 2, h = ct & 3;
+        const float *sv = reinterpret_cast<const float *>(sd + 2 * kSideE) + u * K + h * QH;
+        const uint8_t *si = sd + 2 * kSideE + 64 * K * 4 + u * K + h * QH;
+#pragma unroll
+        for (int q = 0; q < QH; ++q) {
+            uint32_t hh, ll;
+            tc::split_bf16x2(sv[q], 0.f, hh, ll);
+            const uint32_t off = tc::sw128_off_h(si[q], (uint32_t)u);
+            *reinterpret_cast<uint16_t *>(B + off) = (uint16_t)(hh & 0xffffu);
+            *reinterpret_cast<uint16_t *>(B + lo + off) = (uint16_t)(ll & 0xffffu);
+        }
+    }
+}
+
+template <int D, int QH>
+__device__ __forceinline__ void convert_bwd(const TsArgs &a, const CInfo &p, const uint8_t *sd,
+                                            uint8_t *st, int ct, int64_t ch) {
+    uint8_t *A = st, *B = st + kATile;
+    constexpr uint32_t lo = (uint32_t)D * 128u;
+    // valid rows of the chunk = a prefix (halo padding sits at the end of a tile)
+    const int valid = __popc(__ballot_sync(0xffffffffu, p.h0 >= 0)) +
+                      __popc(__ballot_sync(0xffffffffu, p.h1 >= 0));
+    const float4 *raw = reinterpret_cast<const float4 *>(B);
+    const Unit x = unit_of<D>(ct);
+    float4 vv[8];
+    if (x.ok) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int rr = 8 * x.j + r;
+            float4 q = rr < valid ? raw[rr * (D / 4) + x.fq] : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (a.dzc && rr < valid) {             // standalone ABI: dz rows not yet scaled
+                const float cs = __ldg(a.dzc + __ldg(a.halo + ch * kTsChunk + rr));
+                q.x *= cs; q.y *= cs; q.z *= cs; q.w *= cs;
+            }
+            vv[r] = q;
+        }
+    }
+    zero_a(A, ct);
+    tc::cp_async_wait<1>();
+    tc::named_bar(1, kConv);                 // raw reads + A zeroing + side data
+    scatter_edges<kSideEB>(a, p, sd, A, ct);
+    if (x.ok) {
+        const int f = 4 * x.fq;
+        float c8[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) c8[r] = vv[r].x;
+        store_col8(B, lo, f + 0, x.j, c8);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) c8[r] = vv[r].y;
+        store_col8(B, lo, f + 1, x.j, c8);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) c8[r] = vv[r].z;
+        store_col8(B, lo, f + 2, x.j, c8);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) c8[r] = vv[r].w;
+        store_col8(B, lo, f + 3, x.j, c8);
+    }
+}
+
+// ---- epilogue helpers (warp quarter qd: tile rows 32 qd + lane; TMEM lanes likewise)
+// TMEM columns [j0, j0+32) of this warp's 32 rows -> staging (row = lane), scaled
+__device__ __forceinline__ void tmem_to_stg(uint32_t taddr, float scale, float *stg, int lane) {
+    uint32_t r0[16], r1[16];
+    tc::tmem_ld16_nw(taddr, r0);
+    tc::tmem_ld16_nw(taddr + 16u, r1);
+    tc::tmem_wait_ld();
+    float4 *o = reinterpret_cast<float4 *>(stg + lane * kStg);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        o[q] = make_float4(scale * __uint_as_float(r0[4 * q]), scale * __uint_as_float(r0[4 * q + 1]),
+                           scale * __uint_as_float(r0[4 * q + 2]), scale * __uint_as_float(r0[4 * q + 3]));
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        o[4 + q] = make_float4(scale * __uint_as_float(r1[4 * q]), scale * __uint_as_float(r1[4 * q + 1]),
+                               scale * __uint_as_float(r1[4 * q + 2]), scale * __uint_as_float(r1[4 * q + 3]));
+}
+// staging [32 rows][32 cols] -> out[rid_r * D + j0 ...]: lane -> (row 4 i + lane / 8,
+// column quad lane % 8): each instruction writes 4 full 128-B row segments
+template <int D>
+__device__ __forceinline__ void stg_to_global(const float *stg, float *out, int rid, int j0, int lane) {
+    const int cq = lane & 7, rs = lane >> 3;
+    float4 v[8];
+    int rr[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int r = 4 * i + rs;
+        rr[i] = __shfl_sync(0xffffffffu, rid, r);
+        v[i] = *reinterpret_cast<const float4 *>(stg + r * kStg + 4 * cq);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        if (rr[i] >= 0) __stcs(reinterpret_cast<float4 *>(out + (int64_t)rr[i] * D + j0) + cq, v[i]);
+}
+
+template <int D>
+__device__ __forceinline__ void epi_fwd(const TsArgs &a, int t, uint32_t tacc, float *stg, int lane) {
+    const int rid = __ldg(a.rows + (int64_t)t * kTsRows + (tacc >> 16) + lane);
+    const float cr = rid >= 0 ? __ldg(a.c + rid) : 0.f;
+#pragma unroll 1
+    for (int j0 = 0; j0 < D; j0 += 32) {
+        tmem_to_stg(tacc + (uint32_t)j0, cr, stg, lane);
+        __syncwarp();
+        stg_to_global<D>(stg, a.z, rid, j0, lane);
+        __syncwarp();
+    }
+}
+
+// Second relation term of the backward (pins CSC of the cell sources, Eq. 10),
+// warp-cooperative: the warp's 32 rows are taken R = 32 / K at a time, K lanes
+// per row (lane t <-> CBSR position t), so one load instruction samples K
+// columns of one dZ' row (a few 128-B lines) instead of 32 rows' worth. The
+// first kNets net ids of every row are staged in shared memory up front (one
+// load round for all rows), so the sampled loads of successive row groups are
+// independent and overlap. Result: psm[r][t] (row r of the warp, position t).
+constexpr int kNets = 4;
+template <int D, int K>
+__device__ __forceinline__ void pins_term_coop(const TsArgs &a, int rid, float *psm,
+                                               const uint8_t *idsm, int *netsm, float *wsm,
+                                               int lane) {
+    int e0 = 0, deg = 0;
+    float ps = 0.f;
+    if (rid >= 0) {
+        e0 = __ldg(a.p_colptr + rid);
+        deg = __ldg(a.p_colptr + rid + 1) - e0;
+        ps = __ldg(a.p_s + rid);
+#pragma unroll
+        for (int j = 0; j < kNets; ++j)
+            if (j < deg) {
+                const int i = __ldg(a.p_row + e0 + j);
+                netsm[lane * kNets + j] = i;
+                float w = a.p_ewT ? __ldg(a.p_ewT + e0 + j) : 1.f;
+                if (a.p_c) w *= __ldg(a.p_c + i);
+                wsm[lane * kNets + j] = w;
+            }
+    }
+    __syncwarp();
+    constexpr int R = 32 / K;
+    const int t = lane % K, sub = lane / K;
+#pragma unroll 4
+    for (int it = 0; it < K; ++it) {
+        const int r = R * it + sub;
+        const int d = __shfl_sync(0xffffffffu, deg, r);
+        const float pr = __shfl_sync(0xffffffffu, ps, r);
+        const int er = __shfl_sync(0xffffffffu, e0, r);
+        const uint32_t id = idsm[r * K + t];
+        float v = 0.f;
+#pragma unroll
+        for (int j = 0; j < kNets; ++j)
+            if (j < d) v += wsm[r * kNets + j] * __ldg(a.p_dz + (int64_t)netsm[r * kNets + j] * D + id);
+        for (int j = kNets; j < d; ++j) {
+            const int i = __ldg(a.p_row + er + j);
+            float w = a.p_ewT ? __ldg(a.p_ewT + er + j) : 1.f;
+            if (a.p_c) w *= __ldg(a.p_c + i);
+            v += w * __ldg(a.p_dz + (int64_t)i * D + id);
+        }
+        psm[r * (K + 1) + t] = pr * v;
+    }
+}
+
+template <int D, int QH>
+__device__ __forceinline__ void epi_bwd(const TsArgs &a, int t, uint32_t tacc, float *stg,
+                                        uint8_t *idsm, int *netsm, float *wsm, int lane,
+                                        uint64_t *accempty) {
+    constexpr int K = 4 * QH;
+    const int rid = __ldg(a.rows + (int64_t)t * kTsRows + (tacc >> 16) + lane);
+    uint32_t idw[K / 4];
+    float g[K];
+    if (rid >= 0) {
+        const uint8_t *ir = a.hidx + (int64_t)rid * K;
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) idw[q] = __ldg(reinterpret_cast<const uint32_t *>(ir) + q);
+    } else {
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) idw[q] = 0;
+    }
+    auto idx = [&](int q) -> uint32_t { return (idw[q >> 2] >> (8 * (q & 3))) & 0xffu; };
+#pragma unroll
+    for (int q = 0; q < K; ++q) g[q] = 0.f;
+    // sample the accumulator row at the row's own CBSR indices
+#pragma unroll 1
+    for (int j0 = 0; j0 < D; j0 += 32) {
+        tmem_to_stg(tacc + (uint32_t)j0, 1.f, stg, lane);
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+            if ((int)(idx(q) >> 5) == (j0 >> 5)) g[q] = stg[lane * kStg + (idx(q) & 31u)];
+        __syncwarp();
+    }
+    // the accumulator buffer is free for the next tile's MMAs
+    tc::fence_before();
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(accempty);
+    const float sj = rid >= 0 ? __ldg(a.s + rid) : 0.f;
+#pragma unroll
+    for (int q = 0; q < K; ++q) g[q] *= sj;
+    if (a.p_colptr) {
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) reinterpret_cast<uint32_t *>(idsm)[lane * (K / 4) + q] = idw[q];
+        __syncwarp();
+        pins_term_coop<D, K>(a, rid, stg, idsm, netsm, wsm, lane);     // psm aliases stg
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < K; ++q) g[q] += stg[lane * (K + 1) + q];
+        __syncwarp();
+    }
+    if (rid >= 0) {
+        if (a.root) {
+#pragma unroll
+            for (int q = 0; q < K; ++q) g[q] += __ldg(a.root + (int64_t)rid * K + q);
+        }
+        if (a.g_kept) {
+#pragma unroll
+            for (int q = 0; q < K; ++q) a.g_kept[(int64_t)rid * K + q] = g[q];
+        }
+    }
+    if (!a.dx) return;
+    // dense dX row: zeros + the K values at their indices, 32 columns at a time
+#pragma unroll 1
+    for (int j0 = 0; j0 < D; j0 += 32) {
+        float4 *o = reinterpret_cast<float4 *>(stg + lane * kStg);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+            if ((int)(idx(q) >> 5) == (j0 >> 5)) stg[lane * kStg + (idx(q) & 31u)] = g[q];
+        __syncwarp();
+        stg_to_global<D>(stg, a.dx, rid, j0, lane);
+        __syncwarp();
+    }
+}
+
+template <bool BWD, int D, int QH>
+__global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constant__ TsArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t full[kMaxSA], conv[kMaxSA], empty[kMaxSA], accfull[2],
+        accempty[2];
+    __shared__ uint32_t tmem_slot;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int SA = a.SA;
+    constexpr uint32_t ncols = 2 * D;          // two accumulators of D fp32 columns
+    if (tid == 0) {
+        for (int i = 0; i < SA; ++i) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&conv[i], kConv / 32);
+            tc::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&accfull[i], 1);
+            tc::mbar_init(&accempty[i], 4);
+        }
+        tc::fence_mbar_init();
+    }
+    if (warp == 1) {
+        tc::tmem_alloc(&tmem_slot, ncols);
+        tc::tmem_relinquish();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_slot;
+    const long long kt0 = clock64();
+    float *stg_all = reinterpret_cast<float *>(sm + (size_t)SA * a.stage_bytes);
+    const int tb = __ldg(a.cta_beg + blockIdx.x), te = __ldg(a.cta_beg + blockIdx.x + 1);
+    const int cb = tb < te ? __ldg(a.chunk_beg + tb) : 0, ce = tb < te ? __ldg(a.chunk_beg + te) : 0;
+
+    if (warp == 0) {
+        if constexpr (BWD) {
+            int nid0 = -1, nid1 = -1;
+            if (cb < ce) {
+                nid0 = __ldg(a.halo + (int64_t)cb * kTsChunk + lane);
+                nid1 = __ldg(a.halo + (int64_t)cb * kTsChunk + 32 + lane);
+            }
+            for (int ch = cb; ch < ce; ++ch) {
+                const int it = ch - cb;
+                const int slot = it % SA;
+                const uint32_t u = (uint32_t)(it / SA);
+                const int id0 = nid0, id1 = nid1;
+                if (ch + 1 < ce) {
+                    nid0 = __ldg(a.halo + (int64_t)(ch + 1) * kTsChunk + lane);
+                    nid1 = __ldg(a.halo + (int64_t)(ch + 1) * kTsChunk + 32 + lane);
+                }
+                if (u > 0) {
+                    TDBG_T0;
+                    wait_sleep(&empty[slot], (u - 1) & 1u);
+                    if (lane == 0) TDBG_ADD(0);
+                }
+                uint64_t *fb = &full[slot];
+                const uint32_t nv = __popc(__ballot_sync(0xffffffffu, id0 >= 0)) +
+                                    __popc(__ballot_sync(0xffffffffu, id1 >= 0));
+                if (lane == 0) tc::mbar_arrive_expect_tx(fb, nv * (uint32_t)D * 4u);
+                __syncwarp();
+                uint8_t *B = sm + (size_t)slot * a.stage_bytes + kATile;
+                if (id0 >= 0) tc::bulk_g2s(B + (size_t)lane * D * 4, a.dz + (int64_t)id0 * D, D * 4, fb);
+                if (id1 >= 0) tc::bulk_g2s(B + (size_t)(32 + lane) * D * 4, a.dz + (int64_t)id1 * D, D * 4, fb);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = tc::idesc_bf16(kTsRows, D);
+            int it = 0;
+            for (int t = tb, lt = 0; t < te; ++t, ++lt) {
+                const int b = lt & 1;
+                if (lt >= 2) {
+                    TDBG_T0;
+                    wait_sleep(&accempty[b], (uint32_t)((lt / 2 - 1) & 1));
+                    TDBG_ADD(2);
+                }
+                tc::fence_after();
+                const uint32_t d = tmem + (uint32_t)(b * D);
+                const int c0 = __ldg(a.chunk_beg + t), c1 = __ldg(a.chunk_beg + t + 1);
+                for (int ch = c0; ch < c1; ++ch, ++it) {
+                    const int slot = it % SA;
+                    {
+                        TDBG_T0;
+                        wait_sleep(&conv[slot], (uint32_t)((it / SA) & 1));
+                        TDBG_ADD(1);
+                    }
+                    tc::fence_after();
+                    const uint32_t sa = tc::smem_u32(sm + (size_t)slot * a.stage_bytes);
+                    const uint32_t sbh = sa + kATile, sbl = sbh + (uint32_t)D * 128u;
+#pragma unroll
+                    for (int ks = 0; ks < kTsChunk / 16; ++ks) {
+                        const uint32_t ko = ks * 32;
+                        const uint64_t ad = tc::desc_sw128(sa + ko);
+                        tc::mma_bf16(d, ad, tc::desc_sw128(sbh + ko), idesc,
+                                     (ch == c0 && ks == 0) ? 0u : 1u);
+                        tc::mma_bf16(d, ad, tc::desc_sw128(sbl + ko), idesc, 1u);
+                    }
+                    tc::mma_commit(&empty[slot]);
+                }
+                tc::mma_commit(&accfull[b]);
+            }
+        }
+        __syncwarp();
+    } else if (warp < kEpiWarp0) {
+        const int ct = tid - 64;
+        uint8_t *side = sm + (size_t)SA * a.stage_bytes + kStgBytes;
+        // info ring: chunk ch, ch + 1, ch + 2 (issued), ch + 3 (loading)
+        CInfo i0{}, i1{}, i2{}, i3{};
+        if (cb < ce) info_load<BWD>(a, cb, ct, i0);
+        if (cb + 1 < ce) info_load<BWD>(a, cb + 1, ct, i1);
+        if (cb + 2 < ce) info_load<BWD>(a, cb + 2, ct, i2);
+        if (cb < ce) side_issue<BWD, QH>(a, i0, side, ct);
+        tc::cp_async_commit();
+        if (cb + 1 < ce) side_issue<BWD, QH>(a, i1, side + a.side_bytes, ct);
+        tc::cp_async_commit();
+        for (int ch = cb; ch < ce; ++ch) {
+            const int it = ch - cb;
+            if (ch + 3 < ce) info_load<BWD>(a, ch + 3, ct, i3);
+            const int slot = it % SA;
+            const uint32_t u = (uint32_t)(it / SA);
+            uint8_t *st = sm + (size_t)slot * a.stage_bytes;
+            const uint8_t *sd = side + (size_t)(it % kSideSlots) * a.side_bytes;
+            {
+                TDBG_T0;
+                if constexpr (BWD) tc::mbar_wait(&full[slot], u & 1u);
+                else if (u > 0) tc::mbar_wait(&empty[slot], (u - 1) & 1u);
+                if (ct == 0) TDBG_ADD(3);
+            }
+            {
+                TDBG_T0;
+                if constexpr (BWD) convert_bwd<D, QH>(a, i0, sd, st, ct, ch);
+                else convert_fwd<D, QH>(a, i0, sd, st, ct, ch, cb);
+                if (ct == 0) TDBG_ADD(4);
+            }
+            // every converter thread is past the barrier inside convert: the slot
+            // read at step it - 1 is free for chunk ch + 2
+            if (ch + 2 < ce)
+                side_issue<BWD, QH>(a, i2, side + (size_t)((it + 2) % kSideSlots) * a.side_bytes, ct);
+            tc::cp_async_commit();
+            tc::fence_async_smem();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&conv[slot]);
+            i0 = i1; i1 = i2; i2 = i3;
+        }
+        tc::cp_async_wait<0>();
+    } else {
+        const int qd = warp & 3;
+        uint8_t *ew = reinterpret_cast<uint8_t *>(stg_all) + (size_t)(warp - kEpiWarp0) * kEpiWarpBytes;
+        float *stg = reinterpret_cast<float *>(ew);
+        uint8_t *idsm = ew + 32 * kStg * 4;
+        int *netsm = reinterpret_cast<int *>(idsm + 32 * 32);
+        float *wsm = reinterpret_cast<float *>(netsm + 32 * 4);
+        for (int t = tb, lt = 0; t < te; ++t, ++lt) {
+            const int b = lt & 1;
+            {
+                TDBG_T0;
+                wait_sleep(&accfull[b], (uint32_t)((lt / 2) & 1));
+                if (warp == kEpiWarp0 && lane == 0) TDBG_ADD(5);
+            }
+            tc::fence_after();
+            TDBG_T0;
+            const uint32_t tacc = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * D);
+            if constexpr (BWD) {
+                epi_bwd<D, QH>(a, t, tacc, stg, idsm, netsm, wsm, lane, &accempty[b]);
+            } else {
+                epi_fwd<D>(a, t, tacc, stg, lane);
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&accempty[b]);
+            }
+            if (warp == kEpiWarp0 && lane == 0) TDBG_ADD(6);
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (a.dbg && tid == 0) atomicAdd(a.dbg + blockIdx.x * 16 + 8, (unsigned long long)(clock64() - kt0));
+    if (warp == 1) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem, ncols);
+    }
+}
+
+template <bool BWD>
+const void *pick(int D, int k) {
+#define DR_TS_CASE(DD, KK)                                                                        \
+    if (D == DD && k == KK) return (const void *)tspmm_kernel<BWD, DD, KK / 4>;
+    DR_TS_CASE(64, 4) DR_TS_CASE(64, 8) DR_TS_CASE(64, 16) DR_TS_CASE(64, 32)
+    DR_TS_CASE(128, 4) DR_TS_CASE(128, 8) DR_TS_CASE(128, 16) DR_TS_CASE(128, 32)
+#undef DR_TS_CASE
+    return nullptr;
+}
+
+void launch(const TileSet &ts, TsArgs &a, int D, bool bwd, cudaStream_t s) {
+    a.rows = ts.rows;
+    a.chunk_beg = ts.chunk_beg;
+    a.halo = ts.halo;
+    a.eptr = ts.eptr;
+    a.cedge = ts.cedge;
+    a.cta_beg = ts.cta_beg;
+    a.stage_bytes = kATile + 256u * (uint32_t)D;
+    a.side_bytes = (uint32_t)((bwd ? 2 * kSideEB : 2 * kSideE + 64 * a.k * 5) + 127) & ~127u;
+    const size_t budget = 227 * 1024 - 1024 - kStgBytes - (size_t)kSideSlots * a.side_bytes - 512;
+    a.SA = (int)std::min<size_t>(kMaxSA, budget / a.stage_bytes);
+    DR_CHECK(a.SA >= 2, DR_ERR_UNSUPPORTED, "tspmm: shared memory budget");
+    const size_t smem = (size_t)a.SA * a.stage_bytes + kStgBytes + (size_t)kSideSlots * a.side_bytes + 1024;
+    const void *fn = bwd ? pick<true>(D, a.k) : pick<false>(D, a.k);
+    DR_CHECK(fn, DR_ERR_UNSUPPORTED, "tspmm: unsupported D/k");
+    ensure_smem(fn, smem);
+    const int grid = ts.grid;
+    if (grid <= 0) return;
+    static unsigned long long *dbg_buf = nullptr;
+    const char *dbe = getenv("DR_TS_DEBUG");
+    if (dbe && atoi(dbe)) {
+        if (!dbg_buf) DR_CUDA(cudaMalloc(&dbg_buf, 148 * 16 * 8));
+        DR_CUDA(cudaMemsetAsync(dbg_buf, 0, 148 * 16 * 8, s));
+        a.dbg = dbg_buf;
+    }
+    void *args[] = {(void *)&a};
+    DR_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(kThreads), args, smem, s));
+    if (a.dbg) {
+        unsigned long long h[148 * 16];
+        DR_CUDA(cudaStreamSynchronize(s));
+        DR_CUDA(cudaMemcpy(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost));
+        double t[16] = {0};
+        for (int b = 0; b < grid; ++b)
+            for (int q = 0; q < 16; ++q) t[q] += (double)h[b * 16 + q] / grid;
+        fprintf(stderr,
+                "[tspmm %s D=%d k=%d tiles=%d chunks=%lld SA=%d] kcycles/CTA: total %.1f | prod wait "
+                "%.1f | mma wait conv %.1f acc %.1f | conv pre %.1f wait %.1f work %.1f | epi wait "
+                "%.1f work %.1f\n",
+                bwd ? "bwd" : "fwd", D, a.k, ts.n_tiles, (long long)ts.n_chunks, a.SA, t[8] / 1e3,
+                t[0] / 1e3, t[1] / 1e3, t[2] / 1e3, t[9] / 1e3, t[3] / 1e3, t[4] / 1e3, t[5] / 1e3,
+                t[6] / 1e3);
+    }
+}
+
+}  // namespace
+
+bool tspmm_supported(const TileSet &ts, int dim, int k) {
+    const char *e = getenv("DR_TSPMM");               // experiments only: 0 disables
+    if (e && atoi(e) == 0) return false;
+    return ts.n_tiles > 0 && (dim == 64 || dim == 128) && (k == 4 || k == 8 || k == 16 || k == 32);
+}
+
+void launch_tspmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
+                      float *z, cudaStream_t s) {
+    TsArgs a{};
+    a.k = k;
+    a.hval = hval;
+    a.hidx = hidx;
+    a.c = r.c;
+    a.z = z;
+    ProfScope ps("spmm_fwd", s);
+    launch(r.tiles, a, dim, false, s);
+    note_launch("tspmm_fwd");
+}
+
+void launch_tspmm_bwd(const RelDev &r, const float *dz, bool apply_c, const RelDev *r2,
+                      const float *dz2, bool apply_c2, const float *root, const uint8_t *hidx,
+                      int k, int dim, float *g_kept, float *dx, cudaStream_t s) {
+    TsArgs a{};
+    a.k = k;
+    a.hidx = hidx;
+    a.dz = dz;
+    a.dzc = apply_c ? r.c : nullptr;
+    a.s = r.s;
+    if (r2) {
+        a.p_colptr = r2->colptr;
+        a.p_row = r2->row;
+        a.p_ewT = r2->ewT;
+        a.p_s = r2->s;
+        a.p_c = apply_c2 ? r2->c : nullptr;
+        a.p_dz = dz2;
+    }
+    a.root = root;
+    a.dx = dx;
+    a.g_kept = g_kept;
+    ProfScope ps("spmm_bwd", s);
+    launch(r.tilesT, a, dim, true, s);
+    note_launch("tspmm_bwd");
+}
+
+}  // namespace dr

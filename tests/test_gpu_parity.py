@@ -137,9 +137,16 @@ def test_spmm_bwd_parity(designs, name, D, k):
         dense = O.densify(oi, to_np(gk).astype(np.float64), D)
         assert np.array_equal(to_np(dx), dense.astype(np.float32)), rel     # exact scatter
         # accumulate mode adds into the kept positions only
+        # (the accumulate path is the SIMT kernel, the plain one may be the tensor-core
+        # tiled kernel: same values up to rounding, same support)
         dx2 = torch.ones_like(dx)
         dr.spmm_bwd(g, rel, dz, val, idx, D, want_g=False, accumulate=True, dx_out=dx2)
-        assert np.allclose(to_np(dx2), dense + 1.0, rtol=0, atol=1e-6)
+        got = to_np(dx2).astype(np.float64) - 1.0
+        want = O.densify(oi, ref, D)
+        bound = TOL * np.linalg.norm(want, axis=1, keepdims=True) + 3e-7   # + ulp(1.0) of the add
+        assert np.all(np.abs(got - want) <= bound), rel
+        off = O.densify(oi, np.ones_like(ref), D) == 0
+        assert np.all(to_np(dx2)[off] == 1.0), rel
 
 
 def test_spmm_adjoint_on_gpu(designs):
