@@ -397,8 +397,23 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
             if (!seq) DR_CUDA(cudaStreamWaitEvent(s0, C.ev[0], 0));
             BwdTerm t0{&g->rel[DR_NEAR], dz[DR_NEAR], false}, t1{&g->rel[DR_PINS], dz[DR_PINS], false};
             TagScope t("cell");
-            launch_spmm_bwd(g->src_cell, nc, t0, t1, L->wr[DR_NEAR] ? root_c : nullptr, hci,
-                            L->k_cell, L->d_cell, nullptr, dxc, false, s0);
+            const RelDev &rn = g->rel[DR_NEAR];
+            if (!rn.ewT && rn.n_src == nc && tspmm_supported(rn.tilesT, L->d_cell, L->k_cell)) {
+                // tensor-core tiled near term; the low-degree pins term (+ the root
+                // term) first goes to root_c in place with the SIMT kernel, and the
+                // tiled kernel adds it in its epilogue as it would the root term
+                {
+                    TagScope t2("pins");
+                    launch_spmm_bwd(g->rel[DR_PINS].bwd, nc, t1, BwdTerm{},
+                                    L->wr[DR_NEAR] ? root_c : nullptr, hci, L->k_cell, L->d_cell,
+                                    root_c, nullptr, false, s0);
+                }
+                launch_tspmm_bwd(rn, dz[DR_NEAR], false, root_c, hci, L->k_cell, L->d_cell,
+                                 nullptr, dxc, s0);
+            } else {
+                launch_spmm_bwd(g->src_cell, nc, t0, t1, L->wr[DR_NEAR] ? root_c : nullptr, hci,
+                                L->k_cell, L->d_cell, nullptr, dxc, false, s0);
+            }
         }
         if (dxn) {
             if (!seq) DR_CUDA(cudaStreamWaitEvent(s2, C.ev[0], 0));

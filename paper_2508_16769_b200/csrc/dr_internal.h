@@ -88,11 +88,10 @@ int warp_row_threshold();
 // (tspmm.cu): the rows are cut into tiles of <= 128 rows grown as BFS balls
 // over the relation itself (compact neighbourhoods), and each tile lists its
 // halo = the distinct column ids its rows touch, padded to 64-id chunks (-1).
-// Per chunk, the edges of the tile that land in it are stored as uint16: the
-// halfword offset of A[m][u] (m = row slot, u = halo slot in the chunk) in the
-// 128-B-swizzled K-major bf16 A tile, padded per chunk to 8 entries (0xFFFF). A tile's
-// aggregation is then the dense product Adj_tile[128 x U] * X_halo[U x D] with
-// a 0/1 adjacency operand, one 64-wide K chunk at a time (SURVEY §7.3-2a
+// The tile's adjacency restricted to one chunk is a 128 x 64 bit matrix, stored
+// as one 64-bit mask per tile row (1 KB per chunk, whatever the density). A
+// tile's aggregation is then the dense product Adj_tile[128 x U] * X_halo[U x D]
+// with a 0/1 adjacency operand, one 64-wide K chunk at a time (SURVEY §7.3-2a
 // locality, made explicit).
 constexpr int kTsRows = 128;
 constexpr int kTsChunk = 64;
@@ -102,10 +101,12 @@ struct TileSet {
     int32_t *rows = nullptr;        // [n_tiles * 128], -1 padded
     int32_t *chunk_beg = nullptr;   // [n_tiles + 1] chunk range of a tile
     int32_t *halo = nullptr;        // [n_chunks * 64], -1 padded
-    int32_t *eptr = nullptr;        // [n_chunks + 1] into cedge
-    uint16_t *cedge = nullptr;      // [nnz]
+    uint64_t *abits = nullptr;      // [n_chunks * 128] row masks: bit u of [c][m] <=> edge (m, 64 c + u)
     int32_t grid = 0;               // persistent CTAs of the kernels (min(n_tiles, 148))
-    int32_t *cta_beg = nullptr;     // [grid + 1] contiguous tile range per CTA, balanced by chunks
+    int32_t *cta_beg = nullptr;     // [grid + 1] CTA b's chunks are cta_chunks[cta_beg[b], cta_beg[b+1])
+    int32_t *cta_chunks = nullptr;  //   in processing order;
+    int32_t *cta_tiles = nullptr;   // [grid][2] its tiles: first, count (step tile_stride)
+    int32_t tile_stride = 1;
 };
 
 struct RelDev {
@@ -172,13 +173,12 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1,
                      float *dx, bool accumulate, cudaStream_t s);
 
 // Tensor-core tiled SpMM (tspmm.cu) of a relation with a TileSet: forward into
-// z; backward for the tiled relation's source rows, adding the optional second
-// relation r2 of the same source type and the root term (as launch_spmm_bwd).
+// z; backward for the tiled relation's source rows alone, with an optional
+// extra [n_src x k] term added at the kept entries (root + other relations).
 bool tspmm_supported(const TileSet &ts, int dim, int k);
 void launch_tspmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
                       float *z, cudaStream_t s);
-void launch_tspmm_bwd(const RelDev &r, const float *dz, bool apply_c, const RelDev *r2,
-                      const float *dz2, bool apply_c2, const float *root, const uint8_t *hidx,
-                      int k, int dim, float *g_kept, float *dx, cudaStream_t s);
+void launch_tspmm_bwd(const RelDev &r, const float *dz, bool apply_c, const float *extra,
+                      const uint8_t *hidx, int k, int dim, float *g_kept, float *dx, cudaStream_t s);
 
 }  // namespace dr

@@ -113,9 +113,10 @@ std::vector<int64_t> bfs_rank(int32_t n, const std::vector<int32_t> &rp,
 
 // Host form of a TileSet (see dr_internal.h).
 struct HostTiles {
-    std::vector<int32_t> rows, chunk_beg, halo, eptr;
-    std::vector<uint16_t> cedge;
-    std::vector<int32_t> cta_beg;
+    std::vector<int32_t> rows, chunk_beg, halo;
+    std::vector<uint64_t> abits;
+    std::vector<int32_t> cta_beg, cta_chunks, cta_tiles;
+    int32_t tile_stride = 1;
     int32_t n_tiles = 0, grid = 0;
     int64_t n_chunks = 0;
 };
@@ -135,10 +136,8 @@ void build_tiles(int32_t n, const std::vector<int32_t> &rp, const std::vector<in
     std::vector<int32_t> queue;
     queue.reserve(kTsRows * 8);
     std::vector<int32_t> local((size_t)n, -1);
-    std::vector<int32_t> tile, hl, cnt;
+    std::vector<int32_t> tile, hl;
     T.chunk_beg.push_back(0);
-    T.eptr.push_back(0);
-    T.cedge.reserve(col.size());
     size_t pos = 0;
     while (true) {
         while (pos < (size_t)n && assigned[seq[pos]]) ++pos;
@@ -174,46 +173,54 @@ void build_tiles(int32_t n, const std::vector<int32_t> &rp, const std::vector<in
         for (int m = 0; m < kTsRows; ++m) T.rows.push_back(m < (int)tile.size() ? tile[m] : -1);
         for (int64_t u = 0; u < nch * kTsChunk; ++u)
             T.halo.push_back(u < (int64_t)hl.size() ? hl[(size_t)u] : -1);
-        // edges bucketed by chunk (counting sort), row-major inside a chunk
-        cnt.assign((size_t)nch + 1, 0);
-        for (int32_t i : tile)
-            for (int32_t e = rp[i]; e < rp[i + 1]; ++e) cnt[local[col[e]] / kTsChunk + 1]++;
-        // each chunk's list is padded to a multiple of 8 entries (16 B, for the
-        // converters' 16-B async copies) with 0xFFFF (row slot 1023: skipped)
-        for (int64_t q = 1; q <= nch; ++q) cnt[q] = (cnt[q] + 7) & ~7;
-        for (int64_t q = 0; q < nch; ++q) cnt[q + 1] += cnt[q];
-        const size_t base = T.cedge.size();
-        T.cedge.resize(base + (size_t)cnt[nch], (uint16_t)0xFFFF);
-        std::vector<int32_t> cur(cnt.begin(), cnt.end() - 1);
+        // adjacency of the tile as one 64-bit row mask per (chunk, tile row):
+        // bit u of abits[chunk][m] <=> edge (row m, halo slot 64 chunk + u)
+        const size_t base = T.abits.size();
+        T.abits.resize(base + (size_t)nch * kTsRows, 0ull);
         for (int m = 0; m < (int)tile.size(); ++m) {
             const int32_t i = tile[m];
             for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
                 const int32_t u = local[col[e]];
-                // stored as the halfword index of A[m][u] in the K-major SW128 bf16
-                // tile the converters build (16-B chunk (u/8) ^ (m%8) of row m)
-                const int uu = u % kTsChunk;
-                const int off = m * 128 + ((((uu >> 3) ^ (m & 7)) & 7) << 4) + ((uu & 7) << 1);
-                T.cedge[base + cur[u / kTsChunk]++] = (uint16_t)(off >> 1);
+                T.abits[base + (size_t)(u / kTsChunk) * kTsRows + m] |= 1ull << (u % kTsChunk);
             }
         }
-        for (int64_t q = 0; q < nch; ++q) T.eptr.push_back((int32_t)(base + cnt[q + 1]));
         for (int32_t h : hl) local[h] = -1;
         T.n_chunks += nch;
         T.chunk_beg.push_back((int32_t)T.n_chunks);
         ++T.n_tiles;
     }
-    // persistent-kernel work split: CTA b takes the tiles whose first chunk lies in
-    // [b C / grid, (b+1) C / grid) -- contiguous (neighbouring balls share halo
-    // rows in L2) and balanced by chunk count
+    // persistent-kernel work split: CTA b takes a contiguous run of tiles (the
+    // ones whose first chunk lies in [b C / grid, (b+1) C / grid): balanced by
+    // chunk count, every chunk costs the same) -- neighbouring balls share halo
+    // rows, which the CTA then re-reads from L2 (measured better than
+    // round-robin, DR_TS_ORDER=rr); its chunks are cta_chunks[cta_beg[b], cta_beg[b+1])
     T.grid = std::min<int32_t>(T.n_tiles, 148);
-    T.cta_beg.assign((size_t)T.grid + 1, T.n_tiles);
-    int32_t t = 0;
+    T.cta_beg.assign((size_t)T.grid + 1, 0);
+    T.cta_chunks.clear();
+    T.cta_chunks.reserve((size_t)T.n_chunks);
+    const char *ord = getenv("DR_TS_ORDER");
+    const bool rr = ord && std::string(ord) == "rr";
+    int32_t t0 = 0;
     for (int32_t b = 0; b < T.grid; ++b) {
-        const int64_t c0 = T.n_chunks * b / T.grid;
-        while (t < T.n_tiles && T.chunk_beg[t] < c0) ++t;
-        T.cta_beg[b] = t;
+        T.cta_beg[b] = (int32_t)T.cta_chunks.size();
+        if (rr) {
+            int32_t cnt = 0;
+            for (int32_t t = b; t < T.n_tiles; t += T.grid, ++cnt)
+                for (int32_t c = T.chunk_beg[t]; c < T.chunk_beg[t + 1]; ++c) T.cta_chunks.push_back(c);
+            T.cta_tiles.push_back(b);
+            T.cta_tiles.push_back(cnt);
+        } else {
+            const int64_t c1 = T.n_chunks * (b + 1) / T.grid;
+            int32_t t1 = t0;
+            while (t1 < T.n_tiles && (b == T.grid - 1 || T.chunk_beg[t1] < c1)) ++t1;
+            for (int32_t c = T.chunk_beg[t0]; c < T.chunk_beg[t1]; ++c) T.cta_chunks.push_back(c);
+            T.cta_tiles.push_back(t0);
+            T.cta_tiles.push_back(t1 - t0);
+            t0 = t1;
+        }
     }
-    T.cta_beg[0] = 0;
+    T.tile_stride = rr ? T.grid : 1;
+    T.cta_beg[T.grid] = (int32_t)T.cta_chunks.size();
 }
 
 void build_rel(const dr_rel_desc &d, bool validate, HostRel &h) {
@@ -505,10 +512,12 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
             plan(0, (void **)&ts.rows, ht.rows.data(), ht.rows.size() * 4);
             plan(0, (void **)&ts.chunk_beg, ht.chunk_beg.data(), ht.chunk_beg.size() * 4);
             plan(0, (void **)&ts.halo, ht.halo.data(), ht.halo.size() * 4);
-            plan(0, (void **)&ts.eptr, ht.eptr.data(), ht.eptr.size() * 4);
-            plan(0, (void **)&ts.cedge, ht.cedge.data(), ht.cedge.size() * 2);
+            plan(0, (void **)&ts.abits, ht.abits.data(), ht.abits.size() * 8);
             ts.grid = ht.grid;
             plan(0, (void **)&ts.cta_beg, ht.cta_beg.data(), ht.cta_beg.size() * 4);
+            plan(0, (void **)&ts.cta_chunks, ht.cta_chunks.data(), ht.cta_chunks.size() * 4);
+            plan(0, (void **)&ts.cta_tiles, ht.cta_tiles.data(), ht.cta_tiles.size() * 4);
+            ts.tile_stride = ht.tile_stride;
         };
         if (want_tiles) {
             plan_tiles(g->rel[DR_NEAR].tiles, tl);

@@ -8,24 +8,27 @@
 //     backward: G_T  = diag(s_T)  Adj^T[T x H] dZ'[H]               (Eq. 10)
 // with the 0/1 adjacency tile as the A operand (exact in bf16) and the halo's
 // feature rows as the B operand, split x = hi + lo in bf16 (|x - hi - lo| <=
-// 2^-17 |x|; two kind::f16 MMAs per K step, fp32 accumulation in TMEM). The
+// 2^-17 |x|; A B_hi and A B_lo accumulate side by side in TMEM, fp32). The
 // backward then samples G at the source row's own CBSR indices (the D-ReLU mask
-// gradient, Eq. 11), adds the second relation of the source type (pins) and the
-// Sage root term, and writes the dense dX row. Every halo row is read once per
+// gradient, Eq. 11), adds the extra term (Sage root term + the low-degree second
+// relation of the source type, summed beforehand by the SIMT kernel) and writes
+// the dense dX row. Every halo row is read once per
 // tile (compulsory bytes) instead of once per edge, and the per-edge work moves
 // from the L1/shared-memory scatter pipes to the tensor cores.
 //
-// Roles (one persistent CTA per SM, 14 warps; CTA b owns a contiguous range of
-// tiles balanced by chunk count, TileSet::cta_beg):
+// Roles (one persistent CTA per SM, 14 warps; CTA b takes tiles b, b + grid, ...
+// so the SMs sweep consecutive, neighbouring tiles together and shared halo rows
+// come from L2; TileSet::cta_chunks lists each CTA's chunk sequence):
 //   warp 0     producer  (backward): bulk copies (TMA engine) of the chunk's 64
 //                         dZ' halo rows into the stage;
-//   warps 2-9  converters: zero + scatter the 0/1 adjacency chunk [128 x 64];
+//   warps 2-9  converters: expand the chunk's row masks into the 0/1 adjacency
+//                         tile [128 x 64] (bf16);
 //                         forward: densify the halo's CBSR rows straight into the
 //                         K-major hi/lo B tiles; backward: transposing hi/lo split
 //                         of the landed dZ' rows (in place). Their global reads
 //                         are cp.async copies into side slots two chunks ahead;
-//   warp 1     MMA      : one thread, 2 MMAs per K = 16 step into a double-
-//                         buffered TMEM accumulator;
+//   warp 1     MMA      : one thread, one N = 2D MMA per K = 16 step ([B_hi; B_lo]
+//                         stacked along N) into a double-buffered TMEM accumulator;
 //   warps 10-13 epilogue: TMEM -> registers (lane = tile row) -> a per-warp
 //                         [32 rows x 32 cols] staging tile -> 128-bit coalesced
 //                         row stores (4 rows x 128 B per instruction).
@@ -49,13 +52,13 @@ constexpr int kEpiWarp0 = 10;
 constexpr int kMaxSA = 4;
 constexpr int kStg = 36;                       // epilogue staging row stride (floats, 144 B)
 constexpr uint32_t kATile = 16384;             // 128 x 64 bf16
-constexpr uint32_t kEpiWarpBytes = 32 * kStg * 4 + 32 * 32 + 2 * 32 * 4 * 4;   // staging, ids, nets, weights
-constexpr uint32_t kStgBytes = 4 * kEpiWarpBytes;
-constexpr uint16_t kBf16One = 0x3F80;
+constexpr uint32_t kStgBytes = 4 * 32 * kStg * 4;      // epilogue staging, 4 warps
 
 struct TsArgs {
-    const int32_t *rows, *chunk_beg, *halo, *eptr, *cta_beg;
-    const uint16_t *cedge;
+    int32_t n_tiles;
+    const int32_t *rows, *chunk_beg, *halo, *cta_beg, *cta_chunks, *cta_tiles;
+    int tile_stride;
+    const uint64_t *abits;
     int k, SA;
     uint32_t stage_bytes, side_bytes;
     // forward: CBSR of the halo (source) rows, per-row output scale, output
@@ -64,11 +67,9 @@ struct TsArgs {
     const float *c;
     float *z;
     // backward: dZ' rows of the halo (destinations), optional per-halo-row scale
-    // (standalone ABI: dz not yet row-scaled), s_j of the tiled relation, and an
-    // optional second relation term for the same source type (pins CSC)
+    // (standalone ABI: dz not yet row-scaled), s_j of the tiled relation, and the
+    // extra per-kept-entry term added in the epilogue (root term + other relation)
     const float *dz, *dzc, *s;
-    const int32_t *p_colptr, *p_row;
-    const float *p_ewT, *p_s, *p_c, *p_dz;
     const float *root;
     float *dx, *g_kept;
     unsigned long long *dbg;          // DR_TS_DEBUG role timers (cycles per CTA), else null
@@ -112,22 +113,18 @@ __device__ __forceinline__ void store_col8(uint8_t *B, uint32_t lo_off, int f, i
 
 // ---- converter side buffers
 // The converters' global reads for chunk ch are 16/8/4-B async copies
-// (cp.async) into a side slot issued two chunks ahead: the chunk's adjacency
-// entries (padded to 16 B per chunk at graph creation) and, forward, the CBSR
-// rows of its 64 halo ids (thread ct copies its quarter u = ct / 4, h = ct % 4).
-// Addresses (eptr, halo ids) are loaded into registers three chunks ahead.
+// (cp.async) into a side slot issued two chunks ahead: the chunk's 128 row
+// masks (1 KB) and, forward, the CBSR rows of its 64 halo ids (thread ct copies
+// its quarter u = ct / 4, h = ct % 4). Halo ids are loaded into registers three
+// chunks ahead.
 constexpr int kSideSlots = 3;
-constexpr int kSideE = 2048;                   // adjacency entries per slot (4 KB), forward
-constexpr int kSideEB = 2048;                  // backward
+constexpr uint32_t kSideA = 1024;              // 128 x 64-bit row masks
 struct CInfo {
-    int e0, e1;      // adjacency entries [e0, e1) of the chunk
     int id;          // forward: halo id of row u = ct / 4
     int h0, h1;      // backward: halo ids of rows lane, lane + 32 (valid-row count)
 };
 template <bool BWD>
 __device__ __forceinline__ void info_load(const TsArgs &a, int64_t ch, int ct, CInfo &p) {
-    p.e0 = __ldg(a.eptr + ch);
-    p.e1 = __ldg(a.eptr + ch + 1);
     if constexpr (!BWD) {
         p.id = __ldg(a.halo + ch * kTsChunk + (ct >> 2));
     } else {
@@ -136,15 +133,14 @@ __device__ __forceinline__ void info_load(const TsArgs &a, int64_t ch, int ct, C
     }
 }
 template <bool BWD, int QH>
-__device__ __forceinline__ void side_issue(const TsArgs &a, const CInfo &p, uint8_t *sd, int ct) {
-    constexpr int SE = BWD ? kSideEB : kSideE;
-    const int n = min(p.e1 - p.e0, SE);
-    if (8 * ct < n) tc::cp_async16(sd + 16 * ct, a.cedge + p.e0 + 8 * ct, 16);
+__device__ __forceinline__ void side_issue(const TsArgs &a, int64_t ch, const CInfo &p, uint8_t *sd,
+                                           int ct) {
+    if (ct < 64) tc::cp_async16(sd + 16 * ct, a.abits + ch * kTsRows + 2 * ct, 16);
     if constexpr (!BWD) {
         if (p.id >= 0) {
             constexpr int K = 4 * QH;
             const int u = ct >> 2, h = ct & 3;
-            uint8_t *sv = sd + 2 * kSideE + u * K * 4 + h * QH * 4;
+            uint8_t *sv = sd + kSideA + u * K * 4 + h * QH * 4;
             const float *gv = a.hval + (int64_t)p.id * K + h * QH;
             if constexpr (QH == 8) {
                 tc::cp_async16(sv, gv, 16);
@@ -157,7 +153,7 @@ __device__ __forceinline__ void side_issue(const TsArgs &a, const CInfo &p, uint
                 tc::cp_async4(sv, gv, 4);
             }
             if (h == 0) {
-                uint8_t *si = sd + 2 * kSideE + 64 * K * 4 + u * K;
+                uint8_t *si = sd + kSideA + 64 * K * 4 + u * K;
                 const uint8_t *gi = a.hidx + (int64_t)p.id * K;
                 if constexpr (QH == 8) {
                     tc::cp_async16(si, gi, 16);
@@ -174,38 +170,32 @@ __device__ __forceinline__ void side_issue(const TsArgs &a, const CInfo &p, uint
     }
 }
 
-// Zero the [128 x 64] A tile (256 converter threads).
-__device__ __forceinline__ void zero_a(uint8_t *A, int ct) {
-    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+// The [128 x 64] bf16 A tile from the chunk's row masks: thread ct writes row
+// m = ct / 2, halo slots [32 h, 32 h + 32) (h = ct % 2) as four whole 16-B
+// swizzle chunks of 0 / 1.0 -- every element written, no zero fill, no scatter.
+__device__ __forceinline__ void build_a(const uint8_t *sd, uint8_t *A, int ct) {
+    const int m = ct >> 1, h = ct & 1;
+    const uint32_t bits = reinterpret_cast<const uint32_t *>(sd)[2 * m + h];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) reinterpret_cast<uint4 *>(A)[ct + kConv * i] = z;
-}
-__device__ __forceinline__ void put_edge(uint8_t *A, uint32_t v) {   // v = halfword offset
-    if (v != 0xFFFFu) reinterpret_cast<uint16_t *>(A)[v] = kBf16One;
-}
-// edges of the chunk -> 1.0 at A[m][u]: 8 entries per thread from the side slot,
-// any beyond kSideE straight from global
-template <int SE>
-__device__ __forceinline__ void scatter_edges(const TsArgs &a, const CInfo &p, const uint8_t *sd,
-                                              uint8_t *A, int ct) {
-    const int n = p.e1 - p.e0;
-    if (8 * ct < min(n, SE)) {
-        const uint4 w = *reinterpret_cast<const uint4 *>(sd + 16 * ct);
-        put_edge(A, w.x & 0xffffu); put_edge(A, w.x >> 16);
-        put_edge(A, w.y & 0xffffu); put_edge(A, w.y >> 16);
-        put_edge(A, w.z & 0xffffu); put_edge(A, w.z >> 16);
-        put_edge(A, w.w & 0xffffu); put_edge(A, w.w >> 16);
+    for (int c = 0; c < 4; ++c) {
+        const uint32_t byte = bits >> (8 * c);
+        uint32_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t t = byte >> (2 * j);
+            w[j] = (((t & 1u) * 0xFFFFu) | ((t & 2u) * 0x7FFF8000u)) & 0x3F803F80u;
+        }
+        *reinterpret_cast<uint4 *>(A + m * 128 + (((4 * h + c) ^ (m & 7)) << 4)) =
+            make_uint4(w[0], w[1], w[2], w[3]);
     }
-    for (int e = SE + ct; e < n; e += kConv) put_edge(A, __ldg(a.cedge + p.e0 + e));
 }
 
 template <int D, int QH>
 __device__ __forceinline__ void convert_fwd(const TsArgs &a, const CInfo &p, const uint8_t *sd,
-                                            uint8_t *st, int ct, int ch, int cb) {
+                                            uint8_t *st, int ct) {
     uint8_t *A = st, *B = st + kATile;
     constexpr uint32_t lo = (uint32_t)D * 128u;
     constexpr int K = 4 * QH;
-    zero_a(A, ct);
     {
         const uint4 z = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
@@ -213,12 +203,12 @@ __device__ __forceinline__ void convert_fwd(const TsArgs &a, const CInfo &p, con
             reinterpret_cast<uint4 *>(B)[ct + kConv * i] = z;
     }
     tc::cp_async_wait<1>();                 // this chunk's side copies (ch + 1's may fly)
-    tc::named_bar(1, kConv);                // zeros + everyone's side data
-    scatter_edges<kSideE>(a, p, sd, A, ct);
+    tc::named_bar(1, kConv);                // B zeroed + everyone's side data visible
+    build_a(sd, A, ct);
     if (p.id >= 0) {
         const int u = ct >> 2, h = ct & 3;
-        const float *sv = reinterpret_cast<const float *>(sd + 2 * kSideE) + u * K + h * QH;
-        const uint8_t *si = sd + 2 * kSideE + 64 * K * 4 + u * K + h * QH;
+        const float *sv = reinterpret_cast<const float *>(sd + kSideA) + u * K + h * QH;
+        const uint8_t *si = sd + kSideA + 64 * K * 4 + u * K + h * QH;
 #pragma unroll
         for (int q = 0; q < QH; ++q) {
             uint32_t hh, ll;
@@ -253,10 +243,9 @@ __device__ __forceinline__ void convert_bwd(const TsArgs &a, const CInfo &p, con
             vv[r] = q;
         }
     }
-    zero_a(A, ct);
     tc::cp_async_wait<1>();
-    tc::named_bar(1, kConv);                 // raw reads + A zeroing + side data
-    scatter_edges<kSideEB>(a, p, sd, A, ct);
+    tc::named_bar(1, kConv);                 // raw reads done (in place) + side data visible
+    build_a(sd, A, ct);
     if (x.ok) {
         const int f = 4 * x.fq;
         float c8[8];
@@ -277,11 +266,19 @@ __device__ __forceinline__ void convert_bwd(const TsArgs &a, const CInfo &p, con
 
 // ---- epilogue helpers (warp quarter qd: tile rows 32 qd + lane; TMEM lanes likewise)
 // TMEM columns [j0, j0+32) of this warp's 32 rows -> staging (row = lane), scaled
+template <int D>
 __device__ __forceinline__ void tmem_to_stg(uint32_t taddr, float scale, float *stg, int lane) {
-    uint32_t r0[16], r1[16];
+    uint32_t r0[16], r1[16], q0[16], q1[16];
     tc::tmem_ld16_nw(taddr, r0);
     tc::tmem_ld16_nw(taddr + 16u, r1);
+    tc::tmem_ld16_nw(taddr + (uint32_t)D, q0);          // A B_lo half
+    tc::tmem_ld16_nw(taddr + (uint32_t)D + 16u, q1);
     tc::tmem_wait_ld();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        r0[q] = __float_as_uint(__uint_as_float(r0[q]) + __uint_as_float(q0[q]));
+        r1[q] = __float_as_uint(__uint_as_float(r1[q]) + __uint_as_float(q1[q]));
+    }
     float4 *o = reinterpret_cast<float4 *>(stg + lane * kStg);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -316,88 +313,64 @@ __device__ __forceinline__ void epi_fwd(const TsArgs &a, int t, uint32_t tacc, f
     const float cr = rid >= 0 ? __ldg(a.c + rid) : 0.f;
 #pragma unroll 1
     for (int j0 = 0; j0 < D; j0 += 32) {
-        tmem_to_stg(tacc + (uint32_t)j0, cr, stg, lane);
+        tmem_to_stg<D>(tacc + (uint32_t)j0, cr, stg, lane);
         __syncwarp();
         stg_to_global<D>(stg, a.z, rid, j0, lane);
         __syncwarp();
     }
 }
 
-// Second relation term of the backward (pins CSC of the cell sources, Eq. 10),
-// warp-cooperative: the warp's 32 rows are taken R = 32 / K at a time, K lanes
-// per row (lane t <-> CBSR position t), so one load instruction samples K
-// columns of one dZ' row (a few 128-B lines) instead of 32 rows' worth. The
-// first kNets net ids of every row are staged in shared memory up front (one
-// load round for all rows), so the sampled loads of successive row groups are
-// independent and overlap. Result: psm[r][t] (row r of the warp, position t).
-constexpr int kNets = 4;
-template <int D, int K>
-__device__ __forceinline__ void pins_term_coop(const TsArgs &a, int rid, float *psm,
-                                               const uint8_t *idsm, int *netsm, float *wsm,
-                                               int lane) {
-    int e0 = 0, deg = 0;
-    float ps = 0.f;
-    if (rid >= 0) {
-        e0 = __ldg(a.p_colptr + rid);
-        deg = __ldg(a.p_colptr + rid + 1) - e0;
-        ps = __ldg(a.p_s + rid);
+// Per-row inputs of the backward epilogue, loaded one tile ahead (software
+// pipelined across tiles): the row id, its CBSR indices and its extra term
+// (root term + second relation, summed beforehand).
+template <int K>
+struct EpiIn {
+    static constexpr bool kPre = K <= 16;     // K = 32: extra term loaded at use (registers)
+    int rid;
+    uint32_t idw[K / 4];
+    float ex[kPre ? K : 1];
+};
+template <int K>
+__device__ __forceinline__ void load_extra(const TsArgs &a, int rid, float *ex) {
+    if (rid >= 0 && a.root) {
+        const float4 *rr = reinterpret_cast<const float4 *>(a.root + (int64_t)rid * K);
 #pragma unroll
-        for (int j = 0; j < kNets; ++j)
-            if (j < deg) {
-                const int i = __ldg(a.p_row + e0 + j);
-                netsm[lane * kNets + j] = i;
-                float w = a.p_ewT ? __ldg(a.p_ewT + e0 + j) : 1.f;
-                if (a.p_c) w *= __ldg(a.p_c + i);
-                wsm[lane * kNets + j] = w;
-            }
-    }
-    __syncwarp();
-    constexpr int R = 32 / K;
-    const int t = lane % K, sub = lane / K;
-#pragma unroll 4
-    for (int it = 0; it < K; ++it) {
-        const int r = R * it + sub;
-        const int d = __shfl_sync(0xffffffffu, deg, r);
-        const float pr = __shfl_sync(0xffffffffu, ps, r);
-        const int er = __shfl_sync(0xffffffffu, e0, r);
-        const uint32_t id = idsm[r * K + t];
-        float v = 0.f;
-#pragma unroll
-        for (int j = 0; j < kNets; ++j)
-            if (j < d) v += wsm[r * kNets + j] * __ldg(a.p_dz + (int64_t)netsm[r * kNets + j] * D + id);
-        for (int j = kNets; j < d; ++j) {
-            const int i = __ldg(a.p_row + er + j);
-            float w = a.p_ewT ? __ldg(a.p_ewT + er + j) : 1.f;
-            if (a.p_c) w *= __ldg(a.p_c + i);
-            v += w * __ldg(a.p_dz + (int64_t)i * D + id);
+        for (int q = 0; q < K / 4; ++q) {
+            const float4 v = __ldg(rr + q);
+            ex[4 * q] = v.x; ex[4 * q + 1] = v.y; ex[4 * q + 2] = v.z; ex[4 * q + 3] = v.w;
         }
-        psm[r * (K + 1) + t] = pr * v;
+    } else {
+#pragma unroll
+        for (int q = 0; q < K; ++q) ex[q] = 0.f;
     }
+}
+template <int K>
+__device__ __forceinline__ void epi_in_load(const TsArgs &a, int t, int m, EpiIn<K> &e) {
+    e.rid = __ldg(a.rows + (int64_t)t * kTsRows + m);
+    if (e.rid >= 0) {
+        const uint8_t *ir = a.hidx + (int64_t)e.rid * K;
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) e.idw[q] = __ldg(reinterpret_cast<const uint32_t *>(ir) + q);
+    } else {
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) e.idw[q] = 0;
+    }
+    if constexpr (EpiIn<K>::kPre) load_extra<K>(a, e.rid, e.ex);
 }
 
 template <int D, int QH>
-__device__ __forceinline__ void epi_bwd(const TsArgs &a, int t, uint32_t tacc, float *stg,
-                                        uint8_t *idsm, int *netsm, float *wsm, int lane,
-                                        uint64_t *accempty) {
+__device__ __forceinline__ void epi_bwd(const TsArgs &a, const EpiIn<4 * QH> &in, uint32_t tacc,
+                                        float *stg, int lane, uint64_t *accempty) {
     constexpr int K = 4 * QH;
-    const int rid = __ldg(a.rows + (int64_t)t * kTsRows + (tacc >> 16) + lane);
-    uint32_t idw[K / 4];
+    const int rid = in.rid;
+    auto idx = [&](int q) -> uint32_t { return (in.idw[q >> 2] >> (8 * (q & 3))) & 0xffu; };
     float g[K];
-    if (rid >= 0) {
-        const uint8_t *ir = a.hidx + (int64_t)rid * K;
-#pragma unroll
-        for (int q = 0; q < K / 4; ++q) idw[q] = __ldg(reinterpret_cast<const uint32_t *>(ir) + q);
-    } else {
-#pragma unroll
-        for (int q = 0; q < K / 4; ++q) idw[q] = 0;
-    }
-    auto idx = [&](int q) -> uint32_t { return (idw[q >> 2] >> (8 * (q & 3))) & 0xffu; };
 #pragma unroll
     for (int q = 0; q < K; ++q) g[q] = 0.f;
     // sample the accumulator row at the row's own CBSR indices
 #pragma unroll 1
     for (int j0 = 0; j0 < D; j0 += 32) {
-        tmem_to_stg(tacc + (uint32_t)j0, 1.f, stg, lane);
+        tmem_to_stg<D>(tacc + (uint32_t)j0, 1.f, stg, lane);
         __syncwarp();
 #pragma unroll
         for (int q = 0; q < K; ++q)
@@ -409,27 +382,19 @@ __device__ __forceinline__ void epi_bwd(const TsArgs &a, int t, uint32_t tacc, f
     __syncwarp();
     if (lane == 0) tc::mbar_arrive(accempty);
     const float sj = rid >= 0 ? __ldg(a.s + rid) : 0.f;
+    if constexpr (EpiIn<K>::kPre) {
 #pragma unroll
-    for (int q = 0; q < K; ++q) g[q] *= sj;
-    if (a.p_colptr) {
+        for (int q = 0; q < K; ++q) g[q] = sj * g[q] + in.ex[q];
+    } else {
+        float ex[K];
+        load_extra<K>(a, rid, ex);
 #pragma unroll
-        for (int q = 0; q < K / 4; ++q) reinterpret_cast<uint32_t *>(idsm)[lane * (K / 4) + q] = idw[q];
-        __syncwarp();
-        pins_term_coop<D, K>(a, rid, stg, idsm, netsm, wsm, lane);     // psm aliases stg
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < K; ++q) g[q] += stg[lane * (K + 1) + q];
-        __syncwarp();
+        for (int q = 0; q < K; ++q) g[q] = sj * g[q] + ex[q];
     }
-    if (rid >= 0) {
-        if (a.root) {
+    if (rid >= 0 && a.g_kept) {
+        float4 *o = reinterpret_cast<float4 *>(a.g_kept + (int64_t)rid * K);
 #pragma unroll
-            for (int q = 0; q < K; ++q) g[q] += __ldg(a.root + (int64_t)rid * K + q);
-        }
-        if (a.g_kept) {
-#pragma unroll
-            for (int q = 0; q < K; ++q) a.g_kept[(int64_t)rid * K + q] = g[q];
-        }
+        for (int q = 0; q < K / 4; ++q) o[q] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
     }
     if (!a.dx) return;
     // dense dX row: zeros + the K values at their indices, 32 columns at a time
@@ -455,9 +420,12 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
     __shared__ __align__(8) uint64_t full[kMaxSA], conv[kMaxSA], empty[kMaxSA], accfull[2],
         accempty[2];
     __shared__ uint32_t tmem_slot;
+    const long long kt00 = clock64();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int SA = a.SA;
-    constexpr uint32_t ncols = 2 * D;          // two accumulators of D fp32 columns
+    // two accumulators of 2D fp32 columns: [A B_hi | A B_lo], summed in the epilogue
+    // (one N = 2D MMA per K step reads the A tile once)
+    constexpr uint32_t ncols = 4 * D;
     if (tid == 0) {
         for (int i = 0; i < SA; ++i) {
             tc::mbar_init(&full[i], 1);
@@ -479,25 +447,36 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
     tc::fence_after();
     const uint32_t tmem = tmem_slot;
     const long long kt0 = clock64();
+    if (a.dbg && tid == 0) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        a.dbg[blockIdx.x * 16 + 11] = g;                                  // start (ns)
+    }
     float *stg_all = reinterpret_cast<float *>(sm + (size_t)SA * a.stage_bytes);
-    const int tb = __ldg(a.cta_beg + blockIdx.x), te = __ldg(a.cta_beg + blockIdx.x + 1);
-    const int cb = tb < te ? __ldg(a.chunk_beg + tb) : 0, ce = tb < te ? __ldg(a.chunk_beg + te) : 0;
+    // this CTA: tiles blockIdx.x, + gridDim.x, ...; its chunk sequence (same order)
+    // is cta_chunks[base, base + n_it)
+    const int base = __ldg(a.cta_beg + blockIdx.x), n_it = __ldg(a.cta_beg + blockIdx.x + 1) - base;
+    auto cid = [&](int i) -> int { return i < n_it ? __ldg(a.cta_chunks + base + i) : 0; };
+    // its tiles: t0, t0 + stride, ... (n_t of them), in the same order
+    const int t0 = __ldg(a.cta_tiles + 2 * blockIdx.x), n_t = __ldg(a.cta_tiles + 2 * blockIdx.x + 1);
+    const int tstride = a.tile_stride;
 
     if (warp == 0) {
         if constexpr (BWD) {
-            int nid0 = -1, nid1 = -1;
-            if (cb < ce) {
-                nid0 = __ldg(a.halo + (int64_t)cb * kTsChunk + lane);
-                nid1 = __ldg(a.halo + (int64_t)cb * kTsChunk + 32 + lane);
+            int nid0 = -1, nid1 = -1, cn = cid(1);
+            if (n_it > 0) {
+                const int c = cid(0);
+                nid0 = __ldg(a.halo + (int64_t)c * kTsChunk + lane);
+                nid1 = __ldg(a.halo + (int64_t)c * kTsChunk + 32 + lane);
             }
-            for (int ch = cb; ch < ce; ++ch) {
-                const int it = ch - cb;
+            for (int it = 0; it < n_it; ++it) {
                 const int slot = it % SA;
                 const uint32_t u = (uint32_t)(it / SA);
                 const int id0 = nid0, id1 = nid1;
-                if (ch + 1 < ce) {
-                    nid0 = __ldg(a.halo + (int64_t)(ch + 1) * kTsChunk + lane);
-                    nid1 = __ldg(a.halo + (int64_t)(ch + 1) * kTsChunk + 32 + lane);
+                if (it + 1 < n_it) {
+                    nid0 = __ldg(a.halo + (int64_t)cn * kTsChunk + lane);
+                    nid1 = __ldg(a.halo + (int64_t)cn * kTsChunk + 32 + lane);
+                    cn = cid(it + 2);
                 }
                 if (u > 0) {
                     TDBG_T0;
@@ -516,9 +495,10 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t idesc = tc::idesc_bf16(kTsRows, D);
+            const uint32_t idesc = tc::idesc_bf16(kTsRows, 2 * D);
             int it = 0;
-            for (int t = tb, lt = 0; t < te; ++t, ++lt) {
+            for (int lt = 0; lt < n_t; ++lt) {
+                const int t = t0 + lt * tstride;
                 const int b = lt & 1;
                 if (lt >= 2) {
                     TDBG_T0;
@@ -526,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
                     TDBG_ADD(2);
                 }
                 tc::fence_after();
-                const uint32_t d = tmem + (uint32_t)(b * D);
+                const uint32_t d = tmem + (uint32_t)(b * 2 * D);
                 const int c0 = __ldg(a.chunk_beg + t), c1 = __ldg(a.chunk_beg + t + 1);
                 for (int ch = c0; ch < c1; ++ch, ++it) {
                     const int slot = it % SA;
@@ -537,14 +517,12 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
                     }
                     tc::fence_after();
                     const uint32_t sa = tc::smem_u32(sm + (size_t)slot * a.stage_bytes);
-                    const uint32_t sbh = sa + kATile, sbl = sbh + (uint32_t)D * 128u;
+                    const uint32_t sbh = sa + kATile;     // [B_hi ; B_lo] = 2D K-major rows
 #pragma unroll
                     for (int ks = 0; ks < kTsChunk / 16; ++ks) {
                         const uint32_t ko = ks * 32;
-                        const uint64_t ad = tc::desc_sw128(sa + ko);
-                        tc::mma_bf16(d, ad, tc::desc_sw128(sbh + ko), idesc,
+                        tc::mma_bf16(d, tc::desc_sw128(sa + ko), tc::desc_sw128(sbh + ko), idesc,
                                      (ch == c0 && ks == 0) ? 0u : 1u);
-                        tc::mma_bf16(d, ad, tc::desc_sw128(sbl + ko), idesc, 1u);
                     }
                     tc::mma_commit(&empty[slot]);
                 }
@@ -555,18 +533,20 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
     } else if (warp < kEpiWarp0) {
         const int ct = tid - 64;
         uint8_t *side = sm + (size_t)SA * a.stage_bytes + kStgBytes;
-        // info ring: chunk ch, ch + 1, ch + 2 (issued), ch + 3 (loading)
+        // rings over the CTA's chunk sequence: ids c0..c3 (steps it..it+3), infos
+        // i0..i2 (it..it+2); side copies are in flight for it, it + 1
+        int c0 = cid(0), c1 = cid(1), c2 = cid(2), c3 = cid(3);
         CInfo i0{}, i1{}, i2{}, i3{};
-        if (cb < ce) info_load<BWD>(a, cb, ct, i0);
-        if (cb + 1 < ce) info_load<BWD>(a, cb + 1, ct, i1);
-        if (cb + 2 < ce) info_load<BWD>(a, cb + 2, ct, i2);
-        if (cb < ce) side_issue<BWD, QH>(a, i0, side, ct);
+        if (n_it > 0) info_load<BWD>(a, c0, ct, i0);
+        if (n_it > 1) info_load<BWD>(a, c1, ct, i1);
+        if (n_it > 2) info_load<BWD>(a, c2, ct, i2);
+        if (n_it > 0) side_issue<BWD, QH>(a, c0, i0, side, ct);
         tc::cp_async_commit();
-        if (cb + 1 < ce) side_issue<BWD, QH>(a, i1, side + a.side_bytes, ct);
+        if (n_it > 1) side_issue<BWD, QH>(a, c1, i1, side + a.side_bytes, ct);
         tc::cp_async_commit();
-        for (int ch = cb; ch < ce; ++ch) {
-            const int it = ch - cb;
-            if (ch + 3 < ce) info_load<BWD>(a, ch + 3, ct, i3);
+        for (int it = 0; it < n_it; ++it) {
+            const int c4 = cid(it + 4);
+            if (it + 3 < n_it) info_load<BWD>(a, c3, ct, i3);
             const int slot = it % SA;
             const uint32_t u = (uint32_t)(it / SA);
             uint8_t *st = sm + (size_t)slot * a.stage_bytes;
@@ -579,30 +559,35 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
             }
             {
                 TDBG_T0;
-                if constexpr (BWD) convert_bwd<D, QH>(a, i0, sd, st, ct, ch);
-                else convert_fwd<D, QH>(a, i0, sd, st, ct, ch, cb);
+                if constexpr (BWD) convert_bwd<D, QH>(a, i0, sd, st, ct, c0);
+                else convert_fwd<D, QH>(a, i0, sd, st, ct);
                 if (ct == 0) TDBG_ADD(4);
             }
             // every converter thread is past the barrier inside convert: the slot
-            // read at step it - 1 is free for chunk ch + 2
-            if (ch + 2 < ce)
-                side_issue<BWD, QH>(a, i2, side + (size_t)((it + 2) % kSideSlots) * a.side_bytes, ct);
+            // read at step it - 1 is free for step it + 2
+            if (it + 2 < n_it)
+                side_issue<BWD, QH>(a, c2, i2, side + (size_t)((it + 2) % kSideSlots) * a.side_bytes, ct);
             tc::cp_async_commit();
             tc::fence_async_smem();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&conv[slot]);
+            c0 = c1; c1 = c2; c2 = c3; c3 = c4;
             i0 = i1; i1 = i2; i2 = i3;
         }
         tc::cp_async_wait<0>();
     } else {
         const int qd = warp & 3;
-        uint8_t *ew = reinterpret_cast<uint8_t *>(stg_all) + (size_t)(warp - kEpiWarp0) * kEpiWarpBytes;
-        float *stg = reinterpret_cast<float *>(ew);
-        uint8_t *idsm = ew + 32 * kStg * 4;
-        int *netsm = reinterpret_cast<int *>(idsm + 32 * 32);
-        float *wsm = reinterpret_cast<float *>(netsm + 32 * 4);
-        for (int t = tb, lt = 0; t < te; ++t, ++lt) {
+        float *stg = stg_all + (size_t)(warp - kEpiWarp0) * 32 * kStg;
+        EpiIn<4 * QH> cur, nxt;
+        if constexpr (BWD) {
+            if (n_t > 0) epi_in_load<4 * QH>(a, t0, qd * 32 + lane, cur);
+        }
+        for (int lt = 0; lt < n_t; ++lt) {
+            const int t = t0 + lt * tstride;
             const int b = lt & 1;
+            if constexpr (BWD) {
+                if (lt + 1 < n_t) epi_in_load<4 * QH>(a, t + tstride, qd * 32 + lane, nxt);
+            }
             {
                 TDBG_T0;
                 wait_sleep(&accfull[b], (uint32_t)((lt / 2) & 1));
@@ -610,9 +595,10 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
             }
             tc::fence_after();
             TDBG_T0;
-            const uint32_t tacc = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * D);
+            const uint32_t tacc = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * 2 * D);
             if constexpr (BWD) {
-                epi_bwd<D, QH>(a, t, tacc, stg, idsm, netsm, wsm, lane, &accempty[b]);
+                epi_bwd<D, QH>(a, cur, tacc, stg, lane, &accempty[b]);
+                cur = nxt;
             } else {
                 epi_fwd<D>(a, t, tacc, stg, lane);
                 tc::fence_before();
@@ -624,7 +610,14 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
     }
     tc::fence_before();
     __syncthreads();
-    if (a.dbg && tid == 0) atomicAdd(a.dbg + blockIdx.x * 16 + 8, (unsigned long long)(clock64() - kt0));
+    if (a.dbg && tid == 0) {
+        const long long kt1 = clock64();
+        atomicAdd(a.dbg + blockIdx.x * 16 + 8, (unsigned long long)(kt1 - kt0));
+        a.dbg[blockIdx.x * 16 + 10] = (unsigned long long)(kt0 - kt00);   // setup
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        a.dbg[blockIdx.x * 16 + 12] = g;                                  // end (ns)
+    }
     if (warp == 1) {
         tc::fence_after();
         tc::tmem_dealloc(tmem, ncols);
@@ -645,11 +638,14 @@ void launch(const TileSet &ts, TsArgs &a, int D, bool bwd, cudaStream_t s) {
     a.rows = ts.rows;
     a.chunk_beg = ts.chunk_beg;
     a.halo = ts.halo;
-    a.eptr = ts.eptr;
-    a.cedge = ts.cedge;
+    a.abits = ts.abits;
     a.cta_beg = ts.cta_beg;
+    a.cta_chunks = ts.cta_chunks;
+    a.cta_tiles = ts.cta_tiles;
+    a.tile_stride = ts.tile_stride;
+    a.n_tiles = ts.n_tiles;
     a.stage_bytes = kATile + 256u * (uint32_t)D;
-    a.side_bytes = (uint32_t)((bwd ? 2 * kSideEB : 2 * kSideE + 64 * a.k * 5) + 127) & ~127u;
+    a.side_bytes = (uint32_t)(kSideA + (bwd ? 0 : 64 * a.k * 5) + 127) & ~127u;
     const size_t budget = 227 * 1024 - 1024 - kStgBytes - (size_t)kSideSlots * a.side_bytes - 512;
     a.SA = (int)std::min<size_t>(kMaxSA, budget / a.stage_bytes);
     DR_CHECK(a.SA >= 2, DR_ERR_UNSUPPORTED, "tspmm: shared memory budget");
@@ -672,9 +668,19 @@ void launch(const TileSet &ts, TsArgs &a, int D, bool bwd, cudaStream_t s) {
         unsigned long long h[148 * 16];
         DR_CUDA(cudaStreamSynchronize(s));
         DR_CUDA(cudaMemcpy(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost));
-        double t[16] = {0};
-        for (int b = 0; b < grid; ++b)
-            for (int q = 0; q < 16; ++q) t[q] += (double)h[b * 16 + q] / grid;
+        double t[16] = {0}, tmax = 0, setup_max = 0;
+        unsigned long long g0 = ~0ull, g1 = 0, g0max = 0;
+        for (int b = 0; b < grid; ++b) {
+            for (int q = 0; q < 10; ++q) t[q] += (double)h[b * 16 + q] / grid;
+            tmax = std::max(tmax, (double)h[b * 16 + 8]);
+            setup_max = std::max(setup_max, (double)h[b * 16 + 10]);
+            g0 = std::min(g0, h[b * 16 + 11]);
+            g0max = std::max(g0max, h[b * 16 + 11]);
+            g1 = std::max(g1, h[b * 16 + 12]);
+        }
+        fprintf(stderr, "[tspmm %s] max CTA kcycles %.1f, max setup kcycles %.1f, CTA start spread %.1f us, "
+                "first start -> last end %.1f us\n", bwd ? "bwd" : "fwd", tmax / 1e3, setup_max / 1e3,
+                (g0max - g0) / 1e3, (g1 - g0) / 1e3);
         fprintf(stderr,
                 "[tspmm %s D=%d k=%d tiles=%d chunks=%lld SA=%d] kcycles/CTA: total %.1f | prod wait "
                 "%.1f | mma wait conv %.1f acc %.1f | conv pre %.1f wait %.1f work %.1f | epi wait "
@@ -706,24 +712,15 @@ void launch_tspmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, i
     note_launch("tspmm_fwd");
 }
 
-void launch_tspmm_bwd(const RelDev &r, const float *dz, bool apply_c, const RelDev *r2,
-                      const float *dz2, bool apply_c2, const float *root, const uint8_t *hidx,
-                      int k, int dim, float *g_kept, float *dx, cudaStream_t s) {
+void launch_tspmm_bwd(const RelDev &r, const float *dz, bool apply_c, const float *extra,
+                      const uint8_t *hidx, int k, int dim, float *g_kept, float *dx, cudaStream_t s) {
     TsArgs a{};
     a.k = k;
     a.hidx = hidx;
     a.dz = dz;
     a.dzc = apply_c ? r.c : nullptr;
     a.s = r.s;
-    if (r2) {
-        a.p_colptr = r2->colptr;
-        a.p_row = r2->row;
-        a.p_ewT = r2->ewT;
-        a.p_s = r2->s;
-        a.p_c = apply_c2 ? r2->c : nullptr;
-        a.p_dz = dz2;
-    }
-    a.root = root;
+    a.root = extra;
     a.dx = dx;
     a.g_kept = g_kept;
     ProfScope ps("spmm_bwd", s);

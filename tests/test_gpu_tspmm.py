@@ -84,8 +84,9 @@ def test_tspmm_matches_oracle_and_simt(designs, name, D, k, monkeypatch):
     monkeypatch.setenv("DR_TSPMM", "0")
     z_s = dr.spmm_fwd(g, "near", val, idx, D)
     gk_s, _ = dr.spmm_bwd(g, "near", dz, val, idx, D)
-    assert row_err(to_np(z), to_np(z_s).astype(np.float64)) <= 1e-5
-    assert row_err(to_np(gk), to_np(gk_s).astype(np.float64)) <= 1e-5
+    # (bf16 hi/lo split: |x - hi - lo| <= 2^-17 |x| per term on the tensor-core side)
+    assert row_err(to_np(z), to_np(z_s).astype(np.float64)) <= 4e-5
+    assert row_err(to_np(gk), to_np(gk_s).astype(np.float64)) <= 4e-5
 
 
 @pytest.mark.parametrize("D,k", [(64, 8), (128, 16)])

@@ -16,3 +16,5 @@ for f in ['gpurun_out/ab_tiles_c2.txt','gpurun_out/ab_tiles_c4.txt']:
             name, js = line.split(' ',1); j=json.loads(js); sk=j['seq_kernels_ms']
             print(f[-6:-4], name, 'layer', j['layer.fwd_bwd'], {k:v for k,v in sk.items() if 'spmm' in k}, 'sum', round(sum(sk.values()),3))
 PY
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 120 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+python profiles/summarize.py gpurun_out/launches_c2.csv 2 | head -20
