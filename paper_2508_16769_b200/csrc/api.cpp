@@ -347,21 +347,25 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
     if (dxc || dxn) {
         // dZ'_psi = c_psi (dY_psi Wn_psi^T) (row-scaled by the destination normaliser),
         // with the Sage root term (dY_psi Wr_psi^T) at the kept indices as extra columns
+        // split: write dZ' as [hi | lo] bf16 rows for the tensor-core tiled SSpMM;
+        // returns whether it did
         auto dzk = [&](int64_t n, int Kd, const float *dy, int mode, const float *W,
                        const float *Wr, int Kr, const uint8_t *ridx, int rk, float *root,
-                       const float *c, float *out, uint8_t *img, cudaStream_t s) {
+                       const float *c, float *out, uint8_t *img, cudaStream_t s,
+                       bool split) -> bool {
             Tc2RowsDesc d;
             d.n = n; d.N = Kd + (Wr ? Kr : 0); d.G = 1; d.epi = kEpi2Dz;
             d.nseg[0] = 1;
             d.seg[0][0].A = dy; d.seg[0][0].K = D; d.seg[0][0].mask_mode = mode;
             d.mask_in = mask; d.mask_width = D;
             d.bimg[0] = img; d.n_dz = Kd; d.crow = c; d.dz = out;
+            d.dz_split = split;
             if (Wr) { d.root_idx = ridx; d.root_k = rk; d.root = root; }
             if (tc2_rows_supported(d)) {       // B_op[n][kk] = W[n][kk]
                 launch_tc2_pack_b(W, D, D, Kd, 0, d.N, false, img, s);
                 if (Wr) launch_tc2_pack_b(Wr, D, D, Kr, Kd, d.N, false, img, s);
                 launch_tc2_rows(d, s);
-                return;
+                return split;
             }
             ProjBwdArgs a;
             a.n = n; a.N = D; a.K = Kd; a.dy = dy; a.mask = mask; a.mask_mode = mode;
@@ -373,32 +377,36 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
                 r.Wr = Wr; r.hidx = ridx; r.out = root;
                 launch_root_dots(r, s);
             }
+            return false;
         };
+        const RelDev &rn = g->rel[DR_NEAR];
+        const bool near_tiled = dxc && !rn.ewT && rn.n_src == nc &&
+                                tspmm_supported(rn.tilesT, L->d_cell, L->k_cell);
+        bool near_split = false;
         {
             TagScope t("near");
-            dzk(nc, L->d_cell, dyc, mode_near, L->wn[DR_NEAR], L->wr[DR_NEAR], L->d_cell, hci,
-                L->k_cell, root_c, g->rel[DR_NEAR].c, dz[DR_NEAR],
-                (uint8_t *)(tp + T.img_dz[DR_NEAR]), s0);
+            near_split = dzk(nc, L->d_cell, dyc, mode_near, L->wn[DR_NEAR], L->wr[DR_NEAR],
+                             L->d_cell, hci, L->k_cell, root_c, g->rel[DR_NEAR].c, dz[DR_NEAR],
+                             (uint8_t *)(tp + T.img_dz[DR_NEAR]), s0, near_tiled);
         }
         {
             TagScope t("pins");
             dzk(nn, L->d_cell, dyn, kMaskNone, L->wn[DR_PINS], L->wr[DR_PINS], L->d_net, hni,
                 L->k_net, root_n, g->rel[DR_PINS].c, dz[DR_PINS],
-                (uint8_t *)(tp + T.img_dz[DR_PINS]), s1);
+                (uint8_t *)(tp + T.img_dz[DR_PINS]), s1, false);
         }
         if (!seq) DR_CUDA(cudaEventRecord(C.ev[0], s1));                           // dZ_pins, root_n
         {
             TagScope t("pinned");
             dzk(nc, L->d_net, dyc, mode_pinned, L->wn[DR_PINNED], nullptr, 0, nullptr, 0, nullptr,
-                g->rel[DR_PINNED].c, dz[DR_PINNED], (uint8_t *)(tp + T.img_dz[DR_PINNED]), s2);
+                g->rel[DR_PINNED].c, dz[DR_PINNED], (uint8_t *)(tp + T.img_dz[DR_PINNED]), s2, false);
         }
         // SSpMM per source node type (Alg. 2 stage 2-3, ownership instead of atomics)
         if (dxc) {
             if (!seq) DR_CUDA(cudaStreamWaitEvent(s0, C.ev[0], 0));
             BwdTerm t0{&g->rel[DR_NEAR], dz[DR_NEAR], false}, t1{&g->rel[DR_PINS], dz[DR_PINS], false};
             TagScope t("cell");
-            const RelDev &rn = g->rel[DR_NEAR];
-            if (!rn.ewT && rn.n_src == nc && tspmm_supported(rn.tilesT, L->d_cell, L->k_cell)) {
+            if (near_tiled) {
                 // tensor-core tiled near term; the low-degree pins term (+ the root
                 // term) first goes to root_c in place with the SIMT kernel, and the
                 // tiled kernel adds it in its epilogue as it would the root term
@@ -408,8 +416,8 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
                                     L->wr[DR_NEAR] ? root_c : nullptr, hci, L->k_cell, L->d_cell,
                                     root_c, nullptr, false, s0);
                 }
-                launch_tspmm_bwd(rn, dz[DR_NEAR], false, root_c, hci, L->k_cell, L->d_cell,
-                                 nullptr, dxc, s0);
+                launch_tspmm_bwd(rn, dz[DR_NEAR], near_split, false, root_c, hci, L->k_cell,
+                                 L->d_cell, nullptr, dxc, s0);
             } else {
                 launch_spmm_bwd(g->src_cell, nc, t0, t1, L->wr[DR_NEAR] ? root_c : nullptr, hci,
                                 L->k_cell, L->d_cell, nullptr, dxc, false, s0);

@@ -178,7 +178,9 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1,
 bool tspmm_supported(const TileSet &ts, int dim, int k);
 void launch_tspmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
                       float *z, cudaStream_t s);
-void launch_tspmm_bwd(const RelDev &r, const float *dz, bool apply_c, const float *extra,
-                      const uint8_t *hidx, int k, int dim, float *g_kept, float *dx, cudaStream_t s);
+// dz_split: dz holds [hi | lo] bf16 rows (tc2 dz epilogue, Tc2RowsDesc::dz_split).
+void launch_tspmm_bwd(const RelDev &r, const float *dz, bool dz_split, bool apply_c,
+                      const float *extra, const uint8_t *hidx, int k, int dim, float *g_kept,
+                      float *dx, cudaStream_t s);
 
 }  // namespace dr

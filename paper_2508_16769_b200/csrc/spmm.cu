@@ -498,7 +498,7 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, c
     if (n_src <= 0) return;
     if (t0.rel && !t1.rel && !t0.rel->ewT && !accumulate && tspmm_supported(t0.rel->tilesT, dim, k) &&
         t0.rel->n_src == n_src) {                           // tensor-core tiled path
-        launch_tspmm_bwd(*t0.rel, t0.dz, t0.apply_c, root, hidx, k, dim, g_kept, dx, s);
+        launch_tspmm_bwd(*t0.rel, t0.dz, false, t0.apply_c, root, hidx, k, dim, g_kept, dx, s);
         return;
     }
     const int P = choose_P_bwd(k);

@@ -176,6 +176,19 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
     return d;
 }
 
+// Shared-memory matrix descriptor: MN-major, SWIZZLE_128B (cute Layout_MN_SW128_Atom):
+// 8 K-rows x 128 B atoms (16-B chunk c of K-row r at (c ^ (r & 7))), SBO = byte
+// stride between 8-K-row groups, LBO = byte stride between 128-B-wide MN atoms.
+__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
 // Byte offset of fp32 element (r, k) (k < 32) inside a K-major SW128 atom tile.
 __device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t k) {
     return r * 128u + ((((k >> 2) ^ (r & 7u)) & 7u) << 4) + ((k & 3u) << 2);

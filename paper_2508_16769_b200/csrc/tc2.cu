@@ -108,6 +108,7 @@ struct R2Args {
     uint32_t *mask_out;
     float *tap_a, *tap_b;
     int n_dz;
+    int dz_split;
     const float *crow;
     float *dz;
     const uint8_t *root_idx;
@@ -266,6 +267,30 @@ __device__ __forceinline__ void epi_store16(const CUtensorMap *map, int col, int
     sb ^= 1;
 }
 
+// Split variant: 16 columns of this warp's 32 rows as bf16 hi (box at column
+// col of the [n x 2W] bf16 map) and lo (column W + col), 1 KB boxes each.
+__device__ __forceinline__ void epi_store16_split(const CUtensorMap *map, int col, int W, int64_t row0,
+                                                  const float *v, uint8_t *stage, int &sb, int lane) {
+    uint8_t *buf = stage + sb * 2048;
+    if (lane == 0) tc::bulk_wait_read<1>();
+    __syncwarp();
+    uint32_t h[8], l[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) tc::split_bf16x2(v[2 * c], v[2 * c + 1], h[c], l[c]);
+    *reinterpret_cast<uint4 *>(buf + lane * 32) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4 *>(buf + lane * 32 + 16) = make_uint4(h[4], h[5], h[6], h[7]);
+    *reinterpret_cast<uint4 *>(buf + 1024 + lane * 32) = make_uint4(l[0], l[1], l[2], l[3]);
+    *reinterpret_cast<uint4 *>(buf + 1024 + lane * 32 + 16) = make_uint4(l[4], l[5], l[6], l[7]);
+    tc::fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+        tc::tma_store_2d(map, col, (int)row0, buf);
+        tc::tma_store_2d(map, W + col, (int)row0, buf + 1024);
+        tc::bulk_commit();
+    }
+    sb ^= 1;
+}
+
 // epilogue warp (quarter qd): rows r0 + 32 qd + lane of accumulator columns at `acc`
 __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int64_t r0, int qd,
                                               int lane, const float *bias_s, uint8_t *stage,
@@ -306,7 +331,8 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
                 if (jj < a.n_dz) {
 #pragma unroll
                     for (int q = 0; q < 16; ++q) v[q] *= cr;
-                    epi_store16(&a.tmap_out, jj, row0, v, stage, sb, lane);
+                    if (a.dz_split) epi_store16_split(&a.tmap_out, jj, a.n_dz, row0, v, stage, sb, lane);
+                    else epi_store16(&a.tmap_out, jj, row0, v, stage, sb, lane);
                 } else if (a.root && ok) {
                     const int j0 = jj - a.n_dz;
                     while (p < rk) {
@@ -1158,6 +1184,18 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // output map: [n x W] fp32 row-major, box = 16 columns x 32 rows, SWIZZLE_64B
+// [n x 2W] bf16 (split dz rows: hi | lo), box = 16 columns x 32 rows, no swizzle
+static void make_out_tmap_split(CUtensorMap *m, void *Y, int64_t n, int W) {
+    const cuuint64_t dims[2] = {(cuuint64_t)(2 * W), (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)W * 4};
+    const cuuint32_t box[2] = {16, 32};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Y, dims, strides, box,
+                                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DR_CHECK(r == CUDA_SUCCESS, DR_ERR_CUDA, "cuTensorMapEncodeTiled (split out) failed");
+}
+
 static void make_out_tmap(CUtensorMap *m, float *Y, int64_t n, int W) {
     const cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)n};
     const cuuint64_t strides[1] = {(cuuint64_t)W * 4};
@@ -1262,7 +1300,9 @@ void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
     }
     a.epi_off = (uint32_t)((a.SA * st_bytes + (size_t)a.SB * a.bchunk + 1023) / 1024 * 1024);
     const size_t smem = (size_t)a.epi_off + kEpiStage + 1024;
-    if (d.epi == kEpi2Dz) make_out_tmap(&a.tmap_out, d.dz, d.n, d.n_dz);
+    a.dz_split = d.dz_split ? 1 : 0;
+    if (d.epi == kEpi2Dz && d.dz_split) make_out_tmap_split(&a.tmap_out, d.dz, d.n, d.n_dz);
+    else if (d.epi == kEpi2Dz) make_out_tmap(&a.tmap_out, d.dz, d.n, d.n_dz);
     else make_out_tmap(&a.tmap_out, d.y, d.n, d.N);
     const int64_t tiles = (d.n + kTile - 1) / kTile;
     const int64_t grid = tiles < 148 ? tiles : 148;

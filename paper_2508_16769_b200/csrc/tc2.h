@@ -48,6 +48,10 @@ struct Tc2RowsDesc {
     int n_dz = 0;
     const float *crow = nullptr;
     float *dz = nullptr;
+    // dz_split: write dz rows as [hi | lo] bf16 halves (x = hi + lo, |x - hi - lo| <=
+    // 2^-17 |x|, 4 n_dz bytes per row as fp32 would take): the operand format the
+    // tensor-core tiled SSpMM (tspmm.cu) gathers without converting
+    bool dz_split = false;
     const uint8_t *root_idx = nullptr;
     int root_k = 0;
     float *root = nullptr;

@@ -70,6 +70,7 @@ struct TsArgs {
     // (standalone ABI: dz not yet row-scaled), s_j of the tiled relation, and the
     // extra per-kept-entry term added in the epilogue (root term + other relation)
     const float *dz, *dzc, *s;
+    const uint8_t *dzs;               // split dZ' rows ([hi | lo] bf16, 4 D bytes), or null
     const float *root;
     float *dx, *g_kept;
     unsigned long long *dbg;          // DR_TS_DEBUG role timers (cycles per CTA), else null
@@ -125,7 +126,7 @@ struct CInfo {
 };
 template <bool BWD>
 __device__ __forceinline__ void info_load(const TsArgs &a, int64_t ch, int ct, CInfo &p) {
-    if constexpr (!BWD) {
+    if (!BWD || a.dzs) {
         p.id = __ldg(a.halo + ch * kTsChunk + (ct >> 2));
     } else {
         p.h0 = __ldg(a.halo + ch * kTsChunk + (ct & 31));
@@ -167,6 +168,28 @@ __device__ __forceinline__ void side_issue(const TsArgs &a, int64_t ch, const CI
                 }
             }
         }
+    }
+}
+
+// Backward, split dZ' input: the 64 halo rows' [hi | lo] bf16 halves are copied
+// (cp.async, 16-B pieces) straight into the MN-major SW128 B operand of the
+// stage -- K = halo slot u (row u % 8 of 8-row group u / 8, 1 KB apart), N =
+// feature (64-feature atoms 8 KB apart, hi atoms then lo atoms): no conversion.
+// Thread ct copies row u = ct / 4, pieces h, h + 4, ... (h = ct % 4); rows with
+// no halo id are zero-filled.
+template <int D>
+__device__ __forceinline__ void gather_split(const TsArgs &a, const CInfo &p, uint8_t *B, int ct) {
+    constexpr int NP = D / 4;                  // 16-B pieces per split row (hi + lo)
+    const int u = ct >> 2, h = ct & 3;
+    const uint8_t *src = a.dzs + (int64_t)(p.id >= 0 ? p.id : 0) * (4 * D);
+    const uint32_t nb = p.id >= 0 ? 16u : 0u;
+    uint8_t *rowb = B + (u >> 3) * 1024 + (u & 7) * 128;
+#pragma unroll
+    for (int q = 0; q < NP / 4; ++q) {
+        const int pc = h + 4 * q;              // piece: hi 0 .. D/8-1, lo D/8 .. D/4-1
+        const int lo = pc >= D / 8, c = lo ? pc - D / 8 : pc;
+        const int atom = (lo ? D / 64 : 0) + (c >> 3), cc = c & 7;
+        tc::cp_async16(rowb + atom * 8192 + ((cc ^ (u & 7)) << 4), src + 16 * pc, nb);
     }
 }
 
@@ -462,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
     const int tstride = a.tile_stride;
 
     if (warp == 0) {
-        if constexpr (BWD) {
+        if (BWD && !a.dzs) {
             int nid0 = -1, nid1 = -1, cn = cid(1);
             if (n_it > 0) {
                 const int c = cid(0);
@@ -495,7 +518,8 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t idesc = tc::idesc_bf16(kTsRows, 2 * D);
+            const bool mn = BWD && a.dzs != nullptr;          // split input: MN-major B
+            const uint32_t idesc = tc::idesc_bf16(kTsRows, 2 * D) | (mn ? (1u << 16) : 0u);
             int it = 0;
             for (int lt = 0; lt < n_t; ++lt) {
                 const int t = t0 + lt * tstride;
@@ -521,7 +545,9 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
 #pragma unroll
                     for (int ks = 0; ks < kTsChunk / 16; ++ks) {
                         const uint32_t ko = ks * 32;
-                        tc::mma_bf16(d, tc::desc_sw128(sa + ko), tc::desc_sw128(sbh + ko), idesc,
+                        const uint64_t bd = mn ? tc::desc_mn_sw128(sbh + ks * 2048u, 8192u, 1024u)
+                                               : tc::desc_sw128(sbh + ko);
+                        tc::mma_bf16(d, tc::desc_sw128(sa + ko), bd, idesc,
                                      (ch == c0 && ks == 0) ? 0u : 1u);
                     }
                     tc::mma_commit(&empty[slot]);
@@ -537,12 +563,19 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
         // i0..i2 (it..it+2); side copies are in flight for it, it + 1
         int c0 = cid(0), c1 = cid(1), c2 = cid(2), c3 = cid(3);
         CInfo i0{}, i1{}, i2{}, i3{};
+        const bool split = BWD && a.dzs != nullptr;
         if (n_it > 0) info_load<BWD>(a, c0, ct, i0);
         if (n_it > 1) info_load<BWD>(a, c1, ct, i1);
         if (n_it > 2) info_load<BWD>(a, c2, ct, i2);
-        if (n_it > 0) side_issue<BWD, QH>(a, c0, i0, side, ct);
+        if (n_it > 0) {
+            side_issue<BWD, QH>(a, c0, i0, side, ct);
+            if (split) gather_split<D>(a, i0, sm + kATile, ct);
+        }
         tc::cp_async_commit();
-        if (n_it > 1) side_issue<BWD, QH>(a, c1, i1, side + a.side_bytes, ct);
+        if (n_it > 1) {
+            side_issue<BWD, QH>(a, c1, i1, side + a.side_bytes, ct);
+            if (split) gather_split<D>(a, i1, sm + (size_t)(1 % SA) * a.stage_bytes + kATile, ct);
+        }
         tc::cp_async_commit();
         for (int it = 0; it < n_it; ++it) {
             const int c4 = cid(it + 4);
@@ -551,23 +584,50 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
             const uint32_t u = (uint32_t)(it / SA);
             uint8_t *st = sm + (size_t)slot * a.stage_bytes;
             const uint8_t *sd = side + (size_t)(it % kSideSlots) * a.side_bytes;
-            {
+            if (split) {
+                // chunk it + 2's copies go into its stage slot once the MMA of the
+                // chunk that used it (it + 2 - SA) is done, and into its side slot
+                // (read at step it - 1 by everyone: the barrier of step it - 1... is
+                // passed by all before anyone reaches step it's issue -- see below)
+                {
+                    TDBG_T0;
+                    if (it + 2 < n_it) {
+                        const int s2 = (it + 2) % SA;
+                        const uint32_t u2 = (uint32_t)((it + 2) / SA);
+                        if (u2 > 0) tc::mbar_wait(&empty[s2], (u2 - 1) & 1u);
+                    }
+                    if (ct == 0) TDBG_ADD(3);
+                }
+                tc::named_bar(1, kConv);       // all done reading side slot (it + 2) % 3 (step it - 1)
+                if (it + 2 < n_it) {
+                    side_issue<BWD, QH>(a, c2, i2, side + (size_t)((it + 2) % kSideSlots) * a.side_bytes, ct);
+                    gather_split<D>(a, i2, sm + (size_t)((it + 2) % SA) * a.stage_bytes + kATile, ct);
+                }
+                tc::cp_async_commit();
                 TDBG_T0;
-                if constexpr (BWD) tc::mbar_wait(&full[slot], u & 1u);
-                else if (u > 0) tc::mbar_wait(&empty[slot], (u - 1) & 1u);
-                if (ct == 0) TDBG_ADD(3);
-            }
-            {
-                TDBG_T0;
-                if constexpr (BWD) convert_bwd<D, QH>(a, i0, sd, st, ct, c0);
-                else convert_fwd<D, QH>(a, i0, sd, st, ct);
+                tc::cp_async_wait<2>();        // chunk it's copies landed (this thread's)
+                tc::named_bar(1, kConv);       // ... and everyone's
+                build_a(sd, st, ct);
                 if (ct == 0) TDBG_ADD(4);
+            } else {
+                {
+                    TDBG_T0;
+                    if constexpr (BWD) tc::mbar_wait(&full[slot], u & 1u);
+                    else if (u > 0) tc::mbar_wait(&empty[slot], (u - 1) & 1u);
+                    if (ct == 0) TDBG_ADD(3);
+                }
+                {
+                    TDBG_T0;
+                    if constexpr (BWD) convert_bwd<D, QH>(a, i0, sd, st, ct, c0);
+                    else convert_fwd<D, QH>(a, i0, sd, st, ct);
+                    if (ct == 0) TDBG_ADD(4);
+                }
+                // every converter thread is past the barrier inside convert: the slot
+                // read at step it - 1 is free for step it + 2
+                if (it + 2 < n_it)
+                    side_issue<BWD, QH>(a, c2, i2, side + (size_t)((it + 2) % kSideSlots) * a.side_bytes, ct);
+                tc::cp_async_commit();
             }
-            // every converter thread is past the barrier inside convert: the slot
-            // read at step it - 1 is free for step it + 2
-            if (it + 2 < n_it)
-                side_issue<BWD, QH>(a, c2, i2, side + (size_t)((it + 2) % kSideSlots) * a.side_bytes, ct);
-            tc::cp_async_commit();
             tc::fence_async_smem();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&conv[slot]);
@@ -712,12 +772,17 @@ void launch_tspmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, i
     note_launch("tspmm_fwd");
 }
 
-void launch_tspmm_bwd(const RelDev &r, const float *dz, bool apply_c, const float *extra,
-                      const uint8_t *hidx, int k, int dim, float *g_kept, float *dx, cudaStream_t s) {
+void launch_tspmm_bwd(const RelDev &r, const float *dz, bool dz_split, bool apply_c,
+                      const float *extra, const uint8_t *hidx, int k, int dim, float *g_kept,
+                      float *dx, cudaStream_t s) {
     TsArgs a{};
     a.k = k;
     a.hidx = hidx;
     a.dz = dz;
+    if (dz_split) {
+        DR_CHECK(!apply_c, DR_ERR_INVALID_ARGUMENT, "tspmm: split dz must be row-scaled");
+        a.dzs = reinterpret_cast<const uint8_t *>(dz);
+    }
     a.dzc = apply_c ? r.c : nullptr;
     a.s = r.s;
     a.root = extra;

@@ -6,7 +6,7 @@ for C in C2 C4; do
 DR_TS_DEBUG=1 timeout 600 python profiles/spmm_ab.py $C default > gpurun_out/dbg_$C.txt 2>&1
 grep "tspmm" gpurun_out/dbg_$C.txt | sort | uniq -c | sort -rn | awk '{$1="";print}' | sort -u | grep -v "kcycles/CTA: total" | head -4
 grep "tspmm" gpurun_out/dbg_$C.txt | grep "kcycles/CTA: total" | sort -u | tail -2
-timeout 600 python profiles/spmm_ab.py $C default DR_TS_ORDER=rr > gpurun_out/ab_$C.txt 2>&1
+timeout 600 python profiles/spmm_ab.py $C default > gpurun_out/ab_$C.txt 2>&1
 python - $C <<'PY'
 import json,sys
 for line in open('gpurun_out/ab_%s.txt'%sys.argv[1]):
@@ -15,6 +15,3 @@ for line in open('gpurun_out/ab_%s.txt'%sys.argv[1]):
         print(sys.argv[1], name, 'layer', j['layer.fwd_bwd'], {k:v for k,v in sk.items() if 'spmm' in k}, 'sum', round(sum(sk.values()),3))
 PY
 done
-timeout 900 ncu --set full --clock-control none -k regex:tspmm -c 2 -o /tmp/ts_c4 python bench.py --workload C4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_ts.log 2>&1
-ncu -i /tmp/ts_c4.ncu-rep --page raw --csv > gpurun_out/ts_c4_raw.csv 2>/dev/null
-python profiles/ncu_table.py gpurun_out/ts_c4_raw.csv | cut -c1-250
