@@ -45,6 +45,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
     while (!mbar_try_wait(bar, phase)) {
     }
 }
+// Wait with a short sleep between probes: for roles off the critical path
+// (producer, MMA issuer, epilogue), so their polling leaves issue slots to the
+// warps sharing their SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t phase) {
+    while (!mbar_try_wait(bar, phase)) __nanosleep(64);
+}
 
 // ---------------------------------------------------------------- bulk copy (TMA engine)
 // 1-D global -> shared copy of `bytes` (multiple of 16, 16-B aligned), completion

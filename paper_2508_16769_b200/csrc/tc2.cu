@@ -41,7 +41,7 @@ constexpr uint32_t kHalf = 16384;      // one bf16 128 x 64 tile
 constexpr int kMaskStage = 4096;       // 128 rows x up to 8 mask words
 constexpr int kRowsThreads = 320;
 constexpr int kRedThreads = 192;
-constexpr int kEpiStage = 4 * 4096;   // epilogue TMA-store staging (4 warps x 2 x 2 KB)
+constexpr int kEpiStage = 4 * 32 * 36 * 4;   // epilogue staging (4 warps x [32][36] fp32)
 constexpr int kSmemBudget = 227 * 1024 - 1024 - 4096 - kEpiStage;   // opt-in max minus alignment, static smem, staging (rows)
 constexpr int kSmemBudgetRed = 227 * 1024 - 1024 - 6144 - 1024;   // reduce kernel: 6 KB static
 constexpr int kMaxSteps = 16;
@@ -90,7 +90,6 @@ struct R2Seg {
 };
 struct R2Args {
     CUtensorMap tmap[2][2];        // dense segments: [n x K] fp32, box 64 cols x 128 rows
-    CUtensorMap tmap_out;          // y (n x N) or dz (n x n_dz) fp32, box 16 cols x 32 rows, SW64
     int64_t n;
     int N, G, S;
     R2Step step[kMaxSteps];
@@ -235,113 +234,119 @@ __device__ __forceinline__ void rows_convert(const R2Args &a, const R2Step &sp, 
     }
 }
 
-__device__ __forceinline__ float pick16(const float *v, int i) {
-    float r = v[0];
-#pragma unroll
-    for (int q = 1; q < 16; ++q) r = (i == q) ? v[q] : r;
-    return r;
-}
 
 // epilogue warp (quarter qd): rows r0 + 32 qd + lane of accumulator columns at `acc`
-// Stage 16 columns of this warp's 32 rows (lane = row) in a 2-KB SW64 box and
-// TMA-store it to (col, row0) of the output map: coalesced, sector-complete
-// writes instead of 32 row-strided 16-B stores per instruction. Two buffers
-// per warp; a buffer is rewritten once the store issued two calls ago has
-// finished reading it.
-__device__ __forceinline__ void epi_store16(const CUtensorMap *map, int col, int64_t row0,
-                                            const float *v, uint8_t *stage, int &sb, int lane) {
-    uint8_t *buf = stage + sb * 2048;
-    if (lane == 0) tc::bulk_wait_read<1>();
-    __syncwarp();
+// Epilogue staging: per warp a [32 rows][32 columns] fp32 tile (row stride 36
+// floats: conflict-free 128-bit row writes and column-quad reads). A block of
+// 32 accumulator columns goes TMEM -> registers (lane = row) -> staging ->
+// coalesced stores (lane -> row 4 i + lane / 8, column quad lane % 8: each
+// instruction writes 4 rows x 128 B). No asynchronous store state to wait on.
+constexpr int kEStg = 36;
+__device__ __forceinline__ void stg_put(float *stg, int lane, const float *v) {
+    float4 *o = reinterpret_cast<float4 *>(stg + lane * kEStg);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const uint32_t off = (uint32_t)lane * 64u + ((((uint32_t)c ^ ((uint32_t)lane >> 1)) & 3u) << 4);
-        *reinterpret_cast<float4 *>(buf + off) = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-    }
-    tc::fence_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-        tc::tma_store_2d(map, col, (int)row0, buf);
-        tc::bulk_commit();
-    }
-    sb ^= 1;
+    for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
 }
-
-// Split variant: 16 columns of this warp's 32 rows as bf16 hi (box at column
-// col of the [n x 2W] bf16 map) and lo (column W + col), 1 KB boxes each.
-__device__ __forceinline__ void epi_store16_split(const CUtensorMap *map, int col, int W, int64_t row0,
-                                                  const float *v, uint8_t *stage, int &sb, int lane) {
-    uint8_t *buf = stage + sb * 2048;
-    if (lane == 0) tc::bulk_wait_read<1>();
-    __syncwarp();
-    uint32_t h[8], l[8];
+// rows row0 .. row0 + 31 (< n) of an fp32 [n x W] matrix, columns [j, j + 32)
+__device__ __forceinline__ void stg_out_f32(const float *stg, float *out, int64_t W, int64_t row0,
+                                            int64_t n, int j, int lane) {
+    const int cq = lane & 7, rs = lane >> 3;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) tc::split_bf16x2(v[2 * c], v[2 * c + 1], h[c], l[c]);
-    *reinterpret_cast<uint4 *>(buf + lane * 32) = make_uint4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<uint4 *>(buf + lane * 32 + 16) = make_uint4(h[4], h[5], h[6], h[7]);
-    *reinterpret_cast<uint4 *>(buf + 1024 + lane * 32) = make_uint4(l[0], l[1], l[2], l[3]);
-    *reinterpret_cast<uint4 *>(buf + 1024 + lane * 32 + 16) = make_uint4(l[4], l[5], l[6], l[7]);
-    tc::fence_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-        tc::tma_store_2d(map, col, (int)row0, buf);
-        tc::tma_store_2d(map, W + col, (int)row0, buf + 1024);
-        tc::bulk_commit();
+    for (int i = 0; i < 8; ++i) {
+        const int r = 4 * i + rs;
+        const float4 v = *reinterpret_cast<const float4 *>(stg + r * kEStg + 4 * cq);
+        if (row0 + r < n && j + 4 * cq < W) __stcs(reinterpret_cast<float4 *>(out + (row0 + r) * W + j) + cq, v);
     }
-    sb ^= 1;
+}
+// split output ([hi | lo] bf16 rows of 2 W halves): hi at column j, lo at W + j
+__device__ __forceinline__ void stg_out_split(const float *stg, uint8_t *out, int64_t W, int64_t row0,
+                                              int64_t n, int j, int lane) {
+    const int cq = lane & 7, rs = lane >> 3;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int r = 4 * i + rs;
+        const float4 v = *reinterpret_cast<const float4 *>(stg + r * kEStg + 4 * cq);
+        uint2 h, l;
+        tc::split_bf16x2(v.x, v.y, h.x, l.x);
+        tc::split_bf16x2(v.z, v.w, h.y, l.y);
+        if (row0 + r < n && j + 4 * cq < W) {
+            uint8_t *rowp = out + (row0 + r) * W * 4;
+            __stcs(reinterpret_cast<uint2 *>(rowp + 2 * (j + 4 * cq)), h);
+            __stcs(reinterpret_cast<uint2 *>(rowp + 2 * (W + j + 4 * cq)), l);
+        }
+    }
 }
 
 // epilogue warp (quarter qd): rows r0 + 32 qd + lane of accumulator columns at `acc`
 __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int64_t r0, int qd,
-                                              int lane, const float *bias_s, uint8_t *stage,
-                                              int &sb) {
+                                              int lane, const float *bias_s, float *stg) {
     const int N = a.N;
     const int64_t row0 = r0 + qd * 32, row = row0 + lane;
     const bool ok = row < a.n;
     const uint32_t lb = acc + ((uint32_t)(qd * 32) << 16);
     if (a.epi == kEpi2Dz) {
         const float cr = (ok && a.crow) ? __ldg(a.crow + row) : 1.f;
-        uint32_t iw[8];
+        // root term: columns [n_dz, N) sampled at the row's CBSR indices (ascending),
+        // collected in registers (static indices) and stored as whole rows at the end
         const int rk = a.root_k;
+        uint32_t iw[8];
+        float rv[32];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) iw[t] = 0xffffffffu;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) rv[q] = 0.f;
         if (a.root && ok) {
             const uint8_t *ip = a.root_idx + row * rk;
 #pragma unroll
             for (int t = 0; t < 8; ++t)
                 if (4 * t < rk) {
-                    uint32_t w = 0;
+                    uint32_t w = 0xffffffffu;
 #pragma unroll
                     for (int b = 0; b < 4; ++b)
-                        if (4 * t + b < rk) w |= (uint32_t)__ldg(ip + 4 * t + b) << (8 * b);
+                        if (4 * t + b < rk)
+                            w = (w & ~(0xffu << (8 * b))) | ((uint32_t)__ldg(ip + 4 * t + b) << (8 * b));
                     iw[t] = w;
                 }
         }
-        int p = 0;                                     // next root index (ascending)
         for (int j = 0; j < N; j += 32) {
             uint32_t r[2][16];
             tc::tmem_ld16_nw(lb + (uint32_t)j, r[0]);
             if (j + 16 < N) tc::tmem_ld16_nw(lb + (uint32_t)(j + 16), r[1]);
             tc::tmem_wait_ld();
+            float v[32];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int jj = j + 16 * h;
-                if (jj >= N) break;
-                float v[16];
+            for (int q = 0; q < 16; ++q) {
+                v[q] = __uint_as_float(r[0][q]);
+                v[16 + q] = j + 16 < N ? __uint_as_float(r[1][q]) : 0.f;
+            }
 #pragma unroll
-                for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[h][q]);
-                if (jj < a.n_dz) {
+            for (int q = 0; q < 32; ++q)
+                if (j + q < a.n_dz) v[q] *= cr;        // dZ' row scale (not the root term)
+            stg_put(stg, lane, v);
+            __syncwarp();
+            if (j < a.n_dz) {
+                if (a.dz_split) stg_out_split(stg, reinterpret_cast<uint8_t *>(a.dz), a.n_dz, row0, a.n, j, lane);
+                else stg_out_f32(stg, a.dz, a.n_dz, row0, a.n, j, lane);
+            }
+            if (a.root && j + 32 > a.n_dz) {
 #pragma unroll
-                    for (int q = 0; q < 16; ++q) v[q] *= cr;
-                    if (a.dz_split) epi_store16_split(&a.tmap_out, jj, a.n_dz, row0, v, stage, sb, lane);
-                    else epi_store16(&a.tmap_out, jj, row0, v, stage, sb, lane);
-                } else if (a.root && ok) {
-                    const int j0 = jj - a.n_dz;
-                    while (p < rk) {
-                        const int id = (int)((iw[p >> 2] >> (8 * (p & 3))) & 0xffu);
-                        if (id >= j0 + 16) break;
-                        a.root[row * rk + p] = pick16(v, id - j0);
-                        ++p;
-                    }
+                for (int q = 0; q < 32; ++q) {
+                    const int c = a.n_dz + (int)((iw[q >> 2] >> (8 * (q & 3))) & 0xffu) - j;
+                    if (q < rk && c >= 0 && c < 32) rv[q] = stg[lane * kEStg + c];
                 }
+            }
+            __syncwarp();
+        }
+        if (a.root && ok) {
+            if ((rk & 3) == 0) {
+                float4 *o = reinterpret_cast<float4 *>(a.root + row * rk);
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (4 * q < rk) o[q] = make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 32; ++q)
+                    if (q < rk) a.root[row * rk + q] = rv[q];
             }
         }
         return;
@@ -357,43 +362,46 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
         }
         tc::tmem_wait_ld();
         uint32_t word = 0;
+        float y[32];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int jj = j + 16 * h;
-            if (jj >= N) break;
-            float ya[16], yb[16], y[16];
+            float ya[16], yb[16];
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-                ya[q] = __uint_as_float(ra[h][q]) + bias_s[jj + q];
-                yb[q] = a.G == 2 ? __uint_as_float(rb[h][q]) + bias_s[256 + jj + q] : 0.f;
+                ya[q] = jj < N ? __uint_as_float(ra[h][q]) + bias_s[jj + q] : 0.f;
+                yb[q] = (a.G == 2 && jj < N) ? __uint_as_float(rb[h][q]) + bias_s[256 + jj + q] : 0.f;
             }
             if (a.G == 2) {
 #pragma unroll
                 for (int q = 0; q < 16; ++q) {
                     if (a.merge == DR_MERGE_MAX) {
                         const bool m = ya[q] >= yb[q];          // Eq. 14: ties -> near
-                        y[q] = m ? ya[q] : yb[q];
+                        y[16 * h + q] = m ? ya[q] : yb[q];
                         word |= (uint32_t)m << (16 * h + q);
                     } else {
-                        y[q] = ya[q] + yb[q];
+                        y[16 * h + q] = ya[q] + yb[q];
                     }
                 }
-                if (ok && a.tap_a) {
+                if (ok && a.tap_a && jj < N) {
                     float4 *o = reinterpret_cast<float4 *>(a.tap_a + row * N + jj);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) o[q] = make_float4(ya[4 * q], ya[4 * q + 1], ya[4 * q + 2], ya[4 * q + 3]);
                 }
-                if (ok && a.tap_b) {
+                if (ok && a.tap_b && jj < N) {
                     float4 *o = reinterpret_cast<float4 *>(a.tap_b + row * N + jj);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) o[q] = make_float4(yb[4 * q], yb[4 * q + 1], yb[4 * q + 2], yb[4 * q + 3]);
                 }
             } else {
 #pragma unroll
-                for (int q = 0; q < 16; ++q) y[q] = ya[q];
+                for (int q = 0; q < 16; ++q) y[16 * h + q] = ya[q];
             }
-            epi_store16(&a.tmap_out, jj, row0, y, stage, sb, lane);
         }
+        stg_put(stg, lane, y);
+        __syncwarp();
+        stg_out_f32(stg, a.y, N, row0, a.n, j, lane);
+        __syncwarp();
         if (ok && a.G == 2 && a.mask_out) a.mask_out[row * mw + (j >> 5)] = word;
     }
 }
@@ -466,7 +474,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
                 const uint32_t u = it / SA;
                 if (u > 0) {
                     RDBG_T0;
-                    tc::mbar_wait(&empty[slot], (u - 1) & 1u);
+                    tc::mbar_wait_sleep(&empty[slot], (u - 1) & 1u);
                     if (lane == 0) RDBG_ADD(0);
                 }
                 const R2Step sp = a.step[j];
@@ -476,7 +484,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
                     const int bs = (int)(bt % SB);
                     const uint32_t bu = bt / SB;
                     if (lane == 0) {
-                        if (bu > 0) tc::mbar_wait(&bempty[bs], (bu - 1) & 1u);
+                        if (bu > 0) tc::mbar_wait_sleep(&bempty[bs], (bu - 1) & 1u);
                         tc::mbar_arrive_expect_tx(&bfull[bs], a.bchunk);
                         tc::bulk_g2s(bslots + (size_t)bs * a.bchunk,
                                      a.bimg[sp.g] + (size_t)sp.bc * a.bchunk, a.bchunk, &bfull[bs]);
@@ -495,7 +503,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
                 const uint32_t ab = (uint32_t)(t & 1);
                 if (t >= 2) {
                     RDBG_T0;
-                    tc::mbar_wait(&acce[ab], (uint32_t)(((t >> 1) - 1) & 1));
+                    tc::mbar_wait_sleep(&acce[ab], (uint32_t)(((t >> 1) - 1) & 1));
                     RDBG_ADD(2);
                 }
                 tc::fence_after();
@@ -504,17 +512,17 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
                     const int slot = (int)(it % SA);
                     {
                         RDBG_T0;
-                        tc::mbar_wait(&conv[slot], (it / SA) & 1u);
+                        tc::mbar_wait_sleep(&conv[slot], (it / SA) & 1u);
                         RDBG_ADD(1);
                     }
                     const R2Step sp = a.step[j];
                     int bs;
                     if (a.b_resident) {
                         bs = j;
-                        tc::mbar_wait(&bfull[bs], 0u);
+                        tc::mbar_wait_sleep(&bfull[bs], 0u);
                     } else {
                         bs = (int)(bt % SB);
-                        tc::mbar_wait(&bfull[bs], (bt / SB) & 1u);
+                        tc::mbar_wait_sleep(&bfull[bs], (bt / SB) & 1u);
                     }
                     tc::fence_after();
                     const R2Seg &sg = a.seg[sp.g][sp.s];
@@ -567,26 +575,23 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
     } else {
         // ---------------- epilogue
         const int qd = warp & 3;
-        uint8_t *stage = epi_stage + (size_t)(warp - 6) * 4096;
-        int sb = 0;
+        float *stg = reinterpret_cast<float *>(epi_stage + (size_t)(warp - 6) * (32 * 36 * 4));
         for (int64_t t = 0; t < my_tiles; ++t) {
             const int64_t r0 = ((int64_t)blockIdx.x + t * gridDim.x) * kTile;
             const uint32_t ab = (uint32_t)(t & 1);
             {
                 RDBG_T0;
-                tc::mbar_wait(&accf[ab], (uint32_t)((t >> 1) & 1));
+                tc::mbar_wait_sleep(&accf[ab], (uint32_t)((t >> 1) & 1));
                 if (warp == 6 && lane == 0) RDBG_ADD(5);
             }
             tc::fence_after();
             RDBG_T0;
-            rows_epilogue(a, tmem + ab * GN, r0, qd, lane, bias_s, stage, sb);
+            rows_epilogue(a, tmem + ab * GN, r0, qd, lane, bias_s, stg);
             if (warp == 6 && lane == 0) RDBG_ADD(6);
             tc::fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&acce[ab]);
         }
-        if (lane == 0) tc::bulk_wait<0>();             // stores done before smem is released
-        __syncwarp();
     }
     tc::fence_before();
     __syncthreads();
@@ -1015,7 +1020,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
             const uint32_t u = (uint32_t)(it / SA);
             if (u > 0) {
                 RDBG_T0;
-                tc::mbar_wait(&empty[slot], (u - 1) & 1u);
+                tc::mbar_wait_sleep(&empty[slot], (u - 1) & 1u);
                 if (lane == 0) RDBG_ADD(0);
             }
             red_produce(a, rbeg + it * kRRows, rend, sm + (size_t)slot * a.stage_bytes, &full[slot], lane);
@@ -1028,7 +1033,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
                 const int slot = (int)(it % SA);
                 {
                     RDBG_T0;
-                    tc::mbar_wait(&conv[slot], (uint32_t)((it / SA) & 1));
+                    tc::mbar_wait_sleep(&conv[slot], (uint32_t)((it / SA) & 1));
                     RDBG_ADD(1);
                 }
                 tc::fence_after();
@@ -1093,7 +1098,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
         // accumulator -> per-CTA partial (lane = feature row)
         const int qd = warp & 3;
         if (total > 0) {
-            tc::mbar_wait(&accf, 0u);
+            tc::mbar_wait_sleep(&accf, 0u);
             tc::fence_after();
         }
         const int m = qd * 32 + lane;
@@ -1184,29 +1189,6 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // output map: [n x W] fp32 row-major, box = 16 columns x 32 rows, SWIZZLE_64B
-// [n x 2W] bf16 (split dz rows: hi | lo), box = 16 columns x 32 rows, no swizzle
-static void make_out_tmap_split(CUtensorMap *m, void *Y, int64_t n, int W) {
-    const cuuint64_t dims[2] = {(cuuint64_t)(2 * W), (cuuint64_t)n};
-    const cuuint64_t strides[1] = {(cuuint64_t)W * 4};
-    const cuuint32_t box[2] = {16, 32};
-    const cuuint32_t es[2] = {1, 1};
-    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Y, dims, strides, box,
-                                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    DR_CHECK(r == CUDA_SUCCESS, DR_ERR_CUDA, "cuTensorMapEncodeTiled (split out) failed");
-}
-
-static void make_out_tmap(CUtensorMap *m, float *Y, int64_t n, int W) {
-    const cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)n};
-    const cuuint64_t strides[1] = {(cuuint64_t)W * 4};
-    const cuuint32_t box[2] = {16, 32};
-    const cuuint32_t es[2] = {1, 1};
-    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)Y, dims, strides, box,
-                                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    DR_CHECK(r == CUDA_SUCCESS, DR_ERR_CUDA, "cuTensorMapEncodeTiled (out) failed");
-}
-
 // [n x K] fp32 row-major, box = 64 columns x 128 rows, no swizzle (row-major
 // [128][64] landing tile), zero fill out of range
 static void make_tmap(CUtensorMap *m, const float *A, int64_t n, int K) {
@@ -1301,9 +1283,6 @@ void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
     a.epi_off = (uint32_t)((a.SA * st_bytes + (size_t)a.SB * a.bchunk + 1023) / 1024 * 1024);
     const size_t smem = (size_t)a.epi_off + kEpiStage + 1024;
     a.dz_split = d.dz_split ? 1 : 0;
-    if (d.epi == kEpi2Dz && d.dz_split) make_out_tmap_split(&a.tmap_out, d.dz, d.n, d.n_dz);
-    else if (d.epi == kEpi2Dz) make_out_tmap(&a.tmap_out, d.dz, d.n, d.n_dz);
-    else make_out_tmap(&a.tmap_out, d.y, d.n, d.N);
     const int64_t tiles = (d.n + kTile - 1) / kTile;
     const int64_t grid = tiles < 148 ? tiles : 148;
     ProfScope ps(d.epi == kEpi2Dz ? "tc_dz" : "tc_proj", s);

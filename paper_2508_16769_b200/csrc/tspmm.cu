@@ -76,11 +76,9 @@ struct TsArgs {
     unsigned long long *dbg;          // DR_TS_DEBUG role timers (cycles per CTA), else null
 };
 
-// mbarrier wait with a short sleep between probes: for the roles that are not
-// on the critical path (MMA issuer, epilogue, producer), so their polling does
-// not take issue slots from the converter warps sharing their SM sub-partition
+// mbarrier wait with a short sleep between probes (roles off the critical path)
 __device__ __forceinline__ void wait_sleep(uint64_t *bar, uint32_t phase) {
-    while (!tc::mbar_try_wait(bar, phase)) __nanosleep(64);
+    tc::mbar_wait_sleep(bar, phase);
 }
 
 #define TDBG_T0 const long long dbg_t0 = a.dbg ? clock64() : 0
