@@ -103,12 +103,17 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ algorithmic work per kernel tag
-def kernel_work(tag, d, D, k, n_layers):
+def kernel_work(tag, d, D, k, n_layers, tiled=True):
     """(bytes, flops) per launch for a profile tag, SURVEY §8(d) per-unit figures
-    (restated in DESIGN.md 'Algorithmic bytes'). Pair = 4 B value + 1 B index."""
+    (restated in DESIGN.md 'Algorithmic bytes'). Pair = 4 B value + 1 B index.
+    tiled: near's backward runs as the tensor-core tiled kernel (near term + extra)
+    after the SIMT pins term ('spmm_bwd.cell.pins', written into the extra term)."""
     parts = tag.split(".")
     kind = parts[0]
     rel = parts[-1]
+    if kind == "spmm_bwd" and rel == "pins" and len(parts) >= 3 and parts[-2] == "cell":
+        nnz_p = int(d.rel("pins")[1].size)          # pins CSC term + extra read / write
+        return nnz_p * (4 + 4 * k) + d.n_cell * (k + 4 * k + 4 * k), 0.0
     nnz = {r: int(d.rel(r)[1].size) for r in ("near", "pins", "pinned")}
     ndst = {"near": d.n_cell, "pins": d.n_net, "pinned": d.n_cell}
     nsrc = {"near": d.n_cell, "pins": d.n_cell, "pinned": d.n_net}
@@ -116,7 +121,7 @@ def kernel_work(tag, d, D, k, n_layers):
         ew = 4 if rel == "pinned" else 0          # GraphConv s_j folded into a per-edge weight
         return nnz[rel] * (4 + 5 * k + ew) + ndst[rel] * (4 + 4 * D), 0.0
     if kind == "spmm_bwd":
-        rels = ["near", "pins"] if rel == "cell" else ["pinned"]
+        rels = (["near"] if tiled else ["near", "pins"]) if rel == "cell" else ["pinned"]
         n = d.n_cell if rel == "cell" else d.n_net
         return sum(nnz[r] * (4 + 4 * k) for r in rels) + n * (k + 4 * k + 4 * D), 0.0
     if kind == "drelu":
@@ -126,52 +131,70 @@ def kernel_work(tag, d, D, k, n_layers):
         n = d.n_cell if rel == "cell" else d.n_net
         g = 2 if rel == "cell" else 1
         return n * (g * D * 4 + D * 4), 2.0 * n * D * D * g
-    if kind in ("proj_bwd_dz", "dw", "tc_dz"):
+    if kind in ("proj_bwd_dz", "dw"):
         n = ndst.get(rel, d.n_cell)
         return n * 8 * D, 2.0 * n * D * D
+    if kind == "tc_dz":     # dY read (+ merge-mask words for cell rows), dZ' written, root term
+        n = ndst.get(rel, d.n_cell)
+        root = rel in ("near", "pins")
+        mask = D // 8 if rel in ("near", "pinned") else 0
+        return (n * (4 * D + mask + 4 * D + (k + 4 * k if root else 0)),
+                2.0 * n * D * (2 * D if root else D))
     if kind == "tc_proj":
         n = d.n_cell if rel == "cell" else d.n_net
-        if rel == "cell":       # Z_near, Z_pinned read, CBSR root input, Y written
-            return n * (2 * D * 4 + 5 * k + 4 * D), 2.0 * n * D * (3 * D)
+        if rel == "cell":       # Z_near, Z_pinned read, CBSR root input, Y + mask written
+            return n * (2 * D * 4 + 5 * k + 4 * D + D // 8), 2.0 * n * D * (3 * D)
         return n * (D * 4 + 5 * k + 4 * D), 2.0 * n * D * (2 * D)
-    if kind == "tc_dw":
+    if kind == "tc_dw":     # Z rows (+ CBSR root input) and dY rows (+ mask words) read
         n = ndst.get(rel, d.n_cell)
-        kin = 2 * D if rel in ("near", "pins") else D
-        return n * (kin * 4 + D * 4), 2.0 * n * kin * D
+        root = rel in ("near", "pins")
+        mask = D // 8 if rel in ("near", "pinned") else 0
+        kin = 2 * D if root else D
+        return n * (4 * D + (5 * k if root else 0) + 4 * D + mask), 2.0 * n * kin * D
     return 0, 0.0
 
 
-def roofline(prof, d, D, k, n_layers, steps, hbm, bf16, src):
+def load_traffic(workload):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per
+    kernel tag, from the committed ncu capture (profiles/ncu_traffic.json, written
+    by profiles/traffic.py from `ncu --nvtx --print-nvtx-rename kernel` with
+    DR_NVTX=1)."""
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(tp):
+        return {}
+    return json.load(open(tp)).get(workload, {})
+
+
+def roofline(prof, d, D, k, n_layers, steps, hbm, bf16, src, workload="C2", tiled=True):
     """Dominant kernel tag by total device time; achieved = algorithmic bytes
     (or FLOPs) per launch / its mean launch time."""
     if not prof:
         return None, {}
     table = {}
+    traffic_tab = load_traffic(workload)
     for tag, (n, tot, mx) in prof.items():
-        b, f = kernel_work(tag, d, D, k, n_layers)
+        b, f = kernel_work(tag, d, D, k, n_layers, tiled)
         per = tot / max(n, 1)
         table[tag] = dict(launches=n, total_ms=round(tot, 4), mean_ms=round(per, 5),
                           gbs=round(b / (per * 1e-3) / 1e9, 1) if b and per > 0 else None,
-                          tflops=round(f / (per * 1e-3) / 1e12, 2) if f and per > 0 else None)
+                          tflops=round(f / (per * 1e-3) / 1e12, 2) if f and per > 0 else None,
+                          alg_bytes=int(b), dram_bytes_ncu=traffic_tab.get(tag))
     dom = max(prof, key=lambda t: prof[t][1])
     n, tot, _ = prof[dom]
     per_s = tot / max(n, 1) * 1e-3
-    b, f = kernel_work(dom, d, D, k, n_layers)
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(dom.split(".")[0] + "." + dom.split(".")[-1])
+    b, f = kernel_work(dom, d, D, k, n_layers, tiled)
+    traffic = traffic_tab.get(dom)
     kind = dom.split(".")[0]
     if kind.startswith("tc_"):
-        # tcgen05 3xTF32: tensor peak = measured bf16 x nominal tf32/bf16 ratio (1.1/2.25),
-        # useful flops are 1/3 of issued; report whichever roofline binds
-        tf32 = bf16 * (1.1 / 2.25)
-        t_hbm, t_tc = b / (hbm * 1e9), 3.0 * f / (tf32 * 1e12)
+        # tcgen05 with bf16 hi/lo operand splitting: 3 bf16 MMAs per useful product
+        # (issued = 3x useful flops) against the measured bf16 peak; report whichever
+        # roofline binds (HBM for every shape of these workloads)
+        t_hbm, t_tc = b / (hbm * 1e9), 3.0 * f / (bf16 * 1e12)
         if t_tc > t_hbm:
             ach = 3.0 * f / per_s / 1e12
-            rf = {"kernel": dom, "bound": "tensor", "achieved": round(ach, 2), "peak": round(tf32, 1),
-                  "unit": "TFLOP/s", "frac": round(ach / tf32, 4), "traffic": traffic,
-                  "peak_source": "MEASURED_PEAKS.json bf16 x 1.1/2.25 (tf32, issued 3xTF32 flops)"}
+            rf = {"kernel": dom, "bound": "tensor", "achieved": round(ach, 2), "peak": round(bf16, 1),
+                  "unit": "TFLOP/s", "frac": round(ach / bf16, 4), "traffic": traffic,
+                  "peak_source": "MEASURED_PEAKS.json bf16_tflops (issued = 3 x useful, bf16 hi/lo split)"}
         else:
             ach = b / per_s / 1e9
             rf = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm,
@@ -326,7 +349,8 @@ def run_ours(args):
                "note": "graph structure resident (created once); per step H2D x_cell, x_net, "
                        "labels from pinned host, D2H loss"}
 
-    rf, table = roofline(prof, d, D, k, nl, args.steps, hbm, bf16, src)
+    tiled = g.info()["tiles"][0] > 0
+    rf, table = roofline(prof, d, D, k, nl, args.steps, hbm, bf16, src, wl, tiled)
     out = None
     if rank == 0:
         if wl == "C2":

@@ -9,6 +9,8 @@
 #include <mutex>
 #include <unordered_map>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "proj.h"
 #include "tc2.h"
 
@@ -51,7 +53,23 @@ static cudaEvent_t pool_get() {
     return e;
 }
 
+// DR_NVTX=1: every launch is wrapped in an NVTX range named "<base>.<tag>", so
+// `ncu --nvtx --print-nvtx-rename kernel` reports per-tag kernel metrics (the
+// DRAM traffic of profiles/ncu_traffic.json). Off by default (no overhead).
+static bool nvtx_on() {
+    static const bool on = [] {
+        const char *e = getenv("DR_NVTX");
+        return e && atoi(e) != 0;
+    }();
+    return on;
+}
+
 ProfScope::ProfScope(const char *b, cudaStream_t st) {
+    if (nvtx_on()) {
+        const std::string name = t_tag.empty() ? std::string(b) : std::string(b) + "." + t_tag;
+        nvtxRangePushA(name.c_str());
+        nvtx = true;
+    }
     if (!t_prof) return;
     s = st;
     base = b;
@@ -60,6 +78,7 @@ ProfScope::ProfScope(const char *b, cudaStream_t st) {
 }
 
 ProfScope::~ProfScope() {
+    if (nvtx) nvtxRangePop();
     if (!a) return;
     cudaEvent_t e = nullptr;
     try {

@@ -40,6 +40,7 @@ struct ProfScope {
     cudaStream_t s = nullptr;
     cudaEvent_t a = nullptr;
     const char *base = nullptr;
+    bool nvtx = false;
     ProfScope(const char *base, cudaStream_t s);
     ~ProfScope();
 };

@@ -173,6 +173,8 @@ __global__ void __launch_bounds__(256) drelu_extract_kernel(const float *__restr
     const int lane = threadIdx.x & 31;
     const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    uint32_t ltmask;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(ltmask));
     float nv[V];
     if (warp < n) load_row<V>(x + warp * ldx, dim, vec, lane, nv);
     for (int64_t r = warp; r < n; r += nwarps) {
@@ -187,12 +189,13 @@ __global__ void __launch_bounds__(256) drelu_extract_kernel(const float *__restr
             sk[j] = (lane * V + j < dim) ? order_key(v[j]) : 0u;
             sp[j] = j;
         }
-        // odd-even transposition sort, descending by (key, -slot)
+        // odd-even transposition sort, descending by key; it only swaps on a strict
+        // '<', so it is stable: equal keys keep ascending slot (column) order
 #pragma unroll
         for (int round = 0; round < V; ++round) {
 #pragma unroll
             for (int a = round & 1; a + 1 < V; a += 2) {
-                const bool sw = sk[a] < sk[a + 1] || (sk[a] == sk[a + 1] && sp[a] > sp[a + 1]);
+                const bool sw = sk[a] < sk[a + 1];
                 const uint32_t k0 = sk[a], k1 = sk[a + 1];
                 const int p0 = sp[a], p1 = sp[a + 1];
                 sk[a] = sw ? k1 : k0;
@@ -201,11 +204,16 @@ __global__ void __launch_bounds__(256) drelu_extract_kernel(const float *__restr
                 sp[a + 1] = sw ? p0 : p1;
             }
         }
+        // k rounds: the lowest lane holding the warp-wide largest head pops it
+        // (lowest lane = lowest columns among equal keys); the winner test is a
+        // mask compare against %lanemask_lt (no bit-reverse / find-leading-one)
         int taken = 0;
+#pragma unroll 4
         for (int t = 0; t < k; ++t) {
             const uint32_t m = __reduce_max_sync(0xffffffffu, sk[0]);
-            const uint32_t b = __ballot_sync(0xffffffffu, sk[0] == m);
-            if (lane == __ffs(b) - 1) {
+            const bool mine = sk[0] == m;
+            const uint32_t b = __ballot_sync(0xffffffffu, mine);
+            if (mine && (b & ltmask) == 0u) {
                 ++taken;
 #pragma unroll
                 for (int j = 0; j + 1 < V; ++j) sk[j] = sk[j + 1];
@@ -238,7 +246,7 @@ void launch_drelu(const float *x, int64_t n, int dim, int64_t ldx, int k, float 
     ProfScope ps("drelu", s);
     const int threads = 256, rows_per_cta = threads / 32;
     int64_t blocks = (n + rows_per_cta - 1) / rows_per_cta;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > 148 * 8) blocks = 148 * 8;        // one wave: 8 x 256 threads per SM
     const int V = dim <= 32 ? 1 : dim <= 64 ? 2 : dim <= 128 ? 4 : 8;
     const bool vec = dim == 32 * V && (ldx % V) == 0 &&
                      (reinterpret_cast<uintptr_t>(x) % (4 * V)) == 0;

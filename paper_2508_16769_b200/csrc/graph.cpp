@@ -139,12 +139,16 @@ void build_tiles(int32_t n, const std::vector<int32_t> &rp, const std::vector<in
     std::vector<int32_t> tile, hl;
     T.chunk_beg.push_back(0);
     size_t pos = 0;
+    int32_t next_seed = -1;
     while (true) {
-        while (pos < (size_t)n && assigned[seq[pos]]) ++pos;
-        if (pos >= (size_t)n) break;
+        if (next_seed < 0) {
+            while (pos < (size_t)n && assigned[seq[pos]]) ++pos;
+            if (pos >= (size_t)n) break;
+            next_seed = seq[pos];
+        }
         tile.clear();
         queue.clear();
-        const int32_t s0 = seq[pos];
+        const int32_t s0 = next_seed;
         assigned[s0] = 1;
         tile.push_back(s0);
         queue.push_back(s0);
@@ -159,6 +163,19 @@ void build_tiles(int32_t n, const std::vector<int32_t> &rp, const std::vector<in
                 }
             }
         }
+        // next tile grows from the lowest-ranked unassigned neighbour of this one, so
+        // consecutive tiles (one CTA's run) are adjacent and share halo rows in L2
+        next_seed = -1;
+        int64_t best = INT64_MAX;
+        for (int32_t i : tile)
+            for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
+                const int32_t v = col[e];
+                const int64_t r = rank.empty() ? (int64_t)v : rank[v];
+                if (!assigned[v] && r < best) {
+                    best = r;
+                    next_seed = v;
+                }
+            }
         // halo: sorted distinct columns of the tile's rows
         hl.clear();
         for (int32_t i : tile)
