@@ -40,10 +40,10 @@ constexpr uint32_t kStage = 32768;     // 128 x 64 fp32 raw == bf16 hi + lo tile
 constexpr uint32_t kHalf = 16384;      // one bf16 128 x 64 tile
 constexpr int kMaskStage = 4096;       // 128 rows x up to 8 mask words
 constexpr int kRowsThreads = 320;
-constexpr int kRedThreads = 192;
+constexpr int kRedThreads = 320;     // producer, MMA, 2 x 4 converter warps
 constexpr int kEpiStage = 4 * 32 * 36 * 4;   // epilogue staging (4 warps x [32][36] fp32)
 constexpr int kSmemBudget = 227 * 1024 - 1024 - 4096 - kEpiStage;   // opt-in max minus alignment, static smem, staging (rows)
-constexpr int kSmemBudgetRed = 227 * 1024 - 1024 - 6144 - 1024;   // reduce kernel: 6 KB static
+constexpr int kSmemBudgetRed = 227 * 1024 - 1024 - 10240 - 1024;  // reduce kernel: ~10 KB static
 constexpr int kMaxSteps = 16;
 constexpr int kMaxSA = 4, kMaxSB = 16;
 
@@ -758,7 +758,7 @@ __device__ __forceinline__ void red_write(uint8_t *tile, uint32_t lo_off, int W,
 
 // converters: one stage -> A'_g (per group) and B' operands; db unit sums in colsum
 __device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int valid, int ct,
-                                            float (&colsum)[2][4]) {
+                                            float (&colsum)[2][4], int bar) {
     const uint8_t *mk = st + a.off_mask;
     int ci = 0;
     for (int g = 0; g < a.G; ++g) {
@@ -796,7 +796,7 @@ __device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int va
             }
             ++ci;
         }
-        tc::named_bar(1, 128);                      // raw reads done before writes
+        tc::named_bar(bar, 128);                      // raw reads done before writes
         if (dseg) red_write<2>(tile, kHalf, wd, dseg->m0, ct, v);
         {   // zero the CBSR rows and the unused rows [wtot, 128)
             const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -816,7 +816,7 @@ __device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int va
             }
         }
         if (has_cbsr) {
-            tc::named_bar(1, 128);                  // zeros before the scatter
+            tc::named_bar(bar, 128);                  // zeros before the scatter
             const int r = ct >> 1;
 #pragma unroll
             for (int t = 0; t < 16; ++t)
@@ -834,7 +834,7 @@ __device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int va
         float4 v[2][8];
         red_read<2>(reinterpret_cast<const float *>(tile), a.N, valid, ct, mk, a.mw, a.mask_mode, v,
                     colsum);
-        tc::named_bar(1, 128);
+        tc::named_bar(bar, 128);
         red_write<2>(tile, (uint32_t)a.N * 128u, a.N, 0, ct, v);
     }
 }
@@ -908,7 +908,7 @@ __device__ __forceinline__ void red_write_t(uint8_t *tile, uint32_t lo_off, int 
 }
 template <int G, int WD, int WC, int N>
 __device__ __forceinline__ void red_convert_t(const RdArgs &a, uint8_t *st, int valid, int ct,
-                                              float (&colsum)[2][4]) {
+                                              float (&colsum)[2][4], int bar) {
     const uint8_t *mk = st + a.off_mask;
     uint8_t *tz = st;                                   // group 0: dense rows [0, WD)
     uint8_t *th = G == 2 ? st + kStage : st;            // CBSR rows [hm0, hm0 + WC)
@@ -936,7 +936,7 @@ __device__ __forceinline__ void red_convert_t(const RdArgs &a, uint8_t *st, int 
             cw[t] = okr ? w : 0u;
         }
     }
-    tc::named_bar(1, 128);                              // raw reads done before writes
+    tc::named_bar(bar, 128);                              // raw reads done before writes
     red_write_t<WD>(tz, kHalf, 0, ct, v);
     {
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -957,7 +957,7 @@ __device__ __forceinline__ void red_convert_t(const RdArgs &a, uint8_t *st, int 
         }
     }
     if constexpr (WC > 0) {
-        tc::named_bar(1, 128);                          // zeros before the scatter
+        tc::named_bar(bar, 128);                          // zeros before the scatter
         if (r < valid) {
 #pragma unroll
             for (int t = 0; t < 16; ++t)
@@ -974,7 +974,7 @@ __device__ __forceinline__ void red_convert_t(const RdArgs &a, uint8_t *st, int 
     {   // B' = mask(dY)^T
         uint8_t *tile = st + a.off_b;
         red_read_t<N>(reinterpret_cast<const float *>(tile), valid, ct, mk, a.mw, a.mask_mode, v, colsum);
-        tc::named_bar(1, 128);
+        tc::named_bar(bar, 128);
         red_write_t<N>(tile, (uint32_t)N * 128u, 0, ct, v);
     }
 }
@@ -986,7 +986,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
                                               ~(uintptr_t)1023);
     __shared__ __align__(8) uint64_t full[kMaxSA], conv[kMaxSA], empty[kMaxSA], accf;
     __shared__ uint32_t tmem_slot;
-    __shared__ float dbs[8][128];
+    __shared__ float dbs[2][8][128];
     const long long kt0 = clock64();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int SA = a.SA, G = a.G, N = a.N;
@@ -1058,9 +1058,12 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
         }
         __syncwarp();
     } else {
-        const int ct = tid - 64;
+        // two converter groups of 4 warps take alternate stages (their barrier
+        // waits and latencies overlap); group 0 also reads the accumulator out
+        const int grp = (warp - 2) >> 2, bar = 1 + grp;
+        const int ct = tid - 64 - 128 * grp;
         float colsum[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-        for (int64_t it = 0; it < total; ++it) {
+        for (int64_t it = grp; it < total; it += 2) {
             const int slot = (int)(it % SA);
             {
                 RDBG_T0;
@@ -1072,9 +1075,9 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
             {
                 RDBG_T0;
                 if constexpr (G_ > 0)
-                    red_convert_t<G_, WD_, WC_, N_>(a, sm + (size_t)slot * a.stage_bytes, valid, ct, colsum);
+                    red_convert_t<G_, WD_, WC_, N_>(a, sm + (size_t)slot * a.stage_bytes, valid, ct, colsum, bar);
                 else
-                    red_convert(a, sm + (size_t)slot * a.stage_bytes, valid, ct, colsum);
+                    red_convert(a, sm + (size_t)slot * a.stage_bytes, valid, ct, colsum, bar);
                 if (ct == 0) RDBG_ADD(3);
             }
             tc::fence_async_smem();
@@ -1087,23 +1090,25 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
         for (int i = 0; i < 2; ++i) {
             const Unit x = red_unit(N, ct, i);
             if (x.ok)
-                for (int e = 0; e < 4; ++e) dbs[x.j][4 * x.fq + e] = colsum[i][e];
+                for (int e = 0; e < 4; ++e) dbs[grp][x.j][4 * x.fq + e] = colsum[i][e];
         }
-        tc::named_bar(1, 128);
-        for (int c = ct; c < N; c += 128) {
-            float s = 0.f;
-            for (int j = 0; j < 8; ++j) s += dbs[j][c];
-            out[(int64_t)G * kTile * N + c] = s;
-        }
-        // accumulator -> per-CTA partial (lane = feature row)
+        tc::named_bar(3, 256);
+        if (grp == 0)
+            for (int c = ct; c < N; c += 128) {
+                float s = 0.f;
+                for (int q = 0; q < 2; ++q)
+                    for (int j = 0; j < 8; ++j) s += dbs[q][j][c];
+                out[(int64_t)G * kTile * N + c] = s;
+            }
+        // accumulator -> per-CTA partial (lane = feature row), group 0
         const int qd = warp & 3;
-        if (total > 0) {
+        if (total > 0 && grp == 0) {
             tc::mbar_wait_sleep(&accf, 0u);
             tc::fence_after();
         }
         const int m = qd * 32 + lane;
         const uint32_t lb = tmem + ((uint32_t)(qd * 32) << 16);
-        for (int g = 0; g < G; ++g)
+        for (int g = 0; g < (grp == 0 ? G : 0); ++g)
             for (int j = 0; j < N; j += 16) {
                 float v[16];
                 if (total > 0) tc::tmem_ld16(lb + (uint32_t)(g * N + j), v);
