@@ -397,3 +397,31 @@ def test_dense_tcgen05_matches_simt(designs, name, dc, dn, D, kc, kn, monkeypatc
         outs[mode] = dict(dxc=to_np(dxc), dxn=to_np(dxn), **{kk: to_np(vv) for kk, vv in grads.items()})
     for key in outs["0"]:
         assert row_err(outs["0"][key], outs["1"][key]) <= 5e-5, key
+
+
+@pytest.mark.parametrize("name,dc,dn,D,kc,kn", [("C2s", 64, 64, 64, 8, 8), ("C4s", 128, 128, 128, 16, 16)])
+def test_heteroconv_sum_merge_parity(designs, name, dc, dn, D, kc, kn):
+    """Eq. 6 variant: Y_cell = Y_near + Y_pinned, no mask routing."""
+    d = designs[name]
+    g = _graph(d)
+    P = make_params(dc, dn, D, 1, seed=6)
+    L, W = _layer(P, 0, dc, dn, D, kc, kn, merge=dr.DR_MERGE_SUM)
+    Wo = O.layer_params(P, 0)
+    rng = np.random.default_rng(8)
+    xc = cuda(rng.standard_normal((d.n_cell, dc)).astype(np.float32))
+    xn = cuda(rng.standard_normal((d.n_net, dn)).astype(np.float32))
+    yc, yn, tape = dr.heteroconv_fwd(g, L, xc, xn, flags=dr.DR_FWD_TAPS)
+    v = dr.tape_view(g, L, tape, dr.DR_FWD_TAPS)
+    T = _oracle_tape(v, dc, dn, merge="sum")
+    y_near = T["z_near"] @ Wo["wn_near"] + T["Hc"] @ Wo["wr_near"] + Wo["b_near"]
+    y_pinned = T["z_pinned"] @ Wo["w_pinned"] + Wo["b_pinned"]
+    assert row_err(to_np(yc), y_near + y_pinned) <= TOL
+    dyc = rng.standard_normal((d.n_cell, D)).astype(np.float32)
+    dyn = rng.standard_normal((d.n_net, D)).astype(np.float32)
+    grads, dxc, dxn = dr.heteroconv_bwd(g, L, tape, cuda(dyc), cuda(dyn), need_dx=True,
+                                        flags=dr.DR_FWD_TAPS)
+    og, odxc, odxn = O.layer_bwd(O.OGraph(d), Wo, T, dyc, dyn, need_dx=True)
+    for key in og:
+        assert row_err(to_np(grads[key]), og[key]) <= TOL, key
+    assert row_err(to_np(dxc), odxc) <= TOL
+    assert row_err(to_np(dxn), odxn) <= TOL
