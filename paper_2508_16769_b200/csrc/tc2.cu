@@ -277,26 +277,32 @@ __device__ __forceinline__ void stg_out_split(const float *stg, uint8_t *out, in
     }
 }
 
-// epilogue warp (quarter qd): rows r0 + 32 qd + lane of accumulator columns at `acc`
-__device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int64_t r0, int qd,
-                                              int lane, const float *bias_s, float *stg) {
-    const int N = a.N;
-    const int64_t row0 = r0 + qd * 32, row = row0 + lane;
+// Per-row epilogue inputs loaded one tile ahead (their latency overlaps the
+// previous tile): the dZ' row scale and the row's CBSR indices (root term).
+struct EpiPre {
+    float cr;
+    uint32_t iw[8];
+};
+__device__ __forceinline__ void epi_pre_load(const R2Args &a, int64_t row, EpiPre &e) {
     const bool ok = row < a.n;
-    const uint32_t lb = acc + ((uint32_t)(qd * 32) << 16);
-    if (a.epi == kEpi2Dz) {
-        const float cr = (ok && a.crow) ? __ldg(a.crow + row) : 1.f;
-        // root term: columns [n_dz, N) sampled at the row's CBSR indices (ascending),
-        // collected in registers (static indices) and stored as whole rows at the end
+    e.cr = (ok && a.crow) ? __ldg(a.crow + row) : 1.f;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) e.iw[t] = 0xffffffffu;
+    if (a.epi == kEpi2Dz && a.root && ok) {
         const int rk = a.root_k;
-        uint32_t iw[8];
-        float rv[32];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) iw[t] = 0xffffffffu;
-#pragma unroll
-        for (int q = 0; q < 32; ++q) rv[q] = 0.f;
-        if (a.root && ok) {
-            const uint8_t *ip = a.root_idx + row * rk;
+        const uint8_t *ip = a.root_idx + row * rk;
+        if (rk == 16) {
+            const uint4 w = __ldg(reinterpret_cast<const uint4 *>(ip));
+            e.iw[0] = w.x; e.iw[1] = w.y; e.iw[2] = w.z; e.iw[3] = w.w;
+        } else if (rk == 8) {
+            const uint2 w = __ldg(reinterpret_cast<const uint2 *>(ip));
+            e.iw[0] = w.x; e.iw[1] = w.y;
+        } else if (rk == 32) {
+            const uint4 w0 = __ldg(reinterpret_cast<const uint4 *>(ip));
+            const uint4 w1 = __ldg(reinterpret_cast<const uint4 *>(ip) + 1);
+            e.iw[0] = w0.x; e.iw[1] = w0.y; e.iw[2] = w0.z; e.iw[3] = w0.w;
+            e.iw[4] = w1.x; e.iw[5] = w1.y; e.iw[6] = w1.z; e.iw[7] = w1.w;
+        } else {
 #pragma unroll
             for (int t = 0; t < 8; ++t)
                 if (4 * t < rk) {
@@ -305,9 +311,29 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
                     for (int b = 0; b < 4; ++b)
                         if (4 * t + b < rk)
                             w = (w & ~(0xffu << (8 * b))) | ((uint32_t)__ldg(ip + 4 * t + b) << (8 * b));
-                    iw[t] = w;
+                    e.iw[t] = w;
                 }
         }
+    }
+}
+
+// epilogue warp (quarter qd): rows r0 + 32 qd + lane of accumulator columns at `acc`
+__device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int64_t r0, int qd,
+                                              int lane, const float *bias_s, float *stg,
+                                              const EpiPre &pre) {
+    const int N = a.N;
+    const int64_t row0 = r0 + qd * 32, row = row0 + lane;
+    const bool ok = row < a.n;
+    const uint32_t lb = acc + ((uint32_t)(qd * 32) << 16);
+    if (a.epi == kEpi2Dz) {
+        const float cr = pre.cr;
+        // root term: columns [n_dz, N) sampled at the row's CBSR indices (ascending),
+        // collected in registers (static indices) and stored as whole rows at the end
+        const int rk = a.root_k;
+        const uint32_t *iw = pre.iw;
+        float rv[16];                                  // rk <= 16: kept in registers
+#pragma unroll
+        for (int q = 0; q < 16; ++q) rv[q] = 0.f;
         for (int j = 0; j < N; j += 32) {
             uint32_t r[2][16];
             tc::tmem_ld16_nw(lb + (uint32_t)j, r[0]);
@@ -329,23 +355,31 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
                 else stg_out_f32(stg, a.dz, a.n_dz, row0, a.n, j, lane);
             }
             if (a.root && j + 32 > a.n_dz) {
+                if (rk <= 16) {
 #pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    const int c = a.n_dz + (int)((iw[q >> 2] >> (8 * (q & 3))) & 0xffu) - j;
-                    if (q < rk && c >= 0 && c < 32) rv[q] = stg[lane * kEStg + c];
+                    for (int q = 0; q < 16; ++q) {
+                        const int c = a.n_dz + (int)((iw[q >> 2] >> (8 * (q & 3))) & 0xffu) - j;
+                        if (q < rk && c >= 0 && c < 32) rv[q] = stg[lane * kEStg + c];
+                    }
+                } else if (ok) {                       // rk in (16, 32]: stored as found
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        const int c = a.n_dz + (int)((iw[q >> 2] >> (8 * (q & 3))) & 0xffu) - j;
+                        if (q < rk && c >= 0 && c < 32) a.root[row * rk + q] = stg[lane * kEStg + c];
+                    }
                 }
             }
             __syncwarp();
         }
-        if (a.root && ok) {
+        if (a.root && ok && rk <= 16) {
             if ((rk & 3) == 0) {
                 float4 *o = reinterpret_cast<float4 *>(a.root + row * rk);
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
+                for (int q = 0; q < 4; ++q)
                     if (4 * q < rk) o[q] = make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
             } else {
 #pragma unroll
-                for (int q = 0; q < 32; ++q)
+                for (int q = 0; q < 16; ++q)
                     if (q < rk) a.root[row * rk + q] = rv[q];
             }
         }
@@ -576,9 +610,12 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
         // ---------------- epilogue
         const int qd = warp & 3;
         float *stg = reinterpret_cast<float *>(epi_stage + (size_t)(warp - 6) * (32 * 36 * 4));
+        EpiPre pcur, pnxt;
+        if (my_tiles > 0) epi_pre_load(a, (int64_t)blockIdx.x * kTile + qd * 32 + lane, pcur);
         for (int64_t t = 0; t < my_tiles; ++t) {
             const int64_t r0 = ((int64_t)blockIdx.x + t * gridDim.x) * kTile;
             const uint32_t ab = (uint32_t)(t & 1);
+            if (t + 1 < my_tiles) epi_pre_load(a, r0 + (int64_t)gridDim.x * kTile + qd * 32 + lane, pnxt);
             {
                 RDBG_T0;
                 tc::mbar_wait_sleep(&accf[ab], (uint32_t)((t >> 1) & 1));
@@ -586,7 +623,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
             }
             tc::fence_after();
             RDBG_T0;
-            rows_epilogue(a, tmem + ab * GN, r0, qd, lane, bias_s, stg);
+            rows_epilogue(a, tmem + ab * GN, r0, qd, lane, bias_s, stg, pcur);
+            pcur = pnxt;
             if (warp == 6 && lane == 0) RDBG_ADD(6);
             tc::fence_before();
             __syncwarp();
