@@ -163,8 +163,10 @@ __global__ void __launch_bounds__(256) drelu_kernel(const float *__restrict__ x,
 // (ties: lower column first) once; then k rounds pick the warp-wide largest
 // head (redux.max), the lowest lane holding it takes it (ties -> lowest column,
 // since lane l holds columns [lV, lV+V)) and pops its head. That is exactly the
-// top-k under (value desc, column asc) of the binary search above, with ~k*10
-// instead of ~17*20 warp instructions per row (the search kernel is issue-bound).
+// top-k under (value desc, column asc) of the binary search above. The rounds
+// run on keys carrying (31 - lane) in their low 5 bits (one redux, no ballot,
+// per round), with an exactness check and a full-key rerun for the rare rows it
+// flags; the kernel is issue-bound, so instructions per round are what count.
 template <int V>
 __global__ void __launch_bounds__(256) drelu_extract_kernel(const float *__restrict__ x, int64_t n,
                                                             int dim, int64_t ldx, int k, bool vec,
@@ -204,20 +206,43 @@ __global__ void __launch_bounds__(256) drelu_extract_kernel(const float *__restr
                 sp[a + 1] = sw ? p0 : p1;
             }
         }
-        // k rounds: the lowest lane holding the warp-wide largest head pops it
-        // (lowest lane = lowest columns among equal keys); the winner test is a
-        // mask compare against %lanemask_lt (no bit-reverse / find-leading-one)
-        int taken = 0;
+        // k rounds of successive-max on keys whose low 5 bits are replaced by
+        // (31 - lane): one redux.max both finds the largest head and breaks ties to
+        // the lowest lane, with no ballot. Truncation is monotone, so this is exact
+        // unless an element left behind shares the truncated key of the last one
+        // taken -- checked below; such (rare) rows rerun with full keys + ballot.
+        const uint32_t lanebits = 31u - (uint32_t)lane;
+        uint32_t fk[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) fk[j] = sk[j] ? ((sk[j] & ~31u) | lanebits) : 0u;
+        uint32_t m = 0;
 #pragma unroll 4
         for (int t = 0; t < k; ++t) {
-            const uint32_t m = __reduce_max_sync(0xffffffffu, sk[0]);
-            const bool mine = sk[0] == m;
-            const uint32_t b = __ballot_sync(0xffffffffu, mine);
-            if (mine && (b & ltmask) == 0u) {
-                ++taken;
+            m = __reduce_max_sync(0xffffffffu, fk[0]);
+            if (fk[0] == m) {
 #pragma unroll
-                for (int j = 0; j + 1 < V; ++j) sk[j] = sk[j + 1];
-                sk[V - 1] = 0u;
+                for (int j = 0; j + 1 < V; ++j) fk[j] = fk[j + 1];
+                fk[V - 1] = 0u;
+            }
+        }
+        // pops = zeros shifted in = zeros now - zero (padding) keys the lane had
+        int taken = 0;
+#pragma unroll
+        for (int j = 0; j < V; ++j) taken += (fk[j] == 0u ? 1 : 0) - (sk[j] == 0u ? 1 : 0);
+        const bool unsafe = __any_sync(0xffffffffu, fk[0] != 0u && (fk[0] & ~31u) == (m & ~31u));
+        if (unsafe) {
+            taken = 0;
+#pragma unroll 4
+            for (int t = 0; t < k; ++t) {
+                const uint32_t mm = __reduce_max_sync(0xffffffffu, sk[0]);
+                const bool mine = sk[0] == mm;
+                const uint32_t b = __ballot_sync(0xffffffffu, mine);
+                if (mine && (b & ltmask) == 0u) {
+                    ++taken;
+#pragma unroll
+                    for (int j = 0; j + 1 < V; ++j) sk[j] = sk[j + 1];
+                    sk[V - 1] = 0u;
+                }
             }
         }
         uint32_t selm = 0;

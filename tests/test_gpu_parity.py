@@ -425,3 +425,17 @@ def test_heteroconv_sum_merge_parity(designs, name, dc, dn, D, kc, kn):
         assert row_err(to_np(grads[key]), og[key]) <= TOL, key
     assert row_err(to_np(dxc), odxc) <= TOL
     assert row_err(to_np(dxn), odxn) <= TOL
+
+
+@pytest.mark.parametrize("dim,k", [(64, 8), (128, 16), (32, 4), (256, 32)])
+def test_drelu_ulp_near_ties(dim, k):
+    """values a few ulps apart (the fast path's truncated keys collide and the
+    full-key rerun decides): still bit-exact to the oracle"""
+    rng = np.random.default_rng(dim + k)
+    base = np.float32(1.0) + rng.integers(0, 40, size=(2000, dim)).astype(np.float32) * np.float32(2.0 ** -23)
+    sign = np.where(rng.random((2000, dim)) < 0.3, -1.0, 1.0).astype(np.float32)
+    x = (base * sign).astype(np.float32)
+    val, idx = dr.drelu_topk(cuda(x), k)
+    oi, ov = O.drelu(x.astype(np.float64), k)
+    assert np.array_equal(to_np(idx).astype(np.int32), oi)
+    assert np.array_equal(to_np(val), ov.astype(np.float32))
