@@ -6,17 +6,19 @@
 namespace dr {
 namespace {
 
-constexpr int kHeadBlocks = 296;
+constexpr int kHeadBlocks = 148 * 8;      // one wave at 8 x 256 threads per SM
 constexpr int kHeadThreads = 256;
-constexpr int kHeadU = 4;          // rows in flight per warp
+constexpr int kHeadU = 8;          // rows in flight per warp
 
+// S = ceil(N / 32) column slots per lane (compile time: registers for kHeadU rows)
+template <int S>
 __global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a, float inv_n) {
     __shared__ float wpart[kHeadThreads / 32][256 + 2];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int N = a.N;
-    float w[8], accw[8];
+    float w[S], accw[S];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
+    for (int s = 0; s < S; ++s) {
         const int o = lane + 32 * s;
         w[s] = o < N ? __ldg(a.w + o) : 0.f;
         accw[s] = 0.f;
@@ -28,14 +30,14 @@ __global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a, float in
     // (the row loop is latency-bound otherwise: one dependent shuffle chain per row)
     for (int64_t j0 = ((int64_t)blockIdx.x * (kHeadThreads / 32) + wid) * kHeadU; j0 < a.n;
          j0 += nw * kHeadU) {
-        float y[kHeadU][8], p[kHeadU], lab[kHeadU];
+        float y[kHeadU][S], p[kHeadU], lab[kHeadU];
 #pragma unroll
         for (int u = 0; u < kHeadU; ++u) {
             const int64_t j = j0 + u;
             const bool ok = j < a.n;
             lab[u] = ok ? __ldg(a.labels + j) : 0.f;
 #pragma unroll
-            for (int s = 0; s < 8; ++s) {
+            for (int s = 0; s < S; ++s) {
                 const int o = lane + 32 * s;
                 y[u][s] = (ok && o < N) ? __ldg(a.y + j * N + o) : 0.f;
             }
@@ -44,7 +46,7 @@ __global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a, float in
         for (int u = 0; u < kHeadU; ++u) {
             p[u] = 0.f;
 #pragma unroll
-            for (int s = 0; s < 8; ++s) p[u] += y[u][s] * w[s];
+            for (int s = 0; s < S; ++s) p[u] += y[u][s] * w[s];
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
@@ -57,7 +59,7 @@ __global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a, float in
             const float r = p[u] + b - lab[u];
             const float dp = 2.0f * r * inv_n;
 #pragma unroll
-            for (int s = 0; s < 8; ++s) {
+            for (int s = 0; s < S; ++s) {
                 const int o = lane + 32 * s;
                 if (o < N) a.dy[j * N + o] = dp * w[s];
                 accw[s] += y[u][s] * dp;
@@ -67,7 +69,7 @@ __global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a, float in
         }
     }
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
+    for (int s = 0; s < S; ++s) {
         const int o = lane + 32 * s;
         if (o < N) wpart[wid][o] = accw[s];
     }
@@ -139,7 +141,10 @@ size_t head_work_floats(int N) { return (size_t)kHeadBlocks * (N + 2); }
 void launch_head_mse(const HeadArgs &a, cudaStream_t s) {
     const float inv_n = a.n > 0 ? 1.0f / (float)a.n : 0.f;
     ProfScope ps("head_mse", s);
-    head_kernel<<<kHeadBlocks, kHeadThreads, 0, s>>>(a, inv_n);
+    if (a.N <= 32) head_kernel<1><<<kHeadBlocks, kHeadThreads, 0, s>>>(a, inv_n);
+    else if (a.N <= 64) head_kernel<2><<<kHeadBlocks, kHeadThreads, 0, s>>>(a, inv_n);
+    else if (a.N <= 128) head_kernel<4><<<kHeadBlocks, kHeadThreads, 0, s>>>(a, inv_n);
+    else head_kernel<8><<<kHeadBlocks, kHeadThreads, 0, s>>>(a, inv_n);
     note_launch("head_mse");
     head_reduce_kernel<<<(unsigned)((a.N + 2 + 7) / 8), 256, 0, s>>>(a, inv_n);
     note_launch("head_reduce");
