@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "dr_internal.h"
 #include "tc.cuh"
@@ -71,6 +72,7 @@ struct TsArgs {
     // extra per-kept-entry term added in the epilogue (root term + other relation)
     const float *dz, *dzc, *s;
     const uint8_t *dzs;               // split dZ' rows ([hi | lo] bf16, 4 D bytes), or null
+    const void *zeros;                // forward: >= 2 D 128 zero bytes (TMA zero fill of B), or null
     const float *root;
     float *dx, *g_kept;
     unsigned long long *dbg;          // DR_TS_DEBUG role timers (cycles per CTA), else null
@@ -213,11 +215,11 @@ __device__ __forceinline__ void build_a(const uint8_t *sd, uint8_t *A, int ct) {
 
 template <int D, int QH>
 __device__ __forceinline__ void convert_fwd(const TsArgs &a, const CInfo &p, const uint8_t *sd,
-                                            uint8_t *st, int ct) {
+                                            uint8_t *st, int ct, bool zero_b) {
     uint8_t *A = st, *B = st + kATile;
     constexpr uint32_t lo = (uint32_t)D * 128u;
     constexpr int K = 4 * QH;
-    {
+    if (zero_b) {                           // (else the TMA zero-filled it)
         const uint4 z = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
         for (int i = 0; i < (2 * D * 128) / (16 * kConv); ++i)
@@ -483,7 +485,26 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
     const int tstride = a.tile_stride;
 
     if (warp == 0) {
-        if (BWD && !a.dzs) {
+        if (!BWD && a.zeros) {
+            // forward: the B tile of each stage is zero-filled by the TMA engine (bulk
+            // copy of an L2-resident zero buffer) once the MMA has released the slot,
+            // so the converters only scatter the CBSR values into it
+            const uint32_t bb = 2u * (uint32_t)D * 128u;
+            for (int it = 0; it < n_it; ++it) {
+                const int slot = it % SA;
+                const uint32_t u = (uint32_t)(it / SA);
+                if (u > 0) {
+                    TDBG_T0;
+                    wait_sleep(&empty[slot], (u - 1) & 1u);
+                    if (lane == 0) TDBG_ADD(0);
+                }
+                if (lane == 0) {
+                    tc::mbar_arrive_expect_tx(&full[slot], bb);
+                    tc::bulk_g2s(sm + (size_t)slot * a.stage_bytes + kATile, a.zeros, bb, &full[slot]);
+                }
+                __syncwarp();
+            }
+        } else if (BWD && !a.dzs) {
             int nid0 = -1, nid1 = -1, cn = cid(1);
             if (n_it > 0) {
                 const int c = cid(0);
@@ -610,14 +631,14 @@ __global__ void __launch_bounds__(kThreads, 1) tspmm_kernel(const __grid_constan
             } else {
                 {
                     TDBG_T0;
-                    if constexpr (BWD) tc::mbar_wait(&full[slot], u & 1u);
+                    if (BWD || a.zeros) tc::mbar_wait(&full[slot], u & 1u);
                     else if (u > 0) tc::mbar_wait(&empty[slot], (u - 1) & 1u);
                     if (ct == 0) TDBG_ADD(3);
                 }
                 {
                     TDBG_T0;
                     if constexpr (BWD) convert_bwd<D, QH>(a, i0, sd, st, ct, c0);
-                    else convert_fwd<D, QH>(a, i0, sd, st, ct);
+                    else convert_fwd<D, QH>(a, i0, sd, st, ct, a.zeros == nullptr);
                     if (ct == 0) TDBG_ADD(4);
                 }
                 // every converter thread is past the barrier inside convert: the slot
@@ -757,9 +778,28 @@ bool tspmm_supported(const TileSet &ts, int dim, int k) {
     return ts.n_tiles > 0 && (dim == 64 || dim == 128) && (k == 4 || k == 8 || k == 16 || k == 32);
 }
 
+// A 64 KB device buffer of zeros (the forward's TMA zero fill source), made once.
+static const void *zero_buffer() {
+    static void *p = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        if (cudaMalloc(&p, 65536) != cudaSuccess || cudaMemset(p, 0, 65536) != cudaSuccess ||
+            cudaDeviceSynchronize() != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+        }
+    });
+    return p;
+}
+
 void launch_tspmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
                       float *z, cudaStream_t s) {
     TsArgs a{};
+    // DR_TS_ZEROFILL=1: the TMA zero-fills B from an L2-resident zero buffer
+    // instead of the converters (measured slower at C2 and C4: smem fill
+    // bandwidth, not converter issue, bounds it; kept as an experiment)
+    const char *zf = getenv("DR_TS_ZEROFILL");
+    a.zeros = (zf && atoi(zf) == 1) ? zero_buffer() : nullptr;
     a.k = k;
     a.hval = hval;
     a.hidx = hidx;
