@@ -196,12 +196,16 @@ dr_status dr_heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape,
 /* Device views into a tape after dr_heteroconv_fwd (for teacher-forced parity
  * tests): the CBSR of both node types, Z per relation, Y_near/Y_pinned taps
  * (NULL unless DR_FWD_TAPS) and the merge mask (uint32 words, row-major
- * n_cell x ceil(d_out/32), bit d%32 of word d/32 = M[i,d]). */
+ * n_cell x ceil(d_out/32), bit d%32 of word d/32 = M[i,d]). z_split[r] = 1:
+ * Z of relation r is stored as rows of [hi | lo] bf16 halves (d_src values
+ * each, 4 d_src bytes per row), Z = hi + lo -- the tensor-core operand format
+ * the fused path uses when the widths allow (source width % 64 == 0). */
 typedef struct {
     dr_cbsr h_cell, h_net;
     float *z[3];
     float *y_near, *y_pinned;
     uint32_t *mask;
+    int32_t z_split[3];
 } dr_tape_view;
 dr_status dr_heteroconv_tape_view(const dr_graph *g, const dr_layer *L, void *tape,
                                   uint32_t flags, dr_tape_view *view);

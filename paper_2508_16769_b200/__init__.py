@@ -238,14 +238,23 @@ def tape_view(g, layer, tape, flags=0):
         off = ptr - base
         return tape[off:off + nbytes].view(dtype).view(*shape)
     nc, nn, D = g.n_cell, g.n_net, L.d_out
+
+    def zview(r, n, w):
+        """Z of relation r as fp32 (a copy when the tape holds split bf16 rows:
+        [hi | lo] halves, Z = hi + lo)"""
+        if not v.z_split[r]:
+            return sl(v.z[r], (n, w), torch.float32)
+        hl = sl(v.z[r], (n, 2 * w), torch.bfloat16)
+        return hl[:, :w].float() + hl[:, w:].float()
     return dict(
         hc_val=sl(v.h_cell.val, (nc, L.k_cell), torch.float32),
         hc_idx=sl(v.h_cell.idx, (nc, L.k_cell), torch.uint8),
         hn_val=sl(v.h_net.val, (nn, L.k_net), torch.float32),
         hn_idx=sl(v.h_net.idx, (nn, L.k_net), torch.uint8),
-        z_near=sl(v.z[DR_NEAR], (nc, L.d_cell), torch.float32),
-        z_pins=sl(v.z[DR_PINS], (nn, L.d_cell), torch.float32),
-        z_pinned=sl(v.z[DR_PINNED], (nc, L.d_net), torch.float32),
+        z_near=zview(DR_NEAR, nc, L.d_cell),
+        z_pins=zview(DR_PINS, nn, L.d_cell),
+        z_pinned=zview(DR_PINNED, nc, L.d_net),
+        z_split=[int(x) for x in v.z_split],
         y_near=sl(v.y_near, (nc, D), torch.float32),
         y_pinned=sl(v.y_pinned, (nc, D), torch.float32),
         mask=sl(v.mask, (nc, (D + 31) // 32), torch.int32),

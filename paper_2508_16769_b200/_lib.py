@@ -63,7 +63,7 @@ class dr_layer_grad(C.Structure):
 
 class dr_tape_view(C.Structure):
     _fields_ = [("h_cell", dr_cbsr), ("h_net", dr_cbsr), ("z", P * 3), ("y_near", P),
-                ("y_pinned", P), ("mask", P)]
+                ("y_pinned", P), ("mask", P), ("z_split", C.c_int32 * 3)]
 
 
 class dr_profile_entry(C.Structure):

@@ -230,6 +230,30 @@ static void check_layer(const dr_graph *g, const dr_layer *L) {
              "layer: bad merge");
 }
 
+// Z of relation r in the tape as split bf16 rows ([hi | lo], the tc2 operand
+// format: the projection loads them with TMA and skips its fp32 -> hi/lo split;
+// the dW converter transposes 16-bit halves instead of splitting). Opt-in
+// (DR_ZSPLIT=1): measured a net loss at C2 and C4 (projection -12 %, but the
+// SpMM epilogues' split stores and the dW converters' 16-bit transposes cost
+// more, profiles/r01). Needs both tensor-core consumers: source width % 64 == 0
+// and <= 128, d_out <= 128, and [Z | H] stacked in one dW group.
+static bool z_split_ok(const dr_layer *L, int r) {
+    static const bool on = [] {
+        const char *e = getenv("DR_ZSPLIT");
+        const char *f = getenv("DR_DENSE_SIMT");
+        return (e && atoi(e)) && !(f && atoi(f));
+    }();
+    if (!on) return false;
+    if (r != DR_PINNED) {                         // Sage: dW group [Z | H] must fit 128 rows
+        const int hw = r == DR_NEAR ? L->d_cell : L->d_net;
+        if ((r == DR_NEAR ? L->wr[DR_NEAR] : L->wr[DR_PINS]) && L->d_cell + hw > 128 &&
+            (L->d_cell != 128 || hw != 128))
+            return false;
+    }
+    const int K = r == DR_PINNED ? L->d_net : L->d_cell;
+    return K % 64 == 0 && K <= 128 && L->d_out <= 128 && L->d_out % 16 == 0;
+}
+
 // ------------------------------------------------------------------ layer forward / backward
 static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc, const float *xn,
                            float *yc, float *yn, void *tape, uint32_t flags, cudaStream_t st) {
@@ -251,10 +275,12 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[0], s0));                               // H_c ready
     { TagScope t("net"); launch_drelu(xn, nn, L->d_net, L->d_net, L->k_net, hnv, hni, s2); }
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[1], s2));                               // H_n ready
-    { TagScope t("near"); launch_spmm_fwd(g->rel[DR_NEAR], hcv, hci, L->k_cell, L->d_cell, z[DR_NEAR], s0); }  // Eq. 5-7
+    bool zs[3];
+    for (int r = 0; r < 3; ++r) zs[r] = z_split_ok(L, r);
+    { TagScope t("near"); launch_spmm_fwd(g->rel[DR_NEAR], hcv, hci, L->k_cell, L->d_cell, z[DR_NEAR], s0, zs[DR_NEAR]); }  // Eq. 5-7
     if (!seq) DR_CUDA(cudaStreamWaitEvent(s1, C.ev[0], 0));
-    { TagScope t("pins"); launch_spmm_fwd(g->rel[DR_PINS], hcv, hci, L->k_cell, L->d_cell, z[DR_PINS], s1); }
-    { TagScope t("pinned"); launch_spmm_fwd(g->rel[DR_PINNED], hnv, hni, L->k_net, L->d_net, z[DR_PINNED], s2); }
+    { TagScope t("pins"); launch_spmm_fwd(g->rel[DR_PINS], hcv, hci, L->k_cell, L->d_cell, z[DR_PINS], s1, zs[DR_PINS]); }
+    { TagScope t("pinned"); launch_spmm_fwd(g->rel[DR_PINNED], hnv, hni, L->k_net, L->d_net, z[DR_PINNED], s2, zs[DR_PINNED]); }
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[2], s2));                               // Z_pinned ready
     if (!seq) DR_CUDA(cudaStreamWaitEvent(s1, C.ev[1], 0));
     {   // net: Y_net = Z_pins Wn_pins + densify(H_n) Wr_pins + b_pins   (Eq. 7, 9)
@@ -263,7 +289,7 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
         uint8_t *img = (uint8_t *)(tp + T.img_fn);
         d.n = nn; d.N = L->d_out; d.G = 1; d.epi = kEpi2Fwd;
         d.nseg[0] = L->wr[DR_PINS] ? 2 : 1;
-        d.seg[0][0].A = z[DR_PINS]; d.seg[0][0].K = L->d_cell;
+        d.seg[0][0].A = z[DR_PINS]; d.seg[0][0].K = L->d_cell; d.seg[0][0].split = zs[DR_PINS];
         d.seg[0][1].hval = hnv; d.seg[0][1].hidx = hni; d.seg[0][1].k = L->k_net;
         d.seg[0][1].K = L->d_net;
         d.bimg[0] = img; d.bias[0] = L->b[DR_PINS];
@@ -280,6 +306,7 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
             a.Za = z[DR_PINS]; a.Wa = L->wn[DR_PINS]; a.ba = L->b[DR_PINS];
             a.Wr = L->wr[DR_PINS]; a.hval = hnv; a.hidx = hni; a.k = L->k_net;
             a.y = yn;
+            DR_CHECK(!zs[DR_PINS], DR_ERR_UNSUPPORTED, "projection: split Z needs tc2");
             launch_proj_fwd(a, s1);
         }
     }
@@ -292,11 +319,11 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
         Tc2RowsDesc d;
         d.n = nc; d.N = L->d_out; d.G = 2; d.epi = kEpi2Fwd;
         d.nseg[0] = L->wr[DR_NEAR] ? 2 : 1;
-        d.seg[0][0].A = z[DR_NEAR]; d.seg[0][0].K = L->d_cell;
+        d.seg[0][0].A = z[DR_NEAR]; d.seg[0][0].K = L->d_cell; d.seg[0][0].split = zs[DR_NEAR];
         d.seg[0][1].hval = hcv; d.seg[0][1].hidx = hci; d.seg[0][1].k = L->k_cell;
         d.seg[0][1].K = L->d_cell;
         d.nseg[1] = 1;
-        d.seg[1][0].A = z[DR_PINNED]; d.seg[1][0].K = L->d_net;
+        d.seg[1][0].A = z[DR_PINNED]; d.seg[1][0].K = L->d_net; d.seg[1][0].split = zs[DR_PINNED];
         d.bimg[0] = ia; d.bimg[1] = ib;
         d.bias[0] = L->b[DR_NEAR]; d.bias[1] = L->b[DR_PINNED];
         d.merge = L->merge;
@@ -320,6 +347,7 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
             a.mask = (uint32_t *)(tp + T.mask);
             a.tap_a = tap_a;
             a.tap_b = tap_b;
+            DR_CHECK(!zs[DR_NEAR] && !zs[DR_PINNED], DR_ERR_UNSUPPORTED, "projection: split Z needs tc2");
             launch_proj_fwd(a, s0);
         }
     }
@@ -454,11 +482,11 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
     // tensor cores when the shapes allow (tc2 reduce GEMM), else the SIMT kernels
     auto dwt = [&](int64_t n, const float *Za, int wa, float *ga, const float *hv,
                    const uint8_t *hi, int k, int wb, float *gb, const float *dy, int mode,
-                   float *db, float *wk, cudaStream_t s) -> bool {
+                   float *db, float *wk, cudaStream_t s, bool zsplit) -> bool {
         Tc2ReduceDesc d;
         d.n = n; d.N = D; d.dy = dy; d.mask = mask; d.mask_mode = mode; d.db = db;
         Tc2RedSeg sa, sb;
-        sa.Z = Za; sa.w = wa; sa.grad = ga;
+        sa.Z = Za; sa.w = wa; sa.grad = ga; sa.split = zsplit;
         sb.hval = hv; sb.hidx = hi; sb.k = k; sb.w = wb; sb.grad = gb;
         d.G = 1; d.nseg[0] = 1; d.seg[0][0] = sa;
         if (gb && wa + wb <= 128) {
@@ -466,7 +494,10 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
         } else if (gb) {                           // two groups of 128 feature rows
             d.G = 2; d.nseg[1] = 1; d.seg[1][0] = sb;
         }
-        if (!tc2_reduce_supported(d)) return false;
+        if (!tc2_reduce_supported(d)) {
+            DR_CHECK(!zsplit, DR_ERR_UNSUPPORTED, "dW: split Z needs the tensor-core reduce");
+            return false;
+        }
         launch_tc2_reduce(d, wk, s);
         return true;
     };
@@ -474,7 +505,7 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
         TagScope t("near");
         if (!dwt(nc, z[DR_NEAR], L->d_cell, G->wn[DR_NEAR], hcv, hci, L->k_cell, L->d_cell,
                  L->wr[DR_NEAR] ? G->wr[DR_NEAR] : nullptr, dyc, mode_near, G->b[DR_NEAR],
-                 work[0], s0)) {
+                 work[0], s0, z_split_ok(L, DR_NEAR))) {
             dw(nc, L->d_cell, z[DR_NEAR], nullptr, nullptr, 0, dyc, mode_near, G->wn[DR_NEAR],
                G->b[DR_NEAR], work[0], s0);
             TagScope t2("root");
@@ -486,7 +517,7 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
     {
         TagScope t("pinned");
         if (!dwt(nc, z[DR_PINNED], L->d_net, G->wn[DR_PINNED], nullptr, nullptr, 0, 0, nullptr,
-                 dyc, mode_pinned, G->b[DR_PINNED], work[2], s2))
+                 dyc, mode_pinned, G->b[DR_PINNED], work[2], s2, z_split_ok(L, DR_PINNED)))
             dw(nc, L->d_net, z[DR_PINNED], nullptr, nullptr, 0, dyc, mode_pinned,
                G->wn[DR_PINNED], G->b[DR_PINNED], work[2], s2);
     }
@@ -494,7 +525,7 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
         TagScope t("pins");
         if (!dwt(nn, z[DR_PINS], L->d_cell, G->wn[DR_PINS], hnv, hni, L->k_net, L->d_net,
                  L->wr[DR_PINS] ? G->wr[DR_PINS] : nullptr, dyn, kMaskNone, G->b[DR_PINS],
-                 work[1], s1)) {
+                 work[1], s1, z_split_ok(L, DR_PINS))) {
             dw(nn, L->d_cell, z[DR_PINS], nullptr, nullptr, 0, dyn, kMaskNone, G->wn[DR_PINS],
                G->b[DR_PINS], work[1], s1);
             TagScope t2("root");
@@ -792,7 +823,10 @@ dr_status dr_heteroconv_tape_view(const dr_graph *g, const dr_layer *L, void *ta
     std::memset(v, 0, sizeof(*v));
     v->h_cell = dr_cbsr{g->n_cell, L->d_cell, L->k_cell, 1, tp + T.hc_idx, (float *)(tp + T.hc_val)};
     v->h_net = dr_cbsr{g->n_net, L->d_net, L->k_net, 1, tp + T.hn_idx, (float *)(tp + T.hn_val)};
-    for (int r = 0; r < 3; ++r) v->z[r] = (float *)(tp + T.z[r]);
+    for (int r = 0; r < 3; ++r) {
+        v->z[r] = (float *)(tp + T.z[r]);
+        v->z_split[r] = z_split_ok(L, r) ? 1 : 0;
+    }
     if (flags & DR_FWD_TAPS) {
         v->y_near = (float *)(tp + T.tap_a);
         v->y_pinned = (float *)(tp + T.tap_b);

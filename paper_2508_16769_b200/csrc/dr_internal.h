@@ -157,8 +157,9 @@ void launch_drelu(const float *x, int64_t n, int dim, int64_t ldx, int k, float 
                   uint8_t *idx, cudaStream_t s);
 
 // DR-SpMM forward of one relation: z [n_dst x dim] = diag(c) A diag(s) densify(H).
+// z_split: write Z rows as [hi | lo] bf16 halves (the tc2 operand format).
 void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
-                     float *z, cudaStream_t s);
+                     float *z, cudaStream_t s, bool z_split = false);
 
 // SSpMM backward for one source node type, summing up to two relations that
 // share the source type. Term q in {0,1}: relation rel[q] (CSC), its dz, and
@@ -178,7 +179,7 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1,
 // extra [n_src x k] term added at the kept entries (root + other relations).
 bool tspmm_supported(const TileSet &ts, int dim, int k);
 void launch_tspmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
-                      float *z, cudaStream_t s);
+                      float *z, cudaStream_t s, bool z_split = false);
 // dz_split: dz holds [hi | lo] bf16 rows (tc2 dz epilogue, Tc2RowsDesc::dz_split).
 void launch_tspmm_bwd(const RelDev &r, const float *dz, bool dz_split, bool apply_c,
                       const float *extra, const uint8_t *hidx, int k, int dim, float *g_kept,

@@ -30,6 +30,16 @@
 namespace dr {
 namespace {
 
+// x = hi + lo in bf16 (round to nearest), two values packed per word (a low half)
+__device__ __forceinline__ void tc_split_bf16x2(float a, float b, uint32_t &hi, uint32_t &lo) {
+    uint32_t h, l;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));
+    const float ha = __uint_as_float(h << 16), hb = __uint_as_float(h & 0xffff0000u);
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(b - hb), "f"(a - ha));
+    hi = h;
+    lo = l;
+}
+
 constexpr int kU = 4;           // neighbours in flight per lane (memory-level parallelism)
 constexpr int kHubCtas = 296;   // 2 per SM
 
@@ -115,7 +125,34 @@ struct FwdArgs {
     const uint8_t *hidx;
     int k, D, L;
     float *z;
+    int z_split;                     // z rows as [hi | lo] bf16 halves (4 D bytes per row)
 };
+
+// Z output: fp32, or split bf16 halves (x = hi + lo, the tensor-core operand
+// format of the projection / dW kernels, tc2.h)
+__device__ __forceinline__ void store_z4(const FwdArgs &a, int row, int c4, float4 v) {
+    if (!a.z_split) {
+        __stcs(reinterpret_cast<float4 *>(a.z + (int64_t)row * a.D) + c4, v);
+        return;
+    }
+    uint2 h, l;
+    tc_split_bf16x2(v.x, v.y, h.x, l.x);
+    tc_split_bf16x2(v.z, v.w, h.y, l.y);
+    uint8_t *rowp = reinterpret_cast<uint8_t *>(a.z) + (int64_t)row * a.D * 4;
+    __stcs(reinterpret_cast<uint2 *>(rowp + 8 * c4), h);
+    __stcs(reinterpret_cast<uint2 *>(rowp + 2 * a.D + 8 * c4), l);
+}
+__device__ __forceinline__ void store_z1(const FwdArgs &a, int row, int c, float v) {
+    if (!a.z_split) {
+        a.z[(int64_t)row * a.D + c] = v;
+        return;
+    }
+    uint32_t h, l;
+    tc_split_bf16x2(v, 0.f, h, l);
+    uint16_t *rowp = reinterpret_cast<uint16_t *>(a.z) + (int64_t)row * a.D * 2;
+    rowp[c] = (uint16_t)(h & 0xffffu);
+    rowp[a.D + c] = (uint16_t)(l & 0xffffu);
+}
 
 template <int P>
 __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
@@ -142,7 +179,7 @@ __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
             for (int cc = threadIdx.x; cc < D; cc += blockDim.x) {
                 float s = 0.f;
                 for (int q = 0; q < S; ++q) s += sm[(size_t)q * D + cc];
-                a.z[(int64_t)row * D + cc] = cr * s;
+                store_z1(a, row, cc, cr * s);
             }
             __syncthreads();
         }
@@ -162,14 +199,13 @@ __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
         if (valid) {
             const float cr = __ldg(a.c + row);
             const float4 *w4 = reinterpret_cast<const float4 *>(sm + (size_t)wid * R * D);
-            float4 *zr = reinterpret_cast<float4 *>(a.z + (int64_t)row * D);
             for (int c4 = lane; c4 < D4; c4 += 32) {
                 float4 s = w4[c4];
                 for (int q = 1; q < R; ++q) {
                     const float4 t = w4[(size_t)q * D4 + c4];
                     s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
                 }
-                __stcs(zr + c4, make_float4(cr * s.x, cr * s.y, cr * s.z, cr * s.w));
+                store_z4(a, row, c4, make_float4(cr * s.x, cr * s.y, cr * s.z, cr * s.w));
             }
         }
         return;
@@ -187,10 +223,9 @@ __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
     __syncwarp();
     if (valid) {
         const float cr = __ldg(a.c + row);
-        float4 *zr = reinterpret_cast<float4 *>(a.z + (int64_t)row * D);
         for (int c4 = ll; c4 < D4; c4 += L) {
             const float4 v = acc4[c4];
-            __stcs(zr + c4, make_float4(cr * v.x, cr * v.y, cr * v.z, cr * v.w));
+            store_z4(a, row, c4, make_float4(cr * v.x, cr * v.y, cr * v.z, cr * v.w));
         }
     }
 }
@@ -433,10 +468,10 @@ int choose_P(int k, int D) {
 void ensure_smem(const void *fn, size_t bytes);
 
 void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
-                     float *z, cudaStream_t s) {
+                     float *z, cudaStream_t s, bool z_split) {
     if (r.n_dst <= 0) return;
     if (!r.ew && tspmm_supported(r.tiles, dim, k)) {      // tensor-core tiled path
-        launch_tspmm_fwd(r, hval, hidx, k, dim, z, s);
+        launch_tspmm_fwd(r, hval, hidx, k, dim, z, s, z_split);
         return;
     }
     const int P = choose_P(k, dim);
@@ -457,6 +492,7 @@ void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, in
     a.k = k;
     a.D = dim;
     a.z = z;
+    a.z_split = z_split ? 1 : 0;
     int wpc = 8;
     while (wpc > 1 && (size_t)wpc * R * dim * 4 > 96 * 1024) wpc >>= 1;
     const size_t smem = (size_t)wpc * R * dim * 4;

@@ -87,6 +87,7 @@ struct R2Seg {
     const float *hval;
     const uint8_t *hidx;
     int k, K, mask_mode;
+    int split;                     // A rows are [hi | lo] bf16: TMA lands the operand directly
 };
 struct R2Args {
     CUtensorMap tmap[2][2];        // dense segments: [n x K] fp32, box 64 cols x 128 rows
@@ -123,7 +124,15 @@ __device__ __forceinline__ void rows_produce(const R2Args &a, const R2Step &sp, 
                                              uint8_t *st, uint8_t *mk, uint64_t *full, int lane) {
     const R2Seg &s = a.seg[sp.g][sp.s];
     const int rows = (int)(a.n - r0 < kTile ? a.n - r0 : kTile);
-    if (s.A) {
+    if (s.A && s.split) {
+        // split rows: the hi and lo 128 x 64 bf16 boxes arrive 128-B swizzled, i.e.
+        // already the K-major SW128 operand tiles (no converter work)
+        if (lane == 0) {
+            tc::mbar_arrive_expect_tx(full, kStage);
+            tc::tma_load_2d(st, &a.tmap[sp.g][sp.s], sp.c * kChunk, (int)r0, full);
+            tc::tma_load_2d(st + kHalf, &a.tmap[sp.g][sp.s], s.K + sp.c * kChunk, (int)r0, full);
+        }
+    } else if (s.A) {
         // one TMA box: rows r0..r0+127, columns 64c..64c+63 (out-of-range rows and
         // columns arrive as zeros), plus the tile's merge-mask words
         const uint32_t mbytes = s.mask_mode != kMask2None ? rup16((uint32_t)rows * a.mw * 4) : 0u;
@@ -149,6 +158,7 @@ __device__ __forceinline__ void rows_convert(const R2Args &a, const R2Step &sp, 
                                              uint8_t *st, const uint8_t *mk, int ct) {
     const R2Seg &s = a.seg[sp.g][sp.s];
     const int lane = ct & 31, cw = ct >> 5;
+    if (s.A && s.split) return;                        // landed as operand tiles
     if (s.A) {
         const int q = lane & 15;                       // float4 column group of the chunk
         float4 v[16];
@@ -650,6 +660,7 @@ struct RdSeg {
     const float *hval;
     const uint8_t *hidx;
     int k, w, m0;
+    int split;                         // Z rows are [hi | lo] bf16 halves
 };
 struct RdArgs {
     int64_t n;
@@ -794,6 +805,47 @@ __device__ __forceinline__ void red_write(uint8_t *tile, uint32_t lo_off, int W,
     }
 }
 
+// Split dense rows ([hi | lo] bf16, 4 W bytes per row, already the operand's
+// hi/lo values): the transposition to [feature][row] needs no arithmetic, only
+// 16-bit shuffles. Unit (feature quad fq, row octet j) as for fp32 rows: 8 rows x
+// (4 hi + 4 lo bf16) read, 4 features x (8 hi + 8 lo) written as 16-B stores.
+struct SplitU {
+    uint2 h[8], l[8];
+};
+__device__ __forceinline__ void red_read_split(const uint8_t *raw, int W, int valid, const Unit &x,
+                                               SplitU &v) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const int rr = 8 * x.j + r;
+        const uint8_t *row = raw + (size_t)rr * W * 4;
+        const bool ok = rr < valid;
+        v.h[r] = ok ? *reinterpret_cast<const uint2 *>(row + 8 * x.fq) : make_uint2(0u, 0u);
+        v.l[r] = ok ? *reinterpret_cast<const uint2 *>(row + 2 * W + 8 * x.fq) : make_uint2(0u, 0u);
+    }
+}
+__device__ __forceinline__ void red_write_split(uint8_t *tile, uint32_t lo_off, int m0, const Unit &x,
+                                                const SplitU &v) {
+    const int m = m0 + 4 * x.fq;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        // feature e of the quad: its value in row r is half (e & 1) of word (e >> 1)
+        const uint32_t sel = (e & 1) ? 0x7632u : 0x5410u;
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t a0 = (e >> 1) ? v.h[2 * q].y : v.h[2 * q].x;
+            const uint32_t a1 = (e >> 1) ? v.h[2 * q + 1].y : v.h[2 * q + 1].x;
+            const uint32_t b0 = (e >> 1) ? v.l[2 * q].y : v.l[2 * q].x;
+            const uint32_t b1 = (e >> 1) ? v.l[2 * q + 1].y : v.l[2 * q + 1].x;
+            hw[q] = __byte_perm(a0, a1, sel);
+            lw[q] = __byte_perm(b0, b1, sel);
+        }
+        const uint32_t off = tc::sw128_off_h((uint32_t)(m + e), (uint32_t)(8 * x.j));
+        *reinterpret_cast<uint4 *>(tile + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4 *>(tile + lo_off + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+}
+
 // converters: one stage -> A'_g (per group) and B' operands; db unit sums in colsum
 __device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int valid, int ct,
                                             float (&colsum)[2][4], int bar) {
@@ -808,8 +860,18 @@ __device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int va
             wtot += a.seg[g][q].w;
             if (a.seg[g][q].Z) { dseg = &a.seg[g][q]; wd = dseg->w; }
         }
-        if (dseg) red_read<2>(reinterpret_cast<const float *>(tile), wd, valid, ct, mk, 0,
-                              kMask2None, v, nullptr);
+        SplitU sv[2];
+        const bool dsplit = dseg && dseg->split;
+        if (dsplit) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const Unit x = red_unit(wd, ct, i);
+                if (x.ok) red_read_split(tile, wd, valid, x, sv[i]);
+            }
+        } else if (dseg) {
+            red_read<2>(reinterpret_cast<const float *>(tile), wd, valid, ct, mk, 0, kMask2None, v,
+                        nullptr);
+        }
         // CBSR entries of this group: thread -> graph row ct/2, half ct&1 of its k pairs
         float cv[16];
         uint32_t cid[16];
@@ -835,7 +897,15 @@ __device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int va
             ++ci;
         }
         tc::named_bar(bar, 128);                      // raw reads done before writes
-        if (dseg) red_write<2>(tile, kHalf, wd, dseg->m0, ct, v);
+        if (dsplit) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const Unit x = red_unit(wd, ct, i);
+                if (x.ok) red_write_split(tile, kHalf, dseg->m0, x, sv[i]);
+            }
+        } else if (dseg) {
+            red_write<2>(tile, kHalf, wd, dseg->m0, ct, v);
+        }
         {   // zero the CBSR rows and the unused rows [wtot, 128)
             const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int q = 0; q < a.nseg[g]; ++q) {
@@ -952,7 +1022,17 @@ __device__ __forceinline__ void red_convert_t(const RdArgs &a, uint8_t *st, int 
     uint8_t *th = G == 2 ? st + kStage : st;            // CBSR rows [hm0, hm0 + WC)
     constexpr int hm0 = G == 2 ? 0 : WD;
     float4 v[2][8];
-    red_read_t<WD>(reinterpret_cast<const float *>(tz), valid, ct, mk, 0, kMask2None, v, nullptr);
+    SplitU sv[2];
+    const bool zs = a.seg[0][0].split != 0;           // the dense segment is split bf16
+    if (zs) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const Unit x = red_unit_t<WD>(ct, i);
+            if (x.ok) red_read_split(tz, WD, valid, x, sv[i]);
+        }
+    } else {
+        red_read_t<WD>(reinterpret_cast<const float *>(tz), valid, ct, mk, 0, kMask2None, v, nullptr);
+    }
     // CBSR: thread -> graph row r = ct & 63, contiguous half h = ct >> 6 of its k pairs
     const int kc = a.seg[G == 2 ? 1 : 0][G == 2 ? 0 : 1].k;
     const int r = ct & 63, h = ct >> 6, kh = kc >> 1;
@@ -975,7 +1055,15 @@ __device__ __forceinline__ void red_convert_t(const RdArgs &a, uint8_t *st, int 
         }
     }
     tc::named_bar(bar, 128);                              // raw reads done before writes
-    red_write_t<WD>(tz, kHalf, 0, ct, v);
+    if (zs) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const Unit x = red_unit_t<WD>(ct, i);
+            if (x.ok) red_write_split(tz, kHalf, 0, x, sv[i]);
+        }
+    } else {
+        red_write_t<WD>(tz, kHalf, 0, ct, v);
+    }
     {
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
         if constexpr (WC > 0) {
@@ -1232,6 +1320,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // output map: [n x W] fp32 row-major, box = 16 columns x 32 rows, SWIZZLE_64B
+// [n x 2K] bf16 split rows ([hi | lo]), box = 64 columns x 128 rows, 128-B swizzle
+// (= the K-major SW128 operand tile layout)
+static void make_tmap_split(CUtensorMap *m, const float *A, int64_t n, int K) {
+    const cuuint64_t dims[2] = {(cuuint64_t)(2 * K), (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)K * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)kChunk, (cuuint32_t)kTile};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void *)A, dims, strides,
+                                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DR_CHECK(r == CUDA_SUCCESS, DR_ERR_CUDA, "cuTensorMapEncodeTiled (split) failed");
+}
+
 // [n x K] fp32 row-major, box = 64 columns x 128 rows, no swizzle (row-major
 // [128][64] landing tile), zero fill out of range
 static void make_tmap(CUtensorMap *m, const float *A, int64_t n, int K) {
@@ -1248,6 +1350,7 @@ static void make_tmap(CUtensorMap *m, const float *A, int64_t n, int K) {
 
 static bool seg_ok(const Tc2Seg &s) {
     if (s.K < 4 || s.K > 256 || s.K % 4) return false;
+    if (s.A && s.split && (s.K % kChunk || s.mask_mode != kMask2None)) return false;
     if (!s.A && (s.k < 1 || s.k > 32 || s.k > s.K)) return false;
     return true;
 }
@@ -1287,8 +1390,10 @@ void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
         int bc = 0;
         for (int q = 0; q < d.nseg[g]; ++q) {
             const Tc2Seg &sd = d.seg[g][q];
-            a.seg[g][q] = R2Seg{sd.A, sd.hval, sd.hidx, sd.k, sd.K, sd.A ? sd.mask_mode : kMask2None};
-            if (sd.A) make_tmap(&a.tmap[g][q], sd.A, d.n, sd.K);
+            a.seg[g][q] = R2Seg{sd.A, sd.hval, sd.hidx, sd.k, sd.K, sd.A ? sd.mask_mode : kMask2None,
+                                sd.A && sd.split ? 1 : 0};
+            if (sd.A && sd.split) make_tmap_split(&a.tmap[g][q], sd.A, d.n, sd.K);
+            else if (sd.A) make_tmap(&a.tmap[g][q], sd.A, d.n, sd.K);
             const int chunks = (sd.K + kChunk - 1) / kChunk;
             for (int c = 0; c < chunks; ++c)
                 a.step[a.S++] = R2Step{(int8_t)g, (int8_t)q, (int8_t)c, (int8_t)bc++,
@@ -1421,7 +1526,7 @@ void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s) {
         int m0 = 0;
         for (int q = 0; q < d.nseg[g]; ++q) {
             const Tc2RedSeg &sd = d.seg[g][q];
-            a.seg[g][q] = RdSeg{sd.Z, sd.hval, sd.hidx, sd.k, sd.w, m0};
+            a.seg[g][q] = RdSeg{sd.Z, sd.hval, sd.hidx, sd.k, sd.w, m0, sd.Z && sd.split ? 1 : 0};
             if (!sd.Z) {
                 ++ncb;
                 maxk = std::max(maxk, sd.k);

@@ -20,6 +20,7 @@ enum { kEpi2Fwd = 0, kEpi2Dz = 1 };
 
 struct Tc2Seg {
     const float *A = nullptr;          // dense n x K row-major, or nullptr => CBSR
+    bool split = false;                // A holds [hi | lo] bf16 rows (4 K bytes, K % 64 == 0)
     const float *hval = nullptr;       // CBSR n x k (values), idx n x k (uint8)
     const uint8_t *hidx = nullptr;
     int k = 0;
@@ -69,6 +70,7 @@ void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s);
 
 struct Tc2RedSeg {
     const float *Z = nullptr;          // dense n x w, or nullptr => CBSR (hval/hidx/k, width w)
+    bool split = false;                // Z holds [hi | lo] bf16 rows (4 w bytes)
     const float *hval = nullptr;
     const uint8_t *hidx = nullptr;
     int k = 0, w = 0;

@@ -67,6 +67,7 @@ struct TsArgs {
     const uint8_t *hidx;
     const float *c;
     float *z;
+    int z_split;                      // forward output as [hi | lo] bf16 rows
     // backward: dZ' rows of the halo (destinations), optional per-halo-row scale
     // (standalone ABI: dz not yet row-scaled), s_j of the tiled relation, and the
     // extra per-kept-entry term added in the epilogue (root term + other relation)
@@ -330,6 +331,28 @@ __device__ __forceinline__ void stg_to_global(const float *stg, float *out, int 
         if (rr[i] >= 0) __stcs(reinterpret_cast<float4 *>(out + (int64_t)rr[i] * D + j0) + cq, v[i]);
 }
 
+// split output rows ([hi | lo] bf16 halves, 4 D bytes): hi of column j at 2 j,
+// lo at 2 (D + j)
+template <int D>
+__device__ __forceinline__ void stg_to_global_split(const float *stg, uint8_t *out, int rid, int j0,
+                                                    int lane) {
+    const int cq = lane & 7, rs = lane >> 3;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int r = 4 * i + rs;
+        const int rr = __shfl_sync(0xffffffffu, rid, r);
+        const float4 v = *reinterpret_cast<const float4 *>(stg + r * kStg + 4 * cq);
+        uint2 h, l;
+        tc::split_bf16x2(v.x, v.y, h.x, l.x);
+        tc::split_bf16x2(v.z, v.w, h.y, l.y);
+        if (rr >= 0) {
+            uint8_t *rowp = out + (int64_t)rr * D * 4;
+            __stcs(reinterpret_cast<uint2 *>(rowp + 2 * (j0 + 4 * cq)), h);
+            __stcs(reinterpret_cast<uint2 *>(rowp + 2 * (D + j0 + 4 * cq)), l);
+        }
+    }
+}
+
 template <int D>
 __device__ __forceinline__ void epi_fwd(const TsArgs &a, int t, uint32_t tacc, float *stg, int lane) {
     const int rid = __ldg(a.rows + (int64_t)t * kTsRows + (tacc >> 16) + lane);
@@ -338,7 +361,8 @@ __device__ __forceinline__ void epi_fwd(const TsArgs &a, int t, uint32_t tacc, f
     for (int j0 = 0; j0 < D; j0 += 32) {
         tmem_to_stg<D>(tacc + (uint32_t)j0, cr, stg, lane);
         __syncwarp();
-        stg_to_global<D>(stg, a.z, rid, j0, lane);
+        if (a.z_split) stg_to_global_split<D>(stg, reinterpret_cast<uint8_t *>(a.z), rid, j0, lane);
+        else stg_to_global<D>(stg, a.z, rid, j0, lane);
         __syncwarp();
     }
 }
@@ -793,8 +817,9 @@ static const void *zero_buffer() {
 }
 
 void launch_tspmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
-                      float *z, cudaStream_t s) {
+                      float *z, cudaStream_t s, bool z_split) {
     TsArgs a{};
+    a.z_split = z_split ? 1 : 0;
     // DR_TS_ZEROFILL=1: the TMA zero-fills B from an L2-resident zero buffer
     // instead of the converters (measured slower at C2 and C4: smem fill
     // bandwidth, not converter issue, bounds it; kept as an experiment)
