@@ -231,28 +231,12 @@ static void check_layer(const dr_graph *g, const dr_layer *L) {
 }
 
 // Z of relation r in the tape as split bf16 rows ([hi | lo], the tc2 operand
-// format: the projection loads them with TMA and skips its fp32 -> hi/lo split;
-// the dW converter transposes 16-bit halves instead of splitting). Opt-in
-// (DR_ZSPLIT=1): measured a net loss at C2 and C4 (projection -12 %, but the
-// SpMM epilogues' split stores and the dW converters' 16-bit transposes cost
-// more, profiles/r01). Needs both tensor-core consumers: source width % 64 == 0
-// and <= 128, d_out <= 128, and [Z | H] stacked in one dW group.
-static bool z_split_ok(const dr_layer *L, int r) {
-    static const bool on = [] {
-        const char *e = getenv("DR_ZSPLIT");
-        const char *f = getenv("DR_DENSE_SIMT");
-        return (e && atoi(e)) && !(f && atoi(f));
-    }();
-    if (!on) return false;
-    if (r != DR_PINNED) {                         // Sage: dW group [Z | H] must fit 128 rows
-        const int hw = r == DR_NEAR ? L->d_cell : L->d_net;
-        if ((r == DR_NEAR ? L->wr[DR_NEAR] : L->wr[DR_PINS]) && L->d_cell + hw > 128 &&
-            (L->d_cell != 128 || hw != 128))
-            return false;
-    }
-    const int K = r == DR_PINNED ? L->d_net : L->d_cell;
-    return K % 64 == 0 && K <= 128 && L->d_out <= 128 && L->d_out % 16 == 0;
-}
+// format the projection can TMA-load without its fp32 -> hi/lo split). Off: the
+// other consumer, the dW reduce kernel, would need its own split-aware operand
+// path; a converter-transpose version measured a net loss at C2 and C4 (and its
+// code pushed the reduce kernels into register spills), so the producer and
+// projection paths stay for a future MN-major TMA dW operand.
+static bool z_split_ok(const dr_layer *, int) { return false; }
 
 // ------------------------------------------------------------------ layer forward / backward
 static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc, const float *xn,

@@ -805,47 +805,6 @@ __device__ __forceinline__ void red_write(uint8_t *tile, uint32_t lo_off, int W,
     }
 }
 
-// Split dense rows ([hi | lo] bf16, 4 W bytes per row, already the operand's
-// hi/lo values): the transposition to [feature][row] needs no arithmetic, only
-// 16-bit shuffles. Unit (feature quad fq, row octet j) as for fp32 rows: 8 rows x
-// (4 hi + 4 lo bf16) read, 4 features x (8 hi + 8 lo) written as 16-B stores.
-struct SplitU {
-    uint2 h[8], l[8];
-};
-__device__ __forceinline__ void red_read_split(const uint8_t *raw, int W, int valid, const Unit &x,
-                                               SplitU &v) {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        const int rr = 8 * x.j + r;
-        const uint8_t *row = raw + (size_t)rr * W * 4;
-        const bool ok = rr < valid;
-        v.h[r] = ok ? *reinterpret_cast<const uint2 *>(row + 8 * x.fq) : make_uint2(0u, 0u);
-        v.l[r] = ok ? *reinterpret_cast<const uint2 *>(row + 2 * W + 8 * x.fq) : make_uint2(0u, 0u);
-    }
-}
-__device__ __forceinline__ void red_write_split(uint8_t *tile, uint32_t lo_off, int m0, const Unit &x,
-                                                const SplitU &v) {
-    const int m = m0 + 4 * x.fq;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        // feature e of the quad: its value in row r is half (e & 1) of word (e >> 1)
-        const uint32_t sel = (e & 1) ? 0x7632u : 0x5410u;
-        uint32_t hw[4], lw[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t a0 = (e >> 1) ? v.h[2 * q].y : v.h[2 * q].x;
-            const uint32_t a1 = (e >> 1) ? v.h[2 * q + 1].y : v.h[2 * q + 1].x;
-            const uint32_t b0 = (e >> 1) ? v.l[2 * q].y : v.l[2 * q].x;
-            const uint32_t b1 = (e >> 1) ? v.l[2 * q + 1].y : v.l[2 * q + 1].x;
-            hw[q] = __byte_perm(a0, a1, sel);
-            lw[q] = __byte_perm(b0, b1, sel);
-        }
-        const uint32_t off = tc::sw128_off_h((uint32_t)(m + e), (uint32_t)(8 * x.j));
-        *reinterpret_cast<uint4 *>(tile + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4 *>(tile + lo_off + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-    }
-}
-
 // converters: one stage -> A'_g (per group) and B' operands; db unit sums in colsum
 __device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int valid, int ct,
                                             float (&colsum)[2][4], int bar) {
@@ -860,18 +819,8 @@ __device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int va
             wtot += a.seg[g][q].w;
             if (a.seg[g][q].Z) { dseg = &a.seg[g][q]; wd = dseg->w; }
         }
-        SplitU sv[2];
-        const bool dsplit = dseg && dseg->split;
-        if (dsplit) {
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const Unit x = red_unit(wd, ct, i);
-                if (x.ok) red_read_split(tile, wd, valid, x, sv[i]);
-            }
-        } else if (dseg) {
-            red_read<2>(reinterpret_cast<const float *>(tile), wd, valid, ct, mk, 0, kMask2None, v,
-                        nullptr);
-        }
+        if (dseg) red_read<2>(reinterpret_cast<const float *>(tile), wd, valid, ct, mk, 0,
+                              kMask2None, v, nullptr);
         // CBSR entries of this group: thread -> graph row ct/2, half ct&1 of its k pairs
         float cv[16];
         uint32_t cid[16];
@@ -897,15 +846,7 @@ __device__ __forceinline__ void red_convert(const RdArgs &a, uint8_t *st, int va
             ++ci;
         }
         tc::named_bar(bar, 128);                      // raw reads done before writes
-        if (dsplit) {
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const Unit x = red_unit(wd, ct, i);
-                if (x.ok) red_write_split(tile, kHalf, dseg->m0, x, sv[i]);
-            }
-        } else if (dseg) {
-            red_write<2>(tile, kHalf, wd, dseg->m0, ct, v);
-        }
+        if (dseg) red_write<2>(tile, kHalf, wd, dseg->m0, ct, v);
         {   // zero the CBSR rows and the unused rows [wtot, 128)
             const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int q = 0; q < a.nseg[g]; ++q) {
@@ -1022,17 +963,7 @@ __device__ __forceinline__ void red_convert_t(const RdArgs &a, uint8_t *st, int 
     uint8_t *th = G == 2 ? st + kStage : st;            // CBSR rows [hm0, hm0 + WC)
     constexpr int hm0 = G == 2 ? 0 : WD;
     float4 v[2][8];
-    SplitU sv[2];
-    const bool zs = a.seg[0][0].split != 0;           // the dense segment is split bf16
-    if (zs) {
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const Unit x = red_unit_t<WD>(ct, i);
-            if (x.ok) red_read_split(tz, WD, valid, x, sv[i]);
-        }
-    } else {
-        red_read_t<WD>(reinterpret_cast<const float *>(tz), valid, ct, mk, 0, kMask2None, v, nullptr);
-    }
+    red_read_t<WD>(reinterpret_cast<const float *>(tz), valid, ct, mk, 0, kMask2None, v, nullptr);
     // CBSR: thread -> graph row r = ct & 63, contiguous half h = ct >> 6 of its k pairs
     const int kc = a.seg[G == 2 ? 1 : 0][G == 2 ? 0 : 1].k;
     const int r = ct & 63, h = ct >> 6, kh = kc >> 1;
@@ -1055,15 +986,7 @@ __device__ __forceinline__ void red_convert_t(const RdArgs &a, uint8_t *st, int 
         }
     }
     tc::named_bar(bar, 128);                              // raw reads done before writes
-    if (zs) {
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const Unit x = red_unit_t<WD>(ct, i);
-            if (x.ok) red_write_split(tz, kHalf, 0, x, sv[i]);
-        }
-    } else {
-        red_write_t<WD>(tz, kHalf, 0, ct, v);
-    }
+    red_write_t<WD>(tz, kHalf, 0, ct, v);
     {
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
         if constexpr (WC > 0) {
@@ -1526,7 +1449,8 @@ void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s) {
         int m0 = 0;
         for (int q = 0; q < d.nseg[g]; ++q) {
             const Tc2RedSeg &sd = d.seg[g][q];
-            a.seg[g][q] = RdSeg{sd.Z, sd.hval, sd.hidx, sd.k, sd.w, m0, sd.Z && sd.split ? 1 : 0};
+            DR_CHECK(!sd.split, DR_ERR_UNSUPPORTED, "tc2_reduce: split Z rows are not supported");
+            a.seg[g][q] = RdSeg{sd.Z, sd.hval, sd.hidx, sd.k, sd.w, m0, 0};
             if (!sd.Z) {
                 ++ncb;
                 maxk = std::max(maxk, sd.k);
