@@ -314,3 +314,69 @@ def dp_mean(grads_per_rank):
     """Data-parallel gradient = mean of per-rank gradients (north_star; O8)."""
     keys = grads_per_rank[0].keys()
     return {k: sum(g[k] for g in grads_per_rank) / len(grads_per_rank) for k in keys}
+
+
+# ------------------------------------------------------------------ NEXT-2: per-neighbour-group K
+# (SURVEY §8 f2; P:289-293 Alg. 1 stage 2, P:346-350: "D-ReLU will apply respective
+# K-values to the NGs with respect to their sizes ... The more neighbors the NGs have,
+# the fewer features per neighbor are required to pass, which corresponds to smaller
+# K-values"). Reading Q26 (DESIGN.md): a destination row i in degree bin b keeps, from
+# every neighbour j, the top-K_b entries of H_j (the same exact top-k rule), i.e. the
+# first K_b entries of j's value-sorted CBSR row; bins by in-degree: deg <= thr[0] ->
+# kb[0], deg <= thr[1] -> kb[1], else kb[2] (kb[0] >= kb[1] >= kb[2], K1 > K2 > K3).
+
+def drelu_sorted(x, k):
+    """The top-k set of drelu() stored value-descending (ties: lower column first),
+    so every prefix of length K' <= k is the row's exact top-K'. (idx int32, val f64)."""
+    idx, val = drelu(x, k)
+    out_i = np.empty_like(idx)
+    out_v = np.empty_like(val)
+    for r in range(idx.shape[0]):
+        order = np.lexsort((idx[r], -val[r]))          # primary: value desc; then column asc
+        out_i[r] = idx[r][order]
+        out_v[r] = val[r][order]
+    return out_i, out_v
+
+
+def ng_k(ptr, thr, kb):
+    """Per-destination-row K from its in-degree (Q26)."""
+    deg = np.diff(_i64(ptr))
+    return np.where(deg <= thr[0], kb[0], np.where(deg <= thr[1], kb[1], kb[2])).astype(np.int64)
+
+
+def _rows_csr(ptr, col, rows, a=None):
+    """CSR restricted to `rows` (other rows empty), same row count."""
+    ptr = _i64(ptr)
+    keep = np.zeros(ptr.size - 1, bool)
+    keep[rows] = True
+    deg = np.where(keep, np.diff(ptr), 0)
+    p2 = np.zeros_like(ptr)
+    p2[1:] = np.cumsum(deg)
+    sel = np.repeat(keep, np.diff(ptr))
+    return p2, _i32(col)[sel], (None if a is None else _f64(a)[sel])
+
+
+def spmm_fwd_ng(ptr, col, n_dst, c, s, idx_s, val_s, d, thr, kb, a=None):
+    """Z_i = c_i sum_j a_ij s_j densify(first K(i) entries of the value-sorted row j):
+    per degree bin b, the plain SpMM (spmm_fwd) over that bin's rows with the K_b-prefix
+    CBSR; the bins' rows are disjoint, so Z is their sum."""
+    K = ng_k(ptr, thr, kb)
+    z = np.zeros((n_dst, d), np.float64)
+    for kk in sorted(set(int(v) for v in K)):
+        rows = np.nonzero(K == kk)[0]
+        p2, c2, a2 = _rows_csr(ptr, col, rows, a)
+        z += spmm_fwd(p2, c2, n_dst, c, s, _i32(idx_s)[:, :kk], _f64(val_s)[:, :kk], d, a2)
+    return z
+
+
+def spmm_bwd_ng(ptr, col, n_dst, n_src, c, s, idx_s, dz, thr, kb, a=None):
+    """Adjoint of spmm_fwd_ng: g[j,t] = sum over i with j in N(i) and t < K(i) of
+    c_i a_ij s_j dz[i, idx_s[j,t]] (per bin, spmm_bwd on the K_b prefix)."""
+    K = ng_k(ptr, thr, kb)
+    k = _i32(idx_s).shape[1]
+    g = np.zeros((n_src, k), np.float64)
+    for kk in sorted(set(int(v) for v in K)):
+        rows = np.nonzero(K == kk)[0]
+        p2, c2, a2 = _rows_csr(ptr, col, rows, a)
+        g[:, :kk] += spmm_bwd(p2, c2, n_dst, n_src, c, s, _i32(idx_s)[:, :kk], dz, a2)
+    return g
