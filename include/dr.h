@@ -210,6 +210,43 @@ typedef struct {
 dr_status dr_heteroconv_tape_view(const dr_graph *g, const dr_layer *L, void *tape,
                                   uint32_t flags, dr_tape_view *view);
 
+/* ------------------------------------------------------------------ NEXT-2: per-neighbour-group K
+ * Alg. 1 stage 2 and P:346-350: "D-ReLU will apply respective
+ * K-values to the NGs with respect to their sizes ... The more neighbors the NGs
+ * have, the fewer features per neighbor are required to pass". Reading Q26
+ * (DESIGN.md): a destination row with in-degree d keeps, from every neighbour,
+ * the first K(d) entries of the neighbour's value-sorted CBSR row (its exact
+ * top-K(d)), K(d) = kb[0] for d <= thr[0], kb[1] for d <= thr[1], kb[2] above;
+ * k >= kb[0] >= kb[1] >= kb[2] >= 1. Runs on the SIMT kernels (all relations). */
+typedef struct {
+    int32_t thr[2];
+    int32_t kb[3];
+} dr_ng_sched;
+/* D-ReLU with each row's k pairs in value-descending order (ties: lower column
+ * first), so every prefix is an exact top-k'. k <= 32. Same arguments/errors as
+ * dr_drelu_topk. */
+dr_status dr_drelu_topk_sorted(const float *x, int64_t n, int32_t dim, int64_t ldx, dr_cbsr *out,
+                               void *stream);
+/* A schedule bound to one relation of one graph: validates `sched` (BadK unless
+ * 32 >= kb[0] >= kb[1] >= kb[2] >= 1, InvalidArgument unless thr[0] <= thr[1])
+ * and precomputes, on `stream`, K(deg of the destination) for every edge in the
+ * relation's CSC order (nnz bytes of device memory from the graph's allocator),
+ * so the backward reads it coalesced. The plan is immutable once created: any
+ * number of streams may use it after `stream` has reached the creation point.
+ * Destroy it before its graph. */
+typedef struct dr_ng_plan dr_ng_plan;
+dr_status dr_ng_plan_create(const dr_graph *g, dr_rel r, const dr_ng_sched *sched, void *stream,
+                            dr_ng_plan **out);
+dr_status dr_ng_plan_destroy(dr_ng_plan *p);
+/* z[i,:] = c_i * sum_{j in N(i)} a_ij * s_j * densify(first K(deg_i) pairs of h_src[j]),
+ * h_src value-sorted (dr_drelu_topk_sorted), for the plan's graph and relation.
+ * Errors as dr_spmm_fwd, plus BadK when h_src->k < kb[0]. */
+dr_status dr_spmm_fwd_ng(const dr_ng_plan *p, const dr_cbsr *h_src, float *z, void *stream);
+/* Adjoint of dr_spmm_fwd_ng: g[j,t] = sum over i with j in N(i) and t < K(deg_i) of
+ * c_i a_ij s_j dz[i, idx[j,t]]; outputs as dr_spmm_bwd (no accumulate). */
+dr_status dr_spmm_bwd_ng(const dr_ng_plan *p, const float *dz, const dr_cbsr *h_src,
+                         float *g_kept, float *dx, void *stream);
+
 /* ------------------------------------------------------------------ training
  * The 2-layer model of P:464-466: HeteroConv x n_layers -> linear head on
  * cells -> MSE (Q14) -> backward -> [NCCL allreduce of the flat gradient] ->

@@ -179,6 +179,78 @@ def spmm_bwd(g, rel, dz, val, idx, dim, want_g=True, want_dx=False, accumulate=F
     return gk, dx
 
 
+# ------------------------------------------------------------------ NEXT-2 (reading Q26)
+class NgPlan:
+    """dr_ng_plan: the K schedule (thr, kb) of reading Q26 bound to one relation of
+    one graph (per-edge K precomputed on the device). Keeps the graph alive."""
+
+    def __init__(self, g, rel, thr, kb, stream=None):
+        from ._lib import dr_ng_sched
+        s = dr_ng_sched()
+        s.thr[0], s.thr[1] = int(thr[0]), int(thr[1])
+        s.kb[0], s.kb[1], s.kb[2] = int(kb[0]), int(kb[1]), int(kb[2])
+        self.g, self.rel = g, (REL_ID[rel] if isinstance(rel, str) else int(rel))
+        self.thr, self.kb = tuple(thr), tuple(kb)
+        h = C.c_void_p()
+        check(lib().dr_ng_plan_create(g.handle, self.rel, C.byref(s), _stream(stream),
+                                      C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().dr_ng_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def drelu_topk_sorted(x, k, out=None, stream=None):
+    """Eq. 2-3 with each row's k pairs in value-descending order (k <= 32)."""
+    torch = _torch()
+    n, dim = x.shape
+    assert x.dtype == torch.float32 and x.is_cuda and x.stride(1) == 1
+    if out is None:
+        val = torch.empty((n, k), device=x.device, dtype=torch.float32)
+        idx = torch.empty((n, k), device=x.device, dtype=torch.uint8)
+    else:
+        val, idx = out
+    cb = _cbsr(val, idx, dim)
+    check(lib().dr_drelu_topk_sorted(_ptr(x), n, dim, x.stride(0), C.byref(cb),
+                                     _stream(stream)))
+    return val, idx
+
+
+def spmm_fwd_ng(plan, val, idx, dim, out=None, stream=None):
+    """Eq. 5-7 with the destination-degree K schedule of reading Q26: destination i
+    aggregates the first K(deg_i) pairs of each value-sorted source row."""
+    torch = _torch()
+    n_dst = plan.g.n_cell if plan.rel in (DR_NEAR, DR_PINNED) else plan.g.n_net
+    z = out if out is not None else torch.empty((n_dst, dim), device=val.device,
+                                                 dtype=torch.float32)
+    cb = _cbsr(val, idx, dim)
+    check(lib().dr_spmm_fwd_ng(plan.handle, C.byref(cb), _ptr(z), _stream(stream)))
+    return z
+
+
+def spmm_bwd_ng(plan, dz, val, idx, dim, want_g=True, want_dx=False, g_out=None, dx_out=None,
+                stream=None):
+    """Adjoint of spmm_fwd_ng (Eq. 10-11 restricted to each destination's prefix)."""
+    torch = _torch()
+    n, k = val.shape
+    gk = g_out if g_out is not None else (
+        torch.empty((n, k), device=dz.device, dtype=torch.float32) if want_g else None)
+    dx = dx_out if dx_out is not None else (
+        torch.empty((n, dim), device=dz.device, dtype=torch.float32) if want_dx else None)
+    cb = _cbsr(val, idx, dim)
+    check(lib().dr_spmm_bwd_ng(plan.handle, _ptr(dz), C.byref(cb), _ptr(gk), _ptr(dx),
+                               _stream(stream)))
+    return gk, dx
+
+
 # ------------------------------------------------------------------ HeteroConv layer
 LAYER_KEYS = ("wn_near", "wr_near", "b_near", "w_pinned", "b_pinned", "wn_pins", "wr_pins",
               "b_pins")

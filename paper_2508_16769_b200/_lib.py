@@ -66,6 +66,10 @@ class dr_tape_view(C.Structure):
                 ("y_pinned", P), ("mask", P), ("z_split", C.c_int32 * 3)]
 
 
+class dr_ng_sched(C.Structure):
+    _fields_ = [("thr", C.c_int32 * 2), ("kb", C.c_int32 * 3)]
+
+
 class dr_profile_entry(C.Structure):
     _fields_ = [("name", C.c_char * 48), ("launches", C.c_int64), ("total_ms", C.c_double),
                 ("max_ms", C.c_double)]
@@ -90,6 +94,12 @@ _SIGS = {
     "dr_drelu_topk": (C.c_int, [P, C.c_int64, C.c_int32, C.c_int64, C.POINTER(dr_cbsr), P]),
     "dr_spmm_fwd": (C.c_int, [P, C.c_int, C.POINTER(dr_cbsr), P, P]),
     "dr_spmm_bwd": (C.c_int, [P, C.c_int, P, C.POINTER(dr_cbsr), P, P, C.c_int32, P]),
+    "dr_drelu_topk_sorted": (C.c_int, [P, C.c_int64, C.c_int32, C.c_int64,
+                                       C.POINTER(dr_cbsr), P]),
+    "dr_ng_plan_create": (C.c_int, [P, C.c_int, C.POINTER(dr_ng_sched), P, C.POINTER(P)]),
+    "dr_ng_plan_destroy": (C.c_int, [P]),
+    "dr_spmm_fwd_ng": (C.c_int, [P, C.POINTER(dr_cbsr), P, P]),
+    "dr_spmm_bwd_ng": (C.c_int, [P, P, C.POINTER(dr_cbsr), P, P, P]),
     "dr_heteroconv_tape_bytes": (C.c_int, [P, C.POINTER(dr_layer), C.c_uint32,
                                            C.POINTER(C.c_size_t)]),
     "dr_heteroconv_fwd": (C.c_int, [P, C.POINTER(dr_layer), P, P, P, P, P, C.c_uint32, P]),

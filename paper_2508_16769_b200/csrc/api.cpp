@@ -759,6 +759,109 @@ dr_status dr_spmm_bwd(const dr_graph *g, dr_rel r, const float *dz, const dr_cbs
     DR_API_END
 }
 
+// ------------------------------------------------------------------ NEXT-2 (per-neighbour-group K)
+dr_status dr_drelu_topk_sorted(const float *x, int64_t n, int32_t dim, int64_t ldx, dr_cbsr *out,
+                               void *stream) {
+    DR_API_BEGIN
+    check_cbsr(out, "drelu_sorted out");
+    DR_CHECK(n >= 0 && out->n == n && out->dim == dim, DR_ERR_SHAPE_MISMATCH,
+             "drelu_sorted: out->n/dim must equal n/dim");
+    DR_CHECK(ldx >= dim, DR_ERR_SHAPE_MISMATCH, "drelu_sorted: ldx < dim");
+    DR_CHECK(n == 0 || x, DR_ERR_INVALID_ARGUMENT, "drelu_sorted: null x");
+    DR_CHECK(out->k <= 32, DR_ERR_BAD_K, "drelu_sorted: k must be <= 32");
+    launch_drelu(x, n, dim, ldx, out->k, out->val, (uint8_t *)out->idx, (cudaStream_t)stream, true);
+    DR_API_END
+}
+
+}  // extern "C"
+
+struct dr_ng_plan {
+    const dr_graph *g = nullptr;
+    int r = 0;
+    NgSched ng;                          // ng.kT: device [nnz], K(deg row[e]) per CSC edge
+    Alloc alloc;
+    cudaStream_t stream = nullptr;
+};
+
+extern "C" {
+
+dr_status dr_ng_plan_create(const dr_graph *g, dr_rel r, const dr_ng_sched *s, void *stream,
+                            dr_ng_plan **out) {
+    DR_API_BEGIN
+    DR_CHECK(g != nullptr && out != nullptr, DR_ERR_INVALID_ARGUMENT, "ng_plan: null graph/out");
+    DR_CHECK(r >= 0 && r < 3, DR_ERR_INVALID_ARGUMENT, "ng_plan: bad relation");
+    DR_CHECK(s != nullptr, DR_ERR_INVALID_ARGUMENT, "ng_plan: null schedule");
+    DR_CHECK(s->kb[0] >= s->kb[1] && s->kb[1] >= s->kb[2] && s->kb[2] >= 1 && s->kb[0] <= 32,
+             DR_ERR_BAD_K, "ng_plan: need 32 >= kb[0] >= kb[1] >= kb[2] >= 1");
+    DR_CHECK(s->thr[0] <= s->thr[1], DR_ERR_INVALID_ARGUMENT, "ng_plan: need thr[0] <= thr[1]");
+    *out = nullptr;
+    auto *p = new dr_ng_plan;
+    p->g = g;
+    p->r = r;
+    p->alloc = g->alloc;
+    p->stream = (cudaStream_t)stream;
+    p->ng.on = 1;
+    p->ng.thr0 = s->thr[0];
+    p->ng.thr1 = s->thr[1];
+    p->ng.kb0 = s->kb[0];
+    p->ng.kb1 = s->kb[1];
+    p->ng.kb2 = s->kb[2];
+    const RelDev &R = g->rel[r];
+    if (R.nnz > 0) {
+        uint8_t *kT = nullptr;
+        try {
+            kT = (uint8_t *)p->alloc.get((size_t)R.nnz, p->stream);
+            launch_ng_edge_k(R, p->ng, kT, p->stream);
+        } catch (...) {
+            if (kT) p->alloc.put(kT, p->stream);
+            delete p;
+            throw;
+        }
+        p->ng.kT = kT;
+    }
+    *out = p;
+    DR_API_END
+}
+
+dr_status dr_ng_plan_destroy(dr_ng_plan *p) {
+    if (!p) return DR_OK;
+    if (p->ng.kT) {
+        cudaStreamSynchronize(p->stream);
+        p->alloc.put((void *)p->ng.kT, p->stream);
+    }
+    delete p;
+    return DR_OK;
+}
+
+dr_status dr_spmm_fwd_ng(const dr_ng_plan *p, const dr_cbsr *h, float *z, void *stream) {
+    DR_API_BEGIN
+    DR_CHECK(p != nullptr, DR_ERR_INVALID_ARGUMENT, "spmm_fwd_ng: null plan");
+    check_cbsr(h, "spmm_fwd_ng h_src");
+    const RelDev &R = p->g->rel[p->r];
+    DR_CHECK(h->n == R.n_src, DR_ERR_SHAPE_MISMATCH, "spmm_fwd_ng: h_src->n != relation n_src");
+    DR_CHECK(h->k >= p->ng.kb0, DR_ERR_BAD_K, "spmm_fwd_ng: h_src->k < kb[0]");
+    DR_CHECK(R.n_dst == 0 || z, DR_ERR_INVALID_ARGUMENT, "spmm_fwd_ng: null z");
+    launch_spmm_fwd(R, h->val, (const uint8_t *)h->idx, h->k, h->dim, z, (cudaStream_t)stream,
+                    false, p->ng);
+    DR_API_END
+}
+
+dr_status dr_spmm_bwd_ng(const dr_ng_plan *p, const float *dz, const dr_cbsr *h, float *g_kept,
+                         float *dx, void *stream) {
+    DR_API_BEGIN
+    DR_CHECK(p != nullptr, DR_ERR_INVALID_ARGUMENT, "spmm_bwd_ng: null plan");
+    check_cbsr(h, "spmm_bwd_ng h_src");
+    const RelDev &R = p->g->rel[p->r];
+    DR_CHECK(h->n == R.n_src, DR_ERR_SHAPE_MISMATCH, "spmm_bwd_ng: h_src->n != relation n_src");
+    DR_CHECK(h->k >= p->ng.kb0, DR_ERR_BAD_K, "spmm_bwd_ng: h_src->k < kb[0]");
+    DR_CHECK(g_kept || dx, DR_ERR_INVALID_ARGUMENT, "spmm_bwd_ng: both outputs NULL");
+    DR_CHECK(R.n_dst == 0 || dz, DR_ERR_INVALID_ARGUMENT, "spmm_bwd_ng: null dz");
+    BwdTerm t0{&R, dz, true}, t1{};
+    launch_spmm_bwd(R.bwd, R.n_src, t0, t1, nullptr, (const uint8_t *)h->idx, h->k, h->dim,
+                    g_kept, dx, false, (cudaStream_t)stream, p->ng);
+    DR_API_END
+}
+
 dr_status dr_heteroconv_tape_bytes(const dr_graph *g, const dr_layer *L, uint32_t flags,
                                    size_t *bytes) {
     DR_API_BEGIN

@@ -153,13 +153,27 @@ namespace dr {
 
 // ------------------------------------------------------------------ kernels (launchers)
 // D-ReLU (Eq. 2-3): x [n x dim] (ld ldx) -> CBSR val [n x k], idx [n x k] (uint8).
+// sorted: rows in value-descending order (ties: lower column first), k <= 32.
 void launch_drelu(const float *x, int64_t n, int dim, int64_t ldx, int k, float *val,
-                  uint8_t *idx, cudaStream_t s);
+                  uint8_t *idx, cudaStream_t s, bool sorted = false);
+
+// NEXT-2 per-neighbour-group K (reading Q26): a destination row with in-degree d
+// keeps the first K(d) entries of each neighbour's value-sorted CBSR row,
+// K(d) = kb[0] (d <= thr[0]), kb[1] (d <= thr[1]), kb[2] (otherwise). ng.on == 0: off.
+struct NgSched {
+    int on = 0;
+    int thr0 = 0, thr1 = 0, kb0 = 0, kb1 = 0, kb2 = 0;
+    const uint8_t *kT = nullptr;     // backward: K(deg of row[e]) per CSC edge e (launch_ng_edge_k)
+};
+// kT[e] = K(deg_dst(row[e])) for every CSC edge of r (one byte per edge), so the
+// backward reads its destinations' K coalesced beside row[] instead of gathering
+// two rowptr entries per edge.
+void launch_ng_edge_k(const RelDev &r, const NgSched &ng, uint8_t *kT, cudaStream_t s);
 
 // DR-SpMM forward of one relation: z [n_dst x dim] = diag(c) A diag(s) densify(H).
 // z_split: write Z rows as [hi | lo] bf16 halves (the tc2 operand format).
 void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
-                     float *z, cudaStream_t s, bool z_split = false);
+                     float *z, cudaStream_t s, bool z_split = false, NgSched ng = NgSched{});
 
 // SSpMM backward for one source node type, summing up to two relations that
 // share the source type. Term q in {0,1}: relation rel[q] (CSC), its dz, and
@@ -172,7 +186,7 @@ struct BwdTerm {
 };
 void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1,
                      const float *root, const uint8_t *hidx, int k, int dim, float *g_kept,
-                     float *dx, bool accumulate, cudaStream_t s);
+                     float *dx, bool accumulate, cudaStream_t s, NgSched ng = NgSched{});
 
 // Tensor-core tiled SpMM (tspmm.cu) of a relation with a TileSet: forward into
 // z; backward for the tiled relation's source rows alone, with an optional

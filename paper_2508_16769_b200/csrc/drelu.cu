@@ -168,6 +168,26 @@ __global__ void __launch_bounds__(256) drelu_kernel(const float *__restrict__ x,
 // per round), with an exactness check and a full-key rerun for the rare rows it
 // flags; the kernel is issue-bound, so instructions per round are what count.
 template <int V>
+__device__ __forceinline__ int pick_i(const int (&a)[V], int q) {
+    int r = a[0];
+#pragma unroll
+    for (int i = 1; i < V; ++i) r = q == i ? a[i] : r;
+    return r;
+}
+template <int V>
+__device__ __forceinline__ float pick_f(const float (&a)[V], int q) {
+    float r = a[0];
+#pragma unroll
+    for (int i = 1; i < V; ++i) r = q == i ? a[i] : r;
+    return r;
+}
+
+// SORTED: rows stored in extraction order = value descending, ties lower column
+// first (the value-sorted CBSR of NEXT-2, reading Q26): the winner of round t
+// writes its element at position t; no column-order compaction. Rounds whose heads
+// from different lanes tie on the truncated key are ordered by lane, not value, so
+// SORTED also sends those rows to the full-key rerun.
+template <int V, bool SORTED>
 __global__ void __launch_bounds__(256) drelu_extract_kernel(const float *__restrict__ x, int64_t n,
                                                             int dim, int64_t ldx, int k, bool vec,
                                                             float *__restrict__ val,
@@ -211,15 +231,32 @@ __global__ void __launch_bounds__(256) drelu_extract_kernel(const float *__restr
         // the lowest lane, with no ballot. Truncation is monotone, so this is exact
         // unless an element left behind shares the truncated key of the last one
         // taken -- checked below; such (rare) rows rerun with full keys + ballot.
+        // SORTED: the lane's q-th popped element went out in round t_q; the t_q are
+        // packed 5 bits each into `pos` and the stores happen once, after the rounds.
         const uint32_t lanebits = 31u - (uint32_t)lane;
         uint32_t fk[V];
 #pragma unroll
         for (int j = 0; j < V; ++j) fk[j] = sk[j] ? ((sk[j] & ~31u) | lanebits) : 0u;
-        uint32_t m = 0;
+        uint32_t m = 0, prev = 0;
+        uint64_t tpos = 0;
+        int popped = 0;
+        bool amb = false;   // SORTED: two heads from different lanes shared a truncated key
+        (void)prev;
+        (void)tpos;
+        (void)popped;
 #pragma unroll 4
         for (int t = 0; t < k; ++t) {
             m = __reduce_max_sync(0xffffffffu, fk[0]);
+            if constexpr (SORTED) {
+                // the set is still exact, but their order was decided by lane, not value
+                amb |= m != prev && ((m ^ prev) & ~31u) == 0u;
+                prev = m;
+            }
             if (fk[0] == m) {
+                if constexpr (SORTED) {
+                    tpos |= (uint64_t)t << (5 * popped);
+                    ++popped;
+                }
 #pragma unroll
                 for (int j = 0; j + 1 < V; ++j) fk[j] = fk[j + 1];
                 fk[V - 1] = 0u;
@@ -229,15 +266,18 @@ __global__ void __launch_bounds__(256) drelu_extract_kernel(const float *__restr
         int taken = 0;
 #pragma unroll
         for (int j = 0; j < V; ++j) taken += (fk[j] == 0u ? 1 : 0) - (sk[j] == 0u ? 1 : 0);
-        const bool unsafe = __any_sync(0xffffffffu, fk[0] != 0u && (fk[0] & ~31u) == (m & ~31u));
+        const bool unsafe =
+            __any_sync(0xffffffffu, fk[0] != 0u && (fk[0] & ~31u) == (m & ~31u)) || amb;
         if (unsafe) {
             taken = 0;
+            tpos = 0;
 #pragma unroll 4
             for (int t = 0; t < k; ++t) {
                 const uint32_t mm = __reduce_max_sync(0xffffffffu, sk[0]);
                 const bool mine = sk[0] == mm;
                 const uint32_t b = __ballot_sync(0xffffffffu, mine);
                 if (mine && (b & ltmask) == 0u) {
+                    if constexpr (SORTED) tpos |= (uint64_t)t << (5 * taken);
                     ++taken;
 #pragma unroll
                     for (int j = 0; j + 1 < V; ++j) sk[j] = sk[j + 1];
@@ -245,13 +285,24 @@ __global__ void __launch_bounds__(256) drelu_extract_kernel(const float *__restr
                 }
             }
         }
+        float *vo = val + r * k;
+        uint8_t *io = idx + r * k;
+        if constexpr (SORTED) {
+#pragma unroll
+            for (int q = 0; q < V; ++q)
+                if (q < taken) {
+                    const int t = (int)((tpos >> (5 * q)) & 31u);
+                    const int slot = sp[q];
+                    vo[t] = pick_f<V>(v, slot);
+                    io[t] = (uint8_t)(lane * V + slot);
+                }
+            continue;
+        }
         uint32_t selm = 0;
 #pragma unroll
         for (int q = 0; q < V; ++q)
             if (q < taken) selm |= 1u << sp[q];
         int pos = warp_excl_scan(__popc(selm), lane);
-        float *vo = val + r * k;
-        uint8_t *io = idx + r * k;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
             if (selm & (1u << j)) {
@@ -266,7 +317,7 @@ __global__ void __launch_bounds__(256) drelu_extract_kernel(const float *__restr
 }  // namespace
 
 void launch_drelu(const float *x, int64_t n, int dim, int64_t ldx, int k, float *val,
-                  uint8_t *idx, cudaStream_t s) {
+                  uint8_t *idx, cudaStream_t s, bool sorted) {
     if (n <= 0) return;
     ProfScope ps("drelu", s);
     const int threads = 256, rows_per_cta = threads / 32;
@@ -275,15 +326,25 @@ void launch_drelu(const float *x, int64_t n, int dim, int64_t ldx, int k, float 
     const int V = dim <= 32 ? 1 : dim <= 64 ? 2 : dim <= 128 ? 4 : 8;
     const bool vec = dim == 32 * V && (ldx % V) == 0 &&
                      (reinterpret_cast<uintptr_t>(x) % (4 * V)) == 0;
-    if (k <= 32) {
+    DR_CHECK(!sorted || k <= 32, DR_ERR_BAD_K, "value-sorted D-ReLU needs k <= 32");
+    if (k <= 32 && sorted) {
         if (V == 1)
-            drelu_extract_kernel<1><<<(unsigned)blocks, threads, 0, s>>>(x, n, dim, ldx, k, vec, val, idx);
+            drelu_extract_kernel<1, true><<<(unsigned)blocks, threads, 0, s>>>(x, n, dim, ldx, k, vec, val, idx);
         else if (V == 2)
-            drelu_extract_kernel<2><<<(unsigned)blocks, threads, 0, s>>>(x, n, dim, ldx, k, vec, val, idx);
+            drelu_extract_kernel<2, true><<<(unsigned)blocks, threads, 0, s>>>(x, n, dim, ldx, k, vec, val, idx);
         else if (V == 4)
-            drelu_extract_kernel<4><<<(unsigned)blocks, threads, 0, s>>>(x, n, dim, ldx, k, vec, val, idx);
+            drelu_extract_kernel<4, true><<<(unsigned)blocks, threads, 0, s>>>(x, n, dim, ldx, k, vec, val, idx);
         else
-            drelu_extract_kernel<8><<<(unsigned)blocks, threads, 0, s>>>(x, n, dim, ldx, k, vec, val, idx);
+            drelu_extract_kernel<8, true><<<(unsigned)blocks, threads, 0, s>>>(x, n, dim, ldx, k, vec, val, idx);
+    } else if (k <= 32) {
+        if (V == 1)
+            drelu_extract_kernel<1, false><<<(unsigned)blocks, threads, 0, s>>>(x, n, dim, ldx, k, vec, val, idx);
+        else if (V == 2)
+            drelu_extract_kernel<2, false><<<(unsigned)blocks, threads, 0, s>>>(x, n, dim, ldx, k, vec, val, idx);
+        else if (V == 4)
+            drelu_extract_kernel<4, false><<<(unsigned)blocks, threads, 0, s>>>(x, n, dim, ldx, k, vec, val, idx);
+        else
+            drelu_extract_kernel<8, false><<<(unsigned)blocks, threads, 0, s>>>(x, n, dim, ldx, k, vec, val, idx);
     } else if (V == 1)
         drelu_kernel<1, 1><<<(unsigned)blocks, threads, 0, s>>>(x, n, dim, ldx, k, vec, val, idx);
     else if (V == 2)

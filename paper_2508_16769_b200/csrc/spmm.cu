@@ -77,7 +77,7 @@ __device__ __forceinline__ void fwd_accumulate(int e0, int e1, int stride,
                                                const float *__restrict__ ew,
                                                const float *__restrict__ hval,
                                                const uint8_t *__restrict__ hidx, int k, int ll,
-                                               float *acc) {
+                                               float *acc, int kr) {
     int jn[kU];
     float wn[kU];
 #pragma unroll
@@ -95,7 +95,12 @@ __device__ __forceinline__ void fwd_accumulate(int e0, int e1, int stride,
         Pairs<P> pr[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u)
-            if (j[u] >= 0) load_pairs<P>(hval, hidx, (int64_t)j[u] * k + ll * P, pr[u]);
+            if (j[u] >= 0 && ll * P < kr) {                    // lanes beyond the K prefix idle
+                load_pairs<P>(hval, hidx, (int64_t)j[u] * k + ll * P, pr[u]);
+#pragma unroll
+                for (int p = 0; p < P; ++p)
+                    if (ll * P + p >= kr) pr[u].v[p] = 0.f;     // beyond this row's K prefix
+            }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const int ee = e + (kU + u) * stride;
@@ -105,7 +110,7 @@ __device__ __forceinline__ void fwd_accumulate(int e0, int e1, int stride,
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u)
-            if (j[u] >= 0) {
+            if (j[u] >= 0 && ll * P < kr) {
                 float old[P];
 #pragma unroll
                 for (int p = 0; p < P; ++p) old[p] = acc[pr[u].id[p]];
@@ -126,7 +131,13 @@ struct FwdArgs {
     int k, D, L;
     float *z;
     int z_split;                     // z rows as [hi | lo] bf16 halves (4 D bytes per row)
+    NgSched ng;                      // per-neighbour-group K (value-sorted CBSR prefix)
 };
+
+__device__ __forceinline__ int ng_k(const NgSched &ng, int deg, int k) {
+    if (!ng.on) return k;
+    return deg <= ng.thr0 ? ng.kb0 : deg <= ng.thr1 ? ng.kb1 : ng.kb2;
+}
 
 // Z output: fp32, or split bf16 halves (x = hi + lo, the tensor-core operand
 // format of the projection / dW kernels, tc2.h)
@@ -173,7 +184,8 @@ __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
             __syncwarp();
             const int chunk = (e1 - e0 + S - 1) / S;
             const int b0 = min(e1, e0 + sidx * chunk), b1 = min(e1, b0 + chunk);
-            fwd_accumulate<P>(b0, b1, 1, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc);
+            fwd_accumulate<P>(b0, b1, 1, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc,
+                              ng_k(a.ng, e1 - e0, a.k));
             __syncthreads();
             const float cr = __ldg(a.c + row);
             for (int cc = threadIdx.x; cc < D; cc += blockDim.x) {
@@ -192,9 +204,11 @@ __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
         const int row = valid ? __ldg(a.order + pos) : 0;
         for (int c4 = ll; c4 < D4; c4 += L) acc4[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
         __syncwarp();
-        if (valid)
-            fwd_accumulate<P>(__ldg(a.rowptr + row) + sub, __ldg(a.rowptr + row + 1), R, a.col,
-                              a.ew, a.hval, a.hidx, a.k, ll, acc);
+        if (valid) {
+            const int e0 = __ldg(a.rowptr + row), e1 = __ldg(a.rowptr + row + 1);
+            fwd_accumulate<P>(e0 + sub, e1, R, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc,
+                              ng_k(a.ng, e1 - e0, a.k));
+        }
         __syncwarp();
         if (valid) {
             const float cr = __ldg(a.c + row);
@@ -217,9 +231,11 @@ __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
     const int row = valid ? __ldg(a.order + pos) : 0;
     for (int c4 = ll; c4 < D4; c4 += L) acc4[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncwarp();
-    if (valid)
-        fwd_accumulate<P>(__ldg(a.rowptr + row), __ldg(a.rowptr + row + 1), 1, a.col, a.ew,
-                          a.hval, a.hidx, a.k, ll, acc);
+    if (valid) {
+        const int e0 = __ldg(a.rowptr + row), e1 = __ldg(a.rowptr + row + 1);
+        fwd_accumulate<P>(e0, e1, 1, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc,
+                          ng_k(a.ng, e1 - e0, a.k));
+    }
     __syncwarp();
     if (valid) {
         const float cr = __ldg(a.c + row);
@@ -247,13 +263,17 @@ struct BwdArgs {
     int k, D, L;
     float *g_kept, *dx;
     int accumulate;
+    NgSched ng;
 };
 
 // Pull dz[i, id[p]] over CSC entries e0, e0+stride, ... < e1 into a[p].
+// NEXT-2 (ng.on): destination i used only the first K(deg_i) = ng.kT[e] entries of
+// this source row, so positions pos0 + p >= K(deg_i) neither load nor add.
 template <int P>
 __device__ __forceinline__ void bwd_term(const TermDev &t, int e0, int e1, int stride,
-                                         const uint32_t *id, int D, float *a) {
-    int in[kU];
+                                         const uint32_t *id, int D, float *a, const NgSched &ng,
+                                         int pos0, int k) {
+    int in[kU], kn[kU];
     float wn[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -261,19 +281,23 @@ __device__ __forceinline__ void bwd_term(const TermDev &t, int e0, int e1, int s
         const bool ok = ee < e1;
         in[u] = ok ? __ldg(t.row + ee) : -1;
         wn[u] = (ok && t.ewT) ? __ldg(t.ewT + ee) : 1.0f;
+        kn[u] = (ok && ng.on) ? (int)__ldg(ng.kT + ee) : k;
     }
     for (int e = e0; e < e1; e += kU * stride) {
-        int i[kU];
+        int i[kU], ki[kU];
         float w[kU];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) { i[u] = in[u]; w[u] = wn[u]; }
+        for (int u = 0; u < kU; ++u) { i[u] = in[u]; w[u] = wn[u]; ki[u] = kn[u]; }
         float v[kU][P];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-            if (i[u] >= 0) {
+#pragma unroll
+            for (int p = 0; p < P; ++p) v[u][p] = 0.f;
+            if (i[u] >= 0 && pos0 < ki[u]) {
                 const float *dzr = t.dz + (int64_t)i[u] * D;
 #pragma unroll
-                for (int p = 0; p < P; ++p) v[u][p] = __ldg(dzr + id[p]);
+                for (int p = 0; p < P; ++p)
+                    if (pos0 + p < ki[u]) v[u][p] = __ldg(dzr + id[p]);
                 if (t.c) w[u] *= __ldg(t.c + i[u]);
             }
         }
@@ -283,6 +307,7 @@ __device__ __forceinline__ void bwd_term(const TermDev &t, int e0, int e1, int s
             const bool ok = ee < e1;
             in[u] = ok ? __ldg(t.row + ee) : -1;
             wn[u] = (ok && t.ewT) ? __ldg(t.ewT + ee) : 1.0f;
+            kn[u] = (ok && ng.on) ? (int)__ldg(ng.kT + ee) : k;
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u)
@@ -370,7 +395,7 @@ __global__ void __launch_bounds__(256, 4) spmm_bwd_kernel(BwdArgs a) {
                 float acc[P];
 #pragma unroll
                 for (int p = 0; p < P; ++p) acc[p] = 0.f;
-                bwd_term<P>(t, b0, b1, 1, id, a.D, acc);
+                bwd_term<P>(t, b0, b1, 1, id, a.D, acc, a.ng, ll * P, a.k);
                 const float sj = __ldg(t.s + j);
 #pragma unroll
                 for (int p = 0; p < P; ++p) g[p] += sj * acc[p];
@@ -431,7 +456,7 @@ __global__ void __launch_bounds__(256, 4) spmm_bwd_kernel(BwdArgs a) {
 #pragma unroll
             for (int p = 0; p < P; ++p) acc[p] = 0.f;
             bwd_term<P>(t, __ldg(t.colptr + j) + first, __ldg(t.colptr + j + 1), stride, id, a.D,
-                        acc);
+                        acc, a.ng, ll * P, a.k);
             const float sj = __ldg(t.s + j);
 #pragma unroll
             for (int p = 0; p < P; ++p) g[p] += sj * acc[p];
@@ -468,9 +493,9 @@ int choose_P(int k, int D) {
 void ensure_smem(const void *fn, size_t bytes);
 
 void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
-                     float *z, cudaStream_t s, bool z_split) {
+                     float *z, cudaStream_t s, bool z_split, NgSched ng) {
     if (r.n_dst <= 0) return;
-    if (!r.ew && tspmm_supported(r.tiles, dim, k)) {      // tensor-core tiled path
+    if (!ng.on && !r.ew && tspmm_supported(r.tiles, dim, k)) {     // tensor-core tiled path
         launch_tspmm_fwd(r, hval, hidx, k, dim, z, s, z_split);
         return;
     }
@@ -493,6 +518,7 @@ void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, in
     a.D = dim;
     a.z = z;
     a.z_split = z_split ? 1 : 0;
+    a.ng = ng;
     int wpc = 8;
     while (wpc > 1 && (size_t)wpc * R * dim * 4 > 96 * 1024) wpc >>= 1;
     const size_t smem = (size_t)wpc * R * dim * 4;
@@ -530,15 +556,16 @@ static int choose_P_bwd(int k) {
 
 void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, const float *root,
                      const uint8_t *hidx, int k, int dim, float *g_kept, float *dx,
-                     bool accumulate, cudaStream_t s) {
+                     bool accumulate, cudaStream_t s, NgSched ng) {
     if (n_src <= 0) return;
-    if (t0.rel && !t1.rel && !t0.rel->ewT && !accumulate && tspmm_supported(t0.rel->tilesT, dim, k) &&
+    if (!ng.on && t0.rel && !t1.rel && !t0.rel->ewT && !accumulate && tspmm_supported(t0.rel->tilesT, dim, k) &&
         t0.rel->n_src == n_src) {                           // tensor-core tiled path
         launch_tspmm_bwd(*t0.rel, t0.dz, false, t0.apply_c, root, hidx, k, dim, g_kept, dx, s);
         return;
     }
     const int P = choose_P_bwd(k);
     DR_CHECK(P > 0, DR_ERR_BAD_K, "spmm_bwd: unsupported k");
+    DR_CHECK(!ng.on || (ng.kT && !t1.rel), DR_ERR_INVALID_ARGUMENT, "spmm_bwd: NEXT-2 needs kT, one term");
     BwdArgs a{};
     a.order = sched.order;
     a.L = k / P;
@@ -566,6 +593,7 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, c
     a.g_kept = g_kept;
     a.dx = dx;
     a.accumulate = accumulate ? 1 : 0;
+    a.ng = ng;
     int wpc = 8;
     while (wpc > 1 && (size_t)wpc * R * dim * 4 > 96 * 1024) wpc >>= 1;
     size_t smem = (size_t)wpc * R * dim * 4;
@@ -589,6 +617,25 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, c
         spmm_bwd_kernel<1><<<grid, wpc * 32, smem, s>>>(a);
     }
     note_launch("spmm_bwd");
+}
+
+__global__ void ng_edge_k_kernel(const int32_t *__restrict__ row, const int32_t *__restrict__ rowptr,
+                                 int64_t nnz, NgSched ng, uint8_t *__restrict__ kT) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int i = __ldg(row + e);
+        const int deg = __ldg(rowptr + i + 1) - __ldg(rowptr + i);
+        kT[e] = (uint8_t)(deg <= ng.thr0 ? ng.kb0 : deg <= ng.thr1 ? ng.kb1 : ng.kb2);
+    }
+}
+
+void launch_ng_edge_k(const RelDev &r, const NgSched &ng, uint8_t *kT, cudaStream_t s) {
+    if (r.nnz <= 0) return;
+    ProfScope ps("ng_edge_k", s);
+    int64_t blocks = (r.nnz + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    ng_edge_k_kernel<<<(unsigned)blocks, 256, 0, s>>>(r.row, r.rowptr, r.nnz, ng, kT);
+    note_launch("ng_edge_k");
 }
 
 }  // namespace dr
