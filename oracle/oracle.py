@@ -186,10 +186,13 @@ def layer_params(P, l):
     return {k.split(".", 1)[1]: _f64(v) for k, v in P.items() if k.startswith(f"l{l}.")}
 
 
-def layer_fwd(G, W, x_c, x_n, k_c, k_n, merge="max", root=True):
+def layer_fwd(G, W, x_c, x_n, k_c, k_n, merge="max", root=True, k_p=None):
     """One HeteroConv layer (Eq. 2-9):
        H = drelu(X) per node type (Eq. 2-3)
        Z_psi = SpMM_psi(H_src)          (Eq. 5-7, three relations)
+       [per-edge-type k (reading Q27, §8 f3): k_p != k_c gives pins its own cell
+        CBSR H_p = drelu(X_c, k_p); Z_pins = SpMM_pins(H_p); near and the roots keep
+        H_c / H_n]
        Y_near = Z_near Wn + H_c Wr + b  (SageConv mean, Q2 root weight)
        Y_pinned = Z_pinned W + b        (GraphConv both)
        Y_net = Z_pins Wn + H_n Wr + b   (SageConv mean)
@@ -202,7 +205,11 @@ def layer_fwd(G, W, x_c, x_n, k_c, k_n, merge="max", root=True):
     Hc = densify(hc_idx, hc_val, d_c)
     Hn = densify(hn_idx, hn_val, d_n)
     z_near = G.fwd("near", hc_idx, hc_val, d_c)
-    z_pins = G.fwd("pins", hc_idx, hc_val, d_c)
+    if k_p is None or k_p == k_c:
+        hp_idx, hp_val = hc_idx, hc_val
+    else:
+        hp_idx, hp_val = drelu(x_c, k_p)
+    z_pins = G.fwd("pins", hp_idx, hp_val, d_c)
     z_pinned = G.fwd("pinned", hn_idx, hn_val, d_n)
     y_near = z_near @ W["wn_near"] + W["b_near"]
     y_net = z_pins @ W["wn_pins"] + W["b_pins"]
@@ -219,6 +226,7 @@ def layer_fwd(G, W, x_c, x_n, k_c, k_n, merge="max", root=True):
     else:
         raise ValueError(merge)
     tape = dict(hc_idx=hc_idx, hc_val=hc_val, hn_idx=hn_idx, hn_val=hn_val, Hc=Hc, Hn=Hn,
+                hp_idx=hp_idx, hp_val=hp_val,
                 z_near=z_near, z_pins=z_pins, z_pinned=z_pinned, y_near=y_near,
                 y_pinned=y_pinned, M=M, d_c=d_c, d_n=d_n, merge=merge, root=root)
     return y_cell, y_net, tape
@@ -231,7 +239,9 @@ def layer_bwd(G, W, tape, dy_cell, dy_net, need_dx=True):
        dZ_psi = dY_psi Wn_psi^T
        g_c = SSpMM_near(dZ_near) + SSpMM_pins(dZ_pins) + (dY_near Wr_near^T)[idx_c]
        g_n = SSpMM_pinned(dZ_pinned) + (dY_net Wr_pins^T)[idx_n]
-       dX = scatter(g) (D-ReLU mask gradient: zero off the kept support)."""
+       dX = scatter(g) (D-ReLU mask gradient: zero off the kept support).
+       Per-edge-type k (Q27): the pins term is taken at pins' own kept indices and
+       scattered separately, dX_c = scatter(g_near + root, idx_c) + scatter(g_pins, idx_p)."""
     dy_cell, dy_net = _f64(dy_cell), _f64(dy_net)
     if tape["merge"] == "max":
         M = tape["M"]
@@ -254,13 +264,20 @@ def layer_bwd(G, W, tape, dy_cell, dy_net, need_dx=True):
     dx_c = dx_n = None
     if need_dx:
         hc_idx, hn_idx = tape["hc_idx"], tape["hn_idx"]
-        g_c = G.bwd("near", hc_idx, dy_near @ W["wn_near"].T) + \
-            G.bwd("pins", hc_idx, dy_net @ W["wn_pins"].T)
+        hp_idx = tape.get("hp_idx", hc_idx)
+        shared = hp_idx is hc_idx
+        g_c = G.bwd("near", hc_idx, dy_near @ W["wn_near"].T)
+        g_p = G.bwd("pins", hp_idx, dy_net @ W["wn_pins"].T)
+        if shared:
+            g_c = g_c + g_p
         g_n = G.bwd("pinned", hn_idx, dy_pinned @ W["w_pinned"].T)
         if tape["root"]:
             g_c = g_c + gather_at(dy_near @ W["wr_near"].T, hc_idx)
             g_n = g_n + gather_at(dy_net @ W["wr_pins"].T, hn_idx)
         dx_c = densify(hc_idx, g_c, tape["d_c"])
+        if not shared:
+            dx_c = dx_c + densify(hp_idx, g_p, tape["d_c"])
+            tape["g_p"] = g_p
         dx_n = densify(hn_idx, g_n, tape["d_n"])
         tape["g_c"], tape["g_n"] = g_c, g_n
     return grads, dx_c, dx_n
@@ -289,7 +306,7 @@ def adam(theta, grad, m, v, step, lr=2e-4, wd=1e-5, b1=0.9, b2=0.999, eps=1e-8):
 
 
 # ------------------------------------------------------------------ model
-def model_fwd_bwd(G, P, n_layers, k_c, k_n, x_c, x_n, labels, merge="max"):
+def model_fwd_bwd(G, P, n_layers, k_c, k_n, x_c, x_n, labels, merge="max", k_p=None):
     """2-layer model: layers -> head/MSE -> backward; the first
     layer's SSpMM is skipped (input features need no gradient). Returns
     (loss, grads dict keyed like P, tapes)."""
@@ -297,7 +314,7 @@ def model_fwd_bwd(G, P, n_layers, k_c, k_n, x_c, x_n, labels, merge="max"):
     hc, hn = _f64(x_c), _f64(x_n)
     for l in range(n_layers):
         W = layer_params(P, l)
-        hc, hn, tape = layer_fwd(G, W, hc, hn, k_c, k_n, merge=merge)
+        hc, hn, tape = layer_fwd(G, W, hc, hn, k_c, k_n, merge=merge, k_p=k_p)
         tapes.append(tape)
         Ws.append(W)
     loss, hg, dy_c = head_mse(hc, P["head.w"], P["head.b"], labels)

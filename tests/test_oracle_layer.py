@@ -208,3 +208,69 @@ def test_dp_mean_equals_union_gradient():
     gm = O.dp_mean([ga, gb])
     for k in gu:
         assert np.allclose(gm[k], gu[k], rtol=1e-10, atol=1e-13), k
+
+
+# ------------------------------------------------------------------ per-edge-type k (Q27, §8 f3)
+def torch_topk_layer(design, W, x_c, x_n, k_c, k_p, k_n):
+    """Independent route: D-ReLU as a torch.topk mask (tie-free instances), dense
+    adjacency, autograd for the gradients. pins reads drelu(X_c, k_p), near and the
+    near root drelu(X_c, k_c), pinned and the pins root drelu(X_n, k_n)."""
+    def adj(r):
+        ptr, col, nd, ns = design.rel(r)
+        A = torch.zeros(nd, ns, dtype=torch.float64)
+        A[torch.repeat_interleave(torch.arange(nd), torch.as_tensor(np.diff(ptr))),
+          torch.as_tensor(col.astype(np.int64))] = 1.0
+        return A
+
+    def topk_mask(x, k):
+        m = torch.zeros_like(x)
+        m.scatter_(1, torch.topk(x.detach(), k, dim=1).indices, 1.0)
+        return x * m
+    An, Ap, Aq = adj("near"), adj("pins"), adj("pinned")
+    mean = lambda A: A / A.sum(1, keepdim=True).clamp(min=1)
+    sym = lambda A: A / A.sum(1, keepdim=True).clamp(min=1).sqrt() / A.sum(0, keepdim=True).clamp(min=1).sqrt()
+    hc, hp, hn = topk_mask(x_c, k_c), topk_mask(x_c, k_p), topk_mask(x_n, k_n)
+    y_near = mean(An) @ hc @ W["wn_near"] + hc @ W["wr_near"] + W["b_near"]
+    y_pinned = sym(Aq) @ hn @ W["w_pinned"] + W["b_pinned"]
+    y_net = mean(Ap) @ hp @ W["wn_pins"] + hn @ W["wr_pins"] + W["b_pins"]
+    return torch.maximum(y_near, y_pinned), y_net
+
+
+@pytest.mark.parametrize("k_c,k_p", [(4, 8), (8, 2), (4, 4)])
+def test_layer_per_edge_type_k_matches_topk_autograd(k_c, k_p):
+    for seed in range(1, 300):
+        d = make_design("pe", 40, seed, d_cell=16, d_net=16, near_mean=5.0, near_cap=16,
+                        pins_mean=2.5, pins_dmax=12, n_net=25)
+        if all(gaps_ok(d.x_cell, k, 1e-3) for k in (k_c, k_p)) and gaps_ok(d.x_net, 4, 1e-3):
+            break
+    P = make_params(16, 16, 16, 1, seed=seed)
+    G = O.OGraph(d)
+    W = O.layer_params(P, 0)
+    y_c, y_n, tape = O.layer_fwd(G, W, d.x_cell, d.x_net, k_c, 4, k_p=k_p)
+    Wt = {k: torch.tensor(v, requires_grad=True) for k, v in W.items()}
+    xc = torch.tensor(d.x_cell.astype(np.float64), requires_grad=True)
+    xn = torch.tensor(d.x_net.astype(np.float64), requires_grad=True)
+    tc, tn = torch_topk_layer(d, Wt, xc, xn, k_c, k_p, 4)
+    assert np.allclose(y_c, tc.detach().numpy(), rtol=1e-12, atol=1e-12)
+    assert np.allclose(y_n, tn.detach().numpy(), rtol=1e-12, atol=1e-12)
+    rng = np.random.default_rng(seed)
+    dyc, dyn = rng.standard_normal(y_c.shape), rng.standard_normal(y_n.shape)
+    grads, dxc, dxn = O.layer_bwd(G, W, tape, dyc, dyn)
+    (tc * torch.tensor(dyc)).sum().add((tn * torch.tensor(dyn)).sum()).backward()
+    for k in W:
+        assert np.allclose(grads[k], Wt[k].grad.numpy(), rtol=1e-10, atol=1e-12), k
+    assert np.allclose(dxc, xc.grad.numpy(), rtol=1e-10, atol=1e-12)
+    assert np.allclose(dxn, xn.grad.numpy(), rtol=1e-10, atol=1e-12)
+
+
+def test_layer_per_edge_type_k_reduces_to_per_node_type():
+    """Y_cell depends on k_c only and Y_net on k_p only (near/pinned vs pins)."""
+    d = make_config("C1")
+    P = make_params(16, 16, 16, 1, seed=4)
+    G = O.OGraph(d)
+    W = O.layer_params(P, 0)
+    yc, yn, _ = O.layer_fwd(G, W, d.x_cell, d.x_net, 4, 4, k_p=8)
+    yc4, _, _ = O.layer_fwd(G, W, d.x_cell, d.x_net, 4, 4)
+    _, yn8, _ = O.layer_fwd(G, W, d.x_cell, d.x_net, 8, 4)
+    assert np.array_equal(yc, yc4)
+    assert np.array_equal(yn, yn8)
