@@ -161,13 +161,21 @@ dr_status dr_spmm_bwd(const dr_graph *g, dr_rel r, const float *dz, const dr_cbs
  *   Y_cell = max(Y_near, Y_pinned), M = [Y_near >= Y_pinned]      (Eq. 8, Eq. 14)
  * Weights are DEVICE fp32: wn[r] is d_in(src type of r) x d_out; wr[r] is
  * d_in(dst type of r) x d_out or NULL (no root term). wr[DR_PINNED] must be
- * NULL (GraphConv has no root weight; DR_ERR_UNSUPPORTED otherwise). */
+ * NULL (GraphConv has no root weight; DR_ERR_UNSUPPORTED otherwise).
+ * k_pins: per-edge-type k ("k_pinned, k_near, and k_pins"; reading Q27):
+ * 0 = k_cell (per node type). Otherwise pins reads its own cell CBSR
+ *   H_p = drelu(X_c, k_pins),  Z_pins = DR-SpMM_pins(H_p),
+ * near and the near root keep H_c (k_near = k_cell), pinned and the pins root
+ * keep H_n (k_pinned = k_net); the backward adds pins' D-ReLU mask gradient at
+ * H_p's indices: dX_c = scatter(g_near + root, idx_c) + scatter(g_pins, idx_p).
+ * Same restrictions as k_cell. */
 typedef struct {
     int32_t d_cell, d_net, d_out, k_cell, k_net;
     dr_merge merge;
     const float *wn[3];
     const float *wr[3];
     const float *b[3];
+    int32_t k_pins;
 } dr_layer;
 typedef struct {
     float *wn[3];
@@ -206,6 +214,7 @@ typedef struct {
     float *y_near, *y_pinned;
     uint32_t *mask;
     int32_t z_split[3];
+    dr_cbsr h_pins;                 /* pins' source CBSR (== h_cell unless k_pins set) */
 } dr_tape_view;
 dr_status dr_heteroconv_tape_view(const dr_graph *g, const dr_layer *L, void *tape,
                                   uint32_t flags, dr_tape_view *view);
@@ -258,6 +267,7 @@ dr_status dr_spmm_bwd_ng(const dr_ng_plan *p, const float *dz, const dr_cbsr *h_
 typedef struct {
     int32_t n_layers, d_in_cell, d_in_net, d_hidden, k_cell, k_net;
     float lr, weight_decay, beta1, beta2, eps;
+    int32_t k_pins;                 /* per-edge-type k of every layer (dr_layer.k_pins), 0 = k_cell */
 } dr_train_cfg;
 typedef struct dr_trainer dr_trainer;         /* opaque, single-threaded use */
 

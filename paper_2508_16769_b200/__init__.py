@@ -259,11 +259,12 @@ LAYER_KEYS = ("wn_near", "wr_near", "b_near", "w_pinned", "b_pinned", "wn_pins",
 class Layer:
     """dr_layer over torch tensors W (keys as LAYER_KEYS; wr_* may be None)."""
 
-    def __init__(self, W, d_cell, d_net, d_out, k_cell, k_net, merge=DR_MERGE_MAX):
+    def __init__(self, W, d_cell, d_net, d_out, k_cell, k_net, merge=DR_MERGE_MAX, k_pins=0):
         self.W = W
         L = dr_layer()
         L.d_cell, L.d_net, L.d_out, L.k_cell, L.k_net, L.merge = (
             d_cell, d_net, d_out, k_cell, k_net, merge)
+        L.k_pins = k_pins              # per-edge-type k (Q27); 0 = k_cell
         L.wn[DR_NEAR] = W["wn_near"].data_ptr()
         L.wn[DR_PINNED] = W["w_pinned"].data_ptr()
         L.wn[DR_PINS] = W["wn_pins"].data_ptr()
@@ -323,6 +324,8 @@ def tape_view(g, layer, tape, flags=0):
         hc_idx=sl(v.h_cell.idx, (nc, L.k_cell), torch.uint8),
         hn_val=sl(v.h_net.val, (nn, L.k_net), torch.float32),
         hn_idx=sl(v.h_net.idx, (nn, L.k_net), torch.uint8),
+        hp_val=sl(v.h_pins.val, (nc, v.h_pins.k), torch.float32),
+        hp_idx=sl(v.h_pins.idx, (nc, v.h_pins.k), torch.uint8),
         z_near=zview(DR_NEAR, nc, L.d_cell),
         z_pins=zview(DR_PINS, nn, L.d_cell),
         z_pinned=zview(DR_PINNED, nc, L.d_net),
@@ -394,10 +397,11 @@ class Trainer:
     """dr_trainer over a flat device parameter tensor (updated in place)."""
 
     def __init__(self, params, n_layers, d_in_cell, d_in_net, d_hidden, k_cell, k_net,
-                 lr=2e-4, weight_decay=1e-5, beta1=0.9, beta2=0.999, eps=1e-8, nccl_comm=None):
+                 lr=2e-4, weight_decay=1e-5, beta1=0.9, beta2=0.999, eps=1e-8, nccl_comm=None,
+                 k_pins=0):
         torch = _torch()
         cfg = dr_train_cfg(n_layers, d_in_cell, d_in_net, d_hidden, k_cell, k_net, lr,
-                           weight_decay, beta1, beta2, eps)
+                           weight_decay, beta1, beta2, eps, k_pins)
         self.cfg = cfg
         self.n_params = int(lib().dr_train_param_count(C.byref(cfg)))
         assert params.numel() == self.n_params and params.dtype == torch.float32

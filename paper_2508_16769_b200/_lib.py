@@ -54,7 +54,7 @@ class dr_cbsr(C.Structure):
 class dr_layer(C.Structure):
     _fields_ = [("d_cell", C.c_int32), ("d_net", C.c_int32), ("d_out", C.c_int32),
                 ("k_cell", C.c_int32), ("k_net", C.c_int32), ("merge", C.c_int),
-                ("wn", P * 3), ("wr", P * 3), ("b", P * 3)]
+                ("wn", P * 3), ("wr", P * 3), ("b", P * 3), ("k_pins", C.c_int32)]
 
 
 class dr_layer_grad(C.Structure):
@@ -63,7 +63,7 @@ class dr_layer_grad(C.Structure):
 
 class dr_tape_view(C.Structure):
     _fields_ = [("h_cell", dr_cbsr), ("h_net", dr_cbsr), ("z", P * 3), ("y_near", P),
-                ("y_pinned", P), ("mask", P), ("z_split", C.c_int32 * 3)]
+                ("y_pinned", P), ("mask", P), ("z_split", C.c_int32 * 3), ("h_pins", dr_cbsr)]
 
 
 class dr_ng_sched(C.Structure):
@@ -79,7 +79,7 @@ class dr_train_cfg(C.Structure):
     _fields_ = [("n_layers", C.c_int32), ("d_in_cell", C.c_int32), ("d_in_net", C.c_int32),
                 ("d_hidden", C.c_int32), ("k_cell", C.c_int32), ("k_net", C.c_int32),
                 ("lr", C.c_float), ("weight_decay", C.c_float), ("beta1", C.c_float),
-                ("beta2", C.c_float), ("eps", C.c_float)]
+                ("beta2", C.c_float), ("eps", C.c_float), ("k_pins", C.c_int32)]
 
 
 _SIGS = {

@@ -170,8 +170,12 @@ static void check_out_width(int n, const char *what) {
 }
 
 // ------------------------------------------------------------------ tape layout
+// per-edge-type k (Q27): pins' source CBSR width; == k_cell shares H_c
+static int k_pins_of(const dr_layer *L) { return L->k_pins ? L->k_pins : L->k_cell; }
+static bool pins_own(const dr_layer *L) { return k_pins_of(L) != L->k_cell; }
+
 struct TapeLayout {
-    size_t hc_val, hc_idx, hn_val, hn_idx, z[3], mask, tap_a, tap_b;
+    size_t hc_val, hc_idx, hn_val, hn_idx, hp_val, hp_idx, z[3], mask, tap_a, tap_b;
     size_t dz[3], root_c, root_n, work[3];
     size_t img_fa, img_fb, img_fn, img_dz[3];     // packed tcgen05 B operands
     size_t total;
@@ -189,6 +193,9 @@ static TapeLayout tape_layout(const dr_graph *g, const dr_layer *L, uint32_t fla
     t.hc_idx = put(nc * kc);
     t.hn_val = put(nn * kn * 4);
     t.hn_idx = put(nn * kn);
+    const size_t kp = (size_t)k_pins_of(L);
+    t.hp_val = pins_own(L) ? put(nc * kp * 4) : t.hc_val;
+    t.hp_idx = pins_own(L) ? put(nc * kp) : t.hc_idx;
     t.z[DR_NEAR] = put(nc * dc * 4);
     t.z[DR_PINS] = put(nn * dc * 4);
     t.z[DR_PINNED] = put(nc * dn * 4);
@@ -220,6 +227,8 @@ static void check_layer(const dr_graph *g, const dr_layer *L) {
     DR_CHECK(g && L, DR_ERR_INVALID_ARGUMENT, "null graph/layer");
     check_k(L->k_cell, L->d_cell, "layer k_cell/d_cell");
     check_k(L->k_net, L->d_net, "layer k_net/d_net");
+    DR_CHECK(L->k_pins >= 0, DR_ERR_BAD_K, "layer: negative k_pins");
+    check_k(k_pins_of(L), L->d_cell, "layer k_pins/d_cell");
     check_out_width(L->d_out, "layer d_out");
     check_out_width(L->d_cell, "layer d_cell");
     check_out_width(L->d_net, "layer d_net");
@@ -245,6 +254,9 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
     char *tp = (char *)tape;
     float *hcv = (float *)(tp + T.hc_val), *hnv = (float *)(tp + T.hn_val);
     uint8_t *hci = (uint8_t *)(tp + T.hc_idx), *hni = (uint8_t *)(tp + T.hn_idx);
+    float *hpv = (float *)(tp + T.hp_val);
+    uint8_t *hpi = (uint8_t *)(tp + T.hp_idx);
+    const int kp = k_pins_of(L);
     float *z[3];
     for (int r = 0; r < 3; ++r) z[r] = (float *)(tp + T.z[r]);
     const bool seq = (flags & DR_FWD_SEQUENTIAL) != 0 || force_sequential();
@@ -262,8 +274,13 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
     bool zs[3];
     for (int r = 0; r < 3; ++r) zs[r] = z_split_ok(L, r);
     { TagScope t("near"); launch_spmm_fwd(g->rel[DR_NEAR], hcv, hci, L->k_cell, L->d_cell, z[DR_NEAR], s0, zs[DR_NEAR]); }  // Eq. 5-7
-    if (!seq) DR_CUDA(cudaStreamWaitEvent(s1, C.ev[0], 0));
-    { TagScope t("pins"); launch_spmm_fwd(g->rel[DR_PINS], hcv, hci, L->k_cell, L->d_cell, z[DR_PINS], s1, zs[DR_PINS]); }
+    if (pins_own(L)) {          // Q27: pins' own cell CBSR, on its own stream
+        TagScope t("pins");
+        launch_drelu(xc, nc, L->d_cell, L->d_cell, kp, hpv, hpi, s1);
+    } else if (!seq) {
+        DR_CUDA(cudaStreamWaitEvent(s1, C.ev[0], 0));
+    }
+    { TagScope t("pins"); launch_spmm_fwd(g->rel[DR_PINS], hpv, hpi, kp, L->d_cell, z[DR_PINS], s1, zs[DR_PINS]); }
     { TagScope t("pinned"); launch_spmm_fwd(g->rel[DR_PINNED], hnv, hni, L->k_net, L->d_net, z[DR_PINNED], s2, zs[DR_PINNED]); }
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[2], s2));                               // Z_pinned ready
     if (!seq) DR_CUDA(cudaStreamWaitEvent(s1, C.ev[1], 0));
@@ -349,6 +366,9 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
     char *tp = (char *)tape;
     const float *hcv = (float *)(tp + T.hc_val), *hnv = (float *)(tp + T.hn_val);
     const uint8_t *hci = (uint8_t *)(tp + T.hc_idx), *hni = (uint8_t *)(tp + T.hn_idx);
+    const uint8_t *hpi = (uint8_t *)(tp + T.hp_idx);
+    const int kp = k_pins_of(L);
+    const bool own = pins_own(L);
     const uint32_t *mask = (uint32_t *)(tp + T.mask);
     float *z[3], *dz[3];
     for (int r = 0; r < 3; ++r) {
@@ -437,7 +457,20 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
             if (!seq) DR_CUDA(cudaStreamWaitEvent(s0, C.ev[0], 0));
             BwdTerm t0{&g->rel[DR_NEAR], dz[DR_NEAR], false}, t1{&g->rel[DR_PINS], dz[DR_PINS], false};
             TagScope t("cell");
-            if (near_tiled) {
+            if (own) {
+                // Q27: near (+ root) writes the dense dX_c row at idx_c, then the pins
+                // term adds its mask gradient at pins' own kept indices idx_p
+                const float *rootp = L->wr[DR_NEAR] ? root_c : nullptr;
+                if (near_tiled)
+                    launch_tspmm_bwd(rn, dz[DR_NEAR], near_split, false, rootp, hci, L->k_cell,
+                                     L->d_cell, nullptr, dxc, s0);
+                else
+                    launch_spmm_bwd(rn.bwd, nc, t0, BwdTerm{}, rootp, hci, L->k_cell, L->d_cell,
+                                    nullptr, dxc, false, s0);
+                TagScope t2("pins");
+                launch_spmm_bwd(g->rel[DR_PINS].bwd, nc, t1, BwdTerm{}, nullptr, hpi, kp,
+                                L->d_cell, nullptr, dxc, true, s0);
+            } else if (near_tiled) {
                 // tensor-core tiled near term; the low-degree pins term (+ the root
                 // term) first goes to root_c in place with the SIMT kernel, and the
                 // tiled kernel adds it in its epilogue as it would the root term
@@ -910,6 +943,7 @@ dr_status dr_heteroconv_tape_view(const dr_graph *g, const dr_layer *L, void *ta
     std::memset(v, 0, sizeof(*v));
     v->h_cell = dr_cbsr{g->n_cell, L->d_cell, L->k_cell, 1, tp + T.hc_idx, (float *)(tp + T.hc_val)};
     v->h_net = dr_cbsr{g->n_net, L->d_net, L->k_net, 1, tp + T.hn_idx, (float *)(tp + T.hn_val)};
+    v->h_pins = dr_cbsr{g->n_cell, L->d_cell, k_pins_of(L), 1, tp + T.hp_idx, (float *)(tp + T.hp_val)};
     for (int r = 0; r < 3; ++r) {
         v->z[r] = (float *)(tp + T.z[r]);
         v->z_split[r] = z_split_ok(L, r) ? 1 : 0;
@@ -946,6 +980,11 @@ dr_status dr_trainer_create(const dr_train_cfg *c, float *params, int64_t n_para
     check_k(c->k_net, c->d_in_net, "cfg k_net/d_in_net");
     check_k(c->k_cell, c->d_hidden, "cfg k_cell/d_hidden");
     check_k(c->k_net, c->d_hidden, "cfg k_net/d_hidden");
+    DR_CHECK(c->k_pins >= 0, DR_ERR_BAD_K, "cfg: negative k_pins");
+    if (c->k_pins) {
+        check_k(c->k_pins, c->d_in_cell, "cfg k_pins/d_in_cell");
+        check_k(c->k_pins, c->d_hidden, "cfg k_pins/d_hidden");
+    }
     check_out_width(c->d_hidden, "cfg d_hidden");
     check_out_width(c->d_in_cell, "cfg d_in_cell");
     check_out_width(c->d_in_net, "cfg d_in_net");
@@ -976,6 +1015,7 @@ dr_status dr_trainer_create(const dr_train_cfg *c, float *params, int64_t n_para
         l.d_out = c->d_hidden;
         l.k_cell = c->k_cell;
         l.k_net = c->k_net;
+        l.k_pins = c->k_pins;
         l.merge = DR_MERGE_MAX;
     }
     int dc = c->d_in_cell, dn = c->d_in_net;
