@@ -293,6 +293,59 @@ dr_status dr_nccl_unique_id(void *id128);
 dr_status dr_nccl_comm_init(const void *id128, int32_t nranks, int32_t rank, void **comm);
 dr_status dr_nccl_comm_destroy(void *comm);
 
+/* ------------------------------------------------------------------ single-graph multi-GPU
+ * SURVEY §8 f4 (beyond the paper): one relation's DR-SpMM (Eq. 5-7) and SSpMM
+ * (Eq. 10-11) split across `world` ranks by contiguous destination-row ranges
+ * (1-D partition). Rank q owns destinations [dst_part[q], dst_part[q+1]) and
+ * sources [src_part[q], src_part[q+1]). What crosses ranks is the compact
+ * CBSR, not dense features: the forward allgathers every rank's CBSR rows
+ * (k * 5 bytes per source row instead of dim * 4), the backward reduce-scatters
+ * the per-source partial g (k * 4 bytes per row) to the source's owner.
+ * Source rows live in a padded global space of world * max_src rows: global
+ * source j owned by q sits at row q * max_src + (j - src_part[q]); each rank's
+ * block is max_src rows, rows past its count are padding (no edge reads them).
+ * Normalisers are the global ones (Q12), so the union of the ranks' z_local is
+ * dr_spmm_fwd's Z and the sum of their g_part is dr_spmm_bwd's g. */
+typedef struct dr_shard dr_shard;
+typedef struct {
+    int32_t world, rank, max_src;
+    int64_t dst_begin, dst_end, src_begin, src_end, nnz_local;
+    size_t device_bytes;
+} dr_shard_info_t;
+/* Default partition (host only, no GPU): dst_part [world+1] balances edges
+ * (boundaries at the first row whose row_ptr reaches q * nnz / world);
+ * src_part [world+1] = dst_part for a square relation (n_dst == n_src), else
+ * balances rows. */
+dr_status dr_shard_plan(const dr_rel_desc *rel, int32_t world, int64_t *dst_part,
+                        int64_t *src_part);
+/* rel: the GLOBAL relation (HOST CSR, validated as in dr_graph_create).
+ * dst_part / src_part: [world+1] non-decreasing from 0 to n_dst / n_src, or
+ * NULL for dr_shard_plan's. Uploads this rank's row block on `stream`
+ * (synchronised before returning). */
+dr_status dr_shard_create(const dr_rel_desc *rel, int32_t world, int32_t rank,
+                          const int64_t *dst_part, const int64_t *src_part, const dr_allocator *a,
+                          void *stream, dr_shard **out);
+dr_status dr_shard_destroy(dr_shard *s);
+dr_status dr_shard_info(const dr_shard *s, dr_shard_info_t *info);
+/* h_local: n = max_src (this rank's sources, padded); h_all: n = world * max_src,
+ * same dim and k. NCCL allgather of val and idx on nccl_comm (a communicator of
+ * `world` ranks in rank order, from dr_nccl_comm_init); NULL only when world == 1. */
+dr_status dr_shard_allgather_cbsr(const dr_shard *s, const dr_cbsr *h_local, dr_cbsr *h_all,
+                                  void *nccl_comm, void *stream);
+/* z_local: DEVICE [dst_end - dst_begin x dim] = rows dst_begin.. of Z. */
+dr_status dr_shard_spmm_fwd(const dr_shard *s, const dr_cbsr *h_all, float *z_local, void *stream);
+/* dz_local: DEVICE [dst_end - dst_begin x dim] rows of dL/dZ; g_part: DEVICE
+ * [world * max_src x k] this rank's contribution to every source's g. */
+dr_status dr_shard_spmm_bwd(const dr_shard *s, const float *dz_local, const dr_cbsr *h_all,
+                            float *g_part, void *stream);
+/* g_local [max_src x k] = sum over ranks of their g_part rows for this rank's
+ * sources (NCCL reduce-scatter; NULL comm only when world == 1). If dx_local
+ * (DEVICE [max_src x dim]) is given, also writes the dense D-ReLU mask gradient:
+ * g_local scattered to h_local's indices, zeros elsewhere. */
+dr_status dr_shard_reduce_scatter_g(const dr_shard *s, const float *g_part,
+                                    const dr_cbsr *h_local, float *g_local, float *dx_local,
+                                    void *nccl_comm, void *stream);
+
 /* Per-kernel device timing: between dr_profile_begin and dr_profile_end every
  * libdr launch issued by this host thread is bracketed by CUDA events on the
  * stream it is launched on. dr_profile_end synchronises, aggregates by kernel

@@ -251,6 +251,114 @@ def spmm_bwd_ng(plan, dz, val, idx, dim, want_g=True, want_dx=False, g_out=None,
     return gk, dx
 
 
+# ------------------------------------------------------------------ single-graph multi-GPU (§8 f4)
+def _rel_desc(ptr, col, n_src, module, weight=None):
+    from ._lib import dr_rel_desc
+    ptr = np.ascontiguousarray(ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    w = None if weight is None else np.ascontiguousarray(weight, dtype=np.float32)
+    d = dr_rel_desc()
+    d.n_dst, d.n_src, d.nnz = int(ptr.shape[0]) - 1, int(n_src), int(col.shape[0])
+    d.row_ptr = ptr.ctypes.data
+    d.col_idx = col.ctypes.data if col.size else None
+    d.val = None if w is None else w.ctypes.data
+    d.module = int(module)
+    return d, (ptr, col, w)
+
+
+def shard_plan(ptr, col, n_src, world, module=DR_SAGE_MEAN):
+    """dr_shard_plan: default (dst_part, src_part), each int64 [world+1] (host only)."""
+    d, keep = _rel_desc(ptr, col, n_src, module)
+    dp = np.zeros(world + 1, np.int64)
+    sp = np.zeros(world + 1, np.int64)
+    check(lib().dr_shard_plan(C.byref(d), int(world), dp.ctypes.data, sp.ctypes.data))
+    return dp, sp
+
+
+class Shard:
+    """dr_shard: rank `rank`'s destination-row block of one relation (1-D partition
+    over `world` ranks, CBSR allgather / g reduce-scatter exchanges)."""
+
+    def __init__(self, ptr, col, n_src, world, rank, module=DR_SAGE_MEAN, weight=None,
+                 dst_part=None, src_part=None, stream=None):
+        d, keep = _rel_desc(ptr, col, n_src, module, weight)
+        dp = None if dst_part is None else np.ascontiguousarray(dst_part, np.int64)
+        sp = None if src_part is None else np.ascontiguousarray(src_part, np.int64)
+        h = C.c_void_p()
+        check(lib().dr_shard_create(C.byref(d), int(world), int(rank),
+                                    None if dp is None else dp.ctypes.data,
+                                    None if sp is None else sp.ctypes.data, None,
+                                    _stream(stream), C.byref(h)))
+        self.handle = h
+        i = self.info()
+        self.world, self.rank, self.max_src = i["world"], i["rank"], i["max_src"]
+        self.dst_begin, self.dst_end = i["dst_begin"], i["dst_end"]
+        self.src_begin, self.src_end = i["src_begin"], i["src_end"]
+
+    @classmethod
+    def from_design(cls, d, rel, world, rank, **kw):
+        ptr, col, nd, ns = d.rel(rel)
+        kw.setdefault("module", DEFAULT_MODULES[rel])
+        return cls(ptr, col, ns, world, rank, **kw)
+
+    def info(self):
+        from ._lib import dr_shard_info_t
+        i = dr_shard_info_t()
+        check(lib().dr_shard_info(self.handle, C.byref(i)))
+        return {f: getattr(i, f) for f, _ in dr_shard_info_t._fields_}
+
+    def allgather_cbsr(self, val_l, idx_l, dim, val_a=None, idx_a=None, comm=None, stream=None):
+        torch = _torch()
+        k = val_l.shape[1]
+        n_all = self.world * self.max_src
+        if val_a is None:
+            val_a = torch.empty((n_all, k), device=val_l.device, dtype=torch.float32)
+            idx_a = torch.empty((n_all, k), device=val_l.device, dtype=torch.uint8)
+        hl, ha = _cbsr(val_l, idx_l, dim), _cbsr(val_a, idx_a, dim)
+        check(lib().dr_shard_allgather_cbsr(self.handle, C.byref(hl), C.byref(ha),
+                                            C.c_void_p(comm) if comm else None, _stream(stream)))
+        return val_a, idx_a
+
+    def spmm_fwd(self, val_a, idx_a, dim, out=None, stream=None):
+        torch = _torch()
+        z = out if out is not None else torch.empty((self.dst_end - self.dst_begin, dim),
+                                                     device=val_a.device, dtype=torch.float32)
+        ha = _cbsr(val_a, idx_a, dim)
+        check(lib().dr_shard_spmm_fwd(self.handle, C.byref(ha), _ptr(z), _stream(stream)))
+        return z
+
+    def spmm_bwd(self, dz_l, val_a, idx_a, dim, out=None, stream=None):
+        torch = _torch()
+        g = out if out is not None else torch.empty(tuple(val_a.shape), device=dz_l.device,
+                                                     dtype=torch.float32)
+        ha = _cbsr(val_a, idx_a, dim)
+        check(lib().dr_shard_spmm_bwd(self.handle, _ptr(dz_l), C.byref(ha), _ptr(g),
+                                      _stream(stream)))
+        return g
+
+    def reduce_scatter_g(self, g_part, val_l, idx_l, dim, want_dx=True, comm=None, stream=None):
+        torch = _torch()
+        g_l = torch.empty(tuple(val_l.shape), device=g_part.device, dtype=torch.float32)
+        dx = (torch.empty((self.max_src, dim), device=g_part.device, dtype=torch.float32)
+              if want_dx else None)
+        hl = _cbsr(val_l, idx_l, dim)
+        check(lib().dr_shard_reduce_scatter_g(self.handle, _ptr(g_part), C.byref(hl), _ptr(g_l),
+                                              _ptr(dx), C.c_void_p(comm) if comm else None,
+                                              _stream(stream)))
+        return g_l, dx
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().dr_shard_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 # ------------------------------------------------------------------ HeteroConv layer
 LAYER_KEYS = ("wn_near", "wr_near", "b_near", "w_pinned", "b_pinned", "wn_pins", "wr_pins",
               "b_pins")

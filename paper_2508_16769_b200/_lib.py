@@ -70,6 +70,12 @@ class dr_ng_sched(C.Structure):
     _fields_ = [("thr", C.c_int32 * 2), ("kb", C.c_int32 * 3)]
 
 
+class dr_shard_info_t(C.Structure):
+    _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("max_src", C.c_int32),
+                ("dst_begin", C.c_int64), ("dst_end", C.c_int64), ("src_begin", C.c_int64),
+                ("src_end", C.c_int64), ("nnz_local", C.c_int64), ("device_bytes", C.c_size_t)]
+
+
 class dr_profile_entry(C.Structure):
     _fields_ = [("name", C.c_char * 48), ("launches", C.c_int64), ("total_ms", C.c_double),
                 ("max_ms", C.c_double)]
@@ -100,6 +106,15 @@ _SIGS = {
     "dr_ng_plan_destroy": (C.c_int, [P]),
     "dr_spmm_fwd_ng": (C.c_int, [P, C.POINTER(dr_cbsr), P, P]),
     "dr_spmm_bwd_ng": (C.c_int, [P, P, C.POINTER(dr_cbsr), P, P, P]),
+    "dr_shard_plan": (C.c_int, [C.POINTER(dr_rel_desc), C.c_int32, P, P]),
+    "dr_shard_create": (C.c_int, [C.POINTER(dr_rel_desc), C.c_int32, C.c_int32, P, P,
+                                  C.POINTER(dr_allocator), P, C.POINTER(P)]),
+    "dr_shard_destroy": (C.c_int, [P]),
+    "dr_shard_info": (C.c_int, [P, C.POINTER(dr_shard_info_t)]),
+    "dr_shard_allgather_cbsr": (C.c_int, [P, C.POINTER(dr_cbsr), C.POINTER(dr_cbsr), P, P]),
+    "dr_shard_spmm_fwd": (C.c_int, [P, C.POINTER(dr_cbsr), P, P]),
+    "dr_shard_spmm_bwd": (C.c_int, [P, P, C.POINTER(dr_cbsr), P, P]),
+    "dr_shard_reduce_scatter_g": (C.c_int, [P, P, C.POINTER(dr_cbsr), P, P, P, P]),
     "dr_heteroconv_tape_bytes": (C.c_int, [P, C.POINTER(dr_layer), C.c_uint32,
                                            C.POINTER(C.c_size_t)]),
     "dr_heteroconv_fwd": (C.c_int, [P, C.POINTER(dr_layer), P, P, P, P, P, C.c_uint32, P]),

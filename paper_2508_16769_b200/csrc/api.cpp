@@ -11,6 +11,7 @@
 
 #include <nvtx3/nvToolsExt.h>
 
+#include "nccl_api.h"
 #include "proj.h"
 #include "tc2.h"
 
@@ -559,19 +560,7 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
 }
 
 // ------------------------------------------------------------------ NCCL (loaded at run time)
-struct NcclApi {
-    bool ok = false;
-    std::string err;
-    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
-    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
-    ncclResult_t (*commCount)(const ncclComm_t, int *) = nullptr;
-    ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
-                              ncclComm_t, cudaStream_t) = nullptr;
-    const char *(*getErrorString)(ncclResult_t) = nullptr;
-};
-
-static NcclApi &nccl() {
+NcclApi &nccl() {
     static NcclApi api;
     static std::once_flag once;
     std::call_once(once, [] {
@@ -585,21 +574,21 @@ static NcclApi &nccl() {
         api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
         api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
         api.commCount = (decltype(api.commCount))dlsym(h, "ncclCommCount");
+        api.commUserRank = (decltype(api.commUserRank))dlsym(h, "ncclCommUserRank");
         api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+        api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+        api.reduceScatter = (decltype(api.reduceScatter))dlsym(h, "ncclReduceScatter");
+        api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
+        api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
         api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
         api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.commCount &&
-                 api.allReduce && api.getErrorString;
+                 api.commUserRank && api.allReduce && api.allGather && api.reduceScatter &&
+                 api.groupStart && api.groupEnd && api.getErrorString;
         if (!api.ok) api.err = "missing NCCL symbols";
     });
     if (!api.ok) fail(DR_ERR_NCCL, "cannot load NCCL: " + api.err);
     return api;
 }
-
-#define DR_NCCL(call)                                                                        \
-    do {                                                                                     \
-        ncclResult_t r_ = (call);                                                            \
-        if (r_ != ncclSuccess) fail(DR_ERR_NCCL, std::string(#call) + ": " + nccl().getErrorString(r_)); \
-    } while (0)
 
 }  // namespace dr
 

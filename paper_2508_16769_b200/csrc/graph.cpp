@@ -607,6 +607,78 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
     }
 }
 
+namespace dr {
+
+// One relation block with caller-given source normalisers (dr_shard, SURVEY §8
+// f4): rows = this rank's destinations, columns = the padded global source
+// space. build_rel's row normalisers c are already global (a row's edges are
+// all local); the column normalisers s are replaced by the global ones and
+// the forward edge weights recomputed from them. SIMT schedules only (no tiles).
+void build_rel_block(const dr_rel_desc &d, const std::vector<float> &s_glob, Alloc &alloc,
+                     cudaStream_t cs, RelDev &out, std::vector<void *> &blocks, size_t &bytes) {
+    HostRel h;
+    build_rel(d, true, h);
+    if (h.st != DR_OK) fail(h.st, "shard block: " + h.err);
+    DR_CHECK((int64_t)s_glob.size() == (int64_t)d.n_src, DR_ERR_SHAPE_MISMATCH,
+             "shard block: s size");
+    h.s = s_glob;
+    if (h.weighted || d.module != DR_SAGE_MEAN) {
+        h.ew.resize(d.nnz);
+        for (int64_t e = 0; e < d.nnz; ++e)
+            h.ew[e] = (d.val ? d.val[e] : 1.0f) * h.s[d.col_idx[e]];
+    }
+    const int wdeg = warp_row_threshold();
+    const std::vector<int64_t> noloc;
+    make_order(h.deg_in, false, noloc, wdeg, h.order, h.n_hub, h.n_warp);
+    make_order(h.deg_out, false, noloc, wdeg, h.orderT, h.n_hubT, h.n_warpT);
+    out = RelDev{};
+    out.n_dst = h.n_dst;
+    out.n_src = h.n_src;
+    out.nnz = h.nnz;
+    out.module = h.module;
+    out.fwd.n = h.n_dst;
+    out.fwd.n_hub = h.n_hub;
+    out.fwd.n_warp = h.n_warp;
+    out.bwd.n = h.n_src;
+    out.bwd.n_hub = h.n_hubT;
+    out.bwd.n_warp = h.n_warpT;
+    out.max_deg_dst = h.max_in;
+    out.max_deg_src = h.max_out;
+    struct Up {
+        void **dst;
+        const void *src;
+        size_t bytes, off;
+    };
+    std::vector<Up> ups;
+    size_t total = 0;
+    auto plan = [&](void **dst, const void *src, size_t b) {
+        *dst = nullptr;
+        if (b == 0) return;
+        ups.push_back({dst, src, b, total});
+        total += align_up(b);
+    };
+    plan((void **)&out.rowptr, h.rowptr.data(), h.rowptr.size() * 4);
+    plan((void **)&out.col, h.col.data(), h.col.size() * 4);
+    plan((void **)&out.ew, h.ew.data(), h.ew.size() * 4);
+    plan((void **)&out.c, h.c.data(), h.c.size() * 4);
+    plan((void **)&out.s, h.s.data(), h.s.size() * 4);
+    plan((void **)&out.fwd.order, h.order.data(), h.order.size() * 4);
+    plan((void **)&out.bwd.order, h.orderT.data(), h.orderT.size() * 4);
+    plan((void **)&out.ewT, h.ewT.data(), h.ewT.size() * 4);
+    plan((void **)&out.colptr, h.colptr.data(), h.colptr.size() * 4);
+    plan((void **)&out.row, h.row.data(), h.row.size() * 4);
+    char *base = (char *)alloc.get(total, cs);
+    blocks.push_back(base);
+    bytes += total;
+    for (Up &u : ups) {
+        *u.dst = base + u.off;
+        DR_CUDA(cudaMemcpyAsync(*u.dst, u.src, u.bytes, cudaMemcpyHostToDevice, cs));
+    }
+    DR_CUDA(cudaStreamSynchronize(cs));      // host vectors die with this frame
+}
+
+}  // namespace dr
+
 extern "C" dr_status dr_graph_destroy(dr_graph *g) {
     if (!g) return DR_OK;
     cudaStreamSynchronize(g->create_stream);

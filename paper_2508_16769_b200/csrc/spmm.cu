@@ -619,6 +619,30 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, c
     note_launch("spmm_bwd");
 }
 
+// one warp per row: zero the row, then drop the k values at their columns
+__global__ void cbsr_scatter_kernel(const float *__restrict__ g, const uint8_t *__restrict__ idx,
+                                    int64_t n, int k, int dim, float *__restrict__ dx) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
+        float *row = dx + r * dim;
+        for (int c = lane; c < dim; c += 32) row[c] = 0.f;
+        __syncwarp();
+        for (int t = lane; t < k; t += 32) row[__ldg(idx + r * k + t)] = __ldg(g + r * k + t);
+        __syncwarp();
+    }
+}
+
+void launch_cbsr_scatter(const float *g, const uint8_t *idx, int64_t n, int k, int dim, float *dx,
+                         cudaStream_t s) {
+    if (n <= 0) return;
+    ProfScope ps("cbsr_scatter", s);
+    int64_t blocks = (n + 7) / 8;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    cbsr_scatter_kernel<<<(unsigned)blocks, 256, 0, s>>>(g, idx, n, k, dim, dx);
+    note_launch("cbsr_scatter");
+}
+
 __global__ void ng_edge_k_kernel(const int32_t *__restrict__ row, const int32_t *__restrict__ rowptr,
                                  int64_t nnz, NgSched ng, uint8_t *__restrict__ kT) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
