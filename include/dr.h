@@ -311,6 +311,7 @@ typedef struct {
     int32_t world, rank, max_src;
     int64_t dst_begin, dst_end, src_begin, src_end, nnz_local;
     size_t device_bytes;
+    int32_t tiles, tiles_T;         /* tensor-core tiled SpMM tiles of the block (0 => SIMT) */
 } dr_shard_info_t;
 /* Default partition (host only, no GPU): dst_part [world+1] balances edges
  * (boundaries at the first row whose row_ptr reaches q * nnz / world);

@@ -73,7 +73,8 @@ class dr_ng_sched(C.Structure):
 class dr_shard_info_t(C.Structure):
     _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("max_src", C.c_int32),
                 ("dst_begin", C.c_int64), ("dst_end", C.c_int64), ("src_begin", C.c_int64),
-                ("src_end", C.c_int64), ("nnz_local", C.c_int64), ("device_bytes", C.c_size_t)]
+                ("src_end", C.c_int64), ("nnz_local", C.c_int64), ("device_bytes", C.c_size_t),
+                ("tiles", C.c_int32), ("tiles_T", C.c_int32)]
 
 
 class dr_profile_entry(C.Structure):

@@ -171,9 +171,12 @@ struct NgSched {
 // dx[i, :] = 0 except dx[i, idx[i, t]] = g[i, t] (the D-ReLU mask gradient scatter)
 void launch_cbsr_scatter(const float *g, const uint8_t *idx, int64_t n, int k, int dim, float *dx,
                          cudaStream_t s);
-// A relation block uploaded with caller-given column normalisers (graph.cpp; dr_shard)
-void build_rel_block(const dr_rel_desc &d, const std::vector<float> &s_glob, Alloc &alloc,
-                     cudaStream_t cs, RelDev &out, std::vector<void *> &blocks, size_t &bytes);
+// A relation block uploaded with caller-given column normalisers (graph.cpp; dr_shard).
+// own_col0: the block's columns [own_col0, own_col0 + n_dst) are its own rows
+// (square relation, same source and destination partition), else -1.
+void build_rel_block(const dr_rel_desc &d, const std::vector<float> &s_glob, int64_t own_col0,
+                     Alloc &alloc, cudaStream_t cs, RelDev &out, std::vector<void *> &blocks,
+                     size_t &bytes);
 void launch_ng_edge_k(const RelDev &r, const NgSched &ng, uint8_t *kT, cudaStream_t s);
 
 // DR-SpMM forward of one relation: z [n_dst x dim] = diag(c) A diag(s) densify(H).

@@ -121,13 +121,23 @@ struct HostTiles {
     int64_t n_chunks = 0;
 };
 
-// Tiles of <= 128 rows of a square relation (rp, col over n rows), grown as BFS
-// balls over the relation from the lowest-ranked unassigned row (rank = the
-// locality order), so a tile is a compact neighbourhood and its halo small;
-// then per tile the sorted distinct column ids (the halo, padded to 64-id
-// chunks with -1) and, per chunk, its edges as (m << 6 | u).
+// Tiles of <= 128 rows of a relation (rp, col over n rows), grown as BFS balls
+// over the relation from the lowest-ranked unassigned row (rank = the locality
+// order), so a tile is a compact neighbourhood and its halo small; then per
+// tile the sorted distinct column ids (the halo, padded to 64-id chunks with
+// -1) and, per chunk, its edges as (m << 6 | u). Column c is row c + row_off
+// for the BFS when that is in [0, n) (square relation: row_off = 0; a
+// dr_shard block: its own rank's columns), else a leaf. pack: a ball that
+// stops growing is topped up with the next unassigned rows in rank order (a
+// shard block's many edge-free padded rows then share tiles).
 void build_tiles(int32_t n, const std::vector<int32_t> &rp, const std::vector<int32_t> &col,
-                 const std::vector<int64_t> &rank, HostTiles &T) {
+                 const std::vector<int64_t> &rank, HostTiles &T, int64_t n_cols = -1,
+                 int64_t row_off = 0, bool pack = false) {
+    if (n_cols < 0) n_cols = n;
+    auto row_of = [&](int32_t c) -> int32_t {
+        const int64_t v = (int64_t)c + row_off;
+        return (v >= 0 && v < n) ? (int32_t)v : -1;
+    };
     std::vector<int32_t> seq((size_t)n);
     if (rank.empty()) std::iota(seq.begin(), seq.end(), 0);
     else
@@ -135,7 +145,7 @@ void build_tiles(int32_t n, const std::vector<int32_t> &rp, const std::vector<in
     std::vector<char> assigned((size_t)n, 0);
     std::vector<int32_t> queue;
     queue.reserve(kTsRows * 8);
-    std::vector<int32_t> local((size_t)n, -1);
+    std::vector<int32_t> local((size_t)n_cols, -1);
     std::vector<int32_t> tile, hl;
     T.chunk_beg.push_back(0);
     size_t pos = 0;
@@ -155,21 +165,29 @@ void build_tiles(int32_t n, const std::vector<int32_t> &rp, const std::vector<in
         for (size_t qh = 0; qh < queue.size() && (int)tile.size() < kTsRows; ++qh) {
             const int32_t u = queue[qh];
             for (int32_t e = rp[u]; e < rp[u + 1] && (int)tile.size() < kTsRows; ++e) {
-                const int32_t v = col[e];
-                if (!assigned[v]) {
+                const int32_t v = row_of(col[e]);
+                if (v >= 0 && !assigned[v]) {
                     assigned[v] = 1;
                     tile.push_back(v);
                     queue.push_back(v);
                 }
             }
         }
+        if (pack)
+            while ((int)tile.size() < kTsRows) {
+                while (pos < (size_t)n && assigned[seq[pos]]) ++pos;
+                if (pos >= (size_t)n) break;
+                assigned[seq[pos]] = 1;
+                tile.push_back(seq[pos]);
+            }
         // next tile grows from the lowest-ranked unassigned neighbour of this one, so
         // consecutive tiles (one CTA's run) are adjacent and share halo rows in L2
         next_seed = -1;
         int64_t best = INT64_MAX;
         for (int32_t i : tile)
             for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
-                const int32_t v = col[e];
+                const int32_t v = row_of(col[e]);
+                if (v < 0) continue;
                 const int64_t r = rank.empty() ? (int64_t)v : rank[v];
                 if (!assigned[v] && r < best) {
                     best = r;
@@ -614,8 +632,9 @@ namespace dr {
 // space. build_rel's row normalisers c are already global (a row's edges are
 // all local); the column normalisers s are replaced by the global ones and
 // the forward edge weights recomputed from them. SIMT schedules only (no tiles).
-void build_rel_block(const dr_rel_desc &d, const std::vector<float> &s_glob, Alloc &alloc,
-                     cudaStream_t cs, RelDev &out, std::vector<void *> &blocks, size_t &bytes) {
+void build_rel_block(const dr_rel_desc &d, const std::vector<float> &s_glob, int64_t own_col0,
+                     Alloc &alloc, cudaStream_t cs, RelDev &out, std::vector<void *> &blocks,
+                     size_t &bytes) {
     HostRel h;
     build_rel(d, true, h);
     if (h.st != DR_OK) fail(h.st, "shard block: " + h.err);
@@ -631,6 +650,30 @@ void build_rel_block(const dr_rel_desc &d, const std::vector<float> &s_glob, All
     const std::vector<int64_t> noloc;
     make_order(h.deg_in, false, noloc, wdeg, h.order, h.n_hub, h.n_warp);
     make_order(h.deg_out, false, noloc, wdeg, h.orderT, h.n_hubT, h.n_warpT);
+    // tiles for the tensor-core SpMM, opt-in (DR_SHARD_TILES=1), under the rule of
+    // dr_graph_create (unit weights, mean degree >= 8); the BFS links column c to
+    // local row c - own_col0 (own_col0 < 0: no column is a local row). Measured at
+    // C4 near (profiles/r01/shard_time_*.json): the block's tiled forward is at best
+    // 10 % faster than the SIMT one (W = 2, shuffled ids) and slower with spatial
+    // ids, so the SIMT kernels are the default for blocks.
+    HostTiles tl, tlT;
+    const char *tenv = getenv("DR_SHARD_TILES");
+    const bool want_tiles = tenv && atoi(tenv) == 1 && h.ew.empty() && h.ewT.empty() &&
+                            h.n_dst > 0 && h.nnz >= 8LL * h.n_dst;
+    if (want_tiles) {
+        const int64_t off = own_col0 >= 0 ? -own_col0 : -(int64_t)h.n_src - h.n_dst - 1;
+        const int64_t offT = own_col0 >= 0 ? own_col0 : -(int64_t)h.n_src - h.n_dst - 1;
+        build_tiles(h.n_dst, h.rowptr, h.col, noloc, tl, h.n_src, off, true);
+        // a block only tiles well when its row range is spatially compact (node ids
+        // in a locality order): with < 4 edges per halo slot the tiles re-gather
+        // almost every neighbour row per tile and the SIMT kernel is faster
+        if (tl.n_chunks * (int64_t)kTsChunk * 4 > h.nnz) tl = HostTiles{};
+        // the transposed tiles would span every padded source row, most of them
+        // edge-free or remote with a few boundary edges (measured 2-3x slower than
+        // the SIMT SSpMM at C4, W = 2..8): DR_SHARD_TILES_T=1 builds them anyway
+        const char *te = getenv("DR_SHARD_TILES_T");
+        if (te && atoi(te) == 1) build_tiles(h.n_src, h.colptr, h.row, noloc, tlT, h.n_dst, offT, true);
+    }
     out = RelDev{};
     out.n_dst = h.n_dst;
     out.n_src = h.n_src;
@@ -667,6 +710,21 @@ void build_rel_block(const dr_rel_desc &d, const std::vector<float> &s_glob, All
     plan((void **)&out.ewT, h.ewT.data(), h.ewT.size() * 4);
     plan((void **)&out.colptr, h.colptr.data(), h.colptr.size() * 4);
     plan((void **)&out.row, h.row.data(), h.row.size() * 4);
+    auto plan_tiles = [&](TileSet &ts, HostTiles &ht) {
+        ts.n_tiles = ht.n_tiles;
+        ts.n_chunks = ht.n_chunks;
+        ts.grid = ht.grid;
+        ts.tile_stride = ht.tile_stride;
+        plan((void **)&ts.rows, ht.rows.data(), ht.rows.size() * 4);
+        plan((void **)&ts.chunk_beg, ht.chunk_beg.data(), ht.chunk_beg.size() * 4);
+        plan((void **)&ts.halo, ht.halo.data(), ht.halo.size() * 4);
+        plan((void **)&ts.abits, ht.abits.data(), ht.abits.size() * 8);
+        plan((void **)&ts.cta_beg, ht.cta_beg.data(), ht.cta_beg.size() * 4);
+        plan((void **)&ts.cta_chunks, ht.cta_chunks.data(), ht.cta_chunks.size() * 4);
+        plan((void **)&ts.cta_tiles, ht.cta_tiles.data(), ht.cta_tiles.size() * 4);
+    };
+    if (tl.n_tiles) plan_tiles(out.tiles, tl);
+    if (tlT.n_tiles) plan_tiles(out.tilesT, tlT);
     char *base = (char *)alloc.get(total, cs);
     blocks.push_back(base);
     bytes += total;

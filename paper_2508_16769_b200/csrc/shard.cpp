@@ -192,7 +192,11 @@ dr_status dr_shard_create(const dr_rel_desc *rel, int32_t world, int32_t rank,
         s->alloc.a = *a;
         s->alloc.custom = true;
     }
-    build_rel_block(ld, s_pad, s->alloc, s->stream, s->rel, s->blocks, s->bytes);
+    // square relation with the same source and destination ranges: the local
+    // rows are the padded columns [rank * max_src, rank * max_src + rows)
+    const bool own = rel->n_dst == rel->n_src && dp == sp;
+    build_rel_block(ld, s_pad, own ? (int64_t)rank * max_src : -1, s->alloc, s->stream, s->rel,
+                    s->blocks, s->bytes);
     *out = s.release();
     SH_END
 }
@@ -218,6 +222,8 @@ dr_status dr_shard_info(const dr_shard *s, dr_shard_info_t *info) {
     info->src_end = s->src_end;
     info->nnz_local = s->rel.nnz;
     info->device_bytes = s->bytes;
+    info->tiles = s->rel.tiles.n_tiles;
+    info->tiles_T = s->rel.tilesT.n_tiles;
     SH_END
 }
 

@@ -67,6 +67,22 @@ def test_shard_virtual_ranks_parity(designs, name, D, k, world):
         assert row_err(to_np(g), ref) <= TOL, rel
 
 
+def test_shard_near_blocks_tiled_optin(monkeypatch):
+    """DR_SHARD_TILES=1 (opt-in): with node ids in a locality order, near's blocks
+    (unit weights, dense neighbourhoods) run the tensor-core tiled forward, with
+    the same parity; the SSpMM stays SIMT unless DR_SHARD_TILES_T=1."""
+    monkeypatch.setenv("DR_SHARD_TILES", "1")
+    d = make_config("C2", scale=0.1, order="spatial")
+    for world in (1, 2, 4):
+        for q in range(world):
+            i = dr.Shard.from_design(d, "near", world, q).info()
+            assert i["tiles"] > 0, (world, q)
+        ptr, col, nd, ns, z, g, val, idx, dZ, _ = _virtual(d, "near", world, 64, 8, world)
+        c, s = O.normalisers(ptr, col, nd, ns, MOD["near"])
+        oi, ov = to_np(idx).astype(np.int32), to_np(val).astype(np.float64)
+        assert row_err(to_np(z), O.spmm_fwd(ptr, col, nd, c, s, oi, ov, 64)) <= TOL
+
+
 def test_shard_world1_equals_single_graph(designs):
     """One rank: bit-identical to dr_spmm_fwd / dr_spmm_bwd on the SIMT path."""
     d = designs["C2s"]
