@@ -1,5 +1,5 @@
 # C2 step vs the tiled SpMM's stage count (DR_TS_MAXSA): shared-memory footprint
-# against cross-stream concurrency.
+# against cross-stream concurrency. (The DR_TS_MAXSA knob this needs was an experiment, since removed; results in profiles/r01/ab_tspmm_pipeline.txt.)
 mkdir -p gpurun_out
 for r in 1 2; do for SA in 4 3; do   # SA = 2 deadlocks (launch() now rejects it)
 DR_TS_MAXSA=$SA timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
