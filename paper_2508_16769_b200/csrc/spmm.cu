@@ -565,7 +565,8 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, c
     }
     const int P = choose_P_bwd(k);
     DR_CHECK(P > 0, DR_ERR_BAD_K, "spmm_bwd: unsupported k");
-    DR_CHECK(!ng.on || (ng.kT && !t1.rel), DR_ERR_INVALID_ARGUMENT, "spmm_bwd: NEXT-2 needs kT, one term");
+    DR_CHECK(!ng.on || ((ng.kT || !t0.rel || t0.rel->nnz == 0) && !t1.rel), DR_ERR_INVALID_ARGUMENT,
+             "spmm_bwd: NEXT-2 needs kT (relation with edges), one term");
     BwdArgs a{};
     a.order = sched.order;
     a.L = k / P;

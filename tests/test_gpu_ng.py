@@ -160,3 +160,22 @@ def test_spmm_ng_k_below_plan(designs):
     with pytest.raises(dr.DRError) as e:
         dr.spmm_fwd_ng(plan, val, idx, 16)
     assert e.value.status == 2
+
+
+def test_ng_edge_cases():
+    """Empty relations, zero rows and isolated destinations: exact zeros, no errors."""
+    n_cell, n_net = 10, 5
+    empty = (np.zeros(n_cell + 1, np.int64), np.zeros(0, np.int32))
+    rels = {"near": empty, "pins": (np.zeros(n_net + 1, np.int64), np.zeros(0, np.int32)),
+            "pinned": empty}
+    g = dr.Graph(n_cell, n_net, rels)
+    x = torch.randn(n_cell, 16, device="cuda")
+    val, idx = dr.drelu_topk_sorted(x, 4)
+    plan = dr.NgPlan(g, "near", (2, 4), (4, 2, 1))
+    z = dr.spmm_fwd_ng(plan, val, idx, 16)
+    assert torch.count_nonzero(z) == 0
+    gk, dx = dr.spmm_bwd_ng(plan, torch.randn(n_cell, 16, device="cuda"), val, idx, 16,
+                            want_dx=True)
+    assert torch.count_nonzero(gk) == 0 and torch.count_nonzero(dx) == 0
+    v0, i0 = dr.drelu_topk_sorted(torch.empty(0, 16, device="cuda"), 4)
+    assert v0.shape == (0, 4)

@@ -126,3 +126,16 @@ def test_shard_bad_partition(designs):
         dr.Shard(ptr, col, ns, 2, 0, dst_part=[0, nd + 1, nd])
     with pytest.raises(dr.DRError):
         dr.Shard(ptr, col, ns, 2, 2)
+
+
+def test_shard_more_ranks_than_rows():
+    """world larger than the row count: empty ranks own no rows; the union is still exact."""
+    d = make_config("C1")                        # 64 cells, 32 nets
+    for rel in ("pins", "pinned"):
+        ptr, col, nd, ns, z, g, val, idx, dZ, shards = _virtual(d, rel, 48, 16, 4, 3)
+        assert any(sh.dst_end == sh.dst_begin for sh in shards)
+        c, s = O.normalisers(ptr, col, nd, ns, MOD[rel])
+        oi, ov = to_np(idx).astype(np.int32), to_np(val).astype(np.float64)
+        assert row_err(to_np(z), O.spmm_fwd(ptr, col, nd, c, s, oi, ov, 16)) <= TOL
+        ref = O.spmm_bwd(ptr, col, nd, ns, c, s, oi, to_np(dZ).astype(np.float64))
+        assert row_err(to_np(g), ref) <= TOL
