@@ -167,3 +167,26 @@ def test_train_step_per_edge_k_parity():
         ref = og[key] if og[key].ndim == 2 else og[key].reshape(1, -1)
         got = gg[key] if gg[key].ndim == 2 else gg[key].reshape(1, -1)
         assert row_err(got, ref) <= TOL, key
+
+
+def test_per_edge_k_no_nets():
+    """A design whose pins / pinned relations are empty: the k_pins path still runs
+    (pins' D-ReLU, an all-zero pins term) and matches the per-node-type layer."""
+    d = make_config("C1")
+    n_cell, n_net = d.n_cell, 1
+    rels = {"near": d.rel("near")[:2], "pins": (np.zeros(n_net + 1, np.int64), np.zeros(0, np.int32)),
+            "pinned": (np.zeros(n_cell + 1, np.int64), np.zeros(0, np.int32))}
+    g = dr.Graph(n_cell, n_net, rels)
+    P = make_params(16, 16, 16, 1, seed=4)
+    xc = torch.randn(n_cell, 16, device="cuda")
+    xn = torch.randn(n_net, 16, device="cuda")
+    dyc = torch.randn(n_cell, 16, device="cuda")
+    dyn = torch.randn(n_net, 16, device="cuda")
+    outs = []
+    for kp in (0, 8):
+        L, _ = _layer(P, 16, 16, 16, 4, 4, kp)
+        yc, yn, tape = dr.heteroconv_fwd(g, L, xc, xn)
+        gr, dxc, dxn = dr.heteroconv_bwd(g, L, tape, dyc, dyn)
+        outs.append((yc, yn, dxc, dxn))
+    for a, b in zip(*outs):
+        assert torch.allclose(a, b, rtol=0, atol=0)

@@ -139,3 +139,18 @@ def test_shard_more_ranks_than_rows():
         assert row_err(to_np(z), O.spmm_fwd(ptr, col, nd, c, s, oi, ov, 16)) <= TOL
         ref = O.spmm_bwd(ptr, col, nd, ns, c, s, oi, to_np(dZ).astype(np.float64))
         assert row_err(to_np(g), ref) <= TOL
+
+
+def test_shard_empty_relation():
+    ptr, col = np.zeros(11, np.int64), np.zeros(0, np.int32)
+    for world in (1, 2):
+        shards = [dr.Shard(ptr, col, 7, world, q) for q in range(world)]
+        m = shards[0].max_src
+        va = torch.randn(world * m, 4, device="cuda")
+        ia = torch.zeros(world * m, 4, device="cuda", dtype=torch.uint8)
+        ia[:] = torch.arange(4, dtype=torch.uint8, device="cuda")
+        for sh in shards:
+            z = sh.spmm_fwd(va, ia, 16)
+            assert z.shape[0] == sh.dst_end - sh.dst_begin and torch.count_nonzero(z) == 0
+            gp = sh.spmm_bwd(torch.randn(sh.dst_end - sh.dst_begin, 16, device="cuda"), va, ia, 16)
+            assert torch.count_nonzero(gp) == 0
