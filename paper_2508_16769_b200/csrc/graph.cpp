@@ -233,6 +233,8 @@ void build_tiles(int32_t n, const std::vector<int32_t> &rp, const std::vector<in
     T.cta_beg.assign((size_t)T.grid + 1, 0);
     T.cta_chunks.clear();
     T.cta_chunks.reserve((size_t)T.n_chunks);
+    const char *tw = getenv("DR_TS_TILE_W");
+    const int64_t tile_w = tw ? atoi(tw) : 0;
     const char *ord = getenv("DR_TS_ORDER");
     const bool rr = ord && std::string(ord) == "rr";
     int32_t t0 = 0;
@@ -245,9 +247,11 @@ void build_tiles(int32_t n, const std::vector<int32_t> &rp, const std::vector<in
             T.cta_tiles.push_back(b);
             T.cta_tiles.push_back(cnt);
         } else {
-            const int64_t c1 = T.n_chunks * (b + 1) / T.grid;
+            // balanced by cost = chunks + W per tile (the per-tile epilogue and
+            // accumulator hand-off, in chunk units; DR_TS_TILE_W, default below)
+            const int64_t c1 = (T.n_chunks + tile_w * (int64_t)T.n_tiles) * (b + 1) / T.grid;
             int32_t t1 = t0;
-            while (t1 < T.n_tiles && (b == T.grid - 1 || T.chunk_beg[t1] < c1)) ++t1;
+            while (t1 < T.n_tiles && (b == T.grid - 1 || T.chunk_beg[t1] + tile_w * (int64_t)t1 < c1)) ++t1;
             for (int32_t c = T.chunk_beg[t0]; c < T.chunk_beg[t1]; ++c) T.cta_chunks.push_back(c);
             T.cta_tiles.push_back(t0);
             T.cta_tiles.push_back(t1 - t0);
