@@ -121,6 +121,9 @@ struct HostTiles {
     int64_t n_chunks = 0;
 };
 
+struct HostTiles;
+void split_ctas(HostTiles &T, int64_t tile_w);
+
 // Tiles of <= 128 rows of a relation (rp, col over n rows), grown as BFS balls
 // over the relation from the lowest-ranked unassigned row (rank = the locality
 // order), so a tile is a compact neighbourhood and its halo small; then per
@@ -224,17 +227,24 @@ void build_tiles(int32_t n, const std::vector<int32_t> &rp, const std::vector<in
         T.chunk_beg.push_back((int32_t)T.n_chunks);
         ++T.n_tiles;
     }
-    // persistent-kernel work split: CTA b takes a contiguous run of tiles (the
-    // ones whose first chunk lies in [b C / grid, (b+1) C / grid): balanced by
-    // chunk count, every chunk costs the same) -- neighbouring balls share halo
-    // rows, which the CTA then re-reads from L2 (measured better than
-    // round-robin, DR_TS_ORDER=rr); its chunks are cta_chunks[cta_beg[b], cta_beg[b+1])
+    split_ctas(T, -1);
+}
+
+// Persistent-kernel work split of a TileSet: CTA b takes a contiguous run of tiles
+// balanced by cost = chunks + tile_w per tile (tile_w < 0: DR_TS_TILE_W, else 0)
+// -- neighbouring balls share halo rows, which the CTA then re-reads from L2
+// (measured better than round-robin, DR_TS_ORDER=rr); its chunks are
+// cta_chunks[cta_beg[b], cta_beg[b+1]).
+void split_ctas(HostTiles &T, int64_t tile_w) {
+    if (tile_w < 0) {
+        const char *tw = getenv("DR_TS_TILE_W");
+        tile_w = tw ? atoi(tw) : 0;
+    }
     T.grid = std::min<int32_t>(T.n_tiles, 148);
     T.cta_beg.assign((size_t)T.grid + 1, 0);
     T.cta_chunks.clear();
+    T.cta_tiles.clear();
     T.cta_chunks.reserve((size_t)T.n_chunks);
-    const char *tw = getenv("DR_TS_TILE_W");
-    const int64_t tile_w = tw ? atoi(tw) : 0;
     const char *ord = getenv("DR_TS_ORDER");
     const bool rr = ord && std::string(ord) == "rr";
     int32_t t0 = 0;
@@ -247,8 +257,6 @@ void build_tiles(int32_t n, const std::vector<int32_t> &rp, const std::vector<in
             T.cta_tiles.push_back(b);
             T.cta_tiles.push_back(cnt);
         } else {
-            // balanced by cost = chunks + W per tile (the per-tile epilogue and
-            // accumulator hand-off, in chunk units; DR_TS_TILE_W, default below)
             const int64_t c1 = (T.n_chunks + tile_w * (int64_t)T.n_tiles) * (b + 1) / T.grid;
             int32_t t1 = t0;
             while (t1 < T.n_tiles && (b == T.grid - 1 || T.chunk_beg[t1] + tile_w * (int64_t)t1 < c1)) ++t1;
@@ -464,10 +472,23 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
         const bool want_tiles = !identity && !(tenv && atoi(tenv) == 0) && hn.ew.empty() &&
                                 hn.ewT.empty() && hn.n_dst > 0 && hn.nnz >= 8LL * hn.n_dst;
         std::thread tile_th;
+        // symmetric near: one TileSet for both directions, but the backward gets
+        // its own CTA split with per-tile weight 2 (its epilogue samples and
+        // writes dense dX rows: measured C4 backward -10 %, forward best at 0 --
+        // profiles/r01/ab_tile_weight.txt); DR_TS_TILE_W_BWD overrides
+        HostTiles tlB;
         if (want_tiles)
             tile_th = std::thread([&] {
                 build_tiles(hn.n_dst, hn.rowptr, hn.col, rank_c, tl);
-                if (!near_sym) build_tiles(hn.n_src, hn.colptr, hn.row, rank_c, tlT);
+                if (!near_sym) {
+                    build_tiles(hn.n_src, hn.colptr, hn.row, rank_c, tlT);
+                } else {
+                    tlB.n_tiles = tl.n_tiles;
+                    tlB.n_chunks = tl.n_chunks;
+                    tlB.chunk_beg = tl.chunk_beg;
+                    const char *e = getenv("DR_TS_TILE_W_BWD");
+                    split_ctas(tlB, e ? atoi(e) : 2);
+                }
             });
         {
             const std::vector<int64_t> *dst_loc[3] = {&rank_c, &rank_n, &rank_c};
@@ -558,9 +579,18 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
             plan(0, (void **)&ts.cta_tiles, ht.cta_tiles.data(), ht.cta_tiles.size() * 4);
             ts.tile_stride = ht.tile_stride;
         };
+        TileSet bsplit;                     // symmetric near: the backward's CTA split
         if (want_tiles) {
             plan_tiles(g->rel[DR_NEAR].tiles, tl);
-            if (!near_sym) plan_tiles(g->rel[DR_NEAR].tilesT, tlT);
+            if (!near_sym) {
+                plan_tiles(g->rel[DR_NEAR].tilesT, tlT);
+            } else {
+                bsplit.grid = tlB.grid;
+                bsplit.tile_stride = tlB.tile_stride;
+                plan(0, (void **)&bsplit.cta_beg, tlB.cta_beg.data(), tlB.cta_beg.size() * 4);
+                plan(0, (void **)&bsplit.cta_chunks, tlB.cta_chunks.data(), tlB.cta_chunks.size() * 4);
+                plan(0, (void **)&bsplit.cta_tiles, tlB.cta_tiles.data(), tlB.cta_tiles.size() * 4);
+            }
         }
         g->src_cell.n = n_cell;
         g->src_cell.n_hub = hub_c;
@@ -581,7 +611,15 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
             }
         // structural sharing (no second copy): CSC(near) = CSR(near) when symmetric;
         // CSC(pins) = CSR(pinned) and CSC(pinned) = CSR(pins) when pinned == pins^T.
-        if (want_tiles && near_sym) g->rel[DR_NEAR].tilesT = g->rel[DR_NEAR].tiles;
+        if (want_tiles && near_sym) {
+            TileSet &tt = g->rel[DR_NEAR].tilesT;
+            tt = g->rel[DR_NEAR].tiles;
+            tt.grid = bsplit.grid;
+            tt.tile_stride = bsplit.tile_stride;
+            tt.cta_beg = bsplit.cta_beg;
+            tt.cta_chunks = bsplit.cta_chunks;
+            tt.cta_tiles = bsplit.cta_tiles;
+        }
         if (near_sym) {
             g->rel[DR_NEAR].colptr = g->rel[DR_NEAR].rowptr;
             g->rel[DR_NEAR].row = g->rel[DR_NEAR].col;
