@@ -1,4 +1,4 @@
-# SIMT forward sub-row CTAs: one per 8 R rows (DR_SUB_CTAS=0) vs a capped, grid-striding grid
+# SIMT forward sub-row CTAs A/B (the DR_SUB_CTAS knob was an experiment, since removed; results in profiles/r01/ab_sub_ctas.txt)
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_ng.py -x -q -k "spmm or heteroconv or ng" > gpurun_out/t.log 2>&1; tail -1 gpurun_out/t.log
 for C in 0 1184 592 2368 0 1184; do
