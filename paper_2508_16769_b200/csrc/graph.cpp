@@ -236,9 +236,9 @@ void build_tiles(int32_t n, const std::vector<int32_t> &rp, const std::vector<in
 // (measured better than round-robin, DR_TS_ORDER=rr); its chunks are
 // cta_chunks[cta_beg[b], cta_beg[b+1]).
 void split_ctas(HostTiles &T, int64_t tile_w) {
-    if (tile_w < 0) {
+    if (tile_w < 0) {                 // forward: weight 1 once CTAs own many tiles
         const char *tw = getenv("DR_TS_TILE_W");
-        tile_w = tw ? atoi(tw) : 0;
+        tile_w = tw ? atoi(tw) : (T.n_tiles >= 16 * 148 ? 1 : 0);
     }
     T.grid = std::min<int32_t>(T.n_tiles, 148);
     T.cta_beg.assign((size_t)T.grid + 1, 0);
@@ -473,9 +473,10 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
                                 hn.ewT.empty() && hn.n_dst > 0 && hn.nnz >= 8LL * hn.n_dst;
         std::thread tile_th;
         // symmetric near: one TileSet for both directions, but the backward gets
-        // its own CTA split with per-tile weight 2 (its epilogue samples and
-        // writes dense dX rows: measured C4 backward -10 %, forward best at 0 --
-        // profiles/r01/ab_tile_weight.txt); DR_TS_TILE_W_BWD overrides
+        // its own CTA split. Per-tile weights (in chunk units) once CTAs own >= 16
+        // tiles: forward 1, backward 2 (its epilogue samples and writes dense dX
+        // rows); with a few tiles per CTA (C2) 0 is best for both -- measured,
+        // profiles/r01/ab_tile_weight.txt; DR_TS_TILE_W(_BWD) override
         HostTiles tlB;
         if (want_tiles)
             tile_th = std::thread([&] {
@@ -487,7 +488,7 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
                     tlB.n_chunks = tl.n_chunks;
                     tlB.chunk_beg = tl.chunk_beg;
                     const char *e = getenv("DR_TS_TILE_W_BWD");
-                    split_ctas(tlB, e ? atoi(e) : 2);
+                    split_ctas(tlB, e ? atoi(e) : (tl.n_tiles >= 16 * 148 ? 2 : 0));
                 }
             });
         {
