@@ -123,10 +123,14 @@ def _near_graph(rng, pos, mean_deg, cap):
     tree = cKDTree(pos)
     m = min(n, 6000)
     sample = pos[rng.choice(n, size=m, replace=False)]
+    # distances of each sample point to its cap+1 nearest (itself first): the
+    # number within r, capped at cap, is #(dist <= r) - 1 -- one kNN query
+    # instead of a ball query per bisection step
+    kq = int(min(n, cap + 1))
+    dist = np.asarray(tree.query(sample, k=kq, workers=-1)[0]).reshape(m, kq)
 
     def est(r):
-        cnt = tree.query_ball_point(sample, r, return_length=True) - 1
-        return float(np.mean(np.minimum(cnt, cap)))
+        return float(np.mean(np.count_nonzero(dist <= r, axis=1) - 1))
 
     lo, hi = 0.0, 2.0 * np.sqrt(max(mean_deg, 1.0) / np.pi) + 2.0
     while est(hi) < mean_deg and hi < 4 * np.sqrt(n):
@@ -308,24 +312,64 @@ def make_config(name, order="shuffled", scale=1.0, seed=None, D=None):
     return d
 
 
-def make_c5_set(n_designs=100, seed0=5000, D=64, graphs_lo=2, graphs_hi=4):
-    """Mini-CircuitNet-shaped DP set (SURVEY §8.0 C5): designs of 2-4 graphs,
-    each graph 7.3k-9.8k cells with Table-1 ranges for the other statistics.
-    Returns a list of designs, each a list of Design graphs."""
-    out = []
+def _c5_graph(args):
+    i, g, seed0, D, n_cell, ratio, near_mean, pins_mean = args
+    return make_design(f"C5.{i}.{g}", n_cell, seed0 * 100 + i * 10 + g, d_cell=D, d_net=D,
+                       near_mean=near_mean, near_cap=256, net_ratio=ratio,
+                       pins_mean=pins_mean, pins_dmax=500)
+
+
+def c5_specs(n_designs=100, seed0=5000, D=64, graphs_lo=2, graphs_hi=4):
+    """Per-design graph parameters of the C5 set (drawn from per-design seeded
+    streams, no graph built): a list over designs of lists of job tuples
+    (i, g, seed0, D, n_cell, net_ratio, near_mean, pins_mean)."""
+    specs = []
     for i in range(n_designs):
         rng = np.random.Generator(np.random.PCG64(seed0 + i))
         n_graphs = int(rng.integers(graphs_lo, graphs_hi + 1))
-        graphs = []
+        jobs = []
         for g in range(n_graphs):
             n_cell = int(rng.integers(7300, 9800))
             ratio = float(rng.uniform(0.45, 0.95))
-            graphs.append(make_design(
-                f"C5.{i}.{g}", n_cell, seed0 * 100 + i * 10 + g, d_cell=D, d_net=D,
-                near_mean=float(rng.uniform(38, 52)), near_cap=256, net_ratio=ratio,
-                pins_mean=float(rng.uniform(2.2, 3.8)), pins_dmax=500))
-        out.append(graphs)
-    return out
+            near_mean = float(rng.uniform(38, 52))
+            pins_mean = float(rng.uniform(2.2, 3.8))
+            jobs.append((i, g, seed0, D, n_cell, ratio, near_mean, pins_mean))
+        specs.append(jobs)
+    return specs
+
+
+def c5_expected_nnz(jobs):
+    """Expected edge count of one C5 design from its specs (near + pins + pinned),
+    for packing designs onto ranks before they are generated."""
+    return float(sum(n * nm + 2.0 * n * r * pm for (_, _, _, _, n, r, nm, pm) in jobs))
+
+
+def make_c5_set(n_designs=100, seed0=5000, D=64, graphs_lo=2, graphs_hi=4, workers=None,
+                only=None):
+    """Mini-CircuitNet-shaped DP set (SURVEY §8.0 C5): designs of 2-4 graphs,
+    each graph 7.3k-9.8k cells with Table-1 ranges for the other statistics.
+    Returns a list of designs, each a list of Design graphs (with `only`, an
+    iterable of design ids, a dict id -> graphs of just those designs). The
+    per-graph draws come from per-design seeded streams, so `workers`
+    (processes; None = all cores, 1 = serial) and `only` do not change a
+    design."""
+    specs = c5_specs(n_designs, seed0, D, graphs_lo, graphs_hi)
+    ids = list(range(n_designs)) if only is None else sorted(set(int(i) for i in only))
+    jobs = [j for i in ids for j in specs[i]]
+    import os
+    nw = workers if workers is not None else min(len(jobs), os.cpu_count() or 1, 32)
+    if nw > 1 and len(jobs) > 1:
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+        with ProcessPoolExecutor(nw, mp_context=mp.get_context("fork")) as ex:
+            graphs = list(ex.map(_c5_graph, jobs, chunksize=max(1, len(jobs) // (4 * nw))))
+    else:
+        graphs = [_c5_graph(j) for j in jobs]
+    out, q = {}, 0
+    for i in ids:
+        out[i] = graphs[q:q + len(specs[i])]
+        q += len(specs[i])
+    return [out[i] for i in ids] if only is None else out
 
 
 def make_params(d_cell, d_net, d_hidden, n_layers, seed=7):

@@ -79,6 +79,24 @@ typedef struct {
     const int32_t *col_idx;   /* HOST [nnz], strictly increasing within a row, < n_src   */
     const float *val;         /* HOST [nnz] edge weights a_ij > 0; NULL => all 1 */
     dr_module module;
+    /* Optional HOST inputs, each NULL => built / counted by the library:
+     *  col_ptr [n_src+1], row_idx [nnz]: the CSC = CSR(A^T) of Alg. 2 stage 1
+     *      ("Transpose A to CSC"), rows ascending within a column. Checked
+     *      to equal the transpose of the CSR (DR_ERR_TRANSPOSE_MISMATCH) unless
+     *      DR_GRAPH_SKIP_VALIDATION, in which case it is used as given.
+     *  tval [nnz]: a_ij in CSC order (only with col_ptr; NULL => val transposed);
+     *      checked against val like col_ptr / row_idx.
+     *  deg_dst [n_dst], deg_src [n_src]: the degrees the normalisers use (e.g.
+     *      those of a larger graph this one is a part of); >= 0, clamped to >= 1
+     *      (Q12). The degree classes of the schedules always use the CSR's own
+     *      counts.
+     *  norm_dst [n_dst], norm_src [n_src]: c_i and s_j themselves (finite),
+     *      overriding module + degrees for the SpMM and SSpMM of this relation. */
+    const int64_t *col_ptr;
+    const int32_t *row_idx;
+    const float *tval;
+    const int32_t *deg_dst, *deg_src;
+    const float *norm_dst, *norm_src;
 } dr_rel_desc;
 
 typedef struct {
@@ -351,8 +369,9 @@ dr_status dr_shard_reduce_scatter_g(const dr_shard *s, const float *g_part,
  * libdr launch issued by this host thread is bracketed by CUDA events on the
  * stream it is launched on. dr_profile_end synchronises, aggregates by kernel
  * tag ("<kernel>.<relation or role>") and disables profiling; *n_out is the
- * number of distinct tags (entries beyond cap are dropped). Not for use
- * inside CUDA-graph capture. */
+ * number of distinct tags (entries beyond cap are dropped). While profiling,
+ * layers run on the caller's stream (isolated kernel times) and training
+ * steps run eagerly. Not for use inside CUDA-graph capture. */
 typedef struct {
     char name[48];
     int64_t launches;
@@ -360,6 +379,16 @@ typedef struct {
 } dr_profile_entry;
 dr_status dr_profile_begin(void);
 dr_status dr_profile_end(dr_profile_entry *out, int32_t cap, int32_t *n_out);
+
+/* Experiment / test switches (read once from DR_* environment variables when
+ * the library loads; never on a launch path). name is one of: nvtx, no_graph,
+ * dense_simt, tspmm, ts_zerofill, ts_debug, tc2_debug, bwd_p, drelu_bs, tiles,
+ * order_degree, warp_row_deg, ts_tile_w, ts_tile_w_bwd, ts_order_rr,
+ * shard_tiles, shard_tiles_t (see csrc/knobs.cpp). Each selects between
+ * parity-tested kernel paths or adds diagnostics; none changes a result beyond
+ * rounding. Not synchronised with concurrent launches. DR_ERR_INVALID_ARGUMENT
+ * for an unknown name. */
+dr_status dr_debug_set(const char *name, int64_t value);
 
 /* Number of kernels this library launched on this host thread since the last
  * reset (evidence for bench.py's gpu_launches). */

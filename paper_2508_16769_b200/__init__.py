@@ -53,6 +53,11 @@ def launch_count_reset():
     lib().dr_launch_count_reset()
 
 
+def debug_set(name, value):
+    """dr_debug_set: experiment / test switch (see include/dr.h)."""
+    check(lib().dr_debug_set(name.encode(), int(value)))
+
+
 def profile_begin():
     """Start per-kernel CUDA-event timing of libdr launches on this thread."""
     check(lib().dr_profile_begin())
@@ -72,12 +77,23 @@ def profile_end():
 # ------------------------------------------------------------------ graph
 class Graph:
     """Device-resident heterograph (dr_graph_create). `rels` maps 'near'/'pins'/
-    'pinned' to (row_ptr int64 [n_dst+1], col_idx int32 [nnz]) host arrays."""
+    'pinned' to (row_ptr int64 [n_dst+1], col_idx int32 [nnz]) host arrays.
+    Optional per relation (dr_rel_desc): `csc` -> (col_ptr int64, row_idx int32
+    [, tval float32]), `degrees` -> (deg_dst, deg_src) int32 (either may be
+    None), `norms` -> (c, s) float32 (either may be None)."""
 
     def __init__(self, n_cell, n_net, rels, modules=None, weights=None, n_threads=0, flags=0,
-                 stream=None):
+                 stream=None, csc=None, degrees=None, norms=None):
         modules = dict(DEFAULT_MODULES if modules is None else modules)
         weights = dict(weights or {})
+        csc, degrees, norms = dict(csc or {}), dict(degrees or {}), dict(norms or {})
+
+        def arr(a, dt):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(a, dtype=dt)
+            self._keep.append(a)
+            return a.ctypes.data if a.size else None
         dims = {"near": (n_cell, n_cell), "pins": (n_net, n_cell), "pinned": (n_cell, n_net)}
         descs = (dr_rel_desc * 3)()
         self._keep = []
@@ -96,6 +112,14 @@ class Graph:
             d.col_idx = col.ctypes.data if col.size else None
             d.val = None if w is None else w.ctypes.data
             d.module = int(modules[name])
+            if name in csc:
+                t = tuple(csc[name]) + (None,) * (3 - len(csc[name]))
+                d.col_ptr, d.row_idx = arr(t[0], np.int64), arr(t[1], np.int32)
+                d.tval = arr(t[2], np.float32)
+            if name in degrees:
+                d.deg_dst, d.deg_src = arr(degrees[name][0], np.int32), arr(degrees[name][1], np.int32)
+            if name in norms:
+                d.norm_dst, d.norm_src = arr(norms[name][0], np.float32), arr(norms[name][1], np.float32)
         out = C.c_void_p()
         check(lib().dr_graph_create(int(n_cell), int(n_net), descs, None, int(n_threads),
                                     int(flags), _stream(stream), C.byref(out)))

@@ -31,7 +31,9 @@ P = C.c_void_p
 
 class dr_rel_desc(C.Structure):
     _fields_ = [("n_dst", C.c_int32), ("n_src", C.c_int32), ("nnz", C.c_int64),
-                ("row_ptr", P), ("col_idx", P), ("val", P), ("module", C.c_int)]
+                ("row_ptr", P), ("col_idx", P), ("val", P), ("module", C.c_int),
+                ("col_ptr", P), ("row_idx", P), ("tval", P), ("deg_dst", P), ("deg_src", P),
+                ("norm_dst", P), ("norm_src", P)]
 
 
 class dr_allocator(C.Structure):
@@ -134,6 +136,7 @@ _SIGS = {
     "dr_profile_begin": (C.c_int, []),
     "dr_profile_end": (C.c_int, [C.POINTER(dr_profile_entry), C.c_int32, C.POINTER(C.c_int32)]),
     "dr_launch_count": (C.c_int64, []),
+    "dr_debug_set": (C.c_int, [C.c_char_p, C.c_int64]),
     "dr_launch_count_reset": (None, []),
 }
 

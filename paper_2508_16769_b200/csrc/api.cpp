@@ -6,6 +6,8 @@
 
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <unordered_map>
 
@@ -57,13 +59,7 @@ static cudaEvent_t pool_get() {
 // DR_NVTX=1: every launch is wrapped in an NVTX range named "<base>.<tag>", so
 // `ncu --nvtx --print-nvtx-rename kernel` reports per-tag kernel metrics (the
 // DRAM traffic of profiles/ncu_traffic.json). Off by default (no overhead).
-static bool nvtx_on() {
-    static const bool on = [] {
-        const char *e = getenv("DR_NVTX");
-        return e && atoi(e) != 0;
-    }();
-    return on;
-}
+static bool nvtx_on() { return knobs().nvtx != 0; }
 
 ProfScope::ProfScope(const char *b, cudaStream_t st) {
     if (nvtx_on()) {
@@ -96,12 +92,16 @@ TagScope::TagScope(const char *tag) : prev(t_tag) {
 }
 TagScope::~TagScope() { t_tag = prev; }
 
+// cudaFuncSetAttribute applies to the current device's context only: the cache
+// is keyed on (device, kernel) so a process driving several GPUs sets it per device
 void ensure_smem(const void *fn, size_t bytes) {
     static std::mutex mu;
-    static std::unordered_map<const void *, size_t> set;
+    static std::map<std::pair<int, const void *>, size_t> set;
     if (bytes <= 48 * 1024) return;
+    int dev = 0;
+    DR_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(mu);
-    size_t &cur = set[fn];
+    size_t &cur = set[{dev, fn}];
     if (bytes > cur) {
         DR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
         cur = bytes;
@@ -139,12 +139,10 @@ static void wait_on(cudaStream_t waiter, cudaStream_t producer, cudaEvent_t ev) 
     DR_CUDA(cudaStreamWaitEvent(waiter, ev, 0));
 }
 
-// DR_FORCE_SEQUENTIAL=1: every layer runs on the caller's stream (per-kernel
-// timing passes of bench.py; results are bit-identical either way).
-static bool force_sequential() {
-    const char *e = getenv("DR_FORCE_SEQUENTIAL");
-    return e && atoi(e);
-}
+// Between dr_profile_begin and dr_profile_end every layer runs on the caller's
+// stream, so the per-launch events time isolated kernels (results are
+// bit-identical either way).
+static bool force_sequential() { return t_prof; }
 
 static bool is_pow2(int k) { return k > 0 && (k & (k - 1)) == 0; }
 
@@ -581,9 +579,10 @@ NcclApi &nccl() {
         api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
         api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
         api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+        api.commGetAsyncError = (decltype(api.commGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
         api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.commCount &&
                  api.commUserRank && api.allReduce && api.allGather && api.reduceScatter &&
-                 api.groupStart && api.groupEnd && api.getErrorString;
+                 api.groupStart && api.groupEnd && api.getErrorString && api.commGetAsyncError;
         if (!api.ok) api.err = "missing NCCL symbols";
     });
     if (!api.ok) fail(DR_ERR_NCCL, "cannot load NCCL: " + api.err);
@@ -617,9 +616,14 @@ struct dr_trainer {
         const void *xc = nullptr, *xn = nullptr, *lab = nullptr, *loss = nullptr, *gout = nullptr;
         int runs = 0;
         int64_t kernels = 0;                 // kernel nodes (counted as launches per replay)
+        uint64_t last_use = 0;
         cudaGraphExec_t exec = nullptr;
     };
+    // LRU-bounded: training over many designs (one dr_graph each) or fresh input
+    // buffers every step must not grow the cache (or keep execs of dead graphs)
+    static constexpr size_t kMaxGraphs = 128;
     std::vector<GraphEntry> graphs;
+    uint64_t use_clock = 0;
 };
 
 namespace {
@@ -958,7 +962,6 @@ int64_t dr_train_param_count(const dr_train_cfg *c) {
 
 dr_status dr_trainer_create(const dr_train_cfg *c, float *params, int64_t n_params,
                             void *nccl_comm, const dr_allocator *a, dr_trainer **out) {
-    dr_trainer *t = nullptr;
     DR_API_BEGIN
     DR_CHECK(c && params && out, DR_ERR_INVALID_ARGUMENT, "null cfg/params/out");
     *out = nullptr;
@@ -977,7 +980,8 @@ dr_status dr_trainer_create(const dr_train_cfg *c, float *params, int64_t n_para
     check_out_width(c->d_hidden, "cfg d_hidden");
     check_out_width(c->d_in_cell, "cfg d_in_cell");
     check_out_width(c->d_in_net, "cfg d_in_net");
-    t = new dr_trainer();
+    // owned until every step below succeeded (a throw frees it: nothing leaks)
+    std::unique_ptr<dr_trainer, dr_status (*)(dr_trainer *)> t(new dr_trainer(), dr_trainer_destroy);
     t->cfg = *c;
     t->params = params;
     t->n_params = n_params;
@@ -1013,8 +1017,7 @@ dr_status dr_trainer_create(const dr_train_cfg *c, float *params, int64_t n_para
         l.d_net = dn;
         dc = dn = c->d_hidden;
     }
-    *out = t;
-    t = nullptr;
+    *out = t.release();
     DR_API_END
 }
 
@@ -1068,7 +1071,8 @@ static void train_step_body(dr_trainer *t, const dr_graph *g, const float *x_cel
         cur ^= 1;
     }
     // ---- data-parallel gradient exchange: one allreduce (sum) of the flat gradient
-    if (t->comm && t->world > 1)
+    // (issued whenever a communicator is given, also at world size 1)
+    if (t->comm)
         DR_NCCL(nccl().allReduce(t->grad, t->grad, (size_t)t->n_params, ncclFloat32, ncclSum,
                                  t->comm, st));
     const float inv_world = 1.0f / (float)t->world;
@@ -1091,6 +1095,12 @@ dr_status dr_train_step(dr_trainer *t, const dr_graph *g, const float *x_cell, c
     DR_CHECK((g->n_cell == 0 || (x_cell && labels)) && (g->n_net == 0 || x_net),
              DR_ERR_INVALID_ARGUMENT, "null inputs");
     cudaStream_t st = (cudaStream_t)stream;
+    if (t->comm) {       // a peer failure of an earlier step's allreduce surfaces here
+        ncclResult_t ae = ncclSuccess;
+        DR_NCCL(nccl().commGetAsyncError(t->comm, &ae));
+        DR_CHECK(ae == ncclSuccess || ae == ncclInProgress, DR_ERR_NCCL,
+                 std::string("communicator async error: ") + nccl().getErrorString(ae));
+    }
     const dr_train_cfg &c = t->cfg;
     const int nl = c.n_layers, D = c.d_hidden;
     const size_t nc = (size_t)g->n_cell, nn = (size_t)g->n_net;
@@ -1110,8 +1120,7 @@ dr_status dr_train_step(dr_trainer *t, const dr_graph *g, const float *x_cell, c
         t->ws_cap = off;
     }
     t->step += 1;
-    const char *ng = getenv("DR_NO_GRAPH");
-    if (t_prof || (ng && atoi(ng))) {          // per-kernel profiling runs eagerly
+    if (t_prof || knobs().no_graph) {          // per-kernel profiling runs eagerly
         train_step_body(t, g, x_cell, x_net, labels, loss_host, grad_out, t->ws, st);
     } else {
         dr_trainer::GraphEntry *ge = nullptr;
@@ -1119,12 +1128,23 @@ dr_status dr_train_step(dr_trainer *t, const dr_graph *g, const float *x_cell, c
             if (e.graph_uid == g->uid && e.xc == x_cell && e.xn == x_net && e.lab == labels &&
                 e.loss == loss_host && e.gout == grad_out)
                 ge = &e;
+        if (!ge && t->graphs.size() >= dr_trainer::kMaxGraphs) {   // evict the least recently used
+            size_t lru = 0;
+            for (size_t i = 1; i < t->graphs.size(); ++i)
+                if (t->graphs[i].last_use < t->graphs[lru].last_use) lru = i;
+            if (t->graphs[lru].exec) {
+                DR_CUDA(cudaStreamSynchronize(st));          // a replay may still be in flight
+                cudaGraphExecDestroy(t->graphs[lru].exec);
+            }
+            t->graphs.erase(t->graphs.begin() + lru);
+        }
         if (!ge) {
             t->graphs.push_back({});
             ge = &t->graphs.back();
             ge->graph_uid = g->uid; ge->xc = x_cell; ge->xn = x_net; ge->lab = labels;
             ge->loss = loss_host; ge->gout = grad_out;
         }
+        ge->last_use = ++t->use_clock;
         if (ge->exec) {
             DR_CUDA(cudaGraphLaunch(ge->exec, st));
             t_launches += ge->kernels;

@@ -31,6 +31,29 @@ void clear_error();
         if (!(cond)) ::dr::fail(status, msg);                                                \
     } while (0)
 
+// Experiment / profiling switches (knobs.cpp): read once from the environment
+// at library load, overridable through dr_debug_set; never read on a launch path.
+struct Knobs {
+    int64_t nvtx = 0;            // DR_NVTX: NVTX range per launch named by its profile tag
+    int64_t no_graph = 0;        // DR_NO_GRAPH: train steps run eagerly (no CUDA graph)
+    int64_t dense_simt = 0;      // DR_DENSE_SIMT: SIMT projections / dW instead of tcgen05
+    int64_t tspmm = 1;           // DR_TSPMM=0: SIMT kernels for near instead of the tiled ones
+    int64_t ts_zerofill = 0;     // DR_TS_ZEROFILL: TMA zero fill of the tiled forward's B tile
+    int64_t ts_debug = 0;        // DR_TS_DEBUG: per-role cycle counters of the tiled SpMM
+    int64_t tc2_debug = 0;       // DR_TC2_DEBUG: per-role cycle counters of the tc2 GEMMs
+    int64_t bwd_p = 0;           // DR_BWD_P: pairs per lane of the SIMT SSpMM (0 = chosen)
+    int64_t drelu_bs = 0;        // DR_DRELU_BS: binary-search D-ReLU for every k
+    int64_t tiles = 1;           // DR_TILES=0: no BFS-ball tiles at graph creation
+    int64_t order_degree = 0;    // DR_ORDER=degree: degree buckets without the locality rank
+    int64_t warp_row_deg = -1;   // DR_WARP_ROW_DEG: warp-row degree threshold (-1 = 32)
+    int64_t ts_tile_w = -1;      // DR_TS_TILE_W: forward CTA-split tile weight (-1 = adaptive)
+    int64_t ts_tile_w_bwd = -1;  // DR_TS_TILE_W_BWD: backward CTA-split tile weight
+    int64_t ts_order_rr = 0;     // DR_TS_ORDER=rr: round-robin tile assignment
+    int64_t shard_tiles = 0;     // DR_SHARD_TILES: tiled forward for shard blocks
+    int64_t shard_tiles_t = 0;   // DR_SHARD_TILES_T: tiled backward for shard blocks
+};
+const Knobs &knobs();
+
 // Launch bookkeeping: count kernels and surface launch errors immediately.
 void note_launch(const char *name);
 

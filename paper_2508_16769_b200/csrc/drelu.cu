@@ -327,10 +327,7 @@ void launch_drelu(const float *x, int64_t n, int dim, int64_t ldx, int k, float 
     const bool vec = dim == 32 * V && (ldx % V) == 0 &&
                      (reinterpret_cast<uintptr_t>(x) % (4 * V)) == 0;
     DR_CHECK(!sorted || k <= 32, DR_ERR_BAD_K, "value-sorted D-ReLU needs k <= 32");
-    static const bool force_bs = [] {          // A/B only: the binary search for every k
-        const char *e = getenv("DR_DRELU_BS");
-        return e && atoi(e) == 1;
-    }();
+    const bool force_bs = knobs().drelu_bs == 1;   // A/B only: the binary search for every k
     if (k <= 32 && sorted) {
         if (V == 1)
             drelu_extract_kernel<1, true><<<(unsigned)blocks, threads, 0, s>>>(x, n, dim, ldx, k, vec, val, idx);

@@ -237,16 +237,14 @@ void build_tiles(int32_t n, const std::vector<int32_t> &rp, const std::vector<in
 // cta_chunks[cta_beg[b], cta_beg[b+1]).
 void split_ctas(HostTiles &T, int64_t tile_w) {
     if (tile_w < 0) {                 // forward: weight 1 once CTAs own many tiles
-        const char *tw = getenv("DR_TS_TILE_W");
-        tile_w = tw ? atoi(tw) : (T.n_tiles >= 16 * 148 ? 1 : 0);
+        tile_w = knobs().ts_tile_w >= 0 ? knobs().ts_tile_w : (T.n_tiles >= 16 * 148 ? 1 : 0);
     }
     T.grid = std::min<int32_t>(T.n_tiles, 148);
     T.cta_beg.assign((size_t)T.grid + 1, 0);
     T.cta_chunks.clear();
     T.cta_tiles.clear();
     T.cta_chunks.reserve((size_t)T.n_chunks);
-    const char *ord = getenv("DR_TS_ORDER");
-    const bool rr = ord && std::string(ord) == "rr";
+    const bool rr = knobs().ts_order_rr != 0;
     int32_t t0 = 0;
     for (int32_t b = 0; b < T.grid; ++b) {
         T.cta_beg[b] = (int32_t)T.cta_chunks.size();
@@ -325,23 +323,50 @@ void build_rel(const dr_rel_desc &d, bool validate, HostRel &h) {
     }
     for (int64_t e = 0; e < d.nnz; ++e) h.deg_out[ci[e]]++;
     for (int32_t j = 0; j < d.n_src; ++j) h.max_out = std::max(h.max_out, h.deg_out[j]);
-    // normalisers (reading Q12: unweighted counts clamped to >= 1)
+    // optional caller inputs (dr_rel_desc): degrees >= 0, normalisers finite
+    auto bad = [&](dr_status st, const std::string &m) { h.st = st; h.err = m; };
+    if (d.tval && !d.col_ptr) return bad(DR_ERR_INVALID_ARGUMENT, "tval given without col_ptr");
+    if (d.nnz > 0 && (d.col_ptr == nullptr) != (d.row_idx == nullptr))
+        return bad(DR_ERR_INVALID_ARGUMENT, "col_ptr and row_idx must be given together");
+    for (int32_t i = 0; d.deg_dst && i < d.n_dst; ++i)
+        if (d.deg_dst[i] < 0) return bad(DR_ERR_OUT_OF_RANGE, "negative deg_dst");
+    for (int32_t j = 0; d.deg_src && j < d.n_src; ++j)
+        if (d.deg_src[j] < 0) return bad(DR_ERR_OUT_OF_RANGE, "negative deg_src");
+    for (int32_t i = 0; d.norm_dst && i < d.n_dst; ++i)
+        if (!std::isfinite(d.norm_dst[i])) return bad(DR_ERR_NONFINITE, "non-finite norm_dst");
+    for (int32_t j = 0; d.norm_src && j < d.n_src; ++j)
+        if (!std::isfinite(d.norm_src[j])) return bad(DR_ERR_NONFINITE, "non-finite norm_src");
+    // normalisers (reading Q12: unweighted counts clamped to >= 1), from the
+    // caller's degrees or normalisers when given
     h.c.resize(d.n_dst);
     h.s.resize(d.n_src);
     for (int32_t i = 0; i < d.n_dst; ++i) {
-        const double dg = std::max(h.deg_in[i], 1);
-        h.c[i] = (float)(d.module == DR_SAGE_MEAN ? 1.0 / dg : 1.0 / std::sqrt(dg));
+        const double dg = std::max(d.deg_dst ? d.deg_dst[i] : h.deg_in[i], 1);
+        h.c[i] = d.norm_dst ? d.norm_dst[i]
+                            : (float)(d.module == DR_SAGE_MEAN ? 1.0 / dg : 1.0 / std::sqrt(dg));
     }
     for (int32_t j = 0; j < d.n_src; ++j) {
-        const double dg = std::max(h.deg_out[j], 1);
-        h.s[j] = (float)(d.module == DR_SAGE_MEAN ? 1.0 : 1.0 / std::sqrt(dg));
+        const double dg = std::max(d.deg_src ? d.deg_src[j] : h.deg_out[j], 1);
+        h.s[j] = d.norm_src ? d.norm_src[j]
+                            : (float)(d.module == DR_SAGE_MEAN ? 1.0 : 1.0 / std::sqrt(dg));
     }
     // forward per-edge weight a_e * s_j (absent when identically 1)
-    if (h.weighted || d.module != DR_SAGE_MEAN) {
+    bool s_one = true;
+    for (int32_t j = 0; j < d.n_src && s_one; ++j) s_one = h.s[j] == 1.0f;
+    if (h.weighted || d.module != DR_SAGE_MEAN || !s_one) {
         h.ew.resize(d.nnz);
         for (int64_t e = 0; e < d.nnz; ++e) h.ew[e] = (d.val ? d.val[e] : 1.0f) * h.s[ci[e]];
     }
-    // CSC by counting sort (row ids ascending within each column)
+    // CSC (Alg. 2 stage 1): the caller's, used as given when validation
+    // is skipped (and its weights are known), else built by counting sort and the
+    // caller's, if any, checked against it
+    if (d.col_ptr && !validate && (!h.weighted || d.tval)) {
+        h.colptr.resize((size_t)d.n_src + 1);
+        for (int32_t j = 0; j <= d.n_src; ++j) h.colptr[j] = (int32_t)d.col_ptr[j];
+        h.row.assign(d.row_idx, d.row_idx + d.nnz);
+        if (h.weighted) h.ewT.assign(d.tval, d.tval + d.nnz);
+        return;
+    }
     h.colptr.assign((size_t)d.n_src + 1, 0);
     for (int32_t j = 0; j < d.n_src; ++j) h.colptr[j + 1] = h.colptr[j] + h.deg_out[j];
     h.row.resize(d.nnz);
@@ -353,6 +378,18 @@ void build_rel(const dr_rel_desc &d, bool validate, HostRel &h) {
             h.row[p] = i;
             if (h.weighted) h.ewT[p] = d.val[e];
         }
+    if (d.col_ptr) {
+        bool same = d.col_ptr[0] == 0;
+        for (int32_t j = 0; same && j < d.n_src; ++j) same = d.col_ptr[j + 1] == h.colptr[j + 1];
+        for (int64_t p = 0; same && p < d.nnz; ++p) same = d.row_idx[p] == h.row[p];
+        if (same && d.tval) {
+            std::vector<int32_t> pos(h.colptr.begin(), h.colptr.end() - 1);
+            for (int32_t i = 0; same && i < d.n_dst; ++i)
+                for (int64_t e = rp[i]; same && e < rp[i + 1]; ++e)
+                    same = d.tval[pos[ci[e]]++] == (d.val ? d.val[e] : 1.0f);
+        }
+        if (!same) return bad(DR_ERR_TRANSPOSE_MISMATCH, "col_ptr/row_idx/tval is not CSR^T");
+    }
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -365,9 +402,8 @@ size_t vbytes(const std::vector<T> &v) {
 }  // namespace
 
 int warp_row_threshold() {
-    const char *e = getenv("DR_WARP_ROW_DEG");     // experiments only
-    const int env = e ? atoi(e) : -1;
-    return env >= 0 ? env : 32;   // measured best on C2 (k=8) and C4 (k=16): profiles/r01/ab_*.txt
+    const int64_t v = knobs().warp_row_deg;        // experiments only
+    return v >= 0 ? (int)v : 32;   // measured best on C2 (k=8) and C4 (k=16): profiles/r01/ab_*.txt
 }
 
 void *Alloc::get(size_t bytes, cudaStream_t s) {
@@ -450,8 +486,7 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
         // locality ranks: cells by BFS over the near graph,
         // nets by their lowest-ranked member cell; DR_ORDER=degree drops them
         std::vector<int64_t> rank_c, rank_n;
-        const char *ord_env = getenv("DR_ORDER");
-        const bool use_loc = !identity && !(ord_env && std::string(ord_env) == "degree");
+        const bool use_loc = !identity && !knobs().order_degree;
         if (use_loc) {
             rank_c = bfs_rank(n_cell, h[DR_NEAR].rowptr, h[DR_NEAR].col);
             rank_n.assign((size_t)n_net, 0);
@@ -467,9 +502,8 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
         // tiled form of near for the tensor-core SpMM (tspmm.cu): unit weights,
         // dense enough neighbourhoods (mean degree >= 8); DR_TILES=0 disables
         HostTiles tl, tlT;
-        const char *tenv = getenv("DR_TILES");
         const HostRel &hn = h[DR_NEAR];
-        const bool want_tiles = !identity && !(tenv && atoi(tenv) == 0) && hn.ew.empty() &&
+        const bool want_tiles = !identity && knobs().tiles != 0 && hn.ew.empty() &&
                                 hn.ewT.empty() && hn.n_dst > 0 && hn.nnz >= 8LL * hn.n_dst;
         std::thread tile_th;
         // symmetric near: one TileSet for both directions, but the backward gets
@@ -487,8 +521,8 @@ extern "C" dr_status dr_graph_create(int32_t n_cell, int32_t n_net, const dr_rel
                     tlB.n_tiles = tl.n_tiles;
                     tlB.n_chunks = tl.n_chunks;
                     tlB.chunk_beg = tl.chunk_beg;
-                    const char *e = getenv("DR_TS_TILE_W_BWD");
-                    split_ctas(tlB, e ? atoi(e) : (tl.n_tiles >= 16 * 148 ? 2 : 0));
+                    split_ctas(tlB, knobs().ts_tile_w_bwd >= 0 ? knobs().ts_tile_w_bwd
+                                                              : (tl.n_tiles >= 16 * 148 ? 2 : 0));
                 }
             });
         {
@@ -700,8 +734,7 @@ void build_rel_block(const dr_rel_desc &d, const std::vector<float> &s_glob, int
     // 10 % faster than the SIMT one (W = 2, shuffled ids) and slower with spatial
     // ids, so the SIMT kernels are the default for blocks.
     HostTiles tl, tlT;
-    const char *tenv = getenv("DR_SHARD_TILES");
-    const bool want_tiles = tenv && atoi(tenv) == 1 && h.ew.empty() && h.ewT.empty() &&
+    const bool want_tiles = knobs().shard_tiles == 1 && h.ew.empty() && h.ewT.empty() &&
                             h.n_dst > 0 && h.nnz >= 8LL * h.n_dst;
     if (want_tiles) {
         const int64_t off = own_col0 >= 0 ? -own_col0 : -(int64_t)h.n_src - h.n_dst - 1;
@@ -714,8 +747,7 @@ void build_rel_block(const dr_rel_desc &d, const std::vector<float> &s_glob, int
         // the transposed tiles would span every padded source row, most of them
         // edge-free or remote with a few boundary edges (measured 2-3x slower than
         // the SIMT SSpMM at C4, W = 2..8): DR_SHARD_TILES_T=1 builds them anyway
-        const char *te = getenv("DR_SHARD_TILES_T");
-        if (te && atoi(te) == 1) build_tiles(h.n_src, h.colptr, h.row, noloc, tlT, h.n_dst, offT, true);
+        if (knobs().shard_tiles_t == 1) build_tiles(h.n_src, h.colptr, h.row, noloc, tlT, h.n_dst, offT, true);
     }
     out = RelDev{};
     out.n_dst = h.n_dst;

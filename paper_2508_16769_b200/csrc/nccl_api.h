@@ -26,6 +26,7 @@ struct NcclApi {
     ncclResult_t (*groupStart)() = nullptr;
     ncclResult_t (*groupEnd)() = nullptr;
     const char *(*getErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
 };
 
 NcclApi &nccl();    // throws DR_ERR_NCCL when libnccl or a symbol is missing

@@ -53,6 +53,10 @@ void check_rel(const dr_rel_desc *r) {
              "shard: null CSR pointer");
     DR_CHECK(r->module == DR_SAGE_MEAN || r->module == DR_GRAPHCONV_SYM, DR_ERR_INVALID_ARGUMENT,
              "shard: bad module");
+    DR_CHECK(!r->col_ptr && !r->row_idx && !r->tval && !r->deg_dst && !r->deg_src &&
+                 !r->norm_dst && !r->norm_src,
+             DR_ERR_UNSUPPORTED, "shard: the optional CSC / degree / normaliser inputs are not "
+                                 "supported (the shard computes the global ones)");
 }
 
 void default_plan(const dr_rel_desc &r, int world, int64_t *dp, int64_t *sp) {

@@ -77,7 +77,7 @@ __device__ __forceinline__ void fwd_accumulate(int e0, int e1, int stride,
                                                const float *__restrict__ ew,
                                                const float *__restrict__ hval,
                                                const uint8_t *__restrict__ hidx, int k, int ll,
-                                               float *acc, int kr) {
+                                               float *acc, int kr, unsigned smask) {
     int jn[kU];
     float wn[kU];
 #pragma unroll
@@ -109,7 +109,7 @@ __device__ __forceinline__ void fwd_accumulate(int e0, int e1, int stride,
             wn[u] = (ok && ew) ? __ldg(ew + ee) : 1.0f;
         }
 #pragma unroll
-        for (int u = 0; u < kU; ++u)
+        for (int u = 0; u < kU; ++u) {
             if (j[u] >= 0 && ll * P < kr) {
                 float old[P];
 #pragma unroll
@@ -117,6 +117,10 @@ __device__ __forceinline__ void fwd_accumulate(int e0, int e1, int stride,
 #pragma unroll
                 for (int p = 0; p < P; ++p) acc[pr[u].id[p]] = old[p] + w[u] * pr[u].v[p];
             }
+            // lanes of the sub-warp may hit the same column for the next neighbour:
+            // order this read-modify-write before theirs (independent thread scheduling)
+            __syncwarp(smask);
+        }
     }
 }
 
@@ -172,6 +176,7 @@ __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
     const int L = a.L, R = 32 / L, sub = lane / L, ll = lane % L, D = a.D, D4 = D >> 2;
     float *acc = sm + (size_t)(wid * R + sub) * D;
     float4 *acc4 = reinterpret_cast<float4 *>(acc);
+    const unsigned smask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (sub * L));
     const int b = blockIdx.x;
 
     if (b < a.hub_ctas) {
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
             const int chunk = (e1 - e0 + S - 1) / S;
             const int b0 = min(e1, e0 + sidx * chunk), b1 = min(e1, b0 + chunk);
             fwd_accumulate<P>(b0, b1, 1, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc,
-                              ng_k(a.ng, e1 - e0, a.k));
+                              ng_k(a.ng, e1 - e0, a.k), smask);
             __syncthreads();
             const float cr = __ldg(a.c + row);
             for (int cc = threadIdx.x; cc < D; cc += blockDim.x) {
@@ -207,7 +212,7 @@ __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
         if (valid) {
             const int e0 = __ldg(a.rowptr + row), e1 = __ldg(a.rowptr + row + 1);
             fwd_accumulate<P>(e0 + sub, e1, R, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc,
-                              ng_k(a.ng, e1 - e0, a.k));
+                              ng_k(a.ng, e1 - e0, a.k), smask);
         }
         __syncwarp();
         if (valid) {
@@ -234,7 +239,7 @@ __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
     if (valid) {
         const int e0 = __ldg(a.rowptr + row), e1 = __ldg(a.rowptr + row + 1);
         fwd_accumulate<P>(e0, e1, 1, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc,
-                          ng_k(a.ng, e1 - e0, a.k));
+                          ng_k(a.ng, e1 - e0, a.k), smask);
     }
     __syncwarp();
     if (valid) {
@@ -548,8 +553,8 @@ void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, in
 // keeping two independent loads per lane; measured best at C2 (k=8) and C4
 // (k=16) against P = 1 and 4 (profiles/r01/ab_bwdP.txt). Row sums stay in registers.
 static int choose_P_bwd(int k) {
-    const char *e = getenv("DR_BWD_P");              // experiments only
-    if (e && atoi(e) > 0 && k % atoi(e) == 0 && k / atoi(e) <= 32) return atoi(e);
+    const int p = (int)knobs().bwd_p;                // experiments only
+    if (p > 0 && k % p == 0 && k / p <= 32) return p;
     if (k == 1) return 1;
     return k / 2 <= 32 ? 2 : k / 32;
 }

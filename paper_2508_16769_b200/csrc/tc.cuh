@@ -2,10 +2,10 @@
 //
 // Operand tiles in shared memory use the canonical K-major 128-byte-swizzle
 // layout of the UMMA descriptors (cute::UMMA::Layout_K_SW128_Atom): a tile of R
-// rows x 32 fp32 (one 128 B "K atom") stores row r at byte r*128 with its
+// rows x 64 bf16 (one 128 B "K atom") stores row r at byte r*128 with its
 // 16-byte chunk c at position (c ^ (r & 7)); 8-row groups are 1024 B apart
 // (SBO). Tiles must be 1024-B aligned. Wider K is a sequence of such atoms,
-// R*128 B apart. One tf32 MMA consumes K = 8 (32 B): the descriptor start
+// R*128 B apart. One kind::f16 MMA consumes K = 16 (32 B): the descriptor start
 // address advances by 32 B per K step inside an atom.
 #pragma once
 #include <cuda_runtime.h>
@@ -75,15 +75,6 @@ __device__ __forceinline__ void tma_load_2d(void *sdst, const void *tmap, int c0
         : "memory");
 }
 
-// 2-D tensor store (TMA) of a shared-memory box to (c0, c1) of the tensor map,
-// tracked by the issuing thread's bulk async-groups.
-__device__ __forceinline__ void tma_store_2d(const void *tmap, int c0, int c1, const void *ssrc) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-            reinterpret_cast<uint64_t>(tmap)),
-        "r"(c0), "r"(c1), "r"(smem_u32(ssrc))
-        : "memory");
-}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -145,30 +136,12 @@ __device__ __forceinline__ void fence_after() {
 }
 
 // ---------------------------------------------------------------- MMA
-// D[tmem] (+)= A[smem] x B[smem]^T, kind::tf32, fp32 accumulate, issued by one thread.
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
 // Arrive on `bar` once all previously issued MMAs of this thread complete.
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile(
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             smem_u32(bar))
         : "memory");
-}
-
-// Instruction descriptor: kind::tf32, fp32 D, K-major A and B, shape M x N.
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
-    return (1u << 4)                       // D format F32
-           | (2u << 7)                     // A format TF32
-           | (2u << 10)                    // B format TF32
-           | ((uint32_t)(N >> 3) << 17)    // N / 8
-           | ((uint32_t)(M >> 4) << 24);   // M / 16
 }
 
 // Shared-memory matrix descriptor: K-major, SWIZZLE_128B, SBO = 1024 B.
@@ -193,11 +166,6 @@ __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr, uint32_t lbo, 
     d |= (uint64_t)1 << 46;
     d |= (uint64_t)2 << 61;
     return d;
-}
-
-// Byte offset of fp32 element (r, k) (k < 32) inside a K-major SW128 atom tile.
-__device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t k) {
-    return r * 128u + ((((k >> 2) ^ (r & 7u)) & 7u) << 4) + ((k & 3u) << 2);
 }
 
 // ---------------------------------------------------------------- TMEM -> registers
@@ -229,14 +197,6 @@ __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// 3xTF32 split: x = hi + lo with hi = x rounded to tf32 (low 13 mantissa bits
-// cleared after round-to-nearest), lo = x - hi exactly representable in fp32.
-__device__ __forceinline__ void split_tf32(float x, float &hi, float &lo) {
-    uint32_t h;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-    hi = __uint_as_float(h);
-    lo = x - hi;
-}
 
 
 // ---------------------------------------------------------------- warp-specialised pipelines

@@ -1279,8 +1279,7 @@ static bool seg_ok(const Tc2Seg &s) {
 }
 
 bool tc2_rows_supported(const Tc2RowsDesc &d) {
-    const char *e = getenv("DR_DENSE_SIMT");      // A/B switch for tests and profiling
-    if (e && atoi(e)) return false;
+    if (knobs().dense_simt) return false;         // A/B switch for tests and profiling
     if (d.N < 16 || d.N > 256 || d.N % 16) return false;
     if (d.G < 1 || d.G > 2 || 2 * d.G * d.N > 512) return false;
     int steps = 0;
@@ -1359,8 +1358,7 @@ void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
     ProfScope ps(d.epi == kEpi2Dz ? "tc_dz" : "tc_proj", s);
     ensure_smem((const void *)tc2_rows_kernel, smem);
     static unsigned long long *dbg_buf = nullptr;
-    const char *dbe = getenv("DR_TC2_DEBUG");
-    if (dbe && atoi(dbe)) {
+    if (knobs().tc2_debug) {
         if (!dbg_buf) DR_CUDA(cudaMalloc(&dbg_buf, 148 * 16 * 8));
         DR_CUDA(cudaMemsetAsync(dbg_buf, 0, 148 * 16 * 8, s));
         a.dbg = dbg_buf;
@@ -1400,8 +1398,7 @@ static void red_layout(const Tc2ReduceDesc &d, int ncb, int maxk, RdArgs &a) {
 }
 
 bool tc2_reduce_supported(const Tc2ReduceDesc &d) {
-    const char *e = getenv("DR_DENSE_SIMT");
-    if (e && atoi(e)) return false;
+    if (knobs().dense_simt) return false;
     if (d.N < 16 || d.N > 128 || d.N % 16) return false;
     if (d.G < 1 || d.G > 2) return false;
     for (int g = 0; g < d.G; ++g) {
@@ -1478,8 +1475,7 @@ void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s) {
     a.part = work;
     ProfScope ps("tc_dw", s);
     static unsigned long long *dbg_buf = nullptr;
-    const char *dbe = getenv("DR_TC2_DEBUG");
-    if (dbe && atoi(dbe)) {
+    if (knobs().tc2_debug) {
         if (!dbg_buf) DR_CUDA(cudaMalloc(&dbg_buf, 148 * 16 * 8));
         DR_CUDA(cudaMemsetAsync(dbg_buf, 0, 148 * 16 * 8, s));
         a.dbg = dbg_buf;

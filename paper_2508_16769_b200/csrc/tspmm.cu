@@ -761,8 +761,7 @@ void launch(const TileSet &ts, TsArgs &a, int D, bool bwd, cudaStream_t s) {
     const int grid = ts.grid;
     if (grid <= 0) return;
     static unsigned long long *dbg_buf = nullptr;
-    const char *dbe = getenv("DR_TS_DEBUG");
-    if (dbe && atoi(dbe)) {
+    if (knobs().ts_debug) {
         if (!dbg_buf) DR_CUDA(cudaMalloc(&dbg_buf, 148 * 16 * 8));
         DR_CUDA(cudaMemsetAsync(dbg_buf, 0, 148 * 16 * 8, s));
         a.dbg = dbg_buf;
@@ -799,8 +798,7 @@ void launch(const TileSet &ts, TsArgs &a, int D, bool bwd, cudaStream_t s) {
 }  // namespace
 
 bool tspmm_supported(const TileSet &ts, int dim, int k) {
-    const char *e = getenv("DR_TSPMM");               // experiments only: 0 disables
-    if (e && atoi(e) == 0) return false;
+    if (knobs().tspmm == 0) return false;             // experiments only: 0 disables
     return ts.n_tiles > 0 && (dim == 64 || dim == 128) && (k == 4 || k == 8 || k == 16 || k == 32);
 }
 
@@ -825,8 +823,7 @@ void launch_tspmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, i
     // DR_TS_ZEROFILL=1: the TMA zero-fills B from an L2-resident zero buffer
     // instead of the converters (measured slower at C2 and C4: smem fill
     // bandwidth, not converter issue, bounds it; kept as an experiment)
-    const char *zf = getenv("DR_TS_ZEROFILL");
-    a.zeros = (zf && atoi(zf) == 1) ? zero_buffer() : nullptr;
+    a.zeros = knobs().ts_zerofill == 1 ? zero_buffer() : nullptr;
     a.k = k;
     a.hval = hval;
     a.hidx = hidx;

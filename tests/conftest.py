@@ -25,3 +25,17 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture
+def knob():
+    """Set a libdr experiment switch (dr_debug_set) for one test; restored after."""
+    import paper_2508_16769_b200 as dr
+    defaults = {}
+
+    def set_(name, value, default):
+        defaults.setdefault(name, default)
+        dr.debug_set(name, value)
+    yield set_
+    for name, value in defaults.items():
+        dr.debug_set(name, value)

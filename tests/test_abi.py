@@ -83,3 +83,49 @@ def test_graph_validation_errors():
     _expect(7, lambda: dr.Graph(d.n_cell, d.n_net, rels, weights={"near": w}))
     # error message is thread-local detail
     assert "DR_ERR_NONFINITE" in _lib.lib().dr_last_error().decode()
+
+
+def _csc(ptr, col, n_src):
+    """CSC of a CSR (numpy, data layout only)."""
+    rows = np.repeat(np.arange(ptr.size - 1, dtype=np.int64), np.diff(ptr))
+    order = np.lexsort((rows, col))
+    cptr = np.zeros(n_src + 1, np.int64)
+    np.cumsum(np.bincount(col, minlength=n_src), out=cptr[1:])
+    return cptr, rows[order].astype(np.int32), order
+
+
+def test_caller_csc_degree_norm_validation():
+    """dr_rel_desc optional inputs (Alg. 2 stage 1 "Transpose A to CSC"):
+    a caller CSC that is not CSR^T is rejected (TransposeMismatch), and
+    degrees / normalisers are range-checked, all before any device work."""
+    d = make_config("C1")
+    rels = _rels(d)
+    ptr, col = rels["near"]
+    cptr, crow, _ = _csc(ptr, col, d.n_cell)
+    bad = crow.copy()
+    j = int(np.argmax(np.diff(cptr) >= 2))
+    bad[cptr[j]], bad[cptr[j] + 1] = bad[cptr[j] + 1], bad[cptr[j]]     # rows out of order
+    _expect(6, lambda: dr.Graph(d.n_cell, d.n_net, rels, csc={"near": (cptr, bad)}))
+    cp2 = cptr.copy()
+    cp2[1] += 1
+    _expect(6, lambda: dr.Graph(d.n_cell, d.n_net, rels, csc={"near": (cp2, crow)}))
+    # weights: tval must be the CSC-ordered val
+    pp, pc = rels["pins"]
+    w = np.linspace(0.5, 2.0, pc.size).astype(np.float32)
+    qptr, qrow, order = _csc(pp, pc, d.n_cell)
+    wrong = w.copy()                                  # CSR order, not CSC order
+    if not np.array_equal(wrong, w[order]):
+        _expect(6, lambda: dr.Graph(d.n_cell, d.n_net, rels, weights={"pins": w},
+                                    csc={"pins": (qptr, qrow, wrong)}))
+    _expect(1, lambda: dr.Graph(d.n_cell, d.n_net, rels, csc={"pins": (qptr, None)}))
+    deg = np.diff(ptr).astype(np.int32)
+    deg[3] = -1
+    _expect(4, lambda: dr.Graph(d.n_cell, d.n_net, rels, degrees={"near": (deg, None)}))
+    c = np.ones(d.n_cell, np.float32)
+    c[0] = np.inf
+    _expect(7, lambda: dr.Graph(d.n_cell, d.n_net, rels, norms={"pinned": (c, None)}))
+
+
+def test_debug_set_rejects_unknown_names():
+    _expect(1, lambda: dr.debug_set("no_such_knob", 1))
+    dr.debug_set("tspmm", 1)

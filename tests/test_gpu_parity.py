@@ -357,7 +357,7 @@ def test_train_step_c2_runs_and_loss_decreases():
 
 # ------------------------------------------------------------------ tensor-core dense path
 @pytest.mark.parametrize("name,dc,dn,D,kc,kn", HC_CASES)
-def test_dense_tcgen05_matches_simt(designs, name, dc, dn, D, kc, kn, monkeypatch):
+def test_dense_tcgen05_matches_simt(designs, name, dc, dn, D, kc, kn, knob):
     """The tcgen05 2xbf16-split projections / dZ / dW agree with the SIMT fp32
     kernels (both are separately pinned to the oracle above) to 5e-5
     row-normalised: each split operand carries |x - hi - lo| <= 2^-18 |x| and the
@@ -376,7 +376,7 @@ def test_dense_tcgen05_matches_simt(designs, name, dc, dn, D, kc, kn, monkeypatc
     # only on near-ties of Y_near and Y_pinned (the two paths round differently)
     fw = {}
     for mode in ("0", "1"):
-        monkeypatch.setenv("DR_DENSE_SIMT", mode)
+        knob("dense_simt", int(mode), 0)
         yc, yn, tape = dr.heteroconv_fwd(g, L, xc, xn, flags=dr.DR_FWD_TAPS)
         v = dr.tape_view(g, L, tape, dr.DR_FWD_TAPS)
         torch.cuda.synchronize()
@@ -391,7 +391,7 @@ def test_dense_tcgen05_matches_simt(designs, name, dc, dn, D, kc, kn, monkeypatc
     # backward: both paths on the same (tc2) tape
     outs = {}
     for mode in ("0", "1"):
-        monkeypatch.setenv("DR_DENSE_SIMT", mode)
+        knob("dense_simt", int(mode), 0)
         grads, dxc, dxn = dr.heteroconv_bwd(g, L, fw["0"]["tape"], dyc, dyn, flags=dr.DR_FWD_TAPS)
         torch.cuda.synchronize()
         outs[mode] = dict(dxc=to_np(dxc), dxn=to_np(dxn), **{kk: to_np(vv) for kk, vv in grads.items()})

@@ -67,11 +67,11 @@ def test_shard_virtual_ranks_parity(designs, name, D, k, world):
         assert row_err(to_np(g), ref) <= TOL, rel
 
 
-def test_shard_near_blocks_tiled_optin(monkeypatch):
+def test_shard_near_blocks_tiled_optin(knob):
     """DR_SHARD_TILES=1 (opt-in): with node ids in a locality order, near's blocks
     (unit weights, dense neighbourhoods) run the tensor-core tiled forward, with
     the same parity; the SSpMM stays SIMT unless DR_SHARD_TILES_T=1."""
-    monkeypatch.setenv("DR_SHARD_TILES", "1")
+    knob("shard_tiles", 1, 0)
     d = make_config("C2", scale=0.1, order="spatial")
     for world in (1, 2, 4):
         for q in range(world):

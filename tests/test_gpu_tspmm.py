@@ -1,5 +1,5 @@
 """Tensor-core tiled SpMM (csrc/tspmm.cu) against the fp64 oracle and against the
-SIMT kernels (DR_TSPMM=0), on the near relation (the only one tiled: unit
+SIMT kernels (dr.debug_set("tspmm", 0)), on the near relation (the only one tiled: unit
 weights, mean degree >= 8). Covers symmetric and asymmetric near (separate CSC
 tiles), isolated rows (empty-halo tiles), every supported (D, k), the
 standalone ABI backward (dZ row scale applied in the converters) and determinism."""
@@ -67,7 +67,7 @@ def test_tiles_built(designs):
 
 @pytest.mark.parametrize("name,D,k", [("C2s", 64, 8), ("C4s", 128, 16), ("C2s", 128, 4),
                                       ("C2s", 64, 32), ("C4s", 64, 16), ("C2s", 128, 32)])
-def test_tspmm_matches_oracle_and_simt(designs, name, D, k, monkeypatch):
+def test_tspmm_matches_oracle_and_simt(designs, name, D, k, knob):
     d = designs[name]
     g = dr.Graph.from_design(d)
     assert g.info()["tiles"][0] > 0
@@ -81,7 +81,7 @@ def test_tspmm_matches_oracle_and_simt(designs, name, D, k, monkeypatch):
     assert row_err(to_np(gk), ref_g) <= TOL
     assert np.array_equal(to_np(dx), O.densify(oi, to_np(gk).astype(np.float64), D).astype(np.float32))
     # same results as the SIMT kernels up to fp32 rounding
-    monkeypatch.setenv("DR_TSPMM", "0")
+    knob("tspmm", 0, 1)
     z_s = dr.spmm_fwd(g, "near", val, idx, D)
     gk_s, _ = dr.spmm_bwd(g, "near", dz, val, idx, D)
     # (bf16 hi/lo split: |x - hi - lo| <= 2^-17 |x| per term on the tensor-core side)
