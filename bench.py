@@ -324,6 +324,20 @@ def oracle_grads_flat(dr, d, P, nl, k):
                                  np.asarray(og["head.b"], np.float64).reshape(-1)])
 
 
+def row_err(gpu, ref):
+    """max_r max_d |g - o| / max(||o_r||, tau) (SURVEY §8(c) parity metric)."""
+    g = np.atleast_2d(np.asarray(gpu, np.float64))
+    o = np.atleast_2d(np.asarray(ref, np.float64))
+    n = np.linalg.norm(o, axis=1)
+    tau = max(1e-6 * float(np.sqrt(np.mean(n ** 2))), 1e-30)
+    return float((np.abs(g - o).max(axis=1) / np.maximum(n, tau)).max())
+
+
+def split_flat(dr, a, b, nl, D):
+    ua, ub = dr.unflatten(a, nl, D, D, D), dr.unflatten(b, nl, D, D, D)
+    return {kk: (ua[kk], ub[kk]) for kk in ua}
+
+
 def oracle_train_timer(d, P, nl, k):
     """One full oracle training step (fwd, bwd, Adam) on design d, as a closure."""
     from oracle import oracle as O
@@ -374,7 +388,7 @@ def run_c5(args, torch, dist, dr, rank, world, local, dev, hbm, bf16, src):
 
     # ---- step 0 (P3 DP check): the allreduced mean gradient at the initial params
     g_dp = torch.empty_like(flat)
-    tr.step(graphs[0], *inputs[0], grad_out=g_dp)
+    loss0 = tr.step(graphs[0], *inputs[0], grad_out=g_dp)
     dp = {}
     if world > 1:
         flat_l = flat0.clone()
@@ -503,17 +517,29 @@ def run_c5(args, torch, dist, dr, rank, world, local, dev, hbm, bf16, src):
                    "with step i), D2H of the loss + host sync every step; max over ranks"}
     os.sched_setaffinity(0, all_cpus)
 
-    # ---- P3 parity: the step-0 allreduced gradient vs the mean of the fp64 oracle
-    # gradients of every rank's batch (O8), at the initial parameters
+    # ---- P2/P3 parity at full size: the step-0 allreduced gradient vs the mean of
+    # the fp64 oracle gradients of every rank's batch (O8), at the initial params,
+    # free-running (rows whose top-k or merge gap is below fp32 resolution are not
+    # excluded here; the teacher-forced checks are tests/test_gpu_*.py)
     t0 = time.time()
     oloss, og = oracle_grads_flat(dr, bd[0], P, nl, k)
     og_t = torch.as_tensor(og, device=dev)
+    ol_t = torch.tensor([oloss], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(og_t)
+        dist.all_reduce(ol_t)
     og_t /= world
     gd = g_dp.double()
-    dp["grad_vs_oracle_mean_max_rel"] = float((gd - og_t).abs().max() / og_t.abs().max())
-    dp["grad_vs_oracle_tolerance"] = 1e-4
+    worst, worst_key = 0.0, None
+    for key, (a, b) in split_flat(dr, gd.cpu().numpy(), og_t.cpu().numpy(), nl, D).items():
+        e = row_err(a, b)
+        if e > worst:
+            worst, worst_key = e, key
+    dp["oracle_grad_row_err_max"] = worst
+    dp["oracle_grad_row_err_worst_tensor"] = worst_key
+    dp["oracle_grad_tolerance"] = 1e-4
+    dp["oracle_note"] = ("free-running fp32 GPU vs fp64 oracle at full batch size, max over "
+                         "parameter tensors of the row-normalised error (SURVEY §8(c))")
     dp["oracle_s"] = round(time.time() - t0, 2)
 
     table = kernel_table(prof, bd[0], D, k, "C5", tiled=graphs[0].info()["tiles"][0] > 0)
@@ -575,7 +601,7 @@ def run_c5(args, torch, dist, dr, rank, world, local, dev, hbm, bf16, src):
             "clocks": clk,
             "wall_s_timed_loop": round(wall, 3),
             "dp_checks": dp,
-            "oracle_loss_batch0": oloss,
+            "step0_loss": {"gpu": loss0, "oracle_fp64": oloss, "batch": "rank 0 batch 0"},
             "kernels": table,
             "spmm_gate": spmm_gate(table, hbm),
         }

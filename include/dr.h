@@ -382,7 +382,7 @@ dr_status dr_profile_end(dr_profile_entry *out, int32_t cap, int32_t *n_out);
 
 /* Experiment / test switches (read once from DR_* environment variables when
  * the library loads; never on a launch path). name is one of: nvtx, no_graph,
- * dense_simt, tspmm, ts_zerofill, ts_debug, tc2_debug, bwd_p, drelu_bs, tiles,
+ * dense_simt, tspmm, ts_zerofill, ts_debug, tc2_debug, bwd_p, drelu_bs, drelu_tpr, tiles,
  * order_degree, warp_row_deg, ts_tile_w, ts_tile_w_bwd, ts_order_rr,
  * shard_tiles, shard_tiles_t (see csrc/knobs.cpp). Each selects between
  * parity-tested kernel paths or adds diagnostics; none changes a result beyond

@@ -43,6 +43,7 @@ struct Knobs {
     int64_t tc2_debug = 0;       // DR_TC2_DEBUG: per-role cycle counters of the tc2 GEMMs
     int64_t bwd_p = 0;           // DR_BWD_P: pairs per lane of the SIMT SSpMM (0 = chosen)
     int64_t drelu_bs = 0;        // DR_DRELU_BS: binary-search D-ReLU for every k
+    int64_t drelu_tpr = 1;       // DR_DRELU_TPR: 0 warp-per-row only, 1 thread-per-row where faster, 2 wherever supported
     int64_t tiles = 1;           // DR_TILES=0: no BFS-ball tiles at graph creation
     int64_t order_degree = 0;    // DR_ORDER=degree: degree buckets without the locality rank
     int64_t warp_row_deg = -1;   // DR_WARP_ROW_DEG: warp-row degree threshold (-1 = 32)
@@ -53,6 +54,9 @@ struct Knobs {
     int64_t shard_tiles_t = 0;   // DR_SHARD_TILES_T: tiled backward for shard blocks
 };
 const Knobs &knobs();
+
+// Opt a kernel into > 48 KB of dynamic shared memory on the current device (once).
+void ensure_smem(const void *fn, size_t bytes);
 
 // Launch bookkeeping: count kernels and surface launch errors immediately.
 void note_launch(const char *name);

@@ -26,6 +26,7 @@ static Knobs read_env() {
     k.tc2_debug = env_i("DR_TC2_DEBUG", 0);
     k.bwd_p = env_i("DR_BWD_P", 0);
     k.drelu_bs = env_i("DR_DRELU_BS", 0);
+    k.drelu_tpr = env_i("DR_DRELU_TPR", 1);
     k.tiles = env_i("DR_TILES", 1);
     const char *o = getenv("DR_ORDER");
     k.order_degree = (o && std::string(o) == "degree") ? 1 : 0;
@@ -62,6 +63,7 @@ extern "C" dr_status dr_debug_set(const char *name, int64_t value) {
         {"tc2_debug", &g_knobs.tc2_debug},
         {"bwd_p", &g_knobs.bwd_p},
         {"drelu_bs", &g_knobs.drelu_bs},
+        {"drelu_tpr", &g_knobs.drelu_tpr},
         {"tiles", &g_knobs.tiles},
         {"order_degree", &g_knobs.order_degree},
         {"warp_row_deg", &g_knobs.warp_row_deg},

@@ -37,7 +37,9 @@ def designs():
 
 # ------------------------------------------------------------------ D-ReLU
 @pytest.mark.parametrize("dim,k", [(16, 4), (64, 8), (128, 16), (256, 32), (64, 1), (32, 32),
-                                   (128, 64), (96, 8), (4, 2)])
+                                   (128, 64), (96, 8), (4, 2), (32, 2), (32, 8), (32, 16),
+                                   (64, 2), (64, 4), (64, 16), (64, 32), (128, 4), (128, 8),
+                                   (128, 32)])
 def test_drelu_bitexact(dim, k):
     rng = np.random.default_rng(dim * 31 + k)
     x = rng.standard_normal((3000, dim)).astype(np.float32)
@@ -53,6 +55,39 @@ def test_drelu_bitexact(dim, k):
     assert np.array_equal(to_np(idx).astype(np.int32), oi)
     assert np.array_equal(to_np(val), ov.astype(np.float32))
     assert np.array_equal(np.signbit(to_np(val)), np.signbit(ov))
+
+
+@pytest.mark.parametrize("dim,k", [(64, 8), (128, 16), (32, 4), (64, 32), (64, 2), (32, 16), (128, 4)])
+def test_drelu_thread_per_row_matches_warp_kernel(dim, k, knob):
+    """The thread-per-row network D-ReLU (composite keys truncated by log2(dim)
+    bits, exact rerun when the (k+1)-th shares the k-th's truncated key) gives
+    the warp-per-row kernel's output bit for bit, on rows built to hit the rerun:
+    values one ulp apart around the threshold, duplicated values, and a tail of
+    rows that is not a multiple of the 32-row staging group."""
+    rng = np.random.default_rng(dim + 7 * k)
+    n = 4133
+    x = rng.standard_normal((n, dim)).astype(np.float32)
+    for r in range(0, 600):                   # near-ties: neighbours of the k-th value
+        row = np.sort(x[r])[::-1]
+        t = row[k - 1]
+        j = rng.choice(dim, size=3, replace=False)
+        x[r, j[0]] = np.nextafter(t, np.float32(np.inf))
+        x[r, j[1]] = np.nextafter(t, np.float32(-np.inf))
+        x[r, j[2]] = t
+    x[600:900] = np.round(x[600:900] * 2) / 2      # many exact duplicates
+    xg = cuda(x)
+    out = {}
+    for mode in (0, 2):                       # 2: the network kernel for every supported shape
+        knob("drelu_tpr", mode, 1)
+        v, i = dr.drelu_topk(xg, k)
+        vs, is_ = dr.drelu_topk_sorted(xg, k) if k <= 32 else (None, None)
+        torch.cuda.synchronize()
+        out[mode] = (to_np(v), to_np(i), None if vs is None else to_np(vs), None if is_ is None else to_np(is_))
+    for a, b in zip(out[0], out[2]):
+        if a is not None:
+            assert np.array_equal(a, b)
+    oi, ov = O.drelu(x.astype(np.float64), k)
+    assert np.array_equal(out[2][1].astype(np.int32), oi)
 
 
 def test_drelu_strided_rows():
