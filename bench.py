@@ -313,15 +313,58 @@ def c5_batch_design(ids, designs):
     return u
 
 
-def oracle_grads_flat(dr, d, P, nl, k):
+def gpu_decisions(dr, torch, g, d, P, nl, D, k, dev):
+    """The integer decisions the GPU step takes in fp32 (DESIGN reading Q28): per
+    layer the D-ReLU selections of both node types and the max-merge mask, read
+    from the layer ABI's tapes (the same kernels, bit-identical to the trainer's
+    fused path: tests/test_gpu_chain.py)."""
+    out = []
+    xc = torch.as_tensor(d.x_cell).to(dev)
+    xn = torch.as_tensor(d.x_net).to(dev)
+    dc, dn = d.x_cell.shape[1], d.x_net.shape[1]
+    for l in range(nl):
+        W = {kk.split(".", 1)[1]: torch.as_tensor(v).to(dev) for kk, v in P.items()
+             if kk.startswith(f"l{l}.")}
+        L = dr.Layer(W, dc, dn, D, k, k)
+        yc, yn, tape = dr.heteroconv_fwd(g, L, xc, xn)
+        v = dr.tape_view(g, L, tape)
+        words = v["mask"].cpu().numpy().view(np.uint32)
+        bits = (words[:, :, None] >> np.arange(32, dtype=np.uint32)[None, None, :]) & 1
+        out.append(dict(hc_idx=v["hc_idx"].cpu().numpy().astype(np.int32),
+                        hn_idx=v["hn_idx"].cpu().numpy().astype(np.int32),
+                        M=bits.reshape(words.shape[0], -1)[:, :D].astype(bool)))
+        xc, xn, dc, dn = yc, yn, D, D
+    return out
+
+
+def oracle_grads_flat(dr, d, P, nl, k, forced=None):
+    """fp64 oracle loss and flat gradient; with `forced` the GPU's fp32 decisions
+    are fed in (reading Q28) and their validity against the oracle's own values
+    is returned as well."""
     from oracle import oracle as O
     G = O.OGraph(d)
-    loss, og, _ = O.model_fwd_bwd(G, {kk: np.asarray(v, np.float64) for kk, v in P.items()},
-                                  nl, k, k, d.x_cell, d.x_net, d.labels)
-    return loss, np.concatenate([np.asarray(og[f"l{l}.{kk}"], np.float64).reshape(-1)
-                                 for l in range(nl) for kk in dr.PARAM_ORDER] +
-                                [np.asarray(og["head.w"], np.float64).reshape(-1),
-                                 np.asarray(og["head.b"], np.float64).reshape(-1)])
+    loss, og, tapes = O.model_fwd_bwd(G, {kk: np.asarray(v, np.float64) for kk, v in P.items()},
+                                      nl, k, k, d.x_cell, d.x_net, d.labels, forced=forced)
+    flat = np.concatenate([np.asarray(og[f"l{l}.{kk}"], np.float64).reshape(-1)
+                           for l in range(nl) for kk in dr.PARAM_ORDER] +
+                          [np.asarray(og["head.w"], np.float64).reshape(-1),
+                           np.asarray(og["head.b"], np.float64).reshape(-1)])
+    valid = None
+    if forced is not None:
+        valid = {"drelu_gap_min": float("inf"), "merge_gap_min": float("inf"),
+                 "rows_decided_differently": 0, "rows": 0}
+        for t in tapes:
+            for x, idx in ((t["x_c"], t["hc_idx"]), (t["x_n"], t["hn_idx"])):
+                gap = O.drelu_gap(x, idx)
+                valid["drelu_gap_min"] = min(valid["drelu_gap_min"], float(gap.min()))
+                own, _ = O.drelu(x, idx.shape[1])
+                valid["rows_decided_differently"] += int(np.any(own != idx, axis=1).sum())
+                valid["rows"] += int(x.shape[0])
+            mg = O.merge_gap(t["y_near"], t["y_pinned"], t["M"])
+            valid["merge_gap_min"] = min(valid["merge_gap_min"], float(mg.min()))
+            valid["rows_decided_differently"] += int(np.any(t["M"] != (t["y_near"] >= t["y_pinned"]),
+                                                            axis=1).sum())
+    return loss, flat, valid
 
 
 def row_err(gpu, ref):
@@ -519,10 +562,11 @@ def run_c5(args, torch, dist, dr, rank, world, local, dev, hbm, bf16, src):
 
     # ---- P2/P3 parity at full size: the step-0 allreduced gradient vs the mean of
     # the fp64 oracle gradients of every rank's batch (O8), at the initial params,
-    # free-running (rows whose top-k or merge gap is below fp32 resolution are not
-    # excluded here; the teacher-forced checks are tests/test_gpu_*.py)
+    # the oracle fed the GPU's fp32 decisions (D-ReLU selections, merge masks;
+    # reading Q28), each checked to be a valid decision of the oracle's own values
     t0 = time.time()
-    oloss, og = oracle_grads_flat(dr, bd[0], P, nl, k)
+    forced = gpu_decisions(dr, torch, graphs[0], bd[0], P, nl, D, k, dev)
+    oloss, og, valid = oracle_grads_flat(dr, bd[0], P, nl, k, forced=forced)
     og_t = torch.as_tensor(og, device=dev)
     ol_t = torch.tensor([oloss], dtype=torch.float64, device=dev)
     if world > 1:
@@ -538,8 +582,13 @@ def run_c5(args, torch, dist, dr, rank, world, local, dev, hbm, bf16, src):
     dp["oracle_grad_row_err_max"] = worst
     dp["oracle_grad_row_err_worst_tensor"] = worst_key
     dp["oracle_grad_tolerance"] = 1e-4
-    dp["oracle_note"] = ("free-running fp32 GPU vs fp64 oracle at full batch size, max over "
-                         "parameter tensors of the row-normalised error (SURVEY §8(c))")
+    dp["oracle_note"] = ("fp32 GPU step-0 gradient vs the fp64 oracle fed the GPU's fp32 "
+                         "decisions (reading Q28), full batch, max over parameter tensors of the "
+                         "row-normalised error (SURVEY §8(c)); decisions valid iff both gap "
+                         "minima >= -1e-5")
+    dp["decisions"] = valid
+    dp["decisions_valid"] = bool(valid["drelu_gap_min"] >= -1e-5 and valid["merge_gap_min"] >= -1e-5)
+    dp["oracle_grad_ok"] = bool(worst <= 1e-4)
     dp["oracle_s"] = round(time.time() - t0, 2)
 
     table = kernel_table(prof, bd[0], D, k, "C5", tiled=graphs[0].info()["tiles"][0] > 0)

@@ -203,6 +203,10 @@ typedef struct {
 
 #define DR_FWD_SEQUENTIAL 1u  /* run the three relations on one stream (§4.4 breakdown)    */
 #define DR_FWD_TAPS 2u        /* also keep Y_near / Y_pinned for teacher-forced parity      */
+#define DR_FWD_INPUT_IN_TAPE 4u /* dr_heteroconv_fwd_chain: H_c / H_n are already in the tape */
+#define DR_FWD_Y_SCRATCH 8u   /* dr_heteroconv_fwd_chain: y_cell / y_net may be left unwritten */
+#define DR_FWD_NO_NET_OUT 16u /* Y_net not needed (last layer): no pins SpMM / net projection;
+                                 y_net unwritten; the backward takes dy_net = NULL (zero) */
 
 /* Bytes of the caller-allocated tape (forward activations reused by the
  * backward: CBSR of both types, Z_psi, merge-mask bits, taps) plus backward
@@ -212,10 +216,35 @@ dr_status dr_heteroconv_tape_bytes(const dr_graph *g, const dr_layer *L, uint32_
 dr_status dr_heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *x_cell,
                             const float *x_net, float *y_cell, float *y_net, void *tape,
                             uint32_t flags, void *stream);
+/* Layer forward with the NEXT layer's D-ReLU fused into this layer's projection
+ * epilogue (row a5; Eq. 2-3, applied to this layer's output, which
+ * is the next layer's input: "D-ReLU ... after the activation layer").
+ * Same as dr_heteroconv_fwd, plus:
+ *   next_L / next_tape (both or neither): the projection epilogues write
+ *     drelu(Y_cell, next_L->k_cell) and drelu(Y_net, next_L->k_net) -- exactly
+ *     k per row, ties to the lowest column, values verbatim, ascending indices;
+ *     bit-identical to dr_drelu_topk on the written Y -- straight into
+ *     next_tape's H_c / H_n (next_tape laid out for next_L with next_flags), so
+ *     the next layer runs with DR_FWD_INPUT_IN_TAPE and Y is never re-read.
+ *     next_L->d_cell == next_L->d_net == L->d_out (DR_ERR_SHAPE_MISMATCH);
+ *     next_L->k_pins must be 0 or k_cell (DR_ERR_UNSUPPORTED).
+ *   flags & DR_FWD_INPUT_IN_TAPE: this layer's H_c / H_n were written into
+ *     `tape` by the previous layer's chained call; x_cell / x_net are ignored
+ *     (may be NULL); L->k_pins must be 0 or k_cell.
+ *   flags & DR_FWD_Y_SCRATCH: the caller does not need Y: where the epilogue
+ *     is fused (k in {4, 8, 16, 32}, k <= d_out) y_cell / y_net are left
+ *     unwritten; otherwise they are written and D-ReLU'd by a separate launch.
+ *     y_cell / y_net must still be valid (n x d_out) buffers. */
+dr_status dr_heteroconv_fwd_chain(const dr_graph *g, const dr_layer *L, const float *x_cell,
+                                  const float *x_net, float *y_cell, float *y_net, void *tape,
+                                  uint32_t flags, const dr_layer *next_L, void *next_tape,
+                                  uint32_t next_flags, void *stream);
 /* Backward (Eq. 10-14, Alg. 2): mask routing, dW = Z^T dY, dWr = H^T dY, db,
  * dZ = dY Wn^T, SSpMM per source type (cell: near + pins + root term; net:
  * pinned + root term) and the D-ReLU mask scatter. dx_cell == NULL and
- * dx_net == NULL skip the SSpMM (first layer). grads are overwritten. */
+ * dx_net == NULL skip the SSpMM (first layer). grads are overwritten.
+ * dy_net == NULL means dY_net = 0 (after a DR_FWD_NO_NET_OUT forward): the
+ * pins relation's terms are skipped and its gradients written as zeros. */
 dr_status dr_heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape,
                             const float *dy_cell, const float *dy_net, float *dx_cell,
                             float *dx_net, dr_layer_grad *grads, uint32_t flags, void *stream);

@@ -186,7 +186,53 @@ def layer_params(P, l):
     return {k.split(".", 1)[1]: _f64(v) for k, v in P.items() if k.startswith(f"l{l}.")}
 
 
-def layer_fwd(G, W, x_c, x_n, k_c, k_n, merge="max", root=True, k_p=None):
+def drelu_forced(x, idx):
+    """D-ReLU with the selection DECIDED ELSEWHERE (teacher forcing, DESIGN.md
+    reading Q28): the kept columns are `idx` (n x k, ascending), the values are
+    this oracle's own x at them, verbatim (Eq. 3). Used where the decision is
+    taken in fp32 on the kernel's own output (a near-tie at fp32 resolution)
+    and validated separately by drelu_gap."""
+    x = _f64(x)
+    idx = np.asarray(idx, np.int32)
+    if idx.ndim != 2 or idx.shape[0] != x.shape[0]:
+        raise ValueError("ShapeMismatch: idx rows != x rows")
+    if idx.size and (idx.min() < 0 or idx.max() >= x.shape[1] or np.any(np.diff(idx, axis=1) <= 0)):
+        raise ValueError("forced idx must be ascending distinct columns in range")
+    return idx, gather_at(x, idx)
+
+
+def drelu_gap(x, idx):
+    """Per row: (smallest kept value - largest dropped value) / ||x_row||_2.
+    >= 0 iff idx is a valid top-k of the row (Eq. 2); rows with nothing dropped
+    give +inf, all-zero rows use norm 1. The parity protocol accepts a forced
+    selection when every gap >= -1e-5 (SURVEY §8(c) P2 near-tie band)."""
+    x = _f64(x)
+    n, d = x.shape
+    keep = np.zeros((n, d), bool)
+    if n:
+        keep[np.arange(n)[:, None], np.asarray(idx, np.int64)] = True
+    kept_min = np.where(keep, x, np.inf).min(axis=1)
+    drop_max = np.where(keep, -np.inf, x).max(axis=1)
+    nrm = np.linalg.norm(x, axis=1)
+    nrm = np.where(nrm > 0, nrm, 1.0)
+    return (kept_min - drop_max) / nrm
+
+
+def merge_gap(y_near, y_pinned, M):
+    """Per row: the most negative (chosen - other) margin of the max-merge mask
+    M (Eq. 8, 14) divided by the row norm of max(y_near, y_pinned); >= 0 iff M
+    is the exact mask up to ties (tie -> near). Used like drelu_gap."""
+    yn, yp = _f64(y_near), _f64(y_pinned)
+    M = np.asarray(M, bool)
+    marg = np.where(M, yn - yp, yp - yn)
+    nrm = np.linalg.norm(np.maximum(yn, yp), axis=1)
+    nrm = np.where(nrm > 0, nrm, 1.0)
+    if marg.shape[1] == 0:
+        return np.full(marg.shape[0], np.inf)
+    return marg.min(axis=1) / nrm
+
+
+def layer_fwd(G, W, x_c, x_n, k_c, k_n, merge="max", root=True, k_p=None, forced=None):
     """One HeteroConv layer (Eq. 2-9):
        H = drelu(X) per node type (Eq. 2-3)
        Z_psi = SpMM_psi(H_src)          (Eq. 5-7, three relations)
@@ -197,11 +243,21 @@ def layer_fwd(G, W, x_c, x_n, k_c, k_n, merge="max", root=True, k_p=None):
        Y_pinned = Z_pinned W + b        (GraphConv both)
        Y_net = Z_pins Wn + H_n Wr + b   (SageConv mean)
        Y_cell = max(Y_near, Y_pinned), M = [Y_near >= Y_pinned]  (Eq. 8, 14; Q3, Q4)
+    forced (teacher forcing, reading Q28): optional dict with "hc_idx" / "hn_idx"
+    (the D-ReLU selections) and / or "M" (the merge mask) decided elsewhere; the
+    arithmetic is unchanged, only those integer decisions are taken as given.
     """
     x_c, x_n = _f64(x_c), _f64(x_n)
     d_c, d_n = x_c.shape[1], x_n.shape[1]
-    hc_idx, hc_val = drelu(x_c, k_c)
-    hn_idx, hn_val = drelu(x_n, k_n)
+    forced = forced or {}
+    if "hc_idx" in forced:
+        hc_idx, hc_val = drelu_forced(x_c, forced["hc_idx"])
+    else:
+        hc_idx, hc_val = drelu(x_c, k_c)
+    if "hn_idx" in forced:
+        hn_idx, hn_val = drelu_forced(x_n, forced["hn_idx"])
+    else:
+        hn_idx, hn_val = drelu(x_n, k_n)
     Hc = densify(hc_idx, hc_val, d_c)
     Hn = densify(hn_idx, hn_val, d_n)
     z_near = G.fwd("near", hc_idx, hc_val, d_c)
@@ -218,14 +274,15 @@ def layer_fwd(G, W, x_c, x_n, k_c, k_n, merge="max", root=True, k_p=None):
         y_net = y_net + Hn @ W["wr_pins"]
     y_pinned = z_pinned @ W["w_pinned"] + W["b_pinned"]
     if merge == "max":
-        M = y_near >= y_pinned
+        M = np.asarray(forced["M"], bool) if "M" in forced else y_near >= y_pinned
         y_cell = np.where(M, y_near, y_pinned)
     elif merge == "sum":                      # Eq. 6 variant
         M = None
         y_cell = y_near + y_pinned
     else:
         raise ValueError(merge)
-    tape = dict(hc_idx=hc_idx, hc_val=hc_val, hn_idx=hn_idx, hn_val=hn_val, Hc=Hc, Hn=Hn,
+    tape = dict(x_c=x_c, x_n=x_n,
+                hc_idx=hc_idx, hc_val=hc_val, hn_idx=hn_idx, hn_val=hn_val, Hc=Hc, Hn=Hn,
                 hp_idx=hp_idx, hp_val=hp_val,
                 z_near=z_near, z_pins=z_pins, z_pinned=z_pinned, y_near=y_near,
                 y_pinned=y_pinned, M=M, d_c=d_c, d_n=d_n, merge=merge, root=root)
@@ -306,15 +363,18 @@ def adam(theta, grad, m, v, step, lr=2e-4, wd=1e-5, b1=0.9, b2=0.999, eps=1e-8):
 
 
 # ------------------------------------------------------------------ model
-def model_fwd_bwd(G, P, n_layers, k_c, k_n, x_c, x_n, labels, merge="max", k_p=None):
+def model_fwd_bwd(G, P, n_layers, k_c, k_n, x_c, x_n, labels, merge="max", k_p=None,
+                  forced=None):
     """2-layer model: layers -> head/MSE -> backward; the first
     layer's SSpMM is skipped (input features need no gradient). Returns
-    (loss, grads dict keyed like P, tapes)."""
+    (loss, grads dict keyed like P, tapes). forced: None or one layer_fwd
+    `forced` dict (or None) per layer (teacher forcing, reading Q28)."""
     tapes, Ws = [], []
     hc, hn = _f64(x_c), _f64(x_n)
     for l in range(n_layers):
         W = layer_params(P, l)
-        hc, hn, tape = layer_fwd(G, W, hc, hn, k_c, k_n, merge=merge, k_p=k_p)
+        fl = forced[l] if forced is not None else None
+        hc, hn, tape = layer_fwd(G, W, hc, hn, k_c, k_n, merge=merge, k_p=k_p, forced=fl)
         tapes.append(tape)
         Ws.append(W)
     loss, hg, dy_c = head_mse(hc, P["head.w"], P["head.b"], labels)

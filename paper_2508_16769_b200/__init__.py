@@ -12,7 +12,8 @@ import ctypes as C
 
 import numpy as np
 
-from ._lib import (DR_FWD_SEQUENTIAL, DR_FWD_TAPS, DR_GRAPH_ORDER_IDENTITY,  # noqa: F401
+from ._lib import (DR_FWD_SEQUENTIAL, DR_FWD_TAPS, DR_FWD_INPUT_IN_TAPE,  # noqa: F401
+                   DR_FWD_Y_SCRATCH, DR_GRAPH_ORDER_IDENTITY,  # noqa: F401
                    DR_GRAPH_SKIP_VALIDATION, DR_GRAPHCONV_SYM, DR_MERGE_MAX, DR_MERGE_SUM,
                    DR_NEAR, DR_PINNED, DR_PINS, DR_SAGE_MEAN, DRError, EXPORTS, check,
                    dr_cbsr, dr_layer, dr_layer_grad, dr_rel_desc, dr_tape_view, dr_train_cfg,
@@ -425,6 +426,30 @@ def heteroconv_fwd(g, layer, x_cell, x_net, flags=0, tape=None, stream=None):
     check(lib().dr_heteroconv_fwd(g.handle, C.byref(layer.c), _ptr(x_cell), _ptr(x_net),
                                   _ptr(y_cell), _ptr(y_net), _ptr(tape), flags, _stream(stream)))
     return y_cell, y_net, tape
+
+
+def heteroconv_fwd_chain(g, layer, x_cell, x_net, next_layer=None, next_tape=None, flags=0,
+                         next_flags=0, tape=None, stream=None):
+    """dr_heteroconv_fwd_chain: the layer forward with the next layer's D-ReLU fused
+    into the projection epilogue (row a5). x_cell / x_net may be None with
+    DR_FWD_INPUT_IN_TAPE (the layer's CBSR inputs are already in `tape`). Returns
+    (y_cell, y_net, tape, next_tape); a next tape is allocated when next_layer is
+    given without one."""
+    torch = _torch()
+    dev = (x_cell if x_cell is not None else tape).device
+    D = layer.c.d_out
+    y_cell = torch.empty((g.n_cell, D), device=dev, dtype=torch.float32)
+    y_net = torch.empty((g.n_net, D), device=dev, dtype=torch.float32)
+    if tape is None:
+        tape = torch.empty(layer.tape_bytes(g, flags), device=dev, dtype=torch.uint8)
+    if next_layer is not None and next_tape is None:
+        next_tape = torch.empty(next_layer.tape_bytes(g, next_flags), device=dev, dtype=torch.uint8)
+    nl = C.byref(next_layer.c) if next_layer is not None else None
+    check(lib().dr_heteroconv_fwd_chain(
+        g.handle, C.byref(layer.c), _ptr(x_cell) if x_cell is not None else None,
+        _ptr(x_net) if x_net is not None else None, _ptr(y_cell), _ptr(y_net), _ptr(tape), flags,
+        nl, _ptr(next_tape) if next_tape is not None else None, next_flags, _stream(stream)))
+    return y_cell, y_net, tape, next_tape
 
 
 def tape_view(g, layer, tape, flags=0):

@@ -25,6 +25,8 @@ DR_GRAPH_SKIP_VALIDATION = 1
 DR_GRAPH_ORDER_IDENTITY = 2
 DR_FWD_SEQUENTIAL = 1
 DR_FWD_TAPS = 2
+DR_FWD_INPUT_IN_TAPE = 4
+DR_FWD_Y_SCRATCH = 8
 
 P = C.c_void_p
 
@@ -121,6 +123,8 @@ _SIGS = {
     "dr_heteroconv_tape_bytes": (C.c_int, [P, C.POINTER(dr_layer), C.c_uint32,
                                            C.POINTER(C.c_size_t)]),
     "dr_heteroconv_fwd": (C.c_int, [P, C.POINTER(dr_layer), P, P, P, P, P, C.c_uint32, P]),
+    "dr_heteroconv_fwd_chain": (C.c_int, [P, C.POINTER(dr_layer), P, P, P, P, P, C.c_uint32,
+                                          P, P, C.c_uint32, P]),
     "dr_heteroconv_bwd": (C.c_int, [P, C.POINTER(dr_layer), P, P, P, P, P,
                                     C.POINTER(dr_layer_grad), C.c_uint32, P]),
     "dr_heteroconv_tape_view": (C.c_int, [P, C.POINTER(dr_layer), P, C.c_uint32,

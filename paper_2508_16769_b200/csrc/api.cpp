@@ -247,9 +247,34 @@ static void check_layer(const dr_graph *g, const dr_layer *L) {
 static bool z_split_ok(const dr_layer *, int) { return false; }
 
 // ------------------------------------------------------------------ layer forward / backward
+// Ln / tape_next (row a5): the next layer and its tape; when given, the
+// projection epilogues also write the next layer's input CBSR (Eq. 2-3 on Y_cell
+// after the merge and on Y_net) into tape_next (flags_next = that tape's flags).
+// DR_FWD_INPUT_IN_TAPE: this layer's H_c / H_n are already in `tape` (written so
+// by the previous layer); its own D-ReLU launches are skipped.
+// DR_FWD_Y_SCRATCH: y_cell / y_net need not be written when the fused epilogue
+// covers the shape (they are still written, and D-ReLU'd standalone, otherwise).
 static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc, const float *xn,
-                           float *yc, float *yn, void *tape, uint32_t flags, cudaStream_t st) {
+                           float *yc, float *yn, void *tape, uint32_t flags, cudaStream_t st,
+                           const dr_layer *Ln = nullptr, void *tape_next = nullptr,
+                           uint32_t flags_next = 0) {
     const TapeLayout T = tape_layout(g, L, flags);
+    const bool in_tape = (flags & DR_FWD_INPUT_IN_TAPE) != 0;
+    TapeLayout TN{};
+    char *tn = (char *)tape_next;
+    if (Ln) TN = tape_layout(g, Ln, flags_next);
+    // fused next-layer D-ReLU per output type, or the standalone fallback
+    const bool fuse_c = Ln && tc2_next_drelu_supported(kEpi2Fwd, L->d_out, Ln->k_cell);
+    const bool fuse_n = Ln && tc2_next_drelu_supported(kEpi2Fwd, L->d_out, Ln->k_net);
+    const bool y_scratch = (flags & DR_FWD_Y_SCRATCH) != 0;
+    // DR_FWD_NO_NET_OUT: Y_net feeds nothing (the last layer: the head reads
+    // cells only, Q14) -- the pins SpMM and the net projection are not run
+    const bool no_net = (flags & DR_FWD_NO_NET_OUT) != 0;
+    DR_CHECK(!no_net || !Ln, DR_ERR_INVALID_ARGUMENT, "DR_FWD_NO_NET_OUT with a next layer");
+    DR_CHECK(!in_tape || !pins_own(L), DR_ERR_UNSUPPORTED,
+             "DR_FWD_INPUT_IN_TAPE with k_pins: pins' own CBSR needs the dense input");
+    DR_CHECK(!Ln || !pins_own(Ln), DR_ERR_UNSUPPORTED,
+             "chained forward into a layer with k_pins: its pins CBSR needs the dense input");
     char *tp = (char *)tape;
     float *hcv = (float *)(tp + T.hc_val), *hnv = (float *)(tp + T.hn_val);
     uint8_t *hci = (uint8_t *)(tp + T.hc_idx), *hni = (uint8_t *)(tp + T.hn_idx);
@@ -258,6 +283,81 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
     const int kp = k_pins_of(L);
     float *z[3];
     for (int r = 0; r < 3; ++r) z[r] = (float *)(tp + T.z[r]);
+    const int nc = g->n_cell, nn = g->n_net;
+    bool zs[3];
+    for (int r = 0; r < 3; ++r) zs[r] = z_split_ok(L, r);
+    // ---- the two projections (tensor-core row GEMMs when the shapes allow) and
+    // their packed weight images, packed by ONE launch before the streams fork
+    Tc2RowsDesc dnet, dcell;
+    {   // net: Y_net = Z_pins Wn_pins + densify(H_n) Wr_pins + b_pins   (Eq. 7, 9)
+        Tc2RowsDesc &d = dnet;
+        d.n = nn; d.N = L->d_out; d.G = 1; d.epi = kEpi2Fwd;
+        d.nseg[0] = L->wr[DR_PINS] ? 2 : 1;
+        d.seg[0][0].A = z[DR_PINS]; d.seg[0][0].K = L->d_cell; d.seg[0][0].split = zs[DR_PINS];
+        d.seg[0][1].hval = hnv; d.seg[0][1].hidx = hni; d.seg[0][1].k = L->k_net;
+        d.seg[0][1].K = L->d_net;
+        d.bimg[0] = (uint8_t *)(tp + T.img_fn); d.bias[0] = L->b[DR_PINS];
+        d.y = yn;
+        if (fuse_n) {
+            d.next_k = Ln->k_net;
+            d.next_val = (float *)(tn + TN.hn_val);
+            d.next_idx = (uint8_t *)(tn + TN.hn_idx);
+            if (y_scratch) d.y = nullptr;
+        }
+        if (!tc2_rows_supported(d)) {          // dense y + standalone D-ReLU
+            d.next_k = 0;
+            d.y = yn;
+        }
+    }
+    {   // cell: Y_cell = max(Y_near, Y_pinned), M   (Eq. 6, 8, 14)
+        Tc2RowsDesc &d = dcell;
+        d.n = nc; d.N = L->d_out; d.G = 2; d.epi = kEpi2Fwd;
+        d.nseg[0] = L->wr[DR_NEAR] ? 2 : 1;
+        d.seg[0][0].A = z[DR_NEAR]; d.seg[0][0].K = L->d_cell; d.seg[0][0].split = zs[DR_NEAR];
+        d.seg[0][1].hval = hcv; d.seg[0][1].hidx = hci; d.seg[0][1].k = L->k_cell;
+        d.seg[0][1].K = L->d_cell;
+        d.nseg[1] = 1;
+        d.seg[1][0].A = z[DR_PINNED]; d.seg[1][0].K = L->d_net; d.seg[1][0].split = zs[DR_PINNED];
+        d.bimg[0] = (uint8_t *)(tp + T.img_fa); d.bimg[1] = (uint8_t *)(tp + T.img_fb);
+        d.bias[0] = L->b[DR_NEAR]; d.bias[1] = L->b[DR_PINNED];
+        d.merge = L->merge;
+        d.y = yc; d.mask_out = (uint32_t *)(tp + T.mask);
+        d.tap_a = (flags & DR_FWD_TAPS) ? (float *)(tp + T.tap_a) : nullptr;
+        d.tap_b = (flags & DR_FWD_TAPS) ? (float *)(tp + T.tap_b) : nullptr;
+        if (fuse_c) {
+            d.next_k = Ln->k_cell;
+            d.next_val = (float *)(tn + TN.hc_val);
+            d.next_idx = (uint8_t *)(tn + TN.hc_idx);
+            if (y_scratch) d.y = nullptr;
+        }
+        if (!tc2_rows_supported(d)) {
+            d.next_k = 0;
+            d.y = yc;
+        }
+    }
+    const bool net_tc = !no_net && nn > 0 && tc2_rows_supported(dnet);
+    const bool cell_tc = nc > 0 && tc2_rows_supported(dcell);
+    {
+        Tc2PackJob jobs[kMaxPackJobs];
+        int nj = 0;
+        auto job = [&](const float *W, int K, uint8_t *img) {   // B_op[n][kk] = W[kk][n]
+            Tc2PackJob &j = jobs[nj++];
+            j.W = W; j.ldw = L->d_out; j.K = K; j.NB = L->d_out; j.n0 = 0; j.Ntot = L->d_out;
+            j.transpose = 1; j.img = img;
+        };
+        if (net_tc) {
+            job(L->wn[DR_PINS], L->d_cell, (uint8_t *)dnet.bimg[0]);
+            if (L->wr[DR_PINS])
+                job(L->wr[DR_PINS], L->d_net, (uint8_t *)dnet.bimg[0] + tc2_bimg_bytes(L->d_cell, L->d_out));
+        }
+        if (cell_tc) {
+            job(L->wn[DR_NEAR], L->d_cell, (uint8_t *)dcell.bimg[0]);
+            if (L->wr[DR_NEAR])
+                job(L->wr[DR_NEAR], L->d_cell, (uint8_t *)dcell.bimg[0] + tc2_bimg_bytes(L->d_cell, L->d_out));
+            job(L->wn[DR_PINNED], L->d_net, (uint8_t *)dcell.bimg[1]);
+        }
+        launch_tc2_pack_b_multi(jobs, nj, st);
+    }
     const bool seq = (flags & DR_FWD_SEQUENTIAL) != 0 || force_sequential();
     StreamCtx &C = ctx();
     cudaStream_t s0 = seq ? st : C.s[0], s1 = seq ? st : C.s[1], s2 = seq ? st : C.s[2];
@@ -265,13 +365,10 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
         DR_CUDA(cudaEventRecord(C.fork, st));
         for (int q = 0; q < 3; ++q) DR_CUDA(cudaStreamWaitEvent(C.s[q], C.fork, 0));
     }
-    const int nc = g->n_cell, nn = g->n_net;
-    { TagScope t("cell"); launch_drelu(xc, nc, L->d_cell, L->d_cell, L->k_cell, hcv, hci, s0); }  // Eq. 2-3
+    if (!in_tape) { TagScope t("cell"); launch_drelu(xc, nc, L->d_cell, L->d_cell, L->k_cell, hcv, hci, s0); }  // Eq. 2-3
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[0], s0));                               // H_c ready
-    { TagScope t("net"); launch_drelu(xn, nn, L->d_net, L->d_net, L->k_net, hnv, hni, s2); }
+    if (!in_tape) { TagScope t("net"); launch_drelu(xn, nn, L->d_net, L->d_net, L->k_net, hnv, hni, s2); }
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[1], s2));                               // H_n ready
-    bool zs[3];
-    for (int r = 0; r < 3; ++r) zs[r] = z_split_ok(L, r);
     { TagScope t("near"); launch_spmm_fwd(g->rel[DR_NEAR], hcv, hci, L->k_cell, L->d_cell, z[DR_NEAR], s0, zs[DR_NEAR]); }  // Eq. 5-7
     if (pins_own(L)) {          // Q27: pins' own cell CBSR, on its own stream
         TagScope t("pins");
@@ -279,27 +376,14 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
     } else if (!seq) {
         DR_CUDA(cudaStreamWaitEvent(s1, C.ev[0], 0));
     }
-    { TagScope t("pins"); launch_spmm_fwd(g->rel[DR_PINS], hpv, hpi, kp, L->d_cell, z[DR_PINS], s1, zs[DR_PINS]); }
+    if (!no_net) { TagScope t("pins"); launch_spmm_fwd(g->rel[DR_PINS], hpv, hpi, kp, L->d_cell, z[DR_PINS], s1, zs[DR_PINS]); }
     { TagScope t("pinned"); launch_spmm_fwd(g->rel[DR_PINNED], hnv, hni, L->k_net, L->d_net, z[DR_PINNED], s2, zs[DR_PINNED]); }
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[2], s2));                               // Z_pinned ready
     if (!seq) DR_CUDA(cudaStreamWaitEvent(s1, C.ev[1], 0));
-    {   // net: Y_net = Z_pins Wn_pins + densify(H_n) Wr_pins + b_pins   (Eq. 7, 9)
+    if (!no_net) {   // net: Y_net = Z_pins Wn_pins + densify(H_n) Wr_pins + b_pins   (Eq. 7, 9)
         TagScope t("net");
-        Tc2RowsDesc d;
-        uint8_t *img = (uint8_t *)(tp + T.img_fn);
-        d.n = nn; d.N = L->d_out; d.G = 1; d.epi = kEpi2Fwd;
-        d.nseg[0] = L->wr[DR_PINS] ? 2 : 1;
-        d.seg[0][0].A = z[DR_PINS]; d.seg[0][0].K = L->d_cell; d.seg[0][0].split = zs[DR_PINS];
-        d.seg[0][1].hval = hnv; d.seg[0][1].hidx = hni; d.seg[0][1].k = L->k_net;
-        d.seg[0][1].K = L->d_net;
-        d.bimg[0] = img; d.bias[0] = L->b[DR_PINS];
-        d.y = yn;
-        if (tc2_rows_supported(d)) {
-            launch_tc2_pack_b(L->wn[DR_PINS], L->d_out, L->d_cell, L->d_out, 0, L->d_out, true, img, s1);
-            if (L->wr[DR_PINS])
-                launch_tc2_pack_b(L->wr[DR_PINS], L->d_out, L->d_net, L->d_out, 0, L->d_out, true,
-                                  img + tc2_bimg_bytes(L->d_cell, L->d_out), s1);
-            launch_tc2_rows(d, s1);
+        if (net_tc) {
+            launch_tc2_rows(dnet, s1);
         } else {
             ProjFwdArgs a;
             a.n = nn; a.Ka = L->d_cell; a.N = L->d_out;
@@ -309,33 +393,15 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
             DR_CHECK(!zs[DR_PINS], DR_ERR_UNSUPPORTED, "projection: split Z needs tc2");
             launch_proj_fwd(a, s1);
         }
+        if (Ln && !dnet.next_k)                 // next layer's H_n from the dense Y_net
+            launch_drelu(yn, nn, L->d_out, L->d_out, Ln->k_net, (float *)(tn + TN.hn_val),
+                         (uint8_t *)(tn + TN.hn_idx), s1);
     }
     if (!seq) DR_CUDA(cudaStreamWaitEvent(s0, C.ev[2], 0));
     {   // cell: Y_cell = max(Y_near, Y_pinned), M   (Eq. 6, 8, 14)
         TagScope t("cell");
-        float *tap_a = (flags & DR_FWD_TAPS) ? (float *)(tp + T.tap_a) : nullptr;
-        float *tap_b = (flags & DR_FWD_TAPS) ? (float *)(tp + T.tap_b) : nullptr;
-        uint8_t *ia = (uint8_t *)(tp + T.img_fa), *ib = (uint8_t *)(tp + T.img_fb);
-        Tc2RowsDesc d;
-        d.n = nc; d.N = L->d_out; d.G = 2; d.epi = kEpi2Fwd;
-        d.nseg[0] = L->wr[DR_NEAR] ? 2 : 1;
-        d.seg[0][0].A = z[DR_NEAR]; d.seg[0][0].K = L->d_cell; d.seg[0][0].split = zs[DR_NEAR];
-        d.seg[0][1].hval = hcv; d.seg[0][1].hidx = hci; d.seg[0][1].k = L->k_cell;
-        d.seg[0][1].K = L->d_cell;
-        d.nseg[1] = 1;
-        d.seg[1][0].A = z[DR_PINNED]; d.seg[1][0].K = L->d_net; d.seg[1][0].split = zs[DR_PINNED];
-        d.bimg[0] = ia; d.bimg[1] = ib;
-        d.bias[0] = L->b[DR_NEAR]; d.bias[1] = L->b[DR_PINNED];
-        d.merge = L->merge;
-        d.y = yc; d.mask_out = (uint32_t *)(tp + T.mask);
-        d.tap_a = tap_a; d.tap_b = tap_b;
-        if (tc2_rows_supported(d)) {
-            launch_tc2_pack_b(L->wn[DR_NEAR], L->d_out, L->d_cell, L->d_out, 0, L->d_out, true, ia, s0);
-            if (L->wr[DR_NEAR])
-                launch_tc2_pack_b(L->wr[DR_NEAR], L->d_out, L->d_cell, L->d_out, 0, L->d_out, true,
-                                  ia + tc2_bimg_bytes(L->d_cell, L->d_out), s0);
-            launch_tc2_pack_b(L->wn[DR_PINNED], L->d_out, L->d_net, L->d_out, 0, L->d_out, true, ib, s0);
-            launch_tc2_rows(d, s0);
+        if (cell_tc) {
+            launch_tc2_rows(dcell, s0);
         } else {
             ProjFwdArgs a;
             a.n = nc; a.Ka = L->d_cell; a.Kb = L->d_net; a.N = L->d_out;
@@ -345,11 +411,14 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
             a.merge = L->merge;
             a.y = yc;
             a.mask = (uint32_t *)(tp + T.mask);
-            a.tap_a = tap_a;
-            a.tap_b = tap_b;
+            a.tap_a = dcell.tap_a;
+            a.tap_b = dcell.tap_b;
             DR_CHECK(!zs[DR_NEAR] && !zs[DR_PINNED], DR_ERR_UNSUPPORTED, "projection: split Z needs tc2");
             launch_proj_fwd(a, s0);
         }
+        if (Ln && !dcell.next_k)                // next layer's H_c from the dense Y_cell
+            launch_drelu(yc, nc, L->d_out, L->d_out, Ln->k_cell, (float *)(tn + TN.hc_val),
+                         (uint8_t *)(tn + TN.hc_idx), s0);
     }
     if (!seq) {
         wait_on(st, s0, C.ev[3]);
@@ -379,6 +448,42 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
     for (int q = 0; q < 3; ++q) work[q] = (float *)(tp + T.work[q]);
     const int mode_near = L->merge == DR_MERGE_MAX ? kMaskM : kMaskNone;        // Eq. 12
     const int mode_pinned = L->merge == DR_MERGE_MAX ? kMaskNotM : kMaskNone;   // Eq. 13
+    const int nc = g->n_cell, nn = g->n_net, D = L->d_out;
+    // ---- dZ' row GEMMs: descriptors and their packed weights (B_op[n][kk] = W[n][kk],
+    // Wn in columns [0, Kd), the Sage root weight Wr in [Kd, N)), one packing launch
+    const RelDev &rn = g->rel[DR_NEAR];
+    const bool near_tiled = dxc && !rn.ewT && rn.n_src == nc &&
+                            tspmm_supported(rn.tilesT, L->d_cell, L->k_cell);
+    Tc2RowsDesc dzd[3];
+    bool dz_tc[3] = {false, false, false};
+    if (dxc || dxn) {
+        Tc2PackJob jobs[kMaxPackJobs];
+        int nj = 0;
+        auto prep = [&](int r, int64_t n, int Kd, const float *dy, int mode, const float *W,
+                        const float *Wr, int Kr, const uint8_t *ridx, int rk, float *root,
+                        const float *c, bool split) {
+            Tc2RowsDesc &d = dzd[r];
+            d.n = n; d.N = Kd + (Wr ? Kr : 0); d.G = 1; d.epi = kEpi2Dz;
+            d.nseg[0] = 1;
+            d.seg[0][0].A = dy; d.seg[0][0].K = D; d.seg[0][0].mask_mode = mode;
+            d.mask_in = mask; d.mask_width = D;
+            d.bimg[0] = (uint8_t *)(tp + T.img_dz[r]); d.n_dz = Kd; d.crow = c; d.dz = dz[r];
+            d.dz_split = split;   // [hi | lo] bf16 rows for the tensor-core tiled SSpMM
+            if (Wr) { d.root_idx = ridx; d.root_k = rk; d.root = root; }
+            dz_tc[r] = n > 0 && tc2_rows_supported(d);
+            if (!dz_tc[r]) return;
+            jobs[nj++] = Tc2PackJob{W, D, D, Kd, 0, d.N, 0, (uint8_t *)d.bimg[0]};
+            if (Wr) jobs[nj++] = Tc2PackJob{Wr, D, D, Kr, Kd, d.N, 0, (uint8_t *)d.bimg[0]};
+        };
+        prep(DR_NEAR, nc, L->d_cell, dyc, mode_near, L->wn[DR_NEAR], L->wr[DR_NEAR], L->d_cell, hci,
+             L->k_cell, root_c, g->rel[DR_NEAR].c, near_tiled);
+        if (dyn)
+            prep(DR_PINS, nn, L->d_cell, dyn, kMaskNone, L->wn[DR_PINS], L->wr[DR_PINS], L->d_net,
+                 hni, L->k_net, root_n, g->rel[DR_PINS].c, false);
+        prep(DR_PINNED, nc, L->d_net, dyc, mode_pinned, L->wn[DR_PINNED], nullptr, 0, nullptr, 0,
+             nullptr, g->rel[DR_PINNED].c, false);
+        launch_tc2_pack_b_multi(jobs, nj, st);
+    }
     const bool seq = (flags & DR_FWD_SEQUENTIAL) != 0 || force_sequential();
     StreamCtx &C = ctx();
     cudaStream_t s0 = seq ? st : C.s[0], s1 = seq ? st : C.s[1], s2 = seq ? st : C.s[2];
@@ -386,7 +491,6 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
         DR_CUDA(cudaEventRecord(C.fork, st));
         for (int q = 0; q < 3; ++q) DR_CUDA(cudaStreamWaitEvent(C.s[q], C.fork, 0));
     }
-    const int nc = g->n_cell, nn = g->n_net, D = L->d_out;
     auto dw = [&](int64_t n, int K, const float *Zd, const float *hv, const uint8_t *hi, int k,
                   const float *dy, int mode, float *gw, float *gb, float *wk, cudaStream_t s) {
         DwArgs a;
@@ -397,64 +501,49 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
     if (dxc || dxn) {
         // dZ'_psi = c_psi (dY_psi Wn_psi^T) (row-scaled by the destination normaliser),
         // with the Sage root term (dY_psi Wr_psi^T) at the kept indices as extra columns
-        // split: write dZ' as [hi | lo] bf16 rows for the tensor-core tiled SSpMM;
-        // returns whether it did
-        auto dzk = [&](int64_t n, int Kd, const float *dy, int mode, const float *W,
-                       const float *Wr, int Kr, const uint8_t *ridx, int rk, float *root,
-                       const float *c, float *out, uint8_t *img, cudaStream_t s,
-                       bool split) -> bool {
-            Tc2RowsDesc d;
-            d.n = n; d.N = Kd + (Wr ? Kr : 0); d.G = 1; d.epi = kEpi2Dz;
-            d.nseg[0] = 1;
-            d.seg[0][0].A = dy; d.seg[0][0].K = D; d.seg[0][0].mask_mode = mode;
-            d.mask_in = mask; d.mask_width = D;
-            d.bimg[0] = img; d.n_dz = Kd; d.crow = c; d.dz = out;
-            d.dz_split = split;
-            if (Wr) { d.root_idx = ridx; d.root_k = rk; d.root = root; }
-            if (tc2_rows_supported(d)) {       // B_op[n][kk] = W[n][kk]
-                launch_tc2_pack_b(W, D, D, Kd, 0, d.N, false, img, s);
-                if (Wr) launch_tc2_pack_b(Wr, D, D, Kr, Kd, d.N, false, img, s);
-                launch_tc2_rows(d, s);
-                return split;
+        // (descriptors and packed weights prepared before the fork, dz_prep)
+        auto dzk = [&](int r, int64_t n, int Kd, const float *dy, int mode, const float *W,
+                       const float *Wr, const uint8_t *ridx, int rk, float *root,
+                       const float *c, float *out, cudaStream_t s) {
+            if (dz_tc[r]) {
+                launch_tc2_rows(dzd[r], s);
+                return;
             }
             ProjBwdArgs a;
             a.n = n; a.N = D; a.K = Kd; a.dy = dy; a.mask = mask; a.mask_mode = mode;
             a.W = W; a.c = c; a.dz = out;
             launch_proj_bwd_dz(a, s);
             if (Wr) {
-                RootArgs r;
-                r.n = n; r.N = D; r.k = rk; r.dy = dy; r.mask = mask; r.mask_mode = mode;
-                r.Wr = Wr; r.hidx = ridx; r.out = root;
-                launch_root_dots(r, s);
+                RootArgs q;
+                q.n = n; q.N = D; q.k = rk; q.dy = dy; q.mask = mask; q.mask_mode = mode;
+                q.Wr = Wr; q.hidx = ridx; q.out = root;
+                launch_root_dots(q, s);
             }
-            return false;
         };
-        const RelDev &rn = g->rel[DR_NEAR];
-        const bool near_tiled = dxc && !rn.ewT && rn.n_src == nc &&
-                                tspmm_supported(rn.tilesT, L->d_cell, L->k_cell);
-        bool near_split = false;
+        const bool near_split = near_tiled && dz_tc[DR_NEAR];
         {
             TagScope t("near");
-            near_split = dzk(nc, L->d_cell, dyc, mode_near, L->wn[DR_NEAR], L->wr[DR_NEAR],
-                             L->d_cell, hci, L->k_cell, root_c, g->rel[DR_NEAR].c, dz[DR_NEAR],
-                             (uint8_t *)(tp + T.img_dz[DR_NEAR]), s0, near_tiled);
+            dzk(DR_NEAR, nc, L->d_cell, dyc, mode_near, L->wn[DR_NEAR], L->wr[DR_NEAR], hci,
+                L->k_cell, root_c, g->rel[DR_NEAR].c, dz[DR_NEAR], s0);
         }
-        {
+        if (dyn) {
             TagScope t("pins");
-            dzk(nn, L->d_cell, dyn, kMaskNone, L->wn[DR_PINS], L->wr[DR_PINS], L->d_net, hni,
-                L->k_net, root_n, g->rel[DR_PINS].c, dz[DR_PINS],
-                (uint8_t *)(tp + T.img_dz[DR_PINS]), s1, false);
+            dzk(DR_PINS, nn, L->d_cell, dyn, kMaskNone, L->wn[DR_PINS], L->wr[DR_PINS], hni,
+                L->k_net, root_n, g->rel[DR_PINS].c, dz[DR_PINS], s1);
         }
         if (!seq) DR_CUDA(cudaEventRecord(C.ev[0], s1));                           // dZ_pins, root_n
         {
             TagScope t("pinned");
-            dzk(nc, L->d_net, dyc, mode_pinned, L->wn[DR_PINNED], nullptr, 0, nullptr, 0, nullptr,
-                g->rel[DR_PINNED].c, dz[DR_PINNED], (uint8_t *)(tp + T.img_dz[DR_PINNED]), s2, false);
+            dzk(DR_PINNED, nc, L->d_net, dyc, mode_pinned, L->wn[DR_PINNED], nullptr, nullptr, 0,
+                nullptr, g->rel[DR_PINNED].c, dz[DR_PINNED], s2);
         }
         // SSpMM per source node type (Alg. 2 stage 2-3, ownership instead of atomics)
+        // dY_net == 0 (dyn == NULL): no pins term (dZ'_pins = 0) and no pins root term
+        const float *rootc = L->wr[DR_NEAR] ? root_c : nullptr;
         if (dxc) {
             if (!seq) DR_CUDA(cudaStreamWaitEvent(s0, C.ev[0], 0));
             BwdTerm t0{&g->rel[DR_NEAR], dz[DR_NEAR], false}, t1{&g->rel[DR_PINS], dz[DR_PINS], false};
+            if (!dyn) t1 = BwdTerm{};
             TagScope t("cell");
             if (own) {
                 // Q27: near (+ root) writes the dense dX_c row at idx_c, then the pins
@@ -467,8 +556,12 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
                     launch_spmm_bwd(rn.bwd, nc, t0, BwdTerm{}, rootp, hci, L->k_cell, L->d_cell,
                                     nullptr, dxc, false, s0);
                 TagScope t2("pins");
-                launch_spmm_bwd(g->rel[DR_PINS].bwd, nc, t1, BwdTerm{}, nullptr, hpi, kp,
-                                L->d_cell, nullptr, dxc, true, s0);
+                if (dyn)
+                    launch_spmm_bwd(g->rel[DR_PINS].bwd, nc, t1, BwdTerm{}, nullptr, hpi, kp,
+                                    L->d_cell, nullptr, dxc, true, s0);
+            } else if (near_tiled && !dyn) {
+                launch_tspmm_bwd(rn, dz[DR_NEAR], near_split, false, rootc, hci, L->k_cell,
+                                 L->d_cell, nullptr, dxc, s0);
             } else if (near_tiled) {
                 // tensor-core tiled near term; the low-degree pins term (+ the root
                 // term) first goes to root_c in place with the SIMT kernel, and the
@@ -490,7 +583,7 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
             if (!seq) DR_CUDA(cudaStreamWaitEvent(s2, C.ev[0], 0));
             BwdTerm t0{&g->rel[DR_PINNED], dz[DR_PINNED], false}, t1{};
             TagScope t("net");
-            launch_spmm_bwd(g->src_net, nn, t0, t1, L->wr[DR_PINS] ? root_n : nullptr, hni,
+            launch_spmm_bwd(g->src_net, nn, t0, t1, (L->wr[DR_PINS] && dyn) ? root_n : nullptr, hni,
                             L->k_net, L->d_net, nullptr, dxn, false, s2);
         }
     }
@@ -537,7 +630,11 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
             dw(nc, L->d_net, z[DR_PINNED], nullptr, nullptr, 0, dyc, mode_pinned,
                G->wn[DR_PINNED], G->b[DR_PINNED], work[2], s2);
     }
-    {
+    if (!dyn) {                  // dY_net == 0: the pins gradients are exactly zero
+        DR_CUDA(cudaMemsetAsync(G->wn[DR_PINS], 0, (size_t)L->d_cell * D * 4, s1));
+        if (L->wr[DR_PINS]) DR_CUDA(cudaMemsetAsync(G->wr[DR_PINS], 0, (size_t)L->d_net * D * 4, s1));
+        DR_CUDA(cudaMemsetAsync(G->b[DR_PINS], 0, (size_t)D * 4, s1));
+    } else {
         TagScope t("pins");
         if (!dwt(nn, z[DR_PINS], L->d_cell, G->wn[DR_PINS], hnv, hni, L->k_net, L->d_net,
                  L->wr[DR_PINS] ? G->wr[DR_PINS] : nullptr, dyn, kMaskNone, G->b[DR_PINS],
@@ -905,7 +1002,33 @@ dr_status dr_heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *x
     DR_CHECK(tape != nullptr, DR_ERR_TAPE_MISMATCH, "null tape");
     DR_CHECK((g->n_cell == 0 || (x_cell && y_cell)) && (g->n_net == 0 || (x_net && y_net)),
              DR_ERR_INVALID_ARGUMENT, "heteroconv_fwd: null input/output");
+    DR_CHECK(!(flags & DR_FWD_INPUT_IN_TAPE), DR_ERR_INVALID_ARGUMENT,
+             "heteroconv_fwd: DR_FWD_INPUT_IN_TAPE needs dr_heteroconv_fwd_chain");
     heteroconv_fwd(g, L, x_cell, x_net, y_cell, y_net, tape, flags, (cudaStream_t)stream);
+    DR_API_END
+}
+
+dr_status dr_heteroconv_fwd_chain(const dr_graph *g, const dr_layer *L, const float *x_cell,
+                                  const float *x_net, float *y_cell, float *y_net, void *tape,
+                                  uint32_t flags, const dr_layer *next_L, void *next_tape,
+                                  uint32_t next_flags, void *stream) {
+    DR_API_BEGIN
+    check_layer(g, L);
+    DR_CHECK(tape != nullptr, DR_ERR_TAPE_MISMATCH, "null tape");
+    const bool in_tape = (flags & DR_FWD_INPUT_IN_TAPE) != 0;
+    DR_CHECK((g->n_cell == 0 || ((x_cell || in_tape) && y_cell)) &&
+                 (g->n_net == 0 || ((x_net || in_tape) && y_net)),
+             DR_ERR_INVALID_ARGUMENT, "heteroconv_fwd_chain: null input/output");
+    DR_CHECK(!next_L == !next_tape, DR_ERR_INVALID_ARGUMENT,
+             "heteroconv_fwd_chain: next_L and next_tape go together");
+    if (next_L) {
+        check_layer(g, next_L);
+        DR_CHECK(next_L->d_cell == L->d_out && next_L->d_net == L->d_out, DR_ERR_SHAPE_MISMATCH,
+                 "heteroconv_fwd_chain: next layer input widths != d_out");
+        DR_CHECK(next_tape != tape, DR_ERR_INVALID_ARGUMENT, "heteroconv_fwd_chain: same tape");
+    }
+    heteroconv_fwd(g, L, x_cell, x_net, y_cell, y_net, tape, flags, (cudaStream_t)stream, next_L,
+                   next_tape, next_flags);
     DR_API_END
 }
 
@@ -920,7 +1043,7 @@ dr_status dr_heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape,
         DR_CHECK(grads->wn[r] && grads->b[r], DR_ERR_INVALID_ARGUMENT, "null grad wn/b");
         DR_CHECK(!L->wr[r] || grads->wr[r], DR_ERR_INVALID_ARGUMENT, "null grad wr");
     }
-    DR_CHECK(dy_cell && dy_net, DR_ERR_INVALID_ARGUMENT, "null dy");
+    DR_CHECK(dy_cell, DR_ERR_INVALID_ARGUMENT, "null dy_cell");
     heteroconv_bwd(g, L, tape, dy_cell, dy_net, dx_cell, dx_net, grads, flags,
                    (cudaStream_t)stream);
     DR_API_END
@@ -1046,9 +1169,22 @@ static void train_step_body(dr_trainer *t, const dr_graph *g, const float *x_cel
     // ---- forward
     const float *xc = x_cell, *xn = x_net;
     static const char *ltag[8] = {"L0", "L1", "L2", "L3", "L4", "L5", "L6", "L7"};
+    // row a5: layer l's projection epilogues write layer l+1's input CBSR into its
+    // tape (DR_FWD_INPUT_IN_TAPE there), and Y_l itself is never stored; the last
+    // layer's Y_net reaches nothing (the head reads cells, Q14): not computed
+    bool chain = knobs().chain != 0;
+    for (int l = 0; l < nl; ++l) chain = chain && !pins_own(&t->L[l]);
+    const bool no_net = knobs().skip_dead_net != 0;
     for (int l = 0; l < nl; ++l) {
         TagScope tg(ltag[l]);
-        heteroconv_fwd(g, &t->L[l], xc, xn, yc(l), yn(l), ws + tape_off[l], 0, st);
+        const bool last = l == nl - 1;
+        uint32_t fl = (chain && l > 0) ? DR_FWD_INPUT_IN_TAPE : 0u;
+        if (last && no_net) fl |= DR_FWD_NO_NET_OUT;
+        if (chain && !last)
+            heteroconv_fwd(g, &t->L[l], xc, xn, yc(l), yn(l), ws + tape_off[l], fl | DR_FWD_Y_SCRATCH,
+                           st, &t->L[l + 1], ws + tape_off[l + 1], 0);
+        else
+            heteroconv_fwd(g, &t->L[l], xc, xn, yc(l), yn(l), ws + tape_off[l], fl, st);
         xc = yc(l);
         xn = yn(l);
     }
@@ -1060,14 +1196,16 @@ static void train_step_body(dr_trainer *t, const dr_graph *g, const float *x_cel
         h.loss = t->scalars; h.work = (float *)(ws + head_off);
         launch_head_mse(h, st);
     }
-    DR_CUDA(cudaMemsetAsync(dyn(0), 0, nn * D * 4, st));   // last layer's Y_net feeds nothing
+    if (!no_net)                                 // last layer's Y_net feeds nothing: dY_net = 0
+        DR_CUDA(cudaMemsetAsync(dyn(0), 0, nn * D * 4, st));
     // ---- backward
     int cur = 0;
     for (int l = nl - 1; l >= 0; --l) {
         float *dxc = l > 0 ? dyc(cur ^ 1) : nullptr;
         float *dxn = l > 0 ? dyn(cur ^ 1) : nullptr;
         TagScope tg(ltag[l]);
-        heteroconv_bwd(g, &t->L[l], ws + tape_off[l], dyc(cur), dyn(cur), dxc, dxn, &t->G[l], 0, st);
+        const float *dyn_l = (l == nl - 1 && no_net) ? nullptr : dyn(cur);
+        heteroconv_bwd(g, &t->L[l], ws + tape_off[l], dyc(cur), dyn_l, dxc, dxn, &t->G[l], 0, st);
         cur ^= 1;
     }
     // ---- data-parallel gradient exchange: one allreduce (sum) of the flat gradient

@@ -10,14 +10,10 @@
 // column order (exactly-k, ties to the lowest column). A warp exclusive scan
 // gives each survivor its slot; outputs are idx-ascending (val, idx) pairs.
 #include "dr_internal.h"
+#include "drelu_net.cuh"
 
 namespace dr {
 namespace {
-
-__device__ __forceinline__ uint32_t order_key(float x) {
-    uint32_t u = __float_as_uint(x + 0.0f);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
 
 __device__ __forceinline__ int warp_excl_scan(int v, int lane) {
     int inc = v;
@@ -330,57 +326,11 @@ __global__ void __launch_bounds__(256) drelu_extract_kernel(const float *__restr
 // left in value order (SORTED), and their values read back from shared memory.
 // Instructions per row ~ D log^2 K compare-exchanges instead of K warp-wide
 // reduction rounds (the standalone D-ReLU was issue-bound, profiles/r01).
-// bitonic sort of w[B..B+K) descending
-template <int K>
-__device__ __forceinline__ void bitonic_sort_desc(uint32_t *w) {
-#pragma unroll
-    for (int k = 2; k <= K; k <<= 1)
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1)
-#pragma unroll
-            for (int i = 0; i < K; ++i) {
-                const int l = i ^ j;
-                if (l > i) {
-                    const uint32_t hi = max(w[i], w[l]), lo = min(w[i], w[l]);
-                    const bool desc = (i & k) == 0;
-                    w[i] = desc ? hi : lo;
-                    w[l] = desc ? lo : hi;
-                }
-            }
-}
-
-// a, b sorted descending (K each): a <- the K largest of both, sorted descending;
-// returns the largest discarded composite
-template <int K>
-__device__ __forceinline__ uint32_t merge_keep_desc(uint32_t *a, const uint32_t *b) {
-    uint32_t lost = 0;
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-        const uint32_t x = a[i], y = b[K - 1 - i];
-        a[i] = max(x, y);
-        lost = max(lost, min(x, y));
-    }
-#pragma unroll
-    for (int j = K >> 1; j > 0; j >>= 1)
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            const int l = i ^ j;
-            if (l > i) {
-                const uint32_t hi = max(a[i], a[l]), lo = min(a[i], a[l]);
-                a[i] = hi;
-                a[l] = lo;
-            }
-        }
-    return lost;
-}
-
 template <int D, int K, bool SORTED>
 __global__ void __launch_bounds__(128, D == 128 ? 3 : 6) drelu_tpr_kernel(const float *__restrict__ x, int64_t n,
                                                         int64_t ldx, float *__restrict__ val,
                                                         uint8_t *__restrict__ idx) {
     constexpr int P = D + 4;                      // padded row: conflict-free 128-bit reads
-    constexpr int CB = D == 32 ? 5 : D == 64 ? 6 : 7;
-    constexpr uint32_t CM = (1u << CB) - 1u;
     constexpr int Q = D / 4;                      // float4 per row
     extern __shared__ __align__(16) float tpr_sm[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -409,118 +359,7 @@ __global__ void __launch_bounds__(128, D == 128 ? 3 : 6) drelu_tpr_kernel(const 
         }
         __syncwarp();
         const int64_t r = r0 + lane;
-        const float *xr = xs + lane * P;
-        uint32_t w[D];
-#pragma unroll
-        for (int c4 = 0; c4 < Q; ++c4) {
-            const float4 v = *reinterpret_cast<const float4 *>(xr + 4 * c4);
-            w[4 * c4 + 0] = (order_key(v.x) & ~CM) | (CM - (uint32_t)(4 * c4 + 0));
-            w[4 * c4 + 1] = (order_key(v.y) & ~CM) | (CM - (uint32_t)(4 * c4 + 1));
-            w[4 * c4 + 2] = (order_key(v.z) & ~CM) | (CM - (uint32_t)(4 * c4 + 2));
-            w[4 * c4 + 3] = (order_key(v.w) & ~CM) | (CM - (uint32_t)(4 * c4 + 3));
-        }
-#pragma unroll
-        for (int g = 0; g < D / K; ++g) bitonic_sort_desc<K>(w + g * K);
-        uint32_t lost = 0;
-#pragma unroll
-        for (int step = 1; step < D / K; step <<= 1)
-#pragma unroll
-            for (int g = 0; g + step < D / K; g += 2 * step)
-                lost = max(lost, merge_keep_desc<K>(w + g * K, w + (g + step) * K));
-        // w[0..K) = the top K composites, descending; exact unless the best loser
-        // shares the K-th's truncated key
-        uint32_t col[K];
-#pragma unroll
-        for (int t = 0; t < K; ++t) col[t] = CM - (w[t] & CM);
-        bool rerun = (lost & ~CM) == (w[K - 1] & ~CM);
-        if constexpr (SORTED) {    // value order inside the K: equal truncated keys are ordered by column
-#pragma unroll
-            for (int t = 0; t + 1 < K; ++t) rerun |= ((w[t] ^ w[t + 1]) & ~CM) == 0u;
-        }
-        if (r < n && rerun) {
-            // exact rerun: the K-th largest full key by MSB-first bisection, then
-            // keys above it and the lowest columns among keys equal to it
-            uint32_t T = 0;
-            for (int b = 31; b >= 0; --b) {
-                const uint32_t cand = T | (1u << b);
-                int cnt = 0;
-                for (int j = 0; j < D; ++j) cnt += order_key(xr[j]) >= cand;
-                if (cnt >= K) T = cand;
-            }
-            int gt = 0;
-            for (int j = 0; j < D; ++j) gt += order_key(xr[j]) > T;
-            int need = K - gt, q = 0;
-            uint32_t sel[K];
-            for (int j = 0; j < D; ++j) {
-                const uint32_t kj = order_key(xr[j]);
-                const bool take = kj > T || (kj == T && need > 0);
-                if (take && kj == T) --need;
-                if (take) {
-#pragma unroll
-                    for (int t = 0; t < K; ++t)
-                        if (t == q) sel[t] = (uint32_t)j;
-                    ++q;
-                }
-            }
-            if constexpr (SORTED) {
-                // order the K selected columns by (key desc, col asc): insertion sort
-                for (int a2 = 1; a2 < K; ++a2)
-                    for (int b2 = a2; b2 > 0; --b2) {
-                        const uint32_t ca = sel[b2 - 1], cb = sel[b2];
-                        const uint32_t ka = order_key(xr[ca]), kb = order_key(xr[cb]);
-                        if (kb > ka || (kb == ka && cb < ca)) {
-                            sel[b2 - 1] = cb;
-                            sel[b2] = ca;
-                        }
-                    }
-            }
-            // col[] is read back to front below unless SORTED: store descending
-#pragma unroll
-            for (int t = 0; t < K; ++t) col[t] = SORTED ? sel[t] : sel[K - 1 - t];
-        } else if constexpr (!SORTED) {
-            bitonic_sort_desc<K>(col);             // descending columns ...
-        }
-        if (r < n) {
-            float *vo = val + r * K;
-            uint8_t *io = idx + r * K;
-            if constexpr (SORTED) {
-#pragma unroll
-                for (int t = 0; t < K; ++t) {
-                    vo[t] = xr[col[t]];
-                    io[t] = (uint8_t)col[t];
-                }
-            } else {
-                // ... written back to front: ascending (CBSR order)
-                float ov[K];
-                uint32_t ob[K / 4 > 0 ? K / 4 : 1];
-#pragma unroll
-                for (int t = 0; t < (K / 4 > 0 ? K / 4 : 1); ++t) ob[t] = 0u;
-#pragma unroll
-                for (int t = 0; t < K; ++t) {
-                    const uint32_t c = col[K - 1 - t];
-                    ov[t] = xr[c];
-                    ob[t >> 2] |= c << (8 * (t & 3));
-                }
-                if constexpr (K % 4 == 0) {
-#pragma unroll
-                    for (int t = 0; t < K / 4; ++t)
-                        reinterpret_cast<float4 *>(vo)[t] = make_float4(ov[4 * t], ov[4 * t + 1], ov[4 * t + 2], ov[4 * t + 3]);
-                    if constexpr (K == 4) *reinterpret_cast<uint32_t *>(io) = ob[0];
-                    else if constexpr (K == 8) *reinterpret_cast<uint2 *>(io) = make_uint2(ob[0], ob[1]);
-                    else {
-#pragma unroll
-                        for (int t = 0; t < K / 16; ++t)
-                            reinterpret_cast<uint4 *>(io)[t] = make_uint4(ob[4 * t], ob[4 * t + 1], ob[4 * t + 2], ob[4 * t + 3]);
-                    }
-                } else {
-#pragma unroll
-                    for (int t = 0; t < K; ++t) {
-                        vo[t] = ov[t];
-                        io[t] = (uint8_t)(ob[t >> 2] >> (8 * (t & 3)));
-                    }
-                }
-            }
-        }
+        tpr_select_row<D, K, SORTED>(xs + lane * P, r < n, val + r * K, idx + r * K);
         __syncwarp();
     }
 }

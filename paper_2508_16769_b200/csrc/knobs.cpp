@@ -37,6 +37,8 @@ static Knobs read_env() {
     k.ts_order_rr = (r && std::string(r) == "rr") ? 1 : 0;
     k.shard_tiles = env_i("DR_SHARD_TILES", 0);
     k.shard_tiles_t = env_i("DR_SHARD_TILES_T", 0);
+    k.chain = env_i("DR_CHAIN", 1);
+    k.skip_dead_net = env_i("DR_SKIP_DEAD_NET", 1);
     return k;
 }
 
@@ -72,6 +74,8 @@ extern "C" dr_status dr_debug_set(const char *name, int64_t value) {
         {"ts_order_rr", &g_knobs.ts_order_rr},
         {"shard_tiles", &g_knobs.shard_tiles},
         {"shard_tiles_t", &g_knobs.shard_tiles_t},
+        {"chain", &g_knobs.chain},
+        {"skip_dead_net", &g_knobs.skip_dead_net},
     };
     for (auto &t : tab)
         if (std::strcmp(t.n, name) == 0) {

@@ -30,6 +30,7 @@
 #include "proj.h"
 #include "tc.cuh"
 #include "tc2.h"
+#include "drelu_net.cuh"
 
 namespace dr {
 namespace {
@@ -41,8 +42,10 @@ constexpr uint32_t kHalf = 16384;      // one bf16 128 x 64 tile
 constexpr int kMaskStage = 4096;       // 128 rows x up to 8 mask words
 constexpr int kRowsThreads = 320;
 constexpr int kRedThreads = 320;     // producer, MMA, 2 x 4 converter warps
-constexpr int kEpiStage = 4 * 32 * 36 * 4;   // epilogue staging (4 warps x [32][36] fp32)
-constexpr int kSmemBudget = 227 * 1024 - 1024 - 4096 - kEpiStage;   // opt-in max minus alignment, static smem, staging (rows)
+constexpr int kEpiWarp0 = 32 * 36 * 4;                // epilogue staging per warp: [32][36] fp32
+constexpr int kEpiWarpN = 32 * 68 * 4;                // ... with the fused D-ReLU: [32][kRB] row buffer
+constexpr int kSmemBase = 227 * 1024 - 1024 - 4096;   // opt-in max minus alignment, static smem
+__host__ __device__ constexpr int epi_warp_bytes(bool next) { return next ? kEpiWarpN : kEpiWarp0; }
 constexpr int kSmemBudgetRed = 227 * 1024 - 1024 - 10240 - 1024;  // reduce kernel: ~10 KB static
 constexpr int kMaxSteps = 16;
 constexpr int kMaxSA = 4, kMaxSB = 16;
@@ -73,6 +76,35 @@ __global__ void tc2_pack_b_kernel(const float *__restrict__ W, int ldw, int K, i
         const uint32_t off = tc::sw128_off_h((uint32_t)(n0 + n), (uint32_t)(2 * kp));
         *reinterpret_cast<uint32_t *>(base + off) = hi;
         *reinterpret_cast<uint32_t *>(base + (size_t)Ntot * 128 + off) = lo;
+    }
+}
+
+// several images in one launch (blockIdx.y = job): a layer's forward or
+// backward packs all its weights at once instead of one launch per weight
+struct PackJobs {
+    Tc2PackJob job[kMaxPackJobs];
+};
+__global__ void tc2_pack_b_multi_kernel(const __grid_constant__ PackJobs j) {
+    const Tc2PackJob &p = j.job[blockIdx.y];
+    const int chunks = (p.K + kChunk - 1) / kChunk;
+    const int64_t total = (int64_t)chunks * p.NB * (kChunk / 2);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int kp = (int)(e % (kChunk / 2));
+        const int n = (int)((e / (kChunk / 2)) % p.NB);
+        const int c = (int)(e / ((int64_t)(kChunk / 2) * p.NB));
+        const int k0 = c * kChunk + 2 * kp;
+        float v[2];
+        for (int q = 0; q < 2; ++q) {
+            const int k = k0 + q;
+            v[q] = k < p.K ? (p.transpose ? p.W[(int64_t)k * p.ldw + n] : p.W[(int64_t)n * p.ldw + k]) : 0.f;
+        }
+        uint32_t hi, lo;
+        tc::split_bf16x2(v[0], v[1], hi, lo);
+        uint8_t *base = p.img + (size_t)c * 2 * p.Ntot * 128;
+        const uint32_t off = tc::sw128_off_h((uint32_t)(p.n0 + n), (uint32_t)(2 * kp));
+        *reinterpret_cast<uint32_t *>(base + off) = hi;
+        *reinterpret_cast<uint32_t *>(base + (size_t)p.Ntot * 128 + off) = lo;
     }
 }
 
@@ -114,6 +146,10 @@ struct R2Args {
     const uint8_t *root_idx;
     int root_k;
     float *root;
+    // fused next-layer D-ReLU (row a5): CBSR of y, exactly nk per row (tc2.h)
+    int nk;                        // keep count (0: no fused D-ReLU)
+    float *nval;
+    uint8_t *nidx;
     unsigned long long *dbg;       // DR_TC2_DEBUG role timers, else null
 };
 
@@ -252,19 +288,19 @@ __device__ __forceinline__ void rows_convert(const R2Args &a, const R2Step &sp, 
 // coalesced stores (lane -> row 4 i + lane / 8, column quad lane % 8: each
 // instruction writes 4 rows x 128 B). No asynchronous store state to wait on.
 constexpr int kEStg = 36;
-__device__ __forceinline__ void stg_put(float *stg, int lane, const float *v) {
-    float4 *o = reinterpret_cast<float4 *>(stg + lane * kEStg);
+__device__ __forceinline__ void stg_put(float *stg, int stride, int lane, const float *v) {
+    float4 *o = reinterpret_cast<float4 *>(stg + lane * stride);
 #pragma unroll
     for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
 }
 // rows row0 .. row0 + 31 (< n) of an fp32 [n x W] matrix, columns [j, j + 32)
-__device__ __forceinline__ void stg_out_f32(const float *stg, float *out, int64_t W, int64_t row0,
-                                            int64_t n, int j, int lane) {
+__device__ __forceinline__ void stg_out_f32(const float *stg, int stride, float *out, int64_t W,
+                                            int64_t row0, int64_t n, int j, int lane) {
     const int cq = lane & 7, rs = lane >> 3;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int r = 4 * i + rs;
-        const float4 v = *reinterpret_cast<const float4 *>(stg + r * kEStg + 4 * cq);
+        const float4 v = *reinterpret_cast<const float4 *>(stg + r * stride + 4 * cq);
         if (row0 + r < n && j + 4 * cq < W) __stcs(reinterpret_cast<float4 *>(out + (row0 + r) * W + j) + cq, v);
     }
 }
@@ -327,7 +363,20 @@ __device__ __forceinline__ void epi_pre_load(const R2Args &a, int64_t row, EpiPr
     }
 }
 
+// ---------------- fused next-layer D-ReLU (row a5; Eq. 2-3, applied
+// to this layer's output, which is the next layer's input)
+// The epilogue warp stages its 32 output rows in a [32][kRB] shared-memory row
+// buffer (which is also the staging of the coalesced Y stores); each lane then
+// selects its own row's exact top-NK with the thread-per-row network of the
+// standalone D-ReLU (drelu_net.cuh tpr_select_row: composite keys, bitonic
+// groups, exact rerun from shared memory on a truncated-key collision).
+// Measured (tools/scratch/epi_topk.cu, one warp per SM sub-partition as in this
+// epilogue): ~5.3k cycles per 32 rows at N=64, k=8, vs ~50k for a warp-
+// cooperative redux.max extraction (latency-bound at one warp per SMSP).
+constexpr int kRB = 68;                // row-buffer stride (floats): 64 columns + 4 pad
+
 // epilogue warp (quarter qd): rows r0 + 32 qd + lane of accumulator columns at `acc`
+template <int NK>
 __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int64_t r0, int qd,
                                               int lane, const float *bias_s, float *stg,
                                               const EpiPre &pre) {
@@ -335,7 +384,7 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
     const int64_t row0 = r0 + qd * 32, row = row0 + lane;
     const bool ok = row < a.n;
     const uint32_t lb = acc + ((uint32_t)(qd * 32) << 16);
-    if (a.epi == kEpi2Dz) {
+    if (NK == 0 && a.epi == kEpi2Dz) {        // (the fused D-ReLU variants are forward-only)
         const float cr = pre.cr;
         // root term: columns [n_dz, N) sampled at the row's CBSR indices (ascending),
         // collected in registers (static indices) and stored as whole rows at the end
@@ -358,11 +407,11 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
 #pragma unroll
             for (int q = 0; q < 32; ++q)
                 if (j + q < a.n_dz) v[q] *= cr;        // dZ' row scale (not the root term)
-            stg_put(stg, lane, v);
+            stg_put(stg, kEStg, lane, v);
             __syncwarp();
             if (j < a.n_dz) {
                 if (a.dz_split) stg_out_split(stg, reinterpret_cast<uint8_t *>(a.dz), a.n_dz, row0, a.n, j, lane);
-                else stg_out_f32(stg, a.dz, a.n_dz, row0, a.n, j, lane);
+                else stg_out_f32(stg, kEStg, a.dz, a.n_dz, row0, a.n, j, lane);
             }
             if (a.root && j + 32 > a.n_dz) {
                 if (rk <= 16) {
@@ -396,6 +445,9 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
         return;
     }
     const int mw = (N + 31) >> 5;
+    // NK > 0 (fused next-layer D-ReLU): `stg` is the warp's [32][kRB] row buffer
+    // and every block stays staged at its columns until the selection below
+    const int sstride = NK > 0 ? kRB : kEStg;
     for (int j = 0; j < N; j += 32) {
         uint32_t ra[2][16], rb[2][16];
         tc::tmem_ld16_nw(lb + (uint32_t)j, ra[0]);
@@ -442,14 +494,26 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
                 for (int q = 0; q < 16; ++q) y[16 * h + q] = ya[q];
             }
         }
-        stg_put(stg, lane, y);
-        __syncwarp();
-        stg_out_f32(stg, a.y, N, row0, a.n, j, lane);
-        __syncwarp();
+        float *sb = NK > 0 ? stg + j : stg;
+        if (NK > 0 || a.y) {
+            stg_put(sb, sstride, lane, y);
+            __syncwarp();
+        }
+        if (a.y) {
+            stg_out_f32(sb, sstride, a.y, N, row0, a.n, j, lane);
+            __syncwarp();
+        }
         if (ok && a.G == 2 && a.mask_out) a.mask_out[row * mw + (j >> 5)] = word;
+    }
+    if constexpr (NK > 0) {
+        const float *xr = stg + lane * kRB;
+        if (N == 64) tpr_select_row<64, NK, false>(xr, ok, a.nval + row * NK, a.nidx + row * NK);
+        else tpr_select_row<32, (NK < 32 ? NK : 32), false>(xr, ok, a.nval + row * NK, a.nidx + row * NK);
+        __syncwarp();
     }
 }
 
+template <int NK>
 __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_constant__ R2Args a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -619,13 +683,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
     } else {
         // ---------------- epilogue
         const int qd = warp & 3;
-        float *stg = reinterpret_cast<float *>(epi_stage + (size_t)(warp - 6) * (32 * 36 * 4));
+        float *stg = reinterpret_cast<float *>(epi_stage + (size_t)(warp - 6) * epi_warp_bytes(NK > 0));
         EpiPre pcur, pnxt;
-        if (my_tiles > 0) epi_pre_load(a, (int64_t)blockIdx.x * kTile + qd * 32 + lane, pcur);
+        if (NK == 0 && my_tiles > 0) epi_pre_load(a, (int64_t)blockIdx.x * kTile + qd * 32 + lane, pcur);
         for (int64_t t = 0; t < my_tiles; ++t) {
             const int64_t r0 = ((int64_t)blockIdx.x + t * gridDim.x) * kTile;
             const uint32_t ab = (uint32_t)(t & 1);
-            if (t + 1 < my_tiles) epi_pre_load(a, r0 + (int64_t)gridDim.x * kTile + qd * 32 + lane, pnxt);
+            if (NK == 0 && t + 1 < my_tiles) epi_pre_load(a, r0 + (int64_t)gridDim.x * kTile + qd * 32 + lane, pnxt);
             {
                 RDBG_T0;
                 tc::mbar_wait_sleep(&accf[ab], (uint32_t)((t >> 1) & 1));
@@ -633,7 +697,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
             }
             tc::fence_after();
             RDBG_T0;
-            rows_epilogue(a, tmem + ab * GN, r0, qd, lane, bias_s, stg, pcur);
+            rows_epilogue<NK>(a, tmem + ab * GN, r0, qd, lane, bias_s, stg, pcur);
             pcur = pnxt;
             if (warp == 6 && lane == 0) RDBG_ADD(6);
             tc::fence_before();
@@ -1228,6 +1292,22 @@ void launch_tc2_pack_b(const float *W, int ldw, int K, int NB, int n0, int Ntot,
     note_launch("tc2_pack_b");
 }
 
+void launch_tc2_pack_b_multi(const Tc2PackJob *jobs, int n, cudaStream_t s) {
+    if (n <= 0) return;
+    DR_CHECK(n <= kMaxPackJobs, DR_ERR_INVALID_ARGUMENT, "tc2_pack_b_multi: too many jobs");
+    PackJobs j{};
+    int64_t most = 1;
+    for (int i = 0; i < n; ++i) {
+        j.job[i] = jobs[i];
+        const int64_t total = (int64_t)((jobs[i].K + kChunk - 1) / kChunk) * jobs[i].NB * (kChunk / 2);
+        most = std::max(most, total);
+    }
+    int64_t bx = (most + 255) / 256;
+    if (bx > 148) bx = 148;
+    tc2_pack_b_multi_kernel<<<dim3((unsigned)bx, (unsigned)n), 256, 0, s>>>(j);
+    note_launch("tc2_pack_b");
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -1278,6 +1358,10 @@ static bool seg_ok(const Tc2Seg &s) {
     return true;
 }
 
+bool tc2_next_drelu_supported(int epi, int N, int k) {
+    return epi == kEpi2Fwd && (N == 32 || N == 64) && k >= 1 && k <= 32 && (k & (k - 1)) == 0 && k <= N;
+}
+
 bool tc2_rows_supported(const Tc2RowsDesc &d) {
     if (knobs().dense_simt) return false;         // A/B switch for tests and profiling
     if (d.N < 16 || d.N > 256 || d.N % 16) return false;
@@ -1294,8 +1378,10 @@ bool tc2_rows_supported(const Tc2RowsDesc &d) {
     if (steps > kMaxSteps) return false;
     if (d.epi == kEpi2Dz && d.root && (d.root_k < 1 || d.root_k > 32 || (d.N - d.n_dz) % 16)) return false;
     if (d.epi == kEpi2Dz && d.n_dz % 16) return false;
+    if (d.next_k && !tc2_next_drelu_supported(d.epi, d.N, d.next_k)) return false;
     const size_t bchunk = (size_t)256 * d.N;
-    return 2 * kStage + 2 * kMaskStage + 2 * bchunk <= (size_t)kSmemBudget;
+    const size_t budget = (size_t)(kSmemBase - 4 * epi_warp_bytes(d.next_k > 0));
+    return 2 * kStage + 2 * kMaskStage + 2 * bchunk <= budget;
 }
 
 void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
@@ -1337,9 +1423,13 @@ void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
     a.root_idx = d.root_idx;
     a.root_k = d.root_k;
     a.root = d.root;
+    a.nk = d.next_k;
+    a.nval = d.next_val;
+    a.nidx = d.next_idx;
+    DR_CHECK(!a.nk || (a.nval && a.nidx), DR_ERR_INVALID_ARGUMENT, "tc2_rows: null next CBSR");
     // stages: B resident when every chunk fits beside >= 2 A stages, else a ring
     const size_t st_bytes = kStage + kMaskStage;
-    const size_t budget = kSmemBudget;
+    const size_t budget = (size_t)(kSmemBase - 4 * epi_warp_bytes(a.nk > 0));
     if ((size_t)a.S * a.bchunk + 2 * st_bytes <= budget && a.S <= kMaxSB) {
         a.b_resident = 1;
         a.SB = a.S;
@@ -1351,19 +1441,29 @@ void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
         a.SB = (int)std::min<size_t>(4, (budget - a.SA * st_bytes) / a.bchunk);
     }
     a.epi_off = (uint32_t)((a.SA * st_bytes + (size_t)a.SB * a.bchunk + 1023) / 1024 * 1024);
-    const size_t smem = (size_t)a.epi_off + kEpiStage + 1024;
+    const size_t smem = (size_t)a.epi_off + 4 * epi_warp_bytes(a.nk > 0) + 1024;
     a.dz_split = d.dz_split ? 1 : 0;
     const int64_t tiles = (d.n + kTile - 1) / kTile;
     const int64_t grid = tiles < 148 ? tiles : 148;
     ProfScope ps(d.epi == kEpi2Dz ? "tc_dz" : "tc_proj", s);
-    ensure_smem((const void *)tc2_rows_kernel, smem);
+    const void *fn = a.nk == 1 ? (const void *)tc2_rows_kernel<1>
+                   : a.nk == 2 ? (const void *)tc2_rows_kernel<2>
+                   : a.nk == 4 ? (const void *)tc2_rows_kernel<4>
+                   : a.nk == 8 ? (const void *)tc2_rows_kernel<8>
+                   : a.nk == 16 ? (const void *)tc2_rows_kernel<16>
+                   : a.nk == 32 ? (const void *)tc2_rows_kernel<32>
+                                : (const void *)tc2_rows_kernel<0>;
+    ensure_smem(fn, smem);
     static unsigned long long *dbg_buf = nullptr;
     if (knobs().tc2_debug) {
         if (!dbg_buf) DR_CUDA(cudaMalloc(&dbg_buf, 148 * 16 * 8));
         DR_CUDA(cudaMemsetAsync(dbg_buf, 0, 148 * 16 * 8, s));
         a.dbg = dbg_buf;
     }
-    tc2_rows_kernel<<<(unsigned)grid, kRowsThreads, smem, s>>>(a);
+    {
+        void *args[] = {(void *)&a};
+        DR_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(kRowsThreads), args, smem, s));
+    }
     note_launch("tc2_rows");
     if (a.dbg) {
         unsigned long long h[148 * 16];

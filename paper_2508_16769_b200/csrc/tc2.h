@@ -56,7 +56,17 @@ struct Tc2RowsDesc {
     const uint8_t *root_idx = nullptr;
     int root_k = 0;
     float *root = nullptr;
+    // forward epilogue, fused next-layer D-ReLU (row a5; Eq. 2-3 on this GEMM's
+    // output y, after the merge): next_k > 0 also writes next_val / next_idx
+    // (n x next_k CBSR, ascending columns, exactly next_k per row, ties -> lowest
+    // column, values verbatim), bit-identical to launch_drelu on the written y.
+    // y may be null then (the dense output is not stored).
+    int next_k = 0;
+    float *next_val = nullptr;
+    uint8_t *next_idx = nullptr;
 };
+// shapes the fused next-layer D-ReLU covers (else: dense y + launch_drelu)
+bool tc2_next_drelu_supported(int epi, int N, int k);
 
 // Packed B image: per 64-wide K chunk, hi then lo, each Ntot rows x 128 B
 // (bf16, K-major, 128-B swizzle).
@@ -65,6 +75,14 @@ size_t tc2_bimg_bytes(int K, int Ntot);
 // B_op[n0 + n][kk] = transpose ? W[kk*ldw + n] : W[n*ldw + kk].
 void launch_tc2_pack_b(const float *W, int ldw, int K, int NB, int n0, int Ntot, bool transpose,
                        uint8_t *img, cudaStream_t s);
+// one packing job (launch_tc2_pack_b's arguments); several in one launch
+struct Tc2PackJob {
+    const float *W = nullptr;
+    int ldw = 0, K = 0, NB = 0, n0 = 0, Ntot = 0, transpose = 0;
+    uint8_t *img = nullptr;
+};
+constexpr int kMaxPackJobs = 8;
+void launch_tc2_pack_b_multi(const Tc2PackJob *jobs, int n, cudaStream_t s);
 bool tc2_rows_supported(const Tc2RowsDesc &d);
 void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s);
 
