@@ -421,6 +421,13 @@ dr_status dr_debug_set(const char *name, int64_t value);
 
 /* Number of kernels this library launched on this host thread since the last
  * reset (evidence for bench.py's gpu_launches). */
+/* Bandwidth probe for the second roofline: reads the DEVICE
+ * buffer `buf` (16-B aligned, `bytes` long) `reps` times with 128-bit loads on
+ * `stream`, one float per CTA written to `sink` (DEVICE, >= 592 floats) so no
+ * load is dead. The caller times it (read bytes = bytes x reps); a buffer of
+ * about 1/4 of L2 gives the L2 read bandwidth. DR_ERR_INVALID_ARGUMENT on bad
+ * arguments. Not part of the method; a measurement utility. */
+dr_status dr_probe_read(const void *buf, int64_t bytes, int32_t reps, float *sink, void *stream);
 int64_t dr_launch_count(void);
 void dr_launch_count_reset(void);
 

@@ -42,6 +42,12 @@ def _ptr(t):
     return C.c_void_p(0 if t is None else t.data_ptr())
 
 
+def probe_read(buf, reps, sink, stream=None):
+    """dr_probe_read: stream `buf` (a CUDA tensor) `reps` times (L2 / HBM read probe)."""
+    check(lib().dr_probe_read(_ptr(buf), buf.numel() * buf.element_size(), reps, _ptr(sink),
+                              _stream(stream)))
+
+
 def version():
     return lib().dr_version().decode()
 

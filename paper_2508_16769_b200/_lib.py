@@ -140,6 +140,7 @@ _SIGS = {
     "dr_profile_begin": (C.c_int, []),
     "dr_profile_end": (C.c_int, [C.POINTER(dr_profile_entry), C.c_int32, C.POINTER(C.c_int32)]),
     "dr_launch_count": (C.c_int64, []),
+    "dr_probe_read": (C.c_int, [P, C.c_int64, C.c_int32, P, P]),
     "dr_debug_set": (C.c_int, [C.c_char_p, C.c_int64]),
     "dr_launch_count_reset": (None, []),
 }

@@ -427,9 +427,13 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
     }
 }
 
+// defer: queue the weight gradients' fixed-order partial sums there (the caller
+// launches them once for several layers); nullptr: one launch at the end here
 static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, const float *dyc,
                            const float *dyn, float *dxc, float *dxn, dr_layer_grad *G,
-                           uint32_t flags, cudaStream_t st) {
+                           uint32_t flags, cudaStream_t st, Tc2Deferred *defer = nullptr) {
+    Tc2Deferred own_parts;
+    Tc2Deferred *pq = defer ? defer : &own_parts;
     const TapeLayout T = tape_layout(g, L, flags);
     char *tp = (char *)tape;
     const float *hcv = (float *)(tp + T.hc_val), *hnv = (float *)(tp + T.hn_val);
@@ -607,7 +611,7 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
             DR_CHECK(!zsplit, DR_ERR_UNSUPPORTED, "dW: split Z needs the tensor-core reduce");
             return false;
         }
-        launch_tc2_reduce(d, wk, s);
+        launch_tc2_reduce(d, wk, s, pq);
         return true;
     };
     {
@@ -652,6 +656,7 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
         wait_on(st, s1, C.ev[4]);
         wait_on(st, s2, C.ev[5]);
     }
+    if (!defer) launch_tc2_reduce_parts(own_parts, st);   // after the join: every reduce done
 }
 
 // ------------------------------------------------------------------ NCCL (loaded at run time)
@@ -1199,15 +1204,18 @@ static void train_step_body(dr_trainer *t, const dr_graph *g, const float *x_cel
     if (!no_net)                                 // last layer's Y_net feeds nothing: dY_net = 0
         DR_CUDA(cudaMemsetAsync(dyn(0), 0, nn * D * 4, st));
     // ---- backward
+    Tc2Deferred parts;
     int cur = 0;
     for (int l = nl - 1; l >= 0; --l) {
         float *dxc = l > 0 ? dyc(cur ^ 1) : nullptr;
         float *dxn = l > 0 ? dyn(cur ^ 1) : nullptr;
         TagScope tg(ltag[l]);
         const float *dyn_l = (l == nl - 1 && no_net) ? nullptr : dyn(cur);
-        heteroconv_bwd(g, &t->L[l], ws + tape_off[l], dyc(cur), dyn_l, dxc, dxn, &t->G[l], 0, st);
+        heteroconv_bwd(g, &t->L[l], ws + tape_off[l], dyc(cur), dyn_l, dxc, dxn, &t->G[l], 0, st,
+                       &parts);
         cur ^= 1;
     }
+    launch_tc2_reduce_parts(parts, st);          // every layer's weight-gradient sums, one launch
     // ---- data-parallel gradient exchange: one allreduce (sum) of the flat gradient
     // (issued whenever a communicator is given, also at world size 1)
     if (t->comm)

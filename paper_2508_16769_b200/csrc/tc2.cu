@@ -1092,6 +1092,136 @@ __device__ __forceinline__ void red_convert_t(const RdArgs &a, uint8_t *st, int 
     }
 }
 
+// ---- MN-major converters (the specialised shapes): no transposes. dW = A^T B
+// with A = [Z | densify(H)] as [rows][features] and B = mask(dY) as [rows][N]:
+// both operands stay row-major ([K = graph rows][MN]), split in place into bf16
+// hi / lo 128-B-swizzled 64-wide atoms (8 KB each for 64 rows) and are read by
+// the MMA as MN-major operands (cute Layout_MN_SW128: LBO = 8 KB between the
+// 64-wide MN atoms, SBO = 1 KB between 8-row groups, 2 KB per K=16 step).
+// A [64 rows][W] fp32 block: thread ct owns column quad q = ct % (W/4) of rows
+// rg + RG j (RG = 128 / (W/4)); reads and 64-bit swizzled writes are
+// conflict-free.
+template <int W>
+struct MnMap {
+    static constexpr int W4 = W / 4, RG = 128 / W4, NJ = 64 / RG;
+};
+template <int W>
+__device__ __forceinline__ void mn_read(const float *raw, int valid, int ct, const uint8_t *mkraw,
+                                        int mw, int mask_mode, float4 (&v)[MnMap<W>::NJ],
+                                        float *colsum) {
+    using M = MnMap<W>;
+    const int q = ct % M::W4, rg = ct / M::W4, col = 4 * q;
+    const float4 *raw4 = reinterpret_cast<const float4 *>(raw);
+#pragma unroll
+    for (int j = 0; j < M::NJ; ++j) {
+        const int r = rg + M::RG * j;
+        float4 x = raw4[r * M::W4 + q];
+        if (r >= valid) x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (mask_mode != kMask2None) {
+            const uint32_t w = *reinterpret_cast<const uint32_t *>(mkraw + (r * mw + (col >> 5)) * 4);
+            uint32_t b = (w >> (col & 31)) & 0xfu;
+            if (mask_mode == kMask2NotM) b = ~b & 0xfu;
+            if (!(b & 1u)) x.x = 0.f;
+            if (!(b & 2u)) x.y = 0.f;
+            if (!(b & 4u)) x.z = 0.f;
+            if (!(b & 8u)) x.w = 0.f;
+        }
+        v[j] = x;
+        if (colsum) {
+            colsum[0] += x.x;
+            colsum[1] += x.y;
+            colsum[2] += x.z;
+            colsum[3] += x.w;
+        }
+    }
+}
+// hi atoms at tile + 8 KB a, lo atoms at tile + lo_off + 8 KB a
+template <int W>
+__device__ __forceinline__ void mn_write(uint8_t *tile, uint32_t lo_off, int ct,
+                                         const float4 (&v)[MnMap<W>::NJ]) {
+    using M = MnMap<W>;
+    const int q = ct % M::W4, rg = ct / M::W4, c = 4 * q;
+    const uint32_t atom = (uint32_t)(c >> 6) * 8192u;
+#pragma unroll
+    for (int j = 0; j < M::NJ; ++j) {
+        const int r = rg + M::RG * j;
+        uint2 h, l;
+        tc::split_bf16x2(v[j].x, v[j].y, h.x, l.x);
+        tc::split_bf16x2(v[j].z, v[j].w, h.y, l.y);
+        const uint32_t off = atom + tc::sw128_off_h((uint32_t)r, (uint32_t)(c & 63));
+        *reinterpret_cast<uint2 *>(tile + off) = h;
+        *reinterpret_cast<uint2 *>(tile + lo_off + off) = l;
+    }
+}
+template <int G, int WD, int WC, int N>
+__device__ __forceinline__ void red_convert_mn(const RdArgs &a, uint8_t *st, int valid, int ct,
+                                               float *colsum, int bar) {
+    const uint8_t *mk = st + a.off_mask;
+    uint8_t *tz = st;                                   // group 0: Z atoms from 0
+    uint8_t *th = G == 2 ? st + kStage : st + WD * 128; // H atoms (G = 1: right after Z's)
+    float4 vz[MnMap<WD>::NJ];
+    mn_read<WD>(reinterpret_cast<const float *>(tz), valid, ct, mk, 0, kMask2None, vz, nullptr);
+    // CBSR: thread -> graph row r = ct & 63, contiguous half h = ct >> 6 of its k pairs
+    const int kc = WC > 0 ? a.seg[G == 2 ? 1 : 0][G == 2 ? 0 : 1].k : 0;
+    const int r = ct & 63, h = ct >> 6, kh = kc >> 1;
+    float cv[16];
+    uint32_t cw[4];
+    if constexpr (WC > 0) {
+        const uint8_t *cb = st + a.off_cbsr;
+        const float *vals = reinterpret_cast<const float *>(cb) + r * kc + h * kh;
+        const uint8_t *ids = cb + (size_t)kRRows * kc * 4 + r * kc + h * kh;
+        const bool okr = r < valid;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) cv[t] = (t < kh && okr) ? vals[t] : 0.f;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            uint32_t w = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (4 * t + b < kh) w |= (uint32_t)ids[4 * t + b] << (8 * b);
+            cw[t] = okr ? w : 0u;
+        }
+    }
+    tc::named_bar(bar, 128);                              // raw reads done before writes
+    mn_write<WD>(tz, kHalf, ct, vz);
+    {   // zero the H atoms (scattered into below) and, for a lone 64-wide Z, the
+        // unused second feature atom (M = 128 rows of the accumulator)
+        constexpr int ZB = WC > 0 ? WC * 128 : (G == 1 && WD < kTile ? (kTile - WD) * 128 : 0);
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int e0 = 0; e0 < ZB / 16; e0 += 128) {
+            const int e = e0 + ct;
+            if (e < ZB / 16) {
+                *reinterpret_cast<float4 *>(th + 16 * e) = z;
+                *reinterpret_cast<float4 *>(th + kHalf + 16 * e) = z;
+            }
+        }
+    }
+    if constexpr (WC > 0) {
+        tc::named_bar(bar, 128);                          // zeros before the scatter
+        if (r < valid) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+                if (t < kh) {
+                    const int id = (int)((cw[t >> 2] >> (8 * (t & 3))) & 0xffu);
+                    uint32_t hh, ll;
+                    tc::split_bf16x2(cv[t], 0.f, hh, ll);
+                    const uint32_t off = (uint32_t)(id >> 6) * 8192u +
+                                         tc::sw128_off_h((uint32_t)r, (uint32_t)(id & 63));
+                    *reinterpret_cast<uint16_t *>(th + off) = (uint16_t)(hh & 0xffffu);
+                    *reinterpret_cast<uint16_t *>(th + kHalf + off) = (uint16_t)(ll & 0xffffu);
+                }
+        }
+    }
+    {   // B = mask(dY), [rows][N], hi atoms then lo atoms (N * 128 bytes each)
+        uint8_t *tile = st + a.off_b;
+        float4 v[MnMap<N>::NJ];
+        mn_read<N>(reinterpret_cast<const float *>(tile), valid, ct, mk, a.mw, a.mask_mode, v, colsum);
+        tc::named_bar(bar, 128);
+        mn_write<N>(tile, (uint32_t)N * 128u, ct, v);
+    }
+}
+
 template <int G_, int WD_, int WC_, int N_>
 __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid_constant__ RdArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1141,7 +1271,8 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
         }
     } else if (warp == 1) {
         if (lane == 0 && total > 0) {
-            const uint32_t idesc = tc::idesc_bf16(kTile, N);
+            // the specialised shapes read both operands MN-major (bits 15, 16)
+            const uint32_t idesc = tc::idesc_bf16(kTile, N) | (G_ > 0 ? (3u << 15) : 0u);
             for (int64_t it = 0; it < total; ++it) {
                 const int slot = (int)(it % SA);
                 {
@@ -1157,9 +1288,20 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
                     const uint32_t d = tmem + (uint32_t)(g * N);
 #pragma unroll
                     for (int ks = 0; ks < kRRows / 16; ++ks) {
-                        const uint32_t ko = ks * 32;
-                        const uint64_t ah = tc::desc_sw128(sa + ko), al = tc::desc_sw128(sa + kHalf + ko);
-                        const uint64_t bh = tc::desc_sw128(sb + ko), bl = tc::desc_sw128(sb + blo + ko);
+                        uint64_t ah, al, bh, bl;
+                        if constexpr (G_ > 0) {            // K = 16 graph rows = 2 KB
+                            const uint32_t ko = ks * 2048u;
+                            ah = tc::desc_mn_sw128(sa + ko, 8192u, 1024u);
+                            al = tc::desc_mn_sw128(sa + kHalf + ko, 8192u, 1024u);
+                            bh = tc::desc_mn_sw128(sb + ko, 8192u, 1024u);
+                            bl = tc::desc_mn_sw128(sb + blo + ko, 8192u, 1024u);
+                        } else {
+                            const uint32_t ko = ks * 32;
+                            ah = tc::desc_sw128(sa + ko);
+                            al = tc::desc_sw128(sa + kHalf + ko);
+                            bh = tc::desc_sw128(sb + ko);
+                            bl = tc::desc_sw128(sb + blo + ko);
+                        }
                         tc::mma_bf16(d, ah, bh, idesc, (it == 0 && ks == 0) ? 0u : 1u);
                         tc::mma_bf16(d, ah, bl, idesc, 1u);
                         tc::mma_bf16(d, al, bh, idesc, 1u);
@@ -1188,7 +1330,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
             {
                 RDBG_T0;
                 if constexpr (G_ > 0)
-                    red_convert_t<G_, WD_, WC_, N_>(a, sm + (size_t)slot * a.stage_bytes, valid, ct, colsum, bar);
+                    red_convert_mn<G_, WD_, WC_, N_>(a, sm + (size_t)slot * a.stage_bytes, valid, ct, colsum[0], bar);
                 else
                     red_convert(a, sm + (size_t)slot * a.stage_bytes, valid, ct, colsum, bar);
                 if (ct == 0) RDBG_ADD(3);
@@ -1197,13 +1339,20 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&conv[slot]);
         }
-        // db partials: unit (column quad, row octet j) of thread ct, summed over j in a
+        // db partials: per thread unit, then summed over the units of a column in a
         // fixed order
+        for (int e = ct; e < 8 * 128; e += 128) dbs[grp][e >> 7][e & 127] = 0.f;
+        tc::named_bar(3, 256);
+        if constexpr (G_ > 0) {
+            const int q = ct % MnMap<N_>::W4, rg = ct / MnMap<N_>::W4;
+            for (int e = 0; e < 4; ++e) dbs[grp][rg][4 * q + e] = colsum[0][e];
+        } else {
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const Unit x = red_unit(N, ct, i);
-            if (x.ok)
-                for (int e = 0; e < 4; ++e) dbs[grp][x.j][4 * x.fq + e] = colsum[i][e];
+            for (int i = 0; i < 2; ++i) {
+                const Unit x = red_unit(N, ct, i);
+                if (x.ok)
+                    for (int e = 0; e < 4; ++e) dbs[grp][x.j][4 * x.fq + e] = colsum[i][e];
+            }
         }
         tc::named_bar(3, 256);
         if (grp == 0)
@@ -1242,18 +1391,19 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
     }
 }
 
-// Sum per-CTA partials in a fixed order and scatter to the segment outputs.
-struct RdOut {
-    int nout;
-    int g[4], m0[4], w[4];
-    float *dst[4];
-    float *db;
+// Sum per-CTA partials in a fixed order and scatter to the segment outputs; one
+// job per blockIdx.y (several weight gradients in one launch).
+struct PartsJobs {
+    Tc2PartsJob job[Tc2Deferred::kMax];
 };
-__global__ void tc2_reduce_parts_kernel(const float *__restrict__ part, int nparts, int G, int N,
-                                        RdOut o) {
+__global__ void tc2_reduce_parts_kernel(const __grid_constant__ PartsJobs jobs) {
+    const Tc2PartsJob &o = jobs.job[blockIdx.y];
+    const int G = o.G, N = o.N, nparts = o.nparts;
+    const float *__restrict__ part = o.part;
     __shared__ float red[8][33];
     const int64_t len = (int64_t)G * kTile * N + N;
     const int64_t e = (int64_t)blockIdx.x * 32 + threadIdx.x;
+    if ((int64_t)blockIdx.x * 32 >= len) return;          // this job is shorter (block-uniform)
     float acc = 0.f;
     if (e < len)
 #pragma unroll 8
@@ -1533,13 +1683,13 @@ size_t tc2_reduce_work_floats(int G, int N) {
     return (size_t)148 * ((size_t)G * kTile * N + N);
 }
 
-void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s) {
+void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s, Tc2Deferred *defer) {
     DR_CHECK(tc2_reduce_supported(d), DR_ERR_UNSUPPORTED, "tc2_reduce: unsupported shape");
     RdArgs a{};
     a.n = d.n;
     a.N = d.N;
     a.G = d.G;
-    RdOut o{};
+    Tc2PartsJob o{};
     int ncb = 0, maxk = 0;
     for (int g = 0; g < d.G; ++g) {
         a.nseg[g] = d.nseg[g];
@@ -1613,10 +1763,32 @@ void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s) {
                 (long long)d.n, a.N, a.G, a.SA, a.stage_bytes, (long long)a.rows_per_cta, t[8] / 1e3,
                 t[0] / 1e3, t[1] / 1e3, t[2] / 1e3, t[3] / 1e3);
     }
-    const int64_t stride = (int64_t)d.G * kTile * d.N + d.N;
-    tc2_reduce_parts_kernel<<<(unsigned)((stride + 31) / 32), dim3(32, 8), 0, s>>>(work, (int)grid,
-                                                                                   d.G, d.N, o);
+    o.part = work;
+    o.nparts = (int)grid;
+    o.G = d.G;
+    o.N = d.N;
+    if (defer) {
+        DR_CHECK(defer->n < Tc2Deferred::kMax, DR_ERR_INVALID_ARGUMENT, "tc2_reduce: too many deferred");
+        defer->job[defer->n++] = o;
+        return;
+    }
+    Tc2Deferred one;
+    one.job[one.n++] = o;
+    launch_tc2_reduce_parts(one, s);
+}
+
+void launch_tc2_reduce_parts(Tc2Deferred &defer, cudaStream_t s) {
+    if (defer.n == 0) return;
+    PartsJobs j{};
+    int64_t most = 1;
+    for (int i = 0; i < defer.n; ++i) {
+        j.job[i] = defer.job[i];
+        most = std::max<int64_t>(most, (int64_t)defer.job[i].G * kTile * defer.job[i].N + defer.job[i].N);
+    }
+    ProfScope ps("tc_dw_sum", s);
+    tc2_reduce_parts_kernel<<<dim3((unsigned)((most + 31) / 32), (unsigned)defer.n), dim3(32, 8), 0, s>>>(j);
     note_launch("tc2_reduce_parts");
+    defer.n = 0;
 }
 
 }  // namespace dr

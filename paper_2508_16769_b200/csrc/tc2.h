@@ -106,6 +106,25 @@ struct Tc2ReduceDesc {
 };
 bool tc2_reduce_supported(const Tc2ReduceDesc &d);
 size_t tc2_reduce_work_floats(int G, int N);
-void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s);
+// The reduce GEMM leaves per-CTA partials in `work`; a second, fixed-order pass
+// sums them into the gradient tensors (deterministic, no atomics). With `defer`
+// that pass is queued instead of launched, so a whole layer / step sums all its
+// weight gradients in ONE launch (launch_tc2_reduce_parts, on a stream ordered
+// after every queued reduce).
+struct Tc2PartsJob {
+    const float *part = nullptr;
+    int nparts = 0, G = 0, N = 0, nout = 0;
+    int g[4] = {0, 0, 0, 0}, m0[4] = {0, 0, 0, 0}, w[4] = {0, 0, 0, 0};
+    float *dst[4] = {nullptr, nullptr, nullptr, nullptr};
+    float *db = nullptr;
+};
+struct Tc2Deferred {
+    static constexpr int kMax = 8;
+    int n = 0;
+    Tc2PartsJob job[kMax];
+};
+void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s,
+                       Tc2Deferred *defer = nullptr);
+void launch_tc2_reduce_parts(Tc2Deferred &defer, cudaStream_t s);   // flushes (n = 0 after)
 
 }  // namespace dr
