@@ -51,12 +51,27 @@ void make_order(const std::vector<int32_t> &deg, bool identity, const std::vecto
         while ((1 << lg) < d) ++lg;                 // ceil(log2(d)), 0 for d <= 1
         return 1 + (9 - lg);
     };
+    // Locality blocks (DR_ORDER_BLOCK = log2 rows per block, default 12): inside a
+    // class (hub / warp / sub-warp rows, contiguous as the kernels require) rows
+    // are grouped into blocks of 2^lb consecutive locality ranks and degree-bucketed
+    // inside a block, so the rows in flight at once stay spatially close (their
+    // shared neighbours hit L2) while each warp still sees similar degrees. lb < 0:
+    // one block (degree buckets major, the round-1 order). Default (-2): blocks of
+    // 4096 from 256k rows on (C4: SIMT SpMM + SSpMM -3 %), degree-major below (the
+    // working set of a C2 / C5 graph is L2-resident anyway and mixed degrees cost
+    // balance: +3-6 %; profiles/r02/ab_order.txt).
+    int lb = (int)knobs().order_block;
+    if (lb == -2) lb = n >= (1 << 18) ? 12 : -1;
     std::vector<int64_t> key((size_t)n);
     for (int32_t i = 0; i < n; ++i) {
         const int b = bucket(i);
-        const int64_t inner = b == 0 ? (int64_t)(INT32_MAX - deg[i])
-                                     : (loc.empty() ? (int64_t)i : loc[i]);
-        key[i] = ((int64_t)b << 40) | inner;
+        const int cls = b == 0 ? 0 : (deg[i] > warp_deg ? 1 : 2);
+        const int64_t l = loc.empty() ? (int64_t)i : loc[i];
+        int64_t inner;
+        if (b == 0) inner = (int64_t)(INT32_MAX - deg[i]);
+        else if (lb < 0) inner = ((int64_t)b << 32) | (l & 0xffffffffLL);
+        else inner = ((l >> lb) << 36) | ((int64_t)b << 32) | (l & 0xffffffffLL);
+        key[i] = ((int64_t)cls << 60) | inner;
     }
     std::stable_sort(order.begin(), order.end(),
                      [&](int32_t x, int32_t y) { return key[x] < key[y]; });
