@@ -238,13 +238,18 @@ static void check_layer(const dr_graph *g, const dr_layer *L) {
              "layer: bad merge");
 }
 
-// Z of relation r in the tape as split bf16 rows ([hi | lo], the tc2 operand
-// format the projection can TMA-load without its fp32 -> hi/lo split). Off: the
-// other consumer, the dW reduce kernel, would need its own split-aware operand
-// path; a converter-transpose version measured a net loss at C2 and C4 (and its
-// code pushed the reduce kernels into register spills), so the producer and
-// projection paths stay for a future MN-major TMA dW operand.
-static bool z_split_ok(const dr_layer *, int) { return false; }
+// Z of relation r in the tape as split bf16 rows ([hi | lo], x = hi + lo with the
+// same rounding as the converters'): the SpMM epilogues write them, and both
+// consumers TMA-load them as ready operand tiles -- the projection (K-major
+// SW128) and the dW reduce GEMM (MN-major atoms) -- with no conversion. On for
+// the square layers whose consumers take that path (every width 64 or 128,
+// k <= 32 CBSR roots); bit-identical to converting fp32 Z.
+static bool z_split_ok(const dr_layer *L, int) {
+    if (knobs().dense_simt || !knobs().z_split) return false;
+    const int D = L->d_out;
+    return (D == 64 || D == 128) && L->d_cell == D && L->d_net == D && L->k_cell <= 32 &&
+           L->k_net <= 32;
+}
 
 // ------------------------------------------------------------------ layer forward / backward
 // Ln / tape_next (row a5): the next layer and its tape; when given, the

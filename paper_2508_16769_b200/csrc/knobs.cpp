@@ -38,6 +38,7 @@ static Knobs read_env() {
     k.shard_tiles = env_i("DR_SHARD_TILES", 0);
     k.shard_tiles_t = env_i("DR_SHARD_TILES_T", 0);
     k.chain = env_i("DR_CHAIN", 1);
+    k.z_split = env_i("DR_Z_SPLIT", 1);
     k.order_block = env_i("DR_ORDER_BLOCK", -2);
     k.skip_dead_net = env_i("DR_SKIP_DEAD_NET", 1);
     return k;
@@ -76,6 +77,7 @@ extern "C" dr_status dr_debug_set(const char *name, int64_t value) {
         {"shard_tiles", &g_knobs.shard_tiles},
         {"shard_tiles_t", &g_knobs.shard_tiles_t},
         {"chain", &g_knobs.chain},
+        {"z_split", &g_knobs.z_split},
         {"order_block", &g_knobs.order_block},
         {"skip_dead_net", &g_knobs.skip_dead_net},
     };

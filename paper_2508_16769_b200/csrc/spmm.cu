@@ -242,11 +242,25 @@ __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
                           ng_k(a.ng, e1 - e0, a.k), smask);
     }
     __syncwarp();
-    if (valid) {
-        const float cr = __ldg(a.c + row);
-        for (int c4 = ll; c4 < D4; c4 += L) {
-            const float4 v = acc4[c4];
-            store_z4(a, row, c4, make_float4(cr * v.x, cr * v.y, cr * v.z, cr * v.w));
+    // the warp's R accumulator rows are contiguous in shared memory: store them
+    // together, D/4 consecutive lanes per row (coalesced rows, also for split Z)
+    const float4 *w4 = reinterpret_cast<const float4 *>(sm + (size_t)wid * R * D);
+    const int64_t pos0 = (int64_t)a.n_hub + a.n_warp + gw * R;
+    const int rpi = (D4 < 32 && 32 % D4 == 0) ? 32 / D4 : 1;      // rows per warp pass
+    const int lr = rpi > 1 ? lane / D4 : 0, lc = rpi > 1 ? lane - lr * D4 : lane;
+    const int cstep = rpi > 1 ? D4 : 32;
+    // row ids and scales of the warp's R rows, fetched at once (lane r holds row r)
+    const bool lok = lane < R && pos0 + lane < a.n_rows;
+    const int rw_l = lok ? __ldg(a.order + pos0 + lane) : 0;
+    const float cr_l = lok ? __ldg(a.c + rw_l) : 0.f;
+    for (int r0 = 0; r0 < R; r0 += rpi) {
+        const int r = r0 + lr;
+        const int rw = __shfl_sync(0xffffffffu, rw_l, r & 31);
+        const float cr = __shfl_sync(0xffffffffu, cr_l, r & 31);
+        if (r >= R || pos0 + r >= a.n_rows) continue;
+        for (int c4 = lc; c4 < D4; c4 += cstep) {
+            const float4 v = w4[r * D4 + c4];
+            store_z4(a, rw, c4, make_float4(cr * v.x, cr * v.y, cr * v.z, cr * v.w));
         }
     }
 }

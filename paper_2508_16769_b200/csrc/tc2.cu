@@ -727,6 +727,7 @@ struct RdSeg {
     int split;                         // Z rows are [hi | lo] bf16 halves
 };
 struct RdArgs {
+    CUtensorMap zmap[2][2];            // split Z segments: [n x 2w] bf16, box 64 cols x 64 rows, SW128
     int64_t n;
     int N, G;
     int nseg[2];
@@ -753,7 +754,8 @@ __device__ __forceinline__ void red_produce(const RdArgs &a, int64_t rb, int64_t
     for (int g = 0; g < a.G; ++g)
         for (int q = 0; q < a.nseg[g]; ++q) {
             const RdSeg &s = a.seg[g][q];
-            if (s.Z) bytes += (uint32_t)rows * s.w * 4;
+            if (s.Z && s.split) bytes += 2u * (uint32_t)(s.w / 64) * 8192u;   // full TMA boxes
+            else if (s.Z) bytes += (uint32_t)rows * s.w * 4;
             else bytes += rup16((uint32_t)rows * s.k * 4) + rup16((uint32_t)rows * s.k);
         }
     bytes += (uint32_t)rows * a.N * 4;
@@ -764,7 +766,15 @@ __device__ __forceinline__ void red_produce(const RdArgs &a, int64_t rb, int64_t
         for (int g = 0; g < a.G; ++g)
             for (int q = 0; q < a.nseg[g]; ++q) {
                 const RdSeg &s = a.seg[g][q];
-                if (s.Z) {
+                if (s.Z && s.split) {
+                    // the [hi | lo] bf16 rows land as MN-major SW128 atoms: no conversion
+                    // (rows past n arrive as zeros)
+                    for (int at = 0; at < s.w / 64; ++at) {
+                        uint8_t *dst = st + (size_t)g * kStage + (size_t)(s.m0 / 64 + at) * 8192;
+                        tc::tma_load_2d(dst, &a.zmap[g][q], at * 64, (int)rb, full);
+                        tc::tma_load_2d(dst + kHalf, &a.zmap[g][q], s.w + at * 64, (int)rb, full);
+                    }
+                } else if (s.Z) {
                     tc::bulk_g2s(st + (size_t)g * kStage, s.Z + rb * s.w, (uint32_t)rows * s.w * 4, full);
                 } else {
                     uint8_t *cb = st + a.off_cbsr + (size_t)ci * a.cbsr_seg_bytes;
@@ -1160,7 +1170,8 @@ __device__ __forceinline__ void red_convert_mn(const RdArgs &a, uint8_t *st, int
     uint8_t *tz = st;                                   // group 0: Z atoms from 0
     uint8_t *th = G == 2 ? st + kStage : st + WD * 128; // H atoms (G = 1: right after Z's)
     float4 vz[MnMap<WD>::NJ];
-    mn_read<WD>(reinterpret_cast<const float *>(tz), valid, ct, mk, 0, kMask2None, vz, nullptr);
+    const bool zsplit = a.seg[0][0].split != 0;         // Z landed as operand atoms (TMA)
+    if (!zsplit) mn_read<WD>(reinterpret_cast<const float *>(tz), valid, ct, mk, 0, kMask2None, vz, nullptr);
     // CBSR: thread -> graph row r = ct & 63, contiguous half h = ct >> 6 of its k pairs
     const int kc = WC > 0 ? a.seg[G == 2 ? 1 : 0][G == 2 ? 0 : 1].k : 0;
     const int r = ct & 63, h = ct >> 6, kh = kc >> 1;
@@ -1183,7 +1194,7 @@ __device__ __forceinline__ void red_convert_mn(const RdArgs &a, uint8_t *st, int
         }
     }
     tc::named_bar(bar, 128);                              // raw reads done before writes
-    mn_write<WD>(tz, kHalf, ct, vz);
+    if (!zsplit) mn_write<WD>(tz, kHalf, ct, vz);
     {   // zero the H atoms (scattered into below) and, for a lone 64-wide Z, the
         // unused second feature atom (M = 128 rows of the accumulator)
         constexpr int ZB = WC > 0 ? WC * 128 : (G == 1 && WD < kTile ? (kTile - WD) * 128 : 0);
@@ -1475,10 +1486,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // output map: [n x W] fp32 row-major, box = 16 columns x 32 rows, SWIZZLE_64B
 // [n x 2K] bf16 split rows ([hi | lo]), box = 64 columns x 128 rows, 128-B swizzle
 // (= the K-major SW128 operand tile layout)
-static void make_tmap_split(CUtensorMap *m, const float *A, int64_t n, int K) {
+static void make_tmap_split(CUtensorMap *m, const float *A, int64_t n, int K, int box_rows = kTile) {
     const cuuint64_t dims[2] = {(cuuint64_t)(2 * K), (cuuint64_t)n};
     const cuuint64_t strides[1] = {(cuuint64_t)K * 4};
-    const cuuint32_t box[2] = {(cuuint32_t)kChunk, (cuuint32_t)kTile};
+    const cuuint32_t box[2] = {(cuuint32_t)kChunk, (cuuint32_t)box_rows};
     const cuuint32_t es[2] = {1, 1};
     const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void *)A, dims, strides,
                                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1647,6 +1658,21 @@ static void red_layout(const Tc2ReduceDesc &d, int ncb, int maxk, RdArgs &a) {
     a.SA = (int)std::min<size_t>(kMaxSA, (size_t)kSmemBudgetRed / a.stage_bytes);
 }
 
+// The specialised (MN-major) reduce shapes: 1 = [Z 64 | H 64] N 64, 2 = Z 128 / H 128
+// in two groups N 128, 3 = Z 64 N 64, 4 = Z 128 N 128; 0 = the generic kernel.
+static int red_variant(const Tc2ReduceDesc &d) {
+    auto is_seg = [&](int g, int q, bool dense, int w) {
+        return d.seg[g][q].w == w && (d.seg[g][q].Z != nullptr) == dense && (dense || d.seg[g][q].k <= 32);
+    };
+    if (d.G == 1 && d.nseg[0] == 2 && d.N == 64 && is_seg(0, 0, true, 64) && is_seg(0, 1, false, 64)) return 1;
+    if (d.G == 2 && d.nseg[0] == 1 && d.nseg[1] == 1 && d.N == 128 && is_seg(0, 0, true, 128) &&
+        is_seg(1, 0, false, 128))
+        return 2;
+    if (d.G == 1 && d.nseg[0] == 1 && d.N == 64 && is_seg(0, 0, true, 64)) return 3;
+    if (d.G == 1 && d.nseg[0] == 1 && d.N == 128 && is_seg(0, 0, true, 128)) return 4;
+    return 0;
+}
+
 bool tc2_reduce_supported(const Tc2ReduceDesc &d) {
     if (knobs().dense_simt) return false;
     if (d.N < 16 || d.N > 128 || d.N % 16) return false;
@@ -1665,6 +1691,9 @@ bool tc2_reduce_supported(const Tc2ReduceDesc &d) {
             }
         }
         if (w > 128 || dense > 1 || cb > 1) return false;
+        // split Z rows (TMA-loaded operand atoms) only on the MN-major shapes
+        for (int q = 0; q < d.nseg[g]; ++q)
+            if (d.seg[g][q].Z && d.seg[g][q].split && red_variant(d) == 0) return false;
     }
     if (d.mask_mode != kMask2None && (d.N + 31) / 32 > 8) return false;
     int ncb = 0, maxk = 0;
@@ -1696,8 +1725,8 @@ void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s, Tc2D
         int m0 = 0;
         for (int q = 0; q < d.nseg[g]; ++q) {
             const Tc2RedSeg &sd = d.seg[g][q];
-            DR_CHECK(!sd.split, DR_ERR_UNSUPPORTED, "tc2_reduce: split Z rows are not supported");
-            a.seg[g][q] = RdSeg{sd.Z, sd.hval, sd.hidx, sd.k, sd.w, m0, 0};
+            a.seg[g][q] = RdSeg{sd.Z, sd.hval, sd.hidx, sd.k, sd.w, m0, sd.Z && sd.split ? 1 : 0};
+            if (sd.Z && sd.split) make_tmap_split(&a.zmap[g][q], sd.Z, d.n, sd.w, kRRows);
             if (!sd.Z) {
                 ++ncb;
                 maxk = std::max(maxk, sd.k);
@@ -1731,19 +1760,12 @@ void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s, Tc2D
         a.dbg = dbg_buf;
     }
     // specialised converters for the square-layer shapes; generic otherwise
-    auto is_seg = [&](int g, int q, bool dense, int w) {
-        return d.seg[g][q].w == w && (d.seg[g][q].Z != nullptr) == dense && (dense || d.seg[g][q].k <= 32);
-    };
-    const void *fn = (const void *)tc2_reduce_kernel<0, 0, 0, 0>;
-    if (d.G == 1 && d.nseg[0] == 2 && d.N == 64 && is_seg(0, 0, true, 64) && is_seg(0, 1, false, 64))
-        fn = (const void *)tc2_reduce_kernel<1, 64, 64, 64>;
-    else if (d.G == 2 && d.nseg[0] == 1 && d.nseg[1] == 1 && d.N == 128 && is_seg(0, 0, true, 128) &&
-             is_seg(1, 0, false, 128))
-        fn = (const void *)tc2_reduce_kernel<2, 128, 128, 128>;
-    else if (d.G == 1 && d.nseg[0] == 1 && d.N == 64 && is_seg(0, 0, true, 64))
-        fn = (const void *)tc2_reduce_kernel<1, 64, 0, 64>;
-    else if (d.G == 1 && d.nseg[0] == 1 && d.N == 128 && is_seg(0, 0, true, 128))
-        fn = (const void *)tc2_reduce_kernel<1, 128, 0, 128>;
+    const int var = red_variant(d);
+    const void *fn = var == 1 ? (const void *)tc2_reduce_kernel<1, 64, 64, 64>
+                   : var == 2 ? (const void *)tc2_reduce_kernel<2, 128, 128, 128>
+                   : var == 3 ? (const void *)tc2_reduce_kernel<1, 64, 0, 64>
+                   : var == 4 ? (const void *)tc2_reduce_kernel<1, 128, 0, 128>
+                              : (const void *)tc2_reduce_kernel<0, 0, 0, 0>;
     ensure_smem(fn, smem);
     {
         void *args[] = {(void *)&a};

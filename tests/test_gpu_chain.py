@@ -166,3 +166,32 @@ def test_chain_errors(designs):
     with pytest.raises(dr.DRError) as e:
         dr.heteroconv_fwd_chain(g, L1, xc, xn, next_layer=Lp)
     assert e.value.status == 12
+
+
+@pytest.mark.parametrize("name,D,k", [("C2s", 64, 8), ("C4s", 128, 16)])
+def test_split_z_bit_identical(designs, knob, name, D, k):
+    """Z stored as split bf16 rows (read by the projection and the MN-major dW
+    kernel as ready operand tiles) gives bit-identical outputs and gradients to
+    fp32 Z converted by each consumer (same rounding)."""
+    d = designs[name]
+    g = dr.Graph.from_design(d)
+    P = make_params(D, D, D, 1, seed=4)
+    L, _ = _layer(P, 0, D, D, D, k, k)
+    rng = np.random.default_rng(3)
+    xc = cuda(rng.standard_normal((d.n_cell, D)).astype(np.float32))
+    xn = cuda(rng.standard_normal((d.n_net, D)).astype(np.float32))
+    dyc = cuda(rng.standard_normal((d.n_cell, D)).astype(np.float32))
+    dyn = cuda(rng.standard_normal((d.n_net, D)).astype(np.float32))
+    out = {}
+    for zs in (0, 1):
+        knob("z_split", zs, 1)
+        yc, yn, tape = dr.heteroconv_fwd(g, L, xc, xn)
+        v = dr.tape_view(g, L, tape)
+        assert v["z_split"] == [zs, zs, zs]
+        grads, dxc, dxn = dr.heteroconv_bwd(g, L, tape, dyc, dyn, need_dx=True)
+        out[zs] = (yc, yn, grads, dxc, dxn)
+    a, b = out[0], out[1]
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    assert torch.equal(a[3], b[3]) and torch.equal(a[4], b[4])
+    for key in a[2]:
+        assert torch.equal(a[2][key], b[2][key]), key

@@ -400,6 +400,9 @@ def test_dense_tcgen05_matches_simt(designs, name, dc, dn, D, kc, kn, knob):
     relative, and dX stacks the dz GEMM, the SSpMM and the root term."""
     d = designs[name]
     g = _graph(d)
+    # one tape feeds both backward paths: keep Z in fp32 (the SIMT kernels do not
+    # read split Z; test_gpu_chain.py::test_split_z_bit_identical covers split Z)
+    knob("z_split", 0, 1)
     P = make_params(dc, dn, D, 1, seed=8)
     L, W = _layer(P, 0, dc, dn, D, kc, kn)
     rng = np.random.default_rng(12)
