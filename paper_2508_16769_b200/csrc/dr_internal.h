@@ -54,6 +54,7 @@ struct Knobs {
     int64_t shard_tiles_t = 0;   // DR_SHARD_TILES_T: tiled backward for shard blocks
     int64_t order_block = -2;    // DR_ORDER_BLOCK: log2 rows per locality block of the SIMT orders (-1: degree-major, -2: by size)
     int64_t z_split = 1;         // DR_Z_SPLIT=0: Z stored fp32 (converted by each consumer)
+    int64_t drelu_coop = -2;     // DR_DRELU_COOP: lanes per row of the thread-per-row D-ReLU (-2 auto, 0 off)
     int64_t chain = 1;           // DR_CHAIN=0: trainer without the fused next-layer D-ReLU
     int64_t skip_dead_net = 1;   // DR_SKIP_DEAD_NET=0: trainer computes the last layer's Y_net
 };

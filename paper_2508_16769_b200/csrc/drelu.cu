@@ -384,10 +384,183 @@ void launch_tpr(const float *x, int64_t n, int64_t ldx, float *val, uint8_t *idx
     drelu_tpr_kernel<D, K, SORTED><<<(unsigned)blocks, 128, smem, s>>>(x, n, ldx, val, idx);
 }
 
+// Cooperative thread-per-row (ascending-column CBSR): T consecutive lanes share a
+// row, each taking D/T consecutive columns of the staged row: a per-lane network
+// (composites sorted in groups of K, merged keeping the larger K), then log2 T
+// butterfly steps exchange the running top K with __shfl_xor and merge it (both
+// partners end with the same K, and the largest discarded composite). Same
+// composites and the same exact rerun as tpr_select_row, so the selection is
+// identical; a thread holds D/T composites instead of D -- fewer registers, T
+// times more threads per row, more warps resident for the latency-bound network.
+template <int D, int K, int T>
+__global__ void __launch_bounds__(128) drelu_tcoop_kernel(const float *__restrict__ x, int64_t n,
+                                                          int64_t ldx, float *__restrict__ val,
+                                                          uint8_t *__restrict__ idx) {
+    constexpr int P = D + 4, Q = D / 4, RW = 32 / T, W = D / T;   // rows per warp, columns per lane
+    constexpr int CB = D == 32 ? 5 : D == 64 ? 6 : 7;
+    constexpr uint32_t CM = (1u << CB) - 1u;
+    static_assert(W >= K && W % 4 == 0, "each lane needs >= K columns");
+    extern __shared__ __align__(16) float tco_sm[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int rl = lane / T, sl = lane % T;                        // row of the warp, slice
+    // two staging buffers per warp: the next row group streams in (cp.async, no
+    // registers) while this one is reduced
+    float *xsb = tco_sm + (size_t)wid * 2 * RW * P;
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    constexpr int NL = RW * Q / 32;                                // float4 copies per lane
+    auto issue = [&](int64_t rb, float *dst) {
+#pragma unroll
+        for (int u = 0; u < NL; ++u) {
+            const int e = lane + 32 * u, i = e / Q, c4 = e % Q;
+            float *d = dst + i * P + 4 * c4;
+            if (rb + i < n) {
+                const float *src = x + (rb + i) * ldx + 4 * c4;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(d)),
+                             "l"(src)
+                             : "memory");
+            } else {
+                *reinterpret_cast<float4 *>(d) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int buf = 0;
+    if (gw * RW < n) issue(gw * RW, xsb);
+    for (int64_t r0 = gw * RW; r0 < n; r0 += nw * RW) {
+        float *xs = xsb + (size_t)buf * RW * P;
+        const int64_t nx = r0 + nw * RW;
+        if (nx < n) {
+            issue(nx, xsb + (size_t)(buf ^ 1) * RW * P);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncwarp();
+        const int64_t r = r0 + rl;
+        const float *xr = xs + rl * P;
+        uint32_t w[W];
+#pragma unroll
+        for (int c4 = 0; c4 < W / 4; ++c4) {
+            const uint32_t c = (uint32_t)(sl * W + 4 * c4);
+            const float4 q = *reinterpret_cast<const float4 *>(xr + c);
+            w[4 * c4 + 0] = (order_key(q.x) & ~CM) | (CM - (c + 0));
+            w[4 * c4 + 1] = (order_key(q.y) & ~CM) | (CM - (c + 1));
+            w[4 * c4 + 2] = (order_key(q.z) & ~CM) | (CM - (c + 2));
+            w[4 * c4 + 3] = (order_key(q.w) & ~CM) | (CM - (c + 3));
+        }
+#pragma unroll
+        for (int g = 0; g < W / K; ++g) bitonic_sort_desc<K>(w + g * K);
+        uint32_t lost = 0;
+#pragma unroll
+        for (int step = 1; step < W / K; step <<= 1)
+#pragma unroll
+            for (int g = 0; g + step < W / K; g += 2 * step)
+                lost = max(lost, merge_keep_desc<K>(w + g * K, w + (g + step) * K));
+        // butterfly over the T lanes of the row
+#pragma unroll
+        for (int m = 1; m < T; m <<= 1) {
+            uint32_t b[K];
+#pragma unroll
+            for (int t = 0; t < K; ++t) b[t] = __shfl_xor_sync(0xffffffffu, w[t], m);
+            lost = max(lost, __shfl_xor_sync(0xffffffffu, lost, m));
+            lost = max(lost, merge_keep_desc<K>(w, b));
+        }
+        uint32_t col[K];
+#pragma unroll
+        for (int t = 0; t < K; ++t) col[t] = CM - (w[t] & CM);
+        const bool valid = r < n;
+        const bool rerun = (lost & ~CM) == (w[K - 1] & ~CM);
+        if (valid && rerun) {
+            // exact (rare): the K-th largest full key by bisection over the staged row
+            uint32_t Tk = 0;
+            for (int bb = 31; bb >= 0; --bb) {
+                const uint32_t cand = Tk | (1u << bb);
+                int cnt = 0;
+                for (int j = 0; j < D; ++j) cnt += order_key(xr[j]) >= cand;
+                if (cnt >= K) Tk = cand;
+            }
+            int gt = 0;
+            for (int j = 0; j < D; ++j) gt += order_key(xr[j]) > Tk;
+            int need = K - gt, q = 0;
+            uint32_t sel[K];
+            for (int j = 0; j < D; ++j) {
+                const uint32_t kj = order_key(xr[j]);
+                const bool take = kj > Tk || (kj == Tk && need > 0);
+                if (take && kj == Tk) --need;
+                if (take) {
+#pragma unroll
+                    for (int t = 0; t < K; ++t)
+                        if (t == q) sel[t] = (uint32_t)j;
+                    ++q;
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < K; ++t) col[t] = sel[K - 1 - t];   // descending, like below
+        } else {
+            bitonic_sort_desc<K>(col);
+        }
+        // lane sl of the row writes pairs [sl K / T, (sl + 1) K / T) (ascending columns)
+        if (valid) {
+            constexpr int KT = K / T > 0 ? K / T : 1;
+            if (sl * KT < K) {
+#pragma unroll
+                for (int t = 0; t < KT; ++t) {
+                    const int o = sl * KT + t;                      // output slot
+                    uint32_t c = 0;
+#pragma unroll
+                    for (int u = 0; u < K; ++u)
+                        if (u == K - 1 - o) c = col[u];
+                    val[r * K + o] = xr[c];
+                    idx[r * K + o] = (uint8_t)c;
+                }
+            }
+        }
+        __syncwarp();                      // every read of xs done before it is refilled
+        buf ^= 1;
+    }
+}
+
+template <int D, int K, int T>
+void launch_tcoop(const float *x, int64_t n, int64_t ldx, float *val, uint8_t *idx, cudaStream_t s) {
+    const size_t smem = (size_t)4 * 2 * (32 / T) * (D + 4) * sizeof(float);
+    const void *fn = (const void *)drelu_tcoop_kernel<D, K, T>;
+    ensure_smem(fn, smem);
+    static int ps = 0;
+    if (ps == 0) {
+        DR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, 128, smem));
+        if (ps < 1) ps = 1;
+    }
+    const int64_t groups = (n + 32 / T - 1) / (32 / T);
+    const int64_t cap = (int64_t)148 * ps;
+    int64_t blocks = (groups + 3) / 4;
+    if (blocks > cap) blocks = cap;
+    drelu_tcoop_kernel<D, K, T><<<(unsigned)blocks, 128, smem, s>>>(x, n, ldx, val, idx);
+}
+
 template <bool SORTED>
 bool try_tpr(const float *x, int64_t n, int dim, int64_t ldx, int k, float *val, uint8_t *idx,
              cudaStream_t s) {
     if ((ldx % 4) != 0 || (reinterpret_cast<uintptr_t>(x) % 16) != 0) return false;
+    // cooperative rows: default (-2) two lanes per row at D = 128, k <= 16 (C4:
+    // 0.32 -> 0.29 ms at k = 16, 0.25 -> 0.22 ms at k = 8; no gain at D = 64 --
+    // profiles/r02/ab_drelu_coop.json); 0 = off, 1 / 2 / 4 = forced (A/B)
+    int T = (int)knobs().drelu_coop;
+    if (T == -2) T = (dim == 128 && k >= 4 && k <= 16) ? 2 : 0;
+    if (!SORTED && T > 0) {
+#define DR_TCO(DD, KK, TT)                                                                  \
+        if (dim == DD && k == KK && T == TT) {                                              \
+            launch_tcoop<DD, KK, TT>(x, n, ldx, val, idx, s);                               \
+            return true;                                                                    \
+        }
+        DR_TCO(128, 4, 1) DR_TCO(128, 8, 1) DR_TCO(128, 16, 1)
+        DR_TCO(64, 4, 1) DR_TCO(64, 8, 1) DR_TCO(64, 16, 1)
+        DR_TCO(128, 4, 2) DR_TCO(128, 8, 2) DR_TCO(128, 16, 2)
+        DR_TCO(128, 4, 4) DR_TCO(128, 8, 4) DR_TCO(128, 16, 4)
+        DR_TCO(64, 4, 2) DR_TCO(64, 8, 2) DR_TCO(64, 16, 2)
+        DR_TCO(64, 4, 4) DR_TCO(64, 8, 4) DR_TCO(64, 16, 4)
+#undef DR_TCO
+    }
 #define DR_TPR(DD, KK)                                                                      \
     if (dim == DD && k == KK) {                                                             \
         launch_tpr<DD, KK, SORTED>(x, n, ldx, val, idx, s);                                 \

@@ -1,0 +1,34 @@
+"""Every D-ReLU kernel variant (Eq. 2-3) is bit-exact against the
+oracle on tie-heavy rows: the cooperative thread-per-row network at 1, 2 and 4
+lanes per row (knob drelu_coop), the whole-row network and the warp-per-row
+kernels (knob drelu_tpr), at the D / k the workloads use."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+from parity_util import to_np
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+dr = pytest.importorskip("paper_2508_16769_b200")
+
+
+@pytest.mark.parametrize("dim,k", [(128, 16), (128, 8), (128, 4), (64, 8), (64, 16), (64, 4)])
+@pytest.mark.parametrize("coop,tpr", [(1, 1), (2, 1), (4, 1), (0, 1), (0, 0)])
+def test_drelu_variants_bitexact(knob, dim, k, coop, tpr):
+    knob("drelu_coop", coop, -2)
+    knob("drelu_tpr", tpr, 1)
+    rng = np.random.default_rng(dim + 7 * k + coop)
+    x = rng.standard_normal((5003, dim)).astype(np.float32)        # ragged tail of a 32-row group
+    x[:400] = rng.integers(-2, 3, size=(400, dim)).astype(np.float32)
+    x[400] = 0.0
+    x[401, ::2] = -0.0
+    x[402:410] = np.float32(0.75) + rng.integers(0, 3, size=(8, dim)).astype(np.float32) * np.spacing(np.float32(0.75))
+    xg = torch.as_tensor(x).cuda()
+    val, idx = dr.drelu_topk(xg, k)
+    oi, ov = O.drelu(x.astype(np.float64), k)
+    assert np.array_equal(to_np(idx).astype(np.int32), oi)
+    assert np.array_equal(to_np(val), ov.astype(np.float32))
+    assert np.array_equal(np.signbit(to_np(val)), np.signbit(ov))
