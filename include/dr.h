@@ -393,6 +393,35 @@ dr_status dr_shard_spmm_bwd(const dr_shard *s, const float *dz_local, const dr_c
 dr_status dr_shard_reduce_scatter_g(const dr_shard *s, const float *g_part,
                                     const dr_cbsr *h_local, float *g_local, float *dx_local,
                                     void *nccl_comm, void *stream);
+/* ---- the exchange fused into the SpMM over peer memory (f4, beyond the paper).
+ * Instead of an allgather of the CBSR and a reduce-scatter of g, the SIMT SpMM
+ * kernels read every remote source row IN PLACE from its owner's buffer and the
+ * backward writes every per-source contribution IN PLACE into the owner's inbox
+ * -- over NVLink when the owner is another GPU (P2P loads / stores inside the
+ * compute kernel, so the transfer overlaps the math row by row), plain loads
+ * when ranks share a device. val[q] / idx[q]: rank q's LOCAL CBSR (max_src rows,
+ * k pairs, idx uint8) as device pointers usable on this device (cudaIpc- or
+ * symmetric-memory-mapped peers; `peer_buffers` in the Python binding). The
+ * caller orders the ranks: every owner's CBSR written before any rank's
+ * _fwd_peer / _bwd_peer reads it, every rank's _bwd_peer done before the owner's
+ * _inbox_reduce (e.g. a barrier). world <= 8. */
+typedef struct {
+    int32_t world;
+    const float *val[8];
+    const void *idx[8];
+} dr_peer_cbsr;
+/* z_local as dr_shard_spmm_fwd (bit-identical to it on the allgathered CBSR). */
+dr_status dr_shard_spmm_fwd_peer(const dr_shard *s, const dr_peer_cbsr *h, int32_t dim, int32_t k,
+                                 float *z_local, void *stream);
+/* inbox[q]: owner q's inbox, DEVICE [world x max_src x k] usable on this device;
+ * this rank writes its contributions to owner q's sources into slot `rank`
+ * (every slot row of every owner, zeros for sources without local edges). */
+dr_status dr_shard_spmm_bwd_peer(const dr_shard *s, const float *dz_local, const dr_peer_cbsr *h,
+                                 int32_t dim, int32_t k, float *const *inbox, void *stream);
+/* g_local [max_src x k] = sum over slots p = 0 .. world-1 of inbox_local[p] in
+ * that fixed order (deterministic); dx_local as dr_shard_reduce_scatter_g. */
+dr_status dr_shard_inbox_reduce(const dr_shard *s, const float *inbox_local, const dr_cbsr *h_local,
+                                float *g_local, float *dx_local, void *stream);
 
 /* Per-kernel device timing: between dr_profile_begin and dr_profile_end every
  * libdr launch issued by this host thread is bracketed by CUDA events on the

@@ -378,6 +378,45 @@ class Shard:
                                               _stream(stream)))
         return g_l, dx
 
+    # ---- the exchange fused into the SpMM over peer memory (dr_shard_spmm_*_peer)
+    def _peer(self, peers):
+        from ._lib import dr_peer_cbsr
+        pc = dr_peer_cbsr()
+        pc.world = self.world
+        for q, (v, i) in enumerate(peers):
+            pc.val[q] = v if isinstance(v, int) else v.data_ptr()
+            pc.idx[q] = i if isinstance(i, int) else i.data_ptr()
+        return pc
+
+    def spmm_fwd_peer(self, peers, dim, k, out=None, device="cuda", stream=None):
+        """peers: per rank q (val_q, idx_q) -- tensors on this device or raw device
+        pointers (peer-mapped) -- of rank q's local CBSR (max_src x k)."""
+        torch = _torch()
+        z = out if out is not None else torch.empty((self.dst_end - self.dst_begin, dim),
+                                                     device=device, dtype=torch.float32)
+        pc = self._peer(peers)
+        check(lib().dr_shard_spmm_fwd_peer(self.handle, C.byref(pc), int(dim), int(k), _ptr(z),
+                                           _stream(stream)))
+        return z
+
+    def spmm_bwd_peer(self, dz_l, peers, dim, k, inboxes, stream=None):
+        """inboxes: per owner q its inbox ([world x max_src x k] fp32, tensor or raw
+        device pointer); this rank writes slot `rank` of each."""
+        pc = self._peer(peers)
+        arr = (C.c_void_p * 8)(*[(x if isinstance(x, int) else x.data_ptr()) for x in inboxes])
+        check(lib().dr_shard_spmm_bwd_peer(self.handle, _ptr(dz_l), C.byref(pc), int(dim), int(k),
+                                           arr, _stream(stream)))
+
+    def inbox_reduce(self, inbox, val_l, idx_l, dim, want_dx=True, stream=None):
+        torch = _torch()
+        g_l = torch.empty(tuple(val_l.shape), device=val_l.device, dtype=torch.float32)
+        dx = (torch.empty((self.max_src, dim), device=val_l.device, dtype=torch.float32)
+              if want_dx else None)
+        hl = _cbsr(val_l, idx_l, dim)
+        check(lib().dr_shard_inbox_reduce(self.handle, _ptr(inbox), C.byref(hl), _ptr(g_l),
+                                          _ptr(dx), _stream(stream)))
+        return g_l, dx
+
     def close(self):
         if getattr(self, "handle", None):
             lib().dr_shard_destroy(self.handle)
@@ -595,6 +634,22 @@ class Trainer:
             self.close()
         except Exception:
             pass
+
+
+def peer_buffers(shape, dtype, group=None):
+    """Multi-GPU plumbing of the fused peer-memory exchange (f4): a buffer of
+    `shape` on this rank allocated in torch symmetric memory and rendezvoused over
+    `group`, so every rank's copy is addressable from every GPU (NVLink P2P).
+    Returns (local tensor, [device pointer of rank q's buffer for q in ranks])
+    for dr_peer_cbsr / the inboxes. Needs torch.distributed initialised with one
+    GPU per rank on a P2P-capable node."""
+    torch = _torch()
+    import torch.distributed as tdist
+    import torch.distributed._symmetric_memory as symm_mem
+    g = group if group is not None else tdist.group.WORLD
+    t = symm_mem.empty(*shape, dtype=dtype, device=torch.device("cuda", torch.cuda.current_device()))
+    h = symm_mem.rendezvous(t, g)
+    return t, [int(p) for p in h.buffer_ptrs]
 
 
 def nccl_unique_id():

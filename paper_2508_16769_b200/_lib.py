@@ -50,6 +50,10 @@ class dr_graph_info_t(C.Structure):
                 ("chunks", C.c_int64 * 3), ("chunks_T", C.c_int64 * 3)]
 
 
+class dr_peer_cbsr(C.Structure):
+    _fields_ = [("world", C.c_int32), ("val", C.c_void_p * 8), ("idx", C.c_void_p * 8)]
+
+
 class dr_cbsr(C.Structure):
     _fields_ = [("n", C.c_int64), ("dim", C.c_int32), ("k", C.c_int32),
                 ("idx_bytes", C.c_int32), ("idx", P), ("val", P)]
@@ -120,6 +124,10 @@ _SIGS = {
     "dr_shard_spmm_fwd": (C.c_int, [P, C.POINTER(dr_cbsr), P, P]),
     "dr_shard_spmm_bwd": (C.c_int, [P, P, C.POINTER(dr_cbsr), P, P]),
     "dr_shard_reduce_scatter_g": (C.c_int, [P, P, C.POINTER(dr_cbsr), P, P, P, P]),
+    "dr_shard_spmm_fwd_peer": (C.c_int, [P, C.POINTER(dr_peer_cbsr), C.c_int32, C.c_int32, P, P]),
+    "dr_shard_spmm_bwd_peer": (C.c_int, [P, P, C.POINTER(dr_peer_cbsr), C.c_int32, C.c_int32,
+                                         C.POINTER(C.c_void_p), P]),
+    "dr_shard_inbox_reduce": (C.c_int, [P, P, C.POINTER(dr_cbsr), P, P, P]),
     "dr_heteroconv_tape_bytes": (C.c_int, [P, C.POINTER(dr_layer), C.c_uint32,
                                            C.POINTER(C.c_size_t)]),
     "dr_heteroconv_fwd": (C.c_int, [P, C.POINTER(dr_layer), P, P, P, P, P, C.c_uint32, P]),

@@ -192,6 +192,17 @@ void launch_drelu(const float *x, int64_t n, int dim, int64_t ldx, int k, float 
 // NEXT-2 per-neighbour-group K (reading Q26): a destination row with in-degree d
 // keeps the first K(d) entries of each neighbour's value-sorted CBSR row,
 // K(d) = kb[0] (d <= thr[0]), kb[1] (d <= thr[1]), kb[2] (otherwise). ng.on == 0: off.
+// f4, fused exchange over peer memory: the source row j of the padded global
+// space lives in owner q = j / m's buffers at local row j - q m (read in place by
+// the SpMM, through NVLink when q is another GPU); the backward's per-source
+// contributions go to the owner's inbox, slot `rank` (written in place).
+constexpr int kMaxPeers = 8;
+struct PeerSrc {
+    const float *pv[kMaxPeers];
+    const uint8_t *pi[kMaxPeers];
+    float *pg[kMaxPeers];
+    int m, rank;
+};
 struct NgSched {
     int on = 0;
     int thr0 = 0, thr1 = 0, kb0 = 0, kb1 = 0, kb2 = 0;
@@ -201,6 +212,8 @@ struct NgSched {
 // backward reads its destinations' K coalesced beside row[] instead of gathering
 // two rowptr entries per edge.
 // dx[i, :] = 0 except dx[i, idx[i, t]] = g[i, t] (the D-ReLU mask gradient scatter)
+// f4: out = fixed-order sum over `world` stacked [n] blocks of `inbox`
+void launch_inbox_sum(const float *inbox, int world, int64_t n, float *out, cudaStream_t s);
 void launch_cbsr_scatter(const float *g, const uint8_t *idx, int64_t n, int k, int dim, float *dx,
                          cudaStream_t s);
 // A relation block uploaded with caller-given column normalisers (graph.cpp; dr_shard).
@@ -214,7 +227,8 @@ void launch_ng_edge_k(const RelDev &r, const NgSched &ng, uint8_t *kT, cudaStrea
 // DR-SpMM forward of one relation: z [n_dst x dim] = diag(c) A diag(s) densify(H).
 // z_split: write Z rows as [hi | lo] bf16 halves (the tc2 operand format).
 void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
-                     float *z, cudaStream_t s, bool z_split = false, NgSched ng = NgSched{});
+                     float *z, cudaStream_t s, bool z_split = false, NgSched ng = NgSched{},
+                     const PeerSrc *peer = nullptr);
 
 // SSpMM backward for one source node type, summing up to two relations that
 // share the source type. Term q in {0,1}: relation rel[q] (CSC), its dz, and
@@ -227,7 +241,8 @@ struct BwdTerm {
 };
 void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1,
                      const float *root, const uint8_t *hidx, int k, int dim, float *g_kept,
-                     float *dx, bool accumulate, cudaStream_t s, NgSched ng = NgSched{});
+                     float *dx, bool accumulate, cudaStream_t s, NgSched ng = NgSched{},
+                     const PeerSrc *peer = nullptr);
 
 // Tensor-core tiled SpMM (tspmm.cu) of a relation with a TileSet: forward into
 // z; backward for the tiled relation's source rows alone, with an optional

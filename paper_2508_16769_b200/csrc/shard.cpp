@@ -296,4 +296,65 @@ dr_status dr_shard_reduce_scatter_g(const dr_shard *s, const float *g_part, cons
     SH_END
 }
 
+// ---- f4, the exchange fused into the SpMM kernels over peer memory (NVLink P2P)
+static PeerSrc peer_src(const dr_shard *s, const dr_peer_cbsr *h, int dim, int k, float *const *inbox) {
+    DR_CHECK(h != nullptr, DR_ERR_INVALID_ARGUMENT, "shard peer: null dr_peer_cbsr");
+    DR_CHECK(h->world == s->world && s->world <= kMaxPeers, DR_ERR_INVALID_ARGUMENT,
+             "shard peer: world differs from the shard's (or > 8)");
+    DR_CHECK(dim >= 4 && dim <= 256 && dim % 4 == 0, DR_ERR_SHAPE_MISMATCH,
+             "shard peer: dim must be a multiple of 4 in [4, 256]");
+    DR_CHECK(k >= 1 && k <= dim && k <= 128 && (k & (k - 1)) == 0, DR_ERR_BAD_K,
+             "shard peer: k must be a power of two <= min(dim, 128)");
+    PeerSrc p{};
+    p.m = s->max_src;
+    p.rank = s->rank;
+    for (int q = 0; q < s->world; ++q) {
+        DR_CHECK(s->max_src == 0 || (h->val[q] && h->idx[q]), DR_ERR_INVALID_ARGUMENT,
+                 "shard peer: null CBSR pointer");
+        p.pv[q] = h->val[q];
+        p.pi[q] = (const uint8_t *)h->idx[q];
+        if (inbox) {
+            DR_CHECK(s->max_src == 0 || inbox[q], DR_ERR_INVALID_ARGUMENT, "shard peer: null inbox");
+            p.pg[q] = inbox[q];
+        }
+    }
+    return p;
+}
+
+dr_status dr_shard_spmm_fwd_peer(const dr_shard *s, const dr_peer_cbsr *h, int32_t dim, int32_t k,
+                                 float *z, void *stream) {
+    SH_BEGIN
+    DR_CHECK(s != nullptr, DR_ERR_INVALID_ARGUMENT, "shard_spmm_fwd_peer: null shard");
+    const PeerSrc p = peer_src(s, h, dim, k, nullptr);
+    DR_CHECK(s->rel.n_dst == 0 || z, DR_ERR_INVALID_ARGUMENT, "shard_spmm_fwd_peer: null z");
+    launch_spmm_fwd(s->rel, nullptr, nullptr, k, dim, z, (cudaStream_t)stream, false, NgSched{}, &p);
+    SH_END
+}
+
+dr_status dr_shard_spmm_bwd_peer(const dr_shard *s, const float *dz, const dr_peer_cbsr *h,
+                                 int32_t dim, int32_t k, float *const *inbox, void *stream) {
+    SH_BEGIN
+    DR_CHECK(s != nullptr && inbox != nullptr, DR_ERR_INVALID_ARGUMENT,
+             "shard_spmm_bwd_peer: null shard/inbox");
+    const PeerSrc p = peer_src(s, h, dim, k, inbox);
+    DR_CHECK(s->rel.n_dst == 0 || dz, DR_ERR_INVALID_ARGUMENT, "shard_spmm_bwd_peer: null dz");
+    BwdTerm t0{&s->rel, dz, true}, t1{};
+    launch_spmm_bwd(s->rel.bwd, s->rel.n_src, t0, t1, nullptr, nullptr, k, dim, nullptr, nullptr,
+                    false, (cudaStream_t)stream, NgSched{}, &p);
+    SH_END
+}
+
+dr_status dr_shard_inbox_reduce(const dr_shard *s, const float *inbox, const dr_cbsr *hl,
+                                float *g_local, float *dx, void *stream) {
+    SH_BEGIN
+    DR_CHECK(s != nullptr, DR_ERR_INVALID_ARGUMENT, "shard_inbox_reduce: null shard");
+    check_cbsr_rows(hl, s->max_src, "shard_inbox_reduce h_local");
+    DR_CHECK((s->max_src == 0 || (inbox && g_local)), DR_ERR_INVALID_ARGUMENT,
+             "shard_inbox_reduce: null inbox/g");
+    cudaStream_t st = (cudaStream_t)stream;
+    launch_inbox_sum(inbox, s->world, (int64_t)s->max_src * hl->k, g_local, st);
+    if (dx) launch_cbsr_scatter(g_local, (const uint8_t *)hl->idx, s->max_src, hl->k, hl->dim, dx, st);
+    SH_END
+}
+
 }  // extern "C"

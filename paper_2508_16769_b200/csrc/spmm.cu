@@ -71,13 +71,14 @@ __device__ __forceinline__ void load_pairs(const float *__restrict__ hval,
 
 // Accumulate neighbours e0, e0+stride, ... < e1 of one row into `acc` (shared,
 // D floats). Column ids and weights are prefetched one iteration ahead.
-template <int P>
+template <int P, bool PEER = false>
 __device__ __forceinline__ void fwd_accumulate(int e0, int e1, int stride,
                                                const int32_t *__restrict__ col,
                                                const float *__restrict__ ew,
                                                const float *__restrict__ hval,
                                                const uint8_t *__restrict__ hidx, int k, int ll,
-                                               float *acc, int kr, unsigned smask) {
+                                               float *acc, int kr, unsigned smask,
+                                               const PeerSrc *ps = nullptr) {
     int jn[kU];
     float wn[kU];
 #pragma unroll
@@ -96,7 +97,12 @@ __device__ __forceinline__ void fwd_accumulate(int e0, int e1, int stride,
 #pragma unroll
         for (int u = 0; u < kU; ++u)
             if (j[u] >= 0 && ll * P < kr) {                    // lanes beyond the K prefix idle
-                load_pairs<P>(hval, hidx, (int64_t)j[u] * k + ll * P, pr[u]);
+                if constexpr (PEER) {   // row j of owner q = j / m, read in place (peer memory)
+                    const int q = j[u] / ps->m, loc = j[u] - q * ps->m;
+                    load_pairs<P>(ps->pv[q], ps->pi[q], (int64_t)loc * k + ll * P, pr[u]);
+                } else {
+                    load_pairs<P>(hval, hidx, (int64_t)j[u] * k + ll * P, pr[u]);
+                }
 #pragma unroll
                 for (int p = 0; p < P; ++p)
                     if (ll * P + p >= kr) pr[u].v[p] = 0.f;     // beyond this row's K prefix
@@ -125,6 +131,7 @@ __device__ __forceinline__ void fwd_accumulate(int e0, int e1, int stride,
 }
 
 struct FwdArgs {
+    PeerSrc peer;                    // f4 fused exchange (PEER kernels only)
     const int32_t *order;
     int32_t n_hub, n_warp, n_rows;   // [0,n_hub) hubs, [n_hub,n_hub+n_warp) warp rows, rest sub
     int32_t hub_ctas, warp_ctas;     // block ranges: hubs, warp rows, then sub rows
@@ -169,8 +176,8 @@ __device__ __forceinline__ void store_z1(const FwdArgs &a, int row, int c, float
     rowp[a.D + c] = (uint16_t)(l & 0xffffu);
 }
 
-template <int P>
-__global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
+template <int P, bool PEER = false>
+__global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(const __grid_constant__ FwdArgs a) {
     extern __shared__ __align__(16) float sm[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
     const int L = a.L, R = 32 / L, sub = lane / L, ll = lane % L, D = a.D, D4 = D >> 2;
@@ -189,8 +196,8 @@ __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
             __syncwarp();
             const int chunk = (e1 - e0 + S - 1) / S;
             const int b0 = min(e1, e0 + sidx * chunk), b1 = min(e1, b0 + chunk);
-            fwd_accumulate<P>(b0, b1, 1, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc,
-                              ng_k(a.ng, e1 - e0, a.k), smask);
+            fwd_accumulate<P, PEER>(b0, b1, 1, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc,
+                                    ng_k(a.ng, e1 - e0, a.k), smask, &a.peer);
             __syncthreads();
             const float cr = __ldg(a.c + row);
             for (int cc = threadIdx.x; cc < D; cc += blockDim.x) {
@@ -211,8 +218,8 @@ __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
         __syncwarp();
         if (valid) {
             const int e0 = __ldg(a.rowptr + row), e1 = __ldg(a.rowptr + row + 1);
-            fwd_accumulate<P>(e0 + sub, e1, R, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc,
-                              ng_k(a.ng, e1 - e0, a.k), smask);
+            fwd_accumulate<P, PEER>(e0 + sub, e1, R, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc,
+                                    ng_k(a.ng, e1 - e0, a.k), smask, &a.peer);
         }
         __syncwarp();
         if (valid) {
@@ -238,8 +245,8 @@ __global__ void __launch_bounds__(256, 4) spmm_fwd_kernel(FwdArgs a) {
     __syncwarp();
     if (valid) {
         const int e0 = __ldg(a.rowptr + row), e1 = __ldg(a.rowptr + row + 1);
-        fwd_accumulate<P>(e0, e1, 1, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc,
-                          ng_k(a.ng, e1 - e0, a.k), smask);
+        fwd_accumulate<P, PEER>(e0, e1, 1, a.col, a.ew, a.hval, a.hidx, a.k, ll, acc,
+                                ng_k(a.ng, e1 - e0, a.k), smask, &a.peer);
     }
     __syncwarp();
     // the warp's R accumulator rows are contiguous in shared memory: store them
@@ -273,6 +280,7 @@ struct TermDev {
 };
 
 struct BwdArgs {
+    PeerSrc peer;                    // f4 fused exchange (PEER kernels only)
     const int32_t *order;
     int32_t n_hub, n_warp, n_rows, hub_ctas, warp_ctas;
     TermDev t[2];
@@ -351,14 +359,32 @@ __device__ __forceinline__ void load_idx(const uint8_t *__restrict__ hidx, int64
     }
 }
 
+// source row j's CBSR indices and its g row (PEER: the owner's buffers / inbox slot)
+template <bool PEER>
+__device__ __forceinline__ const uint8_t *idx_row(const BwdArgs &a, int j) {
+    if constexpr (PEER) {
+        const int q = j / a.peer.m;
+        return a.peer.pi[q] + (int64_t)(j - q * a.peer.m) * a.k;
+    }
+    return a.hidx + (int64_t)j * a.k;
+}
+template <bool PEER>
+__device__ __forceinline__ float *g_row(const BwdArgs &a, int j) {
+    if constexpr (PEER) {
+        const int q = j / a.peer.m;
+        return a.peer.pg[q] + ((int64_t)a.peer.rank * a.peer.m + (j - q * a.peer.m)) * a.k;
+    }
+    return a.g_kept + (int64_t)j * a.k;
+}
+
 // Write lane ll's P values of source row j: g_kept and/or the dense dX row
 // (zeros + k values, staged in the sub-warp's shared row). Whole warp calls it.
-template <int P>
+template <int P, bool PEER = false>
 __device__ __forceinline__ void bwd_store(const BwdArgs &a, bool valid, int j, int ll,
                                           const uint32_t *id, const float *g, float *srow) {
     const int D = a.D, D4 = D >> 2, L = a.L;
-    if (valid && a.g_kept) {
-        float *gk = a.g_kept + (int64_t)j * a.k + ll * P;
+    if (valid && (PEER || a.g_kept)) {
+        float *gk = g_row<PEER>(a, j) + ll * P;
 #pragma unroll
         for (int p = 0; p < P; ++p) gk[p] = a.accumulate ? gk[p] + g[p] : g[p];
     }
@@ -387,8 +413,8 @@ __device__ __forceinline__ void bwd_store(const BwdArgs &a, bool valid, int j, i
     __syncwarp();
 }
 
-template <int P>
-__global__ void __launch_bounds__(256, 4) spmm_bwd_kernel(BwdArgs a) {
+template <int P, bool PEER = false>
+__global__ void __launch_bounds__(256, 4) spmm_bwd_kernel(const __grid_constant__ BwdArgs a) {
     extern __shared__ __align__(16) float sm[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
     const int L = a.L, R = 32 / L, sub = lane / L, ll = lane % L;
@@ -402,7 +428,7 @@ __global__ void __launch_bounds__(256, 4) spmm_bwd_kernel(BwdArgs a) {
         for (int h = b; h < a.n_hub; h += a.hub_ctas) {
             const int j = __ldg(a.order + h);
             uint32_t id[P];
-            load_idx<P>(a.hidx, (int64_t)j * a.k + ll * P, id);
+            load_idx<P>(idx_row<PEER>(a, j), ll * P, id);
             float g[P];
 #pragma unroll
             for (int p = 0; p < P; ++p) g[p] = 0.f;
@@ -435,8 +461,8 @@ __global__ void __launch_bounds__(256, 4) spmm_bwd_kernel(BwdArgs a) {
                 float gf[P];
 #pragma unroll
                 for (int p = 0; p < P; ++p) gf[p] = part[(size_t)S * a.k + ll * P + p];
-                if (a.g_kept) {
-                    float *gk = a.g_kept + (int64_t)j * a.k + ll * P;
+                if (PEER || a.g_kept) {
+                    float *gk = g_row<PEER>(a, j) + ll * P;
 #pragma unroll
                     for (int p = 0; p < P; ++p) gk[p] = a.accumulate ? gk[p] + gf[p] : gf[p];
                 }
@@ -467,7 +493,7 @@ __global__ void __launch_bounds__(256, 4) spmm_bwd_kernel(BwdArgs a) {
 #pragma unroll
     for (int p = 0; p < P; ++p) { g[p] = 0.f; id[p] = 0; }
     if (valid) {
-        load_idx<P>(a.hidx, (int64_t)j * a.k + ll * P, id);
+        load_idx<P>(idx_row<PEER>(a, j), ll * P, id);
         const int first = warp_rows ? sub : 0, stride = warp_rows ? R : 1;
         for (int q = 0; q < a.n_terms; ++q) {
             const TermDev &t = a.t[q];
@@ -493,7 +519,7 @@ __global__ void __launch_bounds__(256, 4) spmm_bwd_kernel(BwdArgs a) {
 #pragma unroll
         for (int p = 0; p < P; ++p) g[p] += __ldg(a.root + (int64_t)j * a.k + ll * P + p);
     }
-    bwd_store<P>(a, valid && (!warp_rows || sub == 0), j, ll, id, g,
+    bwd_store<P, PEER>(a, valid && (!warp_rows || sub == 0), j, ll, id, g,
                  warp_rows ? sm + (size_t)wid * R * a.D : srow);
 }
 
@@ -512,9 +538,9 @@ int choose_P(int k, int D) {
 void ensure_smem(const void *fn, size_t bytes);
 
 void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, int k, int dim,
-                     float *z, cudaStream_t s, bool z_split, NgSched ng) {
+                     float *z, cudaStream_t s, bool z_split, NgSched ng, const PeerSrc *peer) {
     if (r.n_dst <= 0) return;
-    if (!ng.on && !r.ew && tspmm_supported(r.tiles, dim, k)) {     // tensor-core tiled path
+    if (!peer && !ng.on && !r.ew && tspmm_supported(r.tiles, dim, k)) {     // tensor-core tiled path
         launch_tspmm_fwd(r, hval, hidx, k, dim, z, s, z_split);
         return;
     }
@@ -538,6 +564,7 @@ void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, in
     a.z = z;
     a.z_split = z_split ? 1 : 0;
     a.ng = ng;
+    if (peer) a.peer = *peer;
     int wpc = 8;
     while (wpc > 1 && (size_t)wpc * R * dim * 4 > 96 * 1024) wpc >>= 1;
     const size_t smem = (size_t)wpc * R * dim * 4;
@@ -548,16 +575,15 @@ void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, in
     const unsigned grid = (unsigned)(a.hub_ctas + a.warp_ctas + sub_ctas);
     if (grid == 0) return;
     ProfScope ps("spmm_fwd", s);
-    if (P == 4) {
-        ensure_smem((const void *)spmm_fwd_kernel<4>, smem);
-        spmm_fwd_kernel<4><<<grid, wpc * 32, smem, s>>>(a);
-    } else if (P == 2) {
-        ensure_smem((const void *)spmm_fwd_kernel<2>, smem);
-        spmm_fwd_kernel<2><<<grid, wpc * 32, smem, s>>>(a);
-    } else {
-        ensure_smem((const void *)spmm_fwd_kernel<1>, smem);
-        spmm_fwd_kernel<1><<<grid, wpc * 32, smem, s>>>(a);
-    }
+    const void *fn = peer ? (P == 4 ? (const void *)spmm_fwd_kernel<4, true>
+                             : P == 2 ? (const void *)spmm_fwd_kernel<2, true>
+                                      : (const void *)spmm_fwd_kernel<1, true>)
+                          : (P == 4 ? (const void *)spmm_fwd_kernel<4>
+                             : P == 2 ? (const void *)spmm_fwd_kernel<2>
+                                      : (const void *)spmm_fwd_kernel<1>);
+    ensure_smem(fn, smem);
+    void *args[] = {(void *)&a};
+    DR_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(wpc * 32), args, smem, s));
     note_launch("spmm_fwd");
 }
 
@@ -575,9 +601,11 @@ static int choose_P_bwd(int k) {
 
 void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, const float *root,
                      const uint8_t *hidx, int k, int dim, float *g_kept, float *dx,
-                     bool accumulate, cudaStream_t s, NgSched ng) {
+                     bool accumulate, cudaStream_t s, NgSched ng, const PeerSrc *peer) {
     if (n_src <= 0) return;
-    if (!ng.on && t0.rel && !t1.rel && !t0.rel->ewT && !accumulate && tspmm_supported(t0.rel->tilesT, dim, k) &&
+    DR_CHECK(!peer || (!root && !dx && !accumulate && !ng.on), DR_ERR_INVALID_ARGUMENT,
+             "spmm_bwd: the peer path writes g only");
+    if (!peer && !ng.on && t0.rel && !t1.rel && !t0.rel->ewT && !accumulate && tspmm_supported(t0.rel->tilesT, dim, k) &&
         t0.rel->n_src == n_src) {                           // tensor-core tiled path
         launch_tspmm_bwd(*t0.rel, t0.dz, false, t0.apply_c, root, hidx, k, dim, g_kept, dx, s);
         return;
@@ -614,6 +642,7 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, c
     a.dx = dx;
     a.accumulate = accumulate ? 1 : 0;
     a.ng = ng;
+    if (peer) a.peer = *peer;
     int wpc = 8;
     while (wpc > 1 && (size_t)wpc * R * dim * 4 > 96 * 1024) wpc >>= 1;
     size_t smem = (size_t)wpc * R * dim * 4;
@@ -626,17 +655,27 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, c
     const unsigned grid = (unsigned)(a.hub_ctas + a.warp_ctas + sub_ctas);
     if (grid == 0) return;
     ProfScope ps("spmm_bwd", s);
-    if (P == 4) {
-        ensure_smem((const void *)spmm_bwd_kernel<4>, smem);
-        spmm_bwd_kernel<4><<<grid, wpc * 32, smem, s>>>(a);
-    } else if (P == 2) {
-        ensure_smem((const void *)spmm_bwd_kernel<2>, smem);
-        spmm_bwd_kernel<2><<<grid, wpc * 32, smem, s>>>(a);
-    } else {
-        ensure_smem((const void *)spmm_bwd_kernel<1>, smem);
-        spmm_bwd_kernel<1><<<grid, wpc * 32, smem, s>>>(a);
-    }
+    const void *fn = peer ? (P == 4 ? (const void *)spmm_bwd_kernel<4, true>
+                             : P == 2 ? (const void *)spmm_bwd_kernel<2, true>
+                                      : (const void *)spmm_bwd_kernel<1, true>)
+                          : (P == 4 ? (const void *)spmm_bwd_kernel<4>
+                             : P == 2 ? (const void *)spmm_bwd_kernel<2>
+                                      : (const void *)spmm_bwd_kernel<1>);
+    ensure_smem(fn, smem);
+    void *args[] = {(void *)&a};
+    DR_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(wpc * 32), args, smem, s));
     note_launch("spmm_bwd");
+}
+
+// f4 inbox sum: out[e] = sum over p = 0 .. world-1 of inbox[p][e], fixed order
+__global__ void inbox_sum_kernel(const float *__restrict__ inbox, int world, int64_t n,
+                                 float *__restrict__ out) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        float acc = 0.f;
+        for (int p = 0; p < world; ++p) acc += __ldg(inbox + (int64_t)p * n + e);
+        out[e] = acc;
+    }
 }
 
 // one warp per row: zero the row, then drop the k values at their columns
@@ -651,6 +690,14 @@ __global__ void cbsr_scatter_kernel(const float *__restrict__ g, const uint8_t *
         for (int t = lane; t < k; t += 32) row[__ldg(idx + r * k + t)] = __ldg(g + r * k + t);
         __syncwarp();
     }
+}
+
+void launch_inbox_sum(const float *inbox, int world, int64_t n, float *out, cudaStream_t s) {
+    if (n <= 0) return;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    inbox_sum_kernel<<<(unsigned)blocks, 256, 0, s>>>(inbox, world, n, out);
+    note_launch("inbox_sum");
 }
 
 void launch_cbsr_scatter(const float *g, const uint8_t *idx, int64_t n, int k, int dim, float *dx,
