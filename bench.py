@@ -117,7 +117,7 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ algorithmic work per kernel tag
-def kernel_work(tag, d, D, k, tiled=True):
+def kernel_work(tag, d, D, k, tiled=True, chained=False):
     """(bytes, flops) per launch for a profile tag, SURVEY §8(d) per-unit figures
     (restated in DESIGN.md §5 'Algorithmic bytes'). Pair = 4 B value + 1 B index.
     tiled: near's backward runs as the tensor-core tiled kernel (near term + extra)
@@ -147,9 +147,12 @@ def kernel_work(tag, d, D, k, tiled=True):
                 2.0 * n * D * (2 * D if root else D))
     if kind == "tc_proj":
         n = d.n_cell if rel == "cell" else d.n_net
+        # chained (the trainer's hidden layers, row a5): the next layer's CBSR
+        # (5 k B per row) is written instead of the dense Y (4 D B per row)
+        out = 5 * k if (chained and len(parts) == 3 and parts[1] == "L0") else 4 * D
         if rel == "cell":       # Z_near, Z_pinned read, CBSR root input, Y + mask written
-            return n * (2 * D * 4 + 5 * k + 4 * D + D // 8), 2.0 * n * D * (3 * D)
-        return n * (D * 4 + 5 * k + 4 * D), 2.0 * n * D * (2 * D)
+            return n * (2 * D * 4 + 5 * k + out + D // 8), 2.0 * n * D * (3 * D)
+        return n * (D * 4 + 5 * k + out), 2.0 * n * D * (2 * D)
     if kind == "tc_dw":     # Z rows (+ CBSR root input) and dY rows (+ mask words) read
         n = ndst.get(rel, d.n_cell)
         root = rel in ("near", "pins")
@@ -164,12 +167,12 @@ def load_json(name):
     return json.load(open(p)) if os.path.exists(p) else {}
 
 
-def kernel_table(prof, d, D, k, workload, tiled=True):
+def kernel_table(prof, d, D, k, workload, tiled=True, chained=False):
     traffic = load_json("ncu_traffic.json").get(workload, {})
     bounds = load_json("ncu_bounds.json").get(workload, {})
     table = {}
     for tag, (n, tot, mx) in prof.items():
-        b, f = kernel_work(tag, d, D, k, tiled)
+        b, f = kernel_work(tag, d, D, k, tiled, chained)
         per = tot / max(n, 1)
         tr = traffic.get(tag)
         table[tag] = dict(launches=n, total_ms=round(tot, 4), mean_ms=round(per, 5),
@@ -194,7 +197,10 @@ def roofline(table, hbm, bf16, src):
     b = e["alg_bytes"]
     f = e["alg_flops"]
     kind = dom.split(".")[0]
-    rf = {"kernel": dom, "traffic": e["dram_bytes_ncu"], "ncu_bound": e["ncu_bound"]}
+    rf = {"kernel": dom, "traffic": e["dram_bytes_ncu"], "ncu_bound": e["ncu_bound"],
+          # the unit that actually limits it (ncu, profiles/ncu_bounds.json): the
+          # roofline below is the HBM / tensor ceiling, "latency" = neither is close
+          "limiter": (e["ncu_bound"] or {}).get("bound")}
     if kind.startswith("tc_") and 3.0 * f / (bf16 * 1e12) > b / (hbm * 1e9):
         ach = 3.0 * f / per_s / 1e12
         rf.update(bound="tensor", achieved=round(ach, 2), peak=round(bf16, 1), unit="TFLOP/s",
@@ -595,7 +601,8 @@ def run_c5(args, torch, dist, dr, rank, world, local, dev, hbm, bf16, src):
     dp["oracle_grad_ok"] = bool(worst <= 1e-4)
     dp["oracle_s"] = round(time.time() - t0, 2)
 
-    table = kernel_table(prof, bd[0], D, k, "C5", tiled=graphs[0].info()["tiles"][0] > 0)
+    table = kernel_table(prof, bd[0], D, k, "C5", tiled=graphs[0].info()["tiles"][0] > 0,
+                         chained=True)
     rf = roofline(table, hbm, bf16, src)
     out = None
     if rank == 0:
@@ -729,7 +736,8 @@ def run_single(args, torch, dr, wl, dev, hbm, bf16, src, l2=None, steps=None, wa
         os.environ.pop("DR_FORCE_SEQUENTIAL", None)
         return pr
     prof = kernel_pass(g, step, steps)
-    table = kernel_table(prof, d, D, k, wl, tiled=g.info()["tiles"][0] > 0)
+    table = kernel_table(prof, d, D, k, wl, tiled=g.info()["tiles"][0] > 0,
+                         chained=wl == "C2")
     out = {"ms_per_iter": round(ms / steps, 4), "steps": steps, "warmup": warmup,
            "graph_init_s": round(init_s, 2), "gpu_launches": int(launches), "clocks": clk,
            "roofline": roofline(table, hbm, bf16, src), "spmm_gate": spmm_gate(table, hbm, l2),
