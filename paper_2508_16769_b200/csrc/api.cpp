@@ -262,7 +262,9 @@ static bool z_split_ok(const dr_layer *L, int) {
 static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc, const float *xn,
                            float *yc, float *yn, void *tape, uint32_t flags, cudaStream_t st,
                            const dr_layer *Ln = nullptr, void *tape_next = nullptr,
-                           uint32_t flags_next = 0) {
+                           uint32_t flags_next = 0, const HeadArgs *head = nullptr,
+                           int *head_parts = nullptr) {
+    if (head_parts) *head_parts = 0;
     const TapeLayout T = tape_layout(g, L, flags);
     const bool in_tape = (flags & DR_FWD_INPUT_IN_TAPE) != 0;
     TapeLayout TN{};
@@ -335,9 +337,15 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
             d.next_idx = (uint8_t *)(tn + TN.hc_idx);
             if (y_scratch) d.y = nullptr;
         }
+        if (head && !Ln) {     // the last layer: linear head + MSE in the epilogue, Y not stored
+            d.head_w = head->w; d.head_b = head->b; d.labels = head->labels;
+            d.head_dy = head->dy; d.head_part = head->work;
+            d.y = nullptr;
+        }
         if (!tc2_rows_supported(d)) {
             d.next_k = 0;
             d.y = yc;
+            d.head_w = nullptr;
         }
     }
     const bool net_tc = !no_net && nn > 0 && tc2_rows_supported(dnet);
@@ -406,7 +414,8 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
     {   // cell: Y_cell = max(Y_near, Y_pinned), M   (Eq. 6, 8, 14)
         TagScope t("cell");
         if (cell_tc) {
-            launch_tc2_rows(dcell, s0);
+            const int grid = launch_tc2_rows(dcell, s0);
+            if (dcell.head_w && head_parts) *head_parts = grid;
         } else {
             ProjFwdArgs a;
             a.n = nc; a.Ka = L->d_cell; a.Kb = L->d_net; a.N = L->d_out;
@@ -1185,6 +1194,14 @@ static void train_step_body(dr_trainer *t, const dr_graph *g, const float *x_cel
     bool chain = knobs().chain != 0;
     for (int l = 0; l < nl; ++l) chain = chain && !pins_own(&t->L[l]);
     const bool no_net = knobs().skip_dead_net != 0;
+    // the linear head + MSE (Q14) runs in the last cell projection's epilogue when
+    // the shapes allow (its per-CTA sums finished by one small launch), else as
+    // its own kernels on the stored Y_cell
+    HeadArgs h;
+    h.n = (int64_t)nc; h.N = D; h.y = yc(nl - 1); h.w = t->head_w; h.b = t->head_b;
+    h.labels = labels; h.dy = dyc(0); h.grad_w = t->ghead_w; h.grad_b = t->ghead_b;
+    h.loss = t->scalars; h.work = (float *)(ws + head_off);
+    int head_parts = 0;
     for (int l = 0; l < nl; ++l) {
         TagScope tg(ltag[l]);
         const bool last = l == nl - 1;
@@ -1194,18 +1211,14 @@ static void train_step_body(dr_trainer *t, const dr_graph *g, const float *x_cel
             heteroconv_fwd(g, &t->L[l], xc, xn, yc(l), yn(l), ws + tape_off[l], fl | DR_FWD_Y_SCRATCH,
                            st, &t->L[l + 1], ws + tape_off[l + 1], 0);
         else
-            heteroconv_fwd(g, &t->L[l], xc, xn, yc(l), yn(l), ws + tape_off[l], fl, st);
+            heteroconv_fwd(g, &t->L[l], xc, xn, yc(l), yn(l), ws + tape_off[l], fl, st, nullptr,
+                           nullptr, 0, (last && knobs().head_fuse) ? &h : nullptr, &head_parts);
         xc = yc(l);
         xn = yn(l);
     }
     // ---- head + MSE
-    {
-        HeadArgs h;
-        h.n = (int64_t)nc; h.N = D; h.y = yc(nl - 1); h.w = t->head_w; h.b = t->head_b;
-        h.labels = labels; h.dy = dyc(0); h.grad_w = t->ghead_w; h.grad_b = t->ghead_b;
-        h.loss = t->scalars; h.work = (float *)(ws + head_off);
-        launch_head_mse(h, st);
-    }
+    if (head_parts > 0) launch_head_reduce(h, head_parts, st);
+    else launch_head_mse(h, st);
     if (!no_net)                                 // last layer's Y_net feeds nothing: dY_net = 0
         DR_CUDA(cudaMemsetAsync(dyn(0), 0, nn * D * 4, st));
     // ---- backward

@@ -55,6 +55,7 @@ struct Knobs {
     int64_t order_block = -2;    // DR_ORDER_BLOCK: log2 rows per locality block of the SIMT orders (-1: degree-major, -2: by size)
     int64_t z_split = 1;         // DR_Z_SPLIT=0: Z stored fp32 (converted by each consumer)
     int64_t drelu_coop = -2;     // DR_DRELU_COOP: lanes per row of the thread-per-row D-ReLU (-2 auto, 0 off)
+    int64_t head_fuse = 1;       // DR_HEAD_FUSE=0: trainer head + MSE as its own kernels
     int64_t chain = 1;           // DR_CHAIN=0: trainer without the fused next-layer D-ReLU
     int64_t skip_dead_net = 1;   // DR_SKIP_DEAD_NET=0: trainer computes the last layer's Y_net
 };

@@ -38,6 +38,7 @@ static Knobs read_env() {
     k.shard_tiles = env_i("DR_SHARD_TILES", 0);
     k.shard_tiles_t = env_i("DR_SHARD_TILES_T", 0);
     k.chain = env_i("DR_CHAIN", 1);
+    k.head_fuse = env_i("DR_HEAD_FUSE", 1);
     k.drelu_coop = env_i("DR_DRELU_COOP", -2);
     k.z_split = env_i("DR_Z_SPLIT", 1);
     k.order_block = env_i("DR_ORDER_BLOCK", -2);
@@ -78,6 +79,7 @@ extern "C" dr_status dr_debug_set(const char *name, int64_t value) {
         {"shard_tiles", &g_knobs.shard_tiles},
         {"shard_tiles_t", &g_knobs.shard_tiles_t},
         {"chain", &g_knobs.chain},
+        {"head_fuse", &g_knobs.head_fuse},
         {"drelu_coop", &g_knobs.drelu_coop},
         {"z_split", &g_knobs.z_split},
         {"order_block", &g_knobs.order_block},

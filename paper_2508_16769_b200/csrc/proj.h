@@ -77,6 +77,9 @@ struct HeadArgs {
 };
 size_t head_work_floats(int N);
 void launch_head_mse(const HeadArgs &a, cudaStream_t s);
+// Only the final fixed-order sum of `nparts` per-CTA head partials in a.work
+// (the head fused into the last projection's epilogue, tc2.h head_w).
+void launch_head_reduce(const HeadArgs &a, int nparts, cudaStream_t s);
 
 // Adam with coupled L2 weight decay (reading Q15); grad is scaled by inv_world first.
 void launch_adam(float *theta, const float *grad, float *m, float *v, int64_t n, float lr,

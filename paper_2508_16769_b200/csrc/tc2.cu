@@ -146,6 +146,11 @@ struct R2Args {
     const uint8_t *root_idx;
     int root_k;
     float *root;
+    // fused linear head + MSE (last layer; tc2.h)
+    int head;
+    const float *head_w, *head_b, *labels;
+    float head_inv_n;
+    float *head_dy, *head_part;
     // fused next-layer D-ReLU (row a5): CBSR of y, exactly nk per row (tc2.h)
     int nk;                        // keep count (0: no fused D-ReLU)
     float *nval;
@@ -375,11 +380,72 @@ __device__ __forceinline__ void epi_pre_load(const R2Args &a, int64_t row, EpiPr
 // cooperative redux.max extraction (latency-bound at one warp per SMSP).
 constexpr int kRB = 68;                // row-buffer stride (floats): 64 columns + 4 pad
 
+// y of accumulator columns [j, j + 32) of this lane's row (bias, merge): the same
+// operations in the same order as the forward epilogue's pass, so the same bits
+__device__ __forceinline__ void epi_y32(const R2Args &a, uint32_t lb, int j, const float *bias_s,
+                                        float (&y)[32]) {
+    const int N = a.N;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int jj = j + 16 * h;
+        uint32_t ra[16], rb[16];
+        if (jj < N) {
+            tc::tmem_ld16_nw(lb + (uint32_t)jj, ra);
+            if (a.G == 2) tc::tmem_ld16_nw(lb + (uint32_t)(N + jj), rb);
+            tc::tmem_wait_ld();
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const float ya = jj < N ? __uint_as_float(ra[q]) + bias_s[jj + q] : 0.f;
+            const float yb = (a.G == 2 && jj < N) ? __uint_as_float(rb[q]) + bias_s[256 + jj + q] : 0.f;
+            float v = ya;
+            if (a.G == 2) v = a.merge == DR_MERGE_MAX ? (ya >= yb ? ya : yb) : ya + yb;
+            y[16 * h + q] = v;
+        }
+    }
+}
+
+// Fused linear head + MSE (reading Q14) on the last layer's Y_cell, which is then
+// never stored: per row pred = y . w_h + b_h, r = pred - label, dp = 2 r / n;
+// writes dY = dp w_h (the backward's input) and accumulates, per warp in shared
+// memory in a fixed order, the head gradient sum_rows y dp, sum dp and sum r^2.
+__device__ __forceinline__ void head_epilogue(const R2Args &a, uint32_t lb, int64_t row0, int lane,
+                                           bool ok, float pred, const float *hw, float hb,
+                                           const float *bias_s, float *stg, float *hacc,
+                                           float &accb, float &accl) {
+    const int N = a.N;
+    const int64_t row = row0 + lane;
+    const float r = ok ? pred + hb - __ldg(a.labels + row) : 0.f;
+    const float dp = 2.0f * r * a.head_inv_n;
+    accb += dp;
+    accl += r * r;
+    for (int j = 0; j < N; j += 32) {
+        float y[32];
+        epi_y32(a, lb, j, bias_s, y);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) y[q] = ok ? y[q] * dp : 0.f;
+        stg_put(stg, kEStg, lane, y);
+        __syncwarp();
+        float cs = 0.f;                            // column j + lane over the 32 rows
+#pragma unroll 8
+        for (int rr = 0; rr < 32; ++rr) cs += stg[rr * kEStg + lane];
+        if (j + lane < N) hacc[j + lane] += cs;
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 32; ++q) y[q] = j + q < N ? dp * hw[j + q] : 0.f;
+        stg_put(stg, kEStg, lane, y);
+        __syncwarp();
+        stg_out_f32(stg, kEStg, a.head_dy, N, row0, a.n, j, lane);
+        __syncwarp();
+    }
+}
+
 // epilogue warp (quarter qd): rows r0 + 32 qd + lane of accumulator columns at `acc`
 template <int NK>
 __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int64_t r0, int qd,
                                               int lane, const float *bias_s, float *stg,
-                                              const EpiPre &pre) {
+                                              const EpiPre &pre, const float *hw, float hb,
+                                              float *hacc, float &accb, float &accl) {
     const int N = a.N;
     const int64_t row0 = r0 + qd * 32, row = row0 + lane;
     const bool ok = row < a.n;
@@ -448,6 +514,7 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
     // NK > 0 (fused next-layer D-ReLU): `stg` is the warp's [32][kRB] row buffer
     // and every block stays staged at its columns until the selection below
     const int sstride = NK > 0 ? kRB : kEStg;
+    float pred = 0.f;                              // fused head: y . w_h of this row
     for (int j = 0; j < N; j += 32) {
         uint32_t ra[2][16], rb[2][16];
         tc::tmem_ld16_nw(lb + (uint32_t)j, ra[0]);
@@ -504,7 +571,14 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
             __syncwarp();
         }
         if (ok && a.G == 2 && a.mask_out) a.mask_out[row * mw + (j >> 5)] = word;
+        if constexpr (NK < 0) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+                if (j + q < N) pred += y[q] * hw[j + q];
+        }
     }
+    if constexpr (NK < 0)
+        head_epilogue(a, lb, row0, lane, ok, pred, hw, hb, bias_s, stg, hacc, accb, accl);
     if constexpr (NK > 0) {
         const float *xr = stg + lane * kRB;
         if (N == 64) tpr_select_row<64, NK, false>(xr, ok, a.nval + row * NK, a.nidx + row * NK);
@@ -522,11 +596,25 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
     __shared__ __align__(8) uint64_t bfull[kMaxSB], bempty[kMaxSB], accf[2], acce[2];
     __shared__ uint32_t tmem_slot;
     __shared__ float bias_s[512];
+    // fused head (NK < 0 only): w_h, b_h and the per-epilogue-warp sums
+    float *head_s = nullptr;
+    float (*hacc_s)[258] = nullptr;
+    if constexpr (NK < 0) {
+        __shared__ float head_sh[257];
+        __shared__ float hacc_sh[4][258];
+        head_s = head_sh;
+        hacc_s = hacc_sh;
+    }
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int SA = a.SA, SB = a.SB, S = a.S;
     for (int e = tid; e < 512; e += kRowsThreads) {
         const int g = e >> 8, j = e & 255;
         bias_s[e] = (a.epi == kEpi2Fwd && g < a.G && j < a.N && a.bias[g]) ? a.bias[g][j] : 0.f;
+    }
+    if (NK < 0) {
+        for (int e = tid; e < 257; e += kRowsThreads)
+            head_s[e] = e < a.N ? a.head_w[e] : (e == 256 ? a.head_b[0] : 0.f);
+        for (int e = tid; e < 4 * 258; e += kRowsThreads) hacc_s[e / 258][e % 258] = 0.f;
     }
     uint8_t *stages = sm;
     uint8_t *bslots = sm + (size_t)SA * kStage;
@@ -685,6 +773,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
         const int qd = warp & 3;
         float *stg = reinterpret_cast<float *>(epi_stage + (size_t)(warp - 6) * epi_warp_bytes(NK > 0));
         EpiPre pcur, pnxt;
+        float accb = 0.f, accl = 0.f;              // fused head: sum dp, sum r^2 of this lane
+        float *hacc = hacc_s[warp - 6];
         if (NK == 0 && my_tiles > 0) epi_pre_load(a, (int64_t)blockIdx.x * kTile + qd * 32 + lane, pcur);
         for (int64_t t = 0; t < my_tiles; ++t) {
             const int64_t r0 = ((int64_t)blockIdx.x + t * gridDim.x) * kTile;
@@ -697,12 +787,29 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
             }
             tc::fence_after();
             RDBG_T0;
-            rows_epilogue<NK>(a, tmem + ab * GN, r0, qd, lane, bias_s, stg, pcur);
+            rows_epilogue<NK>(a, tmem + ab * GN, r0, qd, lane, bias_s, stg, pcur, head_s,
+                              head_s[256], hacc, accb, accl);
             pcur = pnxt;
             if (warp == 6 && lane == 0) RDBG_ADD(6);
             tc::fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&acce[ab]);
+        }
+        if (NK < 0) {   // this CTA's partial [sum_rows y dp (N) | sum dp | sum r^2], fixed order
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                accb += __shfl_xor_sync(0xffffffffu, accb, o);
+                accl += __shfl_xor_sync(0xffffffffu, accl, o);
+            }
+            if (lane == 0) {
+                hacc[a.N] += accb;
+                hacc[a.N + 1] += accl;
+            }
+            tc::named_bar(2, 128);
+            const int et = tid - 192;
+            for (int e = et; e < a.N + 2; e += 128)
+                a.head_part[(int64_t)blockIdx.x * (a.N + 2) + e] =
+                    ((hacc_s[0][e] + hacc_s[1][e]) + hacc_s[2][e]) + hacc_s[3][e];
         }
     }
     tc::fence_before();
@@ -1541,12 +1648,12 @@ bool tc2_rows_supported(const Tc2RowsDesc &d) {
     if (d.epi == kEpi2Dz && d.n_dz % 16) return false;
     if (d.next_k && !tc2_next_drelu_supported(d.epi, d.N, d.next_k)) return false;
     const size_t bchunk = (size_t)256 * d.N;
-    const size_t budget = (size_t)(kSmemBase - 4 * epi_warp_bytes(d.next_k > 0));
+    const size_t budget = (size_t)(kSmemBase - 4 * epi_warp_bytes(d.next_k > 0) - (d.head_w ? 5 * 1024 : 0));
     return 2 * kStage + 2 * kMaskStage + 2 * bchunk <= budget;
 }
 
-void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
-    if (d.n <= 0) return;
+int launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
+    if (d.n <= 0) return 0;
     DR_CHECK(tc2_rows_supported(d), DR_ERR_UNSUPPORTED, "tc2_rows: unsupported shape");
     R2Args a{};
     a.n = d.n;
@@ -1584,13 +1691,24 @@ void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
     a.root_idx = d.root_idx;
     a.root_k = d.root_k;
     a.root = d.root;
+    a.head = d.head_w ? 1 : 0;
+    a.head_w = d.head_w;
+    a.head_b = d.head_b;
+    a.labels = d.labels;
+    a.head_inv_n = d.n > 0 ? 1.0f / (float)d.n : 0.f;
+    a.head_dy = d.head_dy;
+    a.head_part = d.head_part;
+    DR_CHECK(!a.head || (d.G == 2 && d.epi == kEpi2Fwd && !d.next_k && d.head_b && d.labels &&
+                         d.head_dy && d.head_part),
+             DR_ERR_INVALID_ARGUMENT, "tc2_rows: bad fused-head arguments");
     a.nk = d.next_k;
     a.nval = d.next_val;
     a.nidx = d.next_idx;
     DR_CHECK(!a.nk || (a.nval && a.nidx), DR_ERR_INVALID_ARGUMENT, "tc2_rows: null next CBSR");
     // stages: B resident when every chunk fits beside >= 2 A stages, else a ring
     const size_t st_bytes = kStage + kMaskStage;
-    const size_t budget = (size_t)(kSmemBase - 4 * epi_warp_bytes(a.nk > 0));
+    // the fused-head variant's own static arrays (5 KB) come out of the same budget
+    const size_t budget = (size_t)(kSmemBase - 4 * epi_warp_bytes(a.nk > 0) - (a.head ? 5 * 1024 : 0));
     if ((size_t)a.S * a.bchunk + 2 * st_bytes <= budget && a.S <= kMaxSB) {
         a.b_resident = 1;
         a.SB = a.S;
@@ -1607,7 +1725,8 @@ void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
     const int64_t tiles = (d.n + kTile - 1) / kTile;
     const int64_t grid = tiles < 148 ? tiles : 148;
     ProfScope ps(d.epi == kEpi2Dz ? "tc_dz" : "tc_proj", s);
-    const void *fn = a.nk == 1 ? (const void *)tc2_rows_kernel<1>
+    const void *fn = a.head ? (const void *)tc2_rows_kernel<-1>   // fused head (NK < 0)
+                   : a.nk == 1 ? (const void *)tc2_rows_kernel<1>
                    : a.nk == 2 ? (const void *)tc2_rows_kernel<2>
                    : a.nk == 4 ? (const void *)tc2_rows_kernel<4>
                    : a.nk == 8 ? (const void *)tc2_rows_kernel<8>
@@ -1640,6 +1759,7 @@ void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
                 (long long)d.n, a.N, a.G, a.S, a.SA, a.SB, a.b_resident, a.epi, t[8] / 1e3,
                 t[0] / 1e3, t[1] / 1e3, t[2] / 1e3, t[3] / 1e3, t[4] / 1e3, t[5] / 1e3, t[6] / 1e3);
     }
+    return (int)grid;
 }
 
 // stage layout of the reduce kernel: [A'_g 32 KB each][B' 256 N][CBSR raw][mask words]

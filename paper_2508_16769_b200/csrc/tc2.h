@@ -64,6 +64,13 @@ struct Tc2RowsDesc {
     int next_k = 0;
     float *next_val = nullptr;
     uint8_t *next_idx = nullptr;
+    // forward epilogue, fused linear head + MSE on Y (the last layer's Y_cell, G =
+    // 2; reading Q14): with head_w set, writes head_dy = dL/dY (n x N) and, per CTA
+    // c < grid (launch_tc2_rows' return value), head_part[c][0..N+2) = the partial
+    // sums of y dp over rows, of dp and of r^2 (dp = 2 (pred - label) / n), which
+    // launch_head_reduce finishes; y may be null.
+    const float *head_w = nullptr, *head_b = nullptr, *labels = nullptr;
+    float *head_dy = nullptr, *head_part = nullptr;
 };
 // shapes the fused next-layer D-ReLU covers (else: dense y + launch_drelu)
 bool tc2_next_drelu_supported(int epi, int N, int k);
@@ -84,7 +91,7 @@ struct Tc2PackJob {
 constexpr int kMaxPackJobs = 8;
 void launch_tc2_pack_b_multi(const Tc2PackJob *jobs, int n, cudaStream_t s);
 bool tc2_rows_supported(const Tc2RowsDesc &d);
-void launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s);
+int launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s);   // returns the grid
 
 struct Tc2RedSeg {
     const float *Z = nullptr;          // dense n x w, or nullptr => CBSR (hval/hidx/k, width w)

@@ -88,13 +88,12 @@ __global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a, float in
 // One warp per output element: lanes take every 32nd block partial, then a
 // fixed butterfly (deterministic; a single-thread loop over 296 dependent loads
 // was latency-bound).
-__global__ void head_reduce_kernel(HeadArgs a, float inv_n) {
+__global__ void head_reduce_kernel(HeadArgs a, float inv_n, int nparts) {
     const int N = a.N, lane = threadIdx.x & 31;
     const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (e >= N + 2) return;
     float s = 0.f;
-#pragma unroll
-    for (int q = lane; q < kHeadBlocks; q += 32) s += a.work[(int64_t)q * (N + 2) + e];
+    for (int q = lane; q < nparts; q += 32) s += a.work[(int64_t)q * (N + 2) + e];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane) return;
@@ -146,7 +145,14 @@ void launch_head_mse(const HeadArgs &a, cudaStream_t s) {
     else if (a.N <= 128) head_kernel<4><<<kHeadBlocks, kHeadThreads, 0, s>>>(a, inv_n);
     else head_kernel<8><<<kHeadBlocks, kHeadThreads, 0, s>>>(a, inv_n);
     note_launch("head_mse");
-    head_reduce_kernel<<<(unsigned)((a.N + 2 + 7) / 8), 256, 0, s>>>(a, inv_n);
+    head_reduce_kernel<<<(unsigned)((a.N + 2 + 7) / 8), 256, 0, s>>>(a, inv_n, kHeadBlocks);
+    note_launch("head_reduce");
+}
+
+void launch_head_reduce(const HeadArgs &a, int nparts, cudaStream_t s) {
+    const float inv_n = a.n > 0 ? 1.0f / (float)a.n : 0.f;
+    ProfScope ps("head_mse", s);
+    head_reduce_kernel<<<(unsigned)((a.N + 2 + 7) / 8), 256, 0, s>>>(a, inv_n, nparts);
     note_launch("head_reduce");
 }
 

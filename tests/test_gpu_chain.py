@@ -195,3 +195,36 @@ def test_split_z_bit_identical(designs, knob, name, D, k):
     assert torch.equal(a[3], b[3]) and torch.equal(a[4], b[4])
     for key in a[2]:
         assert torch.equal(a[2][key], b[2][key]), key
+
+
+@pytest.mark.parametrize("name,D,k", [("C1", 16, 4), ("C2s", 64, 8), ("C4s", 128, 16)])
+def test_trainer_fused_head_matches_separate(designs, knob, name, D, k):
+    """The linear head + MSE fused into the last cell projection's epilogue (Y_cell
+    never stored) against the separate head kernels on the stored Y_cell: the
+    same quantities summed in another fixed order -- loss and every gradient
+    within 1e-6 relative (the oracle parity of the fused path is
+    test_gpu_parity.py::test_train_*)."""
+    from parity_util import row_err
+    d = designs[name]
+    g = dr.Graph.from_design(d)
+    P = make_params(D, D, D, 2, seed=23)
+    rng = np.random.default_rng(6)
+    xc = cuda(rng.standard_normal((d.n_cell, D)).astype(np.float32))
+    xn = cuda(rng.standard_normal((d.n_net, D)).astype(np.float32))
+    lab = cuda(d.labels)
+    out = {}
+    for fuse in (0, 1):
+        knob("head_fuse", fuse, 1)
+        flat = cuda(dr.flatten_params(P, 2))
+        tr = dr.Trainer(flat, 2, D, D, D, k, k)
+        grad = torch.empty_like(flat)
+        loss = tr.step(g, xc, xn, lab, grad_out=grad)
+        out[fuse] = (loss, to_np(grad).astype(np.float64))
+        tr.close()
+    assert abs(out[0][0] - out[1][0]) <= 1e-6 * abs(out[0][0])
+    g0 = dr.unflatten(out[0][1], 2, D, D, D)
+    g1 = dr.unflatten(out[1][1], 2, D, D, D)
+    for key in g0:
+        a = np.atleast_2d(g0[key])
+        b = np.atleast_2d(g1[key])
+        assert row_err(b, a) <= 1e-5, key
