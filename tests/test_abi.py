@@ -129,3 +129,17 @@ def test_caller_csc_degree_norm_validation():
 def test_debug_set_rejects_unknown_names():
     _expect(1, lambda: dr.debug_set("no_such_knob", 1))
     dr.debug_set("tspmm", 1)
+
+
+def test_new_entry_points_validate_before_any_launch():
+    """Round-2 entry points reject bad arguments on the host (no GPU needed):
+    the L2 read probe, the chained forward and the peer-memory shard calls."""
+    L = _lib.lib()
+    assert L.dr_probe_read(None, 1024, 1, None, None) == 1            # null buffers
+    buf = C.create_string_buffer(64)
+    assert L.dr_probe_read(C.cast(buf, C.c_void_p), 8, 1, C.cast(buf, C.c_void_p), None) == 1
+    assert L.dr_heteroconv_fwd_chain(None, None, None, None, None, None, None, 0, None, None, 0,
+                                     None) == 1                         # null graph / layer
+    assert L.dr_shard_spmm_fwd_peer(None, None, 64, 8, None, None) == 1
+    assert L.dr_shard_spmm_bwd_peer(None, None, None, 64, 8, None, None) == 1
+    assert L.dr_shard_inbox_reduce(None, None, None, None, None, None) == 1
