@@ -302,28 +302,35 @@ __device__ __forceinline__ void stg_put(float *stg, int stride, int lane, const 
 __device__ __forceinline__ void stg_out_f32(const float *stg, int stride, float *out, int64_t W,
                                             int64_t row0, int64_t n, int j, int lane) {
     const int cq = lane & 7, rs = lane >> 3;
+    // one 64-bit base and one bound per lane; rows rs, rs + 4, ... are W float4 apart
+    if (j + 4 * cq >= W) return;
+    const int64_t left = n - row0 - rs;
+    float4 *p = reinterpret_cast<float4 *>(out + (row0 + rs) * W + j) + cq;
+    const float *sp = stg + rs * stride + 4 * cq;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int r = 4 * i + rs;
-        const float4 v = *reinterpret_cast<const float4 *>(stg + r * stride + 4 * cq);
-        if (row0 + r < n && j + 4 * cq < W) __stcs(reinterpret_cast<float4 *>(out + (row0 + r) * W + j) + cq, v);
+        const float4 v = *reinterpret_cast<const float4 *>(sp + 4 * i * stride);
+        if (4 * i < left) __stcs(p + (int64_t)i * W, v);
     }
 }
 // split output ([hi | lo] bf16 rows of 2 W halves): hi at column j, lo at W + j
 __device__ __forceinline__ void stg_out_split(const float *stg, uint8_t *out, int64_t W, int64_t row0,
                                               int64_t n, int j, int lane) {
     const int cq = lane & 7, rs = lane >> 3;
+    if (j + 4 * cq >= W) return;
+    const int64_t left = n - row0 - rs;
+    uint8_t *rp = out + (row0 + rs) * W * 4 + 2 * (j + 4 * cq);    // hi piece; lo at + 2 W
+    const float *sp = stg + rs * kEStg + 4 * cq;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int r = 4 * i + rs;
-        const float4 v = *reinterpret_cast<const float4 *>(stg + r * kEStg + 4 * cq);
+        const float4 v = *reinterpret_cast<const float4 *>(sp + 4 * i * kEStg);
         uint2 h, l;
         tc::split_bf16x2(v.x, v.y, h.x, l.x);
         tc::split_bf16x2(v.z, v.w, h.y, l.y);
-        if (row0 + r < n && j + 4 * cq < W) {
-            uint8_t *rowp = out + (row0 + r) * W * 4;
-            __stcs(reinterpret_cast<uint2 *>(rowp + 2 * (j + 4 * cq)), h);
-            __stcs(reinterpret_cast<uint2 *>(rowp + 2 * (W + j + 4 * cq)), l);
+        if (4 * i < left) {
+            uint8_t *q = rp + (int64_t)i * 16 * W;                  // 4 rows of 4 W bytes
+            __stcs(reinterpret_cast<uint2 *>(q), h);
+            __stcs(reinterpret_cast<uint2 *>(q + 2 * W), l);
         }
     }
 }
@@ -394,10 +401,18 @@ __device__ __forceinline__ void epi_y32(const R2Args &a, uint32_t lb, int j, con
             if (a.G == 2) tc::tmem_ld16_nw(lb + (uint32_t)(N + jj), rb);
             tc::tmem_wait_ld();
         }
+        float ba[16], bb[16];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+            const float4 u = *reinterpret_cast<const float4 *>(bias_s + jj + 4 * q4);
+            ba[4 * q4] = u.x; ba[4 * q4 + 1] = u.y; ba[4 * q4 + 2] = u.z; ba[4 * q4 + 3] = u.w;
+            const float4 w = *reinterpret_cast<const float4 *>(bias_s + 256 + jj + 4 * q4);
+            bb[4 * q4] = w.x; bb[4 * q4 + 1] = w.y; bb[4 * q4 + 2] = w.z; bb[4 * q4 + 3] = w.w;
+        }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-            const float ya = jj < N ? __uint_as_float(ra[q]) + bias_s[jj + q] : 0.f;
-            const float yb = (a.G == 2 && jj < N) ? __uint_as_float(rb[q]) + bias_s[256 + jj + q] : 0.f;
+            const float ya = jj < N ? __uint_as_float(ra[q]) + ba[q] : 0.f;
+            const float yb = (a.G == 2 && jj < N) ? __uint_as_float(rb[q]) + bb[q] : 0.f;
             float v = ya;
             if (a.G == 2) v = a.merge == DR_MERGE_MAX ? (ya >= yb ? ya : yb) : ya + yb;
             y[16 * h + q] = v;
@@ -530,10 +545,20 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
         for (int h = 0; h < 2; ++h) {
             const int jj = j + 16 * h;
             float ya[16], yb[16];
+            // the 16 biases of this half as 4 broadcast 128-bit shared loads per group
+            // (jj is a multiple of 16: 64-B aligned)
+            float ba[16], bb[16];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                const float4 u = *reinterpret_cast<const float4 *>(bias_s + jj + 4 * q4);
+                ba[4 * q4] = u.x; ba[4 * q4 + 1] = u.y; ba[4 * q4 + 2] = u.z; ba[4 * q4 + 3] = u.w;
+                const float4 w = *reinterpret_cast<const float4 *>(bias_s + 256 + jj + 4 * q4);
+                bb[4 * q4] = w.x; bb[4 * q4 + 1] = w.y; bb[4 * q4 + 2] = w.z; bb[4 * q4 + 3] = w.w;
+            }
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-                ya[q] = jj < N ? __uint_as_float(ra[h][q]) + bias_s[jj + q] : 0.f;
-                yb[q] = (a.G == 2 && jj < N) ? __uint_as_float(rb[h][q]) + bias_s[256 + jj + q] : 0.f;
+                ya[q] = jj < N ? __uint_as_float(ra[h][q]) + ba[q] : 0.f;
+                yb[q] = (a.G == 2 && jj < N) ? __uint_as_float(rb[h][q]) + bb[q] : 0.f;
             }
             if (a.G == 2) {
 #pragma unroll
@@ -595,7 +620,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
     __shared__ __align__(8) uint64_t full[kMaxSA], conv[kMaxSA], empty[kMaxSA];
     __shared__ __align__(8) uint64_t bfull[kMaxSB], bempty[kMaxSB], accf[2], acce[2];
     __shared__ uint32_t tmem_slot;
-    __shared__ float bias_s[512];
+    __shared__ __align__(16) float bias_s[512];
     // fused head (NK < 0 only): w_h, b_h and the per-epilogue-warp sums
     float *head_s = nullptr;
     float (*hacc_s)[258] = nullptr;
