@@ -423,6 +423,45 @@ dr_status dr_shard_spmm_bwd_peer(const dr_shard *s, const float *dz_local, const
 dr_status dr_shard_inbox_reduce(const dr_shard *s, const float *inbox_local, const dr_cbsr *h_local,
                                 float *g_local, float *dx_local, void *stream);
 
+/* ---- a HeteroConv layer sharded by destination rows (f4, beyond the paper).
+ * One rank owns cell rows [c0, c1) and net rows [n0, n1): its three dr_shard
+ * must share one cell and one net partition -- near: cells -> cells (dst_part ==
+ * src_part), pins: cells -> nets, pinned: nets -> cells (DR_ERR_SHAPE_MISMATCH
+ * otherwise). The layer is Eq. 2-14 on the rank's rows; every exchange goes
+ * through peer memory (dr_peer_cbsr, as dr_shard_spmm_*_peer):
+ *   1. every rank: its local CBSR of cells and nets = dr_drelu_topk of its X rows
+ *      (max_src rows each, zero rows past its range) -- h_cell / h_net.val[rank];
+ *   2. (after all ranks' step 1) dr_shard_layer_fwd: the three SpMMs read remote
+ *      CBSR rows in place, then the projections / max-merge on the local rows;
+ *      y_cell [c1 - c0 x d_out], y_net [n1 - n0 x d_out];
+ *   3. dr_shard_layer_bwd: dZ' and the Sage root terms on the local rows, the
+ *      SSpMMs write every per-source sum into its owner's inbox (cells: [2 x
+ *      world x max_src_cell x k_cell] = near, pins slots; nets: [world x
+ *      max_src_net x k_net]), and this rank's rows' contribution to every weight
+ *      gradient (the caller allreduces `grads` over ranks: dW is a sum over rows);
+ *   4. (after all ranks' step 3) dr_shard_layer_dx: the owner adds up its inbox
+ *      slots in a fixed order (+ its root terms) and scatters the D-ReLU mask
+ *      gradient: dx_cell [c1 - c0 x d_cell], dx_net [n1 - n0 x d_net].
+ * dy_net may not be NULL; no k_pins; the layer set borrows the shards. */
+typedef struct dr_shard_layer dr_shard_layer;
+dr_status dr_shard_layer_create(const dr_shard *near, const dr_shard *pins, const dr_shard *pinned,
+                                dr_shard_layer **out);
+dr_status dr_shard_layer_destroy(dr_shard_layer *sl);
+dr_status dr_shard_layer_tape_bytes(const dr_shard_layer *sl, const dr_layer *L, uint32_t flags,
+                                    size_t *bytes);
+dr_status dr_shard_layer_fwd(const dr_shard_layer *sl, const dr_layer *L, const dr_peer_cbsr *h_cell,
+                             const dr_peer_cbsr *h_net, float *y_cell, float *y_net, void *tape,
+                             uint32_t flags, void *stream);
+dr_status dr_shard_layer_bwd(const dr_shard_layer *sl, const dr_layer *L, void *tape,
+                             const float *dy_cell, const float *dy_net, const dr_peer_cbsr *h_cell,
+                             const dr_peer_cbsr *h_net, float *const *inbox_cell,
+                             float *const *inbox_net, dr_layer_grad *grads, uint32_t flags,
+                             void *stream);
+dr_status dr_shard_layer_dx(const dr_shard_layer *sl, const dr_layer *L, void *tape,
+                            const dr_peer_cbsr *h_cell, const dr_peer_cbsr *h_net,
+                            const float *inbox_cell, const float *inbox_net, float *dx_cell,
+                            float *dx_net, void *stream);
+
 /* Per-kernel device timing: between dr_profile_begin and dr_profile_end every
  * libdr launch issued by this host thread is bracketed by CUDA events on the
  * stream it is launched on. dr_profile_end synchronises, aggregates by kernel

@@ -562,6 +562,100 @@ def heteroconv_bwd(g, layer, tape, dy_cell, dy_net, need_dx=True, flags=0, strea
     return grads, dxc, dxn
 
 
+def _grad_struct(layer, dev):
+    torch = _torch()
+    grads = {k: torch.empty_like(v) for k, v in layer.W.items() if v is not None}
+    G = dr_layer_grad()
+    G.wn[DR_NEAR] = grads["wn_near"].data_ptr()
+    G.wn[DR_PINNED] = grads["w_pinned"].data_ptr()
+    G.wn[DR_PINS] = grads["wn_pins"].data_ptr()
+    G.wr[DR_NEAR] = grads["wr_near"].data_ptr() if "wr_near" in grads else None
+    G.wr[DR_PINS] = grads["wr_pins"].data_ptr() if "wr_pins" in grads else None
+    G.b[DR_NEAR] = grads["b_near"].data_ptr()
+    G.b[DR_PINNED] = grads["b_pinned"].data_ptr()
+    G.b[DR_PINS] = grads["b_pins"].data_ptr()
+    return grads, G
+
+
+class ShardLayer:
+    """dr_shard_layer (f4): a HeteroConv layer over this rank's rows of three
+    dr_shard (near, pins, pinned) sharing one cell and one net partition; the
+    exchanges go through peer memory (lists of per-rank (val, idx) CBSR and
+    per-rank inboxes, tensors or raw device pointers)."""
+
+    def __init__(self, near, pins, pinned):
+        h = C.c_void_p()
+        check(lib().dr_shard_layer_create(near.handle, pins.handle, pinned.handle, C.byref(h)))
+        self.handle = h
+        self.shards = (near, pins, pinned)
+        self.world, self.rank = near.world, near.rank
+        self.n_cell = near.dst_end - near.dst_begin
+        self.n_net = pins.dst_end - pins.dst_begin
+        self.m_cell, self.m_net = near.max_src, pinned.max_src
+
+    def tape_bytes(self, layer, flags=0):
+        n = C.c_size_t()
+        check(lib().dr_shard_layer_tape_bytes(self.handle, C.byref(layer.c), flags, C.byref(n)))
+        return n.value
+
+    def _peer(self, peers):
+        from ._lib import dr_peer_cbsr
+        pc = dr_peer_cbsr()
+        pc.world = self.world
+        for q, (v, i) in enumerate(peers):
+            pc.val[q] = v if isinstance(v, int) else v.data_ptr()
+            pc.idx[q] = i if isinstance(i, int) else i.data_ptr()
+        return pc
+
+    def fwd(self, layer, peers_cell, peers_net, tape=None, flags=0, device="cuda", stream=None):
+        torch = _torch()
+        D = layer.c.d_out
+        yc = torch.empty((self.n_cell, D), device=device, dtype=torch.float32)
+        yn = torch.empty((self.n_net, D), device=device, dtype=torch.float32)
+        if tape is None:
+            tape = torch.empty(self.tape_bytes(layer, flags), device=device, dtype=torch.uint8)
+        hc, hn = self._peer(peers_cell), self._peer(peers_net)
+        check(lib().dr_shard_layer_fwd(self.handle, C.byref(layer.c), C.byref(hc), C.byref(hn),
+                                       _ptr(yc), _ptr(yn), _ptr(tape), flags, _stream(stream)))
+        return yc, yn, tape
+
+    def bwd(self, layer, tape, dy_cell, dy_net, peers_cell, peers_net, inbox_cell, inbox_net,
+            flags=0, stream=None):
+        """Writes this rank's slots of every owner's inboxes; returns this rank's
+        rows' contribution to the weight gradients (sum over ranks = the layer's)."""
+        grads, G = _grad_struct(layer, dy_cell.device)
+        hc, hn = self._peer(peers_cell), self._peer(peers_net)
+        ic = (C.c_void_p * 8)(*[(x if isinstance(x, int) else x.data_ptr()) for x in inbox_cell])
+        inn = (C.c_void_p * 8)(*[(x if isinstance(x, int) else x.data_ptr()) for x in inbox_net])
+        check(lib().dr_shard_layer_bwd(self.handle, C.byref(layer.c), _ptr(tape), _ptr(dy_cell),
+                                       _ptr(dy_net), C.byref(hc), C.byref(hn), ic, inn, C.byref(G),
+                                       flags, _stream(stream)))
+        return grads
+
+    def dx(self, layer, tape, peers_cell, peers_net, inbox_cell_local, inbox_net_local,
+           stream=None):
+        torch = _torch()
+        dev = tape.device
+        dxc = torch.empty((self.n_cell, layer.c.d_cell), device=dev, dtype=torch.float32)
+        dxn = torch.empty((self.n_net, layer.c.d_net), device=dev, dtype=torch.float32)
+        hc, hn = self._peer(peers_cell), self._peer(peers_net)
+        check(lib().dr_shard_layer_dx(self.handle, C.byref(layer.c), _ptr(tape), C.byref(hc),
+                                      C.byref(hn), _ptr(inbox_cell_local), _ptr(inbox_net_local),
+                                      _ptr(dxc), _ptr(dxn), _stream(stream)))
+        return dxc, dxn
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().dr_shard_layer_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 # ------------------------------------------------------------------ training
 PARAM_ORDER = ("wn_near", "wr_near", "b_near", "w_pinned", "b_pinned", "wn_pins", "wr_pins",
                "b_pins")

@@ -128,6 +128,17 @@ _SIGS = {
     "dr_shard_spmm_bwd_peer": (C.c_int, [P, P, C.POINTER(dr_peer_cbsr), C.c_int32, C.c_int32,
                                          C.POINTER(C.c_void_p), P]),
     "dr_shard_inbox_reduce": (C.c_int, [P, P, C.POINTER(dr_cbsr), P, P, P]),
+    "dr_shard_layer_create": (C.c_int, [P, P, P, C.POINTER(P)]),
+    "dr_shard_layer_destroy": (C.c_int, [P]),
+    "dr_shard_layer_tape_bytes": (C.c_int, [P, C.POINTER(dr_layer), C.c_uint32,
+                                            C.POINTER(C.c_size_t)]),
+    "dr_shard_layer_fwd": (C.c_int, [P, C.POINTER(dr_layer), C.POINTER(dr_peer_cbsr),
+                                     C.POINTER(dr_peer_cbsr), P, P, P, C.c_uint32, P]),
+    "dr_shard_layer_bwd": (C.c_int, [P, C.POINTER(dr_layer), P, P, P, C.POINTER(dr_peer_cbsr),
+                                     C.POINTER(dr_peer_cbsr), C.POINTER(C.c_void_p),
+                                     C.POINTER(C.c_void_p), C.POINTER(dr_layer_grad), C.c_uint32, P]),
+    "dr_shard_layer_dx": (C.c_int, [P, C.POINTER(dr_layer), P, C.POINTER(dr_peer_cbsr),
+                                    C.POINTER(dr_peer_cbsr), P, P, P, P, P]),
     "dr_heteroconv_tape_bytes": (C.c_int, [P, C.POINTER(dr_layer), C.c_uint32,
                                            C.POINTER(C.c_size_t)]),
     "dr_heteroconv_fwd": (C.c_int, [P, C.POINTER(dr_layer), P, P, P, P, P, C.c_uint32, P]),

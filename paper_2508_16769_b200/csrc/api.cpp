@@ -251,6 +251,15 @@ static bool z_split_ok(const dr_layer *L, int) {
            L->k_net <= 32;
 }
 
+// f4, a layer over dr_shards (dr_shard_layer_*): this rank's destination rows,
+// every source row read in place from its owner (peer memory), every per-source
+// backward contribution written in place into its owner's inbox
+struct ShardCtx {
+    PeerSrc cell, net;                 // all ranks' local CBSR (pv / pi)
+    PeerSrc near_g, pins_g, pinned_g;  // + the inbox slots each relation writes (pg)
+    int rank;
+};
+
 // ------------------------------------------------------------------ layer forward / backward
 // Ln / tape_next (row a5): the next layer and its tape; when given, the
 // projection epilogues also write the next layer's input CBSR (Eq. 2-3 on Y_cell
@@ -263,10 +272,12 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
                            float *yc, float *yn, void *tape, uint32_t flags, cudaStream_t st,
                            const dr_layer *Ln = nullptr, void *tape_next = nullptr,
                            uint32_t flags_next = 0, const HeadArgs *head = nullptr,
-                           int *head_parts = nullptr) {
+                           int *head_parts = nullptr, const ShardCtx *sh = nullptr) {
     if (head_parts) *head_parts = 0;
     const TapeLayout T = tape_layout(g, L, flags);
-    const bool in_tape = (flags & DR_FWD_INPUT_IN_TAPE) != 0;
+    const bool in_tape = (flags & DR_FWD_INPUT_IN_TAPE) != 0 || sh != nullptr;
+    DR_CHECK(!sh || (!Ln && !head && !pins_own(L)), DR_ERR_UNSUPPORTED,
+             "sharded layer: no chaining, fused head or k_pins");
     TapeLayout TN{};
     char *tn = (char *)tape_next;
     if (Ln) TN = tape_layout(g, Ln, flags_next);
@@ -285,14 +296,21 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
     char *tp = (char *)tape;
     float *hcv = (float *)(tp + T.hc_val), *hnv = (float *)(tp + T.hn_val);
     uint8_t *hci = (uint8_t *)(tp + T.hc_idx), *hni = (uint8_t *)(tp + T.hn_idx);
-    float *hpv = (float *)(tp + T.hp_val);
-    uint8_t *hpi = (uint8_t *)(tp + T.hp_idx);
+    if (sh) {          // this rank's own CBSR (its rows are the local rows)
+        hcv = const_cast<float *>(sh->cell.pv[sh->rank]);
+        hci = const_cast<uint8_t *>(sh->cell.pi[sh->rank]);
+        hnv = const_cast<float *>(sh->net.pv[sh->rank]);
+        hni = const_cast<uint8_t *>(sh->net.pi[sh->rank]);
+    }
+    float *hpv = sh ? hcv : (float *)(tp + T.hp_val);
+    uint8_t *hpi = sh ? hci : (uint8_t *)(tp + T.hp_idx);
     const int kp = k_pins_of(L);
     float *z[3];
     for (int r = 0; r < 3; ++r) z[r] = (float *)(tp + T.z[r]);
     const int nc = g->n_cell, nn = g->n_net;
     bool zs[3];
-    for (int r = 0; r < 3; ++r) zs[r] = z_split_ok(L, r);
+    for (int r = 0; r < 3; ++r) zs[r] = !sh && z_split_ok(L, r);
+    const PeerSrc *pc = sh ? &sh->cell : nullptr, *pn = sh ? &sh->net : nullptr;
     // ---- the two projections (tensor-core row GEMMs when the shapes allow) and
     // their packed weight images, packed by ONE launch before the streams fork
     Tc2RowsDesc dnet, dcell;
@@ -382,15 +400,15 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[0], s0));                               // H_c ready
     if (!in_tape) { TagScope t("net"); launch_drelu(xn, nn, L->d_net, L->d_net, L->k_net, hnv, hni, s2); }
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[1], s2));                               // H_n ready
-    { TagScope t("near"); launch_spmm_fwd(g->rel[DR_NEAR], hcv, hci, L->k_cell, L->d_cell, z[DR_NEAR], s0, zs[DR_NEAR]); }  // Eq. 5-7
+    { TagScope t("near"); launch_spmm_fwd(g->rel[DR_NEAR], hcv, hci, L->k_cell, L->d_cell, z[DR_NEAR], s0, zs[DR_NEAR], NgSched{}, pc); }  // Eq. 5-7
     if (pins_own(L)) {          // Q27: pins' own cell CBSR, on its own stream
         TagScope t("pins");
         launch_drelu(xc, nc, L->d_cell, L->d_cell, kp, hpv, hpi, s1);
     } else if (!seq) {
         DR_CUDA(cudaStreamWaitEvent(s1, C.ev[0], 0));
     }
-    if (!no_net) { TagScope t("pins"); launch_spmm_fwd(g->rel[DR_PINS], hpv, hpi, kp, L->d_cell, z[DR_PINS], s1, zs[DR_PINS]); }
-    { TagScope t("pinned"); launch_spmm_fwd(g->rel[DR_PINNED], hnv, hni, L->k_net, L->d_net, z[DR_PINNED], s2, zs[DR_PINNED]); }
+    if (!no_net) { TagScope t("pins"); launch_spmm_fwd(g->rel[DR_PINS], hpv, hpi, kp, L->d_cell, z[DR_PINS], s1, zs[DR_PINS], NgSched{}, pc); }
+    { TagScope t("pinned"); launch_spmm_fwd(g->rel[DR_PINNED], hnv, hni, L->k_net, L->d_net, z[DR_PINNED], s2, zs[DR_PINNED], NgSched{}, pn); }
     if (!seq) DR_CUDA(cudaEventRecord(C.ev[2], s2));                               // Z_pinned ready
     if (!seq) DR_CUDA(cudaStreamWaitEvent(s1, C.ev[1], 0));
     if (!no_net) {   // net: Y_net = Z_pins Wn_pins + densify(H_n) Wr_pins + b_pins   (Eq. 7, 9)
@@ -445,13 +463,20 @@ static void heteroconv_fwd(const dr_graph *g, const dr_layer *L, const float *xc
 // launches them once for several layers); nullptr: one launch at the end here
 static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, const float *dyc,
                            const float *dyn, float *dxc, float *dxn, dr_layer_grad *G,
-                           uint32_t flags, cudaStream_t st, Tc2Deferred *defer = nullptr) {
+                           uint32_t flags, cudaStream_t st, Tc2Deferred *defer = nullptr,
+                           const ShardCtx *sh = nullptr) {
     Tc2Deferred own_parts;
     Tc2Deferred *pq = defer ? defer : &own_parts;
     const TapeLayout T = tape_layout(g, L, flags);
     char *tp = (char *)tape;
     const float *hcv = (float *)(tp + T.hc_val), *hnv = (float *)(tp + T.hn_val);
     const uint8_t *hci = (uint8_t *)(tp + T.hc_idx), *hni = (uint8_t *)(tp + T.hn_idx);
+    if (sh) {
+        hcv = sh->cell.pv[sh->rank];
+        hci = sh->cell.pi[sh->rank];
+        hnv = sh->net.pv[sh->rank];
+        hni = sh->net.pi[sh->rank];
+    }
     const uint8_t *hpi = (uint8_t *)(tp + T.hp_idx);
     const int kp = k_pins_of(L);
     const bool own = pins_own(L);
@@ -470,7 +495,7 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
     // ---- dZ' row GEMMs: descriptors and their packed weights (B_op[n][kk] = W[n][kk],
     // Wn in columns [0, Kd), the Sage root weight Wr in [Kd, N)), one packing launch
     const RelDev &rn = g->rel[DR_NEAR];
-    const bool near_tiled = dxc && !rn.ewT && rn.n_src == nc &&
+    const bool near_tiled = !sh && dxc && !rn.ewT && rn.n_src == nc &&
                             tspmm_supported(rn.tilesT, L->d_cell, L->k_cell);
     Tc2RowsDesc dzd[3];
     bool dz_tc[3] = {false, false, false};
@@ -558,7 +583,30 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
         // SSpMM per source node type (Alg. 2 stage 2-3, ownership instead of atomics)
         // dY_net == 0 (dyn == NULL): no pins term (dZ'_pins = 0) and no pins root term
         const float *rootc = L->wr[DR_NEAR] ? root_c : nullptr;
-        if (dxc) {
+        if (sh) {
+            // sharded: every relation's per-source sums go straight into the source
+            // owners' inbox slots (the owners add them up, dr_shard_layer_dx)
+            if (dxc) {
+                if (!seq) DR_CUDA(cudaStreamWaitEvent(s0, C.ev[0], 0));
+                TagScope t("cell");
+                const RelDev &rp = g->rel[DR_PINS];
+                launch_spmm_bwd(rn.bwd, rn.n_src, BwdTerm{&rn, dz[DR_NEAR], false}, BwdTerm{}, nullptr,
+                                nullptr, L->k_cell, L->d_cell, nullptr, nullptr, false, s0, NgSched{},
+                                &sh->near_g);
+                if (dyn)
+                    launch_spmm_bwd(rp.bwd, rp.n_src, BwdTerm{&rp, dz[DR_PINS], false}, BwdTerm{},
+                                    nullptr, nullptr, L->k_cell, L->d_cell, nullptr, nullptr, false, s0,
+                                    NgSched{}, &sh->pins_g);
+            }
+            if (dxn) {
+                if (!seq) DR_CUDA(cudaStreamWaitEvent(s2, C.ev[0], 0));
+                TagScope t("net");
+                const RelDev &rq = g->rel[DR_PINNED];
+                launch_spmm_bwd(rq.bwd, rq.n_src, BwdTerm{&rq, dz[DR_PINNED], false}, BwdTerm{},
+                                nullptr, nullptr, L->k_net, L->d_net, nullptr, nullptr, false, s2,
+                                NgSched{}, &sh->pinned_g);
+            }
+        } else if (dxc) {
             if (!seq) DR_CUDA(cudaStreamWaitEvent(s0, C.ev[0], 0));
             BwdTerm t0{&g->rel[DR_NEAR], dz[DR_NEAR], false}, t1{&g->rel[DR_PINS], dz[DR_PINS], false};
             if (!dyn) t1 = BwdTerm{};
@@ -597,7 +645,7 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
                                 L->k_cell, L->d_cell, nullptr, dxc, false, s0);
             }
         }
-        if (dxn) {
+        if (dxn && !sh) {
             if (!seq) DR_CUDA(cudaStreamWaitEvent(s2, C.ev[0], 0));
             BwdTerm t0{&g->rel[DR_PINNED], dz[DR_PINNED], false}, t1{};
             TagScope t("net");
@@ -632,7 +680,7 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
         TagScope t("near");
         if (!dwt(nc, z[DR_NEAR], L->d_cell, G->wn[DR_NEAR], hcv, hci, L->k_cell, L->d_cell,
                  L->wr[DR_NEAR] ? G->wr[DR_NEAR] : nullptr, dyc, mode_near, G->b[DR_NEAR],
-                 work[0], s0, z_split_ok(L, DR_NEAR))) {
+                 work[0], s0, !sh && z_split_ok(L, DR_NEAR))) {
             dw(nc, L->d_cell, z[DR_NEAR], nullptr, nullptr, 0, dyc, mode_near, G->wn[DR_NEAR],
                G->b[DR_NEAR], work[0], s0);
             TagScope t2("root");
@@ -644,7 +692,7 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
     {
         TagScope t("pinned");
         if (!dwt(nc, z[DR_PINNED], L->d_net, G->wn[DR_PINNED], nullptr, nullptr, 0, 0, nullptr,
-                 dyc, mode_pinned, G->b[DR_PINNED], work[2], s2, z_split_ok(L, DR_PINNED)))
+                 dyc, mode_pinned, G->b[DR_PINNED], work[2], s2, !sh && z_split_ok(L, DR_PINNED)))
             dw(nc, L->d_net, z[DR_PINNED], nullptr, nullptr, 0, dyc, mode_pinned,
                G->wn[DR_PINNED], G->b[DR_PINNED], work[2], s2);
     }
@@ -656,7 +704,7 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
         TagScope t("pins");
         if (!dwt(nn, z[DR_PINS], L->d_cell, G->wn[DR_PINS], hnv, hni, L->k_net, L->d_net,
                  L->wr[DR_PINS] ? G->wr[DR_PINS] : nullptr, dyn, kMaskNone, G->b[DR_PINS],
-                 work[1], s1, z_split_ok(L, DR_PINS))) {
+                 work[1], s1, !sh && z_split_ok(L, DR_PINS))) {
             dw(nn, L->d_cell, z[DR_PINS], nullptr, nullptr, 0, dyn, kMaskNone, G->wn[DR_PINS],
                G->b[DR_PINS], work[1], s1);
             TagScope t2("root");
@@ -1065,6 +1113,158 @@ dr_status dr_heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape,
     DR_CHECK(dy_cell, DR_ERR_INVALID_ARGUMENT, "null dy_cell");
     heteroconv_bwd(g, L, tape, dy_cell, dy_net, dx_cell, dx_net, grads, flags,
                    (cudaStream_t)stream);
+    DR_API_END
+}
+
+// ------------------------------------------------------------------ f4: a sharded layer
+}  // extern "C"
+
+struct dr_shard_layer {
+    dr_graph g;                        // local rows; rel[r] = the shard blocks (not owned)
+    int32_t world = 1, rank = 0, m_cell = 0, m_net = 0;
+};
+
+namespace {
+ShardCtx shard_ctx(const dr_shard_layer *sl, const dr_layer *L, const dr_peer_cbsr *hc,
+                   const dr_peer_cbsr *hn, float *const *inbox_c, float *const *inbox_n) {
+    DR_CHECK(hc && hn && hc->world == sl->world && hn->world == sl->world, DR_ERR_INVALID_ARGUMENT,
+             "shard_layer: peer tables missing or of another world size");
+    ShardCtx c{};
+    c.rank = sl->rank;
+    c.cell.m = sl->m_cell;
+    c.net.m = sl->m_net;
+    c.cell.rank = c.net.rank = sl->rank;
+    for (int q = 0; q < sl->world; ++q) {
+        DR_CHECK(hc->val[q] && hc->idx[q] && hn->val[q] && hn->idx[q], DR_ERR_INVALID_ARGUMENT,
+                 "shard_layer: null CBSR pointer in a peer table");
+        c.cell.pv[q] = hc->val[q];
+        c.cell.pi[q] = (const uint8_t *)hc->idx[q];
+        c.net.pv[q] = hn->val[q];
+        c.net.pi[q] = (const uint8_t *)hn->idx[q];
+    }
+    c.near_g = c.pins_g = c.cell;
+    c.pinned_g = c.net;
+    if (inbox_c && inbox_n) {
+        const int64_t slot_c = (int64_t)sl->world * sl->m_cell * L->k_cell;
+        for (int q = 0; q < sl->world; ++q) {
+            DR_CHECK(inbox_c[q] && inbox_n[q], DR_ERR_INVALID_ARGUMENT, "shard_layer: null inbox");
+            c.near_g.pg[q] = inbox_c[q];               // slots [0][rank]
+            c.pins_g.pg[q] = inbox_c[q] + slot_c;      // slots [1][rank]
+            c.pinned_g.pg[q] = inbox_n[q];
+        }
+    }
+    return c;
+}
+void check_shard_layer(const dr_shard_layer *sl, const dr_layer *L) {
+    DR_CHECK(sl != nullptr, DR_ERR_INVALID_ARGUMENT, "shard_layer: null layer set");
+    check_layer(&sl->g, L);
+    DR_CHECK(!pins_own(L), DR_ERR_UNSUPPORTED, "shard_layer: k_pins is not supported");
+}
+}  // namespace
+
+extern "C" {
+
+dr_status dr_shard_layer_create(const dr_shard *near, const dr_shard *pins, const dr_shard *pinned,
+                                dr_shard_layer **out) {
+    DR_API_BEGIN
+    DR_CHECK(near && pins && pinned && out, DR_ERR_INVALID_ARGUMENT, "shard_layer: null argument");
+    *out = nullptr;
+    const int W = near->world;
+    DR_CHECK(pins->world == W && pinned->world == W && pins->rank == near->rank &&
+                 pinned->rank == near->rank && W <= kMaxPeers,
+             DR_ERR_INVALID_ARGUMENT, "shard_layer: shards of different worlds / ranks (or > 8)");
+    // cells: near dst == near src == pinned dst == pins src ranges; nets: pins dst == pinned src
+    DR_CHECK(near->dst_begin == near->src_begin && near->dst_end == near->src_end &&
+                 pinned->dst_begin == near->dst_begin && pinned->dst_end == near->dst_end &&
+                 pins->src_begin == near->src_begin && pins->src_end == near->src_end &&
+                 pins->max_src == near->max_src && pinned->src_begin == pins->dst_begin &&
+                 pinned->src_end == pins->dst_end,
+             DR_ERR_SHAPE_MISMATCH,
+             "shard_layer: the three shards must share one cell and one net partition "
+             "(near: cells -> cells, pins: cells -> nets, pinned: nets -> cells)");
+    std::unique_ptr<dr_shard_layer> sl(new dr_shard_layer());
+    sl->world = W;
+    sl->rank = near->rank;
+    sl->m_cell = near->max_src;
+    sl->m_net = pinned->max_src;
+    sl->g.n_cell = (int32_t)(near->dst_end - near->dst_begin);
+    sl->g.n_net = (int32_t)(pins->dst_end - pins->dst_begin);
+    sl->g.rel[DR_NEAR] = near->rel;
+    sl->g.rel[DR_PINS] = pins->rel;
+    sl->g.rel[DR_PINNED] = pinned->rel;
+    *out = sl.release();
+    DR_API_END
+}
+
+dr_status dr_shard_layer_destroy(dr_shard_layer *sl) {
+    delete sl;
+    return DR_OK;
+}
+
+dr_status dr_shard_layer_tape_bytes(const dr_shard_layer *sl, const dr_layer *L, uint32_t flags,
+                                    size_t *bytes) {
+    DR_API_BEGIN
+    check_shard_layer(sl, L);
+    DR_CHECK(bytes != nullptr, DR_ERR_INVALID_ARGUMENT, "null bytes");
+    *bytes = tape_layout(&sl->g, L, flags).total;
+    DR_API_END
+}
+
+dr_status dr_shard_layer_fwd(const dr_shard_layer *sl, const dr_layer *L, const dr_peer_cbsr *h_cell,
+                             const dr_peer_cbsr *h_net, float *y_cell, float *y_net, void *tape,
+                             uint32_t flags, void *stream) {
+    DR_API_BEGIN
+    check_shard_layer(sl, L);
+    DR_CHECK(tape && (sl->g.n_cell == 0 || y_cell) && (sl->g.n_net == 0 || y_net),
+             DR_ERR_INVALID_ARGUMENT, "shard_layer_fwd: null tape / output");
+    const ShardCtx c = shard_ctx(sl, L, h_cell, h_net, nullptr, nullptr);
+    heteroconv_fwd(&sl->g, L, nullptr, nullptr, y_cell, y_net, tape, flags & ~DR_FWD_NO_NET_OUT,
+                   (cudaStream_t)stream, nullptr, nullptr, 0, nullptr, nullptr, &c);
+    DR_API_END
+}
+
+dr_status dr_shard_layer_bwd(const dr_shard_layer *sl, const dr_layer *L, void *tape,
+                             const float *dy_cell, const float *dy_net, const dr_peer_cbsr *h_cell,
+                             const dr_peer_cbsr *h_net, float *const *inbox_cell,
+                             float *const *inbox_net, dr_layer_grad *grads, uint32_t flags,
+                             void *stream) {
+    DR_API_BEGIN
+    check_shard_layer(sl, L);
+    DR_CHECK(tape && grads && dy_cell && dy_net && inbox_cell && inbox_net, DR_ERR_INVALID_ARGUMENT,
+             "shard_layer_bwd: null argument");
+    for (int r = 0; r < 3; ++r) {
+        DR_CHECK(grads->wn[r] && grads->b[r], DR_ERR_INVALID_ARGUMENT, "null grad wn/b");
+        DR_CHECK(!L->wr[r] || grads->wr[r], DR_ERR_INVALID_ARGUMENT, "null grad wr");
+    }
+    const ShardCtx c = shard_ctx(sl, L, h_cell, h_net, inbox_cell, inbox_net);
+    // dx pointers only switch the SSpMM on: the sharded path writes the inboxes
+    float *on = reinterpret_cast<float *>(tape);
+    heteroconv_bwd(&sl->g, L, tape, dy_cell, dy_net, on, on, grads, flags, (cudaStream_t)stream,
+                   nullptr, &c);
+    DR_API_END
+}
+
+dr_status dr_shard_layer_dx(const dr_shard_layer *sl, const dr_layer *L, void *tape,
+                            const dr_peer_cbsr *h_cell, const dr_peer_cbsr *h_net,
+                            const float *inbox_cell, const float *inbox_net, float *dx_cell,
+                            float *dx_net, void *stream) {
+    DR_API_BEGIN
+    check_shard_layer(sl, L);
+    DR_CHECK(tape && inbox_cell && inbox_net && dx_cell && dx_net, DR_ERR_INVALID_ARGUMENT,
+             "shard_layer_dx: null argument");
+    const ShardCtx c = shard_ctx(sl, L, h_cell, h_net, nullptr, nullptr);
+    const TapeLayout T = tape_layout(&sl->g, L, 0);
+    char *tp = (char *)tape;
+    float *root_c = (float *)(tp + T.root_c), *root_n = (float *)(tp + T.root_n);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nc = sl->g.n_cell, nn = sl->g.n_net;
+    // cells: near and pins slots of every rank (+ the Sage root term), then the mask scatter
+    launch_inbox_root(inbox_cell, 2 * sl->world, (int64_t)sl->m_cell * L->k_cell,
+                      L->wr[DR_NEAR] ? root_c : nullptr, nc * L->k_cell, root_c, st);
+    launch_cbsr_scatter(root_c, c.cell.pi[sl->rank], nc, L->k_cell, L->d_cell, dx_cell, st);
+    launch_inbox_root(inbox_net, sl->world, (int64_t)sl->m_net * L->k_net,
+                      L->wr[DR_PINS] ? root_n : nullptr, nn * L->k_net, root_n, st);
+    launch_cbsr_scatter(root_n, c.net.pi[sl->rank], nn, L->k_net, L->d_net, dx_net, st);
     DR_API_END
 }
 

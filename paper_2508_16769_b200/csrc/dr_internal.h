@@ -182,6 +182,18 @@ struct dr_graph {
     cudaStream_t create_stream = nullptr;
 };
 
+// one relation's destination-row block on one rank (shard.cpp, f4)
+struct dr_shard {
+    int32_t world = 1, rank = 0, max_src = 0;
+    int64_t dst_begin = 0, dst_end = 0, src_begin = 0, src_end = 0;
+    int32_t n_src_glob = 0;
+    dr::RelDev rel;                 // rows = local destinations, cols = padded sources
+    dr::Alloc alloc;
+    std::vector<void *> blocks;
+    size_t bytes = 0;
+    cudaStream_t stream = nullptr;
+};
+
 namespace dr {
 
 // ------------------------------------------------------------------ kernels (launchers)
@@ -213,6 +225,10 @@ struct NgSched {
 // backward reads its destinations' K coalesced beside row[] instead of gathering
 // two rowptr entries per edge.
 // dx[i, :] = 0 except dx[i, idx[i, t]] = g[i, t] (the D-ReLU mask gradient scatter)
+// f4 sharded layer: out[e] = root[e] (root may be null) + sum over nslots slots
+// (slot_stride apart) of inbox[e], fixed order; out may alias root
+void launch_inbox_root(const float *inbox, int nslots, int64_t slot_stride, const float *root,
+                       int64_t n, float *out, cudaStream_t s);
 // f4: out = fixed-order sum over `world` stacked [n] blocks of `inbox`
 void launch_inbox_sum(const float *inbox, int world, int64_t n, float *out, cudaStream_t s);
 void launch_cbsr_scatter(const float *g, const uint8_t *idx, int64_t n, int k, int dim, float *dx,

@@ -14,16 +14,6 @@
 #include "dr_internal.h"
 #include "nccl_api.h"
 
-struct dr_shard {
-    int32_t world = 1, rank = 0, max_src = 0;
-    int64_t dst_begin = 0, dst_end = 0, src_begin = 0, src_end = 0;
-    int32_t n_src_glob = 0;
-    dr::RelDev rel;                 // rows = local destinations, cols = padded sources
-    dr::Alloc alloc;
-    std::vector<void *> blocks;
-    size_t bytes = 0;
-    cudaStream_t stream = nullptr;
-};
 
 using namespace dr;
 

@@ -678,6 +678,17 @@ __global__ void inbox_sum_kernel(const float *__restrict__ inbox, int world, int
     }
 }
 
+// f4 sharded layer: g[e] = root[e] (optional) + sum over slots s of inbox[s][e], fixed order
+__global__ void inbox_root_kernel(const float *__restrict__ inbox, int nslots, int64_t slot_stride,
+                                  const float *root, int64_t n, float *out) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        float acc = root ? root[e] : 0.f;          // (out may alias root: same element)
+        for (int q = 0; q < nslots; ++q) acc += __ldg(inbox + (int64_t)q * slot_stride + e);
+        out[e] = acc;
+    }
+}
+
 // one warp per row: zero the row, then drop the k values at their columns
 __global__ void cbsr_scatter_kernel(const float *__restrict__ g, const uint8_t *__restrict__ idx,
                                     int64_t n, int k, int dim, float *__restrict__ dx) {
@@ -698,6 +709,15 @@ void launch_inbox_sum(const float *inbox, int world, int64_t n, float *out, cuda
     if (blocks > 148 * 8) blocks = 148 * 8;
     inbox_sum_kernel<<<(unsigned)blocks, 256, 0, s>>>(inbox, world, n, out);
     note_launch("inbox_sum");
+}
+
+void launch_inbox_root(const float *inbox, int nslots, int64_t slot_stride, const float *root,
+                       int64_t n, float *out, cudaStream_t s) {
+    if (n <= 0) return;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    inbox_root_kernel<<<(unsigned)blocks, 256, 0, s>>>(inbox, nslots, slot_stride, root, n, out);
+    note_launch("inbox_root");
 }
 
 void launch_cbsr_scatter(const float *g, const uint8_t *idx, int64_t n, int k, int dim, float *dx,
