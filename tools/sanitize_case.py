@@ -33,3 +33,32 @@ for _ in range(3):                       # eager, captured, replayed
     tr.step(g, xc, xn, torch.as_tensor(d.labels).cuda())
 torch.cuda.synchronize()
 print("sanitize case done", file=sys.stderr)
+# f4: peer-memory shard exchange and the sharded layer, 2 virtual ranks
+W = 2
+cp, _ = dr.shard_plan(*d.rel("near")[:2], d.rel("near")[3], W)
+npart, _ = dr.shard_plan(*d.rel("pins")[:2], d.rel("pins")[3], W)
+lays = []
+for r in range(W):
+    sn = dr.Shard.from_design(d, "near", W, r, dst_part=cp, src_part=cp)
+    sp = dr.Shard.from_design(d, "pins", W, r, dst_part=npart, src_part=cp)
+    sq = dr.Shard.from_design(d, "pinned", W, r, dst_part=cp, src_part=npart)
+    lays.append((sn, sp, sq, dr.ShardLayer(sn, sp, sq)))
+mc, mn = lays[0][0].max_src, lays[0][2].max_src
+pc, pn = [], []
+for r in range(W):
+    xl = torch.zeros((mc, D), device="cuda")
+    xl[:int(cp[r + 1] - cp[r])] = xc[int(cp[r]):int(cp[r + 1])]
+    pc.append(dr.drelu_topk(xl, k))
+    xl = torch.zeros((mn, D), device="cuda")
+    xl[:int(npart[r + 1] - npart[r])] = xn[int(npart[r]):int(npart[r + 1])]
+    pn.append(dr.drelu_topk(xl, k))
+outs = [l[3].fwd(L1, pc, pn) for l in lays]
+ibc = [torch.zeros((2, W, mc, k), device="cuda") for _ in range(W)]
+ibn = [torch.zeros((W, mn, k), device="cuda") for _ in range(W)]
+for r, l in enumerate(lays):
+    l[3].bwd(L1, outs[r][2], torch.randn_like(outs[r][0]), torch.randn_like(outs[r][1]), pc, pn, ibc, ibn)
+for r, l in enumerate(lays):
+    l[3].dx(L1, outs[r][2], pc, pn, ibc[r], ibn[r])
+    l[0].spmm_fwd_peer(pc, D, k)
+torch.cuda.synchronize()
+print("sanitize shard case done", file=sys.stderr)
