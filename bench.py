@@ -75,6 +75,8 @@ class Clocks:
         self.lines = []
 
     def start(self):
+        if os.environ.get("BENCH_NO_CLOCKS"):
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -279,18 +281,46 @@ def gpu_local_cpus(dev):
         return None
 
 
-def timed_steps(torch, step, n, flush, events_stream=None):
+def timed_steps(torch, step, n, flush, events_stream=None, chunk=16):
     """n steps, L2 flushed (256 MB write) before each, outside CUDA events on the
-    caller's stream; returns the summed device time in ms."""
+    caller's stream; returns the summed device time in ms.
+    Enqueued in chunks of `chunk` steps, each behind a spin kernel (outside every
+    event pair) that holds the device while the host enqueues the whole chunk, and
+    drained before the next: a host stall (Python, a driver lock held by the
+    nvidia-smi clock sampler) or a full launch queue (~40 C5 steps of kernels) then
+    cannot leave the device idle between a step's events, which bracket device
+    execution only; the garbage collector is off meanwhile. Measured with the
+    events alone: single steps of 1.3-60 ms against a 0.51 ms median (C5), the
+    device having caught up with a stalled host."""
+    import gc
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(n)]
-    for i in range(n):
-        flush.zero_()
-        ev[i][0].record()
-        step(i)
-        ev[i][1].record()
-    torch.cuda.synchronize()
-    return sum(a.elapsed_time(b) for a, b in ev)
+    gc.collect()
+    gc.disable()                             # no collector pause while a chunk is enqueued
+    try:
+        for c0 in range(0, n, chunk):
+            torch.cuda.synchronize()
+            torch.cuda._sleep(int(1e8))      # ~0.05 s at ~2 GHz: the host enqueues the chunk meanwhile
+            for i in range(c0, min(n, c0 + chunk)):
+                flush.zero_()
+                ev[i][0].record()
+                step(i)
+                ev[i][1].record()
+        torch.cuda.synchronize()
+    finally:
+        gc.enable()
+    per = [a.elapsed_time(b) for a, b in ev]
+    timed_steps.last = per
+    if os.environ.get("BENCH_STEP_LIST"):
+        log("per-step ms:", " ".join(f"{x:.3f}" for x in per))
+    return sum(per)
+
+
+def step_stats(per):
+    s = sorted(per)
+    return {"min": round(s[0], 4), "median": round(s[len(s) // 2], 4), "max": round(s[-1], 4),
+            "argmax": int(max(range(len(per)), key=lambda i: per[i])),
+            "first_of_chunks": [round(per[i], 4) for i in range(0, len(per), 16)]}
 
 
 # ------------------------------------------------------------------ C5 schedule
@@ -454,28 +484,38 @@ def run_c5(args, torch, dist, dr, rank, world, local, dev, hbm, bf16, src):
         ref = g_sum / world
         dp["grad_vs_mean_of_rank_grads_max_rel"] = float(
             (g_dp.double() - ref).abs().max() / ref.abs().max().clamp_min(1e-30))
-    # ---- prime: every batch once eagerly, once captured into its CUDA graph
+    # ---- prime: every batch once eagerly, once captured into its CUDA graph, then
+    # two passes enqueued back to back (the driver deepens its launch queue once,
+    # blocking the host for ms: measured at step ~40 of the first deep run,
+    # tools/step_timing.py); then the W warm-up steps with the clock sampler running
     for s in range(S):
         for _ in range(2):
             tr.step(graphs[s], *inputs[s], sync=False)
-    for i in range(args.warmup):
+    torch.cuda.synchronize()
+    for i in range(2 * S):
         tr.step(graphs[i % S], *inputs[i % S], sync=False)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
 
     def step(i):
         tr.step(graphs[i % S], *inputs[i % S], sync=False)
 
     clocks = Clocks(local)
     clocks.start()
-    time.sleep(0.3)
+    t_w = time.time()
+    i = 0
+    while i < args.warmup or time.time() - t_w < 0.3:    # the sampler starts meanwhile
+        step(i)
+        i += 1
+        if i % 16 == 0:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     dr.launch_count_reset()
     wall0 = time.time()
     ms = timed_steps(torch, step, args.steps, flush)
+    step_ms = step_stats(timed_steps.last)
     wall = time.time() - wall0
     launches = dr.launch_count()
     ms_max = ddp.max_over_ranks(ms, dev)
@@ -630,6 +670,7 @@ def run_c5(args, torch, dist, dr, rank, world, local, dev, hbm, bf16, src):
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": round(ms_max / args.steps, 4),
+            "step_ms_rank0": step_ms,
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
@@ -648,8 +689,13 @@ def run_c5(args, torch, dist, dr, rank, world, local, dev, hbm, bf16, src):
                 "parallelism": f"dp{world}",
                 "id_order": "shuffled",
                 "l2": "flushed (256 MB write) before every timed step, outside the events",
-                "priming": f"every batch run once eagerly and once captured (CUDA graph) "
-                           f"before the {args.warmup} warm-up steps",
+                "priming": f"every batch run once eagerly and once captured (CUDA graph), "
+                           f"then two passes enqueued back to back, before the >= {args.warmup} "
+                           f"warm-up steps (0.3 s while the clock sampler starts)",
+                "enqueue": "timed steps enqueued in chunks of 16 behind a 0.05 s spin kernel "
+                           "(outside the events) so host stalls cannot idle the device inside "
+                           "a step's events; garbage collector off; per-step device times in "
+                           "step_ms_rank0",
                 "kernel_times": "per-launch CUDA events in an eager, single-stream pass of 5 "
                                 "steps on batch 0 after the timed region (the timed region "
                                 "replays each batch's CUDA graph on 3 streams)",
@@ -718,7 +764,10 @@ def run_single(args, torch, dr, wl, dev, hbm, bf16, src, l2=None, steps=None, wa
     torch.cuda.synchronize()
     clocks = Clocks(local)
     clocks.start()
-    time.sleep(0.3)
+    t_w = time.time()
+    while time.time() - t_w < 0.3:          # keep the GPU busy while the sampler starts
+        step(0)
+        torch.cuda.synchronize()
     dr.launch_count_reset()
     ms = timed_steps(torch, step, steps, flush)
     launches = dr.launch_count()

@@ -142,7 +142,7 @@ static void wait_on(cudaStream_t waiter, cudaStream_t producer, cudaEvent_t ev) 
 // Between dr_profile_begin and dr_profile_end every layer runs on the caller's
 // stream, so the per-launch events time isolated kernels (results are
 // bit-identical either way).
-static bool force_sequential() { return t_prof; }
+static bool force_sequential() { return t_prof || knobs().seq_streams; }
 
 static bool is_pow2(int k) { return k > 0 && (k & (k - 1)) == 0; }
 

@@ -54,6 +54,9 @@ struct Knobs {
     int64_t shard_tiles_t = 0;   // DR_SHARD_TILES_T: tiled backward for shard blocks
     int64_t order_block = -2;    // DR_ORDER_BLOCK: log2 rows per locality block of the SIMT orders (-1: degree-major, -2: by size)
     int64_t z_split = 1;         // DR_Z_SPLIT=0: Z stored fp32 (converted by each consumer)
+    int64_t tc2_ewg = 1;         // DR_TC2_EWG: epilogue warpgroups of the row GEMM (1 default; 0 auto = 2 for the head / dZ' with root; 2 forced where smem permits)
+    int64_t seq_streams = 0;     // DR_SEQ: every relation on the caller's stream (A/B of the 3-stream schedule)
+    int64_t tpr_stream = 1;      // DR_TPR_STREAM: thread-per-row network in rolled chunks: 1 epilogue + D = 128 standalone, 2 everywhere, 0 never
     int64_t drelu_coop = -2;     // DR_DRELU_COOP: lanes per row of the thread-per-row D-ReLU (-2 auto, 0 off)
     int64_t head_fuse = 1;       // DR_HEAD_FUSE=0: trainer head + MSE as its own kernels
     int64_t chain = 1;           // DR_CHAIN=0: trainer without the fused next-layer D-ReLU

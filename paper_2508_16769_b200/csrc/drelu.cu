@@ -321,12 +321,12 @@ __global__ void __launch_bounds__(256) drelu_extract_kernel(const float *__restr
 // K" steps (elementwise max against the reversed partner, bitonic merge). Each
 // merge discards K composites; the largest discarded one is the (K+1)-th overall,
 // so the selection is exact unless it shares the K-th's truncated key -- those
-// (rare) rows, and rows with such ties, rerun an exact full-key bisection from
+// (rare) rows, and rows with such ties, rerun an exact resolution of the tied elements (tpr_rerun) from
 // shared memory. The K kept columns are sorted ascending (CBSR order) or
 // left in value order (SORTED), and their values read back from shared memory.
 // Instructions per row ~ D log^2 K compare-exchanges instead of K warp-wide
 // reduction rounds (the standalone D-ReLU was issue-bound, profiles/r01).
-template <int D, int K, bool SORTED>
+template <int D, int K, bool SORTED, bool STREAM>
 __global__ void __launch_bounds__(128, D == 128 ? 3 : 6) drelu_tpr_kernel(const float *__restrict__ x, int64_t n,
                                                         int64_t ldx, float *__restrict__ val,
                                                         uint8_t *__restrict__ idx) {
@@ -359,29 +359,28 @@ __global__ void __launch_bounds__(128, D == 128 ? 3 : 6) drelu_tpr_kernel(const 
         }
         __syncwarp();
         const int64_t r = r0 + lane;
-        tpr_select_row<D, K, SORTED>(xs + lane * P, r < n, val + r * K, idx + r * K);
+        tpr_select_row<D, K, SORTED, STREAM>(xs + lane * P, r < n, val + r * K, idx + r * K);
         __syncwarp();
     }
 }
 
-template <int D, int K, bool SORTED>
+template <int D, int K, bool SORTED, bool STREAM>
 void launch_tpr(const float *x, int64_t n, int64_t ldx, float *val, uint8_t *idx, cudaStream_t s) {
     const size_t smem = (size_t)4 * 32 * (D + 4) * sizeof(float);
-    const void *fn = (const void *)drelu_tpr_kernel<D, K, SORTED>;
+    const void *fn = (const void *)drelu_tpr_kernel<D, K, SORTED, STREAM>;
     ensure_smem(fn, smem);
     // persistent: one wave of resident CTAs striding over 32-row groups (a partial
     // second wave would double the time of a one-group-per-warp launch)
-    static int per_sm[2] = {0, 0};
-    int &ps = per_sm[SORTED ? 1 : 0];
+    static int ps = 0;
     if (ps == 0) {
-        DR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, (const void *)drelu_tpr_kernel<D, K, SORTED>, 128, smem));
+        DR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, (const void *)drelu_tpr_kernel<D, K, SORTED, STREAM>, 128, smem));
         if (ps < 1) ps = 1;
     }
     const int64_t groups = (n + 31) / 32;
     const int64_t cap = (int64_t)148 * ps;
     int64_t blocks = (groups + 3) / 4;
     if (blocks > cap) blocks = cap;
-    drelu_tpr_kernel<D, K, SORTED><<<(unsigned)blocks, 128, smem, s>>>(x, n, ldx, val, idx);
+    drelu_tpr_kernel<D, K, SORTED, STREAM><<<(unsigned)blocks, 128, smem, s>>>(x, n, ldx, val, idx);
 }
 
 // Cooperative thread-per-row (ascending-column CBSR): T consecutive lanes share a
@@ -472,29 +471,9 @@ __global__ void __launch_bounds__(128) drelu_tcoop_kernel(const float *__restric
         const bool valid = r < n;
         const bool rerun = (lost & ~CM) == (w[K - 1] & ~CM);
         if (valid && rerun) {
-            // exact (rare): the K-th largest full key by bisection over the staged row
-            uint32_t Tk = 0;
-            for (int bb = 31; bb >= 0; --bb) {
-                const uint32_t cand = Tk | (1u << bb);
-                int cnt = 0;
-                for (int j = 0; j < D; ++j) cnt += order_key(xr[j]) >= cand;
-                if (cnt >= K) Tk = cand;
-            }
-            int gt = 0;
-            for (int j = 0; j < D; ++j) gt += order_key(xr[j]) > Tk;
-            int need = K - gt, q = 0;
+            // exact (rare): the tied elements at the threshold ranked by full key
             uint32_t sel[K];
-            for (int j = 0; j < D; ++j) {
-                const uint32_t kj = order_key(xr[j]);
-                const bool take = kj > Tk || (kj == Tk && need > 0);
-                if (take && kj == Tk) --need;
-                if (take) {
-#pragma unroll
-                    for (int t = 0; t < K; ++t)
-                        if (t == q) sel[t] = (uint32_t)j;
-                    ++q;
-                }
-            }
+            tpr_rerun<D, K, CB>(xr, w[K - 1] & ~CM, sel);
 #pragma unroll
             for (int t = 0; t < K; ++t) col[t] = sel[K - 1 - t];   // descending, like below
         } else {
@@ -542,11 +521,13 @@ template <bool SORTED>
 bool try_tpr(const float *x, int64_t n, int dim, int64_t ldx, int k, float *val, uint8_t *idx,
              cudaStream_t s) {
     if ((ldx % 4) != 0 || (reinterpret_cast<uintptr_t>(x) % 16) != 0) return false;
-    // cooperative rows: default (-2) two lanes per row at D = 128, k <= 16 (C4:
-    // 0.32 -> 0.29 ms at k = 16, 0.25 -> 0.22 ms at k = 8; no gain at D = 64 --
-    // profiles/r02/ab_drelu_coop.json); 0 = off, 1 / 2 / 4 = forced (A/B)
+    // cooperative rows: default (-2) two lanes per row at D = 64, k in {4, 8}
+    // (100k x 64, k = 8: 0.0205 vs 0.0246 ms thread-per-row, 0.0307 warp-per-row);
+    // at D = 128 the rolled thread-per-row network with the cheap rerun is faster
+    // (C4 1M x 128, k = 16: 0.248 vs 0.266 ms) -- profiles/r03/drelu_ab.json;
+    // 0 = off, 1 / 2 / 4 = forced (A/B)
     int T = (int)knobs().drelu_coop;
-    if (T == -2) T = (dim == 128 && k >= 4 && k <= 16) ? 2 : 0;
+    if (T == -2) T = (dim == 64 && (k == 4 || k == 8)) ? 2 : 0;
     if (!SORTED && T > 0) {
 #define DR_TCO(DD, KK, TT)                                                                  \
         if (dim == DD && k == KK && T == TT) {                                              \
@@ -563,17 +544,20 @@ bool try_tpr(const float *x, int64_t n, int dim, int64_t ldx, int k, float *val,
     }
 #define DR_TPR(DD, KK)                                                                      \
     if (dim == DD && k == KK) {                                                             \
-        launch_tpr<DD, KK, SORTED>(x, n, ldx, val, idx, s);                                 \
+        if (knobs().tpr_stream == 1 ? DD == 128 : knobs().tpr_stream == 2)                \
+            launch_tpr<DD, KK, SORTED, true>(x, n, ldx, val, idx, s);                       \
+        else launch_tpr<DD, KK, SORTED, false>(x, n, ldx, val, idx, s);                     \
         return true;                                                                        \
     }
-    // measured (profiles/r02/drelu_ab.json): faster than the warp-per-row kernels at
-    // D = 128 (C4: 0.47 -> 0.33 ms) and at D = 64 with k >= 16; slower at D = 64,
-    // k <= 8 (one long per-thread chain per 32 rows: latency-bound at C2 / C5 sizes)
-    DR_TPR(64, 16) DR_TPR(64, 32)
+    // measured (profiles/r02/drelu_ab.json, profiles/r03/drelu_ab.json): faster than
+    // the warp-per-row kernels at D = 128 (C4: 0.47 -> 0.25 ms) and at D = 64 with
+    // k >= 8 (100k x 64, k = 8: 0.031 -> 0.025 ms once the tied-threshold rerun
+    // became cheap, tpr_rerun)
+    DR_TPR(64, 8) DR_TPR(64, 16) DR_TPR(64, 32)
     DR_TPR(128, 4) DR_TPR(128, 8) DR_TPR(128, 16) DR_TPR(128, 32)
     if (knobs().drelu_tpr == 2) {                 // A/B: every supported shape
         DR_TPR(32, 2) DR_TPR(32, 4) DR_TPR(32, 8) DR_TPR(32, 16)
-        DR_TPR(64, 2) DR_TPR(64, 4) DR_TPR(64, 8)
+        DR_TPR(64, 2) DR_TPR(64, 4)
     }
 #undef DR_TPR
     return false;

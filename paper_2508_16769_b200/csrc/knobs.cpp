@@ -40,6 +40,9 @@ static Knobs read_env() {
     k.chain = env_i("DR_CHAIN", 1);
     k.head_fuse = env_i("DR_HEAD_FUSE", 1);
     k.drelu_coop = env_i("DR_DRELU_COOP", -2);
+    k.tpr_stream = env_i("DR_TPR_STREAM", 1);
+    k.seq_streams = env_i("DR_SEQ", 0);
+    k.tc2_ewg = env_i("DR_TC2_EWG", 1);
     k.z_split = env_i("DR_Z_SPLIT", 1);
     k.order_block = env_i("DR_ORDER_BLOCK", -2);
     k.skip_dead_net = env_i("DR_SKIP_DEAD_NET", 1);
@@ -81,6 +84,9 @@ extern "C" dr_status dr_debug_set(const char *name, int64_t value) {
         {"chain", &g_knobs.chain},
         {"head_fuse", &g_knobs.head_fuse},
         {"drelu_coop", &g_knobs.drelu_coop},
+        {"tpr_stream", &g_knobs.tpr_stream},
+        {"seq_streams", &g_knobs.seq_streams},
+        {"tc2_ewg", &g_knobs.tc2_ewg},
         {"z_split", &g_knobs.z_split},
         {"order_block", &g_knobs.order_block},
         {"skip_dead_net", &g_knobs.skip_dead_net},

@@ -40,7 +40,20 @@ constexpr int kChunk = 64;             // bf16 K per chunk (one 128-B swizzle at
 constexpr uint32_t kStage = 32768;     // 128 x 64 fp32 raw == bf16 hi + lo tiles
 constexpr uint32_t kHalf = 16384;      // one bf16 128 x 64 tile
 constexpr int kMaskStage = 4096;       // 128 rows x up to 8 mask words
-constexpr int kRowsThreads = 320;
+// row GEMM roles. W2 = false (10 warps, 168 registers each): producer, MMA issuer,
+// 4 converter warps, 4 epilogue warps. W2 = true (16 warps, 4 aligned warpgroups
+// with their own register budgets, setmaxnreg): WG0 converters (128), WG1 producer
+// + MMA issuer + 2 idle warps (40), WG2 / WG3 two epilogue warpgroups (168 each)
+// taking alternate tiles (the two TMEM accumulators), so a latency-bound epilogue
+// (one warp per SM sub-partition otherwise) runs two deep.
+template <bool W2> struct RowsRoles {
+    static constexpr int threads = W2 ? 512 : 320;
+    static constexpr int conv0 = W2 ? 0 : 2;       // first of the 4 converter warps
+    static constexpr int prod = W2 ? 4 : 0;
+    static constexpr int mma = W2 ? 5 : 1;
+    static constexpr int epi0 = W2 ? 8 : 6;        // first epilogue warp
+    static constexpr int nepi = W2 ? 8 : 4;
+};
 constexpr int kRedThreads = 320;     // producer, MMA, 2 x 4 converter warps
 constexpr int kEpiWarp0 = 32 * 36 * 4;                // epilogue staging per warp: [32][36] fp32
 constexpr int kEpiWarpN = 32 * 68 * 4;                // ... with the fused D-ReLU: [32][kRB] row buffer
@@ -131,6 +144,7 @@ struct R2Args {
     const uint32_t *mask_in;
     int mw;
     int SA, SB, b_resident;
+    int ewg;                       // epilogue warpgroups (1 or 2; smem permitting)
     uint32_t bchunk;               // bytes of one packed B chunk (hi + lo)
     uint32_t epi_off;              // byte offset of the epilogue staging boxes
     int epi;
@@ -153,6 +167,7 @@ struct R2Args {
     float *head_dy, *head_part;
     // fused next-layer D-ReLU (row a5): CBSR of y, exactly nk per row (tc2.h)
     int nk;                        // keep count (0: no fused D-ReLU)
+    int nk_stream;                 // rolled-chunk network (knob tpr_stream)
     float *nval;
     uint8_t *nidx;
     unsigned long long *dbg;       // DR_TC2_DEBUG role timers, else null
@@ -606,14 +621,21 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
         head_epilogue(a, lb, row0, lane, ok, pred, hw, hb, bias_s, stg, hacc, accb, accl);
     if constexpr (NK > 0) {
         const float *xr = stg + lane * kRB;
-        if (N == 64) tpr_select_row<64, NK, false>(xr, ok, a.nval + row * NK, a.nidx + row * NK);
-        else tpr_select_row<32, (NK < 32 ? NK : 32), false>(xr, ok, a.nval + row * NK, a.nidx + row * NK);
+        if (a.nk_stream) {
+            if (N == 64) tpr_select_row<64, NK, false, true>(xr, ok, a.nval + row * NK, a.nidx + row * NK);
+            else tpr_select_row<32, (NK < 32 ? NK : 32), false, true>(xr, ok, a.nval + row * NK, a.nidx + row * NK);
+        } else {
+            if (N == 64) tpr_select_row<64, NK, false, false>(xr, ok, a.nval + row * NK, a.nidx + row * NK);
+            else tpr_select_row<32, (NK < 32 ? NK : 32), false, false>(xr, ok, a.nval + row * NK, a.nidx + row * NK);
+        }
         __syncwarp();
     }
 }
 
-template <int NK>
-__global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_constant__ R2Args a) {
+template <int NK, bool W2>
+__global__ void __launch_bounds__(RowsRoles<W2>::threads, 1) tc2_rows_kernel(const __grid_constant__ R2Args a) {
+    using RR = RowsRoles<W2>;
+    constexpr int kRowsThreads = RR::threads;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~(uintptr_t)1023);
@@ -626,10 +648,11 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
     float (*hacc_s)[258] = nullptr;
     if constexpr (NK < 0) {
         __shared__ float head_sh[257];
-        __shared__ float hacc_sh[4][258];
+        __shared__ float hacc_sh[8][258];
         head_s = head_sh;
         hacc_s = hacc_sh;
     }
+    const long long kt00 = clock64();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int SA = a.SA, SB = a.SB, S = a.S;
     for (int e = tid; e < 512; e += kRowsThreads) {
@@ -639,12 +662,12 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
     if (NK < 0) {
         for (int e = tid; e < 257; e += kRowsThreads)
             head_s[e] = e < a.N ? a.head_w[e] : (e == 256 ? a.head_b[0] : 0.f);
-        for (int e = tid; e < 4 * 258; e += kRowsThreads) hacc_s[e / 258][e % 258] = 0.f;
+        for (int e = tid; e < 8 * 258; e += kRowsThreads) hacc_s[e / 258][e % 258] = 0.f;
     }
     uint8_t *stages = sm;
     uint8_t *bslots = sm + (size_t)SA * kStage;
     uint8_t *masks = bslots + (size_t)SB * a.bchunk;
-    uint8_t *epi_stage = sm + a.epi_off;        // 4 epilogue warps x 2 x 2 KB (1024-aligned)
+    uint8_t *epi_stage = sm + a.epi_off;        // 4 a.ewg epilogue warps' staging (1024-aligned)
     const uint32_t GN = (uint32_t)(a.G * a.N);
     uint32_t ncols = 32;
     while (ncols < 2 * GN) ncols <<= 1;
@@ -664,7 +687,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
         }
         tc::fence_mbar_init();
     }
-    if (warp == 1) {
+    if (warp == RR::mma) {
         tc::tmem_alloc(&tmem_slot, ncols);
         tc::tmem_relinquish();
     }
@@ -675,8 +698,16 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
     const long long kt0 = clock64();
     const int64_t n_tiles = (a.n + kTile - 1) / kTile;
     const int64_t my_tiles = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (a.dbg && tid == 0) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        a.dbg[blockIdx.x * 16 + 11] = g;                                  // start (ns)
+        a.dbg[blockIdx.x * 16 + 10] = (unsigned long long)(kt0 - kt00);   // setup
+    }
 
-    if (warp == 0) {
+    if (W2 ? (warp >= 4 && warp < 8) : warp < 2) {
+        if constexpr (W2) tc::setmaxnreg_dec<40>();   // 128 (converters) + 40 + 2 x 168: <= 64 K
+    if (warp == RR::prod) {
         // ---------------- producer
         if (a.b_resident) {
             if (lane == 0)
@@ -715,7 +746,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
                 __syncwarp();
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == RR::mma) {
         // ---------------- MMA issuer
         if (lane == 0) {
             const uint32_t idesc = tc::idesc_bf16(kTile, a.N);
@@ -771,9 +802,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
             }
         }
         __syncwarp();
-    } else if (warp < 6) {
+    }
+    } else if (warp >= RR::conv0 && warp < RR::conv0 + 4) {
         // ---------------- converters
-        const int ct = tid - 64;
+        const int ct = tid - 32 * RR::conv0;
         uint32_t it = 0;
         for (int64_t t = 0; t < my_tiles; ++t) {
             const int64_t r0 = ((int64_t)blockIdx.x + t * gridDim.x) * kTile;
@@ -794,31 +826,37 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
             }
         }
     } else {
-        // ---------------- epilogue
-        const int qd = warp & 3;
-        float *stg = reinterpret_cast<float *>(epi_stage + (size_t)(warp - 6) * epi_warp_bytes(NK > 0));
+        if constexpr (W2) tc::setmaxnreg_inc<168>();
+        // ---------------- epilogue: warpgroup eg takes tiles t = eg, eg + ewg, ...
+        // (accumulator t & 1; with ewg = 2 warpgroup eg always owns accumulator eg)
+        const int qd = warp & 3, ew = warp - RR::epi0, eg = ew >> 2, ewg = W2 ? a.ewg : 1;
+        float *stg = reinterpret_cast<float *>(epi_stage + (size_t)ew * epi_warp_bytes(NK > 0));
         EpiPre pcur, pnxt;
         float accb = 0.f, accl = 0.f;              // fused head: sum dp, sum r^2 of this lane
-        float *hacc = hacc_s[warp - 6];
-        if (NK == 0 && my_tiles > 0) epi_pre_load(a, (int64_t)blockIdx.x * kTile + qd * 32 + lane, pcur);
-        for (int64_t t = 0; t < my_tiles; ++t) {
-            const int64_t r0 = ((int64_t)blockIdx.x + t * gridDim.x) * kTile;
-            const uint32_t ab = (uint32_t)(t & 1);
-            if (NK == 0 && t + 1 < my_tiles) epi_pre_load(a, r0 + (int64_t)gridDim.x * kTile + qd * 32 + lane, pnxt);
-            {
+        float (*hacc)[258] = hacc_s + ew;
+        if (eg < ewg) {
+            if (NK == 0 && eg < my_tiles)
+                epi_pre_load(a, ((int64_t)blockIdx.x + (int64_t)eg * gridDim.x) * kTile + qd * 32 + lane, pcur);
+            for (int64_t t = eg; t < my_tiles; t += ewg) {
+                const int64_t r0 = ((int64_t)blockIdx.x + t * gridDim.x) * kTile;
+                const uint32_t ab = (uint32_t)(t & 1);
+                if (NK == 0 && t + ewg < my_tiles)
+                    epi_pre_load(a, r0 + (int64_t)ewg * gridDim.x * kTile + qd * 32 + lane, pnxt);
+                {
+                    RDBG_T0;
+                    tc::mbar_wait_sleep(&accf[ab], (uint32_t)((t >> 1) & 1));
+                    if (ew == 0 && lane == 0) RDBG_ADD(5);
+                }
+                tc::fence_after();
                 RDBG_T0;
-                tc::mbar_wait_sleep(&accf[ab], (uint32_t)((t >> 1) & 1));
-                if (warp == 6 && lane == 0) RDBG_ADD(5);
+                rows_epilogue<NK>(a, tmem + ab * GN, r0, qd, lane, bias_s, stg, pcur, head_s,
+                                  head_s[256], hacc[0], accb, accl);
+                pcur = pnxt;
+                if (ew == 0 && lane == 0) RDBG_ADD(6);
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&acce[ab]);
             }
-            tc::fence_after();
-            RDBG_T0;
-            rows_epilogue<NK>(a, tmem + ab * GN, r0, qd, lane, bias_s, stg, pcur, head_s,
-                              head_s[256], hacc, accb, accl);
-            pcur = pnxt;
-            if (warp == 6 && lane == 0) RDBG_ADD(6);
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&acce[ab]);
         }
         if (NK < 0) {   // this CTA's partial [sum_rows y dp (N) | sum dp | sum r^2], fixed order
 #pragma unroll
@@ -827,19 +865,27 @@ __global__ void __launch_bounds__(kRowsThreads, 1) tc2_rows_kernel(const __grid_
                 accl += __shfl_xor_sync(0xffffffffu, accl, o);
             }
             if (lane == 0) {
-                hacc[a.N] += accb;
-                hacc[a.N + 1] += accl;
+                hacc[0][a.N] += accb;
+                hacc[0][a.N + 1] += accl;
             }
-            tc::named_bar(2, 128);
-            const int et = tid - 192;
-            for (int e = et; e < a.N + 2; e += 128)
-                a.head_part[(int64_t)blockIdx.x * (a.N + 2) + e] =
-                    ((hacc_s[0][e] + hacc_s[1][e]) + hacc_s[2][e]) + hacc_s[3][e];
+            tc::named_bar(2, 32 * RR::nepi);
+            const int et = tid - 32 * RR::epi0;
+            for (int e = et; e < a.N + 2; e += 32 * RR::nepi) {
+                float v = hacc_s[0][e];
+#pragma unroll
+                for (int w8 = 1; w8 < RR::nepi; ++w8) v += hacc_s[w8][e];
+                a.head_part[(int64_t)blockIdx.x * (a.N + 2) + e] = v;
+            }
         }
     }
     tc::fence_before();
     __syncthreads();
-    if (a.dbg && tid == 0) atomicAdd(a.dbg + blockIdx.x * 16 + 8, (unsigned long long)(clock64() - kt0));
+    if (a.dbg && tid == 0) {
+        atomicAdd(a.dbg + blockIdx.x * 16 + 8, (unsigned long long)(clock64() - kt0));
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        a.dbg[blockIdx.x * 16 + 12] = g;                                  // end (ns)
+    }
     if (warp == 1) {
         tc::fence_after();
         tc::tmem_dealloc(tmem, ncols);
@@ -1673,7 +1719,7 @@ bool tc2_rows_supported(const Tc2RowsDesc &d) {
     if (d.epi == kEpi2Dz && d.n_dz % 16) return false;
     if (d.next_k && !tc2_next_drelu_supported(d.epi, d.N, d.next_k)) return false;
     const size_t bchunk = (size_t)256 * d.N;
-    const size_t budget = (size_t)(kSmemBase - 4 * epi_warp_bytes(d.next_k > 0) - (d.head_w ? 5 * 1024 : 0));
+    const size_t budget = (size_t)(kSmemBase - 4 * epi_warp_bytes(d.next_k > 0) - (d.head_w ? 10 * 1024 : 0));
     return 2 * kStage + 2 * kMaskStage + 2 * bchunk <= budget;
 }
 
@@ -1727,14 +1773,40 @@ int launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
                          d.head_dy && d.head_part),
              DR_ERR_INVALID_ARGUMENT, "tc2_rows: bad fused-head arguments");
     a.nk = d.next_k;
+    a.nk_stream = knobs().tpr_stream ? 1 : 0;
     a.nval = d.next_val;
     a.nidx = d.next_idx;
     DR_CHECK(!a.nk || (a.nval && a.nidx), DR_ERR_INVALID_ARGUMENT, "tc2_rows: null next CBSR");
-    // stages: B resident when every chunk fits beside >= 2 A stages, else a ring
+    // stages: two epilogue warpgroups when B stays resident beside >= 3 A stages or
+    // a ring of >= 2 B chunks fits beside 3; else one, with B resident beside >= 2
+    // A stages or a ring. The fused-head variant's own static arrays (~9 KB) come
+    // out of the same budget.
     const size_t st_bytes = kStage + kMaskStage;
-    // the fused-head variant's own static arrays (5 KB) come out of the same budget
-    const size_t budget = (size_t)(kSmemBase - 4 * epi_warp_bytes(a.nk > 0) - (a.head ? 5 * 1024 : 0));
-    if ((size_t)a.S * a.bchunk + 2 * st_bytes <= budget && a.S <= kMaxSB) {
+    auto budget_for = [&](int ewg) {
+        return (size_t)(kSmemBase - 4 * ewg * epi_warp_bytes(a.nk > 0) - (a.head ? 10 * 1024 : 0));
+    };
+    size_t budget = budget_for(2);
+    const bool res2 = (size_t)a.S * a.bchunk + 3 * st_bytes <= budget && a.S <= kMaxSB;
+    const bool ring2 = 3 * st_bytes + 2 * (size_t)a.bchunk <= budget;
+    // measured (C5, profiles/r03/ab_ewg.txt): two warpgroups shorten the fused head
+    // (L1 cell 57.7 -> 53.6 us) and dZ' with the root-term columns, cost 1-2 us where
+    // the 8 epilogue warps slow the converters on the same sub-partitions, and leave
+    // the C5 step unchanged (23.37 k vs 23.45 k graphs/s): off by default (knob
+    // tc2_ewg: 1 default, 0 auto = the head and dZ' with root, 2 forced)
+    const bool heavy_epi = a.head || (a.epi == kEpi2Dz && a.root && a.N > a.n_dz);
+    int want = knobs().tc2_ewg == 0 ? (heavy_epi ? 2 : 1) : (int)knobs().tc2_ewg;
+    if (a.nk) want = 1;            // the 16-warp layout is built for the head and dZ' only
+    a.ewg = (res2 || ring2) && want == 2 ? 2 : 1;
+    if (a.ewg == 1) budget = budget_for(1);
+    if (a.ewg == 2 && res2) {
+        a.b_resident = 1;
+        a.SB = a.S;
+        a.SA = (int)std::min<size_t>(kMaxSA, (budget - (size_t)a.S * a.bchunk) / st_bytes);
+    } else if (a.ewg == 2) {
+        a.b_resident = 0;
+        a.SA = 3;
+        a.SB = (int)std::min<size_t>(4, (budget - 3 * st_bytes) / a.bchunk);
+    } else if ((size_t)a.S * a.bchunk + 2 * st_bytes <= budget && a.S <= kMaxSB) {
         a.b_resident = 1;
         a.SB = a.S;
         a.SA = (int)std::min<size_t>(kMaxSA, (budget - (size_t)a.S * a.bchunk) / st_bytes);
@@ -1745,19 +1817,22 @@ int launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
         a.SB = (int)std::min<size_t>(4, (budget - a.SA * st_bytes) / a.bchunk);
     }
     a.epi_off = (uint32_t)((a.SA * st_bytes + (size_t)a.SB * a.bchunk + 1023) / 1024 * 1024);
-    const size_t smem = (size_t)a.epi_off + 4 * epi_warp_bytes(a.nk > 0) + 1024;
+    const size_t smem = (size_t)a.epi_off + 4 * a.ewg * epi_warp_bytes(a.nk > 0) + 1024;
     a.dz_split = d.dz_split ? 1 : 0;
     const int64_t tiles = (d.n + kTile - 1) / kTile;
     const int64_t grid = tiles < 148 ? tiles : 148;
     ProfScope ps(d.epi == kEpi2Dz ? "tc_dz" : "tc_proj", s);
-    const void *fn = a.head ? (const void *)tc2_rows_kernel<-1>   // fused head (NK < 0)
-                   : a.nk == 1 ? (const void *)tc2_rows_kernel<1>
-                   : a.nk == 2 ? (const void *)tc2_rows_kernel<2>
-                   : a.nk == 4 ? (const void *)tc2_rows_kernel<4>
-                   : a.nk == 8 ? (const void *)tc2_rows_kernel<8>
-                   : a.nk == 16 ? (const void *)tc2_rows_kernel<16>
-                   : a.nk == 32 ? (const void *)tc2_rows_kernel<32>
-                                : (const void *)tc2_rows_kernel<0>;
+    const bool w2 = a.ewg == 2;
+    const void *fn = a.head ? (w2 ? (const void *)tc2_rows_kernel<-1, true>     // fused head (NK < 0)
+                                  : (const void *)tc2_rows_kernel<-1, false>)
+                   : a.nk == 1 ? (const void *)tc2_rows_kernel<1, false>
+                   : a.nk == 2 ? (const void *)tc2_rows_kernel<2, false>
+                   : a.nk == 4 ? (const void *)tc2_rows_kernel<4, false>
+                   : a.nk == 8 ? (const void *)tc2_rows_kernel<8, false>
+                   : a.nk == 16 ? (const void *)tc2_rows_kernel<16, false>
+                   : a.nk == 32 ? (const void *)tc2_rows_kernel<32, false>
+                   : w2 ? (const void *)tc2_rows_kernel<0, true>
+                        : (const void *)tc2_rows_kernel<0, false>;
     ensure_smem(fn, smem);
     static unsigned long long *dbg_buf = nullptr;
     if (knobs().tc2_debug) {
@@ -1767,21 +1842,30 @@ int launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
     }
     {
         void *args[] = {(void *)&a};
-        DR_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(kRowsThreads), args, smem, s));
+        DR_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(w2 ? 512 : 320), args, smem, s));
     }
     note_launch("tc2_rows");
     if (a.dbg) {
         unsigned long long h[148 * 16];
         DR_CUDA(cudaStreamSynchronize(s));
         DR_CUDA(cudaMemcpy(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost));
-        double t[16] = {0};
-        for (int b = 0; b < grid; ++b)
-            for (int q = 0; q < 16; ++q) t[q] += (double)h[b * 16 + q] / grid;
+        double t[16] = {0}, tmax = 0, smax = 0;
+        unsigned long long g0 = ~0ull, g1 = 0, g0max = 0;
+        for (int b = 0; b < grid; ++b) {
+            for (int q = 0; q < 10; ++q) t[q] += (double)h[b * 16 + q] / grid;
+            tmax = std::max(tmax, (double)h[b * 16 + 8]);
+            smax = std::max(smax, (double)h[b * 16 + 10]);
+            g0 = std::min(g0, h[b * 16 + 11]);
+            g0max = std::max(g0max, h[b * 16 + 11]);
+            g1 = std::max(g1, h[b * 16 + 12]);
+        }
+        fprintf(stderr, "[tc2_rows] max CTA kcycles %.1f, max setup kcycles %.1f, CTA start spread %.1f us, "
+                "first start -> last end %.1f us\n", tmax / 1e3, smax / 1e3, (g0max - g0) / 1e3, (g1 - g0) / 1e3);
         fprintf(stderr,
-                "[tc2_rows n=%lld N=%d G=%d S=%d SA=%d SB=%d res=%d epi=%d] kcycles/CTA: total %.1f | "
+                "[tc2_rows n=%lld N=%d G=%d S=%d SA=%d SB=%d res=%d ewg=%d epi=%d] kcycles/CTA: total %.1f | "
                 "prod wait %.1f | mma wait conv %.1f acc %.1f | conv wait %.1f work %.1f | epi wait "
                 "%.1f work %.1f\n",
-                (long long)d.n, a.N, a.G, a.S, a.SA, a.SB, a.b_resident, a.epi, t[8] / 1e3,
+                (long long)d.n, a.N, a.G, a.S, a.SA, a.SB, a.b_resident, a.ewg, a.epi, t[8] / 1e3,
                 t[0] / 1e3, t[1] / 1e3, t[2] / 1e3, t[3] / 1e3, t[4] / 1e3, t[5] / 1e3, t[6] / 1e3);
     }
     return (int)grid;

@@ -228,3 +228,35 @@ def test_trainer_fused_head_matches_separate(designs, knob, name, D, k):
         a = np.atleast_2d(g0[key])
         b = np.atleast_2d(g1[key])
         assert row_err(b, a) <= 1e-5, key
+
+
+@pytest.mark.parametrize("name,D,k", [("C1", 16, 4), ("C2s", 64, 8)])
+def test_trainer_two_epilogue_warpgroups(designs, knob, name, D, k):
+    """The 16-warp row-GEMM layout (knob tc2_ewg = 2: two epilogue warpgroups on
+    alternate tiles, setmaxnreg budgets) against the default 10-warp one: every
+    row's epilogue arithmetic is the same, only the fused head's per-warp partial
+    sums are added over 8 warps instead of 4 -- loss and gradients within 1e-6 /
+    1e-5 row-normalised."""
+    from parity_util import row_err
+    d = designs[name]
+    g = dr.Graph.from_design(d)
+    P = make_params(D, D, D, 2, seed=29)
+    rng = np.random.default_rng(8)
+    xc = cuda(rng.standard_normal((d.n_cell, D)).astype(np.float32))
+    xn = cuda(rng.standard_normal((d.n_net, D)).astype(np.float32))
+    lab = cuda(d.labels)
+    out = {}
+    for ewg in (1, 2, 0):
+        knob("tc2_ewg", ewg, 1)
+        flat = cuda(dr.flatten_params(P, 2))
+        tr = dr.Trainer(flat, 2, D, D, D, k, k)
+        grad = torch.empty_like(flat)
+        loss = tr.step(g, xc, xn, lab, grad_out=grad)
+        out[ewg] = (loss, to_np(grad).astype(np.float64))
+        tr.close()
+    for ewg in (2, 0):
+        assert abs(out[ewg][0] - out[1][0]) <= 1e-6 * abs(out[1][0])
+        g0 = dr.unflatten(out[1][1], 2, D, D, D)
+        g1 = dr.unflatten(out[ewg][1], 2, D, D, D)
+        for key in g0:
+            assert row_err(np.atleast_2d(g1[key]), np.atleast_2d(g0[key])) <= 1e-5, key

@@ -1,7 +1,10 @@
 """Every D-ReLU kernel variant (Eq. 2-3) is bit-exact against the
 oracle on tie-heavy rows: the cooperative thread-per-row network at 1, 2 and 4
-lanes per row (knob drelu_coop), the whole-row network and the warp-per-row
-kernels (knob drelu_tpr), at the D / k the workloads use."""
+lanes per row (knob drelu_coop), the whole-row network unrolled or in rolled
+chunks (knob tpr_stream), the warp-per-row kernels (knob drelu_tpr), and the
+defaults, at the D / k the workloads use. Rows 402-409 hold 1-ulp neighbours,
+whose truncated composite keys tie at the threshold: the exact rerun
+(tpr_rerun) decides them."""
 import numpy as np
 import pytest
 
@@ -16,10 +19,12 @@ dr = pytest.importorskip("paper_2508_16769_b200")
 
 
 @pytest.mark.parametrize("dim,k", [(128, 16), (128, 8), (128, 4), (64, 8), (64, 16), (64, 4)])
-@pytest.mark.parametrize("coop,tpr", [(1, 1), (2, 1), (4, 1), (0, 1), (0, 0)])
-def test_drelu_variants_bitexact(knob, dim, k, coop, tpr):
+@pytest.mark.parametrize("coop,tpr,stream", [(1, 1, 0), (2, 1, 0), (4, 1, 0), (0, 1, 0), (0, 2, 0),
+                                             (0, 2, 2), (0, 0, 0), (-2, 1, 1)])
+def test_drelu_variants_bitexact(knob, dim, k, coop, tpr, stream):
     knob("drelu_coop", coop, -2)
     knob("drelu_tpr", tpr, 1)
+    knob("tpr_stream", stream, 1)
     rng = np.random.default_rng(dim + 7 * k + coop)
     x = rng.standard_normal((5003, dim)).astype(np.float32)        # ragged tail of a 32-row group
     x[:400] = rng.integers(-2, 3, size=(400, dim)).astype(np.float32)
