@@ -565,7 +565,7 @@ void launch_spmm_fwd(const RelDev &r, const float *hval, const uint8_t *hidx, in
     a.z_split = z_split ? 1 : 0;
     a.ng = ng;
     if (peer) a.peer = *peer;
-    int wpc = 8;
+    int wpc = (int)knobs().spmm_wpc;
     while (wpc > 1 && (size_t)wpc * R * dim * 4 > 96 * 1024) wpc >>= 1;
     const size_t smem = (size_t)wpc * R * dim * 4;
     a.hub_ctas = a.n_hub > 0 ? (a.n_hub < kHubCtas ? a.n_hub : kHubCtas) : 0;
@@ -643,7 +643,7 @@ void launch_spmm_bwd(const SrcSched &sched, int n_src, BwdTerm t0, BwdTerm t1, c
     a.accumulate = accumulate ? 1 : 0;
     a.ng = ng;
     if (peer) a.peer = *peer;
-    int wpc = 8;
+    int wpc = (int)knobs().spmm_wpc;
     while (wpc > 1 && (size_t)wpc * R * dim * 4 > 96 * 1024) wpc >>= 1;
     size_t smem = (size_t)wpc * R * dim * 4;
     const size_t hub_need = ((size_t)wpc * R + 1) * k * 4;    // partials + final row

@@ -442,10 +442,9 @@ __device__ __forceinline__ void epi_y32(const R2Args &a, uint32_t lb, int j, con
 __device__ __forceinline__ void head_epilogue(const R2Args &a, uint32_t lb, int64_t row0, int lane,
                                            bool ok, float pred, const float *hw, float hb,
                                            const float *bias_s, float *stg, float *hacc,
-                                           float &accb, float &accl) {
+                                           float &accb, float &accl, float label) {
     const int N = a.N;
-    const int64_t row = row0 + lane;
-    const float r = ok ? pred + hb - __ldg(a.labels + row) : 0.f;
+    const float r = ok ? pred + hb - label : 0.f;
     const float dp = 2.0f * r * a.head_inv_n;
     accb += dp;
     accl += r * r;
@@ -541,6 +540,8 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
         return;
     }
     const int mw = (N + 31) >> 5;
+    // fused head: the row's label is loaded first, its latency under the TMEM reads
+    const float label = (NK < 0 && ok) ? __ldg(a.labels + row) : 0.f;
     // NK > 0 (fused next-layer D-ReLU): `stg` is the warp's [32][kRB] row buffer
     // and every block stays staged at its columns until the selection below
     const int sstride = NK > 0 ? kRB : kEStg;
@@ -618,7 +619,7 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
         }
     }
     if constexpr (NK < 0)
-        head_epilogue(a, lb, row0, lane, ok, pred, hw, hb, bias_s, stg, hacc, accb, accl);
+        head_epilogue(a, lb, row0, lane, ok, pred, hw, hb, bias_s, stg, hacc, accb, accl, label);
     if constexpr (NK > 0) {
         const float *xr = stg + lane * kRB;
         if (a.nk_stream) {

@@ -750,7 +750,7 @@ void launch(const TileSet &ts, TsArgs &a, int D, bool bwd, cudaStream_t s) {
     a.stage_bytes = kATile + 256u * (uint32_t)D;
     a.side_bytes = (uint32_t)(kSideA + (bwd ? 0 : 64 * a.k * 5) + 127) & ~127u;
     const size_t budget = 227 * 1024 - 1024 - kStgBytes - (size_t)kSideSlots * a.side_bytes - 512;
-    a.SA = (int)std::min<size_t>(kMaxSA, budget / a.stage_bytes);
+    a.SA = (int)std::min<size_t>(knobs().ts_sa > 0 ? knobs().ts_sa : kMaxSA, budget / a.stage_bytes);
     // >= 3: the split backward gathers chunk it + 2 into its stage slot while chunk
     // it's slot is still being read (SA = 2 would wait on itself)
     DR_CHECK(a.SA >= 3, DR_ERR_UNSUPPORTED, "tspmm: shared memory budget");
