@@ -155,6 +155,9 @@ def kernel_work(tag, d, D, k, tiled=True, chained=False):
         if rel == "cell":       # Z_near, Z_pinned read, CBSR root input, Y + mask written
             return n * (2 * D * 4 + 5 * k + out + D // 8), 2.0 * n * D * (3 * D)
         return n * (D * 4 + 5 * k + out), 2.0 * n * D * (2 * D)
+    if kind == "tc_dw" and rel == "near_pinned":   # dual B: Z_near, CBSR root, Z_pinned, dY, mask
+        n = d.n_cell
+        return n * (4 * D + 5 * k + 4 * D + 4 * D + D // 8), 2.0 * n * (2 * D) * D + 2.0 * n * D * D
     if kind == "tc_dw":     # Z rows (+ CBSR root input) and dY rows (+ mask words) read
         n = ndst.get(rel, d.n_cell)
         root = rel in ("near", "pins")

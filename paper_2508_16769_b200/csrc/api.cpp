@@ -676,7 +676,29 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
         launch_tc2_reduce(d, wk, s, pq);
         return true;
     };
-    {
+    // near + pinned weight gradients in ONE reduce launch when the layer is a max
+    // merge of the square D = 64 shapes: both read dY_cell, with complementary masks
+    // (Eq. 12-13), so one pass over dY and the mask feeds both B operands (dual B)
+    bool dw_dual = false;
+    if (knobs().dw_dual && !sh && mode_near == kMaskM && mode_pinned == kMaskNotM && L->wr[DR_NEAR] &&
+        D == 64 && L->d_cell == 64 && L->d_net == 64 && L->k_cell <= 32 && z_split_ok(L, DR_NEAR) &&
+        z_split_ok(L, DR_PINNED)) {
+        Tc2ReduceDesc d;
+        d.n = nc; d.N = D; d.dy = dyc; d.mask = mask; d.mask_mode = mode_near; d.db = G->b[DR_NEAR];
+        d.mask_mode1 = mode_pinned; d.db1 = G->b[DR_PINNED];
+        d.G = 2; d.nseg[0] = 2; d.nseg[1] = 1;
+        Tc2RedSeg sz, sh2, sp;
+        sz.Z = z[DR_NEAR]; sz.w = L->d_cell; sz.grad = G->wn[DR_NEAR]; sz.split = true;
+        sh2.hval = hcv; sh2.hidx = hci; sh2.k = L->k_cell; sh2.w = L->d_cell; sh2.grad = G->wr[DR_NEAR];
+        sp.Z = z[DR_PINNED]; sp.w = L->d_net; sp.grad = G->wn[DR_PINNED]; sp.split = true;
+        d.seg[0][0] = sz; d.seg[0][1] = sh2; d.seg[1][0] = sp;
+        if (tc2_reduce_supported(d)) {
+            TagScope t("near_pinned");
+            launch_tc2_reduce(d, work[0], s0, pq);
+            dw_dual = true;
+        }
+    }
+    if (!dw_dual) {
         TagScope t("near");
         if (!dwt(nc, z[DR_NEAR], L->d_cell, G->wn[DR_NEAR], hcv, hci, L->k_cell, L->d_cell,
                  L->wr[DR_NEAR] ? G->wr[DR_NEAR] : nullptr, dyc, mode_near, G->b[DR_NEAR],
@@ -689,7 +711,7 @@ static void heteroconv_bwd(const dr_graph *g, const dr_layer *L, void *tape, con
                    nullptr, work[0], s0);
         }
     }
-    {
+    if (!dw_dual) {
         TagScope t("pinned");
         if (!dwt(nc, z[DR_PINNED], L->d_net, G->wn[DR_PINNED], nullptr, nullptr, 0, 0, nullptr,
                  dyc, mode_pinned, G->b[DR_PINNED], work[2], s2, !sh && z_split_ok(L, DR_PINNED)))

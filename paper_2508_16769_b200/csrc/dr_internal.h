@@ -58,6 +58,7 @@ struct Knobs {
     int64_t seq_streams = 0;     // DR_SEQ: every relation on the caller's stream (A/B of the 3-stream schedule)
     int64_t spmm_wpc = 8;        // DR_SPMM_WPC: warps per CTA of the SIMT SpMM / SSpMM (8, 4, 2)
     int64_t ts_sa = 0;           // DR_TS_SA: cap on the tiled SpMM's A stages (0: as many as fit, <= 4)
+    int64_t dw_dual = 1;         // DR_DW_DUAL: near + pinned weight gradients in one reduce launch (dual B)
     int64_t tpr_stream = 1;      // DR_TPR_STREAM: thread-per-row network in rolled chunks: 1 epilogue + D = 128 standalone, 2 everywhere, 0 never
     int64_t drelu_coop = -2;     // DR_DRELU_COOP: lanes per row of the thread-per-row D-ReLU (-2 auto, 0 off)
     int64_t head_fuse = 1;       // DR_HEAD_FUSE=0: trainer head + MSE as its own kernels

@@ -41,6 +41,7 @@ static Knobs read_env() {
     k.head_fuse = env_i("DR_HEAD_FUSE", 1);
     k.drelu_coop = env_i("DR_DRELU_COOP", -2);
     k.tpr_stream = env_i("DR_TPR_STREAM", 1);
+    k.dw_dual = env_i("DR_DW_DUAL", 1);
     k.spmm_wpc = env_i("DR_SPMM_WPC", 8);
     k.ts_sa = env_i("DR_TS_SA", 0);
     k.seq_streams = env_i("DR_SEQ", 0);
@@ -87,6 +88,7 @@ extern "C" dr_status dr_debug_set(const char *name, int64_t value) {
         {"head_fuse", &g_knobs.head_fuse},
         {"drelu_coop", &g_knobs.drelu_coop},
         {"tpr_stream", &g_knobs.tpr_stream},
+        {"dw_dual", &g_knobs.dw_dual},
         {"spmm_wpc", &g_knobs.spmm_wpc},
         {"ts_sa", &g_knobs.ts_sa},
         {"seq_streams", &g_knobs.seq_streams},

@@ -914,8 +914,10 @@ struct RdArgs {
     const float *dy;
     const uint32_t *mask;
     int mw, mask_mode;
+    int mask_mode1, ndb;                                // dual B (variant 5): group 1's mask, # db vectors
     int SA;
     uint32_t stage_bytes, off_b, off_cbsr, off_mask;   // within a stage
+    uint32_t off_b1;                                    // dual B: group 1's B operand
     uint32_t cbsr_seg_bytes;                            // per CBSR segment: vals (64k*4) + idx (64k)
     int64_t rows_per_cta;
     float *part;                                        // [grid][G*128*N + N]
@@ -1324,6 +1326,38 @@ __device__ __forceinline__ void mn_read(const float *raw, int valid, int ct, con
         }
     }
 }
+// dual B: one read of the raw dY block, both masked versions (mask modes m0 / m1)
+template <int W>
+__device__ __forceinline__ void mn_read2(const float *raw, int valid, int ct, const uint8_t *mkraw,
+                                         int mw, int m0, int m1, float4 (&v0)[MnMap<W>::NJ],
+                                         float4 (&v1)[MnMap<W>::NJ], float *cs0, float *cs1) {
+    using M = MnMap<W>;
+    const int q = ct % M::W4, rg = ct / M::W4, col = 4 * q;
+    const float4 *raw4 = reinterpret_cast<const float4 *>(raw);
+#pragma unroll
+    for (int j = 0; j < M::NJ; ++j) {
+        const int r = rg + M::RG * j;
+        float4 x = raw4[r * M::W4 + q];
+        if (r >= valid) x = make_float4(0.f, 0.f, 0.f, 0.f);
+        const uint32_t w = *reinterpret_cast<const uint32_t *>(mkraw + (r * mw + (col >> 5)) * 4);
+        const uint32_t bm = (w >> (col & 31)) & 0xfu;
+        const uint32_t b0 = m0 == kMask2NotM ? (~bm & 0xfu) : m0 == kMask2M ? bm : 0xfu;
+        const uint32_t b1 = m1 == kMask2NotM ? (~bm & 0xfu) : m1 == kMask2M ? bm : 0xfu;
+        float4 y0 = x, y1 = x;
+        if (!(b0 & 1u)) y0.x = 0.f;
+        if (!(b0 & 2u)) y0.y = 0.f;
+        if (!(b0 & 4u)) y0.z = 0.f;
+        if (!(b0 & 8u)) y0.w = 0.f;
+        if (!(b1 & 1u)) y1.x = 0.f;
+        if (!(b1 & 2u)) y1.y = 0.f;
+        if (!(b1 & 4u)) y1.z = 0.f;
+        if (!(b1 & 8u)) y1.w = 0.f;
+        v0[j] = y0;
+        v1[j] = y1;
+        cs0[0] += y0.x; cs0[1] += y0.y; cs0[2] += y0.z; cs0[3] += y0.w;
+        cs1[0] += y1.x; cs1[1] += y1.y; cs1[2] += y1.z; cs1[3] += y1.w;
+    }
+}
 // hi atoms at tile + 8 KB a, lo atoms at tile + lo_off + 8 KB a
 template <int W>
 __device__ __forceinline__ void mn_write(uint8_t *tile, uint32_t lo_off, int ct,
@@ -1342,12 +1376,15 @@ __device__ __forceinline__ void mn_write(uint8_t *tile, uint32_t lo_off, int ct,
         *reinterpret_cast<uint2 *>(tile + lo_off + off) = l;
     }
 }
+// G = 3: dual B (variant 5): group 0 = [Z | H] as for G = 1, group 1 = a second
+// split Z (TMA-landed atoms, its unused feature atom zeroed once per slot), and
+// two B operands, B0 = mask_mode(dY) at off_b and B1 = mask_mode1(dY) at off_b1
 template <int G, int WD, int WC, int N>
 __device__ __forceinline__ void red_convert_mn(const RdArgs &a, uint8_t *st, int valid, int ct,
-                                               float *colsum, int bar) {
+                                               float (&colsum)[2][4], int bar) {
     const uint8_t *mk = st + a.off_mask;
     uint8_t *tz = st;                                   // group 0: Z atoms from 0
-    uint8_t *th = G == 2 ? st + kStage : st + WD * 128; // H atoms (G = 1: right after Z's)
+    uint8_t *th = G == 2 ? st + kStage : st + WD * 128; // H atoms (G = 1, 3: right after Z's)
     float4 vz[MnMap<WD>::NJ];
     const bool zsplit = a.seg[0][0].split != 0;         // Z landed as operand atoms (TMA)
     if (!zsplit) mn_read<WD>(reinterpret_cast<const float *>(tz), valid, ct, mk, 0, kMask2None, vz, nullptr);
@@ -1403,10 +1440,18 @@ __device__ __forceinline__ void red_convert_mn(const RdArgs &a, uint8_t *st, int
                 }
         }
     }
-    {   // B = mask(dY), [rows][N], hi atoms then lo atoms (N * 128 bytes each)
+    if constexpr (G == 3) {   // B0 = mask_mode(dY) in place, B1 = mask_mode1(dY) at off_b1
+        uint8_t *tile = st + a.off_b;
+        float4 v0[MnMap<N>::NJ], v1[MnMap<N>::NJ];
+        mn_read2<N>(reinterpret_cast<const float *>(tile), valid, ct, mk, a.mw, a.mask_mode, a.mask_mode1,
+                    v0, v1, colsum[0], colsum[1]);
+        tc::named_bar(bar, 128);
+        mn_write<N>(tile, (uint32_t)N * 128u, ct, v0);
+        mn_write<N>(st + a.off_b1, (uint32_t)N * 128u, ct, v1);
+    } else {   // B = mask(dY), [rows][N], hi atoms then lo atoms (N * 128 bytes each)
         uint8_t *tile = st + a.off_b;
         float4 v[MnMap<N>::NJ];
-        mn_read<N>(reinterpret_cast<const float *>(tile), valid, ct, mk, a.mw, a.mask_mode, v, colsum);
+        mn_read<N>(reinterpret_cast<const float *>(tile), valid, ct, mk, a.mw, a.mask_mode, v, colsum[0]);
         tc::named_bar(bar, 128);
         mn_write<N>(tile, (uint32_t)N * 128u, ct, v);
     }
@@ -1438,6 +1483,17 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
         tc::tmem_alloc(&tmem_slot, ncols);
         tc::tmem_relinquish();
     }
+    if constexpr (G_ == 3) {
+        // dual B: group 1 holds one 64-wide Z; its second feature atom (hi and lo)
+        // is never written by TMA or the converters -- zero it once per stage slot
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int e = tid; e < SA * 1024; e += kRedThreads) {
+            uint8_t *t1 = sm + (size_t)(e >> 10) * a.stage_bytes + kStage + 8192;
+            const int u = e & 1023;                       // 512 x 16 B hi, 512 x 16 B lo
+            *reinterpret_cast<float4 *>(t1 + (u < 512 ? 0 : kHalf) + 16 * (u & 511)) = z;
+        }
+        tc::fence_async_smem();
+    }
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
@@ -1445,7 +1501,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
     const int64_t rbeg = (int64_t)blockIdx.x * a.rows_per_cta;
     const int64_t rend = a.n < rbeg + a.rows_per_cta ? a.n : rbeg + a.rows_per_cta;
     const int64_t total = rend > rbeg ? (rend - rbeg + kRRows - 1) / kRRows : 0;
-    float *out = a.part + (int64_t)blockIdx.x * ((int64_t)G * kTile * N + N);
+    float *out = a.part + (int64_t)blockIdx.x * ((int64_t)G * kTile * N + (int64_t)a.ndb * N);
 
     if (warp == 0) {
         for (int64_t it = 0; it < total; ++it) {
@@ -1472,9 +1528,10 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
                 }
                 tc::fence_after();
                 uint8_t *st = sm + (size_t)slot * a.stage_bytes;
-                const uint32_t sb = tc::smem_u32(st + a.off_b), blo = (uint32_t)N * 128u;
+                const uint32_t sb0 = tc::smem_u32(st + a.off_b), blo = (uint32_t)N * 128u;
                 for (int g = 0; g < G; ++g) {
                     const uint32_t sa = tc::smem_u32(st + (size_t)g * kStage);
+                    const uint32_t sb = (G_ == 3 && g == 1) ? tc::smem_u32(st + a.off_b1) : sb0;
                     const uint32_t d = tmem + (uint32_t)(g * N);
 #pragma unroll
                     for (int ks = 0; ks < kRRows / 16; ++ks) {
@@ -1520,7 +1577,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
             {
                 RDBG_T0;
                 if constexpr (G_ > 0)
-                    red_convert_mn<G_, WD_, WC_, N_>(a, sm + (size_t)slot * a.stage_bytes, valid, ct, colsum[0], bar);
+                    red_convert_mn<G_, WD_, WC_, N_>(a, sm + (size_t)slot * a.stage_bytes, valid, ct, colsum, bar);
                 else
                     red_convert(a, sm + (size_t)slot * a.stage_bytes, valid, ct, colsum, bar);
                 if (ct == 0) RDBG_ADD(3);
@@ -1530,28 +1587,31 @@ __global__ void __launch_bounds__(kRedThreads, 1) tc2_reduce_kernel(const __grid
             if (lane == 0) tc::mbar_arrive(&conv[slot]);
         }
         // db partials: per thread unit, then summed over the units of a column in a
-        // fixed order
-        for (int e = ct; e < 8 * 128; e += 128) dbs[grp][e >> 7][e & 127] = 0.f;
-        tc::named_bar(3, 256);
-        if constexpr (G_ > 0) {
-            const int q = ct % MnMap<N_>::W4, rg = ct / MnMap<N_>::W4;
-            for (int e = 0; e < 4; ++e) dbs[grp][rg][4 * q + e] = colsum[0][e];
-        } else {
+        // fixed order (dual B: the same for group 1's B, a second round)
+        for (int d2 = 0; d2 < (G_ == 3 ? 2 : 1); ++d2) {
+            for (int e = ct; e < 8 * 128; e += 128) dbs[grp][e >> 7][e & 127] = 0.f;
+            tc::named_bar(3, 256);
+            if constexpr (G_ > 0) {
+                const int q = ct % MnMap<N_>::W4, rg = ct / MnMap<N_>::W4;
+                for (int e = 0; e < 4; ++e) dbs[grp][rg][4 * q + e] = colsum[d2][e];
+            } else {
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const Unit x = red_unit(N, ct, i);
-                if (x.ok)
-                    for (int e = 0; e < 4; ++e) dbs[grp][x.j][4 * x.fq + e] = colsum[i][e];
+                for (int i = 0; i < 2; ++i) {
+                    const Unit x = red_unit(N, ct, i);
+                    if (x.ok)
+                        for (int e = 0; e < 4; ++e) dbs[grp][x.j][4 * x.fq + e] = colsum[i][e];
+                }
             }
+            tc::named_bar(3, 256);
+            if (grp == 0)
+                for (int c = ct; c < N; c += 128) {
+                    float s = 0.f;
+                    for (int q = 0; q < 2; ++q)
+                        for (int j = 0; j < 8; ++j) s += dbs[q][j][c];
+                    out[(int64_t)G * kTile * N + (int64_t)d2 * N + c] = s;
+                }
+            tc::named_bar(3, 256);                        // dbs reused by the next round
         }
-        tc::named_bar(3, 256);
-        if (grp == 0)
-            for (int c = ct; c < N; c += 128) {
-                float s = 0.f;
-                for (int q = 0; q < 2; ++q)
-                    for (int j = 0; j < 8; ++j) s += dbs[q][j][c];
-                out[(int64_t)G * kTile * N + c] = s;
-            }
         // accumulator -> per-CTA partial (lane = feature row), group 0
         const int qd = warp & 3;
         if (total > 0 && grp == 0) {
@@ -1591,7 +1651,7 @@ __global__ void tc2_reduce_parts_kernel(const __grid_constant__ PartsJobs jobs) 
     const int G = o.G, N = o.N, nparts = o.nparts;
     const float *__restrict__ part = o.part;
     __shared__ float red[8][33];
-    const int64_t len = (int64_t)G * kTile * N + N;
+    const int64_t len = (int64_t)G * kTile * N + (int64_t)o.ndb * N;
     const int64_t e = (int64_t)blockIdx.x * 32 + threadIdx.x;
     if ((int64_t)blockIdx.x * 32 >= len) return;          // this job is shorter (block-uniform)
     float acc = 0.f;
@@ -1605,7 +1665,9 @@ __global__ void tc2_reduce_parts_kernel(const __grid_constant__ PartsJobs jobs) 
 #pragma unroll
     for (int q = 0; q < 8; ++q) s += red[q][threadIdx.x];
     if (e >= (int64_t)G * kTile * N) {
-        if (o.db) o.db[e - (int64_t)G * kTile * N] = s;
+        const int64_t c = e - (int64_t)G * kTile * N;
+        float *db = c < N ? o.db : o.db1;
+        if (db) db[c < N ? c : c - N] = s;
         return;
     }
     const int g = (int)(e / ((int64_t)kTile * N));
@@ -1878,6 +1940,8 @@ static void red_layout(const Tc2ReduceDesc &d, int ncb, int maxk, RdArgs &a) {
     uint32_t off = (uint32_t)d.G * kStage;
     a.off_b = off;
     off += r1k((uint32_t)256 * d.N);
+    a.off_b1 = off;
+    if (d.mask_mode1 >= 0) off += r1k((uint32_t)256 * d.N);   // dual B: group 1's operand
     a.off_cbsr = off;
     a.cbsr_seg_bytes = (uint32_t)(kRRows * maxk * 4 + rup16((uint32_t)kRRows * maxk) + 16);
     a.cbsr_seg_bytes = (a.cbsr_seg_bytes + 127u) & ~127u;
@@ -1889,11 +1953,17 @@ static void red_layout(const Tc2ReduceDesc &d, int ncb, int maxk, RdArgs &a) {
 }
 
 // The specialised (MN-major) reduce shapes: 1 = [Z 64 | H 64] N 64, 2 = Z 128 / H 128
-// in two groups N 128, 3 = Z 64 N 64, 4 = Z 128 N 128; 0 = the generic kernel.
+// in two groups N 128, 3 = Z 64 N 64, 4 = Z 128 N 128, 5 = dual B: [Z 64 | H 64] with
+// B0 and split Z' 64 with B1, N 64; 0 = the generic kernel, -1 = unsupported dual.
 static int red_variant(const Tc2ReduceDesc &d) {
     auto is_seg = [&](int g, int q, bool dense, int w) {
         return d.seg[g][q].w == w && (d.seg[g][q].Z != nullptr) == dense && (dense || d.seg[g][q].k <= 32);
     };
+    if (d.mask_mode1 >= 0)
+        return (d.G == 2 && d.nseg[0] == 2 && d.nseg[1] == 1 && d.N == 64 && is_seg(0, 0, true, 64) &&
+                is_seg(0, 1, false, 64) && is_seg(1, 0, true, 64) && d.seg[0][0].split && d.seg[1][0].split &&
+                d.mask && d.mask_mode != kMask2None)
+                   ? 5 : -1;
     if (d.G == 1 && d.nseg[0] == 2 && d.N == 64 && is_seg(0, 0, true, 64) && is_seg(0, 1, false, 64)) return 1;
     if (d.G == 2 && d.nseg[0] == 1 && d.nseg[1] == 1 && d.N == 128 && is_seg(0, 0, true, 128) &&
         is_seg(1, 0, false, 128))
@@ -1905,6 +1975,7 @@ static int red_variant(const Tc2ReduceDesc &d) {
 
 bool tc2_reduce_supported(const Tc2ReduceDesc &d) {
     if (knobs().dense_simt) return false;
+    if (d.mask_mode1 >= 0 && red_variant(d) != 5) return false;
     if (d.N < 16 || d.N > 128 || d.N % 16) return false;
     if (d.G < 1 || d.G > 2) return false;
     for (int g = 0; g < d.G; ++g) {
@@ -1939,7 +2010,7 @@ bool tc2_reduce_supported(const Tc2ReduceDesc &d) {
 }
 
 size_t tc2_reduce_work_floats(int G, int N) {
-    return (size_t)148 * ((size_t)G * kTile * N + N);
+    return (size_t)148 * ((size_t)G * kTile * N + 2 * (size_t)N);    // up to two db vectors (dual B)
 }
 
 void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s, Tc2Deferred *defer) {
@@ -1970,9 +2041,13 @@ void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s, Tc2D
         }
     }
     o.db = d.db;
+    o.db1 = d.db1;
+    o.ndb = d.mask_mode1 >= 0 ? 2 : 1;
     a.dy = d.dy;
     a.mask = d.mask;
     a.mask_mode = d.mask_mode;
+    a.mask_mode1 = d.mask_mode1;
+    a.ndb = o.ndb;
     a.mw = (d.N + 31) / 32;
     red_layout(d, ncb, maxk, a);
     DR_CHECK(a.SA >= 2, DR_ERR_UNSUPPORTED, "tc2_reduce: shared memory budget");
@@ -1995,6 +2070,7 @@ void launch_tc2_reduce(const Tc2ReduceDesc &d, float *work, cudaStream_t s, Tc2D
                    : var == 2 ? (const void *)tc2_reduce_kernel<2, 128, 128, 128>
                    : var == 3 ? (const void *)tc2_reduce_kernel<1, 64, 0, 64>
                    : var == 4 ? (const void *)tc2_reduce_kernel<1, 128, 0, 128>
+                   : var == 5 ? (const void *)tc2_reduce_kernel<3, 64, 64, 64>
                               : (const void *)tc2_reduce_kernel<0, 0, 0, 0>;
     ensure_smem(fn, smem);
     {
@@ -2035,7 +2111,8 @@ void launch_tc2_reduce_parts(Tc2Deferred &defer, cudaStream_t s) {
     int64_t most = 1;
     for (int i = 0; i < defer.n; ++i) {
         j.job[i] = defer.job[i];
-        most = std::max<int64_t>(most, (int64_t)defer.job[i].G * kTile * defer.job[i].N + defer.job[i].N);
+        most = std::max<int64_t>(most, (int64_t)defer.job[i].G * kTile * defer.job[i].N +
+                                           (int64_t)defer.job[i].ndb * defer.job[i].N);
     }
     ProfScope ps("tc_dw_sum", s);
     tc2_reduce_parts_kernel<<<dim3((unsigned)((most + 31) / 32), (unsigned)defer.n), dim3(32, 8), 0, s>>>(j);

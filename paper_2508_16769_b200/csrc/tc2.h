@@ -110,6 +110,11 @@ struct Tc2ReduceDesc {
     const uint32_t *mask = nullptr;
     int mask_mode = kMask2None;
     float *db = nullptr;
+    // dual B (the near + pinned weight gradients of a max-merge layer in one launch,
+    // Eq. 12-13): mask_mode1 >= 0 gives group 1 its own B = mask_mode1(dY) and bias
+    // gradient db1 (both B operands converted from one read of dY and the mask)
+    int mask_mode1 = -1;
+    float *db1 = nullptr;
 };
 bool tc2_reduce_supported(const Tc2ReduceDesc &d);
 size_t tc2_reduce_work_floats(int G, int N);
@@ -124,6 +129,8 @@ struct Tc2PartsJob {
     int g[4] = {0, 0, 0, 0}, m0[4] = {0, 0, 0, 0}, w[4] = {0, 0, 0, 0};
     float *dst[4] = {nullptr, nullptr, nullptr, nullptr};
     float *db = nullptr;
+    float *db1 = nullptr;              // dual B: group 1's bias gradient
+    int ndb = 1;                       // bias-gradient vectors after the G x 128 x N block
 };
 struct Tc2Deferred {
     static constexpr int kMax = 8;
