@@ -260,3 +260,31 @@ def test_trainer_two_epilogue_warpgroups(designs, knob, name, D, k):
         g1 = dr.unflatten(out[ewg][1], 2, D, D, D)
         for key in g0:
             assert row_err(np.atleast_2d(g1[key]), np.atleast_2d(g0[key])) <= 1e-5, key
+
+
+@pytest.mark.parametrize("name,D,k", [("C2s", 64, 8), ("C2s", 64, 16)])
+def test_dw_dual_bit_identical(designs, knob, name, D, k):
+    """The near and pinned weight gradients in one dual-B reduce launch (one pass
+    over dY and the merge mask, Eq. 12-13's complementary masks as two B operands)
+    against the two separate launches: the same MN-major operands, stages and MMA
+    sequence per group, so every weight and bias gradient is bit-identical; the
+    layer's other outputs are untouched."""
+    d = designs[name]
+    g = dr.Graph.from_design(d)
+    P = make_params(D, D, D, 1, seed=41)
+    L, _ = _layer(P, 0, D, D, D, k, k)
+    rng = np.random.default_rng(12)
+    xc = cuda(rng.standard_normal((d.n_cell, D)).astype(np.float32))
+    xn = cuda(rng.standard_normal((d.n_net, D)).astype(np.float32))
+    dyc = cuda(rng.standard_normal((d.n_cell, D)).astype(np.float32))
+    dyn = cuda(rng.standard_normal((d.n_net, D)).astype(np.float32))
+    out = {}
+    for dual in (0, 1):
+        knob("dw_dual", dual, 1)
+        yc, yn, tape = dr.heteroconv_fwd(g, L, xc, xn)
+        grads, dxc, dxn = dr.heteroconv_bwd(g, L, tape, dyc, dyn, need_dx=True)
+        out[dual] = (grads, dxc, dxn)
+    a, b = out[0], out[1]
+    assert torch.equal(a[1], b[1]) and torch.equal(a[2], b[2])
+    for key in a[0]:
+        assert torch.equal(a[0][key], b[0][key]), key
