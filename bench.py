@@ -284,7 +284,7 @@ def gpu_local_cpus(dev):
         return None
 
 
-def timed_steps(torch, step, n, flush, events_stream=None, chunk=16):
+def timed_steps(torch, step, n, flush, events_stream=None, chunk=16, barrier=None):
     """n steps, L2 flushed (256 MB write) before each, outside CUDA events on the
     caller's stream; returns the summed device time in ms.
     Enqueued in chunks of `chunk` steps, each behind a spin kernel (outside every
@@ -303,6 +303,9 @@ def timed_steps(torch, step, n, flush, events_stream=None, chunk=16):
     try:
         for c0 in range(0, n, chunk):
             torch.cuda.synchronize()
+            if barrier is not None:          # ranks start each chunk together (the step's
+                barrier()                    # allreduce must not wait on a late rank's spin)
+                torch.cuda.synchronize()
             torch.cuda._sleep(int(1e8))      # ~0.05 s at ~2 GHz: the host enqueues the chunk meanwhile
             for i in range(c0, min(n, c0 + chunk)):
                 flush.zero_()
@@ -517,7 +520,7 @@ def run_c5(args, torch, dist, dr, rank, world, local, dev, hbm, bf16, src):
     torch.cuda.synchronize()
     dr.launch_count_reset()
     wall0 = time.time()
-    ms = timed_steps(torch, step, args.steps, flush)
+    ms = timed_steps(torch, step, args.steps, flush, barrier=(dist.barrier if world > 1 else None))
     step_ms = step_stats(timed_steps.last)
     wall = time.time() - wall0
     launches = dr.launch_count()
