@@ -397,7 +397,7 @@ __device__ __forceinline__ void epi_pre_load(const R2Args &a, int64_t row, EpiPr
 // selects its own row's exact top-NK with the thread-per-row network of the
 // standalone D-ReLU (drelu_net.cuh tpr_select_row: composite keys, bitonic
 // groups, exact rerun from shared memory on a truncated-key collision).
-// Measured (tools/scratch/epi_topk.cu, one warp per SM sub-partition as in this
+// Measured (a scratch microbenchmark, one warp per SM sub-partition as in this
 // epilogue): ~5.3k cycles per 32 rows at N=64, k=8, vs ~50k for a warp-
 // cooperative redux.max extraction (latency-bound at one warp per SMSP).
 constexpr int kRB = 68;                // row-buffer stride (floats): 64 columns + 4 pad
