@@ -493,7 +493,11 @@ def run_c5(args, torch, dist, dr, rank, world, local, dev, hbm, bf16, src):
     # ---- prime: every batch once eagerly, once captured into its CUDA graph, then
     # two passes enqueued back to back (the driver deepens its launch queue once,
     # blocking the host for ms: measured at step ~40 of the first deep run,
-    # tools/step_timing.py); then the W warm-up steps with the clock sampler running
+    # tools/step_timing.py); then the W warm-up steps. The clock sampler starts
+    # first (nvidia-smi needs ~0.3 s) and every rank runs the same number of steps
+    # (each step holds an allreduce at N > 1)
+    clocks = Clocks(local)
+    clocks.start()
     for s in range(S):
         for _ in range(2):
             tr.step(graphs[s], *inputs[s], sync=False)
@@ -505,15 +509,8 @@ def run_c5(args, torch, dist, dr, rank, world, local, dev, hbm, bf16, src):
     def step(i):
         tr.step(graphs[i % S], *inputs[i % S], sync=False)
 
-    clocks = Clocks(local)
-    clocks.start()
-    t_w = time.time()
-    i = 0
-    while i < args.warmup or time.time() - t_w < 0.3:    # the sampler starts meanwhile
+    for i in range(args.warmup):
         step(i)
-        i += 1
-        if i % 16 == 0:
-            torch.cuda.synchronize()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -696,8 +693,8 @@ def run_c5(args, torch, dist, dr, rank, world, local, dev, hbm, bf16, src):
                 "id_order": "shuffled",
                 "l2": "flushed (256 MB write) before every timed step, outside the events",
                 "priming": f"every batch run once eagerly and once captured (CUDA graph), "
-                           f"then two passes enqueued back to back, before the >= {args.warmup} "
-                           f"warm-up steps (0.3 s while the clock sampler starts)",
+                           f"then two passes enqueued back to back, before the {args.warmup} "
+                           f"warm-up steps (the clock sampler started before the priming)",
                 "enqueue": "timed steps enqueued in chunks of 16 behind a 0.05 s spin kernel "
                            "(outside the events) so host stalls cannot idle the device inside "
                            "a step's events; garbage collector off; per-step device times in "
