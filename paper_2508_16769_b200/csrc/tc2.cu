@@ -469,6 +469,37 @@ __device__ __forceinline__ void head_epilogue(const R2Args &a, uint32_t lb, int6
     }
 }
 
+// The same head pass on y staged in the warp's [32][kRB] row buffer (N <= 64):
+// column sums of y dp over the warp's rows with dp broadcast from its row's lane
+// (fused multiply-add, rows in ascending order), then dY = dp w_h staged over y
+// and stored coalesced.
+__device__ __forceinline__ void head_epilogue_staged(const R2Args &a, int64_t row0, int lane, bool ok,
+                                                     float pred, const float *hw, float hb, float *stg,
+                                                     float *hacc, float &accb, float &accl, float label) {
+    const int N = a.N;
+    const float r = ok ? pred + hb - label : 0.f;
+    const float dp = 2.0f * r * a.head_inv_n;
+    accb += dp;
+    accl += r * r;
+    for (int j = 0; j < N; j += 32) {
+        float cs = 0.f;                            // column j + lane over the 32 rows
+#pragma unroll 8
+        for (int rr = 0; rr < 32; ++rr)
+            cs = fmaf(stg[rr * kRB + j + lane], __shfl_sync(0xffffffffu, dp, rr), cs);
+        if (j + lane < N) hacc[j + lane] += cs;
+    }
+    __syncwarp();
+    for (int j = 0; j < N; j += 32) {
+        float y[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) y[q] = j + q < N ? dp * hw[j + q] : 0.f;
+        stg_put(stg + j, kRB, lane, y);
+    }
+    __syncwarp();
+    for (int j = 0; j < N; j += 32) stg_out_f32(stg + j, kRB, a.head_dy, N, row0, a.n, j, lane);
+    __syncwarp();
+}
+
 // epilogue warp (quarter qd): rows r0 + 32 qd + lane of accumulator columns at `acc`
 template <int NK>
 __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int64_t r0, int qd,
@@ -544,7 +575,10 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
     const float label = (NK < 0 && ok) ? __ldg(a.labels + row) : 0.f;
     // NK > 0 (fused next-layer D-ReLU): `stg` is the warp's [32][kRB] row buffer
     // and every block stays staged at its columns until the selection below
-    const int sstride = NK > 0 ? kRB : kEStg;
+    // fused head with N <= 64: y stays staged the same way, so the head pass reads it
+    // back from shared memory instead of a second TMEM read + merge
+    const bool rowbuf = NK > 0 || (NK < 0 && N <= 64);
+    const int sstride = rowbuf ? kRB : kEStg;
     float pred = 0.f;                              // fused head: y . w_h of this row
     for (int j = 0; j < N; j += 32) {
         uint32_t ra[2][16], rb[2][16];
@@ -602,8 +636,8 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
                 for (int q = 0; q < 16; ++q) y[16 * h + q] = ya[q];
             }
         }
-        float *sb = NK > 0 ? stg + j : stg;
-        if (NK > 0 || a.y) {
+        float *sb = rowbuf ? stg + j : stg;
+        if (rowbuf || a.y) {
             stg_put(sb, sstride, lane, y);
             __syncwarp();
         }
@@ -618,8 +652,10 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
                 if (j + q < N) pred += y[q] * hw[j + q];
         }
     }
-    if constexpr (NK < 0)
-        head_epilogue(a, lb, row0, lane, ok, pred, hw, hb, bias_s, stg, hacc, accb, accl, label);
+    if constexpr (NK < 0) {
+        if (rowbuf) head_epilogue_staged(a, row0, lane, ok, pred, hw, hb, stg, hacc, accb, accl, label);
+        else head_epilogue(a, lb, row0, lane, ok, pred, hw, hb, bias_s, stg, hacc, accb, accl, label);
+    }
     if constexpr (NK > 0) {
         const float *xr = stg + lane * kRB;
         if (a.nk_stream) {
@@ -831,7 +867,7 @@ __global__ void __launch_bounds__(RowsRoles<W2>::threads, 1) tc2_rows_kernel(con
         // ---------------- epilogue: warpgroup eg takes tiles t = eg, eg + ewg, ...
         // (accumulator t & 1; with ewg = 2 warpgroup eg always owns accumulator eg)
         const int qd = warp & 3, ew = warp - RR::epi0, eg = ew >> 2, ewg = W2 ? a.ewg : 1;
-        float *stg = reinterpret_cast<float *>(epi_stage + (size_t)ew * epi_warp_bytes(NK > 0));
+        float *stg = reinterpret_cast<float *>(epi_stage + (size_t)ew * epi_warp_bytes(NK != 0));
         EpiPre pcur, pnxt;
         float accb = 0.f, accl = 0.f;              // fused head: sum dp, sum r^2 of this lane
         float (*hacc)[258] = hacc_s + ew;
@@ -1782,7 +1818,8 @@ bool tc2_rows_supported(const Tc2RowsDesc &d) {
     if (d.epi == kEpi2Dz && d.n_dz % 16) return false;
     if (d.next_k && !tc2_next_drelu_supported(d.epi, d.N, d.next_k)) return false;
     const size_t bchunk = (size_t)256 * d.N;
-    const size_t budget = (size_t)(kSmemBase - 4 * epi_warp_bytes(d.next_k > 0) - (d.head_w ? 10 * 1024 : 0));
+    const size_t budget = (size_t)(kSmemBase - 4 * epi_warp_bytes(d.next_k > 0 || d.head_w) -
+                                   (d.head_w ? 10 * 1024 : 0));
     return 2 * kStage + 2 * kMaskStage + 2 * bchunk <= budget;
 }
 
@@ -1846,7 +1883,7 @@ int launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
     // out of the same budget.
     const size_t st_bytes = kStage + kMaskStage;
     auto budget_for = [&](int ewg) {
-        return (size_t)(kSmemBase - 4 * ewg * epi_warp_bytes(a.nk > 0) - (a.head ? 10 * 1024 : 0));
+        return (size_t)(kSmemBase - 4 * ewg * epi_warp_bytes(a.nk > 0 || a.head) - (a.head ? 10 * 1024 : 0));
     };
     size_t budget = budget_for(2);
     const bool res2 = (size_t)a.S * a.bchunk + 3 * st_bytes <= budget && a.S <= kMaxSB;
@@ -1880,7 +1917,7 @@ int launch_tc2_rows(const Tc2RowsDesc &d, cudaStream_t s) {
         a.SB = (int)std::min<size_t>(4, (budget - a.SA * st_bytes) / a.bchunk);
     }
     a.epi_off = (uint32_t)((a.SA * st_bytes + (size_t)a.SB * a.bchunk + 1023) / 1024 * 1024);
-    const size_t smem = (size_t)a.epi_off + 4 * a.ewg * epi_warp_bytes(a.nk > 0) + 1024;
+    const size_t smem = (size_t)a.epi_off + 4 * a.ewg * epi_warp_bytes(a.nk > 0 || a.head) + 1024;
     a.dz_split = d.dz_split ? 1 : 0;
     const int64_t tiles = (d.n + kTile - 1) / kTile;
     const int64_t grid = tiles < 148 ? tiles : 148;
