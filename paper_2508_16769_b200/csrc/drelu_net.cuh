@@ -115,29 +115,62 @@ __device__ __forceinline__ uint32_t tpr_top_stream(const float *xr, uint32_t (&t
 // every element with a larger truncated key is in the top K, none with a smaller
 // one is, and among the few whose truncated key equals Tt the best K - gt by
 // (full key desc, column asc) are taken (each ranked by one pass over the row).
-// Same set as ranking full keys; ~(2 + m) D shared reads for m tied elements
-// instead of the 33 D of a 32-step bisection (a rerun lane stalls its warp).
-// sel = the K selected columns, ascending.
+// Same set as ranking full keys; ~(2 + m) D shared reads for m <= 16 tied
+// elements instead of the 33 D of a 32-step bisection (a rerun lane stalls its
+// warp); rows with more ties take the bisection. sel = the K selected columns,
+// ascending.
 template <int D, int K, int CB>
 __device__ __forceinline__ void tpr_rerun(const float *xr, uint32_t Tt, uint32_t (&sel)[K]) {
     constexpr uint32_t CM = (1u << CB) - 1u;
-    int gt = 0;
+    int gt = 0, m = 0;
 #pragma unroll 8
-    for (int j = 0; j < D; ++j) gt += (order_key(xr[j]) & ~CM) > Tt;
-    const int need = K - gt;
+    for (int j = 0; j < D; ++j) {
+        const uint32_t kt = order_key(xr[j]) & ~CM;
+        gt += kt > Tt;
+        m += kt == Tt;
+    }
     int q = 0;
+    if (m <= 16) {
+        // few tied elements (the usual case): rank each by one pass over the row
+        const int need = K - gt;
+        for (int j = 0; j < D; ++j) {
+            const uint32_t kj = order_key(xr[j]);
+            bool take = (kj & ~CM) > Tt;
+            if ((kj & ~CM) == Tt) {
+                int r = 0;
+#pragma unroll 8
+                for (int i = 0; i < D; ++i) {
+                    const uint32_t ki = order_key(xr[i]);
+                    r += ((ki & ~CM) == Tt && (ki > kj || (ki == kj && i < j))) ? 1 : 0;
+                }
+                take = r < need;
+            }
+            if (take) {
+#pragma unroll
+                for (int t = 0; t < K; ++t)
+                    if (t == q) sel[t] = (uint32_t)j;
+                ++q;
+            }
+        }
+        return;
+    }
+    // many ties (e.g. rows of equal or integer values): the K-th largest full key by
+    // MSB-first bisection (33 D reads however many tie), then keys above it and the
+    // lowest columns among keys equal to it
+    uint32_t T = 0;
+    for (int b = 31; b >= 0; --b) {
+        const uint32_t cand = T | (1u << b);
+        int cnt = 0;
+        for (int j = 0; j < D; ++j) cnt += order_key(xr[j]) >= cand;
+        if (cnt >= K) T = cand;
+    }
+    int gtf = 0;
+    for (int j = 0; j < D; ++j) gtf += order_key(xr[j]) > T;
+    int need = K - gtf;
     for (int j = 0; j < D; ++j) {
         const uint32_t kj = order_key(xr[j]);
-        bool take = (kj & ~CM) > Tt;
-        if ((kj & ~CM) == Tt) {
-            int r = 0;
-#pragma unroll 8
-            for (int i = 0; i < D; ++i) {
-                const uint32_t ki = order_key(xr[i]);
-                r += ((ki & ~CM) == Tt && (ki > kj || (ki == kj && i < j))) ? 1 : 0;
-            }
-            take = r < need;
-        }
+        const bool take = kj > T || (kj == T && need > 0);
+        if (take && kj == T) --need;
         if (take) {
 #pragma unroll
             for (int t = 0; t < K; ++t)
