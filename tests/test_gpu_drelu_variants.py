@@ -37,3 +37,34 @@ def test_drelu_variants_bitexact(knob, dim, k, coop, tpr, stream):
     assert np.array_equal(to_np(idx).astype(np.int32), oi)
     assert np.array_equal(to_np(val), ov.astype(np.float32))
     assert np.array_equal(np.signbit(to_np(val)), np.signbit(ov))
+
+
+@pytest.mark.parametrize("dim,k", [(64, 8), (128, 16), (64, 16)])
+@pytest.mark.parametrize("coop,tpr,stream", [(0, 2, 0), (0, 2, 2), (2, 1, 0), (-2, 1, 1)])
+def test_drelu_rerun_tie_counts(knob, dim, k, coop, tpr, stream):
+    """The exact rerun's two regimes (tpr_rerun): m tied elements at the k-th
+    value with m = 2 .. 16 (ranked one by one) and m = 17 .. D (bisection). Each
+    row holds k - 3 larger values and m copies of the threshold value (exact ties:
+    the lowest columns win), the rest smaller; some copies are replaced by 1-ulp
+    neighbours so the truncated keys tie but the full keys do not."""
+    knob("drelu_coop", coop, -2)
+    knob("drelu_tpr", tpr, 1)
+    knob("tpr_stream", stream, 1)
+    rng = np.random.default_rng(11 + dim + k)
+    rows = []
+    for m in [2, 3, 8, 15, 16, 17, 24, dim - (k - 3)]:
+        for ulp in (False, True):
+            x = rng.uniform(-3.0, -1.0, dim).astype(np.float32)
+            cols = rng.permutation(dim)
+            big, tie = cols[:k - 3], cols[k - 3:k - 3 + m]
+            x[big] = rng.uniform(2.0, 3.0, k - 3).astype(np.float32)
+            x[tie] = np.float32(1.25)
+            if ulp:
+                x[tie[::3]] = np.nextafter(np.float32(1.25), np.float32(2.0))
+            rows.append(x)
+    x = np.stack(rows)
+    xg = torch.as_tensor(x).cuda()
+    val, idx = dr.drelu_topk(xg, k)
+    oi, ov = O.drelu(x.astype(np.float64), k)
+    assert np.array_equal(to_np(idx).astype(np.int32), oi)
+    assert np.array_equal(to_np(val), ov.astype(np.float32))
