@@ -394,7 +394,7 @@ void launch_tpr(const float *x, int64_t n, int64_t ldx, float *val, uint8_t *idx
 template <int D, int K, int T>
 __global__ void __launch_bounds__(128) drelu_tcoop_kernel(const float *__restrict__ x, int64_t n,
                                                           int64_t ldx, float *__restrict__ val,
-                                                          uint8_t *__restrict__ idx) {
+                                                          uint8_t *__restrict__ idx, int roll) {
     constexpr int P = D + 4, Q = D / 4, RW = 32 / T, W = D / T;   // rows per warp, columns per lane
     constexpr int CB = D == 32 ? 5 : D == 64 ? 6 : 7;
     constexpr uint32_t CM = (1u << CB) - 1u;
@@ -439,23 +439,42 @@ __global__ void __launch_bounds__(128) drelu_tcoop_kernel(const float *__restric
         const int64_t r = r0 + rl;
         const float *xr = xs + rl * P;
         uint32_t w[W];
-#pragma unroll
-        for (int c4 = 0; c4 < W / 4; ++c4) {
-            const uint32_t c = (uint32_t)(sl * W + 4 * c4);
-            const float4 q = *reinterpret_cast<const float4 *>(xr + c);
-            w[4 * c4 + 0] = (order_key(q.x) & ~CM) | (CM - (c + 0));
-            w[4 * c4 + 1] = (order_key(q.y) & ~CM) | (CM - (c + 1));
-            w[4 * c4 + 2] = (order_key(q.z) & ~CM) | (CM - (c + 2));
-            w[4 * c4 + 3] = (order_key(q.w) & ~CM) | (CM - (c + 3));
-        }
-#pragma unroll
-        for (int g = 0; g < W / K; ++g) bitonic_sort_desc<K>(w + g * K);
         uint32_t lost = 0;
+        if (roll) {
+            // the lane's W columns in rolled chunks of CK (tpr_top_stream's network)
+            constexpr int CK = K < 8 ? 8 : K;
+            static_assert(W % CK == 0, "chunking");
+            uint32_t b[CK];
+            tpr_keys<CK, CB>(xr, sl * W, b);
+            bitonic_sort_desc<CK>(b);
 #pragma unroll
-        for (int step = 1; step < W / K; step <<= 1)
+            for (int t = 0; t < K; ++t) w[t] = b[t];
+            if constexpr (CK > K) lost = b[K];
+#pragma unroll 1
+            for (int c0 = CK; c0 < W; c0 += CK) {
+                tpr_keys<CK, CB>(xr, sl * W + c0, b);
+                bitonic_sort_desc<CK>(b);
+                if constexpr (CK > K) lost = max(lost, b[K]);
+                lost = max(lost, merge_keep_desc<K>(w, b));
+            }
+        } else {
 #pragma unroll
-            for (int g = 0; g + step < W / K; g += 2 * step)
-                lost = max(lost, merge_keep_desc<K>(w + g * K, w + (g + step) * K));
+            for (int c4 = 0; c4 < W / 4; ++c4) {
+                const uint32_t c = (uint32_t)(sl * W + 4 * c4);
+                const float4 q = *reinterpret_cast<const float4 *>(xr + c);
+                w[4 * c4 + 0] = (order_key(q.x) & ~CM) | (CM - (c + 0));
+                w[4 * c4 + 1] = (order_key(q.y) & ~CM) | (CM - (c + 1));
+                w[4 * c4 + 2] = (order_key(q.z) & ~CM) | (CM - (c + 2));
+                w[4 * c4 + 3] = (order_key(q.w) & ~CM) | (CM - (c + 3));
+            }
+#pragma unroll
+            for (int g = 0; g < W / K; ++g) bitonic_sort_desc<K>(w + g * K);
+#pragma unroll
+            for (int step = 1; step < W / K; step <<= 1)
+#pragma unroll
+                for (int g = 0; g + step < W / K; g += 2 * step)
+                    lost = max(lost, merge_keep_desc<K>(w + g * K, w + (g + step) * K));
+        }
         // butterfly over the T lanes of the row
 #pragma unroll
         for (int m = 1; m < T; m <<= 1) {
@@ -514,7 +533,10 @@ void launch_tcoop(const float *x, int64_t n, int64_t ldx, float *val, uint8_t *i
     const int64_t cap = (int64_t)148 * ps;
     int64_t blocks = (groups + 3) / 4;
     if (blocks > cap) blocks = cap;
-    drelu_tcoop_kernel<D, K, T><<<(unsigned)blocks, 128, smem, s>>>(x, n, ldx, val, idx);
+    // rolled per-lane network at D = 128 (C4 1M x 128, k = 16: 0.258 -> 0.242 ms;
+    // 700k: 0.186 -> 0.180), unrolled at D = 64 (equal or faster); tpr_stream 0 / 2 force
+    const int roll = D == 128 ? (knobs().tpr_stream != 0) : (knobs().tpr_stream == 2);
+    drelu_tcoop_kernel<D, K, T><<<(unsigned)blocks, 128, smem, s>>>(x, n, ldx, val, idx, roll);
 }
 
 template <bool SORTED>
@@ -522,12 +544,12 @@ bool try_tpr(const float *x, int64_t n, int dim, int64_t ldx, int k, float *val,
              cudaStream_t s) {
     if ((ldx % 4) != 0 || (reinterpret_cast<uintptr_t>(x) % 16) != 0) return false;
     // cooperative rows: default (-2) two lanes per row at D = 64, k in {4, 8}
-    // (100k x 64, k = 8: 0.0205 vs 0.0246 ms thread-per-row, 0.0307 warp-per-row);
-    // at D = 128 the rolled thread-per-row network with the cheap rerun is faster
-    // (C4 1M x 128, k = 16: 0.248 vs 0.266 ms) -- profiles/r03/drelu_ab.json;
-    // 0 = off, 1 / 2 / 4 = forced (A/B)
+    // (100k x 64, k = 8: 0.0205 vs 0.0246 ms thread-per-row, 0.0307 warp-per-row)
+    // and, with the rolled per-lane network, at D = 128, k in 4..16 (C4 1M x 128,
+    // k = 16: 0.242 vs 0.248 ms rolled thread-per-row; 700k: 0.180 vs 0.191) --
+    // profiles/r03/drelu_ab.json, drelu_ab_roll.json; 0 = off, 1 / 2 / 4 = forced (A/B)
     int T = (int)knobs().drelu_coop;
-    if (T == -2) T = (dim == 64 && (k == 4 || k == 8)) ? 2 : 0;
+    if (T == -2) T = ((dim == 64 && (k == 4 || k == 8)) || (dim == 128 && k >= 4 && k <= 16)) ? 2 : 0;
     if (!SORTED && T > 0) {
 #define DR_TCO(DD, KK, TT)                                                                  \
         if (dim == DD && k == KK && T == TT) {                                              \

@@ -20,7 +20,7 @@ dr = pytest.importorskip("paper_2508_16769_b200")
 
 @pytest.mark.parametrize("dim,k", [(128, 16), (128, 8), (128, 4), (64, 8), (64, 16), (64, 4)])
 @pytest.mark.parametrize("coop,tpr,stream", [(1, 1, 0), (2, 1, 0), (4, 1, 0), (0, 1, 0), (0, 2, 0),
-                                             (0, 2, 2), (0, 0, 0), (-2, 1, 1)])
+                                             (0, 2, 2), (0, 0, 0), (-2, 1, 1), (2, 1, 2), (4, 1, 2)])
 def test_drelu_variants_bitexact(knob, dim, k, coop, tpr, stream):
     knob("drelu_coop", coop, -2)
     knob("drelu_tpr", tpr, 1)
@@ -40,7 +40,7 @@ def test_drelu_variants_bitexact(knob, dim, k, coop, tpr, stream):
 
 
 @pytest.mark.parametrize("dim,k", [(64, 8), (128, 16), (64, 16)])
-@pytest.mark.parametrize("coop,tpr,stream", [(0, 2, 0), (0, 2, 2), (2, 1, 0), (-2, 1, 1)])
+@pytest.mark.parametrize("coop,tpr,stream", [(0, 2, 0), (0, 2, 2), (2, 1, 0), (2, 1, 2), (-2, 1, 1)])
 def test_drelu_rerun_tie_counts(knob, dim, k, coop, tpr, stream):
     """The exact rerun's two regimes (tpr_rerun): m tied elements at the k-th
     value with m = 2 .. 16 (ranked one by one) and m = 17 .. D (bisection). Each

@@ -21,7 +21,8 @@ for n, D, k in [(100_000, 64, 4), (100_000, 64, 2), (100_000, 64, 8), (66_600, 6
     row = {}
     modes = {"warp": dict(drelu_tpr=0), "tpr": dict(drelu_tpr=2, drelu_coop=0, tpr_stream=0),
              "tpr_stream": dict(drelu_tpr=2, drelu_coop=0, tpr_stream=2),
-             "coop": dict(drelu_tpr=2, drelu_coop=2, tpr_stream=0), "default": {}}
+             "coop": dict(drelu_tpr=2, drelu_coop=2, tpr_stream=0),
+             "coop_roll": dict(drelu_tpr=2, drelu_coop=2, tpr_stream=2), "default": {}}
     for name, kn in modes.items():
         base = dict(drelu_tpr=1, drelu_coop=-2, tpr_stream=1)
         base.update(kn)
