@@ -482,17 +482,26 @@ __device__ __forceinline__ void head_epilogue_staged(const R2Args &a, int64_t ro
     accb += dp;
     accl += r * r;
     for (int j = 0; j < N; j += 32) {
-        float cs = 0.f;                            // column j + lane over the 32 rows
+        float c0 = 0.f, c1 = 0.f;                  // column j + lane over the 32 rows
 #pragma unroll 8
-        for (int rr = 0; rr < 32; ++rr)
-            cs = fmaf(stg[rr * kRB + j + lane], __shfl_sync(0xffffffffu, dp, rr), cs);
-        if (j + lane < N) hacc[j + lane] += cs;
+        for (int rr = 0; rr < 32; rr += 2) {
+            c0 = fmaf(stg[rr * kRB + j + lane], __shfl_sync(0xffffffffu, dp, rr), c0);
+            c1 = fmaf(stg[(rr + 1) * kRB + j + lane], __shfl_sync(0xffffffffu, dp, rr + 1), c1);
+        }
+        if (j + lane < N) hacc[j + lane] += c0 + c1;
     }
     __syncwarp();
     for (int j = 0; j < N; j += 32) {
         float y[32];
+        const float4 *h4 = reinterpret_cast<const float4 *>(hw + j);   // zero past N
 #pragma unroll
-        for (int q = 0; q < 32; ++q) y[q] = j + q < N ? dp * hw[j + q] : 0.f;
+        for (int q4 = 0; q4 < 8; ++q4) {
+            const float4 w = h4[q4];
+            y[4 * q4] = dp * w.x;
+            y[4 * q4 + 1] = dp * w.y;
+            y[4 * q4 + 2] = dp * w.z;
+            y[4 * q4 + 3] = dp * w.w;
+        }
         stg_put(stg + j, kRB, lane, y);
     }
     __syncwarp();
@@ -647,9 +656,19 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
         }
         if (ok && a.G == 2 && a.mask_out) a.mask_out[row * mw + (j >> 5)] = word;
         if constexpr (NK < 0) {
+            // y . w_h over this block: w_h as broadcast 128-bit loads (zero past N,
+            // as y is), four partial sums
+            const float4 *h4 = reinterpret_cast<const float4 *>(hw + j);
+            float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
 #pragma unroll
-            for (int q = 0; q < 32; ++q)
-                if (j + q < N) pred += y[q] * hw[j + q];
+            for (int q4 = 0; q4 < 8; ++q4) {
+                const float4 w = h4[q4];
+                p0 = fmaf(y[4 * q4], w.x, p0);
+                p1 = fmaf(y[4 * q4 + 1], w.y, p1);
+                p2 = fmaf(y[4 * q4 + 2], w.z, p2);
+                p3 = fmaf(y[4 * q4 + 3], w.w, p3);
+            }
+            pred += (p0 + p1) + (p2 + p3);
         }
     }
     if constexpr (NK < 0) {
@@ -684,7 +703,7 @@ __global__ void __launch_bounds__(RowsRoles<W2>::threads, 1) tc2_rows_kernel(con
     float *head_s = nullptr;
     float (*hacc_s)[258] = nullptr;
     if constexpr (NK < 0) {
-        __shared__ float head_sh[257];
+        __shared__ __align__(16) float head_sh[260];
         __shared__ float hacc_sh[8][258];
         head_s = head_sh;
         hacc_s = hacc_sh;
