@@ -539,9 +539,15 @@ __device__ __forceinline__ void rows_epilogue(const R2Args &a, uint32_t acc, int
                 v[q] = __uint_as_float(r[0][q]);
                 v[16 + q] = j + 16 < N ? __uint_as_float(r[1][q]) : 0.f;
             }
+            // dZ' row scale (not the root term); n_dz % 16 == 0: uniform per half block
+            if (j < a.n_dz) {
 #pragma unroll
-            for (int q = 0; q < 32; ++q)
-                if (j + q < a.n_dz) v[q] *= cr;        // dZ' row scale (not the root term)
+                for (int q = 0; q < 16; ++q) v[q] *= cr;
+            }
+            if (j + 16 < a.n_dz) {
+#pragma unroll
+                for (int q = 16; q < 32; ++q) v[q] *= cr;
+            }
             stg_put(stg, kEStg, lane, v);
             __syncwarp();
             if (j < a.n_dz) {
